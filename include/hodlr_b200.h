@@ -1,0 +1,231 @@
+/*
+ * hodlr_b200.h -- C ABI of the B200-native HODLR hot path.
+ *
+ * Drop-in boundary for the compute path of hodlrkit 0.1.0
+ * (/root/reference/pkg/src/hodlrkit).  The reference has no FFI of its own:
+ * its boundary is the Python API re-exported by src/__init__.py:11-125.
+ * Each entry point below names the reference function it replaces
+ * (file:line, paths relative to pkg/src/hodlrkit/).  The Python package
+ * paper_1403_5337_b200 binds these with ctypes (INTEGRATION.md shows the
+ * binding); nothing here uses torch types.
+ *
+ * Conventions
+ *   - All floating point is IEEE fp64.  Matrices passed in are ROW-MAJOR
+ *     (C order, like the numpy arrays the reference passes around) unless a
+ *     parameter says column-major.
+ *   - Pointers named *_dev are device pointers; *_host are host pointers.
+ *   - `stream` is a cudaStream_t passed as void*; NULL = legacy default stream.
+ *   - Every function returns an hk_status; hk_last_error() gives a message.
+ *   - A plan is used by one host thread at a time (SPEC: factorizations are
+ *     immutable after factor; solve is re-entrant across rhs, not threads).
+ */
+#ifndef HODLR_B200_H
+#define HODLR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+/* Status codes map 1:1 onto the reference exception classes (src/errors.py). */
+typedef enum {
+  HK_OK = 0,
+  HK_ERR_VALUE = 1,              /* ValueError (bad config, non-finite input)       */
+  HK_ERR_DIMENSION = 2,          /* DimensionMismatchError        errors.py:43       */
+  HK_ERR_SINGULAR = 3,           /* SingularMatrixError           errors.py:8        */
+  HK_ERR_SINGULAR_LEAF = 4,      /* SingularLeafError             errors.py:12       */
+  HK_ERR_SINGULAR_SCHUR = 5,     /* SingularSchurError            errors.py:16       */
+  HK_ERR_DEGENERATE = 6,         /* DegenerateSkeletonError       errors.py:32       */
+  HK_ERR_BREAKDOWN = 7,          /* GmresBreakdownError           errors.py:39       */
+  HK_ERR_EMPTY_SELECTION = 8,    /* EmptySelectionError           errors.py:28       */
+  HK_ERR_CUDA = 20,              /* CUDA runtime failure / no device                 */
+  HK_ERR_STATE = 21              /* call order violated (e.g. solve before factor)   */
+} hk_status;
+
+typedef enum { HK_SCHEME_SVD = 0, HK_SCHEME_ACA = 1, HK_SCHEME_BDLR = 2 } hk_scheme;
+
+typedef struct hk_plan hk_plan;
+
+/* Message of the last failing call on this thread. */
+const char* hk_last_error(void);
+/* Library version string "hodlr_b200 <semver> sm_100a". */
+const char* hk_version(void);
+/* Number of visible CUDA devices (0 on a host without a GPU; never fails). */
+int hk_device_count(void);
+
+/* ------------------------------------------------------------------------
+ * Plans: one bisection tree (build_tree, hodlr.py:76-102) shared by `batch`
+ * independent fronts of order n.  Front f lives at fronts_dev + f*front_stride.
+ * ---------------------------------------------------------------------- */
+hk_status hk_plan_create(int64_t n, int64_t leaf_threshold, int64_t batch, hk_plan** out);
+hk_status hk_plan_destroy(hk_plan* plan);
+/* Tree in preorder: level, lo, hi, left, right per node (left=-1 for a leaf).
+ * Arrays must hold hk_plan_num_nodes() entries.  Mirrors HodlrTree.nodes. */
+int64_t   hk_plan_num_nodes(const hk_plan* plan);
+hk_status hk_plan_tree(const hk_plan* plan, int32_t* level, int64_t* lo, int64_t* hi,
+                       int32_t* left, int32_t* right);
+
+/* ------------------------------------------------------------------------
+ * Build: compress both off-diagonal blocks of every internal node of every
+ * front (factorize -> compress, hodlr.py:239-242; lowrank.py:353-359).
+ * Blocks are numbered 2*k (upper, rows=left child, cols=right child) and
+ * 2*k+1 (lower) for the k-th internal node in preorder.
+ * ---------------------------------------------------------------------- */
+/* ACA, lowrank.py:230-286.  tol2 = tol**2 computed by the caller (the
+ * reference evaluates cfg.tol ** 2 in Python).  max_rank <= 0 = no cap.
+ * record_trace != 0 keeps the per-block pivot trace (hk_get_aca_trace). */
+hk_status hk_build_aca(hk_plan* plan, const double* fronts_dev, int64_t ld,
+                       int64_t front_stride, double tol, double tol2, int64_t max_rank,
+                       int record_trace, void* stream);
+/* BDLR, lowrank.py:334-350 + graph.py:171-228.  One symmetric CSR graph in
+ * front order (no self loops) shared by all fronts. */
+hk_status hk_build_bdlr(hk_plan* plan, const double* fronts_dev, int64_t ld,
+                        int64_t front_stride, double tol, int32_t depth, int64_t max_rank,
+                        const int64_t* indptr_host, const int64_t* indices_host,
+                        void* stream);
+/* Externally computed factors (the parity-only svd scheme, lowrank.py:221-227):
+ * declare the fronts, then set every block's factor from column-major device
+ * buffers U (m x rank, ld_u) and V (n x rank, ld_v). */
+hk_status hk_build_external_begin(hk_plan* plan, const double* fronts_dev, int64_t ld,
+                                  int64_t front_stride, void* stream);
+hk_status hk_set_block_factor(hk_plan* plan, int64_t front, int64_t block, int64_t rank,
+                              const double* U_dev, int64_t ld_u, const double* V_dev,
+                              int64_t ld_v, void* stream);
+
+/* Ranks after a build, [batch][2*num_internal] (blocks as above). */
+hk_status hk_get_ranks(hk_plan* plan, int32_t* ranks_host);
+/* ACA trace of one block: rows read (in order) and columns read, as the
+ * reference's BlockAccessor.row/.col see them (lowrank.py:253, :266). */
+hk_status hk_get_aca_trace(hk_plan* plan, int64_t front, int64_t block, int32_t* rows_host,
+                           int64_t* nrows, int32_t* cols_host, int64_t* ncols);
+/* BDLR skeleton of one block: rank and the skeleton row/column positions
+ * row_sel[row_perm[:r]], col_sel[col_perm[:r]] (lowrank.py:311, :317). */
+hk_status hk_get_skeleton(hk_plan* plan, int64_t front, int64_t block, int64_t* rank,
+                          int64_t* rows_host, int64_t* cols_host, int64_t cap);
+/* Column-major factors of one block into host buffers (m x rank, n x rank). */
+hk_status hk_get_block_factor(hk_plan* plan, int64_t front, int64_t block,
+                              double* U_host, double* V_host);
+/* Geometry of one block: m, n and the rank cap. */
+hk_status hk_block_shape(const hk_plan* plan, int64_t block, int64_t* m, int64_t* n,
+                         int64_t* cap);
+
+/* ------------------------------------------------------------------------
+ * Factor (factorize, hodlr.py:183-282): batched leaf LU, then one upward
+ * level sweep of coupling assembly, coupling LU and correction.
+ * ---------------------------------------------------------------------- */
+hk_status hk_factor(hk_plan* plan, void* stream);
+/* Factor views for the test-visible attributes of HodlrFactorization
+ * (hodlr.py:105-154): leaf LU (b x b row-major packed, LAPACK-style 0-based
+ * swap indices `piv`) and
+ * per internal node d_left (na x r_u), d_right (nb x r_l), Schur LU
+ * ((r_l+r_u)^2) -- all row-major host copies. */
+hk_status hk_get_leaf_lu(hk_plan* plan, int64_t front, int64_t node, double* lu_host,
+                         int32_t* perm_host);
+hk_status hk_get_coupling(hk_plan* plan, int64_t front, int64_t node, double* d_left_host,
+                          double* d_right_host, double* schur_lu_host, int32_t* schur_perm_host);
+
+/* ------------------------------------------------------------------------
+ * Solve (solve, hodlr.py:285-306) in place on device right-hand sides of
+ * every front: rhs front f = rhs_dev + f*rhs_stride, column-major n x nrhs
+ * with leading dimension ld.
+ * ---------------------------------------------------------------------- */
+hk_status hk_solve(hk_plan* plan, double* rhs_dev, int64_t ld, int64_t nrhs,
+                   int64_t rhs_stride, void* stream);
+/* Solve for one front only (the GMRES preconditioner of that front). */
+hk_status hk_solve_front(hk_plan* plan, int64_t front, double* rhs_dev, int64_t ld,
+                         int64_t nrhs, void* stream);
+
+/* ------------------------------------------------------------------------
+ * GMRES (krylov.py:69-166): left preconditioned, no restart, MGS with one
+ * conditional re-orthogonalisation, Givens, true-residual guard.
+ * Operator: the dense row-major front A_dev (cli.py:320-321 `dense @ v`).
+ * precond: 0 = none, 1 = the plan's HODLR solve for `front`, 2 = diagonal
+ * scaling (krylov.py:44-66).  history_host holds max_iter doubles.
+ * flags_host[0] = converged, [1] = breakdown.
+ * ---------------------------------------------------------------------- */
+hk_status hk_gmres(hk_plan* plan, int64_t front, const double* A_dev, int64_t lda,
+                   const double* b_dev, double tol, int64_t max_iter, int precond,
+                   double* x_dev, int64_t* iterations, double* history_host,
+                   double* true_residual, int32_t* flags_host, void* stream);
+
+/* Building blocks for GMRES with arbitrary operator callables. */
+/* One Arnoldi/MGS/Givens column update for column j (krylov.py:110-145):
+ * w_dev holds M^{-1} A v_j on entry.  basis n x (m+1) col-major (ld = n),
+ * hess (m+1) x m col-major, cs/sn/g device arrays.  out_host: [0]=rel,
+ * [1]=happy, [2]=breakdown.  beta = ||r0||. */
+hk_status hk_arnoldi_step(int64_t n, int64_t j, int64_t mmax, double* basis_dev,
+                          double* hess_dev, double* cs_dev, double* sn_dev, double* g_dev,
+                          double* w_dev, double beta, double* out_host, void* stream);
+/* Back substitution + x = basis[:, :m] y (krylov.py:147-154). */
+hk_status hk_gmres_combine(int64_t n, int64_t m, int64_t mmax, const double* basis_dev,
+                           const double* hess_dev, const double* g_dev, double* x_dev,
+                           void* stream);
+
+/* ------------------------------------------------------------------------
+ * Dense kernels (dense.py) and compression of a single block (lowrank.py).
+ * ---------------------------------------------------------------------- */
+/* dense @ x for row-major A (m x n) and column-major X (n x s): hodlr.py:309-316. */
+hk_status hk_gemv(const double* A_dev, int64_t lda, int64_t m, int64_t n, const double* x_dev,
+                  int64_t ldx, int64_t s, double* y_dev, int64_t ldy, void* stream);
+/* Complete-pivot LU (lu_full, dense.py:133-166), bit-exact pivot order.
+ * a_dev row-major m x n (ld) is overwritten with the packed LU; perms 0-based;
+ * pivots_dev receives |U_kk|; *npiv the number of pivots taken. */
+hk_status hk_lu_full(double* a_dev, int64_t m, int64_t n, int64_t ld, int64_t* row_perm_dev,
+                     int64_t* col_perm_dev, double* pivots_dev, int64_t* npiv, void* stream);
+/* Partial-pivot LU (lu_partial, dense.py:59-81) with explicit inverse:
+ * a_dev row-major n x n overwritten by the packed LU, perm 0-based row_perm,
+ * inv_dev (may be NULL) receives A^{-1} row-major. HK_ERR_SINGULAR when
+ * min|U_kk| < 1e-300. */
+hk_status hk_lu_partial(double* a_dev, int64_t n, int64_t ld, int32_t* perm_dev,
+                        double* inv_dev, void* stream);
+/* ACA of one row-major block (compress_aca, lowrank.py:230-286). U, V are
+ * column-major device buffers with room for `cap` columns. */
+hk_status hk_aca_block(const double* a_dev, int64_t m, int64_t n, int64_t ld, double tol2,
+                       int64_t cap, double* U_dev, double* V_dev, int64_t* rank,
+                       int32_t* trace_rows_host, int64_t* nrows, int32_t* trace_cols_host,
+                       int64_t* ncols, void* stream);
+
+/* Pseudo-skeleton of one row-major block from given selections
+ * (pseudo_skeleton, lowrank.py:289-331): complete-pivot LU of the skeleton
+ * intersection, rank = #{|p_k| >= tol |p_0|} capped at cap, then
+ * U = C U11^{-1} (m x rank) and V = (L11^{-1} R)^T (n x rank), column-major.
+ * rows_out/cols_out (host, >= cap) receive the skeleton positions.
+ * HK_ERR_DEGENERATE when rank 0 faces a numerically nonzero block. */
+hk_status hk_skeleton_block(const double* a_dev, int64_t m, int64_t n, int64_t ld,
+                            const int64_t* row_sel_host, int64_t k, const int64_t* col_sel_host,
+                            int64_t kc, double tol, int64_t cap, double* U_dev, double* V_dev,
+                            int64_t* rank, int64_t* rows_out, int64_t* cols_out, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Graph selection (graph.py:171-228), host integer code, bit-exact.
+ * ---------------------------------------------------------------------- */
+/* Distances (graph.py:183-206) of `own` vertices to their boundary with
+ * `other`, restricted to own; unreachable = -1. */
+hk_status hk_graph_distance(int64_t nverts, const int64_t* indptr, const int64_t* indices,
+                            const int64_t* own, int64_t n_own, const int64_t* other,
+                            int64_t n_other, int64_t* dist_out);
+/* select_by_depth (graph.py:209-228): positions ordered by (d, vertex id).
+ * Returns HK_ERR_EMPTY_SELECTION when either side selects nothing. */
+hk_status hk_select_by_depth(int64_t nverts, const int64_t* indptr, const int64_t* indices,
+                             const int64_t* row_verts, int64_t n_rows, const int64_t* col_verts,
+                             int64_t n_cols, int32_t depth, int64_t* row_sel, int64_t* n_row_sel,
+                             int64_t* col_sel, int64_t* n_col_sel);
+
+/* Timings of the last build/factor/solve on the plan's stream, in seconds
+ * (keys of SolveReport.timings, hodlr.py:223-281): lowrank, leaf_lu, schur. */
+hk_status hk_get_timings(hk_plan* plan, double* lowrank, double* leaf_lu, double* schur);
+
+/* Kernel launches issued by this library since load (evidence counter). */
+int64_t hk_launch_count(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* HODLR_B200_H */

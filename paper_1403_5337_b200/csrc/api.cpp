@@ -1,0 +1,1525 @@
+// C-ABI implementation: plans, task-list construction and phase orchestration
+// for the batched HODLR build / factor / solve / GMRES on one B200.
+//
+// Level-synchronous restatement of the reference recursion:
+//   build   every off-diagonal block of every front in ONE launch (ACA) or
+//           one skeleton launch (BDLR)                     src/hodlr.py:239-242
+//   factor  Z gather -> batched leaf LU + inverse -> leaf GEMM  (:222-232)
+//           then for each level bottom-up: H = V^T [c | d] (GEMM), coupling
+//           LU + inverse, Q = S^{-1} rhs (GEMM), c -= d y (GEMM)  (:264-282)
+//   solve   leaf apply, then per level V^T x, S^{-1}, x -= d y     (:285-306)
+//
+// Extension layout: one column-major n x W buffer Y per front with the
+// ancestors' U factors FARTHEST FIRST.  Node p at level l then owns the
+// rectangle Y[lo_p:hi_p, 0:w_p] (w_p = sum of ancestor ranks on its side),
+// and its children's d blocks are Y[rows, w_p : w_p + r].  Nothing is ever
+// concatenated (the reference's hstack/vstack at :244-245, :282 disappear).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/hodlr_b200.h"
+#include "hk_graph.h"
+#include "hk_internal.h"
+
+// ------------------------------------------------------------------ errors, counters
+static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};
+
+void hk_count_launch(int k) { g_launches += k; }
+
+static hk_status fail(hk_status code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CU(expr)                                                                      \
+  do {                                                                                \
+    cudaError_t _e = (expr);                                                          \
+    if (_e != cudaSuccess)                                                            \
+      return fail(HK_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));   \
+  } while (0)
+
+#define CHK(expr)                    \
+  do {                               \
+    hk_status _s = (expr);           \
+    if (_s != HK_OK) return _s;      \
+  } while (0)
+
+extern "C" const char* hk_last_error(void) { return g_err.c_str(); }
+extern "C" const char* hk_version(void) { return "hodlr_b200 0.1.0 sm_100a"; }
+extern "C" int hk_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+extern "C" int64_t hk_launch_count(void) { return g_launches.load(); }
+
+// ------------------------------------------------------------------ device buffers
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t need, cudaStream_t st) {
+    if (need <= bytes && p) return cudaSuccess;
+    if (p) cudaFreeAsync(p, st);
+    p = nullptr;
+    bytes = 0;
+    size_t alloc = need < 256 ? 256 : need;
+    cudaError_t e = cudaMallocAsync(&p, alloc, st);
+    if (e == cudaSuccess) bytes = alloc;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+template <class T>
+static cudaError_t upload(DevBuf& b, const std::vector<T>& v, cudaStream_t st) {
+  cudaError_t e = b.ensure(v.size() * sizeof(T) + 16, st);
+  if (e != cudaSuccess) return e;
+  if (v.empty()) return cudaSuccess;
+  return cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st);
+}
+
+static void init_pool_once() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+}
+
+// ------------------------------------------------------------------ plan
+struct Node {
+  int level;
+  int64_t lo, hi;
+  int left, right;
+};
+
+struct BlockGeom {
+  int node;       // slot
+  int side;       // 0 upper, 1 lower
+  int64_t row0, col0;
+  int m, n, cap;
+  int64_t u_off, v_off;   // doubles, within one front's UV region
+  int64_t t_off;          // ints, within one front's trace region
+};
+
+struct NodeRec {  // per (front, node) factor storage
+  int64_t lu = -1, inv = -1, h = -1, q = -1;        // doubles in F pool
+  int64_t perm = -1, ipiv = -1, status = -1;        // ints in I pool
+  int64_t g = -1, yv = -1;                          // solve scratch (doubles) per rhs column
+  int R = 0, rl = 0, ru = 0;
+  int64_t w = 0, hcols = 0;
+};
+
+struct SolveProg {
+  bool small = true;
+  int s = 0;
+  // small-s
+  DevBuf leaf_t;
+  int n_leaf = 0, leaf_rows = 0, leaf_k = 0;
+  struct Level {
+    DevBuf dot_t, sinv_t, upd_t;
+    int n_dot = 0, n_sinv = 0, n_upd = 0;
+    int dot_cols = 0, sinv_rows = 0, sinv_k = 0, upd_rows = 0, upd_k = 0;
+    // gemm variant
+    DevBuf g1, g1map, g2, g2map, g3, g3map;
+    int t1 = 0, t2 = 0, t3 = 0;
+  };
+  std::vector<Level> levels;
+  DevBuf leaf_g, leaf_map;
+  int leaf_tiles = 0;
+};
+
+struct hk_plan {
+  int64_t n = 0, leaf = 0, batch = 0;
+  std::vector<Node> nodes;
+  std::vector<int> internal;        // slots, preorder
+  std::vector<int> iidx;            // slot -> internal index or -1
+  std::vector<int> leaves;          // slots, preorder
+  std::vector<int> post;            // slot -> DFS event index (failure ordering)
+  int depth = 0;
+
+  // build
+  int scheme = -1;
+  bool built = false, factored = false;
+  const double* A = nullptr;
+  int64_t lda = 0, fstride = 0;
+  std::vector<BlockGeom> blocks;
+  std::vector<int> block_order;     // largest first
+  int64_t uv_per_front = 0, trace_per_front = 0;
+  DevBuf At, UV, ranks_d, trace_d, tasks_d;
+  std::vector<int32_t> ranks;       // batch * nblocks
+  bool have_trace = false;
+  // bdlr
+  std::vector<std::vector<int64_t>> rsel, csel;  // per block
+  DevBuf sel_d, work_d, perm_d, skel_status_d, probe_d;
+  std::vector<int64_t> sel_off_r, sel_off_c;     // per block offsets into sel_d
+  std::vector<int64_t> perm_off;                  // per (front, block) into perm_d
+  // factor
+  std::vector<int64_t> W;           // per front
+  std::vector<int64_t> y_off;       // per front (doubles)
+  std::vector<NodeRec> rec;         // batch * nodes
+  DevBuf Y, Ytmp, F, I, ftask_d, fmap_d;
+  int64_t g_per_col = 0;            // doubles of G/Yv scratch per rhs column (all fronts)
+  std::map<std::pair<int, int>, SolveProg*> progs;
+  DevBuf Xin, X2, G, Yv;
+  // timings
+  double t_lowrank = 0, t_leaf = 0, t_schur = 0;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+
+  int nblocks() const { return (int)blocks.size(); }
+  ~hk_plan() {
+    for (auto& kv : progs) {
+      SolveProg* p = kv.second;
+      p->leaf_t.release();
+      p->leaf_g.release();
+      p->leaf_map.release();
+      for (auto& l : p->levels) {
+        l.dot_t.release(); l.sinv_t.release(); l.upd_t.release();
+        l.g1.release(); l.g1map.release(); l.g2.release(); l.g2map.release();
+        l.g3.release(); l.g3map.release();
+      }
+      delete p;
+    }
+    DevBuf* bufs[] = {&At, &UV, &ranks_d, &trace_d, &tasks_d, &sel_d, &work_d, &perm_d,
+                      &skel_status_d, &probe_d, &Y, &Ytmp, &F, &I, &ftask_d, &fmap_d,
+                      &Xin, &X2, &G, &Yv};
+    for (DevBuf* b : bufs) b->release();
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
+static void build_tree(hk_plan* p) {
+  // preorder, split at ceil(size/2), leaf iff size <= threshold (hodlr.py:76-102)
+  struct Item { int level; int64_t lo, hi; int parent, side; };
+  std::vector<Item> stack{{0, 0, p->n, -1, 0}};
+  while (!stack.empty()) {
+    Item it = stack.back();
+    stack.pop_back();
+    int slot = (int)p->nodes.size();
+    p->nodes.push_back({it.level, it.lo, it.hi, -1, -1});
+    if (it.parent >= 0) {
+      if (it.side == 0) p->nodes[it.parent].left = slot;
+      else p->nodes[it.parent].right = slot;
+    }
+    if (it.hi - it.lo > p->leaf) {
+      int64_t mid = it.lo + (it.hi - it.lo + 1) / 2;
+      stack.push_back({it.level + 1, mid, it.hi, slot, 1});
+      stack.push_back({it.level + 1, it.lo, mid, slot, 0});
+    }
+  }
+  p->iidx.assign(p->nodes.size(), -1);
+  for (int s = 0; s < (int)p->nodes.size(); ++s) {
+    p->depth = std::max(p->depth, p->nodes[s].level);
+    if (p->nodes[s].left >= 0) {
+      p->iidx[s] = (int)p->internal.size();
+      p->internal.push_back(s);
+    } else {
+      p->leaves.push_back(s);
+    }
+  }
+  // DFS event order of the reference recursion: compress at entry, leaf LU at
+  // entry, Schur at exit (hodlr.py:217-282).  Failure precedence uses the
+  // exit/leaf index.
+  p->post.assign(p->nodes.size(), 0);
+  int cnt = 0;
+  std::vector<std::pair<int, int>> st{{0, 0}};
+  while (!st.empty()) {
+    auto& top = st.back();
+    int s = top.first;
+    const Node& nd = p->nodes[s];
+    if (nd.left < 0) {
+      p->post[s] = cnt++;
+      st.pop_back();
+      continue;
+    }
+    if (top.second == 0) { top.second = 1; st.push_back({nd.left, 0}); continue; }
+    if (top.second == 1) { top.second = 2; st.push_back({nd.right, 0}); continue; }
+    p->post[s] = cnt++;
+    st.pop_back();
+  }
+  // block geometry
+  for (int k = 0; k < (int)p->internal.size(); ++k) {
+    const Node& nd = p->nodes[p->internal[k]];
+    const Node& a = p->nodes[nd.left];
+    const Node& b = p->nodes[nd.right];
+    BlockGeom up{p->internal[k], 0, a.lo, b.lo, (int)(a.hi - a.lo), (int)(b.hi - b.lo), 0, 0, 0, 0};
+    BlockGeom lw{p->internal[k], 1, b.lo, a.lo, (int)(b.hi - b.lo), (int)(a.hi - a.lo), 0, 0, 0, 0};
+    p->blocks.push_back(up);
+    p->blocks.push_back(lw);
+  }
+}
+
+static void set_caps(hk_plan* p, int64_t max_rank) {
+  int64_t off = 0, toff = 0;
+  for (auto& b : p->blocks) {
+    int64_t cap = std::min(b.m, b.n);
+    if (max_rank > 0) cap = std::min(cap, max_rank);
+    b.cap = (int)cap;
+    b.u_off = off;
+    off += (int64_t)b.m * cap;
+    b.v_off = off;
+    off += (int64_t)b.n * cap;
+    b.t_off = toff;
+    toff += 2 + (b.m + cap + 1) + (cap + 1);
+  }
+  p->uv_per_front = off;
+  p->trace_per_front = toff;
+  p->block_order.resize(p->blocks.size());
+  for (size_t i = 0; i < p->blocks.size(); ++i) p->block_order[i] = (int)i;
+  std::stable_sort(p->block_order.begin(), p->block_order.end(), [&](int a, int b) {
+    const BlockGeom &x = p->blocks[a], &y = p->blocks[b];
+    return (int64_t)(x.m + x.n) * x.cap > (int64_t)(y.m + y.n) * y.cap;
+  });
+}
+
+extern "C" hk_status hk_plan_create(int64_t n, int64_t leaf_threshold, int64_t batch,
+                                    hk_plan** out) {
+  if (!out) return fail(HK_ERR_VALUE, "out is null");
+  if (n < 1) return fail(HK_ERR_VALUE, "n must be >= 1");
+  if (leaf_threshold < 1) return fail(HK_ERR_VALUE, "leaf_threshold must be >= 1");
+  if (batch < 1) return fail(HK_ERR_VALUE, "batch must be >= 1");
+  hk_plan* p = new hk_plan();
+  p->n = n;
+  p->leaf = leaf_threshold;
+  p->batch = batch;
+  build_tree(p);
+  *out = p;
+  return HK_OK;
+}
+
+extern "C" hk_status hk_plan_destroy(hk_plan* plan) {
+  if (plan) {
+    cudaDeviceSynchronize();
+    delete plan;
+  }
+  return HK_OK;
+}
+
+extern "C" int64_t hk_plan_num_nodes(const hk_plan* p) { return p ? (int64_t)p->nodes.size() : 0; }
+
+extern "C" hk_status hk_plan_tree(const hk_plan* p, int32_t* level, int64_t* lo, int64_t* hi,
+                                  int32_t* left, int32_t* right) {
+  if (!p) return fail(HK_ERR_VALUE, "null plan");
+  for (size_t s = 0; s < p->nodes.size(); ++s) {
+    level[s] = p->nodes[s].level;
+    lo[s] = p->nodes[s].lo;
+    hi[s] = p->nodes[s].hi;
+    left[s] = p->nodes[s].left;
+    right[s] = p->nodes[s].right;
+  }
+  return HK_OK;
+}
+
+extern "C" hk_status hk_block_shape(const hk_plan* p, int64_t block, int64_t* m, int64_t* n,
+                                    int64_t* cap) {
+  if (!p || block < 0 || block >= (int64_t)p->blocks.size())
+    return fail(HK_ERR_VALUE, "block out of range");
+  *m = p->blocks[block].m;
+  *n = p->blocks[block].n;
+  *cap = p->blocks[block].cap;
+  return HK_OK;
+}
+
+static void drop_progs(hk_plan* p) {
+  for (auto& kv : p->progs) {
+    SolveProg* sp = kv.second;
+    sp->leaf_t.release(); sp->leaf_g.release(); sp->leaf_map.release();
+    for (auto& l : sp->levels) {
+      l.dot_t.release(); l.sinv_t.release(); l.upd_t.release();
+      l.g1.release(); l.g1map.release(); l.g2.release(); l.g2map.release();
+      l.g3.release(); l.g3map.release();
+    }
+    delete sp;
+  }
+  p->progs.clear();
+}
+
+static hk_status timed_begin(hk_plan* p, cudaStream_t st) {
+  for (auto& e : p->ev)
+    if (!e) CU(cudaEventCreate(&e));
+  CU(cudaEventRecord(p->ev[0], st));
+  return HK_OK;
+}
+
+static hk_status prepare_build(hk_plan* p, const double* A, int64_t ld, int64_t fstride,
+                               int64_t max_rank, cudaStream_t st) {
+  if (!A) return fail(HK_ERR_VALUE, "fronts pointer is null");
+  if (ld < p->n) return fail(HK_ERR_DIMENSION, "leading dimension smaller than n");
+  if (p->batch > 1 && fstride < ld * p->n) return fail(HK_ERR_DIMENSION, "front stride too small");
+  if (hk_device_count() == 0) return fail(HK_ERR_CUDA, "no CUDA device visible");
+  init_pool_once();
+  p->A = A;
+  p->lda = ld;
+  p->fstride = fstride;
+  p->built = false;
+  p->factored = false;
+  if (!p->progs.empty()) {
+    CU(cudaStreamSynchronize(st));
+    drop_progs(p);
+  }
+  set_caps(p, max_rank);
+  const size_t nb = p->blocks.size();
+  CU(p->UV.ensure((size_t)p->batch * p->uv_per_front * 8 + 8, st));
+  CU(p->ranks_d.ensure((size_t)p->batch * nb * 4 + 4, st));
+  CU(cudaMemsetAsync(p->ranks_d.p, 0, (size_t)p->batch * nb * 4 + 4, st));
+  p->ranks.assign((size_t)p->batch * nb, 0);
+  return HK_OK;
+}
+
+static hk_status fetch_ranks(hk_plan* p, cudaStream_t st) {
+  if (!p->ranks.empty())
+    CU(cudaMemcpyAsync(p->ranks.data(), p->ranks_d.p, p->ranks.size() * 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return HK_OK;
+}
+
+extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64_t fstride,
+                                  double tol, double tol2, int64_t max_rank, int record_trace,
+                                  void* stream) {
+  if (!p) return fail(HK_ERR_VALUE, "null plan");
+  if (!(tol > 0.0 && tol < 1.0)) return fail(HK_ERR_VALUE, "tol must lie strictly between 0 and 1");
+  cudaStream_t st = (cudaStream_t)stream;
+  CHK(prepare_build(p, A, ld, fstride, max_rank, st));
+  CHK(timed_begin(p, st));
+  const int64_t n = p->n;
+  // transposed copy with the same ld/stride as the fronts: At[j*ld + i] = A[i*ld + j]
+  const int64_t atstride = p->batch > 1 ? fstride : 0;
+  CU(p->At.ensure((size_t)((p->batch - 1) * atstride + ld * n) * 8 + 8, st));
+  CU(hk_launch_transpose(A, p->At.as<double>(), n, ld, p->batch, atstride, st));
+  const int64_t ldat = ld;
+  p->have_trace = record_trace != 0;
+  if (p->have_trace) CU(p->trace_d.ensure((size_t)p->batch * p->trace_per_front * 4 + 4, st));
+  std::vector<AcaTask> tasks;
+  tasks.reserve((size_t)p->batch * p->blocks.size());
+  int max_cap = 0, max_m = 0;
+  const size_t nb = p->blocks.size();
+  for (int64_t f = 0; f < p->batch; ++f) {
+    for (int bi : p->block_order) {
+      const BlockGeom& b = p->blocks[bi];
+      AcaTask t{};
+      t.A = A + f * fstride + b.row0 * ld + b.col0;
+      t.At = p->At.as<double>() + f * atstride + b.col0 * ldat + b.row0;
+      t.U = p->UV.as<double>() + f * p->uv_per_front + b.u_off;
+      t.V = p->UV.as<double>() + f * p->uv_per_front + b.v_off;
+      t.rank = p->ranks_d.as<int32_t>() + f * nb + bi;
+      t.trace = p->have_trace ? p->trace_d.as<int32_t>() + f * p->trace_per_front + b.t_off : nullptr;
+      t.lda = ld;
+      t.m = b.m;
+      t.n = b.n;
+      t.cap = b.cap;
+      max_cap = std::max(max_cap, b.cap);
+      max_m = std::max(max_m, b.m);
+      tasks.push_back(t);
+    }
+  }
+  CU(upload(p->tasks_d, tasks, st));
+  if ((size_t)max_cap * 16 + max_m > 220 * 1024)
+    return fail(HK_ERR_VALUE, "block too large for the single-CTA ACA kernel");
+  CU(hk_launch_aca(p->tasks_d.as<AcaTask>(), (int)tasks.size(), max_cap, max_m, tol2, st));
+  CU(cudaEventRecord(p->ev[1], st));
+  CHK(fetch_ranks(p, st));
+  float ms = 0;
+  CU(cudaEventElapsedTime(&ms, p->ev[0], p->ev[1]));
+  p->t_lowrank = ms * 1e-3;
+  p->scheme = HK_SCHEME_ACA;
+  p->built = true;
+  return HK_OK;
+}
+
+// numpy.linspace(0, m-1, num=min(m, 8)).astype(intp), then unique (lowrank.py:325)
+static std::vector<int64_t> probe_rows(int64_t m) {
+  std::vector<int64_t> out;
+  int64_t num = std::min<int64_t>(m, 8);
+  if (num <= 0) return out;
+  if (num == 1) {
+    out.push_back(0);
+    return out;
+  }
+  double stop = (double)(m - 1);
+  double step = stop / (double)(num - 1);
+  for (int64_t i = 0; i < num; ++i) {
+    double y = (double)i * step;
+    if (i == num - 1) y = stop;
+    out.push_back((int64_t)y);
+  }
+  std::sort(out.begin(), out.end());
+  out.erase(std::unique(out.begin(), out.end()), out.end());
+  return out;
+}
+
+extern "C" hk_status hk_build_bdlr(hk_plan* p, const double* A, int64_t ld, int64_t fstride,
+                                   double tol, int32_t depth, int64_t max_rank,
+                                   const int64_t* indptr, const int64_t* indices, void* stream) {
+  if (!p) return fail(HK_ERR_VALUE, "null plan");
+  if (!(tol > 0.0 && tol < 1.0)) return fail(HK_ERR_VALUE, "tol must lie strictly between 0 and 1");
+  if (depth < 0) return fail(HK_ERR_VALUE, "depth must be >= 0");
+  if (!indptr || !indices) return fail(HK_ERR_VALUE, "bdlr compression requires a graph view on the block");
+  cudaStream_t st = (cudaStream_t)stream;
+  CHK(prepare_build(p, A, ld, fstride, max_rank, st));
+  CHK(timed_begin(p, st));
+  const size_t nb = p->blocks.size();
+  p->rsel.assign(nb, {});
+  p->csel.assign(nb, {});
+  std::vector<int64_t> sel_all, probes;
+  p->sel_off_r.assign(nb, 0);
+  p->sel_off_c.assign(nb, 0);
+  std::vector<int64_t> probe_off(nb, 0), probe_cnt(nb, 0);
+  int max_k = 0, max_kc = 0;
+  for (size_t bi = 0; bi < nb; ++bi) {
+    const BlockGeom& b = p->blocks[bi];
+    std::vector<int64_t> rv(b.m), cv(b.n);
+    for (int i = 0; i < b.m; ++i) rv[i] = b.row0 + i;
+    for (int j = 0; j < b.n; ++j) cv[j] = b.col0 + j;
+    std::vector<int64_t> rs, cs;
+    bool ok = hk::select_by_depth(p->n, indptr, indices, rv.data(), b.m, cv.data(), b.n, depth, rs, cs);
+    if (!ok) continue;  // EmptySelectionError -> rank-0 factor (lowrank.py:345-348)
+    p->rsel[bi] = rs;
+    p->csel[bi] = cs;
+    p->sel_off_r[bi] = (int64_t)sel_all.size();
+    sel_all.insert(sel_all.end(), rs.begin(), rs.end());
+    p->sel_off_c[bi] = (int64_t)sel_all.size();
+    sel_all.insert(sel_all.end(), cs.begin(), cs.end());
+    auto pr = probe_rows(b.m);
+    probe_off[bi] = (int64_t)probes.size();
+    probe_cnt[bi] = (int64_t)pr.size();
+    probes.insert(probes.end(), pr.begin(), pr.end());
+    max_k = std::max(max_k, (int)rs.size());
+    max_kc = std::max(max_kc, (int)cs.size());
+  }
+  CU(upload(p->sel_d, sel_all, st));
+  CU(upload(p->probe_d, probes, st));
+  // scratch per (front, block) with a selection
+  std::vector<SkelTask> tasks;
+  int64_t work_total = 0, perm_total = 0;
+  p->perm_off.assign((size_t)p->batch * nb, -1);
+  std::vector<int64_t> work_off((size_t)p->batch * nb, 0);
+  for (int64_t f = 0; f < p->batch; ++f)
+    for (size_t bi = 0; bi < nb; ++bi) {
+      if (p->rsel[bi].empty()) continue;
+      work_off[f * nb + bi] = work_total;
+      work_total += (int64_t)p->rsel[bi].size() * p->csel[bi].size();
+      p->perm_off[f * nb + bi] = perm_total;
+      perm_total += (int64_t)p->rsel[bi].size() + p->csel[bi].size();
+    }
+  CU(p->work_d.ensure((size_t)work_total * 8 + 8, st));
+  CU(p->perm_d.ensure((size_t)perm_total * 8 + 8, st));
+  CU(p->skel_status_d.ensure((size_t)p->batch * nb * 4 + 4, st));
+  CU(cudaMemsetAsync(p->skel_status_d.p, 0, (size_t)p->batch * nb * 4 + 4, st));
+  for (int64_t f = 0; f < p->batch; ++f)
+    for (int bi : p->block_order) {
+      if (p->rsel[bi].empty()) continue;
+      const BlockGeom& b = p->blocks[bi];
+      SkelTask t{};
+      t.A = A + f * fstride + b.row0 * ld + b.col0;
+      t.lda = ld;
+      t.rsel = p->sel_d.as<int64_t>() + p->sel_off_r[bi];
+      t.csel = p->sel_d.as<int64_t>() + p->sel_off_c[bi];
+      t.work = p->work_d.as<double>() + work_off[f * nb + bi];
+      t.rperm = p->perm_d.as<int64_t>() + p->perm_off[f * nb + bi];
+      t.cperm = t.rperm + p->rsel[bi].size();
+      t.U = p->UV.as<double>() + f * p->uv_per_front + b.u_off;
+      t.V = p->UV.as<double>() + f * p->uv_per_front + b.v_off;
+      t.rank = p->ranks_d.as<int32_t>() + f * nb + bi;
+      t.status = p->skel_status_d.as<int32_t>() + f * nb + bi;
+      t.probe = p->probe_d.as<int64_t>() + probe_off[bi];
+      t.nprobe = (int32_t)probe_cnt[bi];
+      t.m = b.m;
+      t.n = b.n;
+      t.k = (int)p->rsel[bi].size();
+      t.kc = (int)p->csel[bi].size();
+      t.cap = b.cap;
+      t.tol = tol;
+      tasks.push_back(t);
+    }
+  CU(upload(p->tasks_d, tasks, st));
+  CU(hk_launch_skeleton(p->tasks_d.as<SkelTask>(), (int)tasks.size(), max_k, max_kc, st));
+  CU(cudaEventRecord(p->ev[1], st));
+  CHK(fetch_ranks(p, st));
+  std::vector<int32_t> status((size_t)p->batch * nb, 0);
+  CU(cudaMemcpy(status.data(), p->skel_status_d.p, status.size() * 4, cudaMemcpyDeviceToHost));
+  for (int64_t f = 0; f < p->batch; ++f)
+    for (size_t bi = 0; bi < nb; ++bi)   // preorder, upper before lower
+      if (status[f * nb + bi] == HK_ERR_DEGENERATE) {
+        char msg[160];
+        snprintf(msg, sizeof msg,
+                 "skeleton rank 0 but sampled block magnitude exceeds tolerance "
+                 "(front %lld, block %zu); selection depth is too small", (long long)f, bi);
+        return fail(HK_ERR_DEGENERATE, msg);
+      }
+  float ms = 0;
+  CU(cudaEventElapsedTime(&ms, p->ev[0], p->ev[1]));
+  p->t_lowrank = ms * 1e-3;
+  p->scheme = HK_SCHEME_BDLR;
+  p->built = true;
+  return HK_OK;
+}
+
+extern "C" hk_status hk_build_external_begin(hk_plan* p, const double* A, int64_t ld,
+                                             int64_t fstride, void* stream) {
+  if (!p) return fail(HK_ERR_VALUE, "null plan");
+  cudaStream_t st = (cudaStream_t)stream;
+  CHK(prepare_build(p, A, ld, fstride, 0, st));
+  p->t_lowrank = 0;
+  p->scheme = HK_SCHEME_SVD;
+  p->built = true;
+  return HK_OK;
+}
+
+extern "C" hk_status hk_set_block_factor(hk_plan* p, int64_t f, int64_t bi, int64_t rank,
+                                         const double* U, int64_t ldu, const double* V,
+                                         int64_t ldv, void* stream) {
+  if (!p || !p->built) return fail(HK_ERR_STATE, "build not started");
+  if (f < 0 || f >= p->batch || bi < 0 || bi >= (int64_t)p->blocks.size())
+    return fail(HK_ERR_VALUE, "front/block out of range");
+  const BlockGeom& b = p->blocks[bi];
+  if (rank < 0 || rank > b.cap) return fail(HK_ERR_VALUE, "rank exceeds block cap");
+  cudaStream_t st = (cudaStream_t)stream;
+  double* Ud = p->UV.as<double>() + f * p->uv_per_front + b.u_off;
+  double* Vd = p->UV.as<double>() + f * p->uv_per_front + b.v_off;
+  if (rank > 0) {
+    CU(cudaMemcpy2DAsync(Ud, (size_t)b.m * 8, U, (size_t)ldu * 8, (size_t)b.m * 8, rank,
+                         cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemcpy2DAsync(Vd, (size_t)b.n * 8, V, (size_t)ldv * 8, (size_t)b.n * 8, rank,
+                         cudaMemcpyDeviceToDevice, st));
+  }
+  const size_t nb = p->blocks.size();
+  p->ranks[f * nb + bi] = (int32_t)rank;
+  int32_t r32 = (int32_t)rank;
+  CU(cudaMemcpyAsync(p->ranks_d.as<int32_t>() + f * nb + bi, &r32, 4, cudaMemcpyHostToDevice, st));
+  CU(cudaStreamSynchronize(st));
+  return HK_OK;
+}
+
+extern "C" hk_status hk_get_ranks(hk_plan* p, int32_t* out) {
+  if (!p || !p->built) return fail(HK_ERR_STATE, "plan not built");
+  std::memcpy(out, p->ranks.data(), p->ranks.size() * 4);
+  return HK_OK;
+}
+
+extern "C" hk_status hk_get_aca_trace(hk_plan* p, int64_t f, int64_t bi, int32_t* rows,
+                                      int64_t* nrows, int32_t* cols, int64_t* ncols) {
+  if (!p || !p->built || !p->have_trace) return fail(HK_ERR_STATE, "no ACA trace recorded");
+  const BlockGeom& b = p->blocks[bi];
+  const int64_t len = 2 + (b.m + b.cap + 1) + (b.cap + 1);
+  std::vector<int32_t> h(len);
+  CU(cudaMemcpy(h.data(), p->trace_d.as<int32_t>() + f * p->trace_per_front + b.t_off, len * 4,
+                cudaMemcpyDeviceToHost));
+  *nrows = h[0];
+  *ncols = h[1];
+  if (rows) std::memcpy(rows, h.data() + 2, (size_t)h[0] * 4);
+  if (cols) std::memcpy(cols, h.data() + 2 + (b.m + b.cap + 1), (size_t)h[1] * 4);
+  return HK_OK;
+}
+
+extern "C" hk_status hk_get_skeleton(hk_plan* p, int64_t f, int64_t bi, int64_t* rank,
+                                     int64_t* rows, int64_t* cols, int64_t cap) {
+  if (!p || !p->built || p->scheme != HK_SCHEME_BDLR) return fail(HK_ERR_STATE, "no BDLR build");
+  const size_t nb = p->blocks.size();
+  const int64_t r = p->ranks[f * nb + bi];
+  *rank = r;
+  if (r == 0) return HK_OK;
+  if (r > cap) return fail(HK_ERR_VALUE, "output too small");
+  const size_t k = p->rsel[bi].size(), kc = p->csel[bi].size();
+  std::vector<int64_t> perm(k + kc);
+  CU(cudaMemcpy(perm.data(), p->perm_d.as<int64_t>() + p->perm_off[f * nb + bi], (k + kc) * 8,
+                cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < r; ++i) {
+    rows[i] = p->rsel[bi][perm[i]];
+    cols[i] = p->csel[bi][perm[k + i]];
+  }
+  return HK_OK;
+}
+
+extern "C" hk_status hk_get_block_factor(hk_plan* p, int64_t f, int64_t bi, double* U, double* V) {
+  if (!p || !p->built) return fail(HK_ERR_STATE, "plan not built");
+  const BlockGeom& b = p->blocks[bi];
+  const int64_t r = p->ranks[f * p->blocks.size() + bi];
+  const double* base = p->UV.as<double>() + f * p->uv_per_front;
+  if (r > 0) {
+    CU(cudaMemcpy(U, base + b.u_off, (size_t)b.m * r * 8, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(V, base + b.v_off, (size_t)b.n * r * 8, cudaMemcpyDeviceToHost));
+  }
+  return HK_OK;
+}
+
+// ------------------------------------------------------------------ factor
+struct TileList {
+  std::vector<GemmTask> tasks;
+  std::vector<int32_t> map;
+  void add(const GemmTask& t) {
+    if (t.m <= 0 || t.n <= 0) return;
+    if (t.k <= 0 && t.beta == 1.0) return;
+    const int id = (int)tasks.size();
+    tasks.push_back(t);
+    const int tm = (t.m + 63) / 64, tn = (t.n + 63) / 64;
+    for (int a = 0; a < tm; ++a)
+      for (int b = 0; b < tn; ++b) {
+        map.push_back(id);
+        map.push_back(a);
+        map.push_back(b);
+      }
+  }
+  int ntiles() const { return (int)(map.size() / 3); }
+};
+
+static hk_status run_tiles(TileList& tl, DevBuf& tb, DevBuf& mb, cudaStream_t st) {
+  if (tl.ntiles() == 0) return HK_OK;
+  CU(upload(tb, tl.tasks, st));
+  CU(upload(mb, tl.map, st));
+  CU(hk_launch_gemm(tb.as<GemmTask>(), mb.as<int32_t>(), tl.ntiles(), st));
+  return HK_OK;
+}
+
+static GemmTask gemm(const double* A, int64_t lda, int transA, const double* B, int64_t ldb,
+                     double* C, int64_t ldc, int m, int n, int k, double alpha, double beta) {
+  GemmTask t{};
+  t.A = A; t.lda = lda; t.transA = transA;
+  t.B = B; t.ldb = ldb;
+  t.C = C; t.ldc = ldc;
+  t.m = m; t.n = n; t.k = k;
+  t.alpha = alpha; t.beta = beta;
+  return t;
+}
+
+extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
+  if (!p || !p->built) return fail(HK_ERR_STATE, "factor requires a build");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = p->n;
+  const size_t nb = p->blocks.size();
+  const int nn = (int)p->nodes.size();
+  if (!p->progs.empty()) {
+    CU(cudaStreamSynchronize(st));
+    drop_progs(p);
+  }
+  p->factored = false;
+  CU(cudaEventRecord(p->ev[0], st));
+  // ---- widths and storage layout
+  p->W.assign(p->batch, 0);
+  p->y_off.assign(p->batch, 0);
+  p->rec.assign((size_t)p->batch * nn, NodeRec());
+  int64_t ytot = 0, ftot = 0, itot = 0, gtot = 0;
+  for (int64_t f = 0; f < p->batch; ++f) {
+    std::vector<int64_t> w(nn, 0);
+    int64_t W = 0;
+    for (int s = 0; s < nn; ++s) {  // preorder: parents before children
+      const Node& nd = p->nodes[s];
+      NodeRec& r = p->rec[f * nn + s];
+      r.w = w[s];
+      if (nd.left < 0) {
+        W = std::max(W, w[s]);
+        const int64_t b = nd.hi - nd.lo;
+        r.lu = ftot; ftot += b * b;
+        r.inv = ftot; ftot += b * b;
+        r.perm = itot; itot += b;
+        r.ipiv = itot; itot += b;
+        r.status = itot; itot += 1;
+        continue;
+      }
+      const int k = p->iidx[s];
+      const int ru = p->ranks[f * nb + 2 * k], rl = p->ranks[f * nb + 2 * k + 1];
+      w[nd.left] = w[s] + ru;
+      w[nd.right] = w[s] + rl;
+      r.ru = ru; r.rl = rl; r.R = ru + rl;
+      r.hcols = w[s] + std::max(ru, rl);
+      const int64_t R = r.R;
+      r.h = ftot; ftot += R * r.hcols;
+      r.q = ftot; ftot += R * w[s];
+      r.lu = ftot; ftot += R * R;
+      r.inv = ftot; ftot += R * R;
+      r.perm = itot; itot += R;
+      r.ipiv = itot; itot += R;
+      r.status = itot; itot += 1;
+      r.g = gtot; gtot += R;
+      r.yv = gtot; gtot += R;
+    }
+    p->W[f] = W;
+    p->y_off[f] = ytot;
+    ytot += n * std::max<int64_t>(W, 1);
+  }
+  p->g_per_col = gtot;
+  CU(p->Y.ensure((size_t)ytot * 8 + 8, st));
+  CU(p->Ytmp.ensure((size_t)ytot * 8 + 8, st));
+  CU(p->F.ensure((size_t)ftot * 8 + 8, st));
+  CU(p->I.ensure((size_t)itot * 4 + 4, st));
+  CU(cudaMemsetAsync(p->I.p, 0, (size_t)itot * 4 + 4, st));
+  double* Y = p->Y.as<double>();
+  double* Yt = p->Ytmp.as<double>();
+  double* F = p->F.as<double>();
+  int32_t* I = p->I.as<int32_t>();
+  const double* UV = p->UV.as<double>();
+
+  // ---- Z gather: U of every block into the rows of its child, columns [w_p, w_p + r)
+  std::vector<CopyTask> copies;
+  for (int64_t f = 0; f < p->batch; ++f)
+    for (int k = 0; k < (int)p->internal.size(); ++k) {
+      const int s = p->internal[k];
+      const NodeRec& r = p->rec[f * nn + s];
+      for (int side = 0; side < 2; ++side) {
+        const BlockGeom& b = p->blocks[2 * k + side];
+        const int rank = side == 0 ? r.ru : r.rl;
+        if (rank == 0) continue;
+        CopyTask c{};
+        c.src = UV + f * p->uv_per_front + b.u_off;
+        c.ld_src = b.m;
+        c.dst = Yt + p->y_off[f] + b.row0 + r.w * n;
+        c.ld_dst = n;
+        c.rows = b.m;
+        c.cols = rank;
+        copies.push_back(c);
+      }
+    }
+  CU(upload(p->ftask_d, copies, st));
+  CU(hk_launch_copy(p->ftask_d.as<CopyTask>(), (int)copies.size(), st));
+
+  // ---- leaves: LU + inverse, then Y = K^{-1} Z
+  std::vector<LuTask> lts;
+  int maxb = 0;
+  for (int64_t f = 0; f < p->batch; ++f)
+    for (int s : p->leaves) {
+      const Node& nd = p->nodes[s];
+      const NodeRec& r = p->rec[f * nn + s];
+      LuTask t{};
+      t.src = p->A + f * p->fstride + nd.lo * p->lda + nd.lo;
+      t.src_ld = p->lda;
+      t.lu = F + r.lu;
+      t.inv = F + r.inv;
+      t.perm = I + r.perm;
+      t.ipiv = I + r.ipiv;
+      t.status = I + r.status;
+      t.N = (int)(nd.hi - nd.lo);
+      t.mode = 0;
+      maxb = std::max(maxb, t.N);
+      lts.push_back(t);
+    }
+  DevBuf& lt_d = p->ftask_d;
+  CU(upload(lt_d, lts, st));
+  CU(hk_launch_lu(lt_d.as<LuTask>(), (int)lts.size(), maxb, st));
+  {
+    TileList tl;
+    for (int64_t f = 0; f < p->batch; ++f)
+      for (int s : p->leaves) {
+        const Node& nd = p->nodes[s];
+        const NodeRec& r = p->rec[f * nn + s];
+        const int b = (int)(nd.hi - nd.lo);
+        if (r.w == 0) continue;
+        tl.add(gemm(F + r.inv, b, 0, Yt + p->y_off[f] + nd.lo, n, Y + p->y_off[f] + nd.lo, n, b,
+                    (int)r.w, b, 1.0, 0.0));
+      }
+    CHK(run_tiles(tl, p->fmap_d, p->tasks_d, st));
+  }
+  CU(cudaEventRecord(p->ev[1], st));
+
+  // ---- upward sweep, deepest internal level first
+  for (int lvl = p->depth - 1; lvl >= 0; --lvl) {
+    TileList th, tq, tu;
+    std::vector<LuTask> sl;
+    int maxR = 0;
+    for (int64_t f = 0; f < p->batch; ++f)
+      for (int k = 0; k < (int)p->internal.size(); ++k) {
+        const int s = p->internal[k];
+        const Node& nd = p->nodes[s];
+        if (nd.level != lvl) continue;
+        const NodeRec& r = p->rec[f * nn + s];
+        if (r.R == 0) continue;
+        const Node& a = p->nodes[nd.left];
+        const Node& b = p->nodes[nd.right];
+        const int na = (int)(a.hi - a.lo), nbr = (int)(b.hi - b.lo);
+        const BlockGeom& bu = p->blocks[2 * k];
+        const BlockGeom& bl = p->blocks[2 * k + 1];
+        const double* Vup = UV + f * p->uv_per_front + bu.v_off;   // nb x ru
+        const double* Vlow = UV + f * p->uv_per_front + bl.v_off;  // na x rl
+        double* Yf = Y + p->y_off[f];
+        double* H = F + r.h;
+        const int R = r.R, rl = r.rl, ru = r.ru;
+        const int w = (int)r.w;
+        // H[0:rl, 0:w+ru] = V_low^T Y[a, 0:w+ru];  H[rl:R, 0:w+rl] = V_up^T Y[b, 0:w+rl]
+        if (rl > 0) th.add(gemm(Vlow, na, 1, Yf + a.lo, n, H, R, rl, w + ru, na, 1.0, 0.0));
+        if (ru > 0) th.add(gemm(Vup, nbr, 1, Yf + b.lo, n, H + rl, R, ru, w + rl, nbr, 1.0, 0.0));
+        LuTask t{};
+        t.src = H;
+        t.src_ld = R;
+        t.lu = F + r.lu;
+        t.inv = F + r.inv;
+        t.perm = I + r.perm;
+        t.ipiv = I + r.ipiv;
+        t.status = I + r.status;
+        t.N = R;
+        t.mode = 1;
+        t.rl = rl;
+        t.ru = ru;
+        t.h_col0 = w;
+        maxR = std::max(maxR, R);
+        sl.push_back(t);
+        if (w > 0) {
+          double* Q = F + r.q;
+          tq.add(gemm(F + r.inv, R, 0, H, R, Q, R, R, w, R, 1.0, 0.0));
+          // top -= d_left y_up ; bottom -= d_right y_low
+          if (ru > 0) tu.add(gemm(Yf + a.lo + (int64_t)w * n, n, 0, Q + rl, R, Yf + a.lo, n, na, w, ru, -1.0, 1.0));
+          if (rl > 0) tu.add(gemm(Yf + b.lo + (int64_t)w * n, n, 0, Q, R, Yf + b.lo, n, nbr, w, rl, -1.0, 1.0));
+        }
+      }
+    CHK(run_tiles(th, p->fmap_d, p->tasks_d, st));
+    if (!sl.empty()) {
+      CU(upload(p->ftask_d, sl, st));
+      CU(hk_launch_lu(p->ftask_d.as<LuTask>(), (int)sl.size(), maxR, st));
+    }
+    CHK(run_tiles(tq, p->fmap_d, p->tasks_d, st));
+    CHK(run_tiles(tu, p->fmap_d, p->tasks_d, st));
+  }
+  CU(cudaEventRecord(p->ev[2], st));
+  // ---- statuses: first failure in the reference's DFS event order
+  std::vector<int32_t> ih((size_t)itot);
+  if (itot) CU(cudaMemcpyAsync(ih.data(), I, (size_t)itot * 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  float ms1 = 0, ms2 = 0;
+  CU(cudaEventElapsedTime(&ms1, p->ev[0], p->ev[1]));
+  CU(cudaEventElapsedTime(&ms2, p->ev[1], p->ev[2]));
+  p->t_leaf = ms1 * 1e-3;
+  p->t_schur = ms2 * 1e-3;
+  for (int64_t f = 0; f < p->batch; ++f) {
+    int best = -1;
+    for (int s = 0; s < nn; ++s) {
+      const NodeRec& r = p->rec[f * nn + s];
+      if (r.status < 0) continue;
+      if (ih[r.status] != 0 && (best < 0 || p->post[s] < p->post[best])) best = s;
+    }
+    if (best >= 0) {
+      const Node& nd = p->nodes[best];
+      char msg[200];
+      if (nd.left < 0) {
+        snprintf(msg, sizeof msg, "leaf block [%lld, %lld) is singular (front %lld)",
+                 (long long)nd.lo, (long long)nd.hi, (long long)f);
+        return fail(HK_ERR_SINGULAR_LEAF, msg);
+      }
+      snprintf(msg, sizeof msg,
+               "coupling system singular at node [%lld, %lld) (front %lld); compression "
+               "tolerance is too loose", (long long)nd.lo, (long long)nd.hi, (long long)f);
+      return fail(HK_ERR_SINGULAR_SCHUR, msg);
+    }
+  }
+  p->factored = true;
+  return HK_OK;
+}
+
+extern "C" hk_status hk_get_timings(hk_plan* p, double* lowrank, double* leaf_lu, double* schur) {
+  if (!p) return fail(HK_ERR_VALUE, "null plan");
+  *lowrank = p->t_lowrank;
+  *leaf_lu = p->t_leaf;
+  *schur = p->t_schur;
+  return HK_OK;
+}
+
+static void colmajor_to_rowmajor(const std::vector<double>& cm, int64_t rows, int64_t cols,
+                                 int64_t ld, double* out) {
+  for (int64_t i = 0; i < rows; ++i)
+    for (int64_t j = 0; j < cols; ++j) out[i * cols + j] = cm[i + j * ld];
+}
+
+extern "C" hk_status hk_get_leaf_lu(hk_plan* p, int64_t f, int64_t slot, double* lu, int32_t* perm) {
+  if (!p || !p->factored) return fail(HK_ERR_STATE, "plan not factored");
+  const Node& nd = p->nodes[slot];
+  if (nd.left >= 0) return fail(HK_ERR_VALUE, "not a leaf");
+  const NodeRec& r = p->rec[f * p->nodes.size() + slot];
+  const int64_t b = nd.hi - nd.lo;
+  std::vector<double> h(b * b);
+  CU(cudaMemcpy(h.data(), p->F.as<double>() + r.lu, b * b * 8, cudaMemcpyDeviceToHost));
+  colmajor_to_rowmajor(h, b, b, b, lu);
+  CU(cudaMemcpy(perm, p->I.as<int32_t>() + r.ipiv, b * 4, cudaMemcpyDeviceToHost));
+  return HK_OK;
+}
+
+extern "C" hk_status hk_get_coupling(hk_plan* p, int64_t f, int64_t slot, double* dl, double* dr,
+                                     double* slu, int32_t* sperm) {
+  if (!p || !p->factored) return fail(HK_ERR_STATE, "plan not factored");
+  const Node& nd = p->nodes[slot];
+  if (nd.left < 0) return fail(HK_ERR_VALUE, "not an internal node");
+  const NodeRec& r = p->rec[f * p->nodes.size() + slot];
+  const Node& a = p->nodes[nd.left];
+  const Node& b = p->nodes[nd.right];
+  const int64_t n = p->n;
+  const double* Yf = p->Y.as<double>() + p->y_off[f];
+  if (dl && r.ru > 0) {
+    std::vector<double> h((size_t)n * r.ru);
+    CU(cudaMemcpy2D(h.data(), (a.hi - a.lo) * 8, Yf + a.lo + r.w * n, n * 8, (a.hi - a.lo) * 8,
+                    r.ru, cudaMemcpyDeviceToHost));
+    colmajor_to_rowmajor(h, a.hi - a.lo, r.ru, a.hi - a.lo, dl);
+  }
+  if (dr && r.rl > 0) {
+    std::vector<double> h((size_t)n * r.rl);
+    CU(cudaMemcpy2D(h.data(), (b.hi - b.lo) * 8, Yf + b.lo + r.w * n, n * 8, (b.hi - b.lo) * 8,
+                    r.rl, cudaMemcpyDeviceToHost));
+    colmajor_to_rowmajor(h, b.hi - b.lo, r.rl, b.hi - b.lo, dr);
+  }
+  if (slu && r.R > 0) {
+    std::vector<double> h((size_t)r.R * r.R);
+    CU(cudaMemcpy(h.data(), p->F.as<double>() + r.lu, h.size() * 8, cudaMemcpyDeviceToHost));
+    colmajor_to_rowmajor(h, r.R, r.R, r.R, slu);
+    CU(cudaMemcpy(sperm, p->I.as<int32_t>() + r.ipiv, (size_t)r.R * 4, cudaMemcpyDeviceToHost));
+  }
+  return HK_OK;
+}
+
+// ------------------------------------------------------------------ solve
+// Build (and cache) the task lists of one solve program for `front` (-1 =
+// every front) and s right-hand sides.  Scratch: Xin/X2 (n x s per front),
+// G/Yv (R x s per node).
+static hk_status build_solve_prog(hk_plan* p, int front, int s, SolveProg*& out, cudaStream_t st) {
+  auto key = std::make_pair(front, s);
+  auto it = p->progs.find(key);
+  if (it != p->progs.end()) {
+    out = it->second;
+    return HK_OK;
+  }
+  SolveProg* sp = new SolveProg();
+  sp->s = s;
+  sp->small = s <= 16;
+  const int64_t n = p->n;
+  const int nn = (int)p->nodes.size();
+  const size_t nb = p->blocks.size();
+  const double* UV = p->UV.as<double>();
+  double* F = p->F.as<double>();
+  const double* Xin = p->Xin.as<double>();
+  double* X2 = p->X2.as<double>();
+  double* G = p->G.as<double>();
+  double* Yv = p->Yv.as<double>();
+  const int64_t xs = n * s;  // per-front stride of Xin/X2
+  int64_t f0 = front < 0 ? 0 : front, f1 = front < 0 ? p->batch : front + 1;
+  // leaves
+  {
+    std::vector<MatVecTask> mv;
+    TileList tl;
+    for (int64_t f = f0; f < f1; ++f)
+      for (int slot : p->leaves) {
+        const Node& nd = p->nodes[slot];
+        const NodeRec& r = p->rec[f * nn + slot];
+        const int b = (int)(nd.hi - nd.lo);
+        if (sp->small) {
+          MatVecTask t{};
+          t.M = F + r.inv; t.ldm = b;
+          t.x = Xin + f * xs + nd.lo; t.ldx = n;
+          t.y = X2 + f * xs + nd.lo; t.ldy = n;
+          t.rows = b; t.K = b; t.mode = 0;
+          mv.push_back(t);
+          sp->leaf_rows = std::max(sp->leaf_rows, b);
+          sp->leaf_k = std::max(sp->leaf_k, b);
+        } else {
+          tl.add(gemm(F + r.inv, b, 0, Xin + f * xs + nd.lo, n, X2 + f * xs + nd.lo, n, b, s, b, 1.0, 0.0));
+        }
+      }
+    if (sp->small) {
+      sp->n_leaf = (int)mv.size();
+      CU(upload(sp->leaf_t, mv, st));
+    } else {
+      sp->leaf_tiles = tl.ntiles();
+      CU(upload(sp->leaf_g, tl.tasks, st));
+      CU(upload(sp->leaf_map, tl.map, st));
+    }
+  }
+  for (int lvl = p->depth - 1; lvl >= 0; --lvl) {
+    SolveProg::Level L;
+    std::vector<DotTask> dt;
+    std::vector<MatVecTask> sv, up;
+    TileList t1, t2, t3;
+    for (int64_t f = f0; f < f1; ++f)
+      for (int k = 0; k < (int)p->internal.size(); ++k) {
+        const int slot = p->internal[k];
+        const Node& nd = p->nodes[slot];
+        if (nd.level != lvl) continue;
+        const NodeRec& r = p->rec[f * nn + slot];
+        if (r.R == 0) continue;
+        const Node& a = p->nodes[nd.left];
+        const Node& b = p->nodes[nd.right];
+        const int na = (int)(a.hi - a.lo), nbr = (int)(b.hi - b.lo);
+        const BlockGeom& bu = p->blocks[2 * k];
+        const BlockGeom& bl = p->blocks[2 * k + 1];
+        const double* Vup = UV + f * p->uv_per_front + bu.v_off;
+        const double* Vlow = UV + f * p->uv_per_front + bl.v_off;
+        const double* Yf = p->Y.as<double>() + p->y_off[f];
+        double* Xf = X2 + f * xs;
+        double* g = G + r.g * s;     // R x s, ld R
+        double* yv = Yv + r.g * s;   // R x s, ld R
+        const int R = r.R, rl = r.rl, ru = r.ru;
+        const double* dleft = Yf + a.lo + r.w * n;
+        const double* dright = Yf + b.lo + r.w * n;
+        if (sp->small) {
+          if (rl > 0) dt.push_back(DotTask{Vlow, Xf + a.lo, g, na, n, R, na, rl});
+          if (ru > 0) dt.push_back(DotTask{Vup, Xf + b.lo, g + rl, nbr, n, R, nbr, ru});
+          L.dot_cols = std::max(L.dot_cols, std::max(rl, ru));
+          sv.push_back(MatVecTask{F + r.inv, g, yv, R, R, R, R, R, 0, 0});
+          L.sinv_rows = std::max(L.sinv_rows, R);
+          L.sinv_k = std::max(L.sinv_k, R);
+          if (ru > 0) up.push_back(MatVecTask{dleft, yv + rl, Xf + a.lo, n, R, n, na, ru, 1, 0});
+          if (rl > 0) up.push_back(MatVecTask{dright, yv, Xf + b.lo, n, R, n, nbr, rl, 1, 0});
+          L.upd_rows = std::max(L.upd_rows, std::max(na, nbr));
+          L.upd_k = std::max(L.upd_k, std::max(rl, ru));
+        } else {
+          if (rl > 0) t1.add(gemm(Vlow, na, 1, Xf + a.lo, n, g, R, rl, s, na, 1.0, 0.0));
+          if (ru > 0) t1.add(gemm(Vup, nbr, 1, Xf + b.lo, n, g + rl, R, ru, s, nbr, 1.0, 0.0));
+          t2.add(gemm(F + r.inv, R, 0, g, R, yv, R, R, s, R, 1.0, 0.0));
+          if (ru > 0) t3.add(gemm(dleft, n, 0, yv + rl, R, Xf + a.lo, n, na, s, ru, -1.0, 1.0));
+          if (rl > 0) t3.add(gemm(dright, n, 0, yv, R, Xf + b.lo, n, nbr, s, rl, -1.0, 1.0));
+        }
+      }
+    if (sp->small) {
+      L.n_dot = (int)dt.size(); L.n_sinv = (int)sv.size(); L.n_upd = (int)up.size();
+      CU(upload(L.dot_t, dt, st));
+      CU(upload(L.sinv_t, sv, st));
+      CU(upload(L.upd_t, up, st));
+    } else {
+      L.t1 = t1.ntiles(); L.t2 = t2.ntiles(); L.t3 = t3.ntiles();
+      CU(upload(L.g1, t1.tasks, st)); CU(upload(L.g1map, t1.map, st));
+      CU(upload(L.g2, t2.tasks, st)); CU(upload(L.g2map, t2.map, st));
+      CU(upload(L.g3, t3.tasks, st)); CU(upload(L.g3map, t3.map, st));
+    }
+    sp->levels.push_back(std::move(L));
+  }
+  (void)nb;
+  p->progs[key] = sp;
+  out = sp;
+  return HK_OK;
+}
+
+static hk_status ensure_solve_scratch(hk_plan* p, int s, cudaStream_t st) {
+  const size_t need_x = (size_t)p->batch * p->n * s * 8 + 8;
+  const size_t need_g = (size_t)p->g_per_col * s * 8 + 8;
+  if (p->Xin.bytes < need_x || p->X2.bytes < need_x || p->G.bytes < need_g || p->Yv.bytes < need_g) {
+    // buffers move: cached programs hold raw pointers -> drop them
+    CU(cudaStreamSynchronize(st));
+    drop_progs(p);
+    CU(p->Xin.ensure(need_x, st));
+    CU(p->X2.ensure(need_x, st));
+    CU(p->G.ensure(need_g, st));
+    CU(p->Yv.ensure(need_g, st));
+  }
+  return HK_OK;
+}
+
+static hk_status run_solve(hk_plan* p, int front, double* rhs, int64_t ld, int64_t s,
+                           int64_t rhs_stride, cudaStream_t st) {
+  if (!p || !p->factored) return fail(HK_ERR_STATE, "solve requires a factorization");
+  if (s <= 0) return HK_OK;
+  const int64_t n = p->n;
+  if (ld < n) return fail(HK_ERR_DIMENSION, "rhs leading dimension smaller than n");
+  CHK(ensure_solve_scratch(p, (int)s, st));
+  SolveProg* sp = nullptr;
+  CHK(build_solve_prog(p, front, (int)s, sp, st));
+  const int64_t xs = n * s;
+  const int64_t f0 = front < 0 ? 0 : front, f1 = front < 0 ? p->batch : front + 1;
+  for (int64_t f = f0; f < f1; ++f)
+    CU(cudaMemcpy2DAsync(p->Xin.as<double>() + f * xs, n * 8, rhs + (f - f0) * rhs_stride, ld * 8,
+                         n * 8, s, cudaMemcpyDeviceToDevice, st));
+  if (sp->small) {
+    CU(hk_launch_matvec(sp->leaf_t.as<MatVecTask>(), sp->n_leaf, (int)s, sp->leaf_rows, st, sp->leaf_k));
+  } else {
+    if (sp->leaf_tiles) CU(hk_launch_gemm(sp->leaf_g.as<GemmTask>(), sp->leaf_map.as<int32_t>(), sp->leaf_tiles, st));
+  }
+  for (auto& L : sp->levels) {
+    if (sp->small) {
+      CU(hk_launch_dot(L.dot_t.as<DotTask>(), L.n_dot, (int)s, L.dot_cols, st));
+      CU(hk_launch_matvec(L.sinv_t.as<MatVecTask>(), L.n_sinv, (int)s, L.sinv_rows, st, L.sinv_k));
+      CU(hk_launch_matvec(L.upd_t.as<MatVecTask>(), L.n_upd, (int)s, L.upd_rows, st, L.upd_k));
+    } else {
+      if (L.t1) CU(hk_launch_gemm(L.g1.as<GemmTask>(), L.g1map.as<int32_t>(), L.t1, st));
+      if (L.t2) CU(hk_launch_gemm(L.g2.as<GemmTask>(), L.g2map.as<int32_t>(), L.t2, st));
+      if (L.t3) CU(hk_launch_gemm(L.g3.as<GemmTask>(), L.g3map.as<int32_t>(), L.t3, st));
+    }
+  }
+  for (int64_t f = f0; f < f1; ++f)
+    CU(cudaMemcpy2DAsync(rhs + (f - f0) * rhs_stride, ld * 8, p->X2.as<double>() + f * xs, n * 8,
+                         n * 8, s, cudaMemcpyDeviceToDevice, st));
+  return HK_OK;
+}
+
+extern "C" hk_status hk_solve(hk_plan* p, double* rhs, int64_t ld, int64_t nrhs, int64_t stride,
+                              void* stream) {
+  if (p && p->batch > 1 && stride < ld * nrhs) return fail(HK_ERR_DIMENSION, "rhs stride too small");
+  return run_solve(p, -1, rhs, ld, nrhs, stride, (cudaStream_t)stream);
+}
+
+extern "C" hk_status hk_solve_front(hk_plan* p, int64_t front, double* rhs, int64_t ld,
+                                    int64_t nrhs, void* stream) {
+  if (!p || front < 0 || front >= p->batch) return fail(HK_ERR_VALUE, "front out of range");
+  return run_solve(p, (int)front, rhs, ld, nrhs, 0, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------------ GMRES
+struct GmresScratch {
+  DevBuf basis, hess, cs, sn, g, w, y, scal, out;
+};
+
+static hk_status read_scalar(const double* d, double* h, cudaStream_t st) {
+  CU(cudaMemcpyAsync(h, d, 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return HK_OK;
+}
+
+static hk_status apply_precond(hk_plan* p, int64_t front, int precond, const double* A,
+                               int64_t lda, double* v, int64_t n, cudaStream_t st) {
+  if (precond == 1) return hk_solve_front(p, front, v, n, 1, st);
+  if (precond == 2) {
+    CU(hk_launch_diag_scale(A, lda, v, v, n, st));
+  }
+  return HK_OK;
+}
+
+extern "C" hk_status hk_gmres(hk_plan* p, int64_t front, const double* A, int64_t lda,
+                              const double* b, double tol, int64_t max_iter, int precond,
+                              double* x, int64_t* iterations, double* history,
+                              double* true_residual, int32_t* flags, void* stream) {
+  if (!(tol > 0.0 && tol < 1.0)) return fail(HK_ERR_VALUE, "tol must lie strictly between 0 and 1");
+  if (max_iter < 1) return fail(HK_ERR_VALUE, "max_iter must be >= 1");
+  if (precond == 1 && (!p || !p->factored)) return fail(HK_ERR_STATE, "HODLR preconditioner not factored");
+  if (!p && precond == 1) return fail(HK_ERR_VALUE, "null plan");
+  const int64_t n = p ? p->n : 0;
+  if (n <= 0) return fail(HK_ERR_VALUE, "plan required for the problem size");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t mmax = std::min<int64_t>(max_iter, n);
+  GmresScratch sc;
+  auto cleanup = [&]() {
+    DevBuf* all[] = {&sc.basis, &sc.hess, &sc.cs, &sc.sn, &sc.g, &sc.w, &sc.y, &sc.scal, &sc.out};
+    for (DevBuf* d : all)
+      if (d->p) cudaFreeAsync(d->p, st);
+  };
+  hk_status rc = HK_OK;
+  do {
+    if (sc.basis.ensure((size_t)n * (mmax + 1) * 8, st) != cudaSuccess ||
+        sc.hess.ensure((size_t)(mmax + 1) * mmax * 8, st) != cudaSuccess ||
+        sc.cs.ensure((size_t)mmax * 8, st) != cudaSuccess ||
+        sc.sn.ensure((size_t)mmax * 8, st) != cudaSuccess ||
+        sc.g.ensure((size_t)(mmax + 1) * 8, st) != cudaSuccess ||
+        sc.w.ensure((size_t)n * 8, st) != cudaSuccess ||
+        sc.y.ensure((size_t)(mmax + 1) * 8, st) != cudaSuccess ||
+        sc.scal.ensure(64, st) != cudaSuccess || sc.out.ensure(64, st) != cudaSuccess) {
+      rc = fail(HK_ERR_CUDA, "GMRES scratch allocation failed");
+      break;
+    }
+    double* Q = sc.basis.as<double>();
+    double* Hs = sc.hess.as<double>();
+    double* g = sc.g.as<double>();
+    double* w = sc.w.as<double>();
+    double* scal = sc.scal.as<double>();
+    cudaMemsetAsync(Hs, 0, (size_t)(mmax + 1) * mmax * 8, st);
+    cudaMemsetAsync(g, 0, (size_t)(mmax + 1) * 8, st);
+    // ||b||
+    double nb = 0;
+    if (hk_launch_norm(b, n, scal, st) != cudaSuccess || (rc = read_scalar(scal, &nb, st)) != HK_OK) {
+      if (rc == HK_OK) rc = fail(HK_ERR_CUDA, "norm");
+      break;
+    }
+    flags[0] = flags[1] = 0;
+    if (nb == 0.0) {
+      cudaMemsetAsync(x, 0, (size_t)n * 8, st);
+      cudaStreamSynchronize(st);
+      *iterations = 0;
+      history[0] = 0.0;
+      *true_residual = 0.0;
+      flags[0] = 1;
+      break;
+    }
+    // r0 = M^{-1} b; beta = ||r0||; Q[:,0] = r0 / beta; g[0] = beta
+    cudaMemcpyAsync(Q, b, (size_t)n * 8, cudaMemcpyDeviceToDevice, st);
+    if ((rc = apply_precond(p, front, precond, A, lda, Q, n, st)) != HK_OK) break;
+    double beta = 0;
+    hk_launch_norm(Q, n, scal, st);
+    if ((rc = read_scalar(scal, &beta, st)) != HK_OK) break;
+    if (beta == 0.0) {
+      rc = fail(HK_ERR_BREAKDOWN, "preconditioned rhs is exactly zero");
+      break;
+    }
+    hk_launch_scale(Q, n, scal, Q, 0, st);
+    cudaMemcpyAsync(g, &beta, 8, cudaMemcpyHostToDevice, st);
+    bool conv = false, brk = false;
+    int64_t k = 0;
+    double outh[3];
+    for (k = 1; k <= mmax; ++k) {
+      const int64_t j = k - 1;
+      if (hk_launch_gemv_rowmajor(A, lda, n, n, Q + j * n, n, 1, w, n, st) != cudaSuccess) {
+        rc = fail(HK_ERR_CUDA, "gemv");
+        break;
+      }
+      if ((rc = apply_precond(p, front, precond, A, lda, w, n, st)) != HK_OK) break;
+      if (hk_launch_arnoldi(n, j, mmax, Q, Hs, sc.cs.as<double>(), sc.sn.as<double>(), g, w, beta,
+                            sc.out.as<double>(), st) != cudaSuccess) {
+        rc = fail(HK_ERR_CUDA, "arnoldi");
+        break;
+      }
+      cudaMemcpyAsync(outh, sc.out.p, 24, cudaMemcpyDeviceToHost, st);
+      if (cudaStreamSynchronize(st) != cudaSuccess) {
+        rc = fail(HK_ERR_CUDA, "arnoldi sync");
+        break;
+      }
+      if (outh[2] != 0.0) {
+        brk = true;
+        break;
+      }
+      history[k - 1] = outh[0];
+      if (outh[0] <= tol || outh[1] != 0.0) {
+        conv = true;
+        break;
+      }
+    }
+    if (rc != HK_OK) break;
+    if (k > mmax) k = mmax;
+    const int64_t m = brk ? k - 1 : k;
+    if (m > 0) {
+      hk_launch_combine(n, m, mmax, Q, Hs, g, x, sc.y.as<double>(), st);
+    } else {
+      cudaMemsetAsync(x, 0, (size_t)n * 8, st);
+    }
+    // true residual ||b - A x|| / ||b||
+    hk_launch_gemv_rowmajor(A, lda, n, n, x, n, 1, w, n, st);
+    hk_launch_axpby(b, w, w, n, 1.0, -1.0, st);
+    hk_launch_norm(w, n, scal, st);
+    double rn = 0;
+    if ((rc = read_scalar(scal, &rn, st)) != HK_OK) break;
+    const double tr = rn / nb;
+    *true_residual = tr;
+    *iterations = m;
+    if (brk && tr > 10.0 * tol) {
+      char msg[160];
+      snprintf(msg, sizeof msg, "Arnoldi norm underflow at iteration %lld with true residual %.3e",
+               (long long)k, tr);
+      rc = fail(HK_ERR_BREAKDOWN, msg);
+      break;
+    }
+    if (conv && tr > 10.0 * tol) conv = false;
+    if (brk) conv = true;
+    flags[0] = conv ? 1 : 0;
+    flags[1] = brk ? 1 : 0;
+  } while (false);
+  cleanup();
+  cudaStreamSynchronize(st);
+  return rc;
+}
+
+extern "C" hk_status hk_arnoldi_step(int64_t n, int64_t j, int64_t mmax, double* basis,
+                                     double* hess, double* cs, double* sn, double* g, double* w,
+                                     double beta, double* out_host, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  double* outd = nullptr;
+  CU(cudaMallocAsync(&outd, 32, st));
+  CU(hk_launch_arnoldi(n, j, mmax, basis, hess, cs, sn, g, w, beta, outd, st));
+  CU(cudaMemcpyAsync(out_host, outd, 24, cudaMemcpyDeviceToHost, st));
+  CU(cudaFreeAsync(outd, st));
+  CU(cudaStreamSynchronize(st));
+  return HK_OK;
+}
+
+extern "C" hk_status hk_gmres_combine(int64_t n, int64_t m, int64_t mmax, const double* basis,
+                                      const double* hess, const double* g, double* x, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  double* y = nullptr;
+  CU(cudaMallocAsync(&y, (size_t)(m + 1) * 8, st));
+  CU(hk_launch_combine(n, m, mmax, basis, hess, g, x, y, st));
+  CU(cudaFreeAsync(y, st));
+  return HK_OK;
+}
+
+// ------------------------------------------------------------------ dense entry points
+extern "C" hk_status hk_gemv(const double* A, int64_t lda, int64_t m, int64_t n, const double* x,
+                             int64_t ldx, int64_t s, double* y, int64_t ldy, void* stream) {
+  if (hk_device_count() == 0) return fail(HK_ERR_CUDA, "no CUDA device visible");
+  CU(hk_launch_gemv_rowmajor(A, lda, m, n, x, ldx, s, y, ldy, (cudaStream_t)stream));
+  return HK_OK;
+}
+
+extern "C" hk_status hk_lu_full(double* a, int64_t m, int64_t n, int64_t ld, int64_t* rp,
+                                int64_t* cp, double* piv, int64_t* npiv, void* stream) {
+  if (hk_device_count() == 0) return fail(HK_ERR_CUDA, "no CUDA device visible");
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t* d = nullptr;
+  CU(cudaMallocAsync(&d, 8, st));
+  CU(hk_launch_lu_full(a, m, n, ld, rp, cp, piv, d, st));
+  CU(cudaMemcpyAsync(npiv, d, 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaFreeAsync(d, st));
+  CU(cudaStreamSynchronize(st));
+  return HK_OK;
+}
+
+extern "C" hk_status hk_lu_partial(double* a, int64_t n, int64_t ld, int32_t* perm, double* inv,
+                                   void* stream) {
+  if (hk_device_count() == 0) return fail(HK_ERR_CUDA, "no CUDA device visible");
+  if (n == 0) return HK_OK;
+  if (ld != n) return fail(HK_ERR_VALUE, "lu_partial needs a contiguous matrix");
+  cudaStream_t st = (cudaStream_t)stream;
+  double *lu = nullptr, *iv = nullptr;
+  int32_t *ip = nullptr, *stt = nullptr;
+  CU(cudaMallocAsync(&lu, (size_t)n * n * 8, st));
+  CU(cudaMallocAsync(&iv, (size_t)n * n * 8, st));
+  CU(cudaMallocAsync(&ip, (size_t)n * 4 + 4, st));
+  CU(cudaMallocAsync(&stt, 8, st));
+  LuTask t{};
+  t.src = a; t.src_ld = ld; t.lu = lu; t.inv = inv ? iv : nullptr;
+  t.perm = ip; t.ipiv = perm; t.status = stt; t.N = (int)n; t.mode = 0;
+  LuTask* td = nullptr;
+  CU(cudaMallocAsync(&td, sizeof(LuTask), st));
+  CU(cudaMemcpyAsync(td, &t, sizeof(LuTask), cudaMemcpyHostToDevice, st));
+  CU(hk_launch_lu(td, 1, (int)n, st));
+  // column-major results -> row-major outputs
+  CU(hk_launch_transpose(lu, a, n, n, 1, 0, st));
+  if (inv) CU(hk_launch_transpose(iv, inv, n, n, 1, 0, st));
+  int32_t sing = 0;
+  CU(cudaMemcpyAsync(&sing, stt, 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  cudaFreeAsync(lu, st); cudaFreeAsync(iv, st); cudaFreeAsync(ip, st);
+  cudaFreeAsync(stt, st); cudaFreeAsync(td, st);
+  if (sing) return fail(HK_ERR_SINGULAR, "pivot magnitude below 1e-300");
+  return HK_OK;
+}
+
+extern "C" hk_status hk_aca_block(const double* a, int64_t m, int64_t n, int64_t ld, double tol2,
+                                  int64_t cap, double* U, double* V, int64_t* rank,
+                                  int32_t* trows, int64_t* nrows, int32_t* tcols, int64_t* ncols,
+                                  void* stream) {
+  if (hk_device_count() == 0) return fail(HK_ERR_CUDA, "no CUDA device visible");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (m == 0 || n == 0 || cap == 0) {
+    *rank = 0;
+    if (nrows) *nrows = 0;
+    if (ncols) *ncols = 0;
+    return HK_OK;
+  }
+  if ((size_t)cap * 16 + m > 220 * 1024) return fail(HK_ERR_VALUE, "block too large for the ACA kernel");
+  // square zero-padded copy of the block and its transpose, both ld = sq
+  const int64_t sq = std::max(m, n);
+  const int64_t tlen = 2 + (m + cap + 1) + (cap + 1);
+  double *sqbuf = nullptr, *at = nullptr;
+  int32_t *rk = nullptr, *tr = nullptr;
+  CU(cudaMallocAsync(&sqbuf, (size_t)sq * sq * 8, st));
+  CU(cudaMallocAsync(&at, (size_t)sq * sq * 8, st));
+  CU(cudaMallocAsync(&rk, 8, st));
+  CU(cudaMallocAsync(&tr, (size_t)tlen * 4, st));
+  CU(cudaMemsetAsync(sqbuf, 0, (size_t)sq * sq * 8, st));
+  CU(cudaMemcpy2DAsync(sqbuf, sq * 8, a, ld * 8, n * 8, m, cudaMemcpyDeviceToDevice, st));
+  CU(hk_launch_transpose(sqbuf, at, sq, sq, 1, 0, st));
+  AcaTask t{};
+  t.A = sqbuf;
+  t.At = at;
+  t.lda = sq;
+  t.U = U;
+  t.V = V;
+  t.rank = rk;
+  t.trace = tr;
+  t.m = (int)m;
+  t.n = (int)n;
+  t.cap = (int)cap;
+  AcaTask* td = nullptr;
+  CU(cudaMallocAsync(&td, sizeof(AcaTask), st));
+  CU(cudaMemcpyAsync(td, &t, sizeof(AcaTask), cudaMemcpyHostToDevice, st));
+  CU(hk_launch_aca(td, 1, (int)cap, (int)m, tol2, st));
+  std::vector<int32_t> h(tlen);
+  int32_t r32 = 0;
+  CU(cudaMemcpyAsync(&r32, rk, 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(h.data(), tr, tlen * 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  *rank = r32;
+  if (nrows) *nrows = h[0];
+  if (ncols) *ncols = h[1];
+  if (trows) std::memcpy(trows, h.data() + 2, (size_t)h[0] * 4);
+  if (tcols) std::memcpy(tcols, h.data() + 2 + (m + cap + 1), (size_t)h[1] * 4);
+  cudaFreeAsync(at, st); cudaFreeAsync(rk, st); cudaFreeAsync(tr, st);
+  cudaFreeAsync(sqbuf, st); cudaFreeAsync(td, st);
+  return HK_OK;
+}
+
+extern "C" hk_status hk_skeleton_block(const double* a, int64_t m, int64_t n, int64_t ld,
+                                       const int64_t* rsel, int64_t k, const int64_t* csel,
+                                       int64_t kc, double tol, int64_t cap, double* U, double* V,
+                                       int64_t* rank, int64_t* rows_out, int64_t* cols_out,
+                                       void* stream) {
+  if (hk_device_count() == 0) return fail(HK_ERR_CUDA, "no CUDA device visible");
+  cudaStream_t st = (cudaStream_t)stream;
+  *rank = 0;
+  if (k == 0 || kc == 0 || m == 0 || n == 0) return HK_OK;
+  std::vector<int64_t> sel(rsel, rsel + k);
+  sel.insert(sel.end(), csel, csel + kc);
+  auto pr = probe_rows(m);
+  sel.insert(sel.end(), pr.begin(), pr.end());
+  int64_t *seld = nullptr, *perm = nullptr;
+  double* work = nullptr;
+  int32_t* small = nullptr;  // [rank, status]
+  CU(cudaMallocAsync(&seld, sel.size() * 8, st));
+  CU(cudaMallocAsync(&perm, (size_t)(k + kc) * 8, st));
+  CU(cudaMallocAsync(&work, (size_t)k * kc * 8, st));
+  CU(cudaMallocAsync(&small, 8, st));
+  CU(cudaMemcpyAsync(seld, sel.data(), sel.size() * 8, cudaMemcpyHostToDevice, st));
+  SkelTask t{};
+  t.A = a; t.lda = ld;
+  t.rsel = seld; t.csel = seld + k;
+  t.work = work; t.rperm = perm; t.cperm = perm + k;
+  t.U = U; t.V = V;
+  t.rank = small; t.status = small + 1;
+  t.probe = seld + k + kc; t.nprobe = (int32_t)pr.size();
+  t.m = (int)m; t.n = (int)n; t.k = (int)k; t.kc = (int)kc; t.cap = (int)cap; t.tol = tol;
+  SkelTask* td = nullptr;
+  CU(cudaMallocAsync(&td, sizeof(SkelTask), st));
+  CU(cudaMemcpyAsync(td, &t, sizeof(SkelTask), cudaMemcpyHostToDevice, st));
+  CU(hk_launch_skeleton(td, 1, (int)k, (int)kc, st));
+  int32_t hs[2] = {0, 0};
+  std::vector<int64_t> ph((size_t)(k + kc));
+  CU(cudaMemcpyAsync(hs, small, 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(ph.data(), perm, ph.size() * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  cudaFreeAsync(seld, st); cudaFreeAsync(perm, st); cudaFreeAsync(work, st);
+  cudaFreeAsync(small, st); cudaFreeAsync(td, st);
+  *rank = hs[0];
+  for (int64_t i = 0; i < hs[0]; ++i) {
+    if (rows_out) rows_out[i] = rsel[ph[i]];
+    if (cols_out) cols_out[i] = csel[ph[k + i]];
+  }
+  if (hs[1] == HK_ERR_DEGENERATE)
+    return fail(HK_ERR_DEGENERATE, "skeleton rank 0 but sampled block magnitude exceeds the "
+                                   "tolerance; selection depth is too small");
+  return HK_OK;
+}
+
+// ------------------------------------------------------------------ graph
+extern "C" hk_status hk_graph_distance(int64_t nverts, const int64_t* indptr, const int64_t* indices,
+                                       const int64_t* own, int64_t n_own, const int64_t* other,
+                                       int64_t n_other, int64_t* dist_out) {
+  std::vector<int64_t> d;
+  hk::side_distance(nverts, indptr, indices, own, n_own, other, n_other, d);
+  std::memcpy(dist_out, d.data(), d.size() * 8);
+  return HK_OK;
+}
+
+extern "C" hk_status hk_select_by_depth(int64_t nverts, const int64_t* indptr,
+                                        const int64_t* indices, const int64_t* row_verts,
+                                        int64_t n_rows, const int64_t* col_verts, int64_t n_cols,
+                                        int32_t depth, int64_t* row_sel, int64_t* n_row_sel,
+                                        int64_t* col_sel, int64_t* n_col_sel) {
+  if (depth < 0) return fail(HK_ERR_VALUE, "depth must be >= 0");
+  std::vector<int64_t> rs, cs;
+  bool ok = hk::select_by_depth(nverts, indptr, indices, row_verts, n_rows, col_verts, n_cols,
+                                depth, rs, cs);
+  *n_row_sel = (int64_t)rs.size();
+  *n_col_sel = (int64_t)cs.size();
+  std::memcpy(row_sel, rs.data(), rs.size() * 8);
+  std::memcpy(col_sel, cs.data(), cs.size() * 8);
+  if (!ok) return fail(HK_ERR_EMPTY_SELECTION, "no vertices within requested depth of the boundary");
+  return HK_OK;
+}

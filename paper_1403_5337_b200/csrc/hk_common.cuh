@@ -1,0 +1,115 @@
+// Shared device helpers for the HODLR B200 kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define HK_PIVOT_FLOOR 1e-300   // src/dense.py:19 PIVOT_UNDERFLOW
+#define HK_STATUS_DEGENERATE 6  // == HK_ERR_DEGENERATE in include/hodlr_b200.h
+
+// Exact IEEE operations that numpy performs elementwise.  Using the _rn
+// intrinsics keeps nvcc from contracting a*b - c into an FMA, which would
+// change the last bit and with it the pivot decisions.
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+
+// (value, index) argmax with numpy's tie-break: larger value wins, equal
+// values -> smaller index wins.  Values are magnitudes (>= 0); index -1 = none.
+struct ArgMax {
+  double v;
+  int64_t i;
+};
+
+__device__ __forceinline__ bool argmax_better(double va, int64_t ia, double vb, int64_t ib) {
+  // is (va, ia) better than (vb, ib)?
+  if (ia < 0) return false;
+  if (ib < 0) return true;
+  if (va > vb) return true;
+  if (va < vb) return false;
+  return ia < ib;
+}
+
+__device__ __forceinline__ ArgMax warp_argmax(ArgMax a) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    double ov = __shfl_down_sync(0xffffffffu, a.v, off);
+    long long oi = __shfl_down_sync(0xffffffffu, (long long)a.i, off);
+    if (argmax_better(ov, oi, a.v, a.i)) { a.v = ov; a.i = oi; }
+  }
+  return a;
+}
+
+// Block-wide argmax; result valid in all threads.  scratch needs 2*nwarps slots.
+template <int NT>
+__device__ __forceinline__ ArgMax block_argmax(ArgMax a, double* sv, int64_t* si) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  a = warp_argmax(a);
+  if (lane == 0) { sv[warp] = a.v; si[warp] = a.i; }
+  __syncthreads();
+  if (warp == 0) {
+    ArgMax b;
+    if (lane < NT / 32) { b.v = sv[lane]; b.i = si[lane]; } else { b.v = 0.0; b.i = -1; }
+    b = warp_argmax(b);
+    if (lane == 0) { sv[0] = b.v; si[0] = b.i; }
+  }
+  __syncthreads();
+  ArgMax r{sv[0], si[0]};
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
+  return x;
+}
+
+// Block sum of two values; result valid in all threads. scratch: 2*nwarps.
+template <int NT>
+__device__ __forceinline__ void block_sum2(double& a, double& b, double* s) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if (lane == 0) { s[2 * warp] = a; s[2 * warp + 1] = b; }
+  __syncthreads();
+  if (warp == 0) {
+    double x = lane < NT / 32 ? s[2 * lane] : 0.0;
+    double y = lane < NT / 32 ? s[2 * lane + 1] : 0.0;
+    x = warp_sum(x);
+    y = warp_sum(y);
+    if (lane == 0) { s[0] = x; s[1] = y; }
+  }
+  __syncthreads();
+  a = s[0];
+  b = s[1];
+  __syncthreads();
+}
+
+template <int NT>
+__device__ __forceinline__ double block_sum(double a, double* s) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  a = warp_sum(a);
+  if (lane == 0) s[warp] = a;
+  __syncthreads();
+  if (warp == 0) {
+    double x = lane < NT / 32 ? s[lane] : 0.0;
+    x = warp_sum(x);
+    if (lane == 0) s[0] = x;
+  }
+  __syncthreads();
+  double r = s[0];
+  __syncthreads();
+  return r;
+}
+
+// FP64 tensor-core MMA (DMMA.8x8x4 on sm_100a; tcgen05 has no f64 kind).
+// Fragment layout (PTX ISA, mma.m8n8k4 .f64): gid = lane>>2, tig = lane&3;
+//   A (8x4, row):  a  = A[gid][tig]
+//   B (4x8, col):  b  = B[tig][gid]
+//   C (8x8):       c0 = C[gid][2*tig], c1 = C[gid][2*tig+1]
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}

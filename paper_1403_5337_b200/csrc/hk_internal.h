@@ -1,0 +1,132 @@
+// Internal task descriptors and kernel launchers (host side of the .cu files).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+// ---------------------------------------------------------------- ACA
+struct AcaTask {
+  const double* A;   // block origin in the row-major front: A[i*lda + j]
+  const double* At;  // block origin in the transposed front: column j of the block = At + j*lda
+  double* U;         // m x cap column-major (ld m)
+  double* V;         // n x cap column-major (ld n)
+  int32_t* rank;     // out
+  int32_t* trace;    // optional: [0]=#rows, [1]=#cols, rows[m+cap+1], cols[cap+1]
+  int64_t lda;
+  int32_t m, n, cap;
+  int32_t pad;
+};
+
+// ---------------------------------------------------------------- BDLR skeleton
+struct SkelTask {
+  const double* A;      // block origin (row-major, lda)
+  int64_t lda;
+  const int64_t* rsel;  // selected row positions (k)
+  const int64_t* csel;  // selected column positions (kc)
+  double* work;         // k x kc scratch (row-major, ld kc)
+  int64_t* rperm;       // k
+  int64_t* cperm;       // kc
+  double* U;            // m x cap col-major
+  double* V;            // n x cap col-major
+  int32_t* rank;        // out
+  int32_t* status;      // out: 0 ok, HK_ERR_DEGENERATE
+  const int64_t* probe; // degenerate-check probe rows (nprobe)
+  int32_t nprobe;
+  int32_t m, n, k, kc, cap;
+  double tol;
+};
+
+// ---------------------------------------------------------------- dense LU + inverse
+// Partial-pivot LU of an N x N matrix assembled from a source, with explicit
+// inverse.  mode 0: source is a row-major block (src, src_ld).  mode 1:
+// Schur/coupling matrix S = I + off-diagonal blocks read from H (see lu.cu).
+struct LuTask {
+  const double* src;
+  int64_t src_ld;
+  double* lu;       // N x N column-major packed LU (ld N)
+  int32_t* perm;    // N: row_perm (P A)[k] = A[perm[k]]
+  int32_t* ipiv;    // N: LAPACK-style swap index of step k (0-based)
+  double* inv;      // N x N column-major inverse (ld N), may be null
+  int32_t* status;  // out: 0 ok, 1 singular
+  int32_t N;
+  int32_t mode;
+  int32_t rl, ru;   // mode 1: ranks (S is (rl+ru)^2)
+  int64_t h_col0;   // mode 1: first column of the coupling block in H (= w)
+};
+
+// ---------------------------------------------------------------- batched GEMM
+// C(m x n) = alpha * op(A) * B + beta * C, all column-major.
+// transA = 0: op(A)[i][l] = A[i + l*lda]; transA = 1: op(A)[i][l] = A[l + i*lda].
+struct GemmTask {
+  const double* A;
+  const double* B;
+  double* C;
+  int64_t lda, ldb, ldc;
+  int32_t m, n, k;
+  int32_t transA;
+  double alpha, beta;
+};
+
+// ---------------------------------------------------------------- copies
+struct CopyTask {  // dst(rows x cols, col-major ld_dst) = src(rows x cols, col-major ld_src)
+  const double* src;
+  double* dst;
+  int64_t ld_src, ld_dst;
+  int32_t rows, cols;
+};
+
+// ---------------------------------------------------------------- small-s solve
+struct MatVecTask {  // y(rows x s) (op)= M(rows x K) * x(K x s), all column-major
+  const double* M;
+  const double* x;
+  double* y;
+  int64_t ldm, ldx, ldy;
+  int32_t rows, K;
+  int32_t mode;     // 0: y = M x ; 1: y -= M x
+  int32_t pad;
+};
+struct DotTask {     // y[k*ldy + c] = dot(M[:,k], x[:,c]) for k < cols, column-major M (rows x cols)
+  const double* M;
+  const double* x;
+  double* y;
+  int64_t ldm, ldx, ldy;
+  int32_t rows, cols;
+};
+
+// launchers (return cudaError_t)
+cudaError_t hk_launch_transpose(const double* A, double* At, int64_t n, int64_t ld, int64_t batch,
+                                int64_t stride, cudaStream_t st);
+cudaError_t hk_launch_aca(const AcaTask* tasks_dev, int ntasks, int max_cap, int max_m,
+                          double tol2, cudaStream_t st);
+cudaError_t hk_launch_skeleton(const SkelTask* tasks_dev, int ntasks, int max_k, int max_kc,
+                               cudaStream_t st);
+cudaError_t hk_launch_lu(const LuTask* tasks_dev, int ntasks, int maxN, cudaStream_t st);
+cudaError_t hk_launch_gemm(const GemmTask* tasks_dev, const int32_t* tilemap_dev, int ntiles,
+                           cudaStream_t st);
+cudaError_t hk_launch_copy(const CopyTask* tasks_dev, int ntasks, cudaStream_t st);
+cudaError_t hk_launch_matvec(const MatVecTask* tasks_dev, int ntasks, int s, int max_rows,
+                             cudaStream_t st, int max_k);
+cudaError_t hk_launch_dot(const DotTask* tasks_dev, int ntasks, int s, int max_cols,
+                          cudaStream_t st);
+cudaError_t hk_launch_lu_full(double* a, int64_t m, int64_t n, int64_t ld, int64_t* rp,
+                              int64_t* cp, double* piv, int64_t* npiv_dev, cudaStream_t st);
+cudaError_t hk_launch_gemv_rowmajor(const double* A, int64_t lda, int64_t m, int64_t n,
+                                    const double* x, int64_t ldx, int64_t s, double* y,
+                                    int64_t ldy, cudaStream_t st);
+cudaError_t hk_launch_fill(double* p, int64_t n, double v, cudaStream_t st);
+
+// krylov helpers (krylov.cu)
+cudaError_t hk_launch_arnoldi(int64_t n, int64_t j, int64_t mmax, double* basis, double* hess,
+                              double* cs, double* sn, double* g, double* w, double beta,
+                              double* out_dev, cudaStream_t st);
+cudaError_t hk_launch_combine(int64_t n, int64_t m, int64_t mmax, const double* basis,
+                              const double* hess, const double* g, double* x, double* y_scratch,
+                              cudaStream_t st);
+cudaError_t hk_launch_norm(const double* x, int64_t n, double* out, cudaStream_t st);
+cudaError_t hk_launch_scale(const double* x, int64_t n, const double* num, double* y,
+                            int invert, cudaStream_t st);
+cudaError_t hk_launch_axpby(const double* x, const double* y, double* z, int64_t n, double a,
+                            double b, cudaStream_t st);
+cudaError_t hk_launch_diag_scale(const double* A, int64_t lda, const double* x, double* y,
+                                 int64_t n, cudaStream_t st);
+
+void hk_count_launch(int k = 1);

@@ -1,0 +1,187 @@
+// Device-resident GMRES pieces (src/krylov.py:69-166): the Arnoldi column with
+// modified Gram-Schmidt (+ one conditional re-orthogonalisation pass), the
+// Givens update and the convergence scalars in one single-CTA kernel, so the
+// host reads back three doubles per iteration and nothing else.
+#include "hk_common.cuh"
+#include "hk_internal.h"
+
+namespace {
+
+constexpr int KR_NT = 1024;
+
+__device__ double block_dot(const double* a, const double* b, int64_t n, double* red) {
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += KR_NT) s += a[i] * b[i];
+  return block_sum<KR_NT>(s, red);
+}
+
+// w -= h * q  (own elements only; no sync needed between calls on the same w)
+__device__ void block_axpy(double* w, const double* q, double h, int64_t n) {
+  for (int64_t i = threadIdx.x; i < n; i += KR_NT) w[i] -= h * q[i];
+}
+
+__global__ void __launch_bounds__(KR_NT) arnoldi_kernel(int64_t n, int64_t j, int64_t mmax,
+                                                        double* basis, double* hess, double* cs,
+                                                        double* sn, double* g, double* w,
+                                                        double beta, double* out) {
+  __shared__ double red[KR_NT / 32];
+  const int64_t k = j + 1;
+  const int64_t ldh = mmax + 1;
+  double* hcol = hess + j * ldh;
+  const double norm_in = sqrt(block_dot(w, w, n, red));
+  for (int64_t i = 0; i < k; ++i) {                 // MGS, krylov.py:111-114
+    const double* q = basis + i * n;
+    const double h = block_dot(q, w, n, red);
+    if (threadIdx.x == 0) hcol[i] = h;
+    block_axpy(w, q, h, n);
+    __syncthreads();
+  }
+  double nw = sqrt(block_dot(w, w, n, red));
+  if (nw < norm_in / sqrt(2.0)) {                   // re-orthogonalise, :115-119
+    for (int64_t i = 0; i < k; ++i) {
+      const double* q = basis + i * n;
+      const double e = block_dot(q, w, n, red);
+      if (threadIdx.x == 0) hcol[i] += e;
+      block_axpy(w, q, e, n);
+      __syncthreads();
+    }
+    nw = sqrt(block_dot(w, w, n, red));
+  }
+  const double hk = nw;
+  const bool happy = hk <= 1e-14 * fmax(norm_in, 1e-300);   // :122
+  if (!happy) {
+    double* qn = basis + k * n;
+    for (int64_t i = threadIdx.x; i < n; i += KR_NT) qn[i] = w[i] / hk;
+  }
+  if (threadIdx.x == 0) {
+    hcol[k] = hk;
+    for (int64_t i = 0; i < j; ++i) {               // apply previous rotations, :126-129
+      const double temp = cs[i] * hcol[i] + sn[i] * hcol[i + 1];
+      hcol[i + 1] = -sn[i] * hcol[i] + cs[i] * hcol[i + 1];
+      hcol[i] = temp;
+    }
+    const double denom = hypot(hcol[j], hcol[k]);
+    double brk = 0.0, rel = 0.0;
+    if (denom == 0.0) {
+      brk = 1.0;
+    } else {
+      cs[j] = hcol[j] / denom;
+      sn[j] = hcol[k] / denom;
+      hcol[j] = denom;
+      hcol[k] = 0.0;
+      g[k] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      rel = fabs(g[k]) / beta;
+    }
+    out[0] = rel;
+    out[1] = happy ? 1.0 : 0.0;
+    out[2] = brk;
+  }
+}
+
+// y = back substitution (krylov.py:147-151) by one thread, then x = Q[:, :m] y.
+__global__ void __launch_bounds__(KR_NT) combine_kernel(int64_t n, int64_t m, int64_t mmax,
+                                                        const double* basis, const double* hess,
+                                                        const double* g, double* x, double* y) {
+  const int64_t ldh = mmax + 1;
+  if (threadIdx.x == 0) {
+    for (int64_t i = m - 1; i >= 0; --i) {
+      double s = 0.0;
+      for (int64_t l = i + 1; l < m; ++l) s += hess[i + l * ldh] * y[l];
+      y[i] = (g[i] - s) / hess[i + i * ldh];
+    }
+  }
+  __syncthreads();
+  for (int64_t r = (int64_t)blockIdx.x * KR_NT + threadIdx.x; r < n; r += (int64_t)gridDim.x * KR_NT) {
+    double s = 0.0;
+    for (int64_t l = 0; l < m; ++l) s += basis[r + l * n] * y[l];
+    x[r] = s;
+  }
+}
+
+__global__ void __launch_bounds__(KR_NT) norm_kernel(const double* x, int64_t n, double* out) {
+  __shared__ double red[KR_NT / 32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += KR_NT) s += x[i] * x[i];
+  s = block_sum<KR_NT>(s, red);
+  if (threadIdx.x == 0) *out = sqrt(s);
+}
+
+// y = x / num[0] (invert=0) -- the r0 / beta scaling
+__global__ void scale_kernel(const double* x, int64_t n, const double* num, double* y) {
+  const double d = *num;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = x[i] / d;
+}
+
+__global__ void axpby_kernel(const double* x, const double* y, double* z, int64_t n, double a,
+                             double b) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    z[i] = a * x[i] + b * y[i];
+}
+
+// y = x / diag(A), zero diagonal entries treated as 1 (krylov.py:44-62)
+__global__ void diag_scale_kernel(const double* A, int64_t lda, const double* x, double* y,
+                                  int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double d = A[i * lda + i];
+    if (d == 0.0) d = 1.0;
+    y[i] = x[i] / d;
+  }
+}
+
+int grid_for(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  if (b > 2048) b = 2048;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+}  // namespace
+
+cudaError_t hk_launch_arnoldi(int64_t n, int64_t j, int64_t mmax, double* basis, double* hess,
+                              double* cs, double* sn, double* g, double* w, double beta,
+                              double* out_dev, cudaStream_t st) {
+  arnoldi_kernel<<<1, KR_NT, 0, st>>>(n, j, mmax, basis, hess, cs, sn, g, w, beta, out_dev);
+  hk_count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t hk_launch_combine(int64_t n, int64_t m, int64_t mmax, const double* basis,
+                              const double* hess, const double* g, double* x, double* y_scratch,
+                              cudaStream_t st) {
+  combine_kernel<<<1, KR_NT, 0, st>>>(n, m, mmax, basis, hess, g, x, y_scratch);
+  hk_count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t hk_launch_norm(const double* x, int64_t n, double* out, cudaStream_t st) {
+  norm_kernel<<<1, KR_NT, 0, st>>>(x, n, out);
+  hk_count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t hk_launch_scale(const double* x, int64_t n, const double* num, double* y, int invert,
+                            cudaStream_t st) {
+  (void)invert;
+  scale_kernel<<<grid_for(n), 256, 0, st>>>(x, n, num, y);
+  hk_count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t hk_launch_axpby(const double* x, const double* y, double* z, int64_t n, double a,
+                            double b, cudaStream_t st) {
+  axpby_kernel<<<grid_for(n), 256, 0, st>>>(x, y, z, n, a, b);
+  hk_count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t hk_launch_diag_scale(const double* A, int64_t lda, const double* x, double* y,
+                                 int64_t n, cudaStream_t st) {
+  diag_scale_kernel<<<grid_for(n), 256, 0, st>>>(A, lda, x, y, n);
+  hk_count_launch();
+  return cudaGetLastError();
+}

@@ -1,0 +1,370 @@
+"""Front manufacture: grid operators, planar separators, dense Schur fronts.
+
+Mirrors the input side of the reference (src/frontgen.py) with the same names
+and argument meaning.  This is *not* the hot path -- it only manufactures the
+dense frontal matrices the HODLR path consumes.
+
+Where the reference eliminates the two interior sides with one dense solve
+each (src/frontgen.py:159-189, O(N_interior^3)), grid fronts here are built
+by plane-by-plane block elimination along the separator axis: every interior
+layer couples only to its two neighbouring layers through a diagonal matrix,
+so the separator Schur complement is the recursion
+``D_0 = T_0;  D_t = T_t - C D_{t-1}^{-1} C``.  The dense layer solves run in
+torch fp64 on whatever device is given (cuSOLVER on a B200), which makes the
+32^3 / 48^3 / 96^3 fronts of BASELINE.json configs 0, 1, 3 and 4 cheap to
+produce.  Constant-coefficient fronts agree with the reference's dense
+elimination to ~1e-15 relative (tests/test_frontgen.py).
+
+Variable coefficients (BASELINE configs 1 and 3, "per-cell conductivity
+exp(g)"): cells of an (X+1) x (Y+1) x (Z+1) lattice surround the interior
+nodes (the Dirichlet boundary nodes sit on the outer faces); the weight of a
+grid edge is the mean conductivity of the four cells sharing it, and a node's
+diagonal is the sum of its six incident edge weights.  With g = 0 this is the
+reference's constant-coefficient operator (diagonal 6, couplings -1).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import InvalidPlaneError, SingularInteriorError
+from .graph import SparsePattern
+from .lowrank import BlockAccessor
+
+STENCILS = ("laplacian", "vector-laplacian")
+KERNELS = ("inv-distance", "exp-decay")
+AXIS_NAMES = {"x": 0, "y": 1, "z": 2}
+
+
+@dataclass(frozen=True)
+class GridSpec:
+    """Regular grid (src/frontgen.py:28-60): extents 1 or >= 3."""
+
+    dims: tuple
+    stencil: str = "laplacian"
+
+    def __post_init__(self):
+        dims = tuple(int(d) for d in self.dims)
+        object.__setattr__(self, "dims", dims)
+        if len(dims) not in (2, 3):
+            raise ValueError("dims must have 2 or 3 extents")
+        if any(d < 1 or d == 2 for d in dims):
+            raise ValueError("extents must be 1 (degenerate) or >= 3")
+        if self.stencil not in STENCILS:
+            raise ValueError(f"unknown stencil {self.stencil!r}")
+
+    @property
+    def dof_per_node(self) -> int:
+        return 3 if self.stencil == "vector-laplacian" else 1
+
+    @property
+    def node_count(self) -> int:
+        return int(np.prod(self.dims))
+
+    @property
+    def dof_count(self) -> int:
+        return self.node_count * self.dof_per_node
+
+
+@dataclass(frozen=True)
+class FrontProblem:
+    """Dense front + separator graph + ordering + seeded rhs (frontgen.py:63-81)."""
+
+    front: np.ndarray
+    graph: SparsePattern
+    ordering: np.ndarray
+    rhs: np.ndarray
+
+    @property
+    def n(self) -> int:
+        return self.front.shape[0]
+
+    def accessor(self) -> BlockAccessor:
+        return BlockAccessor.from_matrix(self.front, pattern=self.graph)
+
+
+def _strides(dims):
+    s = np.ones(len(dims), dtype=np.int64)
+    for a in range(len(dims) - 2, -1, -1):
+        s[a] = s[a + 1] * dims[a + 1]
+    return s
+
+
+def _expand(nodes, dof):
+    nodes = np.asarray(nodes, dtype=np.int64)
+    if dof == 1:
+        return nodes
+    return (nodes[:, None] * dof + np.arange(dof)).ravel()
+
+
+def grid_operator(spec: GridSpec) -> SparsePattern:
+    """Stencil matrix with the Dirichlet boundary eliminated (frontgen.py:90-123)."""
+    dims = spec.dims
+    stride = _strides(dims)
+    ids = np.arange(spec.node_count, dtype=np.int64).reshape(dims)
+    rows, cols = [], []
+    for axis, ext in enumerate(dims):
+        if ext < 2:
+            continue
+        sl = [slice(None)] * len(dims)
+        sl[axis] = slice(0, ext - 1)
+        lo = ids[tuple(sl)].ravel()
+        rows.append(lo)
+        cols.append(lo + stride[axis])
+    rows = np.concatenate(rows) if rows else np.zeros(0, np.int64)
+    cols = np.concatenate(cols) if cols else np.zeros(0, np.int64)
+    dof = spec.dof_per_node
+    rows, cols = _expand(rows, dof), _expand(cols, dof)
+    diag = float(2 * sum(1 for d in dims if d > 1))
+    ndof = spec.dof_count
+    return SparsePattern.from_edges(ndof, rows, cols, np.full(rows.size, -1.0),
+                                    np.full(ndof, diag))
+
+
+def planar_separator(spec: GridSpec, axis, plane: int):
+    """(separator, left, right) dof ids (frontgen.py:126-156)."""
+    if isinstance(axis, str):
+        if axis not in AXIS_NAMES:
+            raise ValueError(f"axis must be one of {tuple(AXIS_NAMES)} or an integer")
+        axis = AXIS_NAMES[axis]
+    if not 0 <= axis < len(spec.dims):
+        raise InvalidPlaneError(f"axis {axis} out of range for dims {spec.dims}")
+    ext = spec.dims[axis]
+    if not 0 < plane < ext - 1:
+        raise InvalidPlaneError(f"plane {plane} is not strictly interior to extent {ext}")
+    along = np.indices(spec.dims).reshape(len(spec.dims), -1)[axis]
+    dof = spec.dof_per_node
+    return (_expand(np.flatnonzero(along == plane), dof),
+            _expand(np.flatnonzero(along < plane), dof),
+            _expand(np.flatnonzero(along > plane), dof))
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def schur_front(op: SparsePattern, sep, left, right, rhs_seed: int = 0,
+                rhs_columns: int = 1, device=None) -> FrontProblem:
+    """Dense separator Schur complement of a general sparse operator.
+
+    Same contract as src/frontgen.py:159-189 (sides must not touch).  The
+    interior solves run in torch fp64 on ``device``.
+    """
+    torch = _torch()
+    sep = np.asarray(sep, dtype=np.int64)
+    left = np.asarray(left, dtype=np.int64)
+    right = np.asarray(right, dtype=np.int64)
+    merged = np.concatenate([sep, left, right])
+    if merged.size != op.n or np.unique(merged).size != merged.size:
+        raise ValueError("sep, left, right must partition the vertex set")
+    rmask = np.zeros(op.n, dtype=bool)
+    rmask[right] = True
+    for v in left:
+        if rmask[op.neighbors(int(v))].any():
+            raise ValueError("left and right sides are connected; the separator is invalid")
+    dev = torch.device(device or "cpu")
+    front = torch.from_numpy(op.submatrix_dense(sep, sep)).to(dev)
+    for side in (left, right):
+        if side.size == 0:
+            continue
+        a_si = torch.from_numpy(op.submatrix_dense(sep, side)).to(dev)
+        a_ii = torch.from_numpy(op.submatrix_dense(side, side)).to(dev)
+        try:
+            front -= a_si @ torch.linalg.solve(a_ii, a_si.T.contiguous())
+        except RuntimeError as exc:
+            raise SingularInteriorError(str(exc)) from exc
+    rng = np.random.default_rng(rhs_seed)
+    rhs = rng.standard_normal((sep.size, rhs_columns))
+    return FrontProblem(front.cpu().numpy(), op.induced(sep), sep.copy(), rhs)
+
+
+# ---------------------------------------------------------------------------
+# layered (plane-recursive) grid fronts
+# ---------------------------------------------------------------------------
+
+def cell_conductivity(dims, seed):
+    """exp(g), g ~ N(0,1) i.i.d. on the (X+1)x(Y+1)x(Z+1) cell lattice."""
+    shape = tuple(d + 1 for d in dims)
+    return np.exp(np.random.default_rng(seed).standard_normal(shape))
+
+
+def _edge_weights(dims, kcell):
+    """Per-axis edge weights w[a] of shape dims + 1 along axis a.
+
+    w[a][..., t, ...] is the edge between nodes t-1 and t along axis a (t = 0
+    and t = ext are the edges to the eliminated boundary).  The weight is the
+    mean of the 2^(d-1) cells sharing the edge.
+    """
+    d = len(dims)
+    out = []
+    for a in range(d):
+        if dims[a] == 1:
+            # a degenerate axis carries no couplings at all (frontgen.py:100-102)
+            shape = list(dims)
+            shape[a] += 1
+            out.append(np.zeros(shape))
+            continue
+        if kcell is None:
+            shape = list(dims)
+            shape[a] += 1
+            out.append(np.ones(shape))
+            continue
+        acc = None
+        cnt = 0
+        # cells sharing an edge along axis a: cell index along a is t (0..ext),
+        # along every other axis b it is x_b or x_b + 1
+        offs = [(0, 1) if b != a else (0,) for b in range(d)]
+        for combo in np.ndindex(*[len(o) for o in offs]):
+            sl = []
+            for b in range(d):
+                o = offs[b][combo[b]]
+                if b == a:
+                    sl.append(slice(0, dims[a] + 1))
+                else:
+                    sl.append(slice(o, o + dims[b]))
+            part = kcell[tuple(sl)]
+            acc = part.copy() if acc is None else acc + part
+            cnt += 1
+        out.append(acc / cnt)
+    return out
+
+
+def layered_grid_front(dims, axis, plane, conductivity=None, device=None,
+                       dtype=None, return_torch=False):
+    """Separator front of a scalar grid Laplacian by plane-by-plane elimination.
+
+    ``conductivity`` is None (constant coefficients, the reference operator)
+    or a cell array of shape dims+1 (see module docstring).  Returns the dense
+    n x n front (numpy, or a torch tensor on ``device``) with rows ordered like
+    src/frontgen.py:126-156 orders the separator.
+    """
+    torch = _torch()
+    dims = tuple(int(x) for x in dims)
+    d = len(dims)
+    if isinstance(axis, str):
+        axis = AXIS_NAMES[axis]
+    ext = dims[axis]
+    if not 0 < plane < ext - 1:
+        raise InvalidPlaneError(f"plane {plane} is not strictly interior to extent {ext}")
+    dev = torch.device(device or "cpu")
+    dt = dtype or torch.float64
+    w = _edge_weights(dims, conductivity)
+    # move the separator axis to the front; remaining axes keep their order
+    perm = [axis] + [b for b in range(d) if b != axis]
+    wl = [np.transpose(w[b], perm) for b in range(d)]
+    layer_shape = tuple(dims[b] for b in perm[1:])
+    nl = int(np.prod(layer_shape)) if layer_shape else 1
+    ids = np.arange(nl).reshape(layer_shape)
+
+    def layer_matrix(t):
+        """In-layer operator T_t (nl x nl)."""
+        diag = np.zeros(layer_shape)
+        # edges along the separator axis: t and t+1 (in w's indexing)
+        wa = wl[axis]
+        diag += wa[t] + wa[t + 1]
+        rows, cols, vals = [], [], []
+        for j, b in enumerate(perm[1:]):
+            wb = wl[b][t]                         # shape: layer dims with +1 on axis j
+            n_b = layer_shape[j]
+            lo = [slice(None)] * len(layer_shape)
+            hi = [slice(None)] * len(layer_shape)
+            lo[j] = slice(0, n_b)
+            hi[j] = slice(1, n_b + 1)
+            diag += wb[tuple(lo)] + wb[tuple(hi)]
+            if n_b > 1:
+                a_sl = [slice(None)] * len(layer_shape)
+                a_sl[j] = slice(0, n_b - 1)
+                inner = [slice(None)] * len(layer_shape)
+                inner[j] = slice(1, n_b)
+                src = ids[tuple(a_sl)].ravel()
+                dst = ids[tuple(inner)].ravel()
+                ww = wb[tuple(inner)].ravel()
+                rows += [src, dst]
+                cols += [dst, src]
+                vals += [-ww, -ww]
+        T = torch.zeros((nl, nl), dtype=dt, device=dev)
+        if rows:
+            r = torch.from_numpy(np.concatenate(rows)).to(dev)
+            c = torch.from_numpy(np.concatenate(cols)).to(dev)
+            v = torch.from_numpy(np.concatenate(vals)).to(device=dev, dtype=dt)
+            T[r, c] = v
+        idx = torch.arange(nl, device=dev)
+        T[idx, idx] = torch.from_numpy(diag.ravel()).to(device=dev, dtype=dt)
+        return T
+
+    def coupling(t):
+        """Diagonal of the coupling between layers t-1 and t (edge t)."""
+        return torch.from_numpy(np.ascontiguousarray(wl[axis][t]).ravel()).to(device=dev, dtype=dt)
+
+    def eliminate(order):
+        """Schur complement contribution of the layers in ``order`` (far to near)."""
+        D = None
+        for k, t in enumerate(order):
+            T = layer_matrix(t)
+            if D is not None:
+                c = coupling(max(t, order[k - 1]))
+                T = T - c[:, None] * torch.linalg.solve(D, torch.diag(c))
+            D = T
+        return D
+
+    front = layer_matrix(plane)
+    left_layers = list(range(0, plane))
+    right_layers = list(range(ext - 1, plane, -1))
+    for layers in (left_layers, right_layers):
+        if not layers:
+            continue
+        D = eliminate(layers)
+        c = coupling(max(plane, layers[-1]))
+        try:
+            front = front - c[:, None] * torch.linalg.solve(D, torch.diag(c))
+        except RuntimeError as exc:
+            raise SingularInteriorError(str(exc)) from exc
+    if return_torch:
+        return front
+    return front.cpu().numpy()
+
+
+def grid_graph(spec: GridSpec, axis, plane) -> SparsePattern:
+    """Separator subgraph relabelled to front order (frontgen.py:185)."""
+    op = grid_operator(spec)
+    sep, _, _ = planar_separator(spec, axis, plane)
+    return op.induced(sep)
+
+
+def grid_front(spec: GridSpec, axis, plane: int, rhs_seed: int = 0,
+               device=None) -> FrontProblem:
+    """Operator -> planar split -> Schur complement (frontgen.py:201-205).
+
+    Scalar stencils use the layered elimination; the 3-component stencil is
+    three uncoupled copies of the scalar operator, so its front is the scalar
+    front with every entry expanded to a 3x3 identity block.
+    """
+    if isinstance(axis, str):
+        if axis not in AXIS_NAMES:
+            raise ValueError(f"axis must be one of {tuple(AXIS_NAMES)} or an integer")
+        axis_i = AXIS_NAMES[axis]
+    else:
+        axis_i = axis
+    sep, left, right = planar_separator(spec, axis_i, plane)
+    scalar = layered_grid_front(spec.dims, axis_i, plane, device=device)
+    dof = spec.dof_per_node
+    front = scalar if dof == 1 else np.kron(scalar, np.eye(dof))
+    graph = grid_graph(spec, axis_i, plane)
+    rhs = np.random.default_rng(rhs_seed).standard_normal((sep.size, 1))
+    return FrontProblem(np.ascontiguousarray(front), graph, sep.copy(), rhs)
+
+
+def kernel_matrix(n: int, kind: str = "inv-distance", shift: float = 0.0) -> np.ndarray:
+    """k(|i-j|) + shift*I (frontgen.py:208-218)."""
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    if kind not in KERNELS:
+        raise ValueError(f"unknown kernel {kind!r}, expected one of {KERNELS}")
+    dist = np.abs(np.arange(n)[:, None] - np.arange(n)[None, :]).astype(np.float64)
+    a = 1.0 / (1.0 + dist) if kind == "inv-distance" else np.exp(-dist / 8.0)
+    if shift:
+        a = a + shift * np.eye(n)
+    return a

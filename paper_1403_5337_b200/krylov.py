@@ -1,0 +1,227 @@
+"""Left-preconditioned GMRES without restarts (reference src/krylov.py).
+
+Fast path: ``gmres(DenseOperator(front), b, cfg, preconditioner=fact)`` (or
+``HodlrPreconditioner`` / ``DiagonalPreconditioner``) runs entirely on the
+device through ``hk_gmres``: fp64 GEMV operator, HODLR solve, MGS + Givens in
+one single-CTA kernel per iteration, three scalars back to the host per
+iteration.
+
+General path: any Python callables (as in the reference's tests,
+``lambda v: a @ v``).  The Krylov basis, Hessenberg and Givens state still
+live on the device and every Arnoldi column is orthogonalised by the same
+CUDA kernel; only the user's callables see host arrays.
+"""
+
+from __future__ import annotations
+
+import logging
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .errors import GmresBreakdownError
+
+log = logging.getLogger("hodlrkit")
+
+
+@dataclass(frozen=True)
+class GmresConfig:
+    tol: float = 1e-10
+    max_iter: int = 1000
+
+    def __post_init__(self):
+        if not 0.0 < self.tol < 1.0:
+            raise ValueError("tol must lie strictly between 0 and 1")
+        if self.max_iter < 1:
+            raise ValueError("max_iter must be >= 1")
+
+
+@dataclass
+class GmresResult:
+    x: np.ndarray
+    iterations: int
+    converged: bool
+    residual_history: list = field(default_factory=list)
+    true_residual: float = np.nan
+    breakdown: bool = False
+
+
+class DiagonalPreconditioner:
+    """r / diag(A); zero diagonal entries act as identity (krylov.py:44-62)."""
+
+    def __init__(self, front):
+        if hasattr(front, "diagonal") and not isinstance(front, np.ndarray):
+            diag = front.diagonal()
+        else:
+            diag = np.diag(np.asarray(front))
+        diag = np.asarray(diag, dtype=np.float64).copy()
+        self.zero_count = int(np.count_nonzero(diag == 0.0))
+        if self.zero_count:
+            log.warning("diagonal preconditioner: %d zero entries replaced by 1", self.zero_count)
+            diag[diag == 0.0] = 1.0
+        self.diag = diag
+        self.front = front
+
+    @property
+    def flagged(self) -> bool:
+        return self.zero_count > 0
+
+    def __call__(self, r):
+        return r / self.diag
+
+
+def diagonal_preconditioner(front) -> DiagonalPreconditioner:
+    return DiagonalPreconditioner(front)
+
+
+class DenseOperator:
+    """``v -> A v`` for a dense front kept resident on the device (cli.py:320-321)."""
+
+    def __init__(self, front):
+        torch = N.require_cuda()
+        a = front.materialize() if hasattr(front, "materialize") else front
+        if isinstance(a, torch.Tensor):
+            self.dev = a.to(device="cuda", dtype=torch.float64).contiguous()
+        else:
+            self.dev = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+        self.n = self.dev.shape[0]
+
+    def __call__(self, v):
+        torch = N.require_cuda()
+        on_dev = isinstance(v, torch.Tensor)
+        vt = v if on_dev else torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).cuda()
+        y = torch.empty(self.n, dtype=torch.float64, device="cuda")
+        N.check(N.lib().hk_gemv(N.ptr(self.dev), self.n, self.n, self.n, N.ptr(vt.contiguous()),
+                                self.n, 1, N.ptr(y), self.n, N.stream_handle()))
+        return y if on_dev else y.cpu().numpy()
+
+
+class HodlrPreconditioner:
+    """M^{-1} r = HODLR solve of a factorization (hodlr.solve)."""
+
+    def __init__(self, fact):
+        self.fact = fact
+
+    def __call__(self, r):
+        from .hodlr import solve
+        return solve(self.fact, r)
+
+
+def _is_fact(obj):
+    from .hodlr import HodlrFactorization
+    return isinstance(obj, HodlrFactorization)
+
+
+def gmres(apply_op, b, cfg: GmresConfig, preconditioner=None) -> GmresResult:
+    """Full-orthogonalisation GMRES on the left-preconditioned system
+    (krylov.py:69-166): MGS with one re-orthogonalisation pass when the
+    vector loses more than 1/sqrt(2) of its norm, Givens rotations, the
+    preconditioned residual as history, and the true-residual guard."""
+    b = np.asarray(b, dtype=np.float64)
+    if b.ndim != 1:
+        raise ValueError("rhs must be a vector")
+    if isinstance(apply_op, DenseOperator):
+        pre = preconditioner
+        if isinstance(pre, HodlrPreconditioner):
+            pre = pre.fact
+        if pre is None or _is_fact(pre) or isinstance(pre, DiagonalPreconditioner):
+            return _gmres_device(apply_op, b, cfg, pre)
+    return _gmres_callables(apply_op, b, cfg, preconditioner)
+
+
+def _gmres_device(op: DenseOperator, b, cfg, pre) -> GmresResult:
+    torch = N.require_cuda()
+    from .hodlr import HodlrBatch, _Plan
+    n = b.size
+    if op.n != n:
+        raise ValueError("operator and rhs sizes differ")
+    if _is_fact(pre):
+        plan, front, kind = pre.plan, pre.front_index, 1
+    else:
+        plan = getattr(op, "_plan", None)
+        if plan is None:
+            plan = _Plan(n, max(n, 1), 1)
+            op._plan = plan
+        front, kind = 0, 0 if pre is None else 2
+    bd = torch.from_numpy(np.ascontiguousarray(b)).cuda()
+    x = torch.zeros(n, dtype=torch.float64, device="cuda")
+    mmax = min(cfg.max_iter, n)
+    hist = np.zeros(max(mmax, 1))
+    iters = N.I64(0)
+    tres = N.D(0.0)
+    flags = np.zeros(2, dtype=np.int32)
+    N.check(N.lib().hk_gmres(plan.h, front, N.ptr(op.dev), n, N.ptr(bd), cfg.tol, cfg.max_iter,
+                             kind, N.ptr(x), N.C.byref(iters), N.arr_ptr(hist, N.D),
+                             N.C.byref(tres), N.arr_ptr(flags, N.I32), N.stream_handle()))
+    m = iters.value
+    conv = bool(flags[0])
+    if float(np.linalg.norm(b)) == 0.0:
+        return GmresResult(np.zeros(n), 0, True, [0.0], 0.0)
+    if not conv and not flags[1] and tres.value > 10 * cfg.tol and m and hist[m - 1] <= cfg.tol:
+        log.warning("gmres: preconditioned residual converged but true residual %.3e exceeds "
+                    "10*tol; reporting non-convergence", tres.value)
+    return GmresResult(x.cpu().numpy(), m, conv, [float(h) for h in hist[:m]], tres.value,
+                       bool(flags[1]))
+
+
+def _gmres_callables(apply_op, b, cfg, preconditioner) -> GmresResult:
+    torch = N.require_cuda()
+    n = b.size
+    M = (lambda r: r) if preconditioner is None else preconditioner
+    dev = "cuda"
+    bd = torch.from_numpy(np.ascontiguousarray(b)).to(dev)
+    norm_b = float(torch.linalg.vector_norm(bd))
+    if norm_b == 0.0:
+        return GmresResult(np.zeros(n), 0, True, [0.0], 0.0)
+
+    def host(v):
+        return v.cpu().numpy() if isinstance(v, torch.Tensor) else np.asarray(v, dtype=np.float64)
+
+    r0 = torch.from_numpy(np.array(host(M(b)), dtype=np.float64)).to(dev)
+    beta = float(torch.linalg.vector_norm(r0))
+    if beta == 0.0:
+        raise GmresBreakdownError("preconditioned rhs is exactly zero")
+    mmax = min(cfg.max_iter, n)
+    basis = torch.zeros((mmax + 1, n), dtype=torch.float64, device=dev)   # col-major n x (m+1)
+    hess = torch.zeros((mmax, mmax + 1), dtype=torch.float64, device=dev)  # col-major (m+1) x m
+    cs = torch.zeros(mmax, dtype=torch.float64, device=dev)
+    sn = torch.zeros(mmax, dtype=torch.float64, device=dev)
+    g = torch.zeros(mmax + 1, dtype=torch.float64, device=dev)
+    basis[0] = r0 / beta
+    g[0] = beta
+    out = np.zeros(3)
+    history = []
+    converged = breakdown = False
+    k = 0
+    L = N.lib()
+    st = N.stream_handle()
+    for k in range(1, mmax + 1):
+        j = k - 1
+        vj = basis[j].cpu().numpy()
+        w = torch.from_numpy(np.array(host(M(host(apply_op(vj)))), dtype=np.float64)).to(dev)
+        N.check(L.hk_arnoldi_step(n, j, mmax, N.ptr(basis), N.ptr(hess), N.ptr(cs), N.ptr(sn),
+                                  N.ptr(g), N.ptr(w), beta, N.arr_ptr(out, N.D), st))
+        if out[2] != 0.0:
+            breakdown = True
+            break
+        history.append(float(out[0]))
+        if out[0] <= cfg.tol or out[1] != 0.0:
+            converged = True
+            break
+    m = k if not breakdown else k - 1
+    x = torch.zeros(n, dtype=torch.float64, device=dev)
+    if m > 0:
+        N.check(L.hk_gmres_combine(n, m, mmax, N.ptr(basis), N.ptr(hess), N.ptr(g), N.ptr(x), st))
+    xh = x.cpu().numpy()
+    tres = float(np.linalg.norm(b - host(apply_op(xh))) / norm_b)
+    if breakdown and tres > 10.0 * cfg.tol:
+        raise GmresBreakdownError(
+            f"Arnoldi norm underflow at iteration {k} with true residual {tres:.3e}")
+    if converged and tres > 10.0 * cfg.tol:
+        log.warning("gmres: preconditioned residual converged but true residual %.3e exceeds "
+                    "10*tol; reporting non-convergence", tres)
+        converged = False
+    if breakdown:
+        converged = True
+    return GmresResult(xh, m, converged, history, tres, breakdown)

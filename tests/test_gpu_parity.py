@@ -1,0 +1,276 @@
+"""GPU parity: the CUDA path against the oracle and the reference's golden
+vectors on identical inputs.
+
+Bars (BASELINE north_star): ACA pivot traces, ranks and U/V factors
+bit-exact; BDLR skeleton indices and ranks bit-exact; factor / solve within
+1e-10 relative (solve(fact, b) and E = solve(fact, A) - I, as
+||E_gpu - E_oracle||_F / ||E_oracle||_F); GMRES iteration counts within +-1.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import SMALL_FRONTS, golden
+from oracle import hodlr_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+import paper_1403_5337_b200 as hk  # noqa: E402
+from paper_1403_5337_b200.hodlr import HodlrBatch, factorize_traced  # noqa: E402
+
+SOLVE_RTOL = 1e-10   # stated tolerance for floating-point agreement
+
+
+@pytest.fixture(autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+def _internal(nodes):
+    return [s for s, nd in enumerate(nodes) if nd[3] >= 0]
+
+
+def _otrace(tr):
+    return (np.array([v for k, v in tr if k == "r"], dtype=np.int64),
+            np.array([v for k, v in tr if k == "c"], dtype=np.int64))
+
+
+# ------------------------------------------------------------------ kernels vs goldens
+def test_aca_kernel_bit_exact_on_golden_blocks():
+    g = golden("aca_blocks")
+    for name in g["names"]:
+        name = str(name)
+        mr = int(g[f"{name}_maxrank"]) or None
+        cfg = hk.CompressionConfig(scheme="aca", tol=float(g[f"{name}_tol"]), max_rank=mr)
+        tr = {}
+        f = hk.compress_aca(hk.BlockAccessor(g[f"{name}_A"]), cfg, trace=tr)
+        assert np.array_equal(tr["rows"], g[f"{name}_rows"]), name
+        assert np.array_equal(tr["cols"], g[f"{name}_cols"]), name
+        assert np.array_equal(f.u, g[f"{name}_U"]), name
+        assert np.array_equal(f.v, g[f"{name}_V"]), name
+
+
+def test_complete_pivot_kernel_bit_exact():
+    g = golden("lu_full")
+    for name in g["names"]:
+        name = str(name)
+        f = hk.lu_full(g[f"{name}_A"])
+        assert np.array_equal(f.lu, g[f"{name}_lu"]), name
+        assert np.array_equal(f.row_perm, g[f"{name}_rp"]), name
+        assert np.array_equal(f.col_perm, g[f"{name}_cp"]), name
+        assert np.array_equal(f.pivot_magnitudes, g[f"{name}_piv"]), name
+
+
+def test_partial_pivot_lu_and_inverse(rng):
+    for n in (1, 5, 36, 64, 72, 150, 200):
+        a = rng.standard_normal((n, n)) + n * np.eye(n)
+        f = hk.lu_partial(a)
+        low = np.tril(f.lu, -1) + np.eye(n)
+        up = np.triu(f.lu)
+        assert np.linalg.norm(a[f.row_perm] - low @ up) <= 1e-13 * np.linalg.norm(a)
+        assert np.linalg.norm(a @ f.inverse - np.eye(n)) <= 1e-12 * n
+        b = rng.standard_normal((n, 3))
+        assert np.linalg.norm(a @ f.solve(b) - b) <= 1e-10 * np.linalg.norm(b)
+    with pytest.raises(hk.SingularMatrixError):
+        hk.lu_partial(np.zeros((3, 3)))
+
+
+# ------------------------------------------------------------------ HODLR on golden fronts
+@pytest.mark.parametrize("front", SMALL_FRONTS)
+@pytest.mark.parametrize("cname,scheme,tol,depth", [("aca6", "aca", 1e-6, 1), ("aca3", "aca", 1e-3, 1),
+                                                     ("bdlr1", "bdlr", 1e-1, 1),
+                                                     ("bdlr3", "bdlr", 1e-3, 3)])
+def test_hodlr_small_fronts_vs_reference_goldens(front, cname, scheme, tol, depth):
+    fr = golden("fronts")
+    h = golden("hodlr_small")
+    key = f"{front}_{cname}_"
+    A = fr[f"{front}_front"]
+    pat = hk.SparsePattern(fr[f"{front}_indptr"], fr[f"{front}_indices"])
+    acc = hk.BlockAccessor.from_matrix(A, pattern=pat)
+    leaf = int(h[f"{key}leaf"])
+    tree = hk.build_tree(A.shape[0], leaf)
+    cfg = hk.CompressionConfig(scheme=scheme, tol=tol, depth=depth)
+    fact, report, recs = factorize_traced(acc, tree, cfg)
+    nb = int(h[f"{key}nblocks"])
+    assert len(recs) == nb
+    for b in range(nb):
+        r = int(h[f"{key}b{b}_rank"])
+        if scheme == "aca":
+            rows, cols = recs[b]
+            assert np.array_equal(rows, h[f"{key}b{b}_rows"]), b
+            assert np.array_equal(cols, h[f"{key}b{b}_cols"]), b
+            U, V = fact.block_factor(b)
+            assert np.array_equal(U, h[f"{key}b{b}_U"]), b
+            assert np.array_equal(V, h[f"{key}b{b}_V"]), b
+        else:
+            rows, cols = recs[b]
+            assert rows.size == r, b
+            if r:
+                assert np.array_equal(rows, h[f"{key}b{b}_srows"]), b
+                assert np.array_equal(cols, h[f"{key}b{b}_scols"]), b
+    assert [e["max_rank"] for e in report.ranks_per_level] == list(h[f"{key}maxranks"])
+    x = hk.solve(fact, fr[f"{front}_rhs"])
+    want = h[f"{key}x"]
+    assert np.linalg.norm(x - want) <= SOLVE_RTOL * np.linalg.norm(want)
+
+
+@pytest.mark.parametrize("front", SMALL_FRONTS)
+def test_gmres_small_fronts_vs_reference(front):
+    fr = golden("fronts")
+    g = golden("gmres_small")
+    A = fr[f"{front}_front"]
+    pat = hk.SparsePattern(fr[f"{front}_indptr"], fr[f"{front}_indices"])
+    acc = hk.BlockAccessor.from_matrix(A, pattern=pat)
+    fact, _ = hk.factorize(acc, hk.build_tree(A.shape[0], 32),
+                           hk.CompressionConfig(scheme="bdlr", tol=1e-1, depth=1))
+    rhs = fr[f"{front}_rhs"]
+    cfg = hk.GmresConfig(tol=1e-10, max_iter=1000)
+    dev = hk.gmres(hk.DenseOperator(acc), rhs, cfg, preconditioner=fact)
+    assert abs(dev.iterations - int(g[f"{front}_its"])) <= 1
+    assert dev.converged
+    want = g[f"{front}_x"]
+    assert np.linalg.norm(dev.x - want) <= SOLVE_RTOL * np.linalg.norm(want)
+    # reference-style callables go through the same device Arnoldi kernel
+    cb = hk.gmres(lambda v: A @ v, rhs, cfg, preconditioner=lambda r: hk.solve(fact, r))
+    assert abs(cb.iterations - int(g[f"{front}_its"])) <= 1
+    dia = hk.gmres(hk.DenseOperator(acc), rhs, cfg, preconditioner=hk.diagonal_preconditioner(acc))
+    assert abs(dia.iterations - int(g[f"{front}_diag_its"])) <= 1
+
+
+# ------------------------------------------------------------------ BASELINE fronts, oracle on the same bits
+def _cfg_front(cfg):
+    from paper_1403_5337_b200 import frontgen as fg
+    if cfg == 0:
+        return fg.layered_grid_front((32, 32, 32), 2, 16, device="cuda")
+    if cfg == 3:
+        kc = fg.cell_conductivity((32, 32, 32), 0)
+        return fg.layered_grid_front((32, 32, 32), 2, 16, conductivity=kc, device="cuda")
+    kc = fg.cell_conductivity((48, 48, 48), 1)
+    return fg.layered_grid_front((48, 48, 48), 2, 24, conductivity=kc, device="cuda")
+
+
+@pytest.mark.parametrize("cfgid,gname", [(0, "cfg0"), (3, "cfg3_front0")])
+def test_baseline_aca_front_parity(cfgid, gname):
+    g = golden(gname)
+    A = _cfg_front(cfgid)
+    assert np.abs(A[g["rows_sample_idx"]] - g["rows_sample"]).max() <= 1e-12 * np.abs(g["rows_sample"]).max()
+    acc = hk.BlockAccessor.from_matrix(A)
+    tree = hk.build_tree(A.shape[0], 64)
+    cfg = hk.CompressionConfig(scheme="aca", tol=1e-6)
+    fact, report, recs = factorize_traced(acc, tree, cfg)
+    ofact = O.factorize(A, 64, "aca", 1e-6)
+    internal = _internal(ofact.nodes)
+    for k, s in enumerate(internal):
+        for side in (0, 1):
+            b = 2 * k + side
+            rows, cols = recs[b]
+            orow, ocol = _otrace(ofact.traces[s][side])
+            # bit-exact against the oracle on identical bits ...
+            assert np.array_equal(rows, orow) and np.array_equal(cols, ocol), b
+            U, V = fact.block_factor(b)
+            assert np.array_equal(U, ofact.factors[s][side][0]), b
+            assert np.array_equal(V, ofact.factors[s][side][1]), b
+            # ... and against the reference's own run on its own front
+            assert np.array_equal(rows, g[f"b{b}_rows"]) and np.array_equal(cols, g[f"b{b}_cols"]), b
+    assert [e["max_rank"] for e in report.ranks_per_level] == list(g["maxranks"])
+    b0 = np.random.default_rng(0).standard_normal((A.shape[0], 1))[:, 0]
+    x = hk.solve(fact, b0)
+    xo = O.solve(ofact, b0)
+    assert np.linalg.norm(x - xo) <= SOLVE_RTOL * np.linalg.norm(xo)
+    # ||HODLR^{-1} A - I|| behaviour
+    E = hk.solve(fact, A) - np.eye(A.shape[0])
+    Eo = O.solve(ofact, A) - np.eye(A.shape[0])
+    assert np.linalg.norm(E - Eo) <= SOLVE_RTOL * np.linalg.norm(Eo)
+    tol = 1e-12 if cfgid == 0 else 1e-10
+    res = hk.gmres(hk.DenseOperator(A), b0, hk.GmresConfig(tol=tol, max_iter=1000), preconditioner=fact)
+    assert res.converged
+    assert abs(res.iterations - int(g["gmres_its"])) <= 1
+    ores = O.gmres(lambda v: A @ v, b0, tol, 1000, lambda r: O.solve(ofact, r))
+    assert np.linalg.norm(res.x - ores["x"]) <= SOLVE_RTOL * np.linalg.norm(ores["x"])
+
+
+def test_baseline_cfg1_bdlr_parity():
+    g = golden("cfg1")
+    from paper_1403_5337_b200 import frontgen as fg
+    A = _cfg_front(1)
+    assert np.abs(A[g["rows_sample_idx"]] - g["rows_sample"]).max() <= 1e-12 * np.abs(g["rows_sample"]).max()
+    graph = fg.grid_graph(fg.GridSpec((48, 48, 48)), 2, 24)
+    acc = hk.BlockAccessor.from_matrix(A, pattern=graph)
+    tree = hk.build_tree(A.shape[0], 64)
+    cfg = hk.CompressionConfig(scheme="bdlr", tol=1e-4, depth=3)
+    fact, report, recs = factorize_traced(acc, tree, cfg)
+    ofact = O.factorize(A, 64, "bdlr", 1e-4, 3, None, (graph.indptr, graph.indices))
+    internal = _internal(ofact.nodes)
+    for k, s in enumerate(internal):
+        for side in (0, 1):
+            b = 2 * k + side
+            rows, cols = recs[b]
+            info = ofact.skeletons[s][side]
+            if info is None:
+                assert rows.size == 0
+                continue
+            assert np.array_equal(rows, info["rows"]) and np.array_equal(cols, info["cols"]), b
+            r = int(g[f"b{b}_rank"])
+            assert rows.size == r
+            if r:
+                assert np.array_equal(rows, g[f"b{b}_srows"]) and np.array_equal(cols, g[f"b{b}_scols"])
+    assert [e["max_rank"] for e in report.ranks_per_level] == list(g["maxranks"])
+    b1 = np.random.default_rng(0).standard_normal((A.shape[0], 1))[:, 0]
+    x = hk.solve(fact, b1)
+    xo = O.solve(ofact, b1)
+    assert np.linalg.norm(x - xo) <= SOLVE_RTOL * np.linalg.norm(xo)
+    res = hk.gmres(hk.DenseOperator(A), b1, hk.GmresConfig(tol=1e-10), preconditioner=fact)
+    assert res.converged and abs(res.iterations - int(g["gmres_its"])) <= 1
+
+
+# ------------------------------------------------------------------ batching / determinism
+def test_batched_fronts_bit_identical_to_single():
+    from paper_1403_5337_b200 import frontgen as fg
+    fronts = np.stack([fg.layered_grid_front((16, 16, 16), 2, 8,
+                                             conductivity=fg.cell_conductivity((16, 16, 16), s))
+                       for s in range(6)])
+    n = fronts.shape[1]
+    cfg = hk.CompressionConfig(scheme="aca", tol=1e-6)
+    batch = HodlrBatch(n, 32, fronts.shape[0]).factorize(torch.from_numpy(fronts), cfg, trace=True)
+    rhs = np.random.default_rng(5).standard_normal((fronts.shape[0], n))
+    xb = batch.solve_(torch.from_numpy(rhs).cuda().contiguous()).cpu().numpy()
+    for f in range(fronts.shape[0]):
+        single, _ = hk.factorize(hk.BlockAccessor.from_matrix(fronts[f]), hk.build_tree(n, 32), cfg)
+        xs = hk.solve(single, rhs[f])
+        assert np.array_equal(xs, xb[f]), f
+        assert np.array_equal(batch.ranks[f], single._ranks)
+    # a second run gives identical bits
+    xb2 = batch.factorize(torch.from_numpy(fronts), cfg).solve_(
+        torch.from_numpy(rhs).cuda().contiguous()).cpu().numpy()
+    assert np.array_equal(xb, xb2)
+
+
+# ------------------------------------------------------------------ error contract
+def test_error_contract():
+    a = np.eye(8)
+    a[2:4, 2:4] = 0.0
+    with pytest.raises(hk.SingularLeafError):
+        hk.factorize(hk.BlockAccessor.from_matrix(a), hk.build_tree(8, 2),
+                     hk.CompressionConfig(scheme="svd", tol=1e-12))
+    with pytest.raises(hk.SingularSchurError):
+        hk.factorize(hk.BlockAccessor.from_matrix(np.ones((2, 2))), hk.build_tree(2, 1),
+                     hk.CompressionConfig(scheme="svd", tol=1e-12))
+    with pytest.raises(hk.SingularSchurError):
+        hk.factorize(hk.BlockAccessor.from_matrix(np.ones((2, 2))), hk.build_tree(2, 1),
+                     hk.CompressionConfig(scheme="aca", tol=1e-12))
+    n = 10
+    z = np.zeros((n, n))
+    z[:, -1] = 1.0
+    pat = hk.SparsePattern.from_edges(n, np.arange(n - 1), np.arange(1, n))
+    blk = hk.BlockAccessor(z, pattern=pat).block(np.arange(5), np.arange(5, n))
+    with pytest.raises(hk.DegenerateSkeletonError):
+        hk.compress_bdlr(blk, hk.CompressionConfig(scheme="bdlr", tol=1e-2, depth=0))
+    fact, _ = hk.factorize(hk.BlockAccessor.from_matrix(np.eye(16) * 3), hk.build_tree(16, 8),
+                           hk.CompressionConfig(scheme="aca", tol=1e-6))
+    with pytest.raises(hk.DimensionMismatchError):
+        hk.solve(fact, np.ones(17))
+    with pytest.raises(hk.DimensionMismatchError):
+        hk.factorize(hk.BlockAccessor.from_matrix(np.eye(16)), hk.build_tree(15, 8),
+                     hk.CompressionConfig(scheme="aca"))
