@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""Benchmark: HODLR build+factor+solve fronts/s (BASELINE.json metric) on the
+batched multifrontal level of BASELINE config 3.
+
+Workload (config.workload "cfg3-batched-level"): every GPU owns
+`--fronts-per-gpu` (default 64, the config's 8-GPU shard) independent 32^3
+variable-coefficient fronts (n = 1024, per-cell conductivity exp(g), g ~
+N(0,1) with seed = global front index; see paper_1403_5337_b200/frontgen.py),
+ACA tol 1e-6, leaf 64.  One step = build (ACA of every off-diagonal block of
+every front) + factor + one HODLR solve with one N(0,1) right-hand side
+(seed = front index) per front.  Weak scaling: fronts per GPU is fixed, the
+fronts shard across ranks with no data-path collective.  The 64 resident
+fronts (537 MB) exceed the 126 MB L2, so no L2 flush is needed between steps.
+
+Also reported: GMRES time-to-1e-10 on front 0 with the HODLR preconditioner
+(the second half of the metric), the ACA kernel against the HBM roofline, the
+CPU oracle (a restatement of the reference, tests-pinned) on a bounded
+sample, and the end-to-end number through the public API with host buffers.
+
+`--impl reference` times the reference algorithm on the host cores (the
+oracle port; the reference is pure Python and cannot be installed on the GPU
+box), same metric and config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+METRIC = "HODLR build+factor+solve fronts/sec (cfg3 batched level, fp64) + GMRES time-to-1e-10"
+UNIT = "fronts/s"
+DIMS = (32, 32, 32)
+PLANE = 16
+LEAF = 64
+TOL = 1e-6
+GMRES_TOL = 1e-10
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--fronts-per-gpu", type=int, default=64)
+    ap.add_argument("--cpu-sample", type=int, default=8, help="fronts in the CPU oracle sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def config_dict(args, world):
+    return {"workload": "cfg3-batched-level", "fronts_per_gpu": args.fronts_per_gpu,
+            "total_fronts": args.fronts_per_gpu * world, "n": 1024, "grid": "32^3 variable-k, plane z=16",
+            "scheme": "aca", "tol": TOL, "leaf": LEAF, "rhs_per_front": 1,
+            "parallelism": f"fronts sharded over {world} GPU(s), no collective",
+            "l2": "inputs (fronts_per_gpu x 8.4 MB) exceed the 126 MB L2; no flush"}
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.idx)],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in Path(self.path).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------- inputs
+def make_front(seed, device):
+    from paper_1403_5337_b200 import frontgen as fg
+    kc = fg.cell_conductivity(DIMS, seed)
+    return fg.layered_grid_front(DIMS, 2, PLANE, conductivity=kc, device=device, return_torch=True)
+
+
+def rhs_for(seed, n):
+    return np.random.default_rng(seed).standard_normal(n)
+
+
+# ---------------------------------------------------------------- CPU oracle
+def oracle_front(args_tuple):
+    A, b = args_tuple
+    from oracle import hodlr_oracle as O
+    fact = O.factorize(A, LEAF, "aca", TOL)
+    O.solve(fact, b)
+    return 1
+
+
+def cpu_sample(fronts_host, rhs_host, threads):
+    """Time the oracle (reference restatement) on a bounded sample."""
+    from threadpoolctl import threadpool_limits
+    t0 = time.perf_counter()
+    if threads == 1:
+        with threadpool_limits(1):
+            for A, b in zip(fronts_host, rhs_host):
+                oracle_front((A, b))
+    else:
+        import multiprocessing as mp
+        ctx = mp.get_context("fork")
+        with ctx.Pool(threads, initializer=_limit_blas) as pool:
+            pool.map(oracle_front, list(zip(fronts_host, rhs_host)))
+    return time.perf_counter() - t0
+
+
+def _limit_blas():
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank, _, world = env_rank()
+    if rank != 0:
+        return 0
+    import torch
+    cores = os.cpu_count() or 1
+    gen = min(cores, 16)
+    fronts = [make_front(s, "cpu").numpy() for s in range(gen)]
+    n = fronts[0].shape[0]
+    tasks = [(fronts[i % gen], rhs_for(i % gen, n)) for i in range(cores)]
+    import multiprocessing as mp
+    ctx = mp.get_context("fork")
+    times = []
+    with ctx.Pool(cores, initializer=_limit_blas) as pool:
+        for k in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            pool.map(oracle_front, tasks, chunksize=1)
+            dt = time.perf_counter() - t0
+            if k >= args.warmup:
+                times.append(dt)
+    total = sum(times)
+    value = len(tasks) * len(times) / total
+    del torch
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_dict(args, world), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"{cores} fronts per step (one per core, {gen} distinct "
+                                       "fronts), oracle/hodlr_oracle.py, 1 BLAS thread each"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+def aca_algorithmic_bytes(tree, ranks):
+    """Compulsory bytes of one ACA launch: per block, the
+    r+1 row and column gathers of the pivot chain plus the U/V writes."""
+    total = 0
+    for f in range(ranks.shape[0]):
+        for k, s in enumerate(tree.internal_nodes()):
+            nd = tree.nodes[s]
+            na = tree.nodes[nd.left].size
+            nb = tree.nodes[nd.right].size
+            for side, r in enumerate((ranks[f, 2 * k], ranks[f, 2 * k + 1])):
+                total += 8 * ((int(r) + 1) + int(r)) * (na + nb)
+    return total
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1403_5337_b200 as hk
+    from paper_1403_5337_b200 import _native as N
+    from paper_1403_5337_b200.hodlr import HodlrBatch
+
+    rank, local, world = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    F = args.fronts_per_gpu
+    seeds = range(rank * F, (rank + 1) * F)
+    fronts = torch.stack([make_front(s, dev) for s in seeds]).contiguous()
+    n = fronts.shape[1]
+    rhs = torch.from_numpy(np.stack([rhs_for(s, n) for s in seeds])).to(dev)
+    work = torch.empty_like(rhs)
+    cfg = hk.CompressionConfig(scheme="aca", tol=TOL)
+    batch = HodlrBatch(n, LEAF, F)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        batch.factorize(fronts, cfg)
+        work.copy_(rhs)
+        batch.solve_(work)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    aca_s = 0.0
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    launches0 = N.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+        aca_s += batch.plan.aca_seconds()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = N.launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * F * args.steps / (ms_max * 1e-3)
+
+    # ---- roofline of the dominant kernel (batched ACA, HBM-bound by its compulsory bytes)
+    peaks = {}
+    pk = ROOT / "MEASURED_PEAKS.json"
+    if pk.exists():
+        peaks = json.loads(pk.read_text())
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    ranks = batch.ranks
+    algo = aca_algorithmic_bytes(batch.tree, ranks)
+    aca_avg = aca_s / args.steps
+    achieved = algo / aca_avg / 1e9
+    roof = {"kernel": "aca_kernel (batched ACA, all blocks of all fronts, one launch)",
+            "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+            "frac": achieved / hbm_peak, "traffic": None,
+            "algorithmic_bytes_per_launch": algo, "launch_ms": aca_avg * 1e3,
+            "share_of_step": aca_avg * 1e3 / (ms_max / args.steps),
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk.exists() else "fallback 6.65 TB/s"}
+
+    # ---- GMRES time-to-1e-10 on front 0 (HODLR preconditioner)
+    gm = {}
+    if rank == 0:
+        fact = batch.factorization(0)
+        op = hk.DenseOperator(fronts[0])
+        b0 = rhs[0].cpu().numpy()
+        hk.gmres(op, b0, hk.GmresConfig(tol=GMRES_TOL), preconditioner=fact)   # warm
+        torch.cuda.synchronize()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        res = hk.gmres(op, b0, hk.GmresConfig(tol=GMRES_TOL), preconditioner=fact)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gm = {"time_to_tol_ms": g0.elapsed_time(g1), "iterations": res.iterations,
+              "converged": bool(res.converged), "true_residual": res.true_residual,
+              "front": "cfg3 front 0 (seed 0), HODLR-ACA 1e-6 preconditioner, dense fp64 GEMV"}
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        host_fronts = fronts.cpu().pin_memory()
+        host_rhs = rhs.cpu().pin_memory()
+        host_x = torch.empty_like(host_rhs).pin_memory()
+        dev_fronts = torch.empty_like(fronts)
+
+        def e2e_step():
+            dev_fronts.copy_(host_fronts, non_blocking=True)
+            batch.factorize(dev_fronts, cfg)
+            work.copy_(host_rhs, non_blocking=True)
+            batch.solve_(work)
+            host_x.copy_(work, non_blocking=True)
+
+        for _ in range(args.warmup):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t2 = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * F * args.steps / (float(t2.item()) * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(host_fronts.numel() * 8 + host_rhs.numel() * 8),
+               "d2h_bytes_per_step": int(host_x.numel() * 8),
+               "path": "HodlrBatch.factorize/solve_ (public API) from pinned host buffers"}
+
+    # ---- CPU baseline: the oracle on a bounded sample, rank 0 at N=1 only
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        k = min(args.cpu_sample, F)
+        fh = [fronts[i].cpu().numpy() for i in range(k)]
+        bh = [rhs[i].cpu().numpy() for i in range(k)]
+        secs = cpu_sample(fh, bh, 1)
+        cpu = {"value": k / secs, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"{k} of the {F} fronts, build+factor+solve, oracle/hodlr_oracle.py "
+                         f"(numpy restatement of the reference), 1 thread, {secs:.1f} s"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": config_dict(args, world), "impl": "ours",
+                "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roof,
+                "cpu_baseline": cpu, "gmres": gm,
+                "ranks_per_level_front0": [e["max_rank"] for e in batch.report(0).ranks_per_level]}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

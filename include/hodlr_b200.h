@@ -219,6 +219,10 @@ hk_status hk_select_by_depth(int64_t nverts, const int64_t* indptr, const int64_
  * (keys of SolveReport.timings, hodlr.py:223-281): lowrank, leaf_lu, schur. */
 hk_status hk_get_timings(hk_plan* plan, double* lowrank, double* leaf_lu, double* schur);
 
+/* Device time of the last batched ACA launch alone (seconds), CUDA events
+ * on the plan's stream around the single aca_kernel launch. */
+hk_status hk_get_aca_time(hk_plan* plan, double* seconds);
+
 /* Kernel launches issued by this library since load (evidence counter). */
 int64_t hk_launch_count(void);
 

@@ -60,6 +60,7 @@ SIGNATURES = {
     "hk_select_by_depth": (C.c_int, [I64, PI64, PI64, PI64, I64, PI64, I64, I32, PI64, PI64,
                                      PI64, PI64]),
     "hk_get_timings": (C.c_int, [P, PD, PD, PD]),
+    "hk_get_aca_time": (C.c_int, [P, PD]),
     "hk_launch_count": (I64, []),
 }
 

@@ -186,7 +186,7 @@ struct hk_plan {
   std::map<std::pair<int, int>, SolveProg*> progs;
   DevBuf Xin, X2, G, Yv;
   // timings
-  double t_lowrank = 0, t_leaf = 0, t_schur = 0;
+  double t_lowrank = 0, t_leaf = 0, t_schur = 0, t_aca = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 
   int nblocks() const { return (int)blocks.size(); }
@@ -358,9 +358,14 @@ static void drop_progs(hk_plan* p) {
   p->progs.clear();
 }
 
-static hk_status timed_begin(hk_plan* p, cudaStream_t st) {
+static hk_status ensure_events(hk_plan* p) {
   for (auto& e : p->ev)
     if (!e) CU(cudaEventCreate(&e));
+  return HK_OK;
+}
+
+static hk_status timed_begin(hk_plan* p, cudaStream_t st) {
+  CHK(ensure_events(p));
   CU(cudaEventRecord(p->ev[0], st));
   return HK_OK;
 }
@@ -439,12 +444,15 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
   CU(upload(p->tasks_d, tasks, st));
   if ((size_t)max_cap * 16 + max_m > 220 * 1024)
     return fail(HK_ERR_VALUE, "block too large for the single-CTA ACA kernel");
+  CU(cudaEventRecord(p->ev[3], st));
   CU(hk_launch_aca(p->tasks_d.as<AcaTask>(), (int)tasks.size(), max_cap, max_m, tol2, st));
   CU(cudaEventRecord(p->ev[1], st));
   CHK(fetch_ranks(p, st));
-  float ms = 0;
+  float ms = 0, ms_aca = 0;
   CU(cudaEventElapsedTime(&ms, p->ev[0], p->ev[1]));
+  CU(cudaEventElapsedTime(&ms_aca, p->ev[3], p->ev[1]));
   p->t_lowrank = ms * 1e-3;
+  p->t_aca = ms_aca * 1e-3;
   p->scheme = HK_SCHEME_ACA;
   p->built = true;
   return HK_OK;
@@ -716,6 +724,7 @@ extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
     drop_progs(p);
   }
   p->factored = false;
+  CHK(ensure_events(p));
   CU(cudaEventRecord(p->ev[0], st));
   // ---- widths and storage layout
   p->W.assign(p->batch, 0);
@@ -922,6 +931,12 @@ extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
     }
   }
   p->factored = true;
+  return HK_OK;
+}
+
+extern "C" hk_status hk_get_aca_time(hk_plan* p, double* seconds) {
+  if (!p) return fail(HK_ERR_VALUE, "null plan");
+  *seconds = p->t_aca;
   return HK_OK;
 }
 

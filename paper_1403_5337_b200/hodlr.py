@@ -166,6 +166,11 @@ class _Plan:
         N.check(N.lib().hk_get_ranks(self.h, N.arr_ptr(out, N.I32)))
         return out.reshape(self.batch, nblocks)
 
+    def aca_seconds(self):
+        t = N.D()
+        N.check(N.lib().hk_get_aca_time(self.h, N.C.byref(t)))
+        return t.value
+
     def timings(self):
         a, b, c = N.D(), N.D(), N.D()
         N.check(N.lib().hk_get_timings(self.h, N.C.byref(a), N.C.byref(b), N.C.byref(c)))
