@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 INCLUDE = PKG.parent / "include"
 LIB = PKG / "libhodlr_b200.so"
-SOURCES = ["aca.cu", "lu.cu", "gemm.cu", "solve.cu", "krylov.cu", "api.cpp", "graph.cpp"]
+SOURCES = ["aca.cu", "lu.cu", "gj.cu", "gemm.cu", "solve.cu", "krylov.cu", "api.cpp", "graph.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -126,8 +126,8 @@ struct BlockGeom {
 };
 
 struct NodeRec {  // per (front, node) factor storage
-  int64_t lu = -1, inv = -1, h = -1, q = -1;        // doubles in F pool
-  int64_t perm = -1, ipiv = -1, status = -1;        // ints in I pool
+  int64_t inv = -1, h = -1, q = -1, m = -1;         // doubles in F pool
+  int64_t status = -1;                              // ints in I pool
   int64_t g = -1, yv = -1;                          // solve scratch (doubles) per rhs column
   int R = 0, rl = 0, ru = 0;
   int64_t w = 0, hcols = 0;
@@ -181,7 +181,7 @@ struct hk_plan {
   std::vector<int64_t> W;           // per front
   std::vector<int64_t> y_off;       // per front (doubles)
   std::vector<NodeRec> rec;         // batch * nodes
-  DevBuf Y, Ytmp, F, I, ftask_d, fmap_d;
+  DevBuf Y, Ytmp, F, I, ftask_d, fmap_d, gj_d, gj2_d, gjs_d;
   int64_t g_per_col = 0;            // doubles of G/Yv scratch per rhs column (all fronts)
   std::map<std::pair<int, int>, SolveProg*> progs;
   DevBuf Xin, X2, G, Yv;
@@ -204,7 +204,7 @@ struct hk_plan {
       delete p;
     }
     DevBuf* bufs[] = {&At, &UV, &ranks_d, &trace_d, &tasks_d, &sel_d, &work_d, &perm_d,
-                      &skel_status_d, &probe_d, &Y, &Ytmp, &F, &I, &ftask_d, &fmap_d,
+                      &skel_status_d, &probe_d, &Y, &Ytmp, &F, &I, &ftask_d, &fmap_d, &gj_d, &gj2_d, &gjs_d,
                       &Xin, &X2, &G, &Yv};
     for (DevBuf* b : bufs) b->release();
     for (auto& e : ev)
@@ -703,14 +703,41 @@ static hk_status run_tiles(TileList& tl, DevBuf& tb, DevBuf& mb, cudaStream_t st
 }
 
 static GemmTask gemm(const double* A, int64_t lda, int transA, const double* B, int64_t ldb,
-                     double* C, int64_t ldc, int m, int n, int k, double alpha, double beta) {
+                     double* C, int64_t ldc, int m, int n, int k, double alpha, double beta,
+                     double diag = 0.0) {
   GemmTask t{};
+  t.diag = diag;
   t.A = A; t.lda = lda; t.transA = transA;
   t.B = B; t.ldb = ldb;
   t.C = C; t.ldc = ldc;
   t.m = m; t.n = n; t.k = k;
   t.alpha = alpha; t.beta = beta;
   return t;
+}
+
+// Run batched Gauss-Jordan inversions, SMEM-resident tasks and large tasks
+// (global scratch) in separate launches.
+static hk_status run_gj(hk_plan* p, std::vector<GjTask>& tasks, cudaStream_t st) {
+  if (tasks.empty()) return HK_OK;
+  std::vector<GjTask> small, large;
+  size_t scratch = 0;
+  int ms = 0, ml = 0;
+  for (auto& t : tasks) {
+    size_t b = hk_gj_scratch_bytes(t.N);
+    if (b == 0) { small.push_back(t); ms = std::max(ms, t.N); }
+    else { t.scratch = (double*)(uintptr_t)scratch; scratch += (b + 255) / 256 * 256; large.push_back(t); ml = std::max(ml, t.N); }
+  }
+  if (!small.empty()) {
+    CU(upload(p->gj_d, small, st));
+    CU(hk_launch_gj(p->gj_d.as<GjTask>(), (int)small.size(), ms, st));
+  }
+  if (!large.empty()) {
+    CU(p->gjs_d.ensure(scratch + 256, st));
+    for (auto& t : large) t.scratch = (double*)(p->gjs_d.as<char>() + (uintptr_t)t.scratch);
+    CU(upload(p->gj2_d, large, st));
+    CU(hk_launch_gj(p->gj2_d.as<GjTask>(), (int)large.size(), ml, st));
+  }
+  return HK_OK;
 }
 
 extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
@@ -741,10 +768,7 @@ extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
       if (nd.left < 0) {
         W = std::max(W, w[s]);
         const int64_t b = nd.hi - nd.lo;
-        r.lu = ftot; ftot += b * b;
         r.inv = ftot; ftot += b * b;
-        r.perm = itot; itot += b;
-        r.ipiv = itot; itot += b;
         r.status = itot; itot += 1;
         continue;
       }
@@ -755,12 +779,11 @@ extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
       r.ru = ru; r.rl = rl; r.R = ru + rl;
       r.hcols = w[s] + std::max(ru, rl);
       const int64_t R = r.R;
+      const int64_t sm = std::min(ru, rl);
       r.h = ftot; ftot += R * r.hcols;
       r.q = ftot; ftot += R * w[s];
-      r.lu = ftot; ftot += R * R;
       r.inv = ftot; ftot += R * R;
-      r.perm = itot; itot += R;
-      r.ipiv = itot; itot += R;
+      r.m = ftot; ftot += sm * sm;
       r.status = itot; itot += 1;
       r.g = gtot; gtot += R;
       r.yv = gtot; gtot += R;
@@ -804,30 +827,24 @@ extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
   CU(upload(p->ftask_d, copies, st));
   CU(hk_launch_copy(p->ftask_d.as<CopyTask>(), (int)copies.size(), st));
 
-  // ---- leaves: LU + inverse, then Y = K^{-1} Z
-  std::vector<LuTask> lts;
-  int maxb = 0;
-  for (int64_t f = 0; f < p->batch; ++f)
-    for (int s : p->leaves) {
-      const Node& nd = p->nodes[s];
-      const NodeRec& r = p->rec[f * nn + s];
-      LuTask t{};
-      t.src = p->A + f * p->fstride + nd.lo * p->lda + nd.lo;
-      t.src_ld = p->lda;
-      t.lu = F + r.lu;
-      t.inv = F + r.inv;
-      t.perm = I + r.perm;
-      t.ipiv = I + r.ipiv;
-      t.status = I + r.status;
-      t.N = (int)(nd.hi - nd.lo);
-      t.mode = 0;
-      maxb = std::max(maxb, t.N);
-      lts.push_back(t);
-    }
-  DevBuf& lt_d = p->ftask_d;
-  CU(upload(lt_d, lts, st));
-  CU(hk_launch_lu(lt_d.as<LuTask>(), (int)lts.size(), maxb, st));
+  // ---- leaves: Gauss-Jordan inverse, then Y = K^{-1} Z (hodlr.py:222-232)
   {
+    std::vector<GjTask> gts;
+    for (int64_t f = 0; f < p->batch; ++f)
+      for (int s : p->leaves) {
+        const Node& nd = p->nodes[s];
+        const NodeRec& r = p->rec[f * nn + s];
+        GjTask t{};
+        t.src = p->A + f * p->fstride + nd.lo * p->lda + nd.lo;
+        t.src_ld = p->lda;
+        t.out = F + r.inv;
+        t.out_ld = nd.hi - nd.lo;
+        t.status = I + r.status;
+        t.N = (int)(nd.hi - nd.lo);
+        t.mode = 0;
+        gts.push_back(t);
+      }
+    CHK(run_gj(p, gts, st));
     TileList tl;
     for (int64_t f = 0; f < p->batch; ++f)
       for (int s : p->leaves) {
@@ -842,11 +859,15 @@ extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
   }
   CU(cudaEventRecord(p->ev[1], st));
 
-  // ---- upward sweep, deepest internal level first
+  // ---- upward sweep, deepest internal level first (hodlr.py:264-282).
+  // The coupling system S = [[I, X], [Y, I]] (X = V_low^T d_left, Y = V_up^T
+  // d_right) is inverted by block elimination of one identity block: only the
+  // Woodbury capacitance M = I - Y X (or I - X Y, whichever is smaller) is
+  // factored, with partial pivoting; S^{-1} is assembled by GEMMs and kept
+  // for the solve phase.  det S = det M, so singular S <=> singular M.
   for (int lvl = p->depth - 1; lvl >= 0; --lvl) {
-    TileList th, tq, tu;
-    std::vector<LuTask> sl;
-    int maxR = 0;
+    TileList th, tm, t4, t5, tq, tu;
+    std::vector<GjTask> gts;
     for (int64_t f = 0; f < p->batch; ++f)
       for (int k = 0; k < (int)p->internal.size(); ++k) {
         const int s = p->internal[k];
@@ -863,39 +884,51 @@ extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
         const double* Vlow = UV + f * p->uv_per_front + bl.v_off;  // na x rl
         double* Yf = Y + p->y_off[f];
         double* H = F + r.h;
+        double* Si = F + r.inv;
+        double* M = F + r.m;
         const int R = r.R, rl = r.rl, ru = r.ru;
         const int w = (int)r.w;
         // H[0:rl, 0:w+ru] = V_low^T Y[a, 0:w+ru];  H[rl:R, 0:w+rl] = V_up^T Y[b, 0:w+rl]
         if (rl > 0) th.add(gemm(Vlow, na, 1, Yf + a.lo, n, H, R, rl, w + ru, na, 1.0, 0.0));
         if (ru > 0) th.add(gemm(Vup, nbr, 1, Yf + b.lo, n, H + rl, R, ru, w + rl, nbr, 1.0, 0.0));
-        LuTask t{};
-        t.src = H;
-        t.src_ld = R;
-        t.lu = F + r.lu;
-        t.inv = F + r.inv;
-        t.perm = I + r.perm;
-        t.ipiv = I + r.ipiv;
-        t.status = I + r.status;
-        t.N = R;
-        t.mode = 1;
-        t.rl = rl;
-        t.ru = ru;
-        t.h_col0 = w;
-        maxR = std::max(maxR, R);
-        sl.push_back(t);
+        const double* X = H + (int64_t)w * R;          // rl x ru
+        const double* Yc = H + rl + (int64_t)w * R;    // ru x rl
+        GjTask g{};
+        g.src_ld = 0;
+        g.out_ld = R;
+        g.status = I + r.status;
+        g.mode = 1;
+        if (ru <= rl) {
+          // M = I_u - Y X ; S^{-1} = [[I - X (-M^{-1} Y), -X M^{-1}], [-M^{-1} Y, M^{-1}]]
+          tm.add(gemm(Yc, R, 0, X, R, M, ru, ru, ru, rl, -1.0, 0.0, 1.0));
+          g.src = M; g.src_ld = ru; g.out = Si + rl + (int64_t)rl * R; g.N = ru;
+          const double* Mi = Si + rl + (int64_t)rl * R;
+          t4.add(gemm(Mi, R, 0, Yc, R, Si + rl, R, ru, rl, ru, -1.0, 0.0));
+          t4.add(gemm(X, R, 0, Mi, R, Si + (int64_t)rl * R, R, rl, ru, ru, -1.0, 0.0));
+          t5.add(gemm(X, R, 0, Si + rl, R, Si, R, rl, rl, ru, -1.0, 0.0, 1.0));
+        } else {
+          // M = I_l - X Y ; S^{-1} = [[M^{-1}, -M^{-1} X], [-Y M^{-1}, I - Y (-M^{-1} X)]]
+          tm.add(gemm(X, R, 0, Yc, R, M, rl, rl, rl, ru, -1.0, 0.0, 1.0));
+          g.src = M; g.src_ld = rl; g.out = Si; g.N = rl;
+          t4.add(gemm(Si, R, 0, X, R, Si + (int64_t)rl * R, R, rl, ru, rl, -1.0, 0.0));
+          t4.add(gemm(Yc, R, 0, Si, R, Si + rl, R, ru, rl, rl, -1.0, 0.0));
+          t5.add(gemm(Yc, R, 0, Si + (int64_t)rl * R, R, Si + rl + (int64_t)rl * R, R, ru, ru, rl,
+                      -1.0, 0.0, 1.0));
+        }
+        gts.push_back(g);
         if (w > 0) {
           double* Q = F + r.q;
-          tq.add(gemm(F + r.inv, R, 0, H, R, Q, R, R, w, R, 1.0, 0.0));
+          tq.add(gemm(Si, R, 0, H, R, Q, R, R, w, R, 1.0, 0.0));
           // top -= d_left y_up ; bottom -= d_right y_low
           if (ru > 0) tu.add(gemm(Yf + a.lo + (int64_t)w * n, n, 0, Q + rl, R, Yf + a.lo, n, na, w, ru, -1.0, 1.0));
           if (rl > 0) tu.add(gemm(Yf + b.lo + (int64_t)w * n, n, 0, Q, R, Yf + b.lo, n, nbr, w, rl, -1.0, 1.0));
         }
       }
     CHK(run_tiles(th, p->fmap_d, p->tasks_d, st));
-    if (!sl.empty()) {
-      CU(upload(p->ftask_d, sl, st));
-      CU(hk_launch_lu(p->ftask_d.as<LuTask>(), (int)sl.size(), maxR, st));
-    }
+    CHK(run_tiles(tm, p->fmap_d, p->tasks_d, st));
+    CHK(run_gj(p, gts, st));
+    CHK(run_tiles(t4, p->fmap_d, p->tasks_d, st));
+    CHK(run_tiles(t5, p->fmap_d, p->tasks_d, st));
     CHK(run_tiles(tq, p->fmap_d, p->tasks_d, st));
     CHK(run_tiles(tu, p->fmap_d, p->tasks_d, st));
   }
@@ -954,17 +987,40 @@ static void colmajor_to_rowmajor(const std::vector<double>& cm, int64_t rows, in
     for (int64_t j = 0; j < cols; ++j) out[i * cols + j] = cm[i + j * ld];
 }
 
+// On-demand partial-pivot LU (inspection of leaf_lus / couplings[].schur_lu;
+// the hot path keeps explicit inverses instead).
+static hk_status lu_on_demand(const LuTask& proto, int N, double* lu_host, int32_t* piv_host) {
+  if (N == 0) return HK_OK;
+  double* lu = nullptr;
+  int32_t *ip = nullptr, *pm = nullptr, *stt = nullptr;
+  LuTask* td = nullptr;
+  CU(cudaMalloc(&lu, (size_t)N * N * 8));
+  CU(cudaMalloc(&ip, (size_t)N * 4));
+  CU(cudaMalloc(&pm, (size_t)N * 4));
+  CU(cudaMalloc(&stt, 8));
+  CU(cudaMalloc(&td, sizeof(LuTask)));
+  LuTask t = proto;
+  t.lu = lu; t.ipiv = ip; t.perm = pm; t.status = stt; t.inv = nullptr; t.N = N;
+  CU(cudaMemcpy(td, &t, sizeof(LuTask), cudaMemcpyHostToDevice));
+  CU(hk_launch_lu(td, 1, N, 0));
+  std::vector<double> h((size_t)N * N);
+  CU(cudaMemcpy(h.data(), lu, h.size() * 8, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(piv_host, ip, (size_t)N * 4, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < N; ++i)
+    for (int j = 0; j < N; ++j) lu_host[(int64_t)i * N + j] = h[i + (int64_t)j * N];
+  cudaFree(lu); cudaFree(ip); cudaFree(pm); cudaFree(stt); cudaFree(td);
+  return HK_OK;
+}
+
 extern "C" hk_status hk_get_leaf_lu(hk_plan* p, int64_t f, int64_t slot, double* lu, int32_t* perm) {
   if (!p || !p->factored) return fail(HK_ERR_STATE, "plan not factored");
   const Node& nd = p->nodes[slot];
   if (nd.left >= 0) return fail(HK_ERR_VALUE, "not a leaf");
-  const NodeRec& r = p->rec[f * p->nodes.size() + slot];
-  const int64_t b = nd.hi - nd.lo;
-  std::vector<double> h(b * b);
-  CU(cudaMemcpy(h.data(), p->F.as<double>() + r.lu, b * b * 8, cudaMemcpyDeviceToHost));
-  colmajor_to_rowmajor(h, b, b, b, lu);
-  CU(cudaMemcpy(perm, p->I.as<int32_t>() + r.ipiv, b * 4, cudaMemcpyDeviceToHost));
-  return HK_OK;
+  LuTask t{};
+  t.src = p->A + f * p->fstride + nd.lo * p->lda + nd.lo;
+  t.src_ld = p->lda;
+  t.mode = 0;
+  return lu_on_demand(t, (int)(nd.hi - nd.lo), lu, perm);
 }
 
 extern "C" hk_status hk_get_coupling(hk_plan* p, int64_t f, int64_t slot, double* dl, double* dr,
@@ -990,10 +1046,14 @@ extern "C" hk_status hk_get_coupling(hk_plan* p, int64_t f, int64_t slot, double
     colmajor_to_rowmajor(h, b.hi - b.lo, r.rl, b.hi - b.lo, dr);
   }
   if (slu && r.R > 0) {
-    std::vector<double> h((size_t)r.R * r.R);
-    CU(cudaMemcpy(h.data(), p->F.as<double>() + r.lu, h.size() * 8, cudaMemcpyDeviceToHost));
-    colmajor_to_rowmajor(h, r.R, r.R, r.R, slu);
-    CU(cudaMemcpy(sperm, p->I.as<int32_t>() + r.ipiv, (size_t)r.R * 4, cudaMemcpyDeviceToHost));
+    LuTask t{};
+    t.src = p->F.as<double>() + r.h;
+    t.src_ld = r.R;
+    t.mode = 1;
+    t.rl = r.rl;
+    t.ru = r.ru;
+    t.h_col0 = r.w;
+    CHK(lu_on_demand(t, r.R, slu, sperm));
   }
   return HK_OK;
 }

@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(NT) gemm_kernel(const GemmTask* __restrict__ t
         double* c = t.C + row + (int64_t)col * t.ldc;
         double v = t.alpha * acc[i][j][h];
         if (t.beta != 0.0) v += t.beta * (*c);
+        if (row == col) v += t.diag;
         *c = v;
       }
     }

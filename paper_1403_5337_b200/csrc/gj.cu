@@ -1,0 +1,124 @@
+// Batched Gauss-Jordan inversion with partial pivoting (leaf blocks and the
+// r x r Woodbury capacitance matrices I - Y X of the coupling systems).
+//
+// One CTA per matrix; the matrix lives in SMEM when it fits (N <= 165), else
+// in a global scratch (L2 resident).  Each elimination step is one rank-1
+// update of the whole N x N array, column-major with the row index fastest
+// so SMEM accesses are conflict-free and global accesses coalesced.
+#include "hk_common.cuh"
+#include "hk_internal.h"
+
+namespace {
+
+constexpr int GJ_NT = 256;
+constexpr size_t GJ_SMEM_CAP = 224 * 1024;
+
+// workspace layout (SMEM or global scratch): W[N*N], colk[N], rowk[N] doubles,
+// then piv[N], cperm[N] ints
+__host__ __device__ inline size_t gj_bytes(int N) {
+  return (size_t)N * N * 8 + (size_t)2 * N * 8 + (size_t)2 * N * 4;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) gj_kernel(const GjTask* __restrict__ tasks, size_t smem_bytes) {
+  const GjTask t = tasks[blockIdx.x];
+  const int N = t.N;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const bool in_smem = gj_bytes(N) <= smem_bytes;
+  double* W = in_smem ? reinterpret_cast<double*>(smraw) : t.scratch;
+  double* colk = W + (size_t)N * N;
+  double* rowk = colk + N;
+  int* piv = reinterpret_cast<int*>(rowk + N);
+  int* cperm = piv + N;
+  __shared__ int s_p, s_sing;
+  if (N == 0) {
+    if (tid == 0) *t.status = 0;
+    return;
+  }
+  if (tid == 0) s_sing = 0;
+  const int64_t NN = (int64_t)N * N;
+  if (t.mode == 0) {
+    for (int64_t idx = tid; idx < NN; idx += NT) {
+      const int i = (int)(idx / N), j = (int)(idx % N);       // coalesced row-major read
+      W[i + (int64_t)j * N] = t.src[(int64_t)i * t.src_ld + j];
+    }
+  } else {
+    for (int64_t idx = tid; idx < NN; idx += NT) {
+      const int i = (int)(idx % N), j = (int)(idx / N);
+      W[idx] = t.src[i + (int64_t)j * t.src_ld];
+    }
+  }
+  __syncthreads();
+  for (int k = 0; k < N; ++k) {
+    if (warp == 0) {
+      ArgMax a{0.0, -1};
+      for (int i = k + lane; i < N; i += 32) {
+        const double v = fabs(W[i + (int64_t)k * N]);
+        if (argmax_better(v, i, a.v, a.i)) { a.v = v; a.i = i; }
+      }
+      a = warp_argmax(a);
+      if (lane == 0) {
+        s_p = (int)a.i;
+        piv[k] = (int)a.i;
+        if (!(a.v >= HK_PIVOT_FLOOR)) s_sing = 1;
+      }
+    }
+    __syncthreads();
+    if (s_sing) break;
+    const int p = s_p;
+    if (p != k) {
+      for (int j = tid; j < N; j += NT) {
+        const double a = W[k + (int64_t)j * N];
+        W[k + (int64_t)j * N] = W[p + (int64_t)j * N];
+        W[p + (int64_t)j * N] = a;
+      }
+      __syncthreads();
+    }
+    const double rinv = 1.0 / W[k + (int64_t)k * N];
+    for (int i = tid; i < N; i += NT) colk[i] = W[i + (int64_t)k * N];
+    for (int j = tid; j < N; j += NT) rowk[j] = (j == k) ? rinv : W[k + (int64_t)j * N] * rinv;
+    __syncthreads();
+    for (int64_t idx = tid; idx < NN; idx += NT) {
+      const int i = (int)(idx % N), j = (int)(idx / N);
+      double v;
+      if (i == k) v = rowk[j];
+      else if (j == k) v = -colk[i] * rinv;
+      else v = W[idx] - colk[i] * rowk[j];
+      W[idx] = v;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *t.status = s_sing;
+  if (s_sing) return;
+  // undo the row pivoting as a column gather: A^{-1}[:, j] = W[:, c(j)]
+  if (tid == 0) {
+    for (int j = 0; j < N; ++j) cperm[j] = j;
+    for (int k = N - 1; k >= 0; --k) {
+      const int a = cperm[k];
+      cperm[k] = cperm[piv[k]];
+      cperm[piv[k]] = a;
+    }
+  }
+  __syncthreads();
+  for (int64_t idx = tid; idx < NN; idx += NT) {
+    const int i = (int)(idx % N), j = (int)(idx / N);
+    t.out[i + (int64_t)j * t.out_ld] = W[i + (int64_t)cperm[j] * N];
+  }
+}
+
+}  // namespace
+
+cudaError_t hk_launch_gj(const GjTask* tasks_dev, int ntasks, int maxN, cudaStream_t st) {
+  if (ntasks == 0) return cudaSuccess;
+  size_t need = gj_bytes(maxN);
+  size_t smem = need <= GJ_SMEM_CAP ? need : 0;
+  cudaError_t e = cudaFuncSetAttribute(gj_kernel<GJ_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)GJ_SMEM_CAP);
+  if (e != cudaSuccess) return e;
+  gj_kernel<GJ_NT><<<ntasks, GJ_NT, smem, st>>>(tasks_dev, smem);
+  hk_count_launch();
+  return cudaGetLastError();
+}
+
+size_t hk_gj_scratch_bytes(int N) { return gj_bytes(N) <= GJ_SMEM_CAP ? 0 : gj_bytes(N); }

@@ -64,6 +64,7 @@ struct GemmTask {
   int32_t m, n, k;
   int32_t transA;
   double alpha, beta;
+  double diag;      // added to C(i,i) after alpha*op(A)*B + beta*C
 };
 
 // ---------------------------------------------------------------- copies
@@ -130,3 +131,20 @@ cudaError_t hk_launch_diag_scale(const double* A, int64_t lda, const double* x, 
                                  int64_t n, cudaStream_t st);
 
 void hk_count_launch(int k = 1);
+
+// ---------------------------------------------------------------- Gauss-Jordan inverse
+// In-place Gauss-Jordan with partial (row) pivoting -> explicit inverse.
+// Pivots equal those of LU with partial pivoting (rows >= k see the same
+// updates), so the singularity test min|pivot| < 1e-300 matches dense.py:76.
+struct GjTask {
+  const double* src;   // mode 0: row-major (src[i*ld + j]); mode 1: column-major (src[i + j*ld])
+  int64_t src_ld;
+  double* out;         // column-major inverse, leading dimension out_ld
+  int64_t out_ld;
+  double* scratch;     // hk_gj_scratch_bytes(N) used when N is too large for SMEM (else null)
+  int32_t* status;     // 0 ok, 1 singular
+  int32_t N;
+  int32_t mode;
+};
+cudaError_t hk_launch_gj(const GjTask* tasks_dev, int ntasks, int maxN, cudaStream_t st);
+size_t hk_gj_scratch_bytes(int N);     // 0 when N fits SMEM
