@@ -37,19 +37,15 @@ __global__ void __launch_bounds__(NT) gj_kernel(const GjTask* __restrict__ tasks
     return;
   }
   if (tid == 0) s_sing = 0;
-  const int64_t NN = (int64_t)N * N;
   if (t.mode == 0) {
-    for (int64_t idx = tid; idx < NN; idx += NT) {
-      const int i = (int)(idx / N), j = (int)(idx % N);       // coalesced row-major read
-      W[i + (int64_t)j * N] = t.src[(int64_t)i * t.src_ld + j];
-    }
+    for (int i = warp; i < N; i += NT / 32)                     // coalesced row-major read
+      for (int j = lane; j < N; j += 32) W[i + (int64_t)j * N] = t.src[(int64_t)i * t.src_ld + j];
   } else {
-    for (int64_t idx = tid; idx < NN; idx += NT) {
-      const int i = (int)(idx % N), j = (int)(idx / N);
-      W[idx] = t.src[i + (int64_t)j * t.src_ld];
-    }
+    for (int j = warp; j < N; j += NT / 32)
+      for (int i = lane; i < N; i += 32) W[i + (int64_t)j * N] = t.src[i + (int64_t)j * t.src_ld];
   }
   __syncthreads();
+  constexpr int NW = NT / 32;
   for (int k = 0; k < N; ++k) {
     if (warp == 0) {
       ArgMax a{0.0, -1};
@@ -67,25 +63,30 @@ __global__ void __launch_bounds__(NT) gj_kernel(const GjTask* __restrict__ tasks
     __syncthreads();
     if (s_sing) break;
     const int p = s_p;
-    if (p != k) {
-      for (int j = tid; j < N; j += NT) {
-        const double a = W[k + (int64_t)j * N];
-        W[k + (int64_t)j * N] = W[p + (int64_t)j * N];
-        W[p + (int64_t)j * N] = a;
-      }
-      __syncthreads();
+    // gather the (swapped) pivot row and column; move old row k to row p
+    for (int j = tid; j < N; j += NT) {
+      const double wk = W[k + (int64_t)j * N];
+      rowk[j] = W[p + (int64_t)j * N];
+      if (p != k) W[p + (int64_t)j * N] = wk;
     }
-    const double rinv = 1.0 / W[k + (int64_t)k * N];
-    for (int i = tid; i < N; i += NT) colk[i] = W[i + (int64_t)k * N];
-    for (int j = tid; j < N; j += NT) rowk[j] = (j == k) ? rinv : W[k + (int64_t)j * N] * rinv;
+    for (int i = tid; i < N; i += NT) {
+      double c;
+      if (i == k) c = 0.0;                          // unused: row k is rewritten below
+      else if (i == p) c = W[k + (int64_t)k * N];
+      else c = W[i + (int64_t)k * N];
+      colk[i] = c;
+    }
     __syncthreads();
-    for (int64_t idx = tid; idx < NN; idx += NT) {
-      const int i = (int)(idx % N), j = (int)(idx / N);
-      double v;
-      if (i == k) v = rowk[j];
-      else if (j == k) v = -colk[i] * rinv;
-      else v = W[idx] - colk[i] * rowk[j];
-      W[idx] = v;
+    const double rinv = 1.0 / rowk[k];
+    // rank-1 update of every entry (column j by warp, rows by lane)
+    for (int j = warp; j < N; j += NW) {
+      const double rj = (j == k) ? 0.0 : rowk[j] * rinv;
+      double* col = W + (int64_t)j * N;
+      if (j == k) {
+        for (int i = lane; i < N; i += 32) col[i] = (i == k) ? rinv : -colk[i] * rinv;
+      } else {
+        for (int i = lane; i < N; i += 32) col[i] = (i == k) ? rj : col[i] - colk[i] * rj;
+      }
     }
     __syncthreads();
   }
@@ -101,9 +102,10 @@ __global__ void __launch_bounds__(NT) gj_kernel(const GjTask* __restrict__ tasks
     }
   }
   __syncthreads();
-  for (int64_t idx = tid; idx < NN; idx += NT) {
-    const int i = (int)(idx % N), j = (int)(idx / N);
-    t.out[i + (int64_t)j * t.out_ld] = W[i + (int64_t)cperm[j] * N];
+  for (int j = warp; j < N; j += NT / 32) {
+    const double* src = W + (int64_t)cperm[j] * N;
+    double* dst = t.out + (int64_t)j * t.out_ld;
+    for (int i = lane; i < N; i += 32) dst[i] = src[i];
   }
 }
 
