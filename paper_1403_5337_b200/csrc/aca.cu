@@ -43,21 +43,81 @@ __global__ void transpose_kernel(const double* __restrict__ A, double* __restric
   }
 }
 
-// res[e] = src[e] - sum_k coef[k] * F[k*len + e], k in order; written to out.
-// Returns nothing; callers fold their own reductions over the owned elements.
+// ---------------------------------------------------------------------------
+// Residual sweep: out[e] = src[e] - sum_{k<rank} coef[k] * F[k*len + e] for the
+// two elements e0 = tid + base, e1 = e0 + NT owned by this thread, k in the
+// reference order with separate IEEE multiply/subtract.  Loads are issued in
+// batches of KB so each thread keeps 2*KB independent L2 requests in flight
+// (the chain itself only depends on the arithmetic).
+template <int NT, int KB>
+__device__ __forceinline__ void sweep2(const double* __restrict__ F, int64_t len, int rank,
+                                       const double* __restrict__ coef, int e0, bool has1,
+                                       double& x0, double& x1) {
+  const double* p0 = F + e0;
+  int k = 0;
+  if (has1) {
+    for (; k + KB <= rank; k += KB) {
+      double a[KB], b[KB];
+#pragma unroll
+      for (int q = 0; q < KB; ++q) {
+        a[q] = __ldcg(p0 + (int64_t)(k + q) * len);
+        b[q] = __ldcg(p0 + (int64_t)(k + q) * len + NT);
+      }
+#pragma unroll
+      for (int q = 0; q < KB; ++q) {
+        const double c = coef[k + q];
+        x0 = sub_rn(x0, mul_rn(c, a[q]));
+        x1 = sub_rn(x1, mul_rn(c, b[q]));
+      }
+    }
+    for (; k < rank; ++k) {
+      const double c = coef[k];
+      x0 = sub_rn(x0, mul_rn(c, __ldcg(p0 + (int64_t)k * len)));
+      x1 = sub_rn(x1, mul_rn(c, __ldcg(p0 + (int64_t)k * len + NT)));
+    }
+  } else {
+    for (; k + KB <= rank; k += KB) {
+      double a[KB];
+#pragma unroll
+      for (int q = 0; q < KB; ++q) a[q] = __ldcg(p0 + (int64_t)(k + q) * len);
+#pragma unroll
+      for (int q = 0; q < KB; ++q) x0 = sub_rn(x0, mul_rn(coef[k + q], a[q]));
+    }
+    for (; k < rank; ++k) x0 = sub_rn(x0, mul_rn(coef[k], __ldcg(p0 + (int64_t)k * len)));
+  }
+}
+
+// dot(x, F[:,k]) for a warp: lanes stride the vector, 4 independent partials.
+__device__ __forceinline__ double warp_dot(const double* __restrict__ x, const double* __restrict__ y,
+                                          int len, int lane) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int i = lane;
+  for (; i + 96 < len; i += 128) {
+    const double y0 = __ldcg(y + i), y1 = __ldcg(y + i + 32), y2 = __ldcg(y + i + 64),
+                 y3 = __ldcg(y + i + 96);
+    s0 += x[i] * y0;
+    s1 += x[i + 32] * y1;
+    s2 += x[i + 64] * y2;
+    s3 += x[i + 96] * y3;
+  }
+  for (; i < len; i += 32) s0 += x[i] * __ldcg(y + i);
+  return warp_sum((s0 + s1) + (s2 + s3));
+}
 
 template <int NT>
-__global__ void __launch_bounds__(NT) aca_kernel(const AcaTask* __restrict__ tasks, double tol2) {
+__global__ void __launch_bounds__(NT) aca_kernel(const AcaTask* __restrict__ tasks, double tol2,
+                                                 int vec_in_smem) {
   const AcaTask t = tasks[blockIdx.x];
   const int m = t.m, n = t.n, cap = t.cap;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
   extern __shared__ __align__(16) unsigned char smraw[];
   double* coef = reinterpret_cast<double*>(smraw);   // [cap]
   double* prod = coef + cap;                         // [cap]
-  unsigned char* used = reinterpret_cast<unsigned char*>(prod + cap);  // [m]
-  __shared__ double red_v[NT / 32];
-  __shared__ int64_t red_i[NT / 32];
-  __shared__ double red_s[2 * (NT / 32)];
+  double* svec = prod + cap;                         // [m + n] when vec_in_smem
+  unsigned char* used = reinterpret_cast<unsigned char*>(svec + (vec_in_smem ? (m + n) : 0));
+  __shared__ double red_v[NW], red_a[NW], red_b[NW];
+  __shared__ int64_t red_i[NW];
   __shared__ int s_row;
 
   int32_t* trows = t.trace ? t.trace + 2 : nullptr;
@@ -91,37 +151,23 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaTask* __restrict__ tas
     for (int k = tid; k < rank; k += NT) coef[k] = U[(int64_t)k * m + row];
     __syncthreads();
 
-    // ---- residual row (lowrank.py:253-256)
+    // ---- residual row (lowrank.py:253-256): V[:, rank] = A[row, :] - U[row, :] V^T
     const double* src = Ab + (int64_t)row * t.lda;
     double* vout = V + (int64_t)rank * n;
     ArgMax best{0.0, -1};
-    {
-      int j = tid;
-      for (; j + NT < n; j += 2 * NT) {
-        double x0 = src[j], x1 = src[j + NT];
-        const double* vp = V + j;
-        for (int k = 0; k < rank; ++k) {
-          const double c = coef[k];
-          x0 = sub_rn(x0, mul_rn(c, vp[0]));
-          x1 = sub_rn(x1, mul_rn(c, vp[NT]));
-          vp += n;
-        }
-        vout[j] = x0;
-        vout[j + NT] = x1;
-        double a0 = fabs(x0), a1 = fabs(x1);
-        if (argmax_better(a0, j, best.v, best.i)) { best.v = a0; best.i = j; }
-        if (argmax_better(a1, j + NT, best.v, best.i)) { best.v = a1; best.i = j + NT; }
-      }
-      for (; j < n; j += NT) {
-        double x0 = src[j];
-        const double* vp = V + j;
-        for (int k = 0; k < rank; ++k) {
-          x0 = sub_rn(x0, mul_rn(coef[k], vp[0]));
-          vp += n;
-        }
-        vout[j] = x0;
-        double a0 = fabs(x0);
-        if (argmax_better(a0, j, best.v, best.i)) { best.v = a0; best.i = j; }
+    for (int base = 0; base < n; base += 2 * NT) {
+      const int e0 = base + tid;
+      if (e0 >= n) break;
+      const bool has1 = e0 + NT < n;
+      double x0 = src[e0], x1 = has1 ? src[e0 + NT] : 0.0;
+      sweep2<NT, 8>(V, n, rank, coef, e0, has1, x0, x1);
+      vout[e0] = x0;
+      double a0 = fabs(x0);
+      if (argmax_better(a0, e0, best.v, best.i)) { best.v = a0; best.i = e0; }
+      if (has1) {
+        vout[e0 + NT] = x1;
+        double a1 = fabs(x1);
+        if (argmax_better(a1, e0 + NT, best.v, best.i)) { best.v = a1; best.i = e0 + NT; }
       }
     }
     best = block_argmax<NT>(best, red_v, red_i);
@@ -141,9 +187,11 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaTask* __restrict__ tas
     }
     // ---- v = res / delta (:265) and the column coefficients
     double vv = 0.0;
+    double* vs = vec_in_smem ? svec + m : vout;
     for (int j = tid; j < n; j += NT) {
-      double v = div_rn(vout[j], delta);
+      const double v = div_rn(vout[j], delta);
       vout[j] = v;
+      if (vec_in_smem) vs[j] = v;
       vv += v * v;
     }
     for (int k = tid; k < rank; k += NT) coef[k] = V[(int64_t)k * n + col];
@@ -151,61 +199,63 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaTask* __restrict__ tas
     ++ncol_ev;
     __syncthreads();
 
-    // ---- residual column (:266-268), plus next-row candidate (:283)
+    // ---- residual column (:266-268) plus next-row candidate (:283)
     const double* csrc = Atb + (int64_t)col * t.lda;
     double* uout = U + (int64_t)rank * m;
+    double* us = vec_in_smem ? svec : uout;
     double uu = 0.0;
     ArgMax nxt{0.0, -1};
-    {
-      int i = tid;
-      for (; i + NT < m; i += 2 * NT) {
-        double x0 = csrc[i], x1 = csrc[i + NT];
-        const double* up = U + i;
-        for (int k = 0; k < rank; ++k) {
-          const double c = coef[k];
-          x0 = sub_rn(x0, mul_rn(c, up[0]));
-          x1 = sub_rn(x1, mul_rn(c, up[NT]));
-          up += m;
-        }
-        uout[i] = x0;
-        uout[i + NT] = x1;
-        uu += x0 * x0 + x1 * x1;
-        if (!used[i]) {
-          double a = fabs(x0);
-          if (argmax_better(a, i, nxt.v, nxt.i)) { nxt.v = a; nxt.i = i; }
-        }
-        if (!used[i + NT]) {
-          double a = fabs(x1);
-          if (argmax_better(a, i + NT, nxt.v, nxt.i)) { nxt.v = a; nxt.i = i + NT; }
-        }
+    for (int base = 0; base < m; base += 2 * NT) {
+      const int e0 = base + tid;
+      if (e0 >= m) break;
+      const bool has1 = e0 + NT < m;
+      double x0 = csrc[e0], x1 = has1 ? csrc[e0 + NT] : 0.0;
+      sweep2<NT, 8>(U, m, rank, coef, e0, has1, x0, x1);
+      uout[e0] = x0;
+      if (vec_in_smem) us[e0] = x0;
+      uu += x0 * x0;
+      if (!used[e0]) {
+        const double a = fabs(x0);
+        if (argmax_better(a, e0, nxt.v, nxt.i)) { nxt.v = a; nxt.i = e0; }
       }
-      for (; i < m; i += NT) {
-        double x0 = csrc[i];
-        const double* up = U + i;
-        for (int k = 0; k < rank; ++k) {
-          x0 = sub_rn(x0, mul_rn(coef[k], up[0]));
-          up += m;
-        }
-        uout[i] = x0;
-        uu += x0 * x0;
-        if (!used[i]) {
-          double a = fabs(x0);
-          if (argmax_better(a, i, nxt.v, nxt.i)) { nxt.v = a; nxt.i = i; }
+      if (has1) {
+        uout[e0 + NT] = x1;
+        if (vec_in_smem) us[e0 + NT] = x1;
+        uu += x1 * x1;
+        if (!used[e0 + NT]) {
+          const double a = fabs(x1);
+          if (argmax_better(a, e0 + NT, nxt.v, nxt.i)) { nxt.v = a; nxt.i = e0 + NT; }
         }
       }
     }
-    nxt = block_argmax<NT>(nxt, red_v, red_i);
-    block_sum2<NT>(uu, vv, red_s);
+    // one combined reduction: next-row argmax, ||u||^2, ||v||^2
+    {
+      nxt = warp_argmax(nxt);
+      uu = warp_sum(uu);
+      vv = warp_sum(vv);
+      if (lane == 0) { red_v[warp] = nxt.v; red_i[warp] = nxt.i; red_a[warp] = uu; red_b[warp] = vv; }
+      __syncthreads();
+      if (warp == 0) {
+        ArgMax b2;
+        double a2 = 0.0, c2 = 0.0;
+        if (lane < NW) { b2.v = red_v[lane]; b2.i = red_i[lane]; a2 = red_a[lane]; c2 = red_b[lane]; }
+        else { b2.v = 0.0; b2.i = -1; }
+        b2 = warp_argmax(b2);
+        a2 = warp_sum(a2);
+        c2 = warp_sum(c2);
+        if (lane == 0) { red_v[0] = b2.v; red_i[0] = b2.i; red_a[0] = a2; red_b[0] = c2; }
+      }
+      // the dots below need every thread's u/v writes: this barrier covers both
+      __syncthreads();
+      nxt.i = red_i[0];
+      uu = red_a[0];
+      vv = red_b[0];
+    }
 
     // ---- stopping estimate (:269-275): cross terms 2 (u.u_k)(v.v_k), warp per k
-    for (int k = warp; k < rank; k += NT / 32) {
-      const double* uk = U + (int64_t)k * m;
-      const double* vk = V + (int64_t)k * n;
-      double su = 0.0, sv = 0.0;
-      for (int i = lane; i < m; i += 32) su += uout[i] * uk[i];
-      for (int j = lane; j < n; j += 32) sv += vout[j] * vk[j];
-      su = warp_sum(su);
-      sv = warp_sum(sv);
+    for (int k = warp; k < rank; k += NW) {
+      const double su = warp_dot(us, U + (int64_t)k * m, m, lane);
+      const double sv = warp_dot(vs, V + (int64_t)k * n, n, lane);
       if (lane == 0) prod[k] = 2.0 * su * sv;
     }
     __syncthreads();
@@ -238,13 +288,17 @@ cudaError_t hk_launch_transpose(const double* A, double* At, int64_t n, int64_t 
 }
 
 cudaError_t hk_launch_aca(const AcaTask* tasks_dev, int ntasks, int max_cap, int max_m,
-                          double tol2, cudaStream_t st) {
+                          double tol2, cudaStream_t st, int max_mn) {
   if (ntasks == 0) return cudaSuccess;
-  size_t smem = (size_t)max_cap * 16 + (size_t)max_m + 16;
+  // the new cross vectors are staged in SMEM for the dot products when that
+  // keeps the CTA small enough for several CTAs per SM
+  size_t base = (size_t)max_cap * 16 + (size_t)max_m + 16;
+  int vec_in_smem = base + (size_t)max_mn * 8 <= 48 * 1024 ? 1 : 0;
+  size_t smem = base + (vec_in_smem ? (size_t)max_mn * 8 : 0);
   cudaError_t e = cudaFuncSetAttribute(aca_kernel<ACA_NT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  aca_kernel<ACA_NT><<<ntasks, ACA_NT, smem, st>>>(tasks_dev, tol2);
+  aca_kernel<ACA_NT><<<ntasks, ACA_NT, smem, st>>>(tasks_dev, tol2, vec_in_smem);
   hk_count_launch();
   return cudaGetLastError();
 }

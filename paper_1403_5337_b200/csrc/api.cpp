@@ -420,7 +420,7 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
   if (p->have_trace) CU(p->trace_d.ensure((size_t)p->batch * p->trace_per_front * 4 + 4, st));
   std::vector<AcaTask> tasks;
   tasks.reserve((size_t)p->batch * p->blocks.size());
-  int max_cap = 0, max_m = 0;
+  int max_cap = 0, max_m = 0, max_mn = 0;
   const size_t nb = p->blocks.size();
   for (int64_t f = 0; f < p->batch; ++f) {
     for (int bi : p->block_order) {
@@ -438,6 +438,7 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
       t.cap = b.cap;
       max_cap = std::max(max_cap, b.cap);
       max_m = std::max(max_m, b.m);
+      max_mn = std::max(max_mn, b.m + b.n);
       tasks.push_back(t);
     }
   }
@@ -445,7 +446,7 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
   if ((size_t)max_cap * 16 + max_m > 220 * 1024)
     return fail(HK_ERR_VALUE, "block too large for the single-CTA ACA kernel");
   CU(cudaEventRecord(p->ev[3], st));
-  CU(hk_launch_aca(p->tasks_d.as<AcaTask>(), (int)tasks.size(), max_cap, max_m, tol2, st));
+  CU(hk_launch_aca(p->tasks_d.as<AcaTask>(), (int)tasks.size(), max_cap, max_m, tol2, st, max_mn));
   CU(cudaEventRecord(p->ev[1], st));
   CHK(fetch_ranks(p, st));
   float ms = 0, ms_aca = 0;
@@ -1505,7 +1506,7 @@ extern "C" hk_status hk_aca_block(const double* a, int64_t m, int64_t n, int64_t
   AcaTask* td = nullptr;
   CU(cudaMallocAsync(&td, sizeof(AcaTask), st));
   CU(cudaMemcpyAsync(td, &t, sizeof(AcaTask), cudaMemcpyHostToDevice, st));
-  CU(hk_launch_aca(td, 1, (int)cap, (int)m, tol2, st));
+  CU(hk_launch_aca(td, 1, (int)cap, (int)m, tol2, st, (int)(m + n)));
   std::vector<int32_t> h(tlen);
   int32_t r32 = 0;
   CU(cudaMemcpyAsync(&r32, rk, 4, cudaMemcpyDeviceToHost, st));

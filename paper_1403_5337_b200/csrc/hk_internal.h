@@ -97,7 +97,7 @@ struct DotTask {     // y[k*ldy + c] = dot(M[:,k], x[:,c]) for k < cols, column-
 cudaError_t hk_launch_transpose(const double* A, double* At, int64_t n, int64_t ld, int64_t batch,
                                 int64_t stride, cudaStream_t st);
 cudaError_t hk_launch_aca(const AcaTask* tasks_dev, int ntasks, int max_cap, int max_m,
-                          double tol2, cudaStream_t st);
+                          double tol2, cudaStream_t st, int max_mn);
 cudaError_t hk_launch_skeleton(const SkelTask* tasks_dev, int ntasks, int max_k, int max_kc,
                                cudaStream_t st);
 cudaError_t hk_launch_lu(const LuTask* tasks_dev, int ntasks, int maxN, cudaStream_t st);
