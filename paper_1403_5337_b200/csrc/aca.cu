@@ -53,37 +53,45 @@ template <int NT, int KB>
 __device__ __forceinline__ void sweep2(const double* __restrict__ F, int64_t len, int rank,
                                        const double* __restrict__ coef, int e0, bool has1,
                                        double& x0, double& x1) {
+  // Register double buffering: the loads of chunk c+1 are in flight while the
+  // subtract chain of chunk c runs.  The products c_k * F[k, e] do not depend
+  // on the chain, so only the subtractions are serial.
   const double* p0 = F + e0;
-  int k = 0;
-  if (has1) {
-    for (; k + KB <= rank; k += KB) {
-      double a[KB], b[KB];
+  const int nfull = rank / KB;
+  double a[KB], b[KB];
+  if (nfull > 0) {
+#pragma unroll
+    for (int q = 0; q < KB; ++q) {
+      a[q] = p0[(int64_t)q * len];
+      b[q] = has1 ? p0[(int64_t)q * len + NT] : 0.0;
+    }
+  }
+  for (int c = 0; c < nfull; ++c) {
+    const int k = c * KB;
+    double pa[KB], pb[KB];
+#pragma unroll
+    for (int q = 0; q < KB; ++q) {
+      const double cc = coef[k + q];
+      pa[q] = mul_rn(cc, a[q]);
+      pb[q] = mul_rn(cc, b[q]);
+    }
+    if (c + 1 < nfull) {
 #pragma unroll
       for (int q = 0; q < KB; ++q) {
-        a[q] = __ldcg(p0 + (int64_t)(k + q) * len);
-        b[q] = __ldcg(p0 + (int64_t)(k + q) * len + NT);
-      }
-#pragma unroll
-      for (int q = 0; q < KB; ++q) {
-        const double c = coef[k + q];
-        x0 = sub_rn(x0, mul_rn(c, a[q]));
-        x1 = sub_rn(x1, mul_rn(c, b[q]));
+        a[q] = p0[(int64_t)(k + KB + q) * len];
+        b[q] = has1 ? p0[(int64_t)(k + KB + q) * len + NT] : 0.0;
       }
     }
-    for (; k < rank; ++k) {
-      const double c = coef[k];
-      x0 = sub_rn(x0, mul_rn(c, __ldcg(p0 + (int64_t)k * len)));
-      x1 = sub_rn(x1, mul_rn(c, __ldcg(p0 + (int64_t)k * len + NT)));
-    }
-  } else {
-    for (; k + KB <= rank; k += KB) {
-      double a[KB];
 #pragma unroll
-      for (int q = 0; q < KB; ++q) a[q] = __ldcg(p0 + (int64_t)(k + q) * len);
-#pragma unroll
-      for (int q = 0; q < KB; ++q) x0 = sub_rn(x0, mul_rn(coef[k + q], a[q]));
+    for (int q = 0; q < KB; ++q) {
+      x0 = sub_rn(x0, pa[q]);
+      x1 = sub_rn(x1, pb[q]);
     }
-    for (; k < rank; ++k) x0 = sub_rn(x0, mul_rn(coef[k], __ldcg(p0 + (int64_t)k * len)));
+  }
+  for (int k = nfull * KB; k < rank; ++k) {
+    const double cc = coef[k];
+    x0 = sub_rn(x0, mul_rn(cc, p0[(int64_t)k * len]));
+    if (has1) x1 = sub_rn(x1, mul_rn(cc, p0[(int64_t)k * len + NT]));
   }
 }
 
@@ -93,24 +101,25 @@ __device__ __forceinline__ double warp_dot(const double* __restrict__ x, const d
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   int i = lane;
   for (; i + 96 < len; i += 128) {
-    const double y0 = __ldcg(y + i), y1 = __ldcg(y + i + 32), y2 = __ldcg(y + i + 64),
-                 y3 = __ldcg(y + i + 96);
+    const double y0 = y[i], y1 = y[i + 32], y2 = y[i + 64], y3 = y[i + 96];
     s0 += x[i] * y0;
     s1 += x[i + 32] * y1;
     s2 += x[i + 64] * y2;
     s3 += x[i + 96] * y3;
   }
-  for (; i < len; i += 32) s0 += x[i] * __ldcg(y + i);
+  for (; i < len; i += 32) s0 += x[i] * y[i];
   return warp_sum((s0 + s1) + (s2 + s3));
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT) aca_kernel(const AcaTask* __restrict__ tasks, double tol2,
+__global__ void __launch_bounds__(NT, 3) aca_kernel(const AcaTask* __restrict__ tasks, double tol2,
                                                  int vec_in_smem) {
   const AcaTask t = tasks[blockIdx.x];
   const int m = t.m, n = t.n, cap = t.cap;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
+  uint64_t t_start = 0;
+  if (t.clock && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   extern __shared__ __align__(16) unsigned char smraw[];
   double* coef = reinterpret_cast<double*>(smraw);   // [cap]
   double* prod = coef + cap;                         // [cap]
@@ -160,7 +169,7 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaTask* __restrict__ tas
       if (e0 >= n) break;
       const bool has1 = e0 + NT < n;
       double x0 = src[e0], x1 = has1 ? src[e0 + NT] : 0.0;
-      sweep2<NT, 8>(V, n, rank, coef, e0, has1, x0, x1);
+      sweep2<NT, 4>(V, n, rank, coef, e0, has1, x0, x1);
       vout[e0] = x0;
       double a0 = fabs(x0);
       if (argmax_better(a0, e0, best.v, best.i)) { best.v = a0; best.i = e0; }
@@ -210,7 +219,7 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaTask* __restrict__ tas
       if (e0 >= m) break;
       const bool has1 = e0 + NT < m;
       double x0 = csrc[e0], x1 = has1 ? csrc[e0 + NT] : 0.0;
-      sweep2<NT, 8>(U, m, rank, coef, e0, has1, x0, x1);
+      sweep2<NT, 4>(U, m, rank, coef, e0, has1, x0, x1);
       uout[e0] = x0;
       if (vec_in_smem) us[e0] = x0;
       uu += x0 * x0;
@@ -273,6 +282,15 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaTask* __restrict__ tas
   if (tid == 0) {
     *t.rank = rank;
     if (t.trace) { t.trace[0] = nrow_ev; t.trace[1] = ncol_ev; }
+    if (t.clock) {
+      uint64_t t_end;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      t.clock[0] = (int64_t)t_start;
+      t.clock[1] = (int64_t)t_end;
+      t.clock[2] = smid;
+    }
   }
 }
 

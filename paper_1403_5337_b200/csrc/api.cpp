@@ -20,6 +20,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -442,6 +443,12 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
       tasks.push_back(t);
     }
   }
+  const char* prof = getenv("HK_ACA_PROFILE");
+  DevBuf clk;
+  if (prof) {
+    CU(clk.ensure(tasks.size() * 24 + 8, st));
+    for (size_t i = 0; i < tasks.size(); ++i) tasks[i].clock = clk.as<int64_t>() + 3 * i;
+  }
   CU(upload(p->tasks_d, tasks, st));
   if ((size_t)max_cap * 16 + max_m > 220 * 1024)
     return fail(HK_ERR_VALUE, "block too large for the single-CTA ACA kernel");
@@ -449,6 +456,19 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
   CU(hk_launch_aca(p->tasks_d.as<AcaTask>(), (int)tasks.size(), max_cap, max_m, tol2, st, max_mn));
   CU(cudaEventRecord(p->ev[1], st));
   CHK(fetch_ranks(p, st));
+  if (prof) {
+    std::vector<int64_t> h(tasks.size() * 3);
+    CU(cudaMemcpy(h.data(), clk.p, h.size() * 8, cudaMemcpyDeviceToHost));
+    FILE* fo = fopen(prof, "w");
+    if (fo) {
+      for (size_t i = 0; i < tasks.size(); ++i)
+        fprintf(fo, "%d %d %d %d %lld %lld %lld\n", tasks[i].m, tasks[i].n,
+                p->ranks[(i / nb) * nb + p->block_order[i % nb]], (int)(i % nb), (long long)h[3 * i],
+                (long long)h[3 * i + 1], (long long)h[3 * i + 2]);
+      fclose(fo);
+    }
+    clk.release();
+  }
   float ms = 0, ms_aca = 0;
   CU(cudaEventElapsedTime(&ms, p->ev[0], p->ev[1]));
   CU(cudaEventElapsedTime(&ms_aca, p->ev[3], p->ev[1]));

@@ -115,10 +115,18 @@ cudaError_t hk_launch_gj(const GjTask* tasks_dev, int ntasks, int maxN, cudaStre
   if (ntasks == 0) return cudaSuccess;
   size_t need = gj_bytes(maxN);
   size_t smem = need <= GJ_SMEM_CAP ? need : 0;
-  cudaError_t e = cudaFuncSetAttribute(gj_kernel<GJ_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)GJ_SMEM_CAP);
-  if (e != cudaSuccess) return e;
-  gj_kernel<GJ_NT><<<ntasks, GJ_NT, smem, st>>>(tasks_dev, smem);
+  cudaError_t e;
+  if (maxN > 80) {   // large systems: more warps per elimination step
+    e = cudaFuncSetAttribute(gj_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)GJ_SMEM_CAP);
+    if (e != cudaSuccess) return e;
+    gj_kernel<1024><<<ntasks, 1024, smem, st>>>(tasks_dev, smem);
+  } else {
+    e = cudaFuncSetAttribute(gj_kernel<GJ_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)GJ_SMEM_CAP);
+    if (e != cudaSuccess) return e;
+    gj_kernel<GJ_NT><<<ntasks, GJ_NT, smem, st>>>(tasks_dev, smem);
+  }
   hk_count_launch();
   return cudaGetLastError();
 }

@@ -11,6 +11,7 @@ struct AcaTask {
   double* V;         // n x cap column-major (ld n)
   int32_t* rank;     // out
   int32_t* trace;    // optional: [0]=#rows, [1]=#cols, rows[m+cap+1], cols[cap+1]
+  int64_t* clock;    // optional profiling probe: [start ns, end ns, smid]
   int64_t lda;
   int32_t m, n, cap;
   int32_t pad;
