@@ -224,13 +224,15 @@ def run_ours(args):
     from paper_1403_5337_b200 import _native as N
     from paper_1403_5337_b200.hodlr import HodlrBatch
 
+    from paper_1403_5337_b200 import multifront as MF
+
     rank, local, world = env_rank()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     F = args.fronts_per_gpu
-    seeds = range(rank * F, (rank + 1) * F)
+    seeds = MF.shard_range(rank, world, F)
     fronts = torch.stack([make_front(s, dev) for s in seeds]).contiguous()
     n = fronts.shape[1]
     rhs = torch.from_numpy(np.stack([rhs_for(s, n) for s in seeds])).to(dev)
@@ -268,11 +270,7 @@ def run_ours(args):
     barrier()
     clk = clocks.stop()
     launches = N.launch_count() - launches0
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = MF.max_over_ranks(e0.elapsed_time(e1), device=dev)
     value = world * F * args.steps / (ms_max * 1e-3)
 
     # ---- roofline of the dominant kernel (batched ACA, HBM-bound by its compulsory bytes)
@@ -334,10 +332,8 @@ def run_ours(args):
             e2e_step()
         e1.record(stream)
         torch.cuda.synchronize()
-        t2 = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * F * args.steps / (float(t2.item()) * 1e-3), "unit": UNIT,
+        e2e_ms = MF.max_over_ranks(e0.elapsed_time(e1), device=dev)
+        e2e = {"value": world * F * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(host_fronts.numel() * 8 + host_rhs.numel() * 8),
                "d2h_bytes_per_step": int(host_x.numel() * 8),
                "path": "HodlrBatch.factorize/solve_ (public API) from pinned host buffers"}
@@ -353,6 +349,8 @@ def run_ours(args):
                "sample": f"{k} of the {F} fronts, build+factor+solve, oracle/hodlr_oracle.py "
                          f"(numpy restatement of the reference), 1 thread, {secs:.1f} s"}
 
+    # per-front ranks of every rank's fronts (the one end-of-run gather)
+    all_ranks = MF.gather_front_scalars(batch.ranks.astype(np.int64), device=dev)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
@@ -360,7 +358,9 @@ def run_ours(args):
                 "data": "synthetic", "config": config_dict(args, world), "impl": "ours",
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roof,
                 "cpu_baseline": cpu, "gmres": gm,
-                "ranks_per_level_front0": [e["max_rank"] for e in batch.report(0).ranks_per_level]}
+                "ranks_per_level_front0": [e["max_rank"] for e in batch.report(0).ranks_per_level],
+                "fronts_gathered": int(all_ranks.shape[0]),
+                "max_block_rank_all_fronts": int(all_ranks.max())}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -7,6 +7,7 @@ device is visible, every compute entry point raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
@@ -14,7 +15,7 @@ from . import errors
 
 _LIB = None
 _LOCK = threading.Lock()
-LIB_PATH = Path(__file__).resolve().with_name("libhodlr_b200.so")
+LIB_PATH = Path(os.environ.get("HK_LIB_PATH") or Path(__file__).resolve().with_name("libhodlr_b200.so"))
 
 P = C.c_void_p
 I64 = C.c_int64

@@ -95,24 +95,64 @@ __device__ __forceinline__ void sweep2(const double* __restrict__ F, int64_t len
   }
 }
 
-// dot(x, F[:,k]) for a warp: lanes stride the vector, 4 independent partials.
-__device__ __forceinline__ double warp_dot(const double* __restrict__ x, const double* __restrict__ y,
-                                          int len, int lane) {
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  int i = lane;
-  for (; i + 96 < len; i += 128) {
-    const double y0 = y[i], y1 = y[i + 32], y2 = y[i + 64], y3 = y[i + 96];
-    s0 += x[i] * y0;
-    s1 += x[i + 32] * y1;
-    s2 += x[i + 64] * y2;
-    s3 += x[i + 96] * y3;
+// Lane l of the warp receives the warp-wide sum of a[l & 15] (butterfly
+// reduce-scatter inside each half-warp, then one exchange between halves).
+__device__ __forceinline__ double transpose_reduce16(double (&a)[16], int lane) {
+#pragma unroll
+  for (int s = 8; s >= 1; s >>= 1) {
+    const bool upper = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const double send = upper ? a[i] : a[i + s];
+      const double keep = upper ? a[i + s] : a[i];
+      a[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
   }
-  for (; i < len; i += 32) s0 += x[i] * y[i];
-  return warp_sum((s0 + s1) + (s2 + s3));
+  return a[0] + __shfl_xor_sync(0xffffffffu, a[0], 16);
+}
+
+// out[k] = x . F[:, k] for k < rank with the sweep's access pattern: every
+// thread owns elements e = tid + NT*q, loads F[e + k*len] for 16 k at a time
+// (coalesced over e, 8 loads in flight per batch), and the per-k sums are
+// reduced by a warp transpose-reduce plus a fixed-order sum over warps
+// (deterministic, independent of scheduling).
+template <int NT>
+__device__ __forceinline__ void dots_pass(const double* __restrict__ F, const double* __restrict__ x,
+                                          int len, int rank, double* __restrict__ out,
+                                          double* __restrict__ part) {
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int k0 = 0; k0 < rank; k0 += 16) {
+    double acc[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+    for (int e = tid; e < len; e += NT) {
+      const double xe = x[e];
+      const double* p = F + e + (int64_t)k0 * len;
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        double a[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[q] = (k0 + 8 * g + q < rank) ? p[(int64_t)(8 * g + q) * len] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[8 * g + q] += xe * a[q];
+      }
+    }
+    const double v = transpose_reduce16(acc, lane);
+    if (lane < 16) part[warp * 16 + lane] = v;
+    __syncthreads();
+    if (warp == 0 && lane < 16 && k0 + lane < rank) {
+      double sum = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) sum += part[w * 16 + lane];
+      out[k0 + lane] = sum;
+    }
+    __syncthreads();
+  }
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT, 3) aca_kernel(const AcaTask* __restrict__ tasks, double tol2,
+__global__ void __launch_bounds__(NT, 2) aca_kernel(const AcaTask* __restrict__ tasks, double tol2,
                                                  int vec_in_smem) {
   const AcaTask t = tasks[blockIdx.x];
   const int m = t.m, n = t.n, cap = t.cap;
@@ -122,8 +162,10 @@ __global__ void __launch_bounds__(NT, 3) aca_kernel(const AcaTask* __restrict__ 
   if (t.clock && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   extern __shared__ __align__(16) unsigned char smraw[];
   double* coef = reinterpret_cast<double*>(smraw);   // [cap]
-  double* prod = coef + cap;                         // [cap]
-  double* svec = prod + cap;                         // [m + n] when vec_in_smem
+  double* du = coef + cap;                           // [cap]  u . u_k
+  double* dv = du + cap;                             // [cap]  v . v_k
+  double* part = dv + cap;                           // [NW * 32] dot partials
+  double* svec = part + NW * 32;                     // [m + n] when vec_in_smem
   unsigned char* used = reinterpret_cast<unsigned char*>(svec + (vec_in_smem ? (m + n) : 0));
   __shared__ double red_v[NW], red_a[NW], red_b[NW];
   __shared__ int64_t red_i[NW];
@@ -261,16 +303,12 @@ __global__ void __launch_bounds__(NT, 3) aca_kernel(const AcaTask* __restrict__ 
       vv = red_b[0];
     }
 
-    // ---- stopping estimate (:269-275): cross terms 2 (u.u_k)(v.v_k), warp per k
-    for (int k = warp; k < rank; k += NW) {
-      const double su = warp_dot(us, U + (int64_t)k * m, m, lane);
-      const double sv = warp_dot(vs, V + (int64_t)k * n, n, lane);
-      if (lane == 0) prod[k] = 2.0 * su * sv;
-    }
-    __syncthreads();
+    // ---- stopping estimate (:269-275): cross terms 2 (u.u_k)(v.v_k)
+    dots_pass<NT>(U, us, m, rank, du, part);
+    dots_pass<NT>(V, vs, n, rank, dv, part);
     const double cross = uu * vv;
     double est = fro2 + cross;
-    for (int k = 0; k < rank; ++k) est += prod[k];
+    for (int k = 0; k < rank; ++k) est += 2.0 * du[k] * dv[k];
     est = fmax(est, cross);
     if (cross <= tol2 * est) break;     // discard this cross and stop
     ++rank;
@@ -310,7 +348,7 @@ cudaError_t hk_launch_aca(const AcaTask* tasks_dev, int ntasks, int max_cap, int
   if (ntasks == 0) return cudaSuccess;
   // the new cross vectors are staged in SMEM for the dot products when that
   // keeps the CTA small enough for several CTAs per SM
-  size_t base = (size_t)max_cap * 16 + (size_t)max_m + 16;
+  size_t base = (size_t)max_cap * 24 + (ACA_NT / 32) * 32 * 8 + (size_t)max_m + 16;
   int vec_in_smem = base + (size_t)max_mn * 8 <= 48 * 1024 ? 1 : 0;
   size_t smem = base + (vec_in_smem ? (size_t)max_mn * 8 : 0);
   cudaError_t e = cudaFuncSetAttribute(aca_kernel<ACA_NT>,

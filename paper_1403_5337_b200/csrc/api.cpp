@@ -420,6 +420,7 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
   p->have_trace = record_trace != 0;
   if (p->have_trace) CU(p->trace_d.ensure((size_t)p->batch * p->trace_per_front * 4 + 4, st));
   std::vector<AcaTask> tasks;
+  std::vector<int64_t> task_key;
   tasks.reserve((size_t)p->batch * p->blocks.size());
   int max_cap = 0, max_m = 0, max_mn = 0;
   const size_t nb = p->blocks.size();
@@ -441,6 +442,7 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
       max_m = std::max(max_m, b.m);
       max_mn = std::max(max_mn, b.m + b.n);
       tasks.push_back(t);
+      task_key.push_back(f * (int64_t)nb + bi);
     }
   }
   const char* prof = getenv("HK_ACA_PROFILE");
@@ -449,8 +451,22 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
     CU(clk.ensure(tasks.size() * 24 + 8, st));
     for (size_t i = 0; i < tasks.size(); ++i) tasks[i].clock = clk.as<int64_t>() + 3 * i;
   }
+  // global largest-first order across fronts: the long root chains start first
+  std::vector<size_t> order(tasks.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) {
+    const AcaTask &a = tasks[x], &b = tasks[y];
+    return (int64_t)(a.m + a.n) * a.cap > (int64_t)(b.m + b.n) * b.cap;
+  });
+  std::vector<AcaTask> sorted(tasks.size());
+  std::vector<size_t> tidx(tasks.size());   // sorted position -> (f * nb + block) key
+  std::vector<int64_t> skey(tasks.size());
+  for (size_t i = 0; i < order.size(); ++i) { sorted[i] = tasks[order[i]]; skey[i] = task_key[order[i]]; }
+  tasks.swap(sorted);
+  task_key.swap(skey);
+  (void)tidx;
   CU(upload(p->tasks_d, tasks, st));
-  if ((size_t)max_cap * 16 + max_m > 220 * 1024)
+  if ((size_t)max_cap * 24 + max_m + 2048 > 220 * 1024)
     return fail(HK_ERR_VALUE, "block too large for the single-CTA ACA kernel");
   CU(cudaEventRecord(p->ev[3], st));
   CU(hk_launch_aca(p->tasks_d.as<AcaTask>(), (int)tasks.size(), max_cap, max_m, tol2, st, max_mn));
@@ -463,7 +479,7 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
     if (fo) {
       for (size_t i = 0; i < tasks.size(); ++i)
         fprintf(fo, "%d %d %d %d %lld %lld %lld\n", tasks[i].m, tasks[i].n,
-                p->ranks[(i / nb) * nb + p->block_order[i % nb]], (int)(i % nb), (long long)h[3 * i],
+                p->ranks[task_key[i]], (int)(task_key[i] % nb), (long long)h[3 * i],
                 (long long)h[3 * i + 1], (long long)h[3 * i + 2]);
       fclose(fo);
     }
