@@ -23,7 +23,7 @@
 
 namespace {
 
-constexpr int ACA_NT = 256;
+constexpr int ACA_NT = 128;
 
 __global__ void transpose_kernel(const double* __restrict__ A, double* __restrict__ At,
                                  int64_t n, int64_t ld, int64_t stride) {
@@ -111,50 +111,90 @@ __device__ __forceinline__ double transpose_reduce16(double (&a)[16], int lane) 
   return a[0] + __shfl_xor_sync(0xffffffffu, a[0], 16);
 }
 
-// out[k] = x . F[:, k] for k < rank with the sweep's access pattern: every
-// thread owns elements e = tid + NT*q, loads F[e + k*len] for 16 k at a time
-// (coalesced over e, 8 loads in flight per batch), and the per-k sums are
-// reduced by a warp transpose-reduce plus a fixed-order sum over warps
+// du[k] = u . U[:, k] and dv[k] = v . V[:, k] for k < rank, with the sweep's
+// access pattern: every thread owns elements e = tid + NT*q, loads 16 columns
+// at a time (coalesced over e, 8 loads in flight per batch); the per-k sums
+// are reduced by a warp transpose-reduce into per-warp SMEM partials, and
+// after ONE barrier per DCH columns summed over warps in a fixed order
 // (deterministic, independent of scheduling).
+constexpr int DCH = 128;
+
 template <int NT>
-__device__ __forceinline__ void dots_pass(const double* __restrict__ F, const double* __restrict__ x,
-                                          int len, int rank, double* __restrict__ out,
-                                          double* __restrict__ part) {
-  constexpr int NW = NT / 32;
+__device__ __forceinline__ void dot_chunk(const double* __restrict__ F, const double* __restrict__ x,
+                                          int len, int k0, int kend, double* __restrict__ part) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int k0 = 0; k0 < rank; k0 += 16) {
+  for (int kb = k0; kb < kend; kb += 16) {
     double acc[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) acc[q] = 0.0;
     for (int e = tid; e < len; e += NT) {
       const double xe = x[e];
-      const double* p = F + e + (int64_t)k0 * len;
+      const double* p = F + e + (int64_t)kb * len;
 #pragma unroll
       for (int g = 0; g < 2; ++g) {
         double a[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) a[q] = (k0 + 8 * g + q < rank) ? p[(int64_t)(8 * g + q) * len] : 0.0;
+        for (int q = 0; q < 8; ++q) a[q] = (kb + 8 * g + q < kend) ? p[(int64_t)(8 * g + q) * len] : 0.0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) acc[8 * g + q] += xe * a[q];
       }
     }
     const double v = transpose_reduce16(acc, lane);
-    if (lane < 16) part[warp * 16 + lane] = v;
+    if (lane < 16) part[warp * DCH + (kb - k0) + lane] = v;
+  }
+}
+
+template <int NT>
+__device__ __forceinline__ void dots_pass(const double* __restrict__ U, const double* __restrict__ u,
+                                          int m, const double* __restrict__ V,
+                                          const double* __restrict__ v, int n, int rank,
+                                          double* __restrict__ du, double* __restrict__ dv,
+                                          double* __restrict__ part) {
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x;
+  for (int k0 = 0; k0 < rank; k0 += DCH) {
+    const int kend = min(rank, k0 + DCH);
+    dot_chunk<NT>(U, u, m, k0, kend, part);
+    dot_chunk<NT>(V, v, n, k0, kend, part + NW * DCH);
     __syncthreads();
-    if (warp == 0 && lane < 16 && k0 + lane < rank) {
-      double sum = 0.0;
+    for (int k = k0 + tid; k < kend; k += NT) {
+      double su = 0.0, sv = 0.0;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) sum += part[w * 16 + lane];
-      out[k0 + lane] = sum;
+      for (int w = 0; w < NW; ++w) {
+        su += part[w * DCH + (k - k0)];
+        sv += part[NW * DCH + w * DCH + (k - k0)];
+      }
+      du[k] = su;
+      dv[k] = sv;
     }
     __syncthreads();
   }
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT, 2) aca_kernel(const AcaTask* __restrict__ tasks, double tol2,
-                                                 int vec_in_smem) {
-  const AcaTask t = tasks[blockIdx.x];
+__device__ void aca_block(const AcaTask& t, double tol2, int vec_in_smem);
+
+// Persistent: CTAs pull tasks from a global counter in list order (largest
+// blocks first), so the long root chains start at t = 0 whatever the hardware
+// dispatch order of CTAs is.
+template <int NT>
+__global__ void __launch_bounds__(NT, 4) aca_kernel(const AcaTask* __restrict__ tasks, int ntasks,
+                                                    int* __restrict__ counter, double tol2,
+                                                    int vec_in_smem) {
+  __shared__ int s_task;
+  for (;;) {
+    if (threadIdx.x == 0) s_task = atomicAdd(counter, 1);
+    __syncthreads();
+    const int ti = s_task;
+    __syncthreads();
+    if (ti >= ntasks) break;
+    aca_block<NT>(tasks[ti], tol2, vec_in_smem);
+    __syncthreads();
+  }
+}
+
+template <int NT>
+__device__ void aca_block(const AcaTask& t, double tol2, int vec_in_smem) {
   const int m = t.m, n = t.n, cap = t.cap;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
@@ -164,8 +204,8 @@ __global__ void __launch_bounds__(NT, 2) aca_kernel(const AcaTask* __restrict__ 
   double* coef = reinterpret_cast<double*>(smraw);   // [cap]
   double* du = coef + cap;                           // [cap]  u . u_k
   double* dv = du + cap;                             // [cap]  v . v_k
-  double* part = dv + cap;                           // [NW * 32] dot partials
-  double* svec = part + NW * 32;                     // [m + n] when vec_in_smem
+  double* part = dv + cap;                           // [2 * NW * DCH] dot partials
+  double* svec = part + 2 * NW * DCH;                // [m + n] when vec_in_smem
   unsigned char* used = reinterpret_cast<unsigned char*>(svec + (vec_in_smem ? (m + n) : 0));
   __shared__ double red_v[NW], red_a[NW], red_b[NW];
   __shared__ int64_t red_i[NW];
@@ -221,7 +261,7 @@ __global__ void __launch_bounds__(NT, 2) aca_kernel(const AcaTask* __restrict__ 
         if (argmax_better(a1, e0 + NT, best.v, best.i)) { best.v = a1; best.i = e0 + NT; }
       }
     }
-    best = block_argmax<NT>(best, red_v, red_i);
+    best = block_argmax<NT, false>(best, red_v, red_i);
     const int col = (int)best.i;
     const double delta = vout[col];
     if (delta == 0.0) {                 // zero residual row: restart (:258-264)
@@ -304,8 +344,7 @@ __global__ void __launch_bounds__(NT, 2) aca_kernel(const AcaTask* __restrict__ 
     }
 
     // ---- stopping estimate (:269-275): cross terms 2 (u.u_k)(v.v_k)
-    dots_pass<NT>(U, us, m, rank, du, part);
-    dots_pass<NT>(V, vs, n, rank, dv, part);
+    dots_pass<NT>(U, us, m, V, vs, n, rank, du, dv, part);
     const double cross = uu * vv;
     double est = fro2 + cross;
     for (int k = 0; k < rank; ++k) est += 2.0 * du[k] * dv[k];
@@ -348,13 +387,26 @@ cudaError_t hk_launch_aca(const AcaTask* tasks_dev, int ntasks, int max_cap, int
   if (ntasks == 0) return cudaSuccess;
   // the new cross vectors are staged in SMEM for the dot products when that
   // keeps the CTA small enough for several CTAs per SM
-  size_t base = (size_t)max_cap * 24 + (ACA_NT / 32) * 32 * 8 + (size_t)max_m + 16;
+  size_t base = (size_t)max_cap * 24 + 2 * (ACA_NT / 32) * DCH * 8 + (size_t)max_m + 16;
   int vec_in_smem = base + (size_t)max_mn * 8 <= 48 * 1024 ? 1 : 0;
   size_t smem = base + (vec_in_smem ? (size_t)max_mn * 8 : 0);
   cudaError_t e = cudaFuncSetAttribute(aca_kernel<ACA_NT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  aca_kernel<ACA_NT><<<ntasks, ACA_NT, smem, st>>>(tasks_dev, tol2, vec_in_smem);
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, aca_kernel<ACA_NT>, ACA_NT, smem);
+  if (e != cudaSuccess) return e;
+  int grid = sms * (per_sm > 0 ? per_sm : 1);
+  if (grid > ntasks) grid = ntasks;
+  int* counter = nullptr;
+  e = cudaMallocAsync(&counter, sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  cudaMemsetAsync(counter, 0, sizeof(int), st);
+  aca_kernel<ACA_NT><<<grid, ACA_NT, smem, st>>>(tasks_dev, ntasks, counter, tol2, vec_in_smem);
+  e = cudaGetLastError();
+  cudaFreeAsync(counter, st);
   hk_count_launch();
-  return cudaGetLastError();
+  return e;
 }

@@ -40,7 +40,9 @@ __device__ __forceinline__ ArgMax warp_argmax(ArgMax a) {
 }
 
 // Block-wide argmax; result valid in all threads.  scratch needs 2*nwarps slots.
-template <int NT>
+// TAIL_SYNC=false drops the trailing barrier when the caller separates the
+// next use of the scratch by another barrier anyway.
+template <int NT, bool TAIL_SYNC = true>
 __device__ __forceinline__ ArgMax block_argmax(ArgMax a, double* sv, int64_t* si) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   a = warp_argmax(a);
@@ -54,7 +56,7 @@ __device__ __forceinline__ ArgMax block_argmax(ArgMax a, double* sv, int64_t* si
   }
   __syncthreads();
   ArgMax r{sv[0], si[0]};
-  __syncthreads();
+  if (TAIL_SYNC) __syncthreads();
   return r;
 }
 
