@@ -445,12 +445,6 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
       task_key.push_back(f * (int64_t)nb + bi);
     }
   }
-  const char* prof = getenv("HK_ACA_PROFILE");
-  DevBuf clk;
-  if (prof) {
-    CU(clk.ensure(tasks.size() * 24 + 8, st));
-    for (size_t i = 0; i < tasks.size(); ++i) tasks[i].clock = clk.as<int64_t>() + 3 * i;
-  }
   // global largest-first order across fronts: the long root chains start first
   std::vector<size_t> order(tasks.size());
   for (size_t i = 0; i < order.size(); ++i) order[i] = i;
@@ -465,6 +459,12 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
   tasks.swap(sorted);
   task_key.swap(skey);
   (void)tidx;
+  const char* prof = getenv("HK_ACA_PROFILE");
+  DevBuf clk;
+  if (prof) {
+    CU(clk.ensure(tasks.size() * 24 + 8, st));
+    for (size_t i = 0; i < tasks.size(); ++i) tasks[i].clock = clk.as<int64_t>() + 3 * i;
+  }
   CU(upload(p->tasks_d, tasks, st));
   if ((size_t)max_cap * 24 + max_m + 2048 > 220 * 1024)
     return fail(HK_ERR_VALUE, "block too large for the single-CTA ACA kernel");
