@@ -43,58 +43,6 @@ __global__ void transpose_kernel(const double* __restrict__ A, double* __restric
   }
 }
 
-// ---------------------------------------------------------------------------
-// Residual sweep: out[e] = src[e] - sum_{k<rank} coef[k] * F[k*len + e] for the
-// two elements e0 = tid + base, e1 = e0 + NT owned by this thread, k in the
-// reference order with separate IEEE multiply/subtract.  Loads are issued in
-// batches of KB so each thread keeps 2*KB independent L2 requests in flight
-// (the chain itself only depends on the arithmetic).
-template <int NT, int KB>
-__device__ __forceinline__ void sweep2(const double* __restrict__ F, int64_t len, int rank,
-                                       const double* __restrict__ coef, int e0, bool has1,
-                                       double& x0, double& x1) {
-  // Register double buffering: the loads of chunk c+1 are in flight while the
-  // subtract chain of chunk c runs.  The products c_k * F[k, e] do not depend
-  // on the chain, so only the subtractions are serial.
-  const double* p0 = F + e0;
-  const int nfull = rank / KB;
-  double a[KB], b[KB];
-  if (nfull > 0) {
-#pragma unroll
-    for (int q = 0; q < KB; ++q) {
-      a[q] = p0[(int64_t)q * len];
-      b[q] = has1 ? p0[(int64_t)q * len + NT] : 0.0;
-    }
-  }
-  for (int c = 0; c < nfull; ++c) {
-    const int k = c * KB;
-    double pa[KB], pb[KB];
-#pragma unroll
-    for (int q = 0; q < KB; ++q) {
-      const double cc = coef[k + q];
-      pa[q] = mul_rn(cc, a[q]);
-      pb[q] = mul_rn(cc, b[q]);
-    }
-    if (c + 1 < nfull) {
-#pragma unroll
-      for (int q = 0; q < KB; ++q) {
-        a[q] = p0[(int64_t)(k + KB + q) * len];
-        b[q] = has1 ? p0[(int64_t)(k + KB + q) * len + NT] : 0.0;
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < KB; ++q) {
-      x0 = sub_rn(x0, pa[q]);
-      x1 = sub_rn(x1, pb[q]);
-    }
-  }
-  for (int k = nfull * KB; k < rank; ++k) {
-    const double cc = coef[k];
-    x0 = sub_rn(x0, mul_rn(cc, p0[(int64_t)k * len]));
-    if (has1) x1 = sub_rn(x1, mul_rn(cc, p0[(int64_t)k * len + NT]));
-  }
-}
-
 // Lane l of the warp receives the warp-wide sum of a[l & 15] (butterfly
 // reduce-scatter inside each half-warp, then one exchange between halves).
 __device__ __forceinline__ double transpose_reduce16(double (&a)[16], int lane) {
@@ -111,76 +59,142 @@ __device__ __forceinline__ double transpose_reduce16(double (&a)[16], int lane) 
   return a[0] + __shfl_xor_sync(0xffffffffu, a[0], 16);
 }
 
-// du[k] = u . U[:, k] and dv[k] = v . V[:, k] for k < rank, with the sweep's
-// access pattern: every thread owns elements e = tid + NT*q, loads 16 columns
-// at a time (coalesced over e, 8 loads in flight per batch); the per-k sums
-// are reduced by a warp transpose-reduce into per-warp SMEM partials, and
-// after ONE barrier per DCH columns summed over warps in a fixed order
-// (deterministic, independent of scheduling).
-constexpr int DCH = 128;
+constexpr int EPT = 4;    // elements per thread per pass group
+constexpr int KC = 16;    // columns per chunk (one transpose-reduce each)
 
+// Fused residual sweep over one cross vector of length `len`:
+//   out[e] = src[e] - sum_{k<nk} coef[k] * F[e + k*len]   (reference k order,
+//            separate IEEE multiply and subtract: bit-exact)
+// and, for k < ndot, the per-warp partial dot products
+//   part[w*pld + k] = sum_{e owned by warp w} pend[e] * F[e + k*len]
+// of the PREVIOUS cross `pend` with the accepted crosses: the stopping-test
+// terms of the pending step ride along with the next step's sweep, so each
+// cross vector is streamed once per step instead of twice.  Elements are
+// owned by thread (e = g0 + tid + q*NT), loads are coalesced over e and
+// batched 8 deep; partial sums are reduced with a warp transpose-reduce and
+// accumulated per warp in a fixed order (deterministic).
+// out == nullptr: dots only.  used != nullptr: column sweep (argmax over
+// untouched rows and the sum of squares are returned); else row sweep
+// (argmax over all entries).
 template <int NT>
-__device__ __forceinline__ void dot_chunk(const double* __restrict__ F, const double* __restrict__ x,
-                                          int len, int k0, int kend, double* __restrict__ part) {
+__device__ __forceinline__ void fused_sweep(const double* __restrict__ F, int len, int nk, int ndot,
+                                            const double* __restrict__ coef,
+                                            const double* __restrict__ src, double* __restrict__ out,
+                                            const double* __restrict__ pend, double* __restrict__ part,
+                                            int pld, const unsigned char* __restrict__ used,
+                                            ArgMax& best, double& sumsq) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int kb = k0; kb < kend; kb += 16) {
-    double acc[16];
+  best.v = 0.0;
+  best.i = -1;
+  sumsq = 0.0;
+  double* mypart = part + warp * pld;
+  for (int k = lane; k < ndot; k += 32) mypart[k] = 0.0;
+  __syncwarp();
+  const int kmax = nk > ndot ? nk : ndot;
+  for (int g0 = 0; g0 < len; g0 += NT * EPT) {
+    double x[EPT], pv[EPT];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) acc[q] = 0.0;
-    for (int e = tid; e < len; e += NT) {
-      const double xe = x[e];
-      const double* p = F + e + (int64_t)kb * len;
+    for (int q = 0; q < EPT; ++q) {
+      const int e = g0 + tid + q * NT;
+      const bool ok = e < len;
+      x[q] = (ok && src) ? src[e] : 0.0;
+      pv[q] = (ok && ndot > 0) ? pend[e] : 0.0;
+    }
+    for (int kb = 0; kb < kmax; kb += KC) {
+      const int kn = nk - kb;             // chain columns left (may be <= 0)
+      const int dn = ndot - kb;           // dot columns left (may be <= 0)
+      double acc[KC];
 #pragma unroll
-      for (int g = 0; g < 2; ++g) {
-        double a[8];
+      for (int j = 0; j < KC; ++j) acc[j] = 0.0;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) a[q] = (kb + 8 * g + q < kend) ? p[(int64_t)(8 * g + q) * len] : 0.0;
+      for (int q = 0; q < EPT; ++q) {
+        const int e = g0 + tid + q * NT;
+        if (e >= len) continue;
+        const double* p = F + e + (int64_t)kb * len;
+        double xq = x[q];
+        const double pq = pv[q];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) acc[8 * g + q] += xe * a[q];
+        for (int h = 0; h < KC / 8; ++h) {
+          double a[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int kk = h * 8 + j;
+            a[j] = (kk < kn || kk < dn) ? p[(int64_t)kk * len] : 0.0;
+          }
+          double pr[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) pr[j] = mul_rn(coef[kb + h * 8 + j], a[j]);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int kk = h * 8 + j;
+            if (kk < kn) xq = sub_rn(xq, pr[j]);
+            if (kk < dn) acc[kk] += pq * a[j];
+          }
+        }
+        x[q] = xq;
+      }
+      if (dn > 0) {
+        const double v = transpose_reduce16(acc, lane);
+        if (lane < 16 && lane < dn) mypart[kb + lane] += v;
       }
     }
-    const double v = transpose_reduce16(acc, lane);
-    if (lane < 16) part[warp * DCH + (kb - k0) + lane] = v;
+    if (out) {
+#pragma unroll
+      for (int q = 0; q < EPT; ++q) {
+        const int e = g0 + tid + q * NT;
+        if (e >= len) continue;
+        out[e] = x[q];
+        const double ax = fabs(x[q]);
+        if (used) {
+          sumsq += x[q] * x[q];
+          if (!used[e] && argmax_better(ax, e, best.v, best.i)) { best.v = ax; best.i = e; }
+        } else if (argmax_better(ax, e, best.v, best.i)) {
+          best.v = ax;
+          best.i = e;
+        }
+      }
+    }
   }
 }
 
+// est = fro2 + cross + sum_k 2 (u.u_k)(v.v_k) over the per-warp partials,
+// reduced in a fixed order; valid in every thread.
 template <int NT>
-__device__ __forceinline__ void dots_pass(const double* __restrict__ U, const double* __restrict__ u,
-                                          int m, const double* __restrict__ V,
-                                          const double* __restrict__ v, int n, int rank,
-                                          double* __restrict__ du, double* __restrict__ dv,
-                                          double* __restrict__ part) {
+__device__ __forceinline__ double stopping_estimate(const double* __restrict__ partU,
+                                                    const double* __restrict__ partV, int pld,
+                                                    int r, double fro2, double cross,
+                                                    double* __restrict__ prod, double* s_est) {
   constexpr int NW = NT / 32;
-  const int tid = threadIdx.x;
-  for (int k0 = 0; k0 < rank; k0 += DCH) {
-    const int kend = min(rank, k0 + DCH);
-    dot_chunk<NT>(U, u, m, k0, kend, part);
-    dot_chunk<NT>(V, v, n, k0, kend, part + NW * DCH);
-    __syncthreads();
-    for (int k = k0 + tid; k < kend; k += NT) {
-      double su = 0.0, sv = 0.0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int k = tid; k < r; k += NT) {
+    double du = 0.0, dv = 0.0;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        su += part[w * DCH + (k - k0)];
-        sv += part[NW * DCH + w * DCH + (k - k0)];
-      }
-      du[k] = su;
-      dv[k] = sv;
+    for (int w = 0; w < NW; ++w) {
+      du += partU[w * pld + k];
+      dv += partV[w * pld + k];
     }
-    __syncthreads();
+    prod[k] = 2.0 * du * dv;
   }
+  __syncthreads();
+  if (warp == 0) {
+    double sacc = 0.0;
+    for (int k = lane; k < r; k += 32) sacc += prod[k];
+    sacc = warp_sum(sacc);
+    if (lane == 0) *s_est = fmax(fro2 + cross + sacc, cross);
+  }
+  __syncthreads();
+  return *s_est;
 }
-
-template <int NT>
-__device__ void aca_block(const AcaTask& t, double tol2, int vec_in_smem);
 
 // Persistent: CTAs pull tasks from a global counter in list order (largest
 // blocks first), so the long root chains start at t = 0 whatever the hardware
 // dispatch order of CTAs is.
 template <int NT>
+__device__ void aca_block(const AcaTask& t, double tol2);
+
+template <int NT>
 __global__ void __launch_bounds__(NT, 4) aca_kernel(const AcaTask* __restrict__ tasks, int ntasks,
-                                                    int* __restrict__ counter, double tol2,
-                                                    int vec_in_smem) {
+                                                    int* __restrict__ counter, double tol2) {
   __shared__ int s_task;
   for (;;) {
     if (threadIdx.x == 0) s_task = atomicAdd(counter, 1);
@@ -188,28 +202,29 @@ __global__ void __launch_bounds__(NT, 4) aca_kernel(const AcaTask* __restrict__ 
     const int ti = s_task;
     __syncthreads();
     if (ti >= ntasks) break;
-    aca_block<NT>(tasks[ti], tol2, vec_in_smem);
+    aca_block<NT>(tasks[ti], tol2);
     __syncthreads();
   }
 }
 
 template <int NT>
-__device__ void aca_block(const AcaTask& t, double tol2, int vec_in_smem) {
+__device__ void aca_block(const AcaTask& t, double tol2) {
   const int m = t.m, n = t.n, cap = t.cap;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
   uint64_t t_start = 0;
   if (t.clock && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   extern __shared__ __align__(16) unsigned char smraw[];
-  double* coef = reinterpret_cast<double*>(smraw);   // [cap]
-  double* du = coef + cap;                           // [cap]  u . u_k
-  double* dv = du + cap;                             // [cap]  v . v_k
-  double* part = dv + cap;                           // [2 * NW * DCH] dot partials
-  double* svec = part + 2 * NW * DCH;                // [m + n] when vec_in_smem
-  unsigned char* used = reinterpret_cast<unsigned char*>(svec + (vec_in_smem ? (m + n) : 0));
+  double* coef = reinterpret_cast<double*>(smraw);                        // [cap + KC]
+  unsigned char* used = reinterpret_cast<unsigned char*>(coef + cap + KC);  // [m]
   __shared__ double red_v[NW], red_a[NW], red_b[NW];
   __shared__ int64_t red_i[NW];
   __shared__ int s_row;
+  __shared__ double s_est;
+  const int pld = cap;
+  double* partU = t.scratch;                 // [NW * cap]
+  double* partV = partU + NW * pld;          // [NW * cap]
+  double* prod = partV + NW * pld;           // [cap]
 
   int32_t* trows = t.trace ? t.trace + 2 : nullptr;
   int32_t* tcols = t.trace ? t.trace + 2 + (m + cap + 1) : nullptr;
@@ -223,103 +238,97 @@ __device__ void aca_block(const AcaTask& t, double tol2, int vec_in_smem) {
     return;
   }
   for (int i = tid; i < m; i += NT) used[i] = 0;
+  // coef beyond the chain length is read (times 0) by the unrolled sweeps
+  for (int k = tid; k < cap + KC; k += NT) coef[k] = 0.0;
   __syncthreads();
 
-  int rank = 0, row = 0, nused = 0;
-  double fro2 = 0.0;
   const double* __restrict__ Ab = t.A;
   const double* __restrict__ Atb = t.At;
   double* __restrict__ U = t.U;
   double* __restrict__ V = t.V;
+  int r = 0, row = 0, nused = 0;
+  bool pending = false;                       // column r holds an undecided cross
+  double uu_p = 0.0, vv_p = 0.0, fro2 = 0.0;
+  ArgMax best, nxt;
+  double dummy, uu;
 
-  while (rank < cap) {
+  for (;;) {
+    const int c = r + (pending ? 1 : 0);     // index of the new candidate
+    const bool can_step = pending ? (c < cap && nused < m) : (c < cap);
+    if (!can_step) {
+      if (pending) {                          // decide the last cross: dots only
+        fused_sweep<NT>(U, m, 0, r, coef, nullptr, nullptr, U + (int64_t)r * m, partU, pld,
+                        nullptr, best, dummy);
+        fused_sweep<NT>(V, n, 0, r, coef, nullptr, nullptr, V + (int64_t)r * n, partV, pld,
+                        nullptr, best, dummy);
+        __syncthreads();
+        const double cross = uu_p * vv_p;
+        const double est = stopping_estimate<NT>(partU, partV, pld, r, fro2, cross, prod, &s_est);
+        if (!(cross <= tol2 * est)) ++r;
+      }
+      break;
+    }
+    // ---- next step (speculative when a cross is pending), lowrank.py:251-283
     if (tid == 0) {
       used[row] = 1;
       if (trows) trows[nrow_ev] = row;
     }
     ++nrow_ev;
     ++nused;
-    for (int k = tid; k < rank; k += NT) coef[k] = U[(int64_t)k * m + row];
+    for (int k = tid; k < c; k += NT) coef[k] = U[(int64_t)k * m + row];
     __syncthreads();
-
-    // ---- residual row (lowrank.py:253-256): V[:, rank] = A[row, :] - U[row, :] V^T
-    const double* src = Ab + (int64_t)row * t.lda;
-    double* vout = V + (int64_t)rank * n;
-    ArgMax best{0.0, -1};
-    for (int base = 0; base < n; base += 2 * NT) {
-      const int e0 = base + tid;
-      if (e0 >= n) break;
-      const bool has1 = e0 + NT < n;
-      double x0 = src[e0], x1 = has1 ? src[e0 + NT] : 0.0;
-      sweep2<NT, 4>(V, n, rank, coef, e0, has1, x0, x1);
-      vout[e0] = x0;
-      double a0 = fabs(x0);
-      if (argmax_better(a0, e0, best.v, best.i)) { best.v = a0; best.i = e0; }
-      if (has1) {
-        vout[e0 + NT] = x1;
-        double a1 = fabs(x1);
-        if (argmax_better(a1, e0 + NT, best.v, best.i)) { best.v = a1; best.i = e0 + NT; }
-      }
-    }
+    // residual row (:253-256) + the pending cross's v dots
+    fused_sweep<NT>(V, n, c, pending ? r : 0, coef, Ab + (int64_t)row * t.lda, V + (int64_t)c * n,
+                    V + (int64_t)r * n, partV, pld, nullptr, best, dummy);
     best = block_argmax<NT, false>(best, red_v, red_i);
     const int col = (int)best.i;
-    const double delta = vout[col];
-    if (delta == 0.0) {                 // zero residual row: restart (:258-264)
+    const double delta = V[(int64_t)c * n + col];
+    if (delta == 0.0) {                       // zero residual row (:258-264)
+      if (pending) {
+        fused_sweep<NT>(U, m, 0, r, coef, nullptr, nullptr, U + (int64_t)r * m, partU, pld,
+                        nullptr, nxt, dummy);
+        __syncthreads();
+        const double cross = uu_p * vv_p;
+        const double est = stopping_estimate<NT>(partU, partV, pld, r, fro2, cross, prod, &s_est);
+        if (cross <= tol2 * est) {            // reject: the reference never read this row
+          --nrow_ev;
+          break;
+        }
+        ++r;
+        fro2 = est;
+        pending = false;
+      }
       if (nused == m) break;
       if (tid == 0) {
-        int r = 0;
-        while (used[r]) ++r;
-        s_row = r;
+        int q = 0;
+        while (used[q]) ++q;
+        s_row = q;
       }
       __syncthreads();
       row = s_row;
       __syncthreads();
       continue;
     }
-    // ---- v = res / delta (:265) and the column coefficients
+    // v = res / delta (:265) over own elements (same ownership as the sweep)
+    double* vout = V + (int64_t)c * n;
     double vv = 0.0;
-    double* vs = vec_in_smem ? svec + m : vout;
-    for (int j = tid; j < n; j += NT) {
-      const double v = div_rn(vout[j], delta);
-      vout[j] = v;
-      if (vec_in_smem) vs[j] = v;
-      vv += v * v;
-    }
-    for (int k = tid; k < rank; k += NT) coef[k] = V[(int64_t)k * n + col];
+    for (int g0 = 0; g0 < n; g0 += NT * EPT)
+#pragma unroll
+      for (int q = 0; q < EPT; ++q) {
+        const int e = g0 + tid + q * NT;
+        if (e < n) {
+          const double v = div_rn(vout[e], delta);
+          vout[e] = v;
+          vv += v * v;
+        }
+      }
+    for (int k = tid; k < c; k += NT) coef[k] = V[(int64_t)k * n + col];
     if (tid == 0 && tcols) tcols[ncol_ev] = col;
     ++ncol_ev;
     __syncthreads();
-
-    // ---- residual column (:266-268) plus next-row candidate (:283)
-    const double* csrc = Atb + (int64_t)col * t.lda;
-    double* uout = U + (int64_t)rank * m;
-    double* us = vec_in_smem ? svec : uout;
-    double uu = 0.0;
-    ArgMax nxt{0.0, -1};
-    for (int base = 0; base < m; base += 2 * NT) {
-      const int e0 = base + tid;
-      if (e0 >= m) break;
-      const bool has1 = e0 + NT < m;
-      double x0 = csrc[e0], x1 = has1 ? csrc[e0 + NT] : 0.0;
-      sweep2<NT, 4>(U, m, rank, coef, e0, has1, x0, x1);
-      uout[e0] = x0;
-      if (vec_in_smem) us[e0] = x0;
-      uu += x0 * x0;
-      if (!used[e0]) {
-        const double a = fabs(x0);
-        if (argmax_better(a, e0, nxt.v, nxt.i)) { nxt.v = a; nxt.i = e0; }
-      }
-      if (has1) {
-        uout[e0 + NT] = x1;
-        if (vec_in_smem) us[e0 + NT] = x1;
-        uu += x1 * x1;
-        if (!used[e0 + NT]) {
-          const double a = fabs(x1);
-          if (argmax_better(a, e0 + NT, nxt.v, nxt.i)) { nxt.v = a; nxt.i = e0 + NT; }
-        }
-      }
-    }
-    // one combined reduction: next-row argmax, ||u||^2, ||v||^2
+    // residual column (:266-268) + next-row candidate (:283) + pending u dots
+    fused_sweep<NT>(U, m, c, pending ? r : 0, coef, Atb + (int64_t)col * t.lda, U + (int64_t)c * m,
+                    U + (int64_t)r * m, partU, pld, used, nxt, uu);
     {
       nxt = warp_argmax(nxt);
       uu = warp_sum(uu);
@@ -336,28 +345,30 @@ __device__ void aca_block(const AcaTask& t, double tol2, int vec_in_smem) {
         c2 = warp_sum(c2);
         if (lane == 0) { red_v[0] = b2.v; red_i[0] = b2.i; red_a[0] = a2; red_b[0] = c2; }
       }
-      // the dots below need every thread's u/v writes: this barrier covers both
       __syncthreads();
       nxt.i = red_i[0];
       uu = red_a[0];
       vv = red_b[0];
     }
-
-    // ---- stopping estimate (:269-275): cross terms 2 (u.u_k)(v.v_k)
-    dots_pass<NT>(U, us, m, V, vs, n, rank, du, dv, part);
-    const double cross = uu * vv;
-    double est = fro2 + cross;
-    for (int k = 0; k < rank; ++k) est += 2.0 * du[k] * dv[k];
-    est = fmax(est, cross);
-    if (cross <= tol2 * est) break;     // discard this cross and stop
-    ++rank;
-    fro2 = est;
-    if (nused == m) break;              // row exhaustion (:279-282)
+    if (pending) {                            // stopping test of the pending cross (:269-275)
+      const double cross = uu_p * vv_p;
+      const double est = stopping_estimate<NT>(partU, partV, pld, r, fro2, cross, prod, &s_est);
+      if (cross <= tol2 * est) {              // reject: drop the speculative step's reads
+        --nrow_ev;
+        --ncol_ev;
+        break;
+      }
+      ++r;
+      fro2 = est;
+    }
+    pending = true;                           // the new cross awaits its test
+    uu_p = uu;
+    vv_p = vv;
     row = (int)nxt.i;
     __syncthreads();
   }
   if (tid == 0) {
-    *t.rank = rank;
+    *t.rank = r;
     if (t.trace) { t.trace[0] = nrow_ev; t.trace[1] = ncol_ev; }
     if (t.clock) {
       uint64_t t_end;
@@ -384,12 +395,9 @@ cudaError_t hk_launch_transpose(const double* A, double* At, int64_t n, int64_t 
 
 cudaError_t hk_launch_aca(const AcaTask* tasks_dev, int ntasks, int max_cap, int max_m,
                           double tol2, cudaStream_t st, int max_mn) {
+  (void)max_mn;
   if (ntasks == 0) return cudaSuccess;
-  // the new cross vectors are staged in SMEM for the dot products when that
-  // keeps the CTA small enough for several CTAs per SM
-  size_t base = (size_t)max_cap * 24 + 2 * (ACA_NT / 32) * DCH * 8 + (size_t)max_m + 16;
-  int vec_in_smem = base + (size_t)max_mn * 8 <= 48 * 1024 ? 1 : 0;
-  size_t smem = base + (vec_in_smem ? (size_t)max_mn * 8 : 0);
+  const size_t smem = (size_t)(max_cap + KC) * 8 + (size_t)max_m + 16;
   cudaError_t e = cudaFuncSetAttribute(aca_kernel<ACA_NT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -404,9 +412,11 @@ cudaError_t hk_launch_aca(const AcaTask* tasks_dev, int ntasks, int max_cap, int
   e = cudaMallocAsync(&counter, sizeof(int), st);
   if (e != cudaSuccess) return e;
   cudaMemsetAsync(counter, 0, sizeof(int), st);
-  aca_kernel<ACA_NT><<<grid, ACA_NT, smem, st>>>(tasks_dev, ntasks, counter, tol2, vec_in_smem);
+  aca_kernel<ACA_NT><<<grid, ACA_NT, smem, st>>>(tasks_dev, ntasks, counter, tol2);
   e = cudaGetLastError();
   cudaFreeAsync(counter, st);
   hk_count_launch();
   return e;
 }
+
+size_t hk_aca_scratch_doubles(int cap) { return (size_t)(2 * (ACA_NT / 32) + 1) * cap + KC; }

@@ -170,7 +170,7 @@ struct hk_plan {
   std::vector<BlockGeom> blocks;
   std::vector<int> block_order;     // largest first
   int64_t uv_per_front = 0, trace_per_front = 0;
-  DevBuf At, UV, ranks_d, trace_d, tasks_d;
+  DevBuf At, UV, ranks_d, trace_d, tasks_d, aca_scr;
   std::vector<int32_t> ranks;       // batch * nblocks
   bool have_trace = false;
   // bdlr
@@ -204,7 +204,7 @@ struct hk_plan {
       }
       delete p;
     }
-    DevBuf* bufs[] = {&At, &UV, &ranks_d, &trace_d, &tasks_d, &sel_d, &work_d, &perm_d,
+    DevBuf* bufs[] = {&aca_scr, &At, &UV, &ranks_d, &trace_d, &tasks_d, &sel_d, &work_d, &perm_d,
                       &skel_status_d, &probe_d, &Y, &Ytmp, &F, &I, &ftask_d, &fmap_d, &gj_d, &gj2_d, &gjs_d,
                       &Xin, &X2, &G, &Yv};
     for (DevBuf* b : bufs) b->release();
@@ -424,6 +424,13 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
   tasks.reserve((size_t)p->batch * p->blocks.size());
   int max_cap = 0, max_m = 0, max_mn = 0;
   const size_t nb = p->blocks.size();
+  size_t scr_per_front = 0;
+  std::vector<size_t> scr_off(nb);
+  for (size_t bi = 0; bi < nb; ++bi) {
+    scr_off[bi] = scr_per_front;
+    scr_per_front += hk_aca_scratch_doubles(p->blocks[bi].cap);
+  }
+  CU(p->aca_scr.ensure((size_t)p->batch * scr_per_front * 8 + 8, st));
   for (int64_t f = 0; f < p->batch; ++f) {
     for (int bi : p->block_order) {
       const BlockGeom& b = p->blocks[bi];
@@ -434,6 +441,7 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
       t.V = p->UV.as<double>() + f * p->uv_per_front + b.v_off;
       t.rank = p->ranks_d.as<int32_t>() + f * nb + bi;
       t.trace = p->have_trace ? p->trace_d.as<int32_t>() + f * p->trace_per_front + b.t_off : nullptr;
+      t.scratch = p->aca_scr.as<double>() + f * scr_per_front + scr_off[bi];
       t.lda = ld;
       t.m = b.m;
       t.n = b.n;
@@ -466,7 +474,7 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
     for (size_t i = 0; i < tasks.size(); ++i) tasks[i].clock = clk.as<int64_t>() + 3 * i;
   }
   CU(upload(p->tasks_d, tasks, st));
-  if ((size_t)max_cap * 24 + max_m + 2048 > 220 * 1024)
+  if ((size_t)(max_cap + 16) * 8 + max_m + 1024 > 220 * 1024)
     return fail(HK_ERR_VALUE, "block too large for the single-CTA ACA kernel");
   CU(cudaEventRecord(p->ev[3], st));
   CU(hk_launch_aca(p->tasks_d.as<AcaTask>(), (int)tasks.size(), max_cap, max_m, tol2, st, max_mn));
@@ -1515,7 +1523,7 @@ extern "C" hk_status hk_aca_block(const double* a, int64_t m, int64_t n, int64_t
     if (ncols) *ncols = 0;
     return HK_OK;
   }
-  if ((size_t)cap * 16 + m > 220 * 1024) return fail(HK_ERR_VALUE, "block too large for the ACA kernel");
+  if ((size_t)(cap + 16) * 8 + m + 1024 > 220 * 1024) return fail(HK_ERR_VALUE, "block too large for the ACA kernel");
   // square zero-padded copy of the block and its transpose, both ld = sq
   const int64_t sq = std::max(m, n);
   const int64_t tlen = 2 + (m + cap + 1) + (cap + 1);
@@ -1528,7 +1536,10 @@ extern "C" hk_status hk_aca_block(const double* a, int64_t m, int64_t n, int64_t
   CU(cudaMemsetAsync(sqbuf, 0, (size_t)sq * sq * 8, st));
   CU(cudaMemcpy2DAsync(sqbuf, sq * 8, a, ld * 8, n * 8, m, cudaMemcpyDeviceToDevice, st));
   CU(hk_launch_transpose(sqbuf, at, sq, sq, 1, 0, st));
+  double* scr = nullptr;
+  CU(cudaMallocAsync(&scr, hk_aca_scratch_doubles((int)cap) * 8, st));
   AcaTask t{};
+  t.scratch = scr;
   t.A = sqbuf;
   t.At = at;
   t.lda = sq;
@@ -1554,7 +1565,7 @@ extern "C" hk_status hk_aca_block(const double* a, int64_t m, int64_t n, int64_t
   if (trows) std::memcpy(trows, h.data() + 2, (size_t)h[0] * 4);
   if (tcols) std::memcpy(tcols, h.data() + 2 + (m + cap + 1), (size_t)h[1] * 4);
   cudaFreeAsync(at, st); cudaFreeAsync(rk, st); cudaFreeAsync(tr, st);
-  cudaFreeAsync(sqbuf, st); cudaFreeAsync(td, st);
+  cudaFreeAsync(sqbuf, st); cudaFreeAsync(td, st); cudaFreeAsync(scr, st);
   return HK_OK;
 }
 

@@ -11,21 +11,59 @@
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, NT = 128, PAD = 4;
+constexpr int BM = 64, BN = 64, BK = 16, NT = 128, STAGES = 4;
+constexpr int SA = BM + 4;   // k-major A rows (transA = 0): conflict-free DMMA fragment loads
+constexpr int ST = BK + 4;   // m/n-major rows (transA = 1 and B)
 
-__global__ void __launch_bounds__(NT) gemm_kernel(const GemmTask* __restrict__ tasks,
-                                                  const int32_t* __restrict__ tilemap) {
-  const int task = tilemap[3 * blockIdx.x];
-  const int tm = tilemap[3 * blockIdx.x + 1];
-  const int tn = tilemap[3 * blockIdx.x + 2];
-  const GemmTask t = tasks[task];
-  __shared__ double As[2][BK][BM + PAD];
-  __shared__ double Bs[2][BK][BN + PAD];
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// One 64x64 tile of C = alpha op(A) B + beta C (+ diag on C's diagonal).
+// Four-stage cp.async pipeline (global -> SMEM without register staging) so the
+// L2 latency of the next k-tiles overlaps the DMMA work of the current one.
+template <int TRANSA>
+__device__ __forceinline__ void gemm_tile(const GemmTask& t, int tm, int tn, double* smem) {
+  constexpr int A_STAGE = TRANSA ? BM * ST : BK * SA;
+  constexpr int B_STAGE = BN * ST;
+  double* As = smem;
+  double* Bs = smem + STAGES * A_STAGE;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gid = lane >> 2, tig = lane & 3;
   const int wm = warp & 1, wn = warp >> 1;
   const int m0 = tm * BM, n0 = tn * BN;
   const int M = t.m, N = t.n, K = t.k;
+  const double* __restrict__ Ag = t.A;
+  const double* __restrict__ Bg = t.B;
+
+  auto load_stage = [&](int kt, int stage) {
+    const int k0 = kt * BK;
+    double* as = As + stage * A_STAGE;
+    double* bs = Bs + stage * B_STAGE;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int idx = tid + NT * q;
+      if (!TRANSA) {
+        const int i = idx % BM, l = idx / BM;
+        const bool ok = (m0 + i < M) && (k0 + l < K);
+        const double* src = ok ? Ag + (m0 + i) + (int64_t)(k0 + l) * t.lda : Ag;
+        cp_async8(as + l * SA + i, src, ok ? 8 : 0);
+      } else {
+        const int l = idx % BK, i = idx / BK;
+        const bool ok = (m0 + i < M) && (k0 + l < K);
+        const double* src = ok ? Ag + (k0 + l) + (int64_t)(m0 + i) * t.lda : Ag;
+        cp_async8(as + i * ST + l, src, ok ? 8 : 0);
+      }
+      const int l = idx % BK, j = idx / BK;
+      const bool okb = (n0 + j < N) && (k0 + l < K);
+      const double* srcb = okb ? Bg + (k0 + l) + (int64_t)(n0 + j) * t.ldb : Bg;
+      cp_async8(bs + j * ST + l, srcb, okb ? 8 : 0);
+    }
+  };
 
   double acc[4][4][2];
 #pragma unroll
@@ -33,60 +71,38 @@ __global__ void __launch_bounds__(NT) gemm_kernel(const GemmTask* __restrict__ t
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  double ra[8], rb[8];
-  auto load_regs = [&](int k0) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int idx = tid + NT * q;
-      int i, l;
-      if (!t.transA) { i = idx % BM; l = idx / BM; }
-      else { i = idx / BK; l = idx % BK; }
-      const int gi = m0 + i, gl = k0 + l;
-      double v = 0.0;
-      if (gi < M && gl < K)
-        v = t.transA ? t.A[gl + (int64_t)gi * t.lda] : t.A[gi + (int64_t)gl * t.lda];
-      ra[q] = v;
-      const int l2 = idx % BK, j2 = idx / BK;
-      const int gj = n0 + j2, gl2 = k0 + l2;
-      rb[q] = (gj < N && gl2 < K) ? t.B[gl2 + (int64_t)gj * t.ldb] : 0.0;
-    }
-  };
-  auto store_regs = [&](int buf) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int idx = tid + NT * q;
-      int i, l;
-      if (!t.transA) { i = idx % BM; l = idx / BM; }
-      else { i = idx / BK; l = idx % BK; }
-      As[buf][l][i] = ra[q];
-      Bs[buf][idx % BK][idx / BK] = rb[q];
-    }
-  };
-
   const int nk = (K + BK - 1) / BK;
-  if (nk > 0) {
-    load_regs(0);
-    store_regs(0);
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_stage(s, s);
+    cp_async_commit();
   }
-  __syncthreads();
   for (int kt = 0; kt < nk; ++kt) {
-    const int buf = kt & 1;
-    if (kt + 1 < nk) load_regs((kt + 1) * BK);
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    const int stage = kt % STAGES;
+    const double* as = As + stage * A_STAGE;
+    const double* bs = Bs + stage * B_STAGE;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double a[4], b[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[buf][kk + tig][wm * 32 + i * 8 + gid];
+      for (int i = 0; i < 4; ++i) {
+        const int r = wm * 32 + i * 8 + gid;
+        a[i] = TRANSA ? as[r * ST + kk + tig] : as[(kk + tig) * SA + r];
+      }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[buf][kk + tig][wn * 32 + j * 8 + gid];
+      for (int j = 0; j < 4; ++j) b[j] = bs[(wn * 32 + j * 8 + gid) * ST + kk + tig];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
-    if (kt + 1 < nk) store_regs(buf ^ 1);
-    __syncthreads();
+    const int nxt = kt + STAGES - 1;
+    if (nxt < nk) load_stage(nxt, nxt % STAGES);
+    cp_async_commit();
   }
+  cp_async_wait<0>();
 
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -106,6 +122,19 @@ __global__ void __launch_bounds__(NT) gemm_kernel(const GemmTask* __restrict__ t
       }
     }
   }
+}
+
+constexpr size_t GEMM_SMEM = (size_t)STAGES * (BM * ST + BN * ST) * 8;   // >= transA=0 layout
+
+__global__ void __launch_bounds__(NT, 2) gemm_kernel(const GemmTask* __restrict__ tasks,
+                                                     const int32_t* __restrict__ tilemap) {
+  extern __shared__ __align__(16) double gsmem[];
+  const int task = tilemap[3 * blockIdx.x];
+  const int tm = tilemap[3 * blockIdx.x + 1];
+  const int tn = tilemap[3 * blockIdx.x + 2];
+  const GemmTask t = tasks[task];
+  if (t.transA) gemm_tile<1>(t, tm, tn, gsmem);
+  else gemm_tile<0>(t, tm, tn, gsmem);
 }
 
 __global__ void copy_kernel(const CopyTask* __restrict__ tasks) {
@@ -129,7 +158,14 @@ __global__ void fill_kernel(double* p, int64_t n, double v) {
 cudaError_t hk_launch_gemm(const GemmTask* tasks_dev, const int32_t* tilemap_dev, int ntiles,
                            cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
-  gemm_kernel<<<ntiles, NT, 0, st>>>(tasks_dev, tilemap_dev);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)GEMM_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  gemm_kernel<<<ntiles, NT, GEMM_SMEM, st>>>(tasks_dev, tilemap_dev);
   hk_count_launch();
   return cudaGetLastError();
 }

@@ -12,6 +12,7 @@ struct AcaTask {
   int32_t* rank;     // out
   int32_t* trace;    // optional: [0]=#rows, [1]=#cols, rows[m+cap+1], cols[cap+1]
   int64_t* clock;    // optional profiling probe: [start ns, end ns, smid]
+  double* scratch;   // hk_aca_scratch_doubles(cap): per-warp dot partials
   int64_t lda;
   int32_t m, n, cap;
   int32_t pad;
@@ -99,6 +100,7 @@ cudaError_t hk_launch_transpose(const double* A, double* At, int64_t n, int64_t 
                                 int64_t stride, cudaStream_t st);
 cudaError_t hk_launch_aca(const AcaTask* tasks_dev, int ntasks, int max_cap, int max_m,
                           double tol2, cudaStream_t st, int max_mn);
+size_t hk_aca_scratch_doubles(int cap);
 cudaError_t hk_launch_skeleton(const SkelTask* tasks_dev, int ntasks, int max_k, int max_kc,
                                cudaStream_t st);
 cudaError_t hk_launch_lu(const LuTask* tasks_dev, int ntasks, int maxN, cudaStream_t st);
