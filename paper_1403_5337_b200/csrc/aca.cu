@@ -23,7 +23,7 @@
 
 namespace {
 
-constexpr int ACA_NT = 128;
+constexpr int ACA_NT = 256;
 
 __global__ void transpose_kernel(const double* __restrict__ A, double* __restrict__ At,
                                  int64_t n, int64_t ld, int64_t stride) {
@@ -59,102 +59,144 @@ __device__ __forceinline__ double transpose_reduce16(double (&a)[16], int lane) 
   return a[0] + __shfl_xor_sync(0xffffffffu, a[0], 16);
 }
 
-constexpr int EPT = 4;    // elements per thread per pass group
-constexpr int KC = 16;    // columns per chunk (one transpose-reduce each)
+constexpr int KC = 8;     // columns per chunk (one transpose-reduce each)
 
-// Fused residual sweep over one cross vector of length `len`:
+// Lane l of the warp receives the warp-wide sum of a[l & 7] (butterfly
+// reduce-scatter inside groups of 8 lanes, then two exchanges between groups).
+__device__ __forceinline__ double transpose_reduce8(double (&a)[8], int lane) {
+#pragma unroll
+  for (int s = 4; s >= 1; s >>= 1) {
+    const bool upper = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const double send = upper ? a[i] : a[i + s];
+      const double keep = upper ? a[i + s] : a[i];
+      a[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  double v = a[0];
+  v += __shfl_xor_sync(0xffffffffu, v, 8);
+  v += __shfl_xor_sync(0xffffffffu, v, 16);
+  return v;
+}
+
+// Fused residual sweep over one cross vector of length `len` (one element per
+// thread, e = g0 + tid):
 //   out[e] = src[e] - sum_{k<nk} coef[k] * F[e + k*len]   (reference k order,
 //            separate IEEE multiply and subtract: bit-exact)
 // and, for k < ndot, the per-warp partial dot products
 //   part[w*pld + k] = sum_{e owned by warp w} pend[e] * F[e + k*len]
 // of the PREVIOUS cross `pend` with the accepted crosses: the stopping-test
 // terms of the pending step ride along with the next step's sweep, so each
-// cross vector is streamed once per step instead of twice.  Elements are
-// owned by thread (e = g0 + tid + q*NT), loads are coalesced over e and
-// batched 8 deep; partial sums are reduced with a warp transpose-reduce and
-// accumulated per warp in a fixed order (deterministic).
-// out == nullptr: dots only.  used != nullptr: column sweep (argmax over
-// untouched rows and the sum of squares are returned); else row sweep
-// (argmax over all entries).
+// cross vector is streamed once per step.  Loads are software-pipelined in
+// chunks of KC columns: the next chunk's loads are in flight while the
+// current chunk's subtract chain runs (coalesced over e).  Partial sums are
+// reduced with a warp transpose-reduce and accumulated per warp in a fixed
+// order (deterministic).  out == nullptr: dots only.  used != nullptr: column
+// sweep (argmax over untouched entries + sum of squares); else row sweep.
 template <int NT>
-__device__ __forceinline__ void fused_sweep(const double* __restrict__ F, int len, int nk, int ndot,
+__device__ __noinline__ void fused_sweep(const double* __restrict__ F, int len, int nk, int ndot,
                                             const double* __restrict__ coef,
                                             const double* __restrict__ src, double* __restrict__ out,
                                             const double* __restrict__ pend, double* __restrict__ part,
                                             int pld, const unsigned char* __restrict__ used,
-                                            ArgMax& best, double& sumsq) {
+                                            ArgMax& best, double& sumsq, double& bestval) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   best.v = 0.0;
   best.i = -1;
+  bestval = 0.0;
   sumsq = 0.0;
   double* mypart = part + warp * pld;
   for (int k = lane; k < ndot; k += 32) mypart[k] = 0.0;
   __syncwarp();
   const int kmax = nk > ndot ? nk : ndot;
-  for (int g0 = 0; g0 < len; g0 += NT * EPT) {
-    double x[EPT], pv[EPT];
+  const int nchunks = (kmax + KC - 1) / KC;
+  for (int g0 = 0; g0 < len; g0 += NT) {
+    const int e = g0 + tid;
+    const bool ok = e < len;
+    double x = (ok && src) ? src[e] : 0.0;
+    const double pv = (ok && ndot > 0) ? pend[e] : 0.0;
+    const double* p = F + (ok ? e : 0);
+    double cur[KC], nxt[KC];
+    if (nchunks > 0) {
 #pragma unroll
-    for (int q = 0; q < EPT; ++q) {
-      const int e = g0 + tid + q * NT;
-      const bool ok = e < len;
-      x[q] = (ok && src) ? src[e] : 0.0;
-      pv[q] = (ok && ndot > 0) ? pend[e] : 0.0;
+      for (int j = 0; j < KC; ++j)
+        cur[j] = (ok && (j < nk || j < ndot)) ? p[(int64_t)j * len] : 0.0;
     }
-    for (int kb = 0; kb < kmax; kb += KC) {
-      const int kn = nk - kb;             // chain columns left (may be <= 0)
-      const int dn = ndot - kb;           // dot columns left (may be <= 0)
-      double acc[KC];
+    for (int c = 0; c < nchunks; ++c) {
+      const int kb = c * KC;
+      if (c + 1 < nchunks) {
 #pragma unroll
-      for (int j = 0; j < KC; ++j) acc[j] = 0.0;
-#pragma unroll
-      for (int q = 0; q < EPT; ++q) {
-        const int e = g0 + tid + q * NT;
-        if (e >= len) continue;
-        const double* p = F + e + (int64_t)kb * len;
-        double xq = x[q];
-        const double pq = pv[q];
-#pragma unroll
-        for (int h = 0; h < KC / 8; ++h) {
-          double a[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int kk = h * 8 + j;
-            a[j] = (kk < kn || kk < dn) ? p[(int64_t)kk * len] : 0.0;
-          }
-          double pr[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) pr[j] = mul_rn(coef[kb + h * 8 + j], a[j]);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int kk = h * 8 + j;
-            if (kk < kn) xq = sub_rn(xq, pr[j]);
-            if (kk < dn) acc[kk] += pq * a[j];
-          }
+        for (int j = 0; j < KC; ++j) {
+          const int kk = kb + KC + j;
+          nxt[j] = (ok && (kk < nk || kk < ndot)) ? p[(int64_t)kk * len] : 0.0;
         }
-        x[q] = xq;
       }
-      if (dn > 0) {
-        const double v = transpose_reduce16(acc, lane);
-        if (lane < 16 && lane < dn) mypart[kb + lane] += v;
+      double pr[KC], acc[KC];
+#pragma unroll
+      for (int j = 0; j < KC; ++j) {
+        pr[j] = mul_rn(coef[kb + j], cur[j]);
+        acc[j] = pv * cur[j];
       }
+#pragma unroll
+      for (int j = 0; j < KC; ++j)
+        if (kb + j < nk) x = sub_rn(x, pr[j]);
+      if (kb < ndot) {                       // warp-uniform
+#pragma unroll
+        for (int j = 0; j < KC; ++j)
+          if (kb + j >= ndot) acc[j] = 0.0;
+        const double v = transpose_reduce8(acc, lane);
+        if (lane < KC && kb + lane < ndot) mypart[kb + lane] += v;
+      }
+#pragma unroll
+      for (int j = 0; j < KC; ++j) cur[j] = nxt[j];
     }
-    if (out) {
-#pragma unroll
-      for (int q = 0; q < EPT; ++q) {
-        const int e = g0 + tid + q * NT;
-        if (e >= len) continue;
-        out[e] = x[q];
-        const double ax = fabs(x[q]);
-        if (used) {
-          sumsq += x[q] * x[q];
-          if (!used[e] && argmax_better(ax, e, best.v, best.i)) { best.v = ax; best.i = e; }
-        } else if (argmax_better(ax, e, best.v, best.i)) {
-          best.v = ax;
-          best.i = e;
-        }
+    if (out && ok) {
+      out[e] = x;
+      const double ax = fabs(x);
+      if (used) {
+        sumsq += x * x;
+        if (!used[e] && argmax_better(ax, e, best.v, best.i)) { best.v = ax; best.i = e; bestval = x; }
+      } else if (argmax_better(ax, e, best.v, best.i)) {
+        best.v = ax;
+        best.i = e;
+        bestval = x;
       }
     }
   }
+}
+
+// Block argmax that also carries the signed value of the winner.
+template <int NT>
+__device__ __forceinline__ ArgMax block_argmax_val(ArgMax a, double val, double* sv, int64_t* si,
+                                                   double* sval, double& out_val) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ov = __shfl_down_sync(0xffffffffu, a.v, off);
+    const long long oi = __shfl_down_sync(0xffffffffu, (long long)a.i, off);
+    const double ox = __shfl_down_sync(0xffffffffu, val, off);
+    if (argmax_better(ov, oi, a.v, a.i)) { a.v = ov; a.i = oi; val = ox; }
+  }
+  if (lane == 0) { sv[warp] = a.v; si[warp] = a.i; sval[warp] = val; }
+  __syncthreads();
+  if (warp == 0) {
+    ArgMax b;
+    double bv = 0.0;
+    if (lane < NT / 32) { b.v = sv[lane]; b.i = si[lane]; bv = sval[lane]; }
+    else { b.v = 0.0; b.i = -1; }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ov = __shfl_down_sync(0xffffffffu, b.v, off);
+      const long long oi = __shfl_down_sync(0xffffffffu, (long long)b.i, off);
+      const double ox = __shfl_down_sync(0xffffffffu, bv, off);
+      if (argmax_better(ov, oi, b.v, b.i)) { b.v = ov; b.i = oi; bv = ox; }
+    }
+    if (lane == 0) { sv[0] = b.v; si[0] = b.i; sval[0] = bv; }
+  }
+  __syncthreads();
+  out_val = sval[0];
+  return ArgMax{sv[0], si[0]};
 }
 
 // est = fro2 + cross + sum_k 2 (u.u_k)(v.v_k) over the per-warp partials,
@@ -190,11 +232,12 @@ __device__ __forceinline__ double stopping_estimate(const double* __restrict__ p
 // blocks first), so the long root chains start at t = 0 whatever the hardware
 // dispatch order of CTAs is.
 template <int NT>
-__device__ void aca_block(const AcaTask& t, double tol2);
+__device__ void aca_block(const AcaTask& t, double tol2, int part_in_smem);
 
 template <int NT>
-__global__ void __launch_bounds__(NT, 4) aca_kernel(const AcaTask* __restrict__ tasks, int ntasks,
-                                                    int* __restrict__ counter, double tol2) {
+__global__ void __launch_bounds__(NT, 2) aca_kernel(const AcaTask* __restrict__ tasks, int ntasks,
+                                                    int* __restrict__ counter, double tol2,
+                                                    int part_in_smem) {
   __shared__ int s_task;
   for (;;) {
     if (threadIdx.x == 0) s_task = atomicAdd(counter, 1);
@@ -202,29 +245,30 @@ __global__ void __launch_bounds__(NT, 4) aca_kernel(const AcaTask* __restrict__ 
     const int ti = s_task;
     __syncthreads();
     if (ti >= ntasks) break;
-    aca_block<NT>(tasks[ti], tol2);
+    aca_block<NT>(tasks[ti], tol2, part_in_smem);
     __syncthreads();
   }
 }
 
 template <int NT>
-__device__ void aca_block(const AcaTask& t, double tol2) {
+__device__ void aca_block(const AcaTask& t, double tol2, int part_in_smem) {
   const int m = t.m, n = t.n, cap = t.cap;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
   uint64_t t_start = 0;
   if (t.clock && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   extern __shared__ __align__(16) unsigned char smraw[];
-  double* coef = reinterpret_cast<double*>(smraw);                        // [cap + KC]
-  unsigned char* used = reinterpret_cast<unsigned char*>(coef + cap + KC);  // [m]
-  __shared__ double red_v[NW], red_a[NW], red_b[NW];
+  // SMEM: coef[cap+KC]; when part_in_smem: partU/partV [NW*cap] and prod[cap]; used[m]
+  double* coef = reinterpret_cast<double*>(smraw);
+  const int pld = cap;
+  double* partU = part_in_smem ? coef + cap + KC : t.scratch;
+  double* partV = partU + NW * pld;
+  double* prod = partV + NW * pld;
+  unsigned char* used = reinterpret_cast<unsigned char*>(part_in_smem ? prod + cap : coef + cap + KC);
+  __shared__ double red_v[NW], red_a[NW], red_b[NW], red_x[NW];
   __shared__ int64_t red_i[NW];
   __shared__ int s_row;
   __shared__ double s_est;
-  const int pld = cap;
-  double* partU = t.scratch;                 // [NW * cap]
-  double* partV = partU + NW * pld;          // [NW * cap]
-  double* prod = partV + NW * pld;           // [cap]
 
   int32_t* trows = t.trace ? t.trace + 2 : nullptr;
   int32_t* tcols = t.trace ? t.trace + 2 + (m + cap + 1) : nullptr;
@@ -250,7 +294,7 @@ __device__ void aca_block(const AcaTask& t, double tol2) {
   bool pending = false;                       // column r holds an undecided cross
   double uu_p = 0.0, vv_p = 0.0, fro2 = 0.0;
   ArgMax best, nxt;
-  double dummy, uu;
+  double dummy, uu, bval;
 
   for (;;) {
     const int c = r + (pending ? 1 : 0);     // index of the new candidate
@@ -258,9 +302,9 @@ __device__ void aca_block(const AcaTask& t, double tol2) {
     if (!can_step) {
       if (pending) {                          // decide the last cross: dots only
         fused_sweep<NT>(U, m, 0, r, coef, nullptr, nullptr, U + (int64_t)r * m, partU, pld,
-                        nullptr, best, dummy);
+                        nullptr, best, dummy, bval);
         fused_sweep<NT>(V, n, 0, r, coef, nullptr, nullptr, V + (int64_t)r * n, partV, pld,
-                        nullptr, best, dummy);
+                        nullptr, best, dummy, bval);
         __syncthreads();
         const double cross = uu_p * vv_p;
         const double est = stopping_estimate<NT>(partU, partV, pld, r, fro2, cross, prod, &s_est);
@@ -279,14 +323,14 @@ __device__ void aca_block(const AcaTask& t, double tol2) {
     __syncthreads();
     // residual row (:253-256) + the pending cross's v dots
     fused_sweep<NT>(V, n, c, pending ? r : 0, coef, Ab + (int64_t)row * t.lda, V + (int64_t)c * n,
-                    V + (int64_t)r * n, partV, pld, nullptr, best, dummy);
-    best = block_argmax<NT, false>(best, red_v, red_i);
+                    V + (int64_t)r * n, partV, pld, nullptr, best, dummy, bval);
+    double delta;
+    best = block_argmax_val<NT>(best, bval, red_v, red_i, red_x, delta);
     const int col = (int)best.i;
-    const double delta = V[(int64_t)c * n + col];
     if (delta == 0.0) {                       // zero residual row (:258-264)
       if (pending) {
         fused_sweep<NT>(U, m, 0, r, coef, nullptr, nullptr, U + (int64_t)r * m, partU, pld,
-                        nullptr, nxt, dummy);
+                        nullptr, nxt, dummy, bval);
         __syncthreads();
         const double cross = uu_p * vv_p;
         const double est = stopping_estimate<NT>(partU, partV, pld, r, fro2, cross, prod, &s_est);
@@ -312,23 +356,18 @@ __device__ void aca_block(const AcaTask& t, double tol2) {
     // v = res / delta (:265) over own elements (same ownership as the sweep)
     double* vout = V + (int64_t)c * n;
     double vv = 0.0;
-    for (int g0 = 0; g0 < n; g0 += NT * EPT)
-#pragma unroll
-      for (int q = 0; q < EPT; ++q) {
-        const int e = g0 + tid + q * NT;
-        if (e < n) {
-          const double v = div_rn(vout[e], delta);
-          vout[e] = v;
-          vv += v * v;
-        }
-      }
+    for (int e = tid; e < n; e += NT) {
+      const double v = div_rn(vout[e], delta);
+      vout[e] = v;
+      vv += v * v;
+    }
     for (int k = tid; k < c; k += NT) coef[k] = V[(int64_t)k * n + col];
     if (tid == 0 && tcols) tcols[ncol_ev] = col;
     ++ncol_ev;
     __syncthreads();
     // residual column (:266-268) + next-row candidate (:283) + pending u dots
     fused_sweep<NT>(U, m, c, pending ? r : 0, coef, Atb + (int64_t)col * t.lda, U + (int64_t)c * m,
-                    U + (int64_t)r * m, partU, pld, used, nxt, uu);
+                    U + (int64_t)r * m, partU, pld, used, nxt, uu, bval);
     {
       nxt = warp_argmax(nxt);
       uu = warp_sum(uu);
@@ -397,7 +436,10 @@ cudaError_t hk_launch_aca(const AcaTask* tasks_dev, int ntasks, int max_cap, int
                           double tol2, cudaStream_t st, int max_mn) {
   (void)max_mn;
   if (ntasks == 0) return cudaSuccess;
-  const size_t smem = (size_t)(max_cap + KC) * 8 + (size_t)max_m + 16;
+  const size_t part_bytes = (size_t)(2 * (ACA_NT / 32) + 1) * max_cap * 8;
+  const size_t base = (size_t)(max_cap + KC) * 8 + (size_t)max_m + 16;
+  const int part_in_smem = base + part_bytes <= 100 * 1024 ? 1 : 0;
+  const size_t smem = base + (part_in_smem ? part_bytes : 0);
   cudaError_t e = cudaFuncSetAttribute(aca_kernel<ACA_NT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -412,7 +454,7 @@ cudaError_t hk_launch_aca(const AcaTask* tasks_dev, int ntasks, int max_cap, int
   e = cudaMallocAsync(&counter, sizeof(int), st);
   if (e != cudaSuccess) return e;
   cudaMemsetAsync(counter, 0, sizeof(int), st);
-  aca_kernel<ACA_NT><<<grid, ACA_NT, smem, st>>>(tasks_dev, ntasks, counter, tol2);
+  aca_kernel<ACA_NT><<<grid, ACA_NT, smem, st>>>(tasks_dev, ntasks, counter, tol2, part_in_smem);
   e = cudaGetLastError();
   cudaFreeAsync(counter, st);
   hk_count_launch();

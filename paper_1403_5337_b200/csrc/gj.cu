@@ -24,6 +24,7 @@ __global__ void __launch_bounds__(NT) gj_kernel(const GjTask* __restrict__ tasks
   const GjTask t = tasks[blockIdx.x];
   const int N = t.N;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
   extern __shared__ __align__(16) unsigned char smraw[];
   const bool in_smem = gj_bytes(N) <= smem_bytes;
   double* W = in_smem ? reinterpret_cast<double*>(smraw) : t.scratch;
@@ -32,42 +33,43 @@ __global__ void __launch_bounds__(NT) gj_kernel(const GjTask* __restrict__ tasks
   int* piv = reinterpret_cast<int*>(rowk + N);
   int* cperm = piv + N;
   __shared__ int s_p, s_sing;
+  __shared__ double s_rinv;
   if (N == 0) {
     if (tid == 0) *t.status = 0;
     return;
   }
-  if (tid == 0) s_sing = 0;
   if (t.mode == 0) {
-    for (int i = warp; i < N; i += NT / 32)                     // coalesced row-major read
+    for (int i = warp; i < N; i += NW)                          // coalesced row-major read
       for (int j = lane; j < N; j += 32) W[i + (int64_t)j * N] = t.src[(int64_t)i * t.src_ld + j];
   } else {
-    for (int j = warp; j < N; j += NT / 32)
+    for (int j = warp; j < N; j += NW)
       for (int i = lane; i < N; i += 32) W[i + (int64_t)j * N] = t.src[i + (int64_t)j * t.src_ld];
   }
   __syncthreads();
-  constexpr int NW = NT / 32;
-  for (int k = 0; k < N; ++k) {
-    if (warp == 0) {
-      ArgMax a{0.0, -1};
-      for (int i = k + lane; i < N; i += 32) {
-        const double v = fabs(W[i + (int64_t)k * N]);
-        if (argmax_better(v, i, a.v, a.i)) { a.v = v; a.i = i; }
-      }
-      a = warp_argmax(a);
-      if (lane == 0) {
-        s_p = (int)a.i;
-        piv[k] = (int)a.i;
-        if (!(a.v >= HK_PIVOT_FLOOR)) s_sing = 1;
-      }
+  // pivot of step 0
+  if (warp == 0) {
+    ArgMax a{0.0, -1};
+    for (int i = lane; i < N; i += 32) {
+      const double v = fabs(W[i]);
+      if (argmax_better(v, i, a.v, a.i)) { a.v = v; a.i = i; }
     }
-    __syncthreads();
+    a = warp_argmax(a);
+    if (lane == 0) {
+      s_p = (int)a.i;
+      s_sing = !(a.v >= HK_PIVOT_FLOOR);
+    }
+  }
+  __syncthreads();
+  for (int k = 0; k < N; ++k) {
     if (s_sing) break;
     const int p = s_p;
-    // gather the (swapped) pivot row and column; move old row k to row p
+    // gather the swapped pivot row / column; move old row k into row p
     for (int j = tid; j < N; j += NT) {
       const double wk = W[k + (int64_t)j * N];
-      rowk[j] = W[p + (int64_t)j * N];
+      const double wp = W[p + (int64_t)j * N];
+      rowk[j] = wp;
       if (p != k) W[p + (int64_t)j * N] = wk;
+      if (j == k) s_rinv = 1.0 / wp;
     }
     for (int i = tid; i < N; i += NT) {
       double c;
@@ -76,16 +78,33 @@ __global__ void __launch_bounds__(NT) gj_kernel(const GjTask* __restrict__ tasks
       else c = W[i + (int64_t)k * N];
       colk[i] = c;
     }
+    if (tid == 0) piv[k] = p;
     __syncthreads();
-    const double rinv = 1.0 / rowk[k];
-    // rank-1 update of every entry (column j by warp, rows by lane)
+    const double rinv = s_rinv;
+    // rank-1 update (column j by warp, rows by lane); the warp owning column
+    // k+1 also finds the next pivot while it writes that column
     for (int j = warp; j < N; j += NW) {
-      const double rj = (j == k) ? 0.0 : rowk[j] * rinv;
       double* col = W + (int64_t)j * N;
       if (j == k) {
         for (int i = lane; i < N; i += 32) col[i] = (i == k) ? rinv : -colk[i] * rinv;
-      } else {
-        for (int i = lane; i < N; i += 32) col[i] = (i == k) ? rj : col[i] - colk[i] * rj;
+        continue;
+      }
+      const double rj = rowk[j] * rinv;
+      ArgMax a{0.0, -1};
+      for (int i = lane; i < N; i += 32) {
+        const double v = (i == k) ? rj : col[i] - colk[i] * rj;
+        col[i] = v;
+        if (j == k + 1 && i > k) {
+          const double av = fabs(v);
+          if (argmax_better(av, i, a.v, a.i)) { a.v = av; a.i = i; }
+        }
+      }
+      if (j == k + 1) {
+        a = warp_argmax(a);
+        if (lane == 0) {
+          s_p = (int)a.i;
+          s_sing = !(a.v >= HK_PIVOT_FLOOR);
+        }
       }
     }
     __syncthreads();
@@ -102,7 +121,7 @@ __global__ void __launch_bounds__(NT) gj_kernel(const GjTask* __restrict__ tasks
     }
   }
   __syncthreads();
-  for (int j = warp; j < N; j += NT / 32) {
+  for (int j = warp; j < N; j += NW) {
     const double* src = W + (int64_t)cperm[j] * N;
     double* dst = t.out + (int64_t)j * t.out_ld;
     for (int i = lane; i < N; i += 32) dst[i] = src[i];
