@@ -19,6 +19,126 @@ __host__ __device__ inline size_t gj_bytes(int N) {
   return (size_t)N * N * 8 + (size_t)2 * N * 8 + (size_t)2 * N * 4;
 }
 
+// SMEM-resident variant, N <= 32*MAXQ: every lane owns rows lane + 32q of the
+// column its warp updates; the pivot column is cached in registers; all SMEM
+// addressing is 32-bit.  Two barriers per elimination step.
+template <int NT, int MAXQ>
+__global__ void __launch_bounds__(NT) gj_smem_kernel(const GjTask* __restrict__ tasks) {
+  const GjTask t = tasks[blockIdx.x];
+  const int N = t.N;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
+  extern __shared__ __align__(16) double Ws[];   // N*N column-major, then rowk[N], colk[N]
+  double* rowk = Ws + N * N;
+  double* colk = rowk + N;
+  __shared__ int piv[32 * MAXQ];
+  __shared__ int cperm[32 * MAXQ];
+  __shared__ int s_p, s_sing;
+  __shared__ double s_rinv;
+  if (N == 0) {
+    if (tid == 0) *t.status = 0;
+    return;
+  }
+  if (t.mode == 0) {
+    for (int i = warp; i < N; i += NW)
+      for (int j = lane; j < N; j += 32) Ws[i + j * N] = t.src[(int64_t)i * t.src_ld + j];
+  } else {
+    for (int j = warp; j < N; j += NW)
+      for (int i = lane; i < N; i += 32) Ws[i + j * N] = t.src[i + (int64_t)j * t.src_ld];
+  }
+  __syncthreads();
+  if (warp == 0) {
+    ArgMax a{0.0, -1};
+    for (int i = lane; i < N; i += 32) {
+      const double v = fabs(Ws[i]);
+      if (argmax_better(v, i, a.v, a.i)) { a.v = v; a.i = i; }
+    }
+    a = warp_argmax(a);
+    if (lane == 0) {
+      s_p = (int)a.i;
+      s_sing = !(a.v >= HK_PIVOT_FLOOR);
+    }
+  }
+  __syncthreads();
+  for (int k = 0; k < N; ++k) {
+    if (s_sing) break;
+    const int p = s_p;
+    for (int j = tid; j < N; j += NT) {
+      const double wk = Ws[k + j * N];
+      const double wp = Ws[p + j * N];
+      rowk[j] = wp;
+      if (p != k) Ws[p + j * N] = wk;
+      if (j == k) s_rinv = 1.0 / wp;
+    }
+    for (int i = tid; i < N; i += NT) {
+      double c;
+      if (i == k) c = 0.0;
+      else if (i == p) c = Ws[k + k * N];
+      else c = Ws[i + k * N];
+      colk[i] = c;
+    }
+    if (tid == 0) piv[k] = p;
+    __syncthreads();
+    const double rinv = s_rinv;
+    double ck[MAXQ];
+#pragma unroll
+    for (int q = 0; q < MAXQ; ++q) {
+      const int i = lane + 32 * q;
+      ck[q] = (i < N) ? colk[i] : 0.0;
+    }
+    for (int j = warp; j < N; j += NW) {
+      double* col = Ws + j * N;
+      if (j == k) {
+#pragma unroll
+        for (int q = 0; q < MAXQ; ++q) {
+          const int i = lane + 32 * q;
+          if (i < N) col[i] = (i == k) ? rinv : -ck[q] * rinv;
+        }
+        continue;
+      }
+      const double rj = rowk[j] * rinv;
+      const bool nextcol = (j == k + 1);
+      ArgMax a{0.0, -1};
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const int i = lane + 32 * q;
+        if (i < N) {
+          const double v = (i == k) ? rj : col[i] - ck[q] * rj;
+          col[i] = v;
+          if (nextcol && i > k) {
+            const double av = fabs(v);
+            if (argmax_better(av, i, a.v, a.i)) { a.v = av; a.i = i; }
+          }
+        }
+      }
+      if (nextcol) {
+        a = warp_argmax(a);
+        if (lane == 0) {
+          s_p = (int)a.i;
+          s_sing = !(a.v >= HK_PIVOT_FLOOR);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *t.status = s_sing;
+  if (s_sing) return;
+  if (tid == 0) {
+    for (int j = 0; j < N; ++j) cperm[j] = j;
+    for (int k = N - 1; k >= 0; --k) {
+      const int a = cperm[k];
+      cperm[k] = cperm[piv[k]];
+      cperm[piv[k]] = a;
+    }
+  }
+  __syncthreads();
+  for (int j = warp; j < N; j += NW) {
+    const double* src = Ws + cperm[j] * N;
+    double* dst = t.out + (int64_t)j * t.out_ld;
+    for (int i = lane; i < N; i += 32) dst[i] = src[i];
+  }
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT) gj_kernel(const GjTask* __restrict__ tasks, size_t smem_bytes) {
   const GjTask t = tasks[blockIdx.x];
@@ -130,8 +250,22 @@ __global__ void __launch_bounds__(NT) gj_kernel(const GjTask* __restrict__ tasks
 
 }  // namespace
 
+template <int NT, int MAXQ>
+static cudaError_t launch_gj_smem(const GjTask* tasks_dev, int ntasks, int maxN, cudaStream_t st) {
+  const size_t smem = (size_t)maxN * maxN * 8 + (size_t)2 * maxN * 8;
+  cudaError_t e = cudaFuncSetAttribute(gj_smem_kernel<NT, MAXQ>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  gj_smem_kernel<NT, MAXQ><<<ntasks, NT, smem, st>>>(tasks_dev);
+  hk_count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t hk_launch_gj(const GjTask* tasks_dev, int ntasks, int maxN, cudaStream_t st) {
   if (ntasks == 0) return cudaSuccess;
+  if (maxN <= 64) return launch_gj_smem<128, 2>(tasks_dev, ntasks, maxN, st);
+  if (maxN <= 128) return launch_gj_smem<256, 4>(tasks_dev, ntasks, maxN, st);
+  if (maxN <= 160) return launch_gj_smem<256, 5>(tasks_dev, ntasks, maxN, st);
   size_t need = gj_bytes(maxN);
   size_t smem = need <= GJ_SMEM_CAP ? need : 0;
   cudaError_t e;
