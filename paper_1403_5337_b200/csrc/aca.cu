@@ -81,26 +81,27 @@ __device__ __forceinline__ double transpose_reduce8(double (&a)[8], int lane) {
 }
 
 // Fused residual sweep over one cross vector of length `len` (one element per
-// thread, e = g0 + tid):
-//   out[e] = src[e] - sum_{k<nk} coef[k] * F[e + k*len]   (reference k order,
-//            separate IEEE multiply and subtract: bit-exact)
+// thread, e = g0 + tid).  F is ROW-major with row stride ldf (a multiple of
+// KC), so element e's columns kb..kb+7 are 64 contiguous bytes: four 16-byte
+// loads with immediate offsets per chunk.
+//   F[e, out_col] = src[e] - sum_{k<nk} coef[k] * F[e, k]   (reference k order,
+//                   separate IEEE multiply and subtract: bit-exact)
 // and, for k < ndot, the per-warp partial dot products
-//   part[w*pld + k] = sum_{e owned by warp w} pend[e] * F[e + k*len]
-// of the PREVIOUS cross `pend` with the accepted crosses: the stopping-test
-// terms of the pending step ride along with the next step's sweep, so each
-// cross vector is streamed once per step.  Loads are software-pipelined in
-// chunks of KC columns: the next chunk's loads are in flight while the
-// current chunk's subtract chain runs (coalesced over e).  Partial sums are
-// reduced with a warp transpose-reduce and accumulated per warp in a fixed
-// order (deterministic).  out == nullptr: dots only.  used != nullptr: column
-// sweep (argmax over untouched entries + sum of squares); else row sweep.
+//   part[w*pld + k] = sum_{e owned by warp w} F[e, pend_col] * F[e, k]
+// of the PREVIOUS cross with the accepted crosses: the stopping-test terms of
+// the pending step ride along with the next step's sweep, so each cross vector
+// is streamed once per step.  Chunks are software-pipelined (the next chunk's
+// loads are in flight while the current chunk's subtract chain runs).
+// Partial sums use a warp transpose-reduce and a fixed per-warp order
+// (deterministic).  out_col < 0: dots only.  used != nullptr: column sweep
+// (argmax over untouched entries + sum of squares); else row sweep.
 template <int NT>
-__device__ __noinline__ void fused_sweep(const double* __restrict__ F, int len, int nk, int ndot,
-                                            const double* __restrict__ coef,
-                                            const double* __restrict__ src, double* __restrict__ out,
-                                            const double* __restrict__ pend, double* __restrict__ part,
-                                            int pld, const unsigned char* __restrict__ used,
-                                            ArgMax& best, double& sumsq, double& bestval) {
+__device__ __noinline__ void fused_sweep(const double* __restrict__ F, int ldf, int len, int nk,
+                                         int ndot, const double* __restrict__ coef,
+                                         const double* __restrict__ src, int out_col, int pend_col,
+                                         double* __restrict__ part, int pld,
+                                         const unsigned char* __restrict__ used, ArgMax& best,
+                                         double& sumsq, double& bestval) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   best.v = 0.0;
   best.i = -1;
@@ -114,45 +115,52 @@ __device__ __noinline__ void fused_sweep(const double* __restrict__ F, int len, 
   for (int g0 = 0; g0 < len; g0 += NT) {
     const int e = g0 + tid;
     const bool ok = e < len;
+    const double* row = F + (int64_t)(ok ? e : 0) * ldf;
     double x = (ok && src) ? src[e] : 0.0;
-    const double pv = (ok && ndot > 0) ? pend[e] : 0.0;
-    const double* p = F + (ok ? e : 0);
-    double cur[KC], nxt[KC];
+    const double pv = (ok && ndot > 0) ? __ldca(row + pend_col) : 0.0;
+    double2 cur[KC / 2], nxt[KC / 2];
     if (nchunks > 0) {
 #pragma unroll
-      for (int j = 0; j < KC; ++j)
-        cur[j] = (ok && (j < nk || j < ndot)) ? p[(int64_t)j * len] : 0.0;
+      for (int q = 0; q < KC / 2; ++q) cur[q] = __ldca(reinterpret_cast<const double2*>(row) + q);
     }
     for (int c = 0; c < nchunks; ++c) {
       const int kb = c * KC;
       if (c + 1 < nchunks) {
+        const double2* nr = reinterpret_cast<const double2*>(row + kb + KC);
 #pragma unroll
-        for (int j = 0; j < KC; ++j) {
-          const int kk = kb + KC + j;
-          nxt[j] = (ok && (kk < nk || kk < ndot)) ? p[(int64_t)kk * len] : 0.0;
-        }
+        for (int q = 0; q < KC / 2; ++q) nxt[q] = __ldca(nr + q);
       }
-      double pr[KC], acc[KC];
+      double a[KC];
 #pragma unroll
-      for (int j = 0; j < KC; ++j) {
-        pr[j] = mul_rn(coef[kb + j], cur[j]);
-        acc[j] = pv * cur[j];
-      }
+      for (int q = 0; q < KC / 2; ++q) { a[2 * q] = cur[q].x; a[2 * q + 1] = cur[q].y; }
+      double pr[KC];
 #pragma unroll
-      for (int j = 0; j < KC; ++j)
-        if (kb + j < nk) x = sub_rn(x, pr[j]);
-      if (kb < ndot) {                       // warp-uniform
+      for (int j = 0; j < KC; ++j) pr[j] = mul_rn(coef[kb + j], a[j]);
+      if (kb + KC <= nk) {
+#pragma unroll
+        for (int j = 0; j < KC; ++j) x = sub_rn(x, pr[j]);
+      } else {
 #pragma unroll
         for (int j = 0; j < KC; ++j)
-          if (kb + j >= ndot) acc[j] = 0.0;
+          if (kb + j < nk) x = sub_rn(x, pr[j]);
+      }
+      if (kb < ndot) {                       // warp-uniform
+        double acc[KC];
+        if (kb + KC <= ndot) {
+#pragma unroll
+          for (int j = 0; j < KC; ++j) acc[j] = pv * a[j];
+        } else {
+#pragma unroll
+          for (int j = 0; j < KC; ++j) acc[j] = (kb + j < ndot) ? pv * a[j] : 0.0;
+        }
         const double v = transpose_reduce8(acc, lane);
         if (lane < KC && kb + lane < ndot) mypart[kb + lane] += v;
       }
 #pragma unroll
-      for (int j = 0; j < KC; ++j) cur[j] = nxt[j];
+      for (int q = 0; q < KC / 2; ++q) cur[q] = nxt[q];
     }
-    if (out && ok) {
-      out[e] = x;
+    if (out_col >= 0 && ok) {
+      const_cast<double*>(row)[out_col] = x;
       const double ax = fabs(x);
       if (used) {
         sumsq += x * x;
@@ -288,8 +296,9 @@ __device__ void aca_block(const AcaTask& t, double tol2, int part_in_smem) {
 
   const double* __restrict__ Ab = t.A;
   const double* __restrict__ Atb = t.At;
-  double* __restrict__ U = t.U;
-  double* __restrict__ V = t.V;
+  double* __restrict__ U = t.U;      // row-major m x ldu
+  double* __restrict__ V = t.V;      // row-major n x ldv
+  const int ldu = t.ldu, ldv = t.ldv;
   int r = 0, row = 0, nused = 0;
   bool pending = false;                       // column r holds an undecided cross
   double uu_p = 0.0, vv_p = 0.0, fro2 = 0.0;
@@ -301,10 +310,10 @@ __device__ void aca_block(const AcaTask& t, double tol2, int part_in_smem) {
     const bool can_step = pending ? (c < cap && nused < m) : (c < cap);
     if (!can_step) {
       if (pending) {                          // decide the last cross: dots only
-        fused_sweep<NT>(U, m, 0, r, coef, nullptr, nullptr, U + (int64_t)r * m, partU, pld,
-                        nullptr, best, dummy, bval);
-        fused_sweep<NT>(V, n, 0, r, coef, nullptr, nullptr, V + (int64_t)r * n, partV, pld,
-                        nullptr, best, dummy, bval);
+        fused_sweep<NT>(U, ldu, m, 0, r, coef, nullptr, -1, r, partU, pld, nullptr, best, dummy,
+                        bval);
+        fused_sweep<NT>(V, ldv, n, 0, r, coef, nullptr, -1, r, partV, pld, nullptr, best, dummy,
+                        bval);
         __syncthreads();
         const double cross = uu_p * vv_p;
         const double est = stopping_estimate<NT>(partU, partV, pld, r, fro2, cross, prod, &s_est);
@@ -319,18 +328,18 @@ __device__ void aca_block(const AcaTask& t, double tol2, int part_in_smem) {
     }
     ++nrow_ev;
     ++nused;
-    for (int k = tid; k < c; k += NT) coef[k] = U[(int64_t)k * m + row];
+    for (int k = tid; k < c; k += NT) coef[k] = __ldca(U + (int64_t)row * ldu + k);
     __syncthreads();
     // residual row (:253-256) + the pending cross's v dots
-    fused_sweep<NT>(V, n, c, pending ? r : 0, coef, Ab + (int64_t)row * t.lda, V + (int64_t)c * n,
-                    V + (int64_t)r * n, partV, pld, nullptr, best, dummy, bval);
+    fused_sweep<NT>(V, ldv, n, c, pending ? r : 0, coef, Ab + (int64_t)row * t.lda, c, r, partV,
+                    pld, nullptr, best, dummy, bval);
     double delta;
     best = block_argmax_val<NT>(best, bval, red_v, red_i, red_x, delta);
     const int col = (int)best.i;
     if (delta == 0.0) {                       // zero residual row (:258-264)
       if (pending) {
-        fused_sweep<NT>(U, m, 0, r, coef, nullptr, nullptr, U + (int64_t)r * m, partU, pld,
-                        nullptr, nxt, dummy, bval);
+        fused_sweep<NT>(U, ldu, m, 0, r, coef, nullptr, -1, r, partU, pld, nullptr, nxt, dummy,
+                        bval);
         __syncthreads();
         const double cross = uu_p * vv_p;
         const double est = stopping_estimate<NT>(partU, partV, pld, r, fro2, cross, prod, &s_est);
@@ -354,20 +363,20 @@ __device__ void aca_block(const AcaTask& t, double tol2, int part_in_smem) {
       continue;
     }
     // v = res / delta (:265) over own elements (same ownership as the sweep)
-    double* vout = V + (int64_t)c * n;
     double vv = 0.0;
     for (int e = tid; e < n; e += NT) {
-      const double v = div_rn(vout[e], delta);
-      vout[e] = v;
+      double* vp = V + (int64_t)e * ldv + c;
+      const double v = div_rn(*vp, delta);
+      *vp = v;
       vv += v * v;
     }
-    for (int k = tid; k < c; k += NT) coef[k] = V[(int64_t)k * n + col];
+    for (int k = tid; k < c; k += NT) coef[k] = __ldca(V + (int64_t)col * ldv + k);
     if (tid == 0 && tcols) tcols[ncol_ev] = col;
     ++ncol_ev;
     __syncthreads();
     // residual column (:266-268) + next-row candidate (:283) + pending u dots
-    fused_sweep<NT>(U, m, c, pending ? r : 0, coef, Atb + (int64_t)col * t.lda, U + (int64_t)c * m,
-                    U + (int64_t)r * m, partU, pld, used, nxt, uu, bval);
+    fused_sweep<NT>(U, ldu, m, c, pending ? r : 0, coef, Atb + (int64_t)col * t.lda, c, r, partU,
+                    pld, used, nxt, uu, bval);
     {
       nxt = warp_argmax(nxt);
       uu = warp_sum(uu);

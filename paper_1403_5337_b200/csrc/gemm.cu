@@ -140,10 +140,14 @@ __global__ void __launch_bounds__(NT, 2) gemm_kernel(const GemmTask* __restrict_
 __global__ void copy_kernel(const CopyTask* __restrict__ tasks) {
   const CopyTask t = tasks[blockIdx.y];
   const int64_t tot = (int64_t)t.rows * t.cols;
+  // rows fastest when the destination is column-major (the Z gather), else columns
+  const bool rows_fast = t.dst_rs == 1;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < tot;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(idx % t.rows), j = (int)(idx / t.rows);
-    t.dst[i + (int64_t)j * t.ld_dst] = t.src[i + (int64_t)j * t.ld_src];
+    int i, j;
+    if (rows_fast) { i = (int)(idx % t.rows); j = (int)(idx / t.rows); }
+    else { j = (int)(idx % t.cols); i = (int)(idx / t.cols); }
+    t.dst[i * t.dst_rs + j * t.dst_cs] = t.src[i * t.src_rs + j * t.src_cs];
   }
 }
 
