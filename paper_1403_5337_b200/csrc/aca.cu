@@ -81,9 +81,10 @@ __device__ __forceinline__ double transpose_reduce8(double (&a)[8], int lane) {
 }
 
 // Fused residual sweep over one cross vector of length `len` (one element per
-// thread, e = g0 + tid).  F is ROW-major with row stride ldf (a multiple of
-// KC), so element e's columns kb..kb+7 are 64 contiguous bytes: four 16-byte
-// loads with immediate offsets per chunk.
+// thread, e = g0 + tid).  F is COLUMN-major with a power-of-two leading
+// dimension LD = 1 << LDLOG (a template constant), so the eight loads of a
+// column chunk are immediate offsets from one per-thread pointer and every
+// warp-wide load is one coalesced 256-byte segment.
 //   F[e, out_col] = src[e] - sum_{k<nk} coef[k] * F[e, k]   (reference k order,
 //                   separate IEEE multiply and subtract: bit-exact)
 // and, for k < ndot, the per-warp partial dot products
@@ -95,13 +96,14 @@ __device__ __forceinline__ double transpose_reduce8(double (&a)[8], int lane) {
 // Partial sums use a warp transpose-reduce and a fixed per-warp order
 // (deterministic).  out_col < 0: dots only.  used != nullptr: column sweep
 // (argmax over untouched entries + sum of squares); else row sweep.
-template <int NT>
-__device__ __noinline__ void fused_sweep(const double* __restrict__ F, int ldf, int len, int nk,
-                                         int ndot, const double* __restrict__ coef,
+template <int NT, int LDLOG>
+__device__ __forceinline__ void fused_sweep_impl(const double* __restrict__ F, int len, int nk, int ndot,
+                                         const double* __restrict__ coef,
                                          const double* __restrict__ src, int out_col, int pend_col,
                                          double* __restrict__ part, int pld,
                                          const unsigned char* __restrict__ used, ArgMax& best,
                                          double& sumsq, double& bestval) {
+  constexpr int64_t LD = int64_t(1) << LDLOG;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   best.v = 0.0;
   best.i = -1;
@@ -112,55 +114,47 @@ __device__ __noinline__ void fused_sweep(const double* __restrict__ F, int ldf, 
   __syncwarp();
   const int kmax = nk > ndot ? nk : ndot;
   const int nchunks = (kmax + KC - 1) / KC;
+#pragma unroll 1
   for (int g0 = 0; g0 < len; g0 += NT) {
     const int e = g0 + tid;
     const bool ok = e < len;
-    const double* row = F + (int64_t)(ok ? e : 0) * ldf;
+    const double* col = F + (ok ? e : 0);       // this element in column 0
     double x = (ok && src) ? src[e] : 0.0;
-    const double pv = (ok && ndot > 0) ? __ldca(row + pend_col) : 0.0;
-    double2 cur[KC / 2], nxt[KC / 2];
+    const double pv = (ok && ndot > 0) ? __ldca(col + (int64_t)pend_col * LD) : 0.0;
+    double cur[KC], nxt[KC];
+    const double* pk = col;
     if (nchunks > 0) {
 #pragma unroll
-      for (int q = 0; q < KC / 2; ++q) cur[q] = __ldca(reinterpret_cast<const double2*>(row) + q);
+      for (int j = 0; j < KC; ++j) cur[j] = __ldca(pk + j * LD);
     }
+#pragma unroll 1
     for (int c = 0; c < nchunks; ++c) {
       const int kb = c * KC;
+      pk += KC * LD;
       if (c + 1 < nchunks) {
-        const double2* nr = reinterpret_cast<const double2*>(row + kb + KC);
 #pragma unroll
-        for (int q = 0; q < KC / 2; ++q) nxt[q] = __ldca(nr + q);
+        for (int j = 0; j < KC; ++j) nxt[j] = __ldca(pk + j * LD);
       }
-      double a[KC];
-#pragma unroll
-      for (int q = 0; q < KC / 2; ++q) { a[2 * q] = cur[q].x; a[2 * q + 1] = cur[q].y; }
-      double pr[KC];
-#pragma unroll
-      for (int j = 0; j < KC; ++j) pr[j] = mul_rn(coef[kb + j], a[j]);
-      if (kb + KC <= nk) {
-#pragma unroll
-        for (int j = 0; j < KC; ++j) x = sub_rn(x, pr[j]);
-      } else {
-#pragma unroll
-        for (int j = 0; j < KC; ++j)
-          if (kb + j < nk) x = sub_rn(x, pr[j]);
-      }
-      if (kb < ndot) {                       // warp-uniform
+      if (kb < ndot) {                       // warp-uniform: dots first, then the chain
         double acc[KC];
-        if (kb + KC <= ndot) {
 #pragma unroll
-          for (int j = 0; j < KC; ++j) acc[j] = pv * a[j];
-        } else {
-#pragma unroll
-          for (int j = 0; j < KC; ++j) acc[j] = (kb + j < ndot) ? pv * a[j] : 0.0;
-        }
+        for (int j = 0; j < KC; ++j) acc[j] = (kb + j < ndot) ? pv * cur[j] : 0.0;
         const double v = transpose_reduce8(acc, lane);
         if (lane < KC && kb + lane < ndot) mypart[kb + lane] += v;
       }
+      if (kb + KC <= nk) {
 #pragma unroll
-      for (int q = 0; q < KC / 2; ++q) cur[q] = nxt[q];
+        for (int j = 0; j < KC; ++j) x = sub_rn(x, mul_rn(coef[kb + j], cur[j]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < KC; ++j)
+          if (kb + j < nk) x = sub_rn(x, mul_rn(coef[kb + j], cur[j]));
+      }
+#pragma unroll
+      for (int j = 0; j < KC; ++j) cur[j] = nxt[j];
     }
     if (out_col >= 0 && ok) {
-      const_cast<double*>(row)[out_col] = x;
+      const_cast<double*>(col)[(int64_t)out_col * LD] = x;
       const double ax = fabs(x);
       if (used) {
         sumsq += x * x;
@@ -172,6 +166,28 @@ __device__ __noinline__ void fused_sweep(const double* __restrict__ F, int ldf, 
       }
     }
   }
+}
+
+// One call target for the caller (keeps its register allocation small); the
+// leading dimension is dispatched once, inside, to the specialised loop.
+template <int NT>
+__device__ __noinline__ void fused_sweep(int ldlog, const double* __restrict__ F, int len, int nk,
+                                         int ndot, const double* __restrict__ coef,
+                                         const double* __restrict__ src, int out_col, int pend_col,
+                                         double* __restrict__ part, int pld,
+                                         const unsigned char* __restrict__ used, ArgMax& best,
+                                         double& sumsq, double& bestval) {
+#define HK_SWEEP_CASE(L)                                                                         \
+  case L:                                                                                        \
+    fused_sweep_impl<NT, L>(F, len, nk, ndot, coef, src, out_col, pend_col, part, pld, used,   \
+                            best, sumsq, bestval);                                               \
+    return;
+  switch (ldlog) {
+    HK_SWEEP_CASE(6) HK_SWEEP_CASE(7) HK_SWEEP_CASE(8) HK_SWEEP_CASE(9) HK_SWEEP_CASE(10)
+    HK_SWEEP_CASE(11) HK_SWEEP_CASE(12) HK_SWEEP_CASE(13)
+    default: return;
+  }
+#undef HK_SWEEP_CASE
 }
 
 // Block argmax that also carries the signed value of the winner.
@@ -296,9 +312,10 @@ __device__ void aca_block(const AcaTask& t, double tol2, int part_in_smem) {
 
   const double* __restrict__ Ab = t.A;
   const double* __restrict__ Atb = t.At;
-  double* __restrict__ U = t.U;      // row-major m x ldu
-  double* __restrict__ V = t.V;      // row-major n x ldv
-  const int ldu = t.ldu, ldv = t.ldv;
+  double* __restrict__ U = t.U;      // column-major m x cap, leading dimension 2^ldu
+  double* __restrict__ V = t.V;      // column-major n x cap, leading dimension 2^ldv
+  const int ldlog = t.ldu;                   // U and V share one power-of-two leading dimension
+  const int64_t LDU = int64_t(1) << ldlog, LDV = LDU;
   int r = 0, row = 0, nused = 0;
   bool pending = false;                       // column r holds an undecided cross
   double uu_p = 0.0, vv_p = 0.0, fro2 = 0.0;
@@ -310,10 +327,8 @@ __device__ void aca_block(const AcaTask& t, double tol2, int part_in_smem) {
     const bool can_step = pending ? (c < cap && nused < m) : (c < cap);
     if (!can_step) {
       if (pending) {                          // decide the last cross: dots only
-        fused_sweep<NT>(U, ldu, m, 0, r, coef, nullptr, -1, r, partU, pld, nullptr, best, dummy,
-                        bval);
-        fused_sweep<NT>(V, ldv, n, 0, r, coef, nullptr, -1, r, partV, pld, nullptr, best, dummy,
-                        bval);
+        fused_sweep<NT>(ldlog, U, m, 0, r, coef, nullptr, -1, r, partU, pld, nullptr, best, dummy, bval);
+        fused_sweep<NT>(ldlog, V, n, 0, r, coef, nullptr, -1, r, partV, pld, nullptr, best, dummy, bval);
         __syncthreads();
         const double cross = uu_p * vv_p;
         const double est = stopping_estimate<NT>(partU, partV, pld, r, fro2, cross, prod, &s_est);
@@ -328,18 +343,17 @@ __device__ void aca_block(const AcaTask& t, double tol2, int part_in_smem) {
     }
     ++nrow_ev;
     ++nused;
-    for (int k = tid; k < c; k += NT) coef[k] = __ldca(U + (int64_t)row * ldu + k);
+    for (int k = tid; k < c; k += NT) coef[k] = __ldca(U + row + (int64_t)k * LDU);
     __syncthreads();
     // residual row (:253-256) + the pending cross's v dots
-    fused_sweep<NT>(V, ldv, n, c, pending ? r : 0, coef, Ab + (int64_t)row * t.lda, c, r, partV,
-                    pld, nullptr, best, dummy, bval);
+    fused_sweep<NT>(ldlog, V, n, c, pending ? r : 0, coef, Ab + (int64_t)row * t.lda, c, r, partV, pld,
+              nullptr, best, dummy, bval);
     double delta;
     best = block_argmax_val<NT>(best, bval, red_v, red_i, red_x, delta);
     const int col = (int)best.i;
     if (delta == 0.0) {                       // zero residual row (:258-264)
       if (pending) {
-        fused_sweep<NT>(U, ldu, m, 0, r, coef, nullptr, -1, r, partU, pld, nullptr, nxt, dummy,
-                        bval);
+        fused_sweep<NT>(ldlog, U, m, 0, r, coef, nullptr, -1, r, partU, pld, nullptr, nxt, dummy, bval);
         __syncthreads();
         const double cross = uu_p * vv_p;
         const double est = stopping_estimate<NT>(partU, partV, pld, r, fro2, cross, prod, &s_est);
@@ -365,18 +379,18 @@ __device__ void aca_block(const AcaTask& t, double tol2, int part_in_smem) {
     // v = res / delta (:265) over own elements (same ownership as the sweep)
     double vv = 0.0;
     for (int e = tid; e < n; e += NT) {
-      double* vp = V + (int64_t)e * ldv + c;
+      double* vp = V + e + (int64_t)c * LDV;
       const double v = div_rn(*vp, delta);
       *vp = v;
       vv += v * v;
     }
-    for (int k = tid; k < c; k += NT) coef[k] = __ldca(V + (int64_t)col * ldv + k);
+    for (int k = tid; k < c; k += NT) coef[k] = __ldca(V + col + (int64_t)k * LDV);
     if (tid == 0 && tcols) tcols[ncol_ev] = col;
     ++ncol_ev;
     __syncthreads();
     // residual column (:266-268) + next-row candidate (:283) + pending u dots
-    fused_sweep<NT>(U, ldu, m, c, pending ? r : 0, coef, Atb + (int64_t)col * t.lda, c, r, partU,
-                    pld, used, nxt, uu, bval);
+    fused_sweep<NT>(ldlog, U, m, c, pending ? r : 0, coef, Atb + (int64_t)col * t.lda, c, r, partU, pld,
+              used, nxt, uu, bval);
     {
       nxt = warp_argmax(nxt);
       uu = warp_sum(uu);

@@ -122,7 +122,8 @@ struct BlockGeom {
   int side;       // 0 upper, 1 lower
   int64_t row0, col0;
   int m, n, cap;
-  int ld;         // row stride of the row-major U (m x ld) and V (n x ld): cap rounded up to 8
+  int ldu, ldv;          // leading dimensions of the column-major U (m x cap) and V (n x cap)
+  int ldu_log, ldv_log;  // both are powers of two >= 64 (compile-time strides in aca.cu)
   int64_t u_off, v_off;   // doubles, within one front's UV region
   int64_t t_off;          // ints, within one front's trace region
 };
@@ -268,8 +269,12 @@ static void build_tree(hk_plan* p) {
     const Node& nd = p->nodes[p->internal[k]];
     const Node& a = p->nodes[nd.left];
     const Node& b = p->nodes[nd.right];
-    BlockGeom up{p->internal[k], 0, a.lo, b.lo, (int)(a.hi - a.lo), (int)(b.hi - b.lo), 0, 0, 0, 0, 0};
-    BlockGeom lw{p->internal[k], 1, b.lo, a.lo, (int)(b.hi - b.lo), (int)(a.hi - a.lo), 0, 0, 0, 0, 0};
+    BlockGeom up{};
+    up.node = p->internal[k]; up.side = 0; up.row0 = a.lo; up.col0 = b.lo;
+    up.m = (int)(a.hi - a.lo); up.n = (int)(b.hi - b.lo);
+    BlockGeom lw{};
+    lw.node = p->internal[k]; lw.side = 1; lw.row0 = b.lo; lw.col0 = a.lo;
+    lw.m = (int)(b.hi - b.lo); lw.n = (int)(a.hi - a.lo);
     p->blocks.push_back(up);
     p->blocks.push_back(lw);
   }
@@ -281,12 +286,16 @@ static void set_caps(hk_plan* p, int64_t max_rank) {
     int64_t cap = std::min(b.m, b.n);
     if (max_rank > 0) cap = std::min(cap, max_rank);
     b.cap = (int)cap;
-    b.ld = (int)((cap + 7) / 8 * 8);
-    if (b.ld == 0) b.ld = 8;
+    auto pow2log = [](int v) { int l = 6; while ((1 << l) < v) ++l; return l; };
+    // one shared power-of-two leading dimension for U and V (aca.cu template)
+    b.ldu_log = b.ldv_log = std::max(pow2log(b.m), pow2log(b.n));
+    b.ldu = 1 << b.ldu_log;
+    b.ldv = 1 << b.ldv_log;
+    // +8 columns of slack: the ACA prefetches whole 8-column chunks
     b.u_off = off;
-    off += (int64_t)b.m * b.ld;
+    off += (int64_t)b.ldu * (cap + 8);
     b.v_off = off;
-    off += (int64_t)b.n * b.ld;
+    off += (int64_t)b.ldv * (cap + 8);
     b.t_off = toff;
     toff += 2 + (b.m + cap + 1) + (cap + 1);
   }
@@ -449,8 +458,9 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
       t.m = b.m;
       t.n = b.n;
       t.cap = b.cap;
-      t.ldu = b.ld;
-      t.ldv = b.ld;
+      t.ldu = b.ldu_log;
+      t.ldv = b.ldv_log;
+      if (b.ldu_log > 13 || b.ldv_log > 13) return fail(HK_ERR_VALUE, "block too large for the ACA kernel (max 8192 rows)");
       max_cap = std::max(max_cap, b.cap);
       max_m = std::max(max_m, b.m);
       max_mn = std::max(max_mn, b.m + b.n);
@@ -610,7 +620,8 @@ extern "C" hk_status hk_build_bdlr(hk_plan* p, const double* A, int64_t ld, int6
       t.k = (int)p->rsel[bi].size();
       t.kc = (int)p->csel[bi].size();
       t.cap = b.cap;
-      t.ldf = b.ld;
+      t.ldu = b.ldu;
+      t.ldv = b.ldv;
       t.tol = tol;
       tasks.push_back(t);
     }
@@ -661,8 +672,8 @@ extern "C" hk_status hk_set_block_factor(hk_plan* p, int64_t f, int64_t bi, int6
   double* Vd = p->UV.as<double>() + f * p->uv_per_front + b.v_off;
   if (rank > 0) {   // column-major input -> row-major pool
     std::vector<CopyTask> ct(2);
-    ct[0] = CopyTask{U, Ud, 1, ldu, b.ld, 1, b.m, (int32_t)rank};
-    ct[1] = CopyTask{V, Vd, 1, ldv, b.ld, 1, b.n, (int32_t)rank};
+    ct[0] = CopyTask{U, Ud, 1, ldu, 1, b.ldu, b.m, (int32_t)rank};
+    ct[1] = CopyTask{V, Vd, 1, ldv, 1, b.ldv, b.n, (int32_t)rank};
     DevBuf tb;
     CU(upload(tb, ct, st));
     CU(hk_launch_copy(tb.as<CopyTask>(), 2, st));
@@ -722,14 +733,11 @@ extern "C" hk_status hk_get_block_factor(hk_plan* p, int64_t f, int64_t bi, doub
   const BlockGeom& b = p->blocks[bi];
   const int64_t r = p->ranks[f * p->blocks.size() + bi];
   const double* base = p->UV.as<double>() + f * p->uv_per_front;
-  if (r > 0) {   // row-major pool -> column-major host (m x r, n x r)
-    std::vector<double> h((size_t)std::max(b.m, b.n) * b.ld);
-    CU(cudaMemcpy(h.data(), base + b.u_off, (size_t)b.m * b.ld * 8, cudaMemcpyDeviceToHost));
-    for (int i = 0; i < b.m; ++i)
-      for (int k = 0; k < r; ++k) U[i + (int64_t)k * b.m] = h[(size_t)i * b.ld + k];
-    CU(cudaMemcpy(h.data(), base + b.v_off, (size_t)b.n * b.ld * 8, cudaMemcpyDeviceToHost));
-    for (int i = 0; i < b.n; ++i)
-      for (int k = 0; k < r; ++k) V[i + (int64_t)k * b.n] = h[(size_t)i * b.ld + k];
+  if (r > 0) {   // padded column-major pool -> dense column-major host (m x r, n x r)
+    CU(cudaMemcpy2D(U, (size_t)b.m * 8, base + b.u_off, (size_t)b.ldu * 8, (size_t)b.m * 8, r,
+                    cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy2D(V, (size_t)b.n * 8, base + b.v_off, (size_t)b.ldv * 8, (size_t)b.n * 8, r,
+                    cudaMemcpyDeviceToHost));
   }
   return HK_OK;
 }
@@ -875,9 +883,9 @@ extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
         const int rank = side == 0 ? r.ru : r.rl;
         if (rank == 0) continue;
         CopyTask c{};
-        c.src = UV + f * p->uv_per_front + b.u_off;   // row-major m x ld
-        c.src_rs = b.ld;
-        c.src_cs = 1;
+        c.src = UV + f * p->uv_per_front + b.u_off;   // column-major m x cap, ld ldu
+        c.src_rs = 1;
+        c.src_cs = b.ldu;
         c.dst = Yt + p->y_off[f] + b.row0 + r.w * n;   // column-major, ld n
         c.dst_rs = 1;
         c.dst_cs = n;
@@ -951,9 +959,8 @@ extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
         const int R = r.R, rl = r.rl, ru = r.ru;
         const int w = (int)r.w;
         // H[0:rl, 0:w+ru] = V_low^T Y[a, 0:w+ru];  H[rl:R, 0:w+rl] = V_up^T Y[b, 0:w+rl]
-        // V row-major (rows x ld): V^T is column-major with leading dimension ld
-        if (rl > 0) th.add(gemm(Vlow, bl.ld, 0, Yf + a.lo, n, H, R, rl, w + ru, na, 1.0, 0.0));
-        if (ru > 0) th.add(gemm(Vup, bu.ld, 0, Yf + b.lo, n, H + rl, R, ru, w + rl, nbr, 1.0, 0.0));
+        if (rl > 0) th.add(gemm(Vlow, bl.ldv, 1, Yf + a.lo, n, H, R, rl, w + ru, na, 1.0, 0.0));
+        if (ru > 0) th.add(gemm(Vup, bu.ldv, 1, Yf + b.lo, n, H + rl, R, ru, w + rl, nbr, 1.0, 0.0));
         const double* X = H + (int64_t)w * R;          // rl x ru
         const double* Yc = H + rl + (int64_t)w * R;    // ru x rl
         GjTask g{};
@@ -1179,7 +1186,7 @@ static hk_status build_solve_prog(hk_plan* p, int front, int s, SolveProg*& out,
   }
   for (int lvl = p->depth - 1; lvl >= 0; --lvl) {
     SolveProg::Level L;
-    std::vector<MatVecTask> dt;
+    std::vector<DotTask> dt;
     std::vector<MatVecTask> sv, up;
     TileList t1, t2, t3;
     for (int64_t f = f0; f < f1; ++f)
@@ -1204,9 +1211,9 @@ static hk_status build_solve_prog(hk_plan* p, int front, int s, SolveProg*& out,
         const double* dleft = Yf + a.lo + r.w * n;
         const double* dright = Yf + b.lo + r.w * n;
         if (sp->small) {
-          // g = V^T x: V row-major is V^T column-major (r x n_side, ld) -> thread per row k
-          if (rl > 0) dt.push_back(MatVecTask{Vlow, Xf + a.lo, g, bl.ld, n, R, rl, na, 0, 0});
-          if (ru > 0) dt.push_back(MatVecTask{Vup, Xf + b.lo, g + rl, bu.ld, n, R, ru, nbr, 0, 0});
+          // g = V^T x: warp per column of V (coalesced)
+          if (rl > 0) dt.push_back(DotTask{Vlow, Xf + a.lo, g, bl.ldv, n, R, na, rl});
+          if (ru > 0) dt.push_back(DotTask{Vup, Xf + b.lo, g + rl, bu.ldv, n, R, nbr, ru});
           L.dot_cols = std::max(L.dot_cols, std::max(rl, ru));
           L.dot_k = std::max(L.dot_k, std::max(na, nbr));
           sv.push_back(MatVecTask{F + r.inv, g, yv, R, R, R, R, R, 0, 0});
@@ -1217,8 +1224,8 @@ static hk_status build_solve_prog(hk_plan* p, int front, int s, SolveProg*& out,
           L.upd_rows = std::max(L.upd_rows, std::max(na, nbr));
           L.upd_k = std::max(L.upd_k, std::max(rl, ru));
         } else {
-          if (rl > 0) t1.add(gemm(Vlow, bl.ld, 0, Xf + a.lo, n, g, R, rl, s, na, 1.0, 0.0));
-          if (ru > 0) t1.add(gemm(Vup, bu.ld, 0, Xf + b.lo, n, g + rl, R, ru, s, nbr, 1.0, 0.0));
+          if (rl > 0) t1.add(gemm(Vlow, bl.ldv, 1, Xf + a.lo, n, g, R, rl, s, na, 1.0, 0.0));
+          if (ru > 0) t1.add(gemm(Vup, bu.ldv, 1, Xf + b.lo, n, g + rl, R, ru, s, nbr, 1.0, 0.0));
           t2.add(gemm(F + r.inv, R, 0, g, R, yv, R, R, s, R, 1.0, 0.0));
           if (ru > 0) t3.add(gemm(dleft, n, 0, yv + rl, R, Xf + a.lo, n, na, s, ru, -1.0, 1.0));
           if (rl > 0) t3.add(gemm(dright, n, 0, yv, R, Xf + b.lo, n, nbr, s, rl, -1.0, 1.0));
@@ -1279,7 +1286,7 @@ static hk_status run_solve(hk_plan* p, int front, double* rhs, int64_t ld, int64
   }
   for (auto& L : sp->levels) {
     if (sp->small) {
-      CU(hk_launch_matvec(L.dot_t.as<MatVecTask>(), L.n_dot, (int)s, L.dot_cols, st, L.dot_k));
+      CU(hk_launch_dot(L.dot_t.as<DotTask>(), L.n_dot, (int)s, L.dot_cols, st));
       CU(hk_launch_matvec(L.sinv_t.as<MatVecTask>(), L.n_sinv, (int)s, L.sinv_rows, st, L.sinv_k));
       CU(hk_launch_matvec(L.upd_t.as<MatVecTask>(), L.n_upd, (int)s, L.upd_rows, st, L.upd_k));
     } else {
@@ -1543,7 +1550,7 @@ extern "C" hk_status hk_aca_block(const double* a, int64_t m, int64_t n, int64_t
     if (ncols) *ncols = 0;
     return HK_OK;
   }
-  if ((size_t)(cap + 16) * 8 + m + 1024 > 220 * 1024) return fail(HK_ERR_VALUE, "block too large for the ACA kernel");
+  if ((size_t)(cap + 16) * 8 + m + 1024 > 200 * 1024) return fail(HK_ERR_VALUE, "block too large for the ACA kernel");
   // square zero-padded copy of the block and its transpose, both ld = sq
   const int64_t sq = std::max(m, n);
   const int64_t tlen = 2 + (m + cap + 1) + (cap + 1);
@@ -1558,10 +1565,13 @@ extern "C" hk_status hk_aca_block(const double* a, int64_t m, int64_t n, int64_t
   CU(hk_launch_transpose(sqbuf, at, sq, sq, 1, 0, st));
   double* scr = nullptr;
   CU(cudaMallocAsync(&scr, hk_aca_scratch_doubles((int)cap) * 8, st));
-  const int ldr = (int)((cap + 7) / 8 * 8);
+  int lmu = 6;
+  while ((1 << lmu) < std::max(m, n)) ++lmu;
+  const int lmv = lmu;
+  if (lmu > 13 || lmv > 13) return fail(HK_ERR_VALUE, "block too large for the ACA kernel (max 8192 rows)");
   double *Ur = nullptr, *Vr = nullptr;
-  CU(cudaMallocAsync(&Ur, (size_t)m * ldr * 8, st));
-  CU(cudaMallocAsync(&Vr, (size_t)n * ldr * 8, st));
+  CU(cudaMallocAsync(&Ur, ((size_t)1 << lmu) * (cap + 8) * 8, st));
+  CU(cudaMallocAsync(&Vr, ((size_t)1 << lmv) * (cap + 8) * 8, st));
   AcaTask t{};
   t.scratch = scr;
   t.A = sqbuf;
@@ -1569,8 +1579,8 @@ extern "C" hk_status hk_aca_block(const double* a, int64_t m, int64_t n, int64_t
   t.lda = sq;
   t.U = Ur;
   t.V = Vr;
-  t.ldu = ldr;
-  t.ldv = ldr;
+  t.ldu = lmu;
+  t.ldv = lmv;
   t.rank = rk;
   t.trace = tr;
   t.m = (int)m;
@@ -1587,8 +1597,8 @@ extern "C" hk_status hk_aca_block(const double* a, int64_t m, int64_t n, int64_t
   CU(cudaStreamSynchronize(st));
   if (r32 > 0) {   // row-major working factors -> the caller's column-major buffers
     std::vector<CopyTask> ct(2);
-    ct[0] = CopyTask{Ur, U, ldr, 1, 1, m, (int32_t)m, r32};
-    ct[1] = CopyTask{Vr, V, ldr, 1, 1, n, (int32_t)n, r32};
+    ct[0] = CopyTask{Ur, U, 1, (int64_t)1 << lmu, 1, m, (int32_t)m, r32};
+    ct[1] = CopyTask{Vr, V, 1, (int64_t)1 << lmv, 1, n, (int32_t)n, r32};
     CopyTask* ctd = nullptr;
     CU(cudaMallocAsync(&ctd, sizeof(CopyTask) * 2, st));
     CU(cudaMemcpyAsync(ctd, ct.data(), sizeof(CopyTask) * 2, cudaMemcpyHostToDevice, st));
@@ -1629,15 +1639,11 @@ extern "C" hk_status hk_skeleton_block(const double* a, int64_t m, int64_t n, in
   CU(cudaMallocAsync(&work, (size_t)k * kc * 8, st));
   CU(cudaMallocAsync(&small, 8, st));
   CU(cudaMemcpyAsync(seld, sel.data(), sel.size() * 8, cudaMemcpyHostToDevice, st));
-  const int ldr = (int)((std::max<int64_t>(cap, 1) + 7) / 8 * 8);
-  double *Ur = nullptr, *Vr = nullptr;
-  CU(cudaMallocAsync(&Ur, (size_t)m * ldr * 8, st));
-  CU(cudaMallocAsync(&Vr, (size_t)n * ldr * 8, st));
   SkelTask t{};
   t.A = a; t.lda = ld;
   t.rsel = seld; t.csel = seld + k;
   t.work = work; t.rperm = perm; t.cperm = perm + k;
-  t.U = Ur; t.V = Vr; t.ldf = ldr;
+  t.U = U; t.V = V; t.ldu = (int32_t)m; t.ldv = (int32_t)n;
   t.rank = small; t.status = small + 1;
   t.probe = seld + k + kc; t.nprobe = (int32_t)pr.size();
   t.m = (int)m; t.n = (int)n; t.k = (int)k; t.kc = (int)kc; t.cap = (int)cap; t.tol = tol;
@@ -1650,17 +1656,6 @@ extern "C" hk_status hk_skeleton_block(const double* a, int64_t m, int64_t n, in
   CU(cudaMemcpyAsync(hs, small, 8, cudaMemcpyDeviceToHost, st));
   CU(cudaMemcpyAsync(ph.data(), perm, ph.size() * 8, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
-  if (hs[0] > 0 && hs[1] == 0) {   // row-major working factors -> column-major outputs
-    CopyTask ct[2] = {CopyTask{Ur, U, ldr, 1, 1, m, (int32_t)m, hs[0]},
-                      CopyTask{Vr, V, ldr, 1, 1, n, (int32_t)n, hs[0]}};
-    CopyTask* ctd = nullptr;
-    CU(cudaMallocAsync(&ctd, sizeof(ct), st));
-    CU(cudaMemcpyAsync(ctd, ct, sizeof(ct), cudaMemcpyHostToDevice, st));
-    CU(hk_launch_copy(ctd, 2, st));
-    CU(cudaStreamSynchronize(st));
-    cudaFreeAsync(ctd, st);
-  }
-  cudaFreeAsync(Ur, st); cudaFreeAsync(Vr, st);
   cudaFreeAsync(seld, st); cudaFreeAsync(perm, st); cudaFreeAsync(work, st);
   cudaFreeAsync(small, st); cudaFreeAsync(td, st);
   *rank = hs[0];

@@ -7,15 +7,15 @@
 struct AcaTask {
   const double* A;   // block origin in the row-major front: A[i*lda + j]
   const double* At;  // block origin in the transposed front: column j of the block = At + j*lda
-  double* U;         // m x cap ROW-major (row stride ldu, a multiple of 8)
-  double* V;         // n x cap ROW-major (row stride ldv)
+  double* U;         // m x cap column-major, leading dimension 1 << ldu
+  double* V;         // n x cap column-major, leading dimension 1 << ldv
   int32_t* rank;     // out
   int32_t* trace;    // optional: [0]=#rows, [1]=#cols, rows[m+cap+1], cols[cap+1]
   int64_t* clock;    // optional profiling probe: [start ns, end ns, smid]
   double* scratch;   // hk_aca_scratch_doubles(cap): per-warp dot partials
   int64_t lda;
   int32_t m, n, cap;
-  int32_t ldu, ldv;
+  int32_t ldu, ldv;  // log2 of the leading dimensions (6..13)
 };
 
 // ---------------------------------------------------------------- BDLR skeleton
@@ -27,11 +27,11 @@ struct SkelTask {
   double* work;         // k x kc scratch (row-major, ld kc)
   int64_t* rperm;       // k
   int64_t* cperm;       // kc
-  double* U;            // m x cap ROW-major, row stride ldf
-  double* V;            // n x cap ROW-major, row stride ldf
+  double* U;            // m x cap column-major, leading dimension ldu
+  double* V;            // n x cap column-major, leading dimension ldv
   int32_t* rank;        // out
   int32_t* status;      // out: 0 ok, HK_ERR_DEGENERATE
-  int32_t ldf;
+  int32_t ldu, ldv;
   const int64_t* probe; // degenerate-check probe rows (nprobe)
   int32_t nprobe;
   int32_t m, n, k, kc, cap;

@@ -267,20 +267,20 @@ __global__ void __launch_bounds__(NT) skeleton_kernel(const SkelTask* __restrict
   const double* W = t.work;   // packed LU, row-major ld kc
   // C~ = C U11^{-1}: row i solves x U11 = C[i, :] (thread per row)
   for (int i = tid; i < m; i += NT) {
-    double* x = t.U + (int64_t)i * t.ldf;     // row i of U (row-major)
+    double* x = t.U + i;                      // row i of U (column-major, ld ldu)
     for (int l = 0; l < r; ++l) {
       double s = t.A[(int64_t)i * t.lda + t.csel[t.cperm[l]]];
-      for (int p = 0; p < l; ++p) s -= x[p] * W[(int64_t)p * kc + l];
-      x[l] = s / W[(int64_t)l * kc + l];
+      for (int p = 0; p < l; ++p) s -= x[(int64_t)p * t.ldu] * W[(int64_t)p * kc + l];
+      x[(int64_t)l * t.ldu] = s / W[(int64_t)l * kc + l];
     }
   }
   // R~ = L11^{-1} R[rperm[:r]] (thread per column), V = R~^T
   for (int c = tid; c < n; c += NT) {
-    double* z = t.V + (int64_t)c * t.ldf;     // row c of V (row-major)
+    double* z = t.V + c;                      // row c of V (column-major, ld ldv)
     for (int a = 0; a < r; ++a) {
       double s = t.A[t.rsel[t.rperm[a]] * t.lda + c];
-      for (int p = 0; p < a; ++p) s -= W[(int64_t)a * kc + p] * z[p];
-      z[a] = s;
+      for (int p = 0; p < a; ++p) s -= W[(int64_t)a * kc + p] * z[(int64_t)p * t.ldv];
+      z[(int64_t)a * t.ldv] = s;
     }
   }
 }
