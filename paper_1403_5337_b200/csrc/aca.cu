@@ -23,7 +23,6 @@
 
 namespace {
 
-constexpr int ACA_NT = 256;
 
 __global__ void transpose_kernel(const double* __restrict__ A, double* __restrict__ At,
                                  int64_t n, int64_t ld, int64_t stride) {
@@ -259,7 +258,7 @@ template <int NT>
 __device__ void aca_block(const AcaTask& t, double tol2, int part_in_smem);
 
 template <int NT>
-__global__ void __launch_bounds__(NT, 2) aca_kernel(const AcaTask* __restrict__ tasks, int ntasks,
+__global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 512 / NT)) aca_kernel(const AcaTask* __restrict__ tasks, int ntasks,
                                                     int* __restrict__ counter, double tol2,
                                                     int part_in_smem) {
   __shared__ int s_task;
@@ -455,33 +454,72 @@ cudaError_t hk_launch_transpose(const double* A, double* At, int64_t n, int64_t 
   return cudaGetLastError();
 }
 
-cudaError_t hk_launch_aca(const AcaTask* tasks_dev, int ntasks, int max_cap, int max_m,
-                          double tol2, cudaStream_t st, int max_mn) {
-  (void)max_mn;
-  if (ntasks == 0) return cudaSuccess;
-  const size_t part_bytes = (size_t)(2 * (ACA_NT / 32) + 1) * max_cap * 8;
+template <int NT>
+static cudaError_t launch_class(const AcaTask* tasks_dev, int ntasks, int max_cap, int max_m,
+                                double tol2, int* counter, cudaStream_t st) {
+  const size_t part_bytes = (size_t)(2 * (NT / 32) + 1) * max_cap * 8;
   const size_t base = (size_t)(max_cap + KC) * 8 + (size_t)max_m + 16;
-  const int part_in_smem = base + part_bytes <= 100 * 1024 ? 1 : 0;
+  const int part_in_smem = base + part_bytes <= 64 * 1024 ? 1 : 0;
   const size_t smem = base + (part_in_smem ? part_bytes : 0);
-  cudaError_t e = cudaFuncSetAttribute(aca_kernel<ACA_NT>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(aca_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, aca_kernel<ACA_NT>, ACA_NT, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, aca_kernel<NT>, NT, smem);
   if (e != cudaSuccess) return e;
   int grid = sms * (per_sm > 0 ? per_sm : 1);
   if (grid > ntasks) grid = ntasks;
+  aca_kernel<NT><<<grid, NT, smem, st>>>(tasks_dev, ntasks, counter, tol2, part_in_smem);
+  hk_count_launch();
+  return cudaGetLastError();
+}
+
+// Tasks arrive grouped by CTA size class (64/128/256/512 threads: one element
+// of the longer cross vector per thread) and largest-first inside a class.
+// Each class is one persistent launch; classes run concurrently on the given
+// streams (caller forks/joins them).
+cudaError_t hk_launch_aca_classes(const AcaTask* tasks_dev, const int* class_begin,
+                                  const int* class_max_cap, const int* class_max_m, double tol2,
+                                  int* counters_dev, cudaStream_t* streams) {
+  static const int NTS[4] = {512, 256, 128, 64};
+  for (int c = 0; c < 4; ++c) {
+    const int nt = class_begin[c + 1] - class_begin[c];
+    if (nt == 0) continue;
+    const AcaTask* td = tasks_dev + class_begin[c];
+    cudaError_t e;
+    switch (NTS[c]) {
+      case 512: e = launch_class<512>(td, nt, class_max_cap[c], class_max_m[c], tol2, counters_dev + c, streams[c]); break;
+      case 256: e = launch_class<256>(td, nt, class_max_cap[c], class_max_m[c], tol2, counters_dev + c, streams[c]); break;
+      case 128: e = launch_class<128>(td, nt, class_max_cap[c], class_max_m[c], tol2, counters_dev + c, streams[c]); break;
+      default: e = launch_class<64>(td, nt, class_max_cap[c], class_max_m[c], tol2, counters_dev + c, streams[c]); break;
+    }
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t hk_launch_aca(const AcaTask* tasks_dev, int ntasks, int max_cap, int max_m,
+                          double tol2, cudaStream_t st, int max_mn) {
+  // single class (the one-block API): 64..512 threads by the longer vector
+  if (ntasks == 0) return cudaSuccess;
   int* counter = nullptr;
-  e = cudaMallocAsync(&counter, sizeof(int), st);
+  cudaError_t e = cudaMallocAsync(&counter, sizeof(int), st);
   if (e != cudaSuccess) return e;
   cudaMemsetAsync(counter, 0, sizeof(int), st);
-  aca_kernel<ACA_NT><<<grid, ACA_NT, smem, st>>>(tasks_dev, ntasks, counter, tol2, part_in_smem);
-  e = cudaGetLastError();
+  const int L = max_mn;   // caller passes max(m, n) here
+  if (L > 256) e = launch_class<512>(tasks_dev, ntasks, max_cap, max_m, tol2, counter, st);
+  else if (L > 128) e = launch_class<256>(tasks_dev, ntasks, max_cap, max_m, tol2, counter, st);
+  else if (L > 64) e = launch_class<128>(tasks_dev, ntasks, max_cap, max_m, tol2, counter, st);
+  else e = launch_class<64>(tasks_dev, ntasks, max_cap, max_m, tol2, counter, st);
   cudaFreeAsync(counter, st);
-  hk_count_launch();
   return e;
 }
 
-size_t hk_aca_scratch_doubles(int cap) { return (size_t)(2 * (ACA_NT / 32) + 1) * cap + KC; }
+int hk_aca_class(int m, int n) {
+  const int L = m > n ? m : n;
+  return L > 256 ? 0 : L > 128 ? 1 : L > 64 ? 2 : 3;
+}
+
+size_t hk_aca_scratch_doubles(int cap) { return (size_t)(2 * (512 / 32) + 1) * cap + KC; }

@@ -172,7 +172,9 @@ struct hk_plan {
   std::vector<BlockGeom> blocks;
   std::vector<int> block_order;     // largest first
   int64_t uv_per_front = 0, trace_per_front = 0;
-  DevBuf At, UV, ranks_d, trace_d, tasks_d, aca_scr;
+  DevBuf At, UV, ranks_d, trace_d, tasks_d, aca_scr, aca_cnt;
+  cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t side_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<int32_t> ranks;       // batch * nblocks
   bool have_trace = false;
   // bdlr
@@ -206,7 +208,11 @@ struct hk_plan {
       }
       delete p;
     }
-    DevBuf* bufs[] = {&aca_scr, &At, &UV, &ranks_d, &trace_d, &tasks_d, &sel_d, &work_d, &perm_d,
+    for (auto& x : side)
+      if (x) cudaStreamDestroy(x);
+    for (auto& x : side_ev)
+      if (x) cudaEventDestroy(x);
+    DevBuf* bufs[] = {&aca_cnt, &aca_scr, &At, &UV, &ranks_d, &trace_d, &tasks_d, &sel_d, &work_d, &perm_d,
                       &skel_status_d, &probe_d, &Y, &Ytmp, &F, &I, &ftask_d, &fmap_d, &gj_d, &gj2_d, &gjs_d,
                       &Xin, &X2, &G, &Yv};
     for (DevBuf* b : bufs) b->release();
@@ -371,6 +377,14 @@ static void drop_progs(hk_plan* p) {
   p->progs.clear();
 }
 
+static hk_status ensure_side_streams(hk_plan* p) {
+  for (int c = 0; c < 4; ++c) {
+    if (!p->side[c]) CU(cudaStreamCreateWithFlags(&p->side[c], cudaStreamNonBlocking));
+    if (!p->side_ev[c]) CU(cudaEventCreateWithFlags(&p->side_ev[c], cudaEventDisableTiming));
+  }
+  return HK_OK;
+}
+
 static hk_status ensure_events(hk_plan* p) {
   for (auto& e : p->ev)
     if (!e) CU(cudaEventCreate(&e));
@@ -473,6 +487,8 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
   for (size_t i = 0; i < order.size(); ++i) order[i] = i;
   std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) {
     const AcaTask &a = tasks[x], &b = tasks[y];
+    const int ca = hk_aca_class(a.m, a.n), cb = hk_aca_class(b.m, b.n);
+    if (ca != cb) return ca < cb;
     return (int64_t)(a.m + a.n) * a.cap > (int64_t)(b.m + b.n) * b.cap;
   });
   std::vector<AcaTask> sorted(tasks.size());
@@ -491,8 +507,29 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
   CU(upload(p->tasks_d, tasks, st));
   if ((size_t)(max_cap + 16) * 8 + max_m + 1024 > 220 * 1024)
     return fail(HK_ERR_VALUE, "block too large for the single-CTA ACA kernel");
+  int cls_begin[5] = {0, 0, 0, 0, 0}, cls_cap[4] = {0, 0, 0, 0}, cls_m[4] = {0, 0, 0, 0};
+  for (const auto& t : tasks) {
+    const int c = hk_aca_class(t.m, t.n);
+    cls_begin[c + 1]++;
+    cls_cap[c] = std::max(cls_cap[c], t.cap);
+    cls_m[c] = std::max(cls_m[c], t.m);
+  }
+  for (int c = 0; c < 4; ++c) cls_begin[c + 1] += cls_begin[c];
+  CHK(ensure_side_streams(p));
+  CU(p->aca_cnt.ensure(64, st));
+  CU(cudaMemsetAsync(p->aca_cnt.p, 0, 64, st));
   CU(cudaEventRecord(p->ev[3], st));
-  CU(hk_launch_aca(p->tasks_d.as<AcaTask>(), (int)tasks.size(), max_cap, max_m, tol2, st, max_mn));
+  cudaStream_t ss[4];
+  for (int c = 0; c < 4; ++c) {   // fork
+    ss[c] = p->side[c];
+    CU(cudaStreamWaitEvent(ss[c], p->ev[3], 0));
+  }
+  CU(hk_launch_aca_classes(p->tasks_d.as<AcaTask>(), cls_begin, cls_cap, cls_m, tol2,
+                           p->aca_cnt.as<int>(), ss));
+  for (int c = 0; c < 4; ++c) {   // join
+    CU(cudaEventRecord(p->side_ev[c], ss[c]));
+    CU(cudaStreamWaitEvent(st, p->side_ev[c], 0));
+  }
   CU(cudaEventRecord(p->ev[1], st));
   CHK(fetch_ranks(p, st));
   if (prof) {
@@ -1589,7 +1626,7 @@ extern "C" hk_status hk_aca_block(const double* a, int64_t m, int64_t n, int64_t
   AcaTask* td = nullptr;
   CU(cudaMallocAsync(&td, sizeof(AcaTask), st));
   CU(cudaMemcpyAsync(td, &t, sizeof(AcaTask), cudaMemcpyHostToDevice, st));
-  CU(hk_launch_aca(td, 1, (int)cap, (int)m, tol2, st, (int)(m + n)));
+  CU(hk_launch_aca(td, 1, (int)cap, (int)m, tol2, st, (int)std::max(m, n)));
   std::vector<int32_t> h(tlen);
   int32_t r32 = 0;
   CU(cudaMemcpyAsync(&r32, rk, 4, cudaMemcpyDeviceToHost, st));

@@ -102,6 +102,10 @@ cudaError_t hk_launch_transpose(const double* A, double* At, int64_t n, int64_t 
 cudaError_t hk_launch_aca(const AcaTask* tasks_dev, int ntasks, int max_cap, int max_m,
                           double tol2, cudaStream_t st, int max_mn);
 size_t hk_aca_scratch_doubles(int cap);
+int hk_aca_class(int m, int n);   // 0..3 -> 512/256/128/64-thread CTAs
+cudaError_t hk_launch_aca_classes(const AcaTask* tasks_dev, const int* class_begin,
+                                  const int* class_max_cap, const int* class_max_m, double tol2,
+                                  int* counters_dev, cudaStream_t* streams);
 cudaError_t hk_launch_skeleton(const SkelTask* tasks_dev, int ntasks, int max_k, int max_kc,
                                cudaStream_t st);
 cudaError_t hk_launch_lu(const LuTask* tasks_dev, int ntasks, int maxN, cudaStream_t st);
