@@ -222,6 +222,61 @@ __device__ __forceinline__ ArgMax block_argmax_val(ArgMax a, double val, double*
   return ArgMax{sv[0], si[0]};
 }
 
+// SMEM-resident sweep for small blocks (len <= NT): F column-major in SMEM with
+// leading dimension ldf, src with element stride sstride.  Same arithmetic and
+// dot-partial layout as fused_sweep_impl (bit-exact), no global traffic.
+template <int NT>
+__device__ __forceinline__ void smem_sweep(const double* __restrict__ F, int ldf, int len, int nk,
+                                           int ndot, const double* __restrict__ coef,
+                                           const double* __restrict__ src, int sstride,
+                                           int out_col, int pend_col, double* __restrict__ part,
+                                           int pld, const unsigned char* __restrict__ used,
+                                           ArgMax& best, double& sumsq, double& bestval,
+                                           double& xout) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  best.v = 0.0;
+  best.i = -1;
+  bestval = 0.0;
+  sumsq = 0.0;
+  double* mypart = part + warp * pld;
+  for (int k = lane; k < ndot; k += 32) mypart[k] = 0.0;
+  __syncwarp();
+  const int e = tid;
+  const bool ok = e < len;
+  const double* col = F + (ok ? e : 0);
+  double x = (ok && src) ? src[e * sstride] : 0.0;
+  const double pv = (ok && ndot > 0) ? col[pend_col * ldf] : 0.0;
+  const int kmax = nk > ndot ? nk : ndot;
+  for (int kb = 0; kb < kmax; kb += KC) {
+    double cur[KC];
+#pragma unroll
+    for (int j = 0; j < KC; ++j) cur[j] = (kb + j < kmax) ? col[(kb + j) * ldf] : 0.0;
+    if (kb < ndot) {
+      double acc[KC];
+#pragma unroll
+      for (int j = 0; j < KC; ++j) acc[j] = (kb + j < ndot) ? pv * cur[j] : 0.0;
+      const double v = transpose_reduce8(acc, lane);
+      if (lane < KC && kb + lane < ndot) mypart[kb + lane] += v;
+    }
+#pragma unroll
+    for (int j = 0; j < KC; ++j)
+      if (kb + j < nk) x = sub_rn(x, mul_rn(coef[kb + j], cur[j]));
+  }
+  xout = x;
+  if (out_col >= 0 && ok) {
+    const_cast<double*>(col)[out_col * ldf] = x;
+    const double ax = fabs(x);
+    if (used) {
+      sumsq += x * x;
+      if (!used[e] && argmax_better(ax, e, best.v, best.i)) { best.v = ax; best.i = e; bestval = x; }
+    } else if (argmax_better(ax, e, best.v, best.i)) {
+      best.v = ax;
+      best.i = e;
+      bestval = x;
+    }
+  }
+}
+
 // est = fro2 + cross + sum_k 2 (u.u_k)(v.v_k) over the per-warp partials,
 // reduced in a fixed order; valid in every thread.
 template <int NT>
@@ -269,6 +324,24 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 512 / NT)) aca_kernel(con
     __syncthreads();
     if (ti >= ntasks) break;
     aca_block<NT>(tasks[ti], tol2, part_in_smem);
+    __syncthreads();
+  }
+}
+
+template <int NT>
+__device__ void aca_block_smem(const AcaTask& t, double tol2);
+
+template <int NT>
+__global__ void __launch_bounds__(NT) aca_smem_kernel(const AcaTask* __restrict__ tasks, int ntasks,
+                                                      int* __restrict__ counter, double tol2) {
+  __shared__ int s_task;
+  for (;;) {
+    if (threadIdx.x == 0) s_task = atomicAdd(counter, 1);
+    __syncthreads();
+    const int ti = s_task;
+    __syncthreads();
+    if (ti >= ntasks) break;
+    aca_block_smem<NT>(tasks[ti], tol2);
     __syncthreads();
   }
 }
@@ -443,6 +516,188 @@ __device__ void aca_block(const AcaTask& t, double tol2, int part_in_smem) {
   }
 }
 
+template <int NT>
+__device__ void aca_block_smem(const AcaTask& t, double tol2) {
+  const int m = t.m, n = t.n, cap = t.cap;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
+  uint64_t t_start = 0;
+  if (t.clock && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  extern __shared__ __align__(16) unsigned char smraw[];
+  // SMEM: Us[m x cap] (ld m), Vs[n x cap] (ld n), As[m x n] (ld n+1), coef[cap+KC],
+  // partU/partV [NW*cap], prod[cap], used[m]
+  const int ldus = m, ldvs = n, ldas = n + 1;
+  double* Us = reinterpret_cast<double*>(smraw);
+  double* Vs = Us + (size_t)m * cap;
+  double* As = Vs + (size_t)n * cap;
+  double* coef = As + (size_t)m * ldas;
+  const int pld = cap;
+  double* partU = coef + cap + KC;
+  double* partV = partU + NW * pld;
+  double* prod = partV + NW * pld;
+  unsigned char* used = reinterpret_cast<unsigned char*>(prod + cap);
+  __shared__ double red_v[NW], red_a[NW], red_b[NW], red_x[NW];
+  __shared__ int64_t red_i[NW];
+  __shared__ int s_row;
+  __shared__ double s_est;
+
+  int32_t* trows = t.trace ? t.trace + 2 : nullptr;
+  int32_t* tcols = t.trace ? t.trace + 2 + (m + cap + 1) : nullptr;
+  int nrow_ev = 0, ncol_ev = 0;
+
+  if (m == 0 || n == 0 || cap == 0) {
+    if (tid == 0) {
+      *t.rank = 0;
+      if (t.trace) { t.trace[0] = 0; t.trace[1] = 0; }
+    }
+    return;
+  }
+  for (int i = tid; i < m; i += NT) used[i] = 0;
+  for (int k = tid; k < cap + KC; k += NT) coef[k] = 0.0;
+  for (int i = 0; i < m; ++i)
+    for (int j = tid; j < n; j += NT) As[i * ldas + j] = t.A[(int64_t)i * t.lda + j];
+  __syncthreads();
+
+  const double* __restrict__ Ab = t.A;
+  const double* __restrict__ Atb = t.At;
+  double* __restrict__ U = Us;
+  double* __restrict__ V = Vs;
+  const int LDU = ldus, LDV = ldvs;
+  double xreg = 0.0;
+  int r = 0, row = 0, nused = 0;
+  bool pending = false;                       // column r holds an undecided cross
+  double uu_p = 0.0, vv_p = 0.0, fro2 = 0.0;
+  ArgMax best, nxt;
+  double dummy, uu, bval;
+
+  for (;;) {
+    const int c = r + (pending ? 1 : 0);     // index of the new candidate
+    const bool can_step = pending ? (c < cap && nused < m) : (c < cap);
+    if (!can_step) {
+      if (pending) {                          // decide the last cross: dots only
+        smem_sweep<NT>(U, ldus, m, 0, r, coef, nullptr, 1, -1, r, partU, pld, nullptr, best, dummy, bval, xreg);
+        smem_sweep<NT>(V, ldvs, n, 0, r, coef, nullptr, 1, -1, r, partV, pld, nullptr, best, dummy, bval, xreg);
+        __syncthreads();
+        const double cross = uu_p * vv_p;
+        const double est = stopping_estimate<NT>(partU, partV, pld, r, fro2, cross, prod, &s_est);
+        if (!(cross <= tol2 * est)) ++r;
+      }
+      break;
+    }
+    // ---- next step (speculative when a cross is pending), lowrank.py:251-283
+    if (tid == 0) {
+      used[row] = 1;
+      if (trows) trows[nrow_ev] = row;
+    }
+    ++nrow_ev;
+    ++nused;
+    for (int k = tid; k < c; k += NT) coef[k] = U[row + k * LDU];
+    __syncthreads();
+    // residual row (:253-256) + the pending cross's v dots
+    smem_sweep<NT>(V, ldvs, n, c, pending ? r : 0, coef, As + row * ldas, 1, c, r, partV, pld,
+                   nullptr, best, dummy, bval, xreg);
+    double delta;
+    best = block_argmax_val<NT>(best, bval, red_v, red_i, red_x, delta);
+    const int col = (int)best.i;
+    if (delta == 0.0) {                       // zero residual row (:258-264)
+      if (pending) {
+        smem_sweep<NT>(U, ldus, m, 0, r, coef, nullptr, 1, -1, r, partU, pld, nullptr, nxt, dummy, bval, xreg);
+        __syncthreads();
+        const double cross = uu_p * vv_p;
+        const double est = stopping_estimate<NT>(partU, partV, pld, r, fro2, cross, prod, &s_est);
+        if (cross <= tol2 * est) {            // reject: the reference never read this row
+          --nrow_ev;
+          break;
+        }
+        ++r;
+        fro2 = est;
+        pending = false;
+      }
+      if (nused == m) break;
+      if (tid == 0) {
+        int q = 0;
+        while (used[q]) ++q;
+        s_row = q;
+      }
+      __syncthreads();
+      row = s_row;
+      __syncthreads();
+      continue;
+    }
+    // v = res / delta (:265) over own elements (same ownership as the sweep)
+    double vv = 0.0;
+    if (tid < n) {
+      const double v = div_rn(xreg, delta);
+      V[tid + c * LDV] = v;
+      vv += v * v;
+    }
+    for (int k = tid; k < c; k += NT) coef[k] = V[col + k * LDV];
+    if (tid == 0 && tcols) tcols[ncol_ev] = col;
+    ++ncol_ev;
+    __syncthreads();
+    // residual column (:266-268) + next-row candidate (:283) + pending u dots
+    smem_sweep<NT>(U, ldus, m, c, pending ? r : 0, coef, As + col, ldas, c, r, partU, pld, used,
+                   nxt, uu, bval, xreg);
+    {
+      nxt = warp_argmax(nxt);
+      uu = warp_sum(uu);
+      vv = warp_sum(vv);
+      if (lane == 0) { red_v[warp] = nxt.v; red_i[warp] = nxt.i; red_a[warp] = uu; red_b[warp] = vv; }
+      __syncthreads();
+      if (warp == 0) {
+        ArgMax b2;
+        double a2 = 0.0, c2 = 0.0;
+        if (lane < NW) { b2.v = red_v[lane]; b2.i = red_i[lane]; a2 = red_a[lane]; c2 = red_b[lane]; }
+        else { b2.v = 0.0; b2.i = -1; }
+        b2 = warp_argmax(b2);
+        a2 = warp_sum(a2);
+        c2 = warp_sum(c2);
+        if (lane == 0) { red_v[0] = b2.v; red_i[0] = b2.i; red_a[0] = a2; red_b[0] = c2; }
+      }
+      __syncthreads();
+      nxt.i = red_i[0];
+      uu = red_a[0];
+      vv = red_b[0];
+    }
+    if (pending) {                            // stopping test of the pending cross (:269-275)
+      const double cross = uu_p * vv_p;
+      const double est = stopping_estimate<NT>(partU, partV, pld, r, fro2, cross, prod, &s_est);
+      if (cross <= tol2 * est) {              // reject: drop the speculative step's reads
+        --nrow_ev;
+        --ncol_ev;
+        break;
+      }
+      ++r;
+      fro2 = est;
+    }
+    pending = true;                           // the new cross awaits its test
+    uu_p = uu;
+    vv_p = vv;
+    row = (int)nxt.i;
+    __syncthreads();
+  }
+  {
+    const int64_t LDG_ = int64_t(1) << t.ldu;
+    for (int k = 0; k < r; ++k) {
+      for (int i = tid; i < m; i += NT) t.U[i + k * LDG_] = Us[i + k * ldus];
+      for (int j = tid; j < n; j += NT) t.V[j + k * LDG_] = Vs[j + k * ldvs];
+    }
+  }
+  if (tid == 0) {
+    *t.rank = r;
+    if (t.trace) { t.trace[0] = nrow_ev; t.trace[1] = ncol_ev; }
+    if (t.clock) {
+      uint64_t t_end;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      t.clock[0] = (int64_t)t_start;
+      t.clock[1] = (int64_t)t_end;
+      t.clock[2] = smid;
+    }
+  }
+}
+
 }  // namespace
 
 cudaError_t hk_launch_transpose(const double* A, double* At, int64_t n, int64_t ld, int64_t batch,
@@ -476,6 +731,28 @@ static cudaError_t launch_class(const AcaTask* tasks_dev, int ntasks, int max_ca
   return cudaGetLastError();
 }
 
+template <int NT>
+static cudaError_t launch_smem_class(const AcaTask* tasks_dev, int ntasks, int max_cap, int max_m,
+                                     double tol2, int* counter, cudaStream_t st) {
+  // Us + Vs + As + coef + partials + prod + used, for m, n <= NT
+  const size_t smem = (size_t)(2 * NT * max_cap + NT * (NT + 1) + max_cap + KC +
+                               (2 * (NT / 32) + 1) * max_cap) * 8 + (size_t)max_m + 16;
+  (void)max_m;
+  cudaError_t e = cudaFuncSetAttribute(aca_smem_kernel<NT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, aca_smem_kernel<NT>, NT, smem);
+  if (e != cudaSuccess) return e;
+  int grid = sms * (per_sm > 0 ? per_sm : 1);
+  if (grid > ntasks) grid = ntasks;
+  aca_smem_kernel<NT><<<grid, NT, smem, st>>>(tasks_dev, ntasks, counter, tol2);
+  hk_count_launch();
+  return cudaGetLastError();
+}
+
 // Tasks arrive grouped by CTA size class (64/128/256/512 threads: one element
 // of the longer cross vector per thread) and largest-first inside a class.
 // Each class is one persistent launch; classes run concurrently on the given
@@ -493,7 +770,7 @@ cudaError_t hk_launch_aca_classes(const AcaTask* tasks_dev, const int* class_beg
       case 512: e = launch_class<512>(td, nt, class_max_cap[c], class_max_m[c], tol2, counters_dev + c, streams[c]); break;
       case 256: e = launch_class<256>(td, nt, class_max_cap[c], class_max_m[c], tol2, counters_dev + c, streams[c]); break;
       case 128: e = launch_class<128>(td, nt, class_max_cap[c], class_max_m[c], tol2, counters_dev + c, streams[c]); break;
-      default: e = launch_class<64>(td, nt, class_max_cap[c], class_max_m[c], tol2, counters_dev + c, streams[c]); break;
+      default: e = launch_smem_class<64>(td, nt, class_max_cap[c], class_max_m[c], tol2, counters_dev + c, streams[c]); break;
     }
     if (e != cudaSuccess) return e;
   }
@@ -512,7 +789,7 @@ cudaError_t hk_launch_aca(const AcaTask* tasks_dev, int ntasks, int max_cap, int
   if (L > 256) e = launch_class<512>(tasks_dev, ntasks, max_cap, max_m, tol2, counter, st);
   else if (L > 128) e = launch_class<256>(tasks_dev, ntasks, max_cap, max_m, tol2, counter, st);
   else if (L > 64) e = launch_class<128>(tasks_dev, ntasks, max_cap, max_m, tol2, counter, st);
-  else e = launch_class<64>(tasks_dev, ntasks, max_cap, max_m, tol2, counter, st);
+  else e = launch_smem_class<64>(tasks_dev, ntasks, max_cap, max_m, tol2, counter, st);
   cudaFreeAsync(counter, st);
   return e;
 }

@@ -19,6 +19,159 @@ __host__ __device__ inline size_t gj_bytes(int N) {
   return (size_t)N * N * 8 + (size_t)2 * N * 8 + (size_t)2 * N * 4;
 }
 
+// Register-resident Gauss-Jordan, N <= min(NW*CPW, 32*RPL).  The matrix is
+// distributed column-cyclically: warp w holds columns j = w + NW*jj (jj < CPW),
+// lane l holds rows i = l + 32*q (q < RPL), so W[i][j] lives in w_[jj][q] of
+// warp j%NW / lane i%32.  Pivoting is implicit (no physical row swaps): step k
+// takes the largest |W[i][k]| over rows not yet used as pivots (ties: lowest
+// row), so the pivot magnitudes are those of LU with partial pivoting and the
+// singularity test min|pivot| < 1e-300 is the reference's (dense.py:76-77).
+// With pivot rows p_k the result satisfies A^{-1}[i][c] = W[p_i][q(c)],
+// q = p^{-1}, applied by the final gather.  Per step: the owner warp of
+// column k finds the pivot (shuffles), the lane holding row p publishes the
+// scaled pivot row; every warp updates its columns in registers (one DFMA +
+// one select per element).  Two barriers per step, double-buffered SMEM.
+template <int NW, int CPW, int RPL>
+__global__ void __launch_bounds__(NW * 32, 1) gj_reg_kernel(const GjTask* __restrict__ tasks) {
+  constexpr int NT = NW * 32;
+  const GjTask t = tasks[blockIdx.x];
+  const int N = t.N;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  extern __shared__ __align__(16) double gsm[];   // stage N*N, colk[2][N], rowk[2][N]
+  double* stage = gsm;
+  double* colk = stage + N * N;
+  double* rowk = colk + 2 * N;
+  __shared__ int s_p[2], s_sing, pivrow[32 * RPL], invp[32 * RPL];
+  __shared__ double s_rinv[2];
+  __shared__ unsigned char usedrow[32 * RPL];
+  if (N == 0) {
+    if (tid == 0) *t.status = 0;
+    return;
+  }
+  // load through SMEM (coalesced), then into registers
+  if (t.mode == 0) {
+    for (int i = warp; i < N; i += NW)
+      for (int j = lane; j < N; j += 32) stage[i + j * N] = t.src[(int64_t)i * t.src_ld + j];
+  } else {
+    for (int j = warp; j < N; j += NW)
+      for (int i = lane; i < N; i += 32) stage[i + j * N] = t.src[i + (int64_t)j * t.src_ld];
+  }
+  for (int i = tid; i < 32 * RPL; i += NT) usedrow[i] = 0;
+  if (tid == 0) s_sing = 0;
+  __syncthreads();
+  double w_[CPW][RPL];
+#pragma unroll
+  for (int jj = 0; jj < CPW; ++jj)
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+      const int i = lane + 32 * q, j = warp + NW * jj;
+      w_[jj][q] = (i < N && j < N) ? stage[i + j * N] : 0.0;
+    }
+  for (int k = 0; k < N; ++k) {
+    const int buf = k & 1;
+    double* ck_s = colk + buf * N;
+    double* rk_s = rowk + buf * N;
+    // ---- owner warp of column k: pivot search over unused rows, publish column k
+    if (warp == k % NW) {
+      const int jk = k / NW;
+      double val[RPL];
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) {
+        double v = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < CPW; ++jj)
+          if (jj == jk) v = w_[jj][q];
+        val[q] = v;
+      }
+      ArgMax a{0.0, -1};
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) {
+        const int i = lane + 32 * q;
+        if (i < N) {
+          ck_s[i] = val[q];
+          if (!usedrow[i]) {
+            const double av = fabs(val[q]);
+            if (argmax_better(av, i, a.v, a.i)) { a.v = av; a.i = i; }
+          }
+        }
+      }
+      a = warp_argmax(a);
+      if (lane == 0) {
+        const int p = (int)a.i;
+        s_p[buf] = p;
+        if (!(a.v >= HK_PIVOT_FLOOR)) s_sing = 1;
+        else {
+          usedrow[p] = 1;
+          pivrow[k] = p;
+        }
+      }
+    }
+    __syncthreads();
+    if (s_sing) break;
+    const int p = s_p[buf];
+    const double piv = ck_s[p];
+    const double rinv = 1.0 / piv;
+    // ---- the lane holding row p publishes the scaled pivot row of its warp's columns
+    if (lane == (p & 31)) {
+      const int qp = p >> 5;
+#pragma unroll
+      for (int jj = 0; jj < CPW; ++jj) {
+        const int j = warp + NW * jj;
+        if (j < N) {
+          double v = 0.0;
+#pragma unroll
+          for (int q = 0; q < RPL; ++q)
+            if (q == qp) v = w_[jj][q];
+          rk_s[j] = (j == k) ? rinv : v * rinv;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- elimination in registers
+    double ck[RPL];
+    bool isp[RPL];
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+      const int i = lane + 32 * q;
+      ck[q] = (i < N) ? ck_s[i] : 0.0;
+      isp[q] = (i == p);
+    }
+#pragma unroll
+    for (int jj = 0; jj < CPW; ++jj) {
+      const int j = warp + NW * jj;
+      if (j >= N) break;
+      const double rj = rk_s[j];
+      if (j == k) {
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) w_[jj][q] = isp[q] ? rinv : -ck[q] * rinv;
+      } else {
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+          const double v = fma(-ck[q], rj, w_[jj][q]);
+          w_[jj][q] = isp[q] ? rj : v;
+        }
+      }
+    }
+  }
+  if (tid == 0) *t.status = s_sing;
+  if (s_sing) return;
+  // ---- A^{-1}[i][c] = W[p_i][q(c)]
+#pragma unroll
+  for (int jj = 0; jj < CPW; ++jj)
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+      const int i = lane + 32 * q, j = warp + NW * jj;
+      if (i < N && j < N) stage[i + j * N] = w_[jj][q];
+    }
+  for (int k = tid; k < N; k += NT) invp[pivrow[k]] = k;
+  __syncthreads();
+  for (int c = warp; c < N; c += NW) {
+    const int qc = invp[c];
+    double* dst = t.out + (int64_t)c * t.out_ld;
+    for (int i = lane; i < N; i += 32) dst[i] = stage[pivrow[i] + qc * N];
+  }
+}
+
 // SMEM-resident variant, N <= 32*MAXQ: every lane owns rows lane + 32q of the
 // column its warp updates; the pivot column is cached in registers; all SMEM
 // addressing is 32-bit.  Two barriers per elimination step.
@@ -261,11 +414,22 @@ static cudaError_t launch_gj_smem(const GjTask* tasks_dev, int ntasks, int maxN,
   return cudaGetLastError();
 }
 
+template <int NW, int CPW, int RPL>
+static cudaError_t launch_gj_reg(const GjTask* tasks_dev, int ntasks, int maxN, cudaStream_t st) {
+  const size_t smem = ((size_t)maxN * maxN + 4 * (size_t)maxN) * 8;
+  cudaError_t e = cudaFuncSetAttribute(gj_reg_kernel<NW, CPW, RPL>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  gj_reg_kernel<NW, CPW, RPL><<<ntasks, NW * 32, smem, st>>>(tasks_dev);
+  hk_count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t hk_launch_gj(const GjTask* tasks_dev, int ntasks, int maxN, cudaStream_t st) {
   if (ntasks == 0) return cudaSuccess;
-  if (maxN <= 64) return launch_gj_smem<128, 2>(tasks_dev, ntasks, maxN, st);
-  if (maxN <= 128) return launch_gj_smem<256, 4>(tasks_dev, ntasks, maxN, st);
-  if (maxN <= 160) return launch_gj_smem<256, 5>(tasks_dev, ntasks, maxN, st);
+  if (maxN <= 64) return launch_gj_reg<4, 16, 2>(tasks_dev, ntasks, maxN, st);
+  if (maxN <= 128) return launch_gj_reg<8, 16, 4>(tasks_dev, ntasks, maxN, st);
+  if (maxN <= 160) return launch_gj_reg<8, 20, 5>(tasks_dev, ntasks, maxN, st);
   size_t need = gj_bytes(maxN);
   size_t smem = need <= GJ_SMEM_CAP ? need : 0;
   cudaError_t e;
