@@ -67,88 +67,85 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_reg_kernel(const GjTask* __rest
       const int i = lane + 32 * q, j = warp + NW * jj;
       w_[jj][q] = (i < N && j < N) ? stage[i + j * N] : 0.0;
     }
-  for (int k = 0; k < N; ++k) {
-    const int buf = k & 1;
-    double* ck_s = colk + buf * N;
-    double* rk_s = rowk + buf * N;
-    // ---- owner warp of column k: pivot search over unused rows, publish column k
-    if (warp == k % NW) {
-      const int jk = k / NW;
-      double val[RPL];
+  // k = w + NW*kk: the column slot kk of the owner warp is a compile-time
+  // constant inside the unrolled kk loop (no register-array select chains)
 #pragma unroll
-      for (int q = 0; q < RPL; ++q) {
-        double v = 0.0;
+  for (int kk = 0; kk < CPW; ++kk) {
+    for (int w = 0; w < NW; ++w) {
+      const int k = w + NW * kk;
+      if (k >= N) break;
+      const int buf = k & 1;
+      double* ck_s = colk + buf * N;
+      double* rk_s = rowk + buf * N;
+      if (warp == w) {                // owner of column k: pivot over unused rows
+        ArgMax a{0.0, -1};
 #pragma unroll
-        for (int jj = 0; jj < CPW; ++jj)
-          if (jj == jk) v = w_[jj][q];
-        val[q] = v;
-      }
-      ArgMax a{0.0, -1};
-#pragma unroll
-      for (int q = 0; q < RPL; ++q) {
-        const int i = lane + 32 * q;
-        if (i < N) {
-          ck_s[i] = val[q];
-          if (!usedrow[i]) {
-            const double av = fabs(val[q]);
-            if (argmax_better(av, i, a.v, a.i)) { a.v = av; a.i = i; }
+        for (int q = 0; q < RPL; ++q) {
+          const int i = lane + 32 * q;
+          if (i < N) {
+            ck_s[i] = w_[kk][q];
+            if (!usedrow[i]) {
+              const double av = fabs(w_[kk][q]);
+              if (argmax_better(av, i, a.v, a.i)) { a.v = av; a.i = i; }
+            }
+          }
+        }
+        a = warp_argmax(a);
+        if (lane == 0) {
+          const int p = (int)a.i;
+          s_p[buf] = p;
+          if (!(a.v >= HK_PIVOT_FLOOR)) s_sing = 1;
+          else {
+            usedrow[p] = 1;
+            pivrow[k] = p;
           }
         }
       }
-      a = warp_argmax(a);
-      if (lane == 0) {
-        const int p = (int)a.i;
-        s_p[buf] = p;
-        if (!(a.v >= HK_PIVOT_FLOOR)) s_sing = 1;
-        else {
-          usedrow[p] = 1;
-          pivrow[k] = p;
+      __syncthreads();
+      if (s_sing) break;
+      const int p = s_p[buf];
+      const double rinv = 1.0 / ck_s[p];
+      // pivot row of this warp's columns, published by the lane that holds row p
+      const int qp = p >> 5;
+      if (lane == (p & 31)) {
+        switch (qp) {   // warp-uniform
+#define HK_PUB(Q)                                                         \
+  case Q:                                                                 \
+    if (Q < RPL) {                                                        \
+      _Pragma("unroll") for (int jj = 0; jj < CPW; ++jj) {               \
+        const int j = warp + NW * jj;                                     \
+        if (j < N) rk_s[j] = (j == k) ? rinv : w_[jj][Q < RPL ? Q : 0] * rinv; \
+      }                                                                   \
+    }                                                                     \
+    break;
+          HK_PUB(0) HK_PUB(1) HK_PUB(2) HK_PUB(3) HK_PUB(4) HK_PUB(5) HK_PUB(6) HK_PUB(7)
+#undef HK_PUB
+          default: break;
         }
       }
-    }
-    __syncthreads();
-    if (s_sing) break;
-    const int p = s_p[buf];
-    const double piv = ck_s[p];
-    const double rinv = 1.0 / piv;
-    // ---- the lane holding row p publishes the scaled pivot row of its warp's columns
-    if (lane == (p & 31)) {
-      const int qp = p >> 5;
+      __syncthreads();
+      double ck[RPL];
+      bool isp[RPL];
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) {
+        const int i = lane + 32 * q;
+        ck[q] = (i < N) ? ck_s[i] : 0.0;
+        isp[q] = (i == p);
+      }
 #pragma unroll
       for (int jj = 0; jj < CPW; ++jj) {
         const int j = warp + NW * jj;
-        if (j < N) {
-          double v = 0.0;
+        if (j >= N) break;
+        const double rj = rk_s[j];
+        if (jj == kk && warp == w) {
 #pragma unroll
-          for (int q = 0; q < RPL; ++q)
-            if (q == qp) v = w_[jj][q];
-          rk_s[j] = (j == k) ? rinv : v * rinv;
-        }
-      }
-    }
-    __syncthreads();
-    // ---- elimination in registers
-    double ck[RPL];
-    bool isp[RPL];
+          for (int q = 0; q < RPL; ++q) w_[jj][q] = isp[q] ? rinv : -ck[q] * rinv;
+        } else {
 #pragma unroll
-    for (int q = 0; q < RPL; ++q) {
-      const int i = lane + 32 * q;
-      ck[q] = (i < N) ? ck_s[i] : 0.0;
-      isp[q] = (i == p);
-    }
-#pragma unroll
-    for (int jj = 0; jj < CPW; ++jj) {
-      const int j = warp + NW * jj;
-      if (j >= N) break;
-      const double rj = rk_s[j];
-      if (j == k) {
-#pragma unroll
-        for (int q = 0; q < RPL; ++q) w_[jj][q] = isp[q] ? rinv : -ck[q] * rinv;
-      } else {
-#pragma unroll
-        for (int q = 0; q < RPL; ++q) {
-          const double v = fma(-ck[q], rj, w_[jj][q]);
-          w_[jj][q] = isp[q] ? rj : v;
+          for (int q = 0; q < RPL; ++q) {
+            const double v = fma(-ck[q], rj, w_[jj][q]);
+            w_[jj][q] = isp[q] ? rj : v;
+          }
         }
       }
     }
@@ -427,9 +424,9 @@ static cudaError_t launch_gj_reg(const GjTask* tasks_dev, int ntasks, int maxN, 
 
 cudaError_t hk_launch_gj(const GjTask* tasks_dev, int ntasks, int maxN, cudaStream_t st) {
   if (ntasks == 0) return cudaSuccess;
-  if (maxN <= 64) return launch_gj_reg<4, 16, 2>(tasks_dev, ntasks, maxN, st);
-  if (maxN <= 128) return launch_gj_reg<8, 16, 4>(tasks_dev, ntasks, maxN, st);
-  if (maxN <= 160) return launch_gj_reg<8, 20, 5>(tasks_dev, ntasks, maxN, st);
+  if (maxN <= 64) return launch_gj_reg<8, 8, 2>(tasks_dev, ntasks, maxN, st);
+  if (maxN <= 128) return launch_gj_reg<16, 8, 4>(tasks_dev, ntasks, maxN, st);
+  if (maxN <= 160) return launch_gj_reg<16, 10, 5>(tasks_dev, ntasks, maxN, st);
   size_t need = gj_bytes(maxN);
   size_t smem = need <= GJ_SMEM_CAP ? need : 0;
   cudaError_t e;
