@@ -80,7 +80,7 @@ __device__ __forceinline__ double transpose_reduce8(double (&a)[8], int lane) {
 // cross-lane cost is amortised over EPT elements.  Fixed reduction order
 // (deterministic).  out_col < 0: dots only.  used != nullptr: column sweep
 // (argmax over untouched entries + sum of squares); else row sweep.
-template <int NT, int EPT, int LDLOG>
+template <int NT, int EPT, int LDLOG, bool SMEM>
 __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len, int nk, int ndot,
                                            const double* __restrict__ coef,
                                            const double* __restrict__ src, int sstride,
@@ -119,7 +119,7 @@ __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len
       for (int q = 0; q < EPT; ++q)
 #pragma unroll
         for (int j = 0; j < KC; ++j)
-          a[q][j] = (ok[q] && (full || kb + j < kmax)) ? __ldca(pk[q] + j * LD) : 0.0;
+          a[q][j] = (ok[q] && (full || kb + j < kmax)) ? (SMEM ? pk[q][j * LD] : __ldca(pk[q] + j * LD)) : 0.0;
 #pragma unroll
       for (int q = 0; q < EPT; ++q) pk[q] += KC * LD;
       if (kb < ndot) {                       // warp-uniform
@@ -175,7 +175,7 @@ __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len
 
 // One call target per (NT, EPT) for the caller (keeps its register allocation
 // small); the leading dimension is dispatched once, inside.
-template <int NT, int EPT>
+template <int NT, int EPT, bool SMEM>
 __device__ __noinline__ void sweep(int ldlog, const double* __restrict__ F, int len, int nk, int ndot,
                                    const double* __restrict__ coef, const double* __restrict__ src,
                                    int sstride, int out_col, int pend_col, double* __restrict__ part,
@@ -183,7 +183,7 @@ __device__ __noinline__ void sweep(int ldlog, const double* __restrict__ F, int 
                                    double& sumsq, double& bestval, double* xout) {
 #define HK_SWEEP_CASE(L)                                                                       \
   case L:                                                                                      \
-    sweep_impl<NT, EPT, L>(F, len, nk, ndot, coef, src, sstride, out_col, pend_col, part, pld, \
+    sweep_impl<NT, EPT, L, SMEM>(F, len, nk, ndot, coef, src, sstride, out_col, pend_col, part, pld, \
                            used, best, sumsq, bestval, xout);                                  \
     return;
   switch (ldlog) {
@@ -338,8 +338,8 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
     const bool can_step = pending ? (c < cap && nused < m) : (c < cap);
     if (!can_step) {
       if (pending) {                          // decide the last cross: dots only
-        sweep<NT, EPT>(ldlog, U, m, 0, r, coef, nullptr, 1, -1, r, partU, pld, nullptr, best, dummy, bval, xv);
-        sweep<NT, EPT>(ldlog, V, n, 0, r, coef, nullptr, 1, -1, r, partV, pld, nullptr, best, dummy, bval, xv);
+        sweep<NT, EPT, SMEM>(ldlog, U, m, 0, r, coef, nullptr, 1, -1, r, partU, pld, nullptr, best, dummy, bval, xv);
+        sweep<NT, EPT, SMEM>(ldlog, V, n, 0, r, coef, nullptr, 1, -1, r, partV, pld, nullptr, best, dummy, bval, xv);
         bar<NT>();
         const double cross = uu_p * vv_p;
         const double est = stopping_estimate<NT>(partU, partV, pld, r, fro2, cross, prod, &s_est);
@@ -356,14 +356,14 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
     for (int k = tid; k < c; k += NT) coef[k] = U[row + (int64_t)k * LD];
     bar<NT>();
     // residual row (:253-256) + the pending cross's v dots
-    sweep<NT, EPT>(ldlog, V, n, c, pending ? r : 0, coef, rowsrc_base + (int64_t)row * rowsrc_ld, 1,
+    sweep<NT, EPT, SMEM>(ldlog, V, n, c, pending ? r : 0, coef, rowsrc_base + (int64_t)row * rowsrc_ld, 1,
                    c, r, partV, pld, nullptr, best, dummy, bval, xv);
     double delta;
     best = block_argmax_val<NT>(best, bval, red_v, red_i, red_x, delta);
     const int col = (int)best.i;
     if (delta == 0.0) {                       // zero residual row (:258-264)
       if (pending) {
-        sweep<NT, EPT>(ldlog, U, m, 0, r, coef, nullptr, 1, -1, r, partU, pld, nullptr, nxt, dummy, bval, xv);
+        sweep<NT, EPT, SMEM>(ldlog, U, m, 0, r, coef, nullptr, 1, -1, r, partU, pld, nullptr, nxt, dummy, bval, xv);
         bar<NT>();
         const double cross = uu_p * vv_p;
         const double est = stopping_estimate<NT>(partU, partV, pld, r, fro2, cross, prod, &s_est);
@@ -412,7 +412,7 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
     bar<NT>();
     // residual column (:266-268) + next-row candidate (:283) + pending u dots
     const double* csrc = SMEM ? As + col : t.At + (int64_t)col * t.lda;
-    sweep<NT, EPT>(ldlog, U, m, c, pending ? r : 0, coef, csrc, SMEM ? ldas : 1, c, r, partU, pld,
+    sweep<NT, EPT, SMEM>(ldlog, U, m, c, pending ? r : 0, coef, csrc, SMEM ? ldas : 1, c, r, partU, pld,
                    used, nxt, uu, bval, xv);
     {
       nxt = warp_argmax(nxt);
@@ -550,7 +550,7 @@ static cudaError_t launch_class_id(int cls, const AcaTask* td, int nt, int max_c
     case 0: return launch_cls<128, 4, false>(td, nt, max_cap, max_m, 0, tol2, counter, st);
     case 1: return launch_cls<64, 4, false>(td, nt, max_cap, max_m, 0, tol2, counter, st);
     case 2: return launch_cls<32, 4, false>(td, nt, max_cap, max_m, 0, tol2, counter, st);
-    default: return launch_cls<32, 2, true>(td, nt, max_cap, max_m, 6, tol2, counter, st);
+    default: return launch_cls<32, 2, false>(td, nt, max_cap, max_m, 0, tol2, counter, st);
   }
 }
 
