@@ -11,7 +11,7 @@
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, NT = 128, STAGES = 4;
+constexpr int BM = 64, BN = 64, BK = 16, NT = 256, STAGES = 4;
 constexpr int SA = BM + 4;   // k-major A rows (transA = 0): conflict-free DMMA fragment loads
 constexpr int ST = BK + 4;   // m/n-major rows (transA = 1 and B)
 
@@ -24,8 +24,11 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // One 64x64 tile of C = alpha op(A) B + beta C (+ diag on C's diagonal).
-// Four-stage cp.async pipeline (global -> SMEM without register staging) so the
-// L2 latency of the next k-tiles overlaps the DMMA work of the current one.
+// 8 warps (2 along m x 4 along n), each owning a 32x16 sub-tile of 4x2 DMMA
+// 8x8 accumulators.  Four-stage cp.async pipeline (global -> SMEM without
+// register staging) so the L2 latency of the next k-tiles overlaps the DMMA
+// work of the current one; for beta != 0 the C values are fetched into
+// registers before the k loop so the epilogue does not wait on memory.
 template <int TRANSA>
 __device__ __forceinline__ void gemm_tile(const GemmTask& t, int tm, int tn, double* smem) {
   constexpr int A_STAGE = TRANSA ? BM * ST : BK * SA;
@@ -34,18 +37,33 @@ __device__ __forceinline__ void gemm_tile(const GemmTask& t, int tm, int tn, dou
   double* Bs = smem + STAGES * A_STAGE;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gid = lane >> 2, tig = lane & 3;
-  const int wm = warp & 1, wn = warp >> 1;
+  const int wm = warp & 1, wn = warp >> 1;       // 2 x 4 warps
   const int m0 = tm * BM, n0 = tn * BN;
   const int M = t.m, N = t.n, K = t.k;
   const double* __restrict__ Ag = t.A;
   const double* __restrict__ Bg = t.B;
+
+  // C prefetch (beta != 0): the 16 values this thread will update
+  double cpre[4][2][2];
+  if (t.beta != 0.0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int row = m0 + wm * 32 + i * 8 + gid;
+          const int col = n0 + wn * 16 + j * 8 + 2 * tig + h;
+          cpre[i][j][h] = (row < M && col < N) ? t.C[row + (int64_t)col * t.ldc] : 0.0;
+        }
+  }
 
   auto load_stage = [&](int kt, int stage) {
     const int k0 = kt * BK;
     double* as = As + stage * A_STAGE;
     double* bs = Bs + stage * B_STAGE;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < 4; ++q) {
       const int idx = tid + NT * q;
       if (!TRANSA) {
         const int i = idx % BM, l = idx / BM;
@@ -65,11 +83,11 @@ __device__ __forceinline__ void gemm_tile(const GemmTask& t, int tm, int tn, dou
     }
   };
 
-  double acc[4][4][2];
+  double acc[4][2][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int nk = (K + BK - 1) / BK;
 #pragma unroll
@@ -85,18 +103,18 @@ __device__ __forceinline__ void gemm_tile(const GemmTask& t, int tm, int tn, dou
     const double* bs = Bs + stage * B_STAGE;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double a[4], b[4];
+      double a[4], b[2];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int r = wm * 32 + i * 8 + gid;
         a[i] = TRANSA ? as[r * ST + kk + tig] : as[(kk + tig) * SA + r];
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = bs[(wn * 32 + j * 8 + gid) * ST + kk + tig];
+      for (int j = 0; j < 2; ++j) b[j] = bs[(wn * 16 + j * 8 + gid) * ST + kk + tig];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
     const int nxt = kt + STAGES - 1;
     if (nxt < nk) load_stage(nxt, nxt % STAGES);
@@ -109,16 +127,15 @@ __device__ __forceinline__ void gemm_tile(const GemmTask& t, int tm, int tn, dou
     const int row = m0 + wm * 32 + i * 8 + gid;
     if (row >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < 2; ++j) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int col = n0 + wn * 32 + j * 8 + 2 * tig + h;
+        const int col = n0 + wn * 16 + j * 8 + 2 * tig + h;
         if (col >= N) continue;
-        double* c = t.C + row + (int64_t)col * t.ldc;
         double v = t.alpha * acc[i][j][h];
-        if (t.beta != 0.0) v += t.beta * (*c);
+        if (t.beta != 0.0) v += t.beta * cpre[i][j][h];
         if (row == col) v += t.diag;
-        *c = v;
+        t.C[row + (int64_t)col * t.ldc] = v;
       }
     }
   }
