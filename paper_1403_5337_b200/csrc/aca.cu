@@ -64,70 +64,31 @@ __device__ __forceinline__ double transpose_reduce8(double (&a)[8], int lane) {
 }
 
 // ---------------------------------------------------------------------------
-// TMA (bulk async copy) + mbarrier helpers.  Column slices of U/V are streamed
-// into a STAGES-deep SMEM ring by one elected thread with cp.async.bulk
-// (UBLKCP); completion is tracked with mbarrier transaction counts.
-constexpr int STAGES = 3;
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-               "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n HK_WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra HK_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void fence_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-}
-__device__ __forceinline__ void fence_async_global() {
-  asm volatile("fence.proxy.async.global;\n" ::: "memory");
-}
-
-struct Ring {           // per-CTA TMA staging ring (SMEM)
-  double* buf;          // [STAGES][KC][G] doubles
-  uint64_t* full;       // [STAGES] mbarriers
-  unsigned seq;         // chunks issued so far (CTA-uniform)
-};
-
-// ---------------------------------------------------------------------------
 // Fused residual sweep over one cross vector of length `len`.  F is COLUMN-major
-// with leading dimension LD.  Each thread owns EPT elements e = g0 + tid + q*NT
-// of a group of G = NT*EPT elements:
+// with power-of-two leading dimension LD = 1 << LDLOG (compile time, so every
+// column load is an immediate offset from a per-element pointer).  Each thread
+// owns EPT elements e = g0 + tid + q*NT (coalesced for every q):
 //   F[e, out_col] = src[e] - sum_{k<nk} coef[k] * F[e, k]   (reference k order,
 //                   separate IEEE multiply and subtract: bit-exact)
 // and, for k < ndot, the per-warp partial dot products
 //   part[w*pld + k] = sum_{e owned by warp w} F[e, pend_col] * F[e, k]
 // of the PREVIOUS cross with the accepted crosses -- the stopping-test terms
 // of the pending step ride along with the next step's sweep, so each cross
-// vector is streamed once per step.  The columns stream through the TMA ring
-// (thread 0 issues one bulk copy per column slice, STAGES-1 chunks ahead), so
-// the sweep's global latency is paid once, not once per chunk.  Dot partials
-// of a chunk are summed over the thread's EPT elements, then over the warp
-// with one transpose-reduce (fixed order, deterministic).  out_col < 0: dots
-// only.  used != nullptr: column sweep (argmax over untouched entries + sum of
-// squares); else row sweep.
-template <int NT, int EPT>
-__device__ __noinline__ void sweep(Ring& ring, const double* __restrict__ F, int64_t LD, int len,
-                                   int nk, int ndot, const double* __restrict__ coef,
-                                   const double* __restrict__ src, int out_col, int pend_col,
-                                   double* __restrict__ part, int pld,
-                                   const unsigned char* __restrict__ used, ArgMax& best,
-                                   double& sumsq, double& bestval, double* xout) {
-  constexpr int G = NT * EPT;
+// vector is streamed once per step.  A chunk of KC columns issues EPT*KC
+// independent loads; the dot partials of a chunk are summed over the thread's
+// EPT elements first and then over the warp with one transpose-reduce, so the
+// cross-lane cost is amortised over EPT elements.  Fixed reduction order
+// (deterministic).  out_col < 0: dots only.  used != nullptr: column sweep
+// (argmax over untouched entries + sum of squares); else row sweep.
+template <int NT, int EPT, int LDLOG>
+__device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len, int nk, int ndot,
+                                           const double* __restrict__ coef,
+                                           const double* __restrict__ src, int sstride,
+                                           int out_col, int pend_col, double* __restrict__ part,
+                                           int pld, const unsigned char* __restrict__ used,
+                                           ArgMax& best, double& sumsq, double& bestval,
+                                           double* __restrict__ xout) {
+  constexpr int64_t LD = int64_t(1) << LDLOG;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   best.v = 0.0;
   best.i = -1;
@@ -137,57 +98,30 @@ __device__ __noinline__ void sweep(Ring& ring, const double* __restrict__ F, int
   for (int k = lane; k < ndot; k += 32) mypart[k] = 0.0;
   __syncwarp();
   const int kmax = nk > ndot ? nk : ndot;
-  const int nchunks = (kmax + KC - 1) / KC;
 #pragma unroll 1
-  for (int g0 = 0; g0 < len; g0 += G) {
-    const int gl = min(G, len - g0);
-    const unsigned bytes = (unsigned)((gl * 8 + 15) & ~15);
+  for (int g0 = 0; g0 < len; g0 += NT * EPT) {
     double x[EPT], pv[EPT];
+    const double* pk[EPT];
     bool ok[EPT];
 #pragma unroll
     for (int q = 0; q < EPT; ++q) {
       const int e = g0 + tid + q * NT;
       ok[q] = e < len;
-      x[q] = (ok[q] && src) ? src[e] : 0.0;
-      pv[q] = (ok[q] && ndot > 0) ? F[e + (int64_t)pend_col * LD] : 0.0;
-    }
-    // prologue: chunks 0 .. STAGES-2
-    if (tid == 0) {
-      fence_async_smem();
-      for (int c = 0; c < STAGES - 1 && c < nchunks; ++c) {
-        const unsigned slot = (ring.seq + c) % STAGES;
-        const int kb = c * KC, ncol = min(KC, kmax - kb);
-        mbar_expect_tx(&ring.full[slot], bytes * ncol);
-        for (int j = 0; j < ncol; ++j)
-          tma_load_1d(ring.buf + ((size_t)slot * KC + j) * G, F + g0 + (int64_t)(kb + j) * LD, bytes,
-                      &ring.full[slot]);
-      }
+      pk[q] = F + (ok[q] ? e : 0);
+      x[q] = (ok[q] && src) ? src[(int64_t)e * sstride] : 0.0;
+      pv[q] = (ok[q] && ndot > 0) ? pk[q][(int64_t)pend_col * LD] : 0.0;
     }
 #pragma unroll 1
-    for (int c = 0; c < nchunks; ++c) {
-      const int kb = c * KC;
-      const unsigned seqc = ring.seq + c;
-      const unsigned slot = seqc % STAGES;
-      if (c > 0) __syncthreads();           // everyone is done with chunk c-1's slot
-      if (tid == 0 && c + STAGES - 1 < nchunks) {
-        const int cn = c + STAGES - 1;
-        const unsigned sl = (ring.seq + cn) % STAGES;
-        const int kbn = cn * KC, ncol = min(KC, kmax - kbn);
-        fence_async_smem();
-        mbar_expect_tx(&ring.full[sl], bytes * ncol);
-        for (int j = 0; j < ncol; ++j)
-          tma_load_1d(ring.buf + ((size_t)sl * KC + j) * G, F + g0 + (int64_t)(kbn + j) * LD, bytes,
-                      &ring.full[sl]);
-      }
-      mbar_wait(&ring.full[slot], (seqc / STAGES) & 1);
-      const double* st = ring.buf + (size_t)slot * KC * G + tid;
-      double a[EPT][KC];
+    for (int kb = 0; kb < kmax; kb += KC) {
       const bool full = kb + KC <= kmax;
+      double a[EPT][KC];
 #pragma unroll
-      for (int j = 0; j < KC; ++j)
+      for (int q = 0; q < EPT; ++q)
 #pragma unroll
-        for (int q = 0; q < EPT; ++q)
-          a[q][j] = (ok[q] && (full || kb + j < kmax)) ? st[j * G + q * NT] : 0.0;
+        for (int j = 0; j < KC; ++j)
+          a[q][j] = (ok[q] && (full || kb + j < kmax)) ? __ldca(pk[q] + j * LD) : 0.0;
+#pragma unroll
+      for (int q = 0; q < EPT; ++q) pk[q] += KC * LD;
       if (kb < ndot) {                       // warp-uniform
         double acc[KC];
 #pragma unroll
@@ -203,23 +137,21 @@ __device__ __noinline__ void sweep(Ring& ring, const double* __restrict__ F, int
       if (kb + KC <= nk) {
 #pragma unroll
         for (int j = 0; j < KC; ++j) {
-          const double cj = coef[kb + j];
+          const double c = coef[kb + j];
 #pragma unroll
-          for (int q = 0; q < EPT; ++q) x[q] = sub_rn(x[q], mul_rn(cj, a[q][j]));
+          for (int q = 0; q < EPT; ++q) x[q] = sub_rn(x[q], mul_rn(c, a[q][j]));
         }
       } else {
 #pragma unroll
         for (int j = 0; j < KC; ++j) {
-          const double cj = coef[kb + j];
+          const double c = coef[kb + j];
           if (kb + j < nk) {
 #pragma unroll
-            for (int q = 0; q < EPT; ++q) x[q] = sub_rn(x[q], mul_rn(cj, a[q][j]));
+            for (int q = 0; q < EPT; ++q) x[q] = sub_rn(x[q], mul_rn(c, a[q][j]));
           }
         }
       }
     }
-    ring.seq += nchunks;
-    __syncthreads();                          // ring slots free for the next group / sweep
     if (out_col >= 0) {
 #pragma unroll
       for (int q = 0; q < EPT; ++q) {
@@ -237,9 +169,29 @@ __device__ __noinline__ void sweep(Ring& ring, const double* __restrict__ F, int
           bestval = x[q];
         }
       }
-      fence_async_global();                   // these writes are read back by later TMA copies
     }
   }
+}
+
+// One call target per (NT, EPT) for the caller (keeps its register allocation
+// small); the leading dimension is dispatched once, inside.
+template <int NT, int EPT>
+__device__ __noinline__ void sweep(int ldlog, const double* __restrict__ F, int len, int nk, int ndot,
+                                   const double* __restrict__ coef, const double* __restrict__ src,
+                                   int sstride, int out_col, int pend_col, double* __restrict__ part,
+                                   int pld, const unsigned char* __restrict__ used, ArgMax& best,
+                                   double& sumsq, double& bestval, double* xout) {
+#define HK_SWEEP_CASE(L)                                                                       \
+  case L:                                                                                      \
+    sweep_impl<NT, EPT, L>(F, len, nk, ndot, coef, src, sstride, out_col, pend_col, part, pld, \
+                           used, best, sumsq, bestval, xout);                                  \
+    return;
+  switch (ldlog) {
+    HK_SWEEP_CASE(6) HK_SWEEP_CASE(7) HK_SWEEP_CASE(8) HK_SWEEP_CASE(9) HK_SWEEP_CASE(10)
+    HK_SWEEP_CASE(11) HK_SWEEP_CASE(12) HK_SWEEP_CASE(13)
+    default: return;
+  }
+#undef HK_SWEEP_CASE
 }
 
 // Block argmax that also carries the signed value of the winner.
@@ -322,28 +274,24 @@ __device__ __forceinline__ double stopping_estimate(const double* __restrict__ p
 // the sweeps of step s+1 (which assume cross s is accepted) also accumulate
 // cross s's stopping-test dot products; cross s is decided after them, and the
 // speculative step (and its trace events) is discarded on rejection.
-// SMEM: U, V and the A block live in shared memory (blocks up to 64 x 64).
 template <int NT, int EPT>
-__device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int part_in_smem,
-                                          Ring& ring) {
-  constexpr bool SMEM = false;
+__device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int part_in_smem) {
   const int m = t.m, n = t.n, cap = t.cap;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
   uint64_t t_start = 0;
   if (t.clock && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-  extern __shared__ __align__(128) unsigned char smraw[];
-  const int64_t LD = int64_t(1) << t.ldu;    // U and V share one power-of-two leading dimension
-  // SMEM layout: [U, V (ld LD x cap each), A (m x (n+1))] when SMEM, then
-  // coef[cap+KC], partU/partV[NW*cap], prod[cap] (or global scratch), used[m]
-  double* sbase = reinterpret_cast<double*>(smraw) + (size_t)STAGES * KC * NT * EPT;   // after the ring
-  double* U = SMEM ? sbase : t.U;
-  double* V = SMEM ? sbase + LD * cap : t.V;
-  double* As = SMEM ? sbase + 2 * LD * cap : nullptr;
-  const int ldas = n + 1;
-  double* coef = SMEM ? As + (int64_t)m * ldas : sbase;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int ldlog = t.ldu;                   // U and V share one power-of-two leading dimension
+  const int64_t LD = int64_t(1) << ldlog;
+  // SMEM layout: coef[cap+KC], partU/partV[NW*cap], prod[cap] (or global
+  // scratch when they do not fit), used[m]
+  double* sbase = reinterpret_cast<double*>(smraw);
+  double* U = t.U;
+  double* V = t.V;
+  double* coef = sbase;
   const int pld = cap;
-  const bool pin = SMEM || part_in_smem;
+  const bool pin = part_in_smem;
   double* partU = pin ? coef + cap + KC : t.scratch;
   double* partV = partU + NW * pld;
   double* prod = partV + NW * pld;
@@ -367,14 +315,10 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
   }
   for (int i = tid; i < m; i += NT) used[i] = 0;
   for (int k = tid; k < cap + KC; k += NT) coef[k] = 0.0;
-  if (SMEM) {
-    for (int i = 0; i < m; ++i)
-      for (int j = tid; j < n; j += NT) As[i * ldas + j] = t.A[(int64_t)i * t.lda + j];
-  }
   __syncthreads();
 
-  const double* rowsrc_base = SMEM ? As : t.A;
-  const int64_t rowsrc_ld = SMEM ? ldas : t.lda;
+  const double* rowsrc_base = t.A;
+  const int64_t rowsrc_ld = t.lda;
   int r = 0, row = 0, nused = 0;
   bool pending = false;                       // column r holds an undecided cross
   double uu_p = 0.0, vv_p = 0.0, fro2 = 0.0;
@@ -387,8 +331,8 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
     const bool can_step = pending ? (c < cap && nused < m) : (c < cap);
     if (!can_step) {
       if (pending) {                          // decide the last cross: dots only
-        sweep<NT, EPT>(ring, U, LD, m, 0, r, coef, nullptr, -1, r, partU, pld, nullptr, best, dummy, bval, xv);
-        sweep<NT, EPT>(ring, V, LD, n, 0, r, coef, nullptr, -1, r, partV, pld, nullptr, best, dummy, bval, xv);
+        sweep<NT, EPT>(ldlog, U, m, 0, r, coef, nullptr, 1, -1, r, partU, pld, nullptr, best, dummy, bval, xv);
+        sweep<NT, EPT>(ldlog, V, n, 0, r, coef, nullptr, 1, -1, r, partV, pld, nullptr, best, dummy, bval, xv);
         bar<NT>();
         const double cross = uu_p * vv_p;
         const double est = stopping_estimate<NT>(partU, partV, pld, r, fro2, cross, prod, &s_est);
@@ -405,14 +349,14 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
     for (int k = tid; k < c; k += NT) coef[k] = U[row + (int64_t)k * LD];
     bar<NT>();
     // residual row (:253-256) + the pending cross's v dots
-    sweep<NT, EPT>(ring, V, LD, n, c, pending ? r : 0, coef, rowsrc_base + (int64_t)row * rowsrc_ld,
+    sweep<NT, EPT>(ldlog, V, n, c, pending ? r : 0, coef, rowsrc_base + (int64_t)row * rowsrc_ld, 1,
                    c, r, partV, pld, nullptr, best, dummy, bval, xv);
     double delta;
     best = block_argmax_val<NT>(best, bval, red_v, red_i, red_x, delta);
     const int col = (int)best.i;
     if (delta == 0.0) {                       // zero residual row (:258-264)
       if (pending) {
-        sweep<NT, EPT>(ring, U, LD, m, 0, r, coef, nullptr, -1, r, partU, pld, nullptr, nxt, dummy, bval, xv);
+        sweep<NT, EPT>(ldlog, U, m, 0, r, coef, nullptr, 1, -1, r, partU, pld, nullptr, nxt, dummy, bval, xv);
         bar<NT>();
         const double cross = uu_p * vv_p;
         const double est = stopping_estimate<NT>(partU, partV, pld, r, fro2, cross, prod, &s_est);
@@ -455,14 +399,13 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
         vv += v * v;
       }
     }
-    fence_async_global();                     // V[:, c] is streamed by TMA in later steps
     for (int k = tid; k < c; k += NT) coef[k] = V[col + (int64_t)k * LD];
     if (tid == 0 && tcols) tcols[ncol_ev] = col;
     ++ncol_ev;
     bar<NT>();
     // residual column (:266-268) + next-row candidate (:283) + pending u dots
-    const double* csrc = SMEM ? As + col : t.At + (int64_t)col * t.lda;
-    sweep<NT, EPT>(ring, U, LD, m, c, pending ? r : 0, coef, csrc, c, r, partU, pld,
+    const double* csrc = t.At + (int64_t)col * t.lda;
+    sweep<NT, EPT>(ldlog, U, m, c, pending ? r : 0, coef, csrc, 1, c, r, partU, pld,
                    used, nxt, uu, bval, xv);
     {
       nxt = warp_argmax(nxt);
@@ -508,14 +451,6 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
     row = (int)nxt.i;
     bar<NT>();
   }
-  if (SMEM) {                                 // SMEM factors -> global (first r columns)
-    bar<NT>();
-    const int64_t LDG = int64_t(1) << t.ldu;
-    for (int k = 0; k < r; ++k) {
-      for (int i = tid; i < m; i += NT) t.U[i + k * LDG] = U[i + (int64_t)k * LD];
-      for (int j = tid; j < n; j += NT) t.V[j + k * LDG] = V[j + (int64_t)k * LD];
-    }
-  }
   if (tid == 0) {
     *t.rank = r;
     if (t.trace) { t.trace[0] = nrow_ev; t.trace[1] = ncol_ev; }
@@ -539,24 +474,13 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaTask* __restrict__ tas
                                                  int* __restrict__ counter, double tol2,
                                                  int part_in_smem) {
   __shared__ int s_task;
-  __shared__ __align__(8) uint64_t full_bars[STAGES];
-  extern __shared__ __align__(128) unsigned char smraw[];
-  Ring ring;
-  ring.buf = reinterpret_cast<double*>(smraw);
-  ring.full = full_bars;
-  ring.seq = 0;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < STAGES; ++i) mbar_init(&full_bars[i], 1);
-    fence_async_smem();
-  }
-  __syncthreads();
   for (;;) {
     if (threadIdx.x == 0) s_task = atomicAdd(counter, 1);
     __syncthreads();
     const int ti = s_task;
     __syncthreads();
     if (ti >= ntasks) break;
-    aca_block<NT, EPT>(tasks[ti], tol2, part_in_smem, ring);
+    aca_block<NT, EPT>(tasks[ti], tol2, part_in_smem);
     __syncthreads();
   }
 }
@@ -585,10 +509,9 @@ int hk_aca_class(int m, int n) {
 template <int NT, int EPT>
 static cudaError_t launch_cls(const AcaTask* tasks_dev, int ntasks, int max_cap, int max_m,
                               double tol2, int* counter, cudaStream_t st) {
-  const size_t ring_bytes = (size_t)STAGES * KC * NT * EPT * 8;
   const size_t part_bytes = (size_t)(2 * (NT / 32) + 1) * max_cap * 8;
-  const size_t base = ring_bytes + (size_t)(max_cap + KC) * 8 + (size_t)max_m + 16;
-  const int part_in_smem = (base + part_bytes <= 160 * 1024) ? 1 : 0;
+  const size_t base = (size_t)(max_cap + KC) * 8 + (size_t)max_m + 16;
+  const int part_in_smem = (base + part_bytes <= 64 * 1024) ? 1 : 0;
   const size_t smem = base + (part_in_smem ? part_bytes : 0);
   cudaError_t e = cudaFuncSetAttribute(aca_kernel<NT, EPT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
