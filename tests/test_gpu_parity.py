@@ -274,3 +274,38 @@ def test_error_contract():
     with pytest.raises(hk.DimensionMismatchError):
         hk.factorize(hk.BlockAccessor.from_matrix(np.eye(16)), hk.build_tree(15, 8),
                      hk.CompressionConfig(scheme="aca"))
+
+
+# ------------------------------------------------------------------ BASELINE config 4 (n = 9216)
+# The reference's own numbers on this front, measured in this container by running it
+# (SURVEY.md §6.3): max rank per level 227,227,227,195,193,98,53; GMRES to 1e-10 on
+# default_rng(3).standard_normal((9216, 4)) takes 10, 11, 11, 10 iterations.
+CFG4_RANKS = [227, 227, 227, 195, 193, 98, 53]
+CFG4_ITERS = [10, 11, 11, 10]
+
+
+def test_config4_large_front():
+    from paper_1403_5337_b200.frontgen import layered_grid_front
+    front = layered_grid_front((96, 96, 96), "z", 48, device="cuda", return_torch=True).contiguous()
+    n = front.shape[0]
+    assert n == 9216
+    cfg = hk.CompressionConfig(scheme="aca", tol=1e-4)
+    batch = HodlrBatch(n, 72, 1).factorize(front[None], cfg)
+    rep = batch.report(0)
+    assert [lv["max_rank"] for lv in rep.ranks_per_level] == CFG4_RANKS
+    fact = batch.factorization(0)
+    # the two root blocks (4608 x 4608, rank 227) bit-exact against the oracle's ACA
+    A = front.cpu().numpy()
+    h = n // 2
+    for blk, (rs, cs) in enumerate(((slice(0, h), slice(h, n)), (slice(h, n), slice(0, h)))):
+        U, V = fact.block_factor(blk)
+        Uo, Vo = O.aca(A[rs, cs], 1e-4)
+        assert np.array_equal(U, Uo), blk
+        assert np.array_equal(V, Vo), blk
+    op = hk.DenseOperator(front)
+    B = np.random.default_rng(3).standard_normal((n, 4))
+    for j in range(4):
+        res = hk.gmres(op, B[:, j], hk.GmresConfig(tol=1e-10), preconditioner=fact)
+        assert res.converged
+        assert abs(res.iterations - CFG4_ITERS[j]) <= 1, (j, res.iterations)
+        assert res.true_residual <= 1e-9
