@@ -15,7 +15,9 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 INCLUDE = PKG.parent / "include"
-LIB = PKG / "libhodlr_b200.so"
+LIB = Path(os.environ["HK_LIB_OUT"]) if os.environ.get("HK_LIB_OUT") else PKG / "libhodlr_b200.so"
+# experiment knob: extra nvcc flags (e.g. "-DHK_ACA_LB1") for variant builds written to HK_LIB_OUT
+EXTRA = os.environ.get("HK_NVCC_EXTRA", "").split()
 SOURCES = ["aca.cu", "lu.cu", "gj.cu", "gemm.cu", "solve.cu", "krylov.cu", "api.cpp", "graph.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -37,14 +39,14 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not needs_build():
         return LIB
-    objdir = PKG / "build"
-    objdir.mkdir(exist_ok=True)
+    objdir = PKG / "build" / (LIB.stem if os.environ.get("HK_LIB_OUT") else "")
+    objdir.mkdir(parents=True, exist_ok=True)
     objs = []
     procs = []
     for src in SOURCES:
         obj = objdir / (src + ".o")
         cmd = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-               "-Xcompiler", "-fvisibility=hidden", "-I", str(INCLUDE), "-c", str(CSRC / src),
+               "-Xcompiler", "-fvisibility=hidden", *EXTRA, "-I", str(INCLUDE), "-c", str(CSRC / src),
                "-o", str(obj)]
         if src.endswith(".cu"):
             cmd[1:1] = ["-Xptxas", "-v"] if verbose else []

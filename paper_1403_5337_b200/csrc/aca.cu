@@ -42,13 +42,16 @@ __global__ void transpose_kernel(const double* __restrict__ A, double* __restric
   }
 }
 
-constexpr int KC = 8;     // columns per chunk (one transpose-reduce each)
+#ifndef HK_ACA_KC
+#define HK_ACA_KC 8
+#endif
+constexpr int KC = HK_ACA_KC;   // columns per chunk (one transpose-reduce each): 8 or 16
 
-// Lane l of the warp receives the warp-wide sum of a[l & 7] (butterfly
-// reduce-scatter inside groups of 8 lanes, then two exchanges between groups).
-__device__ __forceinline__ double transpose_reduce8(double (&a)[8], int lane) {
+// Lane l of the warp receives the warp-wide sum of a[l & (KC-1)] (butterfly
+// reduce-scatter inside groups of KC lanes, then exchanges between groups).
+__device__ __forceinline__ double transpose_reduce(double (&a)[KC], int lane) {
 #pragma unroll
-  for (int s = 4; s >= 1; s >>= 1) {
+  for (int s = KC / 2; s >= 1; s >>= 1) {
     const bool upper = (lane & s) != 0;
 #pragma unroll
     for (int i = 0; i < s; ++i) {
@@ -58,9 +61,87 @@ __device__ __forceinline__ double transpose_reduce8(double (&a)[8], int lane) {
     }
   }
   double v = a[0];
-  v += __shfl_xor_sync(0xffffffffu, v, 8);
-  v += __shfl_xor_sync(0xffffffffu, v, 16);
+#pragma unroll
+  for (int o = KC; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// ---------------------------------------------------------------------------
+// U/V column loads: plain weak loads, L1-cached (the CTA's own earlier stores
+// are visible after its barriers; no other CTA writes this block's U/V)
+__device__ __forceinline__ double ld_col(const double* p) { return *p; }
+
+// Chunk helpers of the fused sweep (KC columns x EPT elements per thread).
+//
+// dots: part[w*pld + kb + j] += sum over the warp's elements of pv[e] * a[e][j]
+// (EPT-sum in registers, then one transpose-reduce across the warp).  MASK
+// zeroes the columns j with kb + j >= ndot (the chunk straddling ndot).
+template <int EPT, bool MASK>
+__device__ __forceinline__ void chunk_dots(const double (&a)[EPT][KC], const double (&pv)[EPT], int kb,
+                                           int ndot, double* __restrict__ mypart, int lane) {
+  double acc[KC];
+#pragma unroll
+  for (int j = 0; j < KC; ++j) {
+    double sacc = 0.0;
+#pragma unroll
+    for (int q = 0; q < EPT; ++q) sacc = fma(pv[q], a[q][j], sacc);
+    acc[j] = (!MASK || kb + j < ndot) ? sacc : 0.0;
+  }
+  const double v = transpose_reduce(acc, lane);
+  if (lane < KC && (!MASK || kb + lane < ndot)) mypart[kb + lane] += v;
+}
+
+// residual update x[e] -= coef[k] * a[e][k] in k order (separate IEEE
+// multiply and subtract: bit-exact with the reference); PART: only k < nk.
+template <int EPT, bool PART>
+__device__ __forceinline__ void chunk_sub(double (&x)[EPT], const double (&a)[EPT][KC],
+                                          const double* __restrict__ coef, int kb, int nk) {
+#pragma unroll
+  for (int j = 0; j < KC; ++j) {
+    const double c = coef[kb + j];
+    if (!PART || kb + j < nk) {
+#pragma unroll
+      for (int q = 0; q < EPT; ++q) x[q] = sub_rn(x[q], mul_rn(c, a[q][j]));
+    }
+  }
+}
+
+template <int EPT, int LDLOG>
+__device__ __forceinline__ void chunk_load_full(double (&a)[EPT][KC], const double* const (&pk)[EPT],
+                                                int kb) {
+  constexpr int64_t LD = int64_t(1) << LDLOG;
+#pragma unroll
+  for (int q = 0; q < EPT; ++q) {
+    const double* p = pk[q] + (int64_t)kb * LD;
+#pragma unroll
+    for (int j = 0; j < KC; ++j) a[q][j] = ld_col(p + j * LD);
+  }
+}
+
+// L1 prefetch of a whole chunk (issued one chunk ahead)
+template <int EPT, int LDLOG>
+__device__ __forceinline__ void chunk_prefetch(const double* const (&pk)[EPT], int kb) {
+  constexpr int64_t LD = int64_t(1) << LDLOG;
+#pragma unroll
+  for (int q = 0; q < EPT; ++q) {
+    const double* p = pk[q] + (int64_t)kb * LD;
+#pragma unroll
+    for (int j = 0; j < KC; ++j) asm volatile("prefetch.global.L1 [%0];" ::"l"(p + j * LD));
+  }
+}
+
+// Both halves of a full chunk's work; the chunk's column range is [kb, kb+KC).
+template <int EPT>
+__device__ __forceinline__ void chunk_process(double (&x)[EPT], const double (&a)[EPT][KC],
+                                              const double (&pv)[EPT], const double* __restrict__ coef,
+                                              int kb, int nk, int ndot, double* __restrict__ mypart,
+                                              int lane) {
+  if (kb < ndot) {                               // warp-uniform
+    if (kb + KC <= ndot) chunk_dots<EPT, false>(a, pv, kb, ndot, mypart, lane);
+    else chunk_dots<EPT, true>(a, pv, kb, ndot, mypart, lane);
+  }
+  if (kb + KC <= nk) chunk_sub<EPT, false>(x, a, coef, kb, nk);
+  else if (kb < nk) chunk_sub<EPT, true>(x, a, coef, kb, nk);
 }
 
 // ---------------------------------------------------------------------------
@@ -75,11 +156,12 @@ __device__ __forceinline__ double transpose_reduce8(double (&a)[8], int lane) {
 // of the PREVIOUS cross with the accepted crosses -- the stopping-test terms
 // of the pending step ride along with the next step's sweep, so each cross
 // vector is streamed once per step.  A chunk of KC columns issues EPT*KC
-// independent loads; the dot partials of a chunk are summed over the thread's
-// EPT elements first and then over the warp with one transpose-reduce, so the
-// cross-lane cost is amortised over EPT elements.  Fixed reduction order
-// (deterministic).  out_col < 0: dots only.  used != nullptr: column sweep
-// (argmax over untouched entries + sum of squares); else row sweep.
+// independent loads; chunks that lie entirely inside the block are loaded
+// unpredicated, with the next chunk prefetched into L1 while the current one
+// is reduced; the ragged tail goes through a predicated path.  The dot partials of a chunk are summed over the thread's
+// EPT elements first and then over the warp with one transpose-reduce.  Fixed
+// reduction order (deterministic).  out_col < 0: dots only.  used != nullptr:
+// column sweep (argmax over untouched entries + sum of squares); else row sweep.
 template <int NT, int EPT, int LDLOG>
 __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len, int nk, int ndot,
                                            const double* __restrict__ coef,
@@ -103,6 +185,7 @@ __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len
     double x[EPT], pv[EPT];
     const double* pk[EPT];
     bool ok[EPT];
+    const bool gfull = g0 + NT * EPT <= len;      // warp-uniform
 #pragma unroll
     for (int q = 0; q < EPT; ++q) {
       const int e = g0 + tid + q * NT;
@@ -111,46 +194,28 @@ __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len
       x[q] = (ok[q] && src) ? src[(int64_t)e * sstride] : 0.0;
       pv[q] = (ok[q] && ndot > 0) ? pk[q][(int64_t)pend_col * LD] : 0.0;
     }
+    int kb = 0;
+    if (gfull) {
+      const int kfull = (kmax / KC) * KC;
 #pragma unroll 1
-    for (int kb = 0; kb < kmax; kb += KC) {
-      const bool full = kb + KC <= kmax;
+      for (; kb < kfull; kb += KC) {
+        double a[EPT][KC];
+        chunk_load_full<EPT, LDLOG>(a, pk, kb);
+        // the next chunk's lines are pulled into L1 while this one is reduced
+        // (prefetch distance 1 measured best: 2..4 thrash L1)
+        if (kb + KC < kfull) chunk_prefetch<EPT, LDLOG>(pk, kb + KC);
+        chunk_process<EPT>(x, a, pv, coef, kb, nk, ndot, mypart, lane);
+      }
+    }
+#pragma unroll 1
+    for (; kb < kmax; kb += KC) {                 // ragged tail (predicated loads)
       double a[EPT][KC];
 #pragma unroll
       for (int q = 0; q < EPT; ++q)
 #pragma unroll
         for (int j = 0; j < KC; ++j)
-          a[q][j] = (ok[q] && (full || kb + j < kmax)) ? __ldca(pk[q] + j * LD) : 0.0;
-#pragma unroll
-      for (int q = 0; q < EPT; ++q) pk[q] += KC * LD;
-      if (kb < ndot) {                       // warp-uniform
-        double acc[KC];
-#pragma unroll
-        for (int j = 0; j < KC; ++j) {
-          double sacc = 0.0;
-#pragma unroll
-          for (int q = 0; q < EPT; ++q) sacc = fma(pv[q], a[q][j], sacc);
-          acc[j] = (kb + j < ndot) ? sacc : 0.0;
-        }
-        const double v = transpose_reduce8(acc, lane);
-        if (lane < KC && kb + lane < ndot) mypart[kb + lane] += v;
-      }
-      if (kb + KC <= nk) {
-#pragma unroll
-        for (int j = 0; j < KC; ++j) {
-          const double c = coef[kb + j];
-#pragma unroll
-          for (int q = 0; q < EPT; ++q) x[q] = sub_rn(x[q], mul_rn(c, a[q][j]));
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < KC; ++j) {
-          const double c = coef[kb + j];
-          if (kb + j < nk) {
-#pragma unroll
-            for (int q = 0; q < EPT; ++q) x[q] = sub_rn(x[q], mul_rn(c, a[q][j]));
-          }
-        }
-      }
+          a[q][j] = (ok[q] && kb + j < kmax) ? ld_col(pk[q] + (int64_t)(kb + j) * LD) : 0.0;
+      chunk_process<EPT>(x, a, pv, coef, kb, nk, ndot, mypart, lane);
     }
     if (out_col >= 0) {
 #pragma unroll
@@ -496,11 +561,12 @@ cudaError_t hk_launch_transpose(const double* A, double* At, int64_t n, int64_t 
   return cudaGetLastError();
 }
 
-// Size classes: CTA shape by the longer cross vector L = max(m, n).
-//   class 0: L > 256        128 threads x 4 elements (global U/V)
-//   class 1: 128 < L <= 256  64 threads x 4 elements
-//   class 2: 64 < L <= 128   32 threads x 4 elements (one warp, no block barriers)
-//   class 3: L <= 64         32 threads x 2 elements
+// Size classes by the longer cross vector L = max(m, n); every class runs
+// 2 elements per thread (measured best against 1 and 4 on config 3):
+//   class 0: L > 256         256 threads
+//   class 1: 128 < L <= 256  128 threads
+//   class 2: 64 < L <= 128    64 threads
+//   class 3: L <= 64          32 threads (one warp, no block barriers)
 int hk_aca_class(int m, int n) {
   const int L = m > n ? m : n;
   return L > 256 ? 0 : L > 128 ? 1 : L > 64 ? 2 : 3;
@@ -528,13 +594,25 @@ static cudaError_t launch_cls(const AcaTask* tasks_dev, int ntasks, int max_cap,
   return cudaGetLastError();
 }
 
+// CTA shape (threads x elements per thread) of each size class.
+#ifndef HK_ACA_T0
+#define HK_ACA_T0 256
+#define HK_ACA_E0 2
+#define HK_ACA_T1 128
+#define HK_ACA_E1 2
+#define HK_ACA_T2 64
+#define HK_ACA_E2 2
+#define HK_ACA_T3 32
+#define HK_ACA_E3 2
+#endif
+
 static cudaError_t launch_class_id(int cls, const AcaTask* td, int nt, int max_cap, int max_m,
                                    double tol2, int* counter, cudaStream_t st) {
   switch (cls) {
-    case 0: return launch_cls<128, 4>(td, nt, max_cap, max_m, tol2, counter, st);
-    case 1: return launch_cls<64, 4>(td, nt, max_cap, max_m, tol2, counter, st);
-    case 2: return launch_cls<32, 4>(td, nt, max_cap, max_m, tol2, counter, st);
-    default: return launch_cls<32, 2>(td, nt, max_cap, max_m, tol2, counter, st);
+    case 0: return launch_cls<HK_ACA_T0, HK_ACA_E0>(td, nt, max_cap, max_m, tol2, counter, st);
+    case 1: return launch_cls<HK_ACA_T1, HK_ACA_E1>(td, nt, max_cap, max_m, tol2, counter, st);
+    case 2: return launch_cls<HK_ACA_T2, HK_ACA_E2>(td, nt, max_cap, max_m, tol2, counter, st);
+    default: return launch_cls<HK_ACA_T3, HK_ACA_E3>(td, nt, max_cap, max_m, tol2, counter, st);
   }
 }
 
@@ -567,4 +645,4 @@ cudaError_t hk_launch_aca(const AcaTask* tasks_dev, int ntasks, int max_cap, int
   return e;
 }
 
-size_t hk_aca_scratch_doubles(int cap) { return (size_t)(2 * (128 / 32) + 1) * cap + KC; }
+size_t hk_aca_scratch_doubles(int cap) { return (size_t)(2 * (512 / 32) + 1) * cap + 16; }
