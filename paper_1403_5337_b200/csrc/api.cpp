@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -32,6 +33,26 @@
 
 // ------------------------------------------------------------------ errors, counters
 static thread_local std::string g_err;
+
+// HK_HOST_PROFILE=1: print host-side phase times (planning vs launching vs
+// waiting) of build / factor / solve to stderr.
+static bool host_profile() {
+  static int on = -1;
+  if (on < 0) on = getenv("HK_HOST_PROFILE") ? 1 : 0;
+  return on == 1;
+}
+struct HostClock {
+  const char* what;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit HostClock(const char* w) : what(w) {}
+  void mark(const char* phase) {
+    if (!host_profile()) return;
+    auto t1 = std::chrono::steady_clock::now();
+    fprintf(stderr, "[hk host] %s %s %.1f us\n", what, phase,
+            std::chrono::duration<double, std::micro>(t1 - t0).count());
+    t0 = t1;
+  }
+};
 static std::atomic<long long> g_launches{0};
 
 void hk_count_launch(int k) { g_launches += k; }
@@ -97,6 +118,77 @@ static cudaError_t upload(DevBuf& b, const std::vector<T>& v, cudaStream_t st) {
   return cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st);
 }
 
+// Pinned host staging for task arrays.  An API call packs the task arrays of
+// one phase into pinned memory, moves them to the device with ONE asynchronous
+// copy (commit) and launches that phase; the host then plans the next phase
+// while the GPU runs this one.  Storage is a list of fixed segments (pinned
+// host + device twin) so that committed regions never move; segments are
+// reused by the next call only after that call's own synchronisation point.
+struct Staging {
+  struct Seg {
+    char* host = nullptr;
+    char* dev = nullptr;
+    size_t cap = 0, used = 0, committed = 0;
+  };
+  std::vector<Seg> segs;
+  size_t cur = 0;
+  static constexpr size_t kSeg = size_t(4) << 20;
+  void reset() {
+    for (auto& g : segs) g.used = g.committed = 0;
+    cur = 0;
+  }
+  // returns a device pointer valid for launches enqueued after the next commit()
+  void* push(const void* src, size_t bytes, cudaStream_t st) {
+    for (;;) {
+      if (cur == segs.size()) {
+        Seg g;
+        g.cap = std::max(kSeg, bytes + 256);
+        if (cudaHostAlloc((void**)&g.host, g.cap, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+        if (cudaMallocAsync((void**)&g.dev, g.cap, st) != cudaSuccess) {
+          cudaFreeHost(g.host);
+          return nullptr;
+        }
+        segs.push_back(g);
+      }
+      Seg& g = segs[cur];
+      const size_t off = (g.used + 255) & ~size_t(255);
+      if (off + bytes <= g.cap) {
+        if (bytes) memcpy(g.host + off, src, bytes);
+        g.used = off + bytes;
+        return g.dev + off;
+      }
+      if (commit_seg(g, st) != cudaSuccess) return nullptr;   // full: flush, next segment
+      ++cur;
+    }
+  }
+  template <class T>
+  T* push(const std::vector<T>& v, cudaStream_t st) {
+    return reinterpret_cast<T*>(push(v.data(), v.size() * sizeof(T), st));
+  }
+  static cudaError_t commit_seg(Seg& g, cudaStream_t st) {
+    if (g.used <= g.committed) return cudaSuccess;
+    cudaError_t e = cudaMemcpyAsync(g.dev + g.committed, g.host + g.committed, g.used - g.committed,
+                                    cudaMemcpyHostToDevice, st);
+    g.committed = g.used;
+    return e;
+  }
+  cudaError_t commit(cudaStream_t st) {
+    for (size_t i = 0; i <= cur && i < segs.size(); ++i) {
+      cudaError_t e = commit_seg(segs[i], st);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  void release() {
+    for (auto& g : segs) {
+      if (g.host) cudaFreeHost(g.host);
+      if (g.dev) cudaFree(g.dev);
+    }
+    segs.clear();
+    cur = 0;
+  }
+};
+
 static void init_pool_once() {
   static bool done = false;
   if (done) return;
@@ -136,22 +228,28 @@ struct NodeRec {  // per (front, node) factor storage
   int64_t w = 0, hcols = 0;
 };
 
+// A cached solve program: task arrays in the plan's program staging (pstage),
+// valid until the next factorization drops them.
 struct SolveProg {
   bool small = true;
   int s = 0;
   // small-s
-  DevBuf leaf_t;
+  const MatVecTask* leaf_t = nullptr;
   int n_leaf = 0, leaf_rows = 0, leaf_k = 0;
   struct Level {
-    DevBuf dot_t, sinv_t, upd_t;
+    const DotTask* dot_t = nullptr;
+    const MatVecTask* sinv_t = nullptr;
+    const MatVecTask* upd_t = nullptr;
     int n_dot = 0, n_sinv = 0, n_upd = 0;
     int dot_cols = 0, dot_k = 0, sinv_rows = 0, sinv_k = 0, upd_rows = 0, upd_k = 0;
     // gemm variant
-    DevBuf g1, g1map, g2, g2map, g3, g3map;
+    const GemmTask *g1 = nullptr, *g2 = nullptr, *g3 = nullptr;
+    const int32_t *g1map = nullptr, *g2map = nullptr, *g3map = nullptr;
     int t1 = 0, t2 = 0, t3 = 0;
   };
   std::vector<Level> levels;
-  DevBuf leaf_g, leaf_map;
+  const GemmTask* leaf_g = nullptr;
+  const int32_t* leaf_map = nullptr;
   int leaf_tiles = 0;
 };
 
@@ -187,6 +285,8 @@ struct hk_plan {
   std::vector<int64_t> y_off;       // per front (doubles)
   std::vector<NodeRec> rec;         // batch * nodes
   DevBuf Y, Ytmp, F, I, ftask_d, fmap_d, gj_d, gj2_d, gjs_d;
+  Staging stage;                    // pinned task arena of the current build / factor call
+  Staging pstage;                   // task arrays of the cached solve programs
   int64_t g_per_col = 0;            // doubles of G/Yv scratch per rhs column (all fronts)
   std::map<std::pair<int, int>, SolveProg*> progs;
   DevBuf Xin, X2, G, Yv;
@@ -196,18 +296,7 @@ struct hk_plan {
 
   int nblocks() const { return (int)blocks.size(); }
   ~hk_plan() {
-    for (auto& kv : progs) {
-      SolveProg* p = kv.second;
-      p->leaf_t.release();
-      p->leaf_g.release();
-      p->leaf_map.release();
-      for (auto& l : p->levels) {
-        l.dot_t.release(); l.sinv_t.release(); l.upd_t.release();
-        l.g1.release(); l.g1map.release(); l.g2.release(); l.g2map.release();
-        l.g3.release(); l.g3map.release();
-      }
-      delete p;
-    }
+    for (auto& kv : progs) delete kv.second;
     for (auto& x : side)
       if (x) cudaStreamDestroy(x);
     for (auto& x : side_ev)
@@ -216,6 +305,8 @@ struct hk_plan {
                       &skel_status_d, &probe_d, &Y, &Ytmp, &F, &I, &ftask_d, &fmap_d, &gj_d, &gj2_d, &gjs_d,
                       &Xin, &X2, &G, &Yv};
     for (DevBuf* b : bufs) b->release();
+    stage.release();
+    pstage.release();
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
   }
@@ -363,18 +454,11 @@ extern "C" hk_status hk_block_shape(const hk_plan* p, int64_t block, int64_t* m,
   return HK_OK;
 }
 
+// callers synchronise the stream first: the programs' task arrays are reused
 static void drop_progs(hk_plan* p) {
-  for (auto& kv : p->progs) {
-    SolveProg* sp = kv.second;
-    sp->leaf_t.release(); sp->leaf_g.release(); sp->leaf_map.release();
-    for (auto& l : sp->levels) {
-      l.dot_t.release(); l.sinv_t.release(); l.upd_t.release();
-      l.g1.release(); l.g1map.release(); l.g2.release(); l.g2map.release();
-      l.g3.release(); l.g3map.release();
-    }
-    delete sp;
-  }
+  for (auto& kv : p->progs) delete kv.second;
   p->progs.clear();
+  p->pstage.reset();
 }
 
 static hk_status ensure_side_streams(hk_plan* p) {
@@ -435,6 +519,7 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
   if (!p) return fail(HK_ERR_VALUE, "null plan");
   if (!(tol > 0.0 && tol < 1.0)) return fail(HK_ERR_VALUE, "tol must lie strictly between 0 and 1");
   cudaStream_t st = (cudaStream_t)stream;
+  HostClock hc("build_aca");
   CHK(prepare_build(p, A, ld, fstride, max_rank, st));
   CHK(timed_begin(p, st));
   const int64_t n = p->n;
@@ -504,7 +589,10 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
     CU(clk.ensure(tasks.size() * 24 + 8, st));
     for (size_t i = 0; i < tasks.size(); ++i) tasks[i].clock = clk.as<int64_t>() + 3 * i;
   }
-  CU(upload(p->tasks_d, tasks, st));
+  p->stage.reset();
+  const AcaTask* tasks_dev = p->stage.push(tasks, st);
+  if (!tasks_dev) return fail(HK_ERR_CUDA, "pinned staging allocation failed");
+  CU(p->stage.commit(st));
   if ((size_t)(max_cap + 16) * 8 + max_m + 1024 > 220 * 1024)
     return fail(HK_ERR_VALUE, "block too large for the single-CTA ACA kernel");
   int cls_begin[5] = {0, 0, 0, 0, 0}, cls_cap[4] = {0, 0, 0, 0}, cls_m[4] = {0, 0, 0, 0};
@@ -524,14 +612,16 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
     ss[c] = p->side[c];
     CU(cudaStreamWaitEvent(ss[c], p->ev[3], 0));
   }
-  CU(hk_launch_aca_classes(p->tasks_d.as<AcaTask>(), cls_begin, cls_cap, cls_m, tol2,
+  CU(hk_launch_aca_classes(tasks_dev, cls_begin, cls_cap, cls_m, tol2,
                            p->aca_cnt.as<int>(), ss));
   for (int c = 0; c < 4; ++c) {   // join
     CU(cudaEventRecord(p->side_ev[c], ss[c]));
     CU(cudaStreamWaitEvent(st, p->side_ev[c], 0));
   }
   CU(cudaEventRecord(p->ev[1], st));
+  hc.mark("plan+launch");
   CHK(fetch_ranks(p, st));
+  hc.mark("wait");
   if (prof) {
     std::vector<int64_t> h(tasks.size() * 3);
     CU(cudaMemcpy(h.data(), clk.p, h.size() * 8, cudaMemcpyDeviceToHost));
@@ -799,11 +889,24 @@ struct TileList {
   int ntiles() const { return (int)(map.size() / 3); }
 };
 
-static hk_status run_tiles(TileList& tl, DevBuf& tb, DevBuf& mb, cudaStream_t st) {
+// A factorization phase is planned on the host into a list of ops whose task
+// arrays live in the pinned staging; flush() commits and launches them.
+struct Op {
+  enum Kind { COPY, GEMM, GJ, EVENT } kind;
+  const void* a = nullptr;   // device task array
+  const int32_t* map = nullptr;
+  int n = 0, maxN = 0;       // tasks / tiles, largest GJ order
+  int ev = 0;
+};
+
+static hk_status stage_tiles(hk_plan* p, std::vector<Op>& ops, const TileList& tl, cudaStream_t st) {
   if (tl.ntiles() == 0) return HK_OK;
-  CU(upload(tb, tl.tasks, st));
-  CU(upload(mb, tl.map, st));
-  CU(hk_launch_gemm(tb.as<GemmTask>(), mb.as<int32_t>(), tl.ntiles(), st));
+  Op o{Op::GEMM};
+  o.a = p->stage.push(tl.tasks, st);
+  o.map = p->stage.push(tl.map, st);
+  if (!o.a || !o.map) return fail(HK_ERR_CUDA, "pinned staging allocation failed");
+  o.n = tl.ntiles();
+  ops.push_back(o);
   return HK_OK;
 }
 
@@ -820,9 +923,11 @@ static GemmTask gemm(const double* A, int64_t lda, int transA, const double* B, 
   return t;
 }
 
-// Run batched Gauss-Jordan inversions, SMEM-resident tasks and large tasks
-// (global scratch) in separate launches.
-static hk_status run_gj(hk_plan* p, std::vector<GjTask>& tasks, cudaStream_t st) {
+// Batched Gauss-Jordan inversions: SMEM/register-resident tasks and large
+// tasks (global scratch at p->gjs_d, shared by every stage since the stages
+// run in stream order) in separate launches.
+static hk_status stage_gj(hk_plan* p, std::vector<Op>& ops, std::vector<GjTask>& tasks,
+                          cudaStream_t st) {
   if (tasks.empty()) return HK_OK;
   std::vector<GjTask> small, large;
   size_t scratch = 0;
@@ -830,18 +935,38 @@ static hk_status run_gj(hk_plan* p, std::vector<GjTask>& tasks, cudaStream_t st)
   for (auto& t : tasks) {
     size_t b = hk_gj_scratch_bytes(t.N);
     if (b == 0) { small.push_back(t); ms = std::max(ms, t.N); }
-    else { t.scratch = (double*)(uintptr_t)scratch; scratch += (b + 255) / 256 * 256; large.push_back(t); ml = std::max(ml, t.N); }
+    else {
+      t.scratch = (double*)(p->gjs_d.as<char>() + scratch);
+      scratch += (b + 255) / 256 * 256;
+      large.push_back(t);
+      ml = std::max(ml, t.N);
+    }
   }
-  if (!small.empty()) {
-    CU(upload(p->gj_d, small, st));
-    CU(hk_launch_gj(p->gj_d.as<GjTask>(), (int)small.size(), ms, st));
+  if (scratch > p->gjs_d.bytes) return fail(HK_ERR_STATE, "internal: GJ scratch undersized");
+  for (auto* v : {&small, &large}) {
+    if (v->empty()) continue;
+    Op o{Op::GJ};
+    o.a = p->stage.push(*v, st);
+    if (!o.a) return fail(HK_ERR_CUDA, "pinned staging allocation failed");
+    o.n = (int)v->size();
+    o.maxN = v == &small ? ms : ml;
+    ops.push_back(o);
   }
-  if (!large.empty()) {
-    CU(p->gjs_d.ensure(scratch + 256, st));
-    for (auto& t : large) t.scratch = (double*)(p->gjs_d.as<char>() + (uintptr_t)t.scratch);
-    CU(upload(p->gj2_d, large, st));
-    CU(hk_launch_gj(p->gj2_d.as<GjTask>(), (int)large.size(), ml, st));
+  return HK_OK;
+}
+
+// commit the staged task arrays and launch the ops planned so far
+static hk_status flush(hk_plan* p, std::vector<Op>& ops, cudaStream_t st) {
+  CU(p->stage.commit(st));
+  for (const Op& o : ops) {
+    switch (o.kind) {
+      case Op::COPY: CU(hk_launch_copy((const CopyTask*)o.a, o.n, st)); break;
+      case Op::GEMM: CU(hk_launch_gemm((const GemmTask*)o.a, o.map, o.n, st)); break;
+      case Op::GJ: CU(hk_launch_gj((const GjTask*)o.a, o.n, o.maxN, st)); break;
+      case Op::EVENT: CU(cudaEventRecord(p->ev[o.ev], st)); break;
+    }
   }
+  ops.clear();
   return HK_OK;
 }
 
@@ -856,6 +981,7 @@ extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
     drop_progs(p);
   }
   p->factored = false;
+  HostClock hc("factor");
   CHK(ensure_events(p));
   CU(cudaEventRecord(p->ev[0], st));
   // ---- widths and storage layout
@@ -903,6 +1029,30 @@ extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
   CU(p->F.ensure((size_t)ftot * 8 + 8, st));
   CU(p->I.ensure((size_t)itot * 4 + 4, st));
   CU(cudaMemsetAsync(p->I.p, 0, (size_t)itot * 4 + 4, st));
+  // large Gauss-Jordan scratch: the largest single stage (stages run in order)
+  {
+    size_t need = 0, leaf_need = 0;
+    for (int s : p->leaves) {
+      const size_t b = hk_gj_scratch_bytes((int)(p->nodes[s].hi - p->nodes[s].lo));
+      leaf_need += (b + 255) / 256 * 256;
+    }
+    need = leaf_need * p->batch;
+    for (int lvl = 0; lvl < p->depth; ++lvl) {
+      size_t lv = 0;
+      for (int64_t f = 0; f < p->batch; ++f)
+        for (int s : p->internal) {
+          if (p->nodes[s].level != lvl) continue;
+          const NodeRec& r = p->rec[f * nn + s];
+          if (r.R == 0) continue;
+          const size_t b = hk_gj_scratch_bytes(std::min(r.ru, r.rl));
+          lv += (b + 255) / 256 * 256;
+        }
+      need = std::max(need, lv);
+    }
+    if (need) CU(p->gjs_d.ensure(need + 256, st));
+  }
+  p->stage.reset();
+  std::vector<Op> ops;
   double* Y = p->Y.as<double>();
   double* Yt = p->Ytmp.as<double>();
   double* F = p->F.as<double>();
@@ -931,8 +1081,13 @@ extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
         copies.push_back(c);
       }
     }
-  CU(upload(p->ftask_d, copies, st));
-  CU(hk_launch_copy(p->ftask_d.as<CopyTask>(), (int)copies.size(), st));
+  if (!copies.empty()) {
+    Op o{Op::COPY};
+    o.a = p->stage.push(copies, st);
+    if (!o.a) return fail(HK_ERR_CUDA, "pinned staging allocation failed");
+    o.n = (int)copies.size();
+    ops.push_back(o);
+  }
 
   // ---- leaves: Gauss-Jordan inverse, then Y = K^{-1} Z (hodlr.py:222-232)
   {
@@ -951,7 +1106,7 @@ extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
         t.mode = 0;
         gts.push_back(t);
       }
-    CHK(run_gj(p, gts, st));
+    CHK(stage_gj(p, ops, gts, st));
     TileList tl;
     for (int64_t f = 0; f < p->batch; ++f)
       for (int s : p->leaves) {
@@ -962,9 +1117,15 @@ extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
         tl.add(gemm(F + r.inv, b, 0, Yt + p->y_off[f] + nd.lo, n, Y + p->y_off[f] + nd.lo, n, b,
                     (int)r.w, b, 1.0, 0.0));
       }
-    CHK(run_tiles(tl, p->fmap_d, p->tasks_d, st));
+    CHK(stage_tiles(p, ops, tl, st));
   }
-  CU(cudaEventRecord(p->ev[1], st));
+  {
+    Op o{Op::EVENT};
+    o.ev = 1;
+    ops.push_back(o);
+  }
+  hc.mark("plan leaves");
+  CHK(flush(p, ops, st));        // the GPU starts on the leaves while the levels are planned
 
   // ---- upward sweep, deepest internal level first (hodlr.py:264-282).
   // The coupling system S = [[I, X], [Y, I]] (X = V_low^T d_left, Y = V_up^T
@@ -1031,19 +1192,22 @@ extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
           if (rl > 0) tu.add(gemm(Yf + b.lo + (int64_t)w * n, n, 0, Q, R, Yf + b.lo, n, nbr, w, rl, -1.0, 1.0));
         }
       }
-    CHK(run_tiles(th, p->fmap_d, p->tasks_d, st));
-    CHK(run_tiles(tm, p->fmap_d, p->tasks_d, st));
-    CHK(run_gj(p, gts, st));
-    CHK(run_tiles(t4, p->fmap_d, p->tasks_d, st));
-    CHK(run_tiles(t5, p->fmap_d, p->tasks_d, st));
-    CHK(run_tiles(tq, p->fmap_d, p->tasks_d, st));
-    CHK(run_tiles(tu, p->fmap_d, p->tasks_d, st));
+    CHK(stage_tiles(p, ops, th, st));
+    CHK(stage_tiles(p, ops, tm, st));
+    CHK(stage_gj(p, ops, gts, st));
+    CHK(stage_tiles(p, ops, t4, st));
+    CHK(stage_tiles(p, ops, t5, st));
+    CHK(stage_tiles(p, ops, tq, st));
+    CHK(stage_tiles(p, ops, tu, st));
+    CHK(flush(p, ops, st));
   }
   CU(cudaEventRecord(p->ev[2], st));
+  hc.mark("plan+launch levels");
   // ---- statuses: first failure in the reference's DFS event order
   std::vector<int32_t> ih((size_t)itot);
   if (itot) CU(cudaMemcpyAsync(ih.data(), I, (size_t)itot * 4, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
+  hc.mark("wait");
   float ms1 = 0, ms2 = 0;
   CU(cudaEventElapsedTime(&ms1, p->ev[0], p->ev[1]));
   CU(cudaEventElapsedTime(&ms2, p->ev[1], p->ev[2]));
@@ -1214,11 +1378,13 @@ static hk_status build_solve_prog(hk_plan* p, int front, int s, SolveProg*& out,
       }
     if (sp->small) {
       sp->n_leaf = (int)mv.size();
-      CU(upload(sp->leaf_t, mv, st));
+      sp->leaf_t = p->pstage.push(mv, st);
+      if (!sp->leaf_t) { delete sp; return fail(HK_ERR_CUDA, "pinned staging allocation failed"); }
     } else {
       sp->leaf_tiles = tl.ntiles();
-      CU(upload(sp->leaf_g, tl.tasks, st));
-      CU(upload(sp->leaf_map, tl.map, st));
+      sp->leaf_g = p->pstage.push(tl.tasks, st);
+      sp->leaf_map = p->pstage.push(tl.map, st);
+      if (!sp->leaf_g || !sp->leaf_map) { delete sp; return fail(HK_ERR_CUDA, "pinned staging allocation failed"); }
     }
   }
   for (int lvl = p->depth - 1; lvl >= 0; --lvl) {
@@ -1268,20 +1434,25 @@ static hk_status build_solve_prog(hk_plan* p, int front, int s, SolveProg*& out,
           if (rl > 0) t3.add(gemm(dright, n, 0, yv, R, Xf + b.lo, n, nbr, s, rl, -1.0, 1.0));
         }
       }
+    bool ok = true;
     if (sp->small) {
       L.n_dot = (int)dt.size(); L.n_sinv = (int)sv.size(); L.n_upd = (int)up.size();
-      CU(upload(L.dot_t, dt, st));
-      CU(upload(L.sinv_t, sv, st));
-      CU(upload(L.upd_t, up, st));
+      L.dot_t = p->pstage.push(dt, st);
+      L.sinv_t = p->pstage.push(sv, st);
+      L.upd_t = p->pstage.push(up, st);
+      ok = L.dot_t && L.sinv_t && L.upd_t;
     } else {
       L.t1 = t1.ntiles(); L.t2 = t2.ntiles(); L.t3 = t3.ntiles();
-      CU(upload(L.g1, t1.tasks, st)); CU(upload(L.g1map, t1.map, st));
-      CU(upload(L.g2, t2.tasks, st)); CU(upload(L.g2map, t2.map, st));
-      CU(upload(L.g3, t3.tasks, st)); CU(upload(L.g3map, t3.map, st));
+      L.g1 = p->pstage.push(t1.tasks, st); L.g1map = p->pstage.push(t1.map, st);
+      L.g2 = p->pstage.push(t2.tasks, st); L.g2map = p->pstage.push(t2.map, st);
+      L.g3 = p->pstage.push(t3.tasks, st); L.g3map = p->pstage.push(t3.map, st);
+      ok = L.g1 && L.g1map && L.g2 && L.g2map && L.g3 && L.g3map;
     }
+    if (!ok) { delete sp; return fail(HK_ERR_CUDA, "pinned staging allocation failed"); }
     sp->levels.push_back(std::move(L));
   }
   (void)nb;
+  CU(p->pstage.commit(st));
   p->progs[key] = sp;
   out = sp;
   return HK_OK;
@@ -1308,33 +1479,48 @@ static hk_status run_solve(hk_plan* p, int front, double* rhs, int64_t ld, int64
   if (s <= 0) return HK_OK;
   const int64_t n = p->n;
   if (ld < n) return fail(HK_ERR_DIMENSION, "rhs leading dimension smaller than n");
+  HostClock hc("solve");
   CHK(ensure_solve_scratch(p, (int)s, st));
   SolveProg* sp = nullptr;
   CHK(build_solve_prog(p, front, (int)s, sp, st));
+  hc.mark("prog");
   const int64_t xs = n * s;
   const int64_t f0 = front < 0 ? 0 : front, f1 = front < 0 ? p->batch : front + 1;
-  for (int64_t f = f0; f < f1; ++f)
-    CU(cudaMemcpy2DAsync(p->Xin.as<double>() + f * xs, n * 8, rhs + (f - f0) * rhs_stride, ld * 8,
-                         n * 8, s, cudaMemcpyDeviceToDevice, st));
-  if (sp->small) {
-    CU(hk_launch_matvec(sp->leaf_t.as<MatVecTask>(), sp->n_leaf, (int)s, sp->leaf_rows, st, sp->leaf_k));
+  // one copy when the fronts' rhs blocks are packed like Xin (ld = n, stride = n*s)
+  const bool packed = ld == n && (f1 - f0 == 1 || rhs_stride == xs);
+  if (packed) {
+    CU(cudaMemcpyAsync(p->Xin.as<double>() + f0 * xs, rhs, (size_t)(f1 - f0) * xs * 8,
+                       cudaMemcpyDeviceToDevice, st));
   } else {
-    if (sp->leaf_tiles) CU(hk_launch_gemm(sp->leaf_g.as<GemmTask>(), sp->leaf_map.as<int32_t>(), sp->leaf_tiles, st));
+    for (int64_t f = f0; f < f1; ++f)
+      CU(cudaMemcpy2DAsync(p->Xin.as<double>() + f * xs, n * 8, rhs + (f - f0) * rhs_stride, ld * 8,
+                           n * 8, s, cudaMemcpyDeviceToDevice, st));
+  }
+  if (sp->small) {
+    CU(hk_launch_matvec(sp->leaf_t, sp->n_leaf, (int)s, sp->leaf_rows, st, sp->leaf_k));
+  } else {
+    if (sp->leaf_tiles) CU(hk_launch_gemm(sp->leaf_g, sp->leaf_map, sp->leaf_tiles, st));
   }
   for (auto& L : sp->levels) {
     if (sp->small) {
-      CU(hk_launch_dot(L.dot_t.as<DotTask>(), L.n_dot, (int)s, L.dot_cols, st));
-      CU(hk_launch_matvec(L.sinv_t.as<MatVecTask>(), L.n_sinv, (int)s, L.sinv_rows, st, L.sinv_k));
-      CU(hk_launch_matvec(L.upd_t.as<MatVecTask>(), L.n_upd, (int)s, L.upd_rows, st, L.upd_k));
+      CU(hk_launch_dot(L.dot_t, L.n_dot, (int)s, L.dot_cols, st));
+      CU(hk_launch_matvec(L.sinv_t, L.n_sinv, (int)s, L.sinv_rows, st, L.sinv_k));
+      CU(hk_launch_matvec(L.upd_t, L.n_upd, (int)s, L.upd_rows, st, L.upd_k));
     } else {
-      if (L.t1) CU(hk_launch_gemm(L.g1.as<GemmTask>(), L.g1map.as<int32_t>(), L.t1, st));
-      if (L.t2) CU(hk_launch_gemm(L.g2.as<GemmTask>(), L.g2map.as<int32_t>(), L.t2, st));
-      if (L.t3) CU(hk_launch_gemm(L.g3.as<GemmTask>(), L.g3map.as<int32_t>(), L.t3, st));
+      if (L.t1) CU(hk_launch_gemm(L.g1, L.g1map, L.t1, st));
+      if (L.t2) CU(hk_launch_gemm(L.g2, L.g2map, L.t2, st));
+      if (L.t3) CU(hk_launch_gemm(L.g3, L.g3map, L.t3, st));
     }
   }
-  for (int64_t f = f0; f < f1; ++f)
-    CU(cudaMemcpy2DAsync(rhs + (f - f0) * rhs_stride, ld * 8, p->X2.as<double>() + f * xs, n * 8,
-                         n * 8, s, cudaMemcpyDeviceToDevice, st));
+  if (packed) {
+    CU(cudaMemcpyAsync(rhs, p->X2.as<double>() + f0 * xs, (size_t)(f1 - f0) * xs * 8,
+                       cudaMemcpyDeviceToDevice, st));
+  } else {
+    for (int64_t f = f0; f < f1; ++f)
+      CU(cudaMemcpy2DAsync(rhs + (f - f0) * rhs_stride, ld * 8, p->X2.as<double>() + f * xs, n * 8,
+                           n * 8, s, cudaMemcpyDeviceToDevice, st));
+  }
+  hc.mark("launch");
   return HK_OK;
 }
 

@@ -22,7 +22,7 @@ OURS = ("aca_kernel", "gemm_kernel", "gj_", "matvec_kernel", "dot_kernel", "tran
 
 def short(name: str) -> str:
     name = re.sub(r"^void ", "", name)
-    name = re.sub(r"\(anonymous namespace\)::", "", name)
+    name = re.sub(r"\(anonymous namespace\)::|<unnamed>::", "", name)
     depth, out = 0, []
     for ch in name:                     # drop the argument list, keep template args
         if ch == "(" and depth == 0:
