@@ -955,16 +955,45 @@ static hk_status stage_gj(hk_plan* p, std::vector<Op>& ops, std::vector<GjTask>&
   return HK_OK;
 }
 
+// HK_HOST_PROFILE: an event after every launched op gives in-situ per-op GPU
+// times (kernel + any idle gap before it) for the factorization.
+struct OpProfile {
+  std::vector<cudaEvent_t> ev;
+  std::vector<std::string> label;
+  size_t used = 0;
+  void reset() { used = 0; label.clear(); }
+  void mark(const std::string& l, cudaStream_t st) {
+    if (used == ev.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev.push_back(e);
+    }
+    cudaEventRecord(ev[used++], st);
+    label.push_back(l);
+  }
+  void print(const char* what) {
+    for (size_t i = 1; i < used; ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      fprintf(stderr, "[hk gpu] %s %-28s %8.1f us\n", what, label[i].c_str(), ms * 1e3);
+    }
+  }
+};
+static OpProfile g_opprof;
+
 // commit the staged task arrays and launch the ops planned so far
 static hk_status flush(hk_plan* p, std::vector<Op>& ops, cudaStream_t st) {
   CU(p->stage.commit(st));
+  const bool prof = host_profile();
   for (const Op& o : ops) {
+    char lbl[64] = "";
     switch (o.kind) {
-      case Op::COPY: CU(hk_launch_copy((const CopyTask*)o.a, o.n, st)); break;
-      case Op::GEMM: CU(hk_launch_gemm((const GemmTask*)o.a, o.map, o.n, st)); break;
-      case Op::GJ: CU(hk_launch_gj((const GjTask*)o.a, o.n, o.maxN, st)); break;
+      case Op::COPY: CU(hk_launch_copy((const CopyTask*)o.a, o.n, st)); snprintf(lbl, 64, "copy x%d", o.n); break;
+      case Op::GEMM: CU(hk_launch_gemm((const GemmTask*)o.a, o.map, o.n, st)); snprintf(lbl, 64, "gemm %d tiles", o.n); break;
+      case Op::GJ: CU(hk_launch_gj((const GjTask*)o.a, o.n, o.maxN, st)); snprintf(lbl, 64, "gj x%d N<=%d", o.n, o.maxN); break;
       case Op::EVENT: CU(cudaEventRecord(p->ev[o.ev], st)); break;
     }
+    if (prof && lbl[0]) g_opprof.mark(lbl, st);
   }
   ops.clear();
   return HK_OK;
@@ -984,6 +1013,10 @@ extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
   HostClock hc("factor");
   CHK(ensure_events(p));
   CU(cudaEventRecord(p->ev[0], st));
+  if (host_profile()) {
+    g_opprof.reset();
+    g_opprof.mark("start", st);
+  }
   // ---- widths and storage layout
   p->W.assign(p->batch, 0);
   p->y_off.assign(p->batch, 0);
@@ -1208,6 +1241,7 @@ extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
   if (itot) CU(cudaMemcpyAsync(ih.data(), I, (size_t)itot * 4, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
   hc.mark("wait");
+  if (host_profile()) g_opprof.print("factor");
   float ms1 = 0, ms2 = 0;
   CU(cudaEventElapsedTime(&ms1, p->ev[0], p->ev[1]));
   CU(cudaEventElapsedTime(&ms2, p->ev[1], p->ev[2]));

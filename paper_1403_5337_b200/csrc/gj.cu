@@ -1,10 +1,13 @@
 // Batched Gauss-Jordan inversion with partial pivoting (leaf blocks and the
 // r x r Woodbury capacitance matrices I - Y X of the coupling systems).
 //
-// One CTA per matrix; the matrix lives in SMEM when it fits (N <= 165), else
-// in a global scratch (L2 resident).  Each elimination step is one rank-1
-// update of the whole N x N array, column-major with the row index fastest
-// so SMEM accesses are conflict-free and global accesses coalesced.
+// One CTA per matrix.  N <= 160: the matrix is held in registers, distributed
+// over the warps by column blocks (gj_df_kernel / gj_blk_kernel below).
+// Larger N (config 4's top levels): gj_kernel keeps the matrix in SMEM or a
+// global scratch and applies one rank-1 update per elimination step.  Pivoting
+// is partial (largest |entry| among rows not yet used, lowest row on ties), so
+// the singularity test min|pivot| < 1e-300 is the reference's
+// (src/dense.py:76-77).
 #include "hk_common.cuh"
 #include "hk_internal.h"
 
@@ -19,128 +22,134 @@ __host__ __device__ inline size_t gj_bytes(int N) {
   return (size_t)N * N * 8 + (size_t)2 * N * 8 + (size_t)2 * N * 4;
 }
 
-// Register-resident Gauss-Jordan, N <= min(NW*CPW, 32*RPL).  The matrix is
-// distributed column-cyclically: warp w holds columns j = w + NW*jj (jj < CPW),
-// lane l holds rows i = l + 32*q (q < RPL), so W[i][j] lives in w_[jj][q] of
-// warp j%NW / lane i%32.  Pivoting is implicit (no physical row swaps): step k
-// takes the largest |W[i][k]| over rows not yet used as pivots (ties: lowest
-// row), so the pivot magnitudes are those of LU with partial pivoting and the
-// singularity test min|pivot| < 1e-300 is the reference's (dense.py:76-77).
-// With pivot rows p_k the result satisfies A^{-1}[i][c] = W[p_i][q(c)],
-// q = p^{-1}, applied by the final gather.  Per step: the owner warp of
-// column k finds the pivot (shuffles), the lane holding row p publishes the
-// scaled pivot row; every warp updates its columns in registers (one DFMA +
-// one select per element).  Two barriers per step, double-buffered SMEM.
+// Panel-blocked Gauss-Jordan (same implicit partial pivoting, same per-element
+// arithmetic and order as the unblocked elimination, so bit-identical results).  Warp w
+// owns the CPW consecutive columns j = w*CPW + jj; lane l holds rows
+// l + 32q.  Panel P is the column block of warp P: that warp alone runs the CPW
+// pivot steps of its panel (warp-synchronous, no CTA barrier), saving for every
+// step the pre-step pivot column and 1/pivot in SMEM; after ONE CTA barrier
+// every other warp replays the CPW steps on its own columns (pivot-row entries
+// broadcast by shuffle from the lane that holds the row).  N/CPW barriers per
+// matrix instead of N.  Per pivot step: the used-row mask lives in registers
+// (every warp sees every pivot), the search is three REDUX reductions
+// (warp_argmax_idx), and each lane computes the reciprocal of its own
+// candidate while the reduction runs.  Every branch is on values ptxas can
+// prove warp-uniform, so no shuffle takes the divergent-warp fallback.
 template <int NW, int CPW, int RPL>
-__global__ void __launch_bounds__(NW * 32, 1) gj_reg_kernel(const GjTask* __restrict__ tasks) {
+__global__ void __launch_bounds__(NW * 32, 1) gj_blk_kernel(const GjTask* __restrict__ tasks) {
   constexpr int NT = NW * 32;
+  constexpr int NR = 32 * RPL;
   const GjTask t = tasks[blockIdx.x];
-  const int N = t.N;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  extern __shared__ __align__(16) double gsm[];   // stage N*N, colk[2][N], rowk[2][N]
-  double* stage = gsm;
-  double* colk = stage + N * N;
-  double* rowk = colk + 2 * N;
-  __shared__ int s_p[2], s_sing, pivrow[32 * RPL], invp[32 * RPL];
-  __shared__ double s_rinv[2];
-  __shared__ unsigned char usedrow[32 * RPL];
+  const int N = __shfl_sync(0xffffffffu, t.N, 0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = uniform_warp_id();
+  __shared__ double ckbuf[2][CPW][NR];
+  __shared__ double rinvbuf[2][CPW];
+  __shared__ int pbuf[2][CPW];
+  __shared__ int s_sing, pivrow[NR], invp[NR];
   if (N == 0) {
     if (tid == 0) *t.status = 0;
     return;
   }
-  // load through SMEM (coalesced), then into registers
-  if (t.mode == 0) {
-    for (int i = warp; i < N; i += NW)
-      for (int j = lane; j < N; j += 32) stage[i + j * N] = t.src[(int64_t)i * t.src_ld + j];
-  } else {
-    for (int j = warp; j < N; j += NW)
-      for (int i = lane; i < N; i += 32) stage[i + j * N] = t.src[i + (int64_t)j * t.src_ld];
-  }
-  for (int i = tid; i < 32 * RPL; i += NT) usedrow[i] = 0;
-  if (tid == 0) s_sing = 0;
-  __syncthreads();
   double w_[CPW][RPL];
 #pragma unroll
   for (int jj = 0; jj < CPW; ++jj)
 #pragma unroll
     for (int q = 0; q < RPL; ++q) {
-      const int i = lane + 32 * q, j = warp + NW * jj;
-      w_[jj][q] = (i < N && j < N) ? stage[i + j * N] : 0.0;
+      const int i = lane + 32 * q, j = warp * CPW + jj;
+      const bool in = i < N && j < N;
+      const int64_t off = t.mode == 0 ? (int64_t)i * t.src_ld + j : i + (int64_t)j * t.src_ld;
+      w_[jj][q] = in ? t.src[off] : 0.0;
     }
-  // k = w + NW*kk: the column slot kk of the owner warp is a compile-time
-  // constant inside the unrolled kk loop (no register-array select chains)
+  unsigned used = 0;                     // bit q: row lane + 32q already a pivot row
+  if (tid == 0) s_sing = 0;
+  __syncthreads();
+  const int npan = (N + CPW - 1) / CPW;
+  for (int P = 0; P < npan; ++P) {
+    const int buf = P & 1;
+    const int nl = min(CPW, N - P * CPW);
+    if (warp == P) {
+      int sing = 0;
 #pragma unroll
-  for (int kk = 0; kk < CPW; ++kk) {
-    for (int w = 0; w < NW; ++w) {
-      const int k = w + NW * kk;
-      if (k >= N) break;
-      const int buf = k & 1;
-      double* ck_s = colk + buf * N;
-      double* rk_s = rowk + buf * N;
-      if (warp == w) {                // owner of column k: pivot over unused rows
-        ArgMax a{0.0, -1};
+      for (int l = 0; l < CPW; ++l) {
+        if (l >= nl) break;
+        const int c = P * CPW + l;
+        // lane-local best over its unused rows (lowest q on ties), its
+        // reciprocal computed while the warp reduction runs
+        double bv = 0.0, bw = 1.0;
+        int bi = 0x7fffffff;
+        bool have = false;
 #pragma unroll
         for (int q = 0; q < RPL; ++q) {
           const int i = lane + 32 * q;
-          if (i < N) {
-            ck_s[i] = w_[kk][q];
-            if (!usedrow[i]) {
-              const double av = fabs(w_[kk][q]);
-              if (argmax_better(av, i, a.v, a.i)) { a.v = av; a.i = i; }
+          const double av = fabs(w_[l][q]);
+          if (i < N && !((used >> q) & 1u) && (!have || av > bv)) {
+            bv = av; bw = w_[l][q]; bi = i; have = true;
+          }
+        }
+        const double myrinv = __drcp_rn(bw);
+        const int p = warp_argmax_idx(bv, have, bi);
+        const int lp = p & 31, qp = p >> 5;
+        const double pivabs = __shfl_sync(0xffffffffu, bv, lp);
+        if (!(pivabs >= HK_PIVOT_FLOOR)) { sing = 1; break; }
+        const double rinv = __shfl_sync(0xffffffffu, myrinv, lp);
+        double ck[RPL];
+        bool isp[RPL];
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+          const int i = lane + 32 * q;
+          ck[q] = w_[l][q];
+          isp[q] = i == p;
+          if (i < N) ckbuf[buf][l][i] = ck[q];
+        }
+        if (lane == lp) used |= 1u << qp;
+        if (lane == 0) {
+          rinvbuf[buf][l] = rinv;
+          pbuf[buf][l] = p;
+          pivrow[c] = p;
+        }
+#pragma unroll
+        for (int jj = 0; jj < CPW; ++jj) {
+          if (jj == l) {
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) w_[jj][q] = isp[q] ? rinv : -ck[q] * rinv;
+          } else {
+            double src = w_[jj][0];
+#pragma unroll
+            for (int q = 1; q < RPL; ++q) src = (qp == q) ? w_[jj][q] : src;
+            const double rj = __shfl_sync(0xffffffffu, src, lp) * rinv;
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) {
+              const double v = fma(-ck[q], rj, w_[jj][q]);
+              w_[jj][q] = isp[q] ? rj : v;
             }
           }
         }
-        a = warp_argmax(a);
-        if (lane == 0) {
-          const int p = (int)a.i;
-          s_p[buf] = p;
-          if (!(a.v >= HK_PIVOT_FLOOR)) s_sing = 1;
-          else {
-            usedrow[p] = 1;
-            pivrow[k] = p;
-          }
+      }
+      if (sing && lane == 0) s_sing = 1;
+    }
+    __syncthreads();
+    if (__shfl_sync(0xffffffffu, s_sing, 0)) break;
+    if (warp != P) {
+#pragma unroll 1
+      for (int l = 0; l < nl; ++l) {
+        const int p = __shfl_sync(0xffffffffu, pbuf[buf][l], 0);
+        const double rinv = rinvbuf[buf][l];
+        const int qp = p >> 5, lp = p & 31;
+        if (lane == lp) used |= 1u << qp;
+        double ck[RPL];
+        bool isp[RPL];
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+          const int i = lane + 32 * q;
+          ck[q] = (i < N) ? ckbuf[buf][l][i] : 0.0;
+          isp[q] = i == p;
         }
-      }
-      __syncthreads();
-      if (s_sing) break;
-      const int p = s_p[buf];
-      const double rinv = 1.0 / ck_s[p];
-      // pivot row of this warp's columns, published by the lane that holds row p
-      const int qp = p >> 5;
-      if (lane == (p & 31)) {
-        switch (qp) {   // warp-uniform
-#define HK_PUB(Q)                                                         \
-  case Q:                                                                 \
-    if (Q < RPL) {                                                        \
-      _Pragma("unroll") for (int jj = 0; jj < CPW; ++jj) {               \
-        const int j = warp + NW * jj;                                     \
-        if (j < N) rk_s[j] = (j == k) ? rinv : w_[jj][Q < RPL ? Q : 0] * rinv; \
-      }                                                                   \
-    }                                                                     \
-    break;
-          HK_PUB(0) HK_PUB(1) HK_PUB(2) HK_PUB(3) HK_PUB(4) HK_PUB(5) HK_PUB(6) HK_PUB(7)
-#undef HK_PUB
-          default: break;
-        }
-      }
-      __syncthreads();
-      double ck[RPL];
-      bool isp[RPL];
 #pragma unroll
-      for (int q = 0; q < RPL; ++q) {
-        const int i = lane + 32 * q;
-        ck[q] = (i < N) ? ck_s[i] : 0.0;
-        isp[q] = (i == p);
-      }
+        for (int jj = 0; jj < CPW; ++jj) {
+          double src = w_[jj][0];
 #pragma unroll
-      for (int jj = 0; jj < CPW; ++jj) {
-        const int j = warp + NW * jj;
-        if (j >= N) break;
-        const double rj = rk_s[j];
-        if (jj == kk && warp == w) {
-#pragma unroll
-          for (int q = 0; q < RPL; ++q) w_[jj][q] = isp[q] ? rinv : -ck[q] * rinv;
-        } else {
+          for (int q = 1; q < RPL; ++q) src = (qp == q) ? w_[jj][q] : src;
+          const double rj = __shfl_sync(0xffffffffu, src, lp) * rinv;
 #pragma unroll
           for (int q = 0; q < RPL; ++q) {
             const double v = fma(-ck[q], rj, w_[jj][q]);
@@ -150,143 +159,185 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_reg_kernel(const GjTask* __rest
       }
     }
   }
-  if (tid == 0) *t.status = s_sing;
-  if (s_sing) return;
-  // ---- A^{-1}[i][c] = W[p_i][q(c)]
+  const int singular = __shfl_sync(0xffffffffu, s_sing, 0);
+  if (tid == 0) *t.status = singular;
+  if (singular) return;
+  for (int k = tid; k < N; k += NT) invp[pivrow[k]] = k;
+  __syncthreads();
 #pragma unroll
   for (int jj = 0; jj < CPW; ++jj)
 #pragma unroll
     for (int q = 0; q < RPL; ++q) {
-      const int i = lane + 32 * q, j = warp + NW * jj;
-      if (i < N && j < N) stage[i + j * N] = w_[jj][q];
+      const int r = lane + 32 * q, j = warp * CPW + jj;
+      if (r < N && j < N) t.out[invp[r] + (int64_t)pivrow[j] * t.out_ld] = w_[jj][q];
     }
-  for (int k = tid; k < N; k += NT) invp[pivrow[k]] = k;
-  __syncthreads();
-  for (int c = warp; c < N; c += NW) {
-    const int qc = invp[c];
-    double* dst = t.out + (int64_t)c * t.out_ld;
-    for (int i = lane; i < N; i += 32) dst[i] = stage[pivrow[i] + qc * N];
-  }
 }
 
-// SMEM-resident variant, N <= 32*MAXQ: every lane owns rows lane + 32q of the
-// column its warp updates; the pivot column is cached in registers; all SMEM
-// addressing is 32-bit.  Two barriers per elimination step.
-template <int NT, int MAXQ>
-__global__ void __launch_bounds__(NT) gj_smem_kernel(const GjTask* __restrict__ tasks) {
+// Dataflow Gauss-Jordan (no CTA barrier inside the elimination).  Same
+// distribution, pivoting and per-element arithmetic as gj_blk_kernel (bit-
+// identical results).  Every pivot step c is published once -- the pre-step
+// pivot column, the pivot row and 1/pivot, in SMEM slots that are never
+// reused -- followed by a release store of the step counter.  Each warp walks
+// the steps in order: the owner of column c runs the pivot step on its
+// registers and publishes it, every other warp waits for the counter (acquire)
+// and replays the step on its own columns.  The owner of the next panel is
+// therefore never more than one step behind, and the critical path is one
+// pivot search + update per step instead of a CTA barrier per panel.
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+
+template <int NW, int CPW, int RPL>
+__global__ void __launch_bounds__(NW * 32, 1) gj_df_kernel(const GjTask* __restrict__ tasks) {
+  constexpr int NT = NW * 32;
+  constexpr int NR = 32 * RPL;
   const GjTask t = tasks[blockIdx.x];
-  const int N = t.N;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = NT / 32;
-  extern __shared__ __align__(16) double Ws[];   // N*N column-major, then rowk[N], colk[N]
-  double* rowk = Ws + N * N;
-  double* colk = rowk + N;
-  __shared__ int piv[32 * MAXQ];
-  __shared__ int cperm[32 * MAXQ];
-  __shared__ int s_p, s_sing;
-  __shared__ double s_rinv;
+  const int N = __shfl_sync(0xffffffffu, t.N, 0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = uniform_warp_id();
+  extern __shared__ __align__(16) double ckall[];   // [N][NR] pre-step pivot columns
+  __shared__ double rinv_s[NR];
+  __shared__ int p_s[NR], invp[NR];
+  __shared__ int s_pub;                             // number of published steps
   if (N == 0) {
     if (tid == 0) *t.status = 0;
     return;
   }
-  if (t.mode == 0) {
-    for (int i = warp; i < N; i += NW)
-      for (int j = lane; j < N; j += 32) Ws[i + j * N] = t.src[(int64_t)i * t.src_ld + j];
-  } else {
-    for (int j = warp; j < N; j += NW)
-      for (int i = lane; i < N; i += 32) Ws[i + j * N] = t.src[i + (int64_t)j * t.src_ld];
-  }
-  __syncthreads();
-  if (warp == 0) {
-    ArgMax a{0.0, -1};
-    for (int i = lane; i < N; i += 32) {
-      const double v = fabs(Ws[i]);
-      if (argmax_better(v, i, a.v, a.i)) { a.v = v; a.i = i; }
-    }
-    a = warp_argmax(a);
-    if (lane == 0) {
-      s_p = (int)a.i;
-      s_sing = !(a.v >= HK_PIVOT_FLOOR);
-    }
-  }
-  __syncthreads();
-  for (int k = 0; k < N; ++k) {
-    if (s_sing) break;
-    const int p = s_p;
-    for (int j = tid; j < N; j += NT) {
-      const double wk = Ws[k + j * N];
-      const double wp = Ws[p + j * N];
-      rowk[j] = wp;
-      if (p != k) Ws[p + j * N] = wk;
-      if (j == k) s_rinv = 1.0 / wp;
-    }
-    for (int i = tid; i < N; i += NT) {
-      double c;
-      if (i == k) c = 0.0;
-      else if (i == p) c = Ws[k + k * N];
-      else c = Ws[i + k * N];
-      colk[i] = c;
-    }
-    if (tid == 0) piv[k] = p;
-    __syncthreads();
-    const double rinv = s_rinv;
-    double ck[MAXQ];
+  double w_[CPW][RPL];
 #pragma unroll
-    for (int q = 0; q < MAXQ; ++q) {
-      const int i = lane + 32 * q;
-      ck[q] = (i < N) ? colk[i] : 0.0;
-    }
-    for (int j = warp; j < N; j += NW) {
-      double* col = Ws + j * N;
-      if (j == k) {
+  for (int jj = 0; jj < CPW; ++jj)
 #pragma unroll
-        for (int q = 0; q < MAXQ; ++q) {
+    for (int q = 0; q < RPL; ++q) {
+      const int i = lane + 32 * q, j = warp * CPW + jj;
+      const bool in = i < N && j < N;
+      const int64_t off = t.mode == 0 ? (int64_t)i * t.src_ld + j : i + (int64_t)j * t.src_ld;
+      w_[jj][q] = in ? t.src[off] : 0.0;
+    }
+  unsigned used = 0;
+  if (tid == 0) s_pub = 0;
+  __syncthreads();
+  bool singular = false;
+  // walk every step in order (panel-major, so the column slot l is a compile-
+  // time constant for the owner's register accesses)
+  const int npan = (N + CPW - 1) / CPW;
+  for (int P = 0; P < npan; ++P) {
+    if (__shfl_sync(0xffffffffu, (int)singular, 0)) break;
+#pragma unroll
+    for (int l = 0; l < CPW; ++l) {
+      const int c = P * CPW + l;
+      if (c >= N) break;
+      double* ck_s = ckall + (size_t)c * NR;
+      if (warp == P) {
+        double bv = 0.0, bw = 1.0;
+        int bi = 0x7fffffff;
+        bool have = false;
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
           const int i = lane + 32 * q;
-          if (i < N) col[i] = (i == k) ? rinv : -ck[q] * rinv;
+          const double av = fabs(w_[l][q]);
+          if (i < N && !((used >> q) & 1u) && (!have || av > bv)) {
+            bv = av; bw = w_[l][q]; bi = i; have = true;
+          }
         }
-        continue;
-      }
-      const double rj = rowk[j] * rinv;
-      const bool nextcol = (j == k + 1);
-      ArgMax a{0.0, -1};
+        const double myrinv = __drcp_rn(bw);
+        const int p = warp_argmax_idx(bv, have, bi);
+        const int lp = p & 31, qp = p >> 5;
+        const double pivabs = __shfl_sync(0xffffffffu, bv, lp);
+        if (__any_sync(0xffffffffu, !(pivabs >= HK_PIVOT_FLOOR))) {
+          if (lane == 0) {
+            p_s[c] = -1;
+            st_release_cta(&s_pub, c + 1);
+          }
+          singular = true;
+          break;
+        }
+        const double rinv = __shfl_sync(0xffffffffu, myrinv, lp);
+        double ck[RPL];
+        bool isp[RPL];
 #pragma unroll
-      for (int q = 0; q < MAXQ; ++q) {
-        const int i = lane + 32 * q;
-        if (i < N) {
-          const double v = (i == k) ? rj : col[i] - ck[q] * rj;
-          col[i] = v;
-          if (nextcol && i > k) {
-            const double av = fabs(v);
-            if (argmax_better(av, i, a.v, a.i)) { a.v = av; a.i = i; }
+        for (int q = 0; q < RPL; ++q) {
+          const int i = lane + 32 * q;
+          ck[q] = w_[l][q];
+          isp[q] = i == p;
+          if (i < N) ck_s[i] = ck[q];
+        }
+        if (lane == lp) used |= 1u << qp;
+        if (lane == 0) {
+          rinv_s[c] = rinv;
+          p_s[c] = p;
+        }
+        __syncwarp();
+        if (lane == 0) st_release_cta(&s_pub, c + 1);
+#pragma unroll
+        for (int jj = 0; jj < CPW; ++jj) {
+          if (jj == l) {
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) w_[jj][q] = isp[q] ? rinv : -ck[q] * rinv;
+          } else {
+            double src = w_[jj][0];
+#pragma unroll
+            for (int q = 1; q < RPL; ++q) src = (qp == q) ? w_[jj][q] : src;
+            const double rj = __shfl_sync(0xffffffffu, src, lp) * rinv;
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) {
+              const double v = fma(-ck[q], rj, w_[jj][q]);
+              w_[jj][q] = isp[q] ? rj : v;
+            }
+          }
+        }
+      } else {
+        while (__shfl_sync(0xffffffffu, ld_acquire_cta(&s_pub), 0) <= c) {
+        }
+        const int p = __shfl_sync(0xffffffffu, lane == 0 ? p_s[c] : 0, 0);
+        if (p < 0) {
+          singular = true;
+          break;
+        }
+        const double rinv = rinv_s[c];
+        const int qp = p >> 5, lp = p & 31;
+        if (lane == lp) used |= 1u << qp;
+        double ck[RPL];
+        bool isp[RPL];
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+          const int i = lane + 32 * q;
+          ck[q] = (i < N) ? ck_s[i] : 0.0;
+          isp[q] = i == p;
+        }
+#pragma unroll
+        for (int jj = 0; jj < CPW; ++jj) {
+          double src = w_[jj][0];
+#pragma unroll
+          for (int q = 1; q < RPL; ++q) src = (qp == q) ? w_[jj][q] : src;
+          const double rj = __shfl_sync(0xffffffffu, src, lp) * rinv;
+#pragma unroll
+          for (int q = 0; q < RPL; ++q) {
+            const double v = fma(-ck[q], rj, w_[jj][q]);
+            w_[jj][q] = isp[q] ? rj : v;
           }
         }
       }
-      if (nextcol) {
-        a = warp_argmax(a);
-        if (lane == 0) {
-          s_p = (int)a.i;
-          s_sing = !(a.v >= HK_PIVOT_FLOOR);
-        }
-      }
-    }
-    __syncthreads();
-  }
-  if (tid == 0) *t.status = s_sing;
-  if (s_sing) return;
-  if (tid == 0) {
-    for (int j = 0; j < N; ++j) cperm[j] = j;
-    for (int k = N - 1; k >= 0; --k) {
-      const int a = cperm[k];
-      cperm[k] = cperm[piv[k]];
-      cperm[piv[k]] = a;
     }
   }
   __syncthreads();
-  for (int j = warp; j < N; j += NW) {
-    const double* src = Ws + cperm[j] * N;
-    double* dst = t.out + (int64_t)j * t.out_ld;
-    for (int i = lane; i < N; i += 32) dst[i] = src[i];
+  if (singular) {
+    if (tid == 0) *t.status = 1;
+    return;
   }
+  if (tid == 0) *t.status = 0;
+  for (int k = tid; k < N; k += NT) invp[p_s[k]] = k;
+  __syncthreads();
+#pragma unroll
+  for (int jj = 0; jj < CPW; ++jj)
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+      const int r = lane + 32 * q, j = warp * CPW + jj;
+      if (r < N && j < N) t.out[invp[r] + (int64_t)p_s[j] * t.out_ld] = w_[jj][q];
+    }
 }
 
 template <int NT>
@@ -400,24 +451,22 @@ __global__ void __launch_bounds__(NT) gj_kernel(const GjTask* __restrict__ tasks
 
 }  // namespace
 
-template <int NT, int MAXQ>
-static cudaError_t launch_gj_smem(const GjTask* tasks_dev, int ntasks, int maxN, cudaStream_t st) {
-  const size_t smem = (size_t)maxN * maxN * 8 + (size_t)2 * maxN * 8;
-  cudaError_t e = cudaFuncSetAttribute(gj_smem_kernel<NT, MAXQ>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  gj_smem_kernel<NT, MAXQ><<<ntasks, NT, smem, st>>>(tasks_dev);
-  hk_count_launch();
-  return cudaGetLastError();
-}
-
 template <int NW, int CPW, int RPL>
 static cudaError_t launch_gj_reg(const GjTask* tasks_dev, int ntasks, int maxN, cudaStream_t st) {
-  const size_t smem = ((size_t)maxN * maxN + 4 * (size_t)maxN) * 8;
-  cudaError_t e = cudaFuncSetAttribute(gj_reg_kernel<NW, CPW, RPL>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  gj_reg_kernel<NW, CPW, RPL><<<ntasks, NW * 32, smem, st>>>(tasks_dev);
+  if constexpr (CPW * RPL > 32) {   // 512 threads x 128 registers: the dataflow variant would spill
+    gj_blk_kernel<NW, CPW, RPL><<<ntasks, NW * 32, 0, st>>>(tasks_dev);
+  } else {
+    const size_t smem = (size_t)maxN * 32 * RPL * 8;
+    static bool attr = false;   // one attribute call per instantiation
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(gj_df_kernel<NW, CPW, RPL>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)((size_t)NW * CPW * 32 * RPL * 8));
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    gj_df_kernel<NW, CPW, RPL><<<ntasks, NW * 32, smem, st>>>(tasks_dev);
+  }
   hk_count_launch();
   return cudaGetLastError();
 }
