@@ -171,7 +171,12 @@ __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len
                                            ArgMax& best, double& sumsq, double& bestval,
                                            double* __restrict__ xout) {
   constexpr int64_t LD = int64_t(1) << LDLOG;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = uniform_warp_id();
+  // call arguments are not provably uniform across the call boundary
+  len = __shfl_sync(0xffffffffu, len, 0);
+  nk = __shfl_sync(0xffffffffu, nk, 0);
+  ndot = __shfl_sync(0xffffffffu, ndot, 0);
+  out_col = __shfl_sync(0xffffffffu, out_col, 0);
   best.v = 0.0;
   best.i = -1;
   bestval = 0.0;
@@ -259,43 +264,40 @@ __device__ __noinline__ void sweep(int ldlog, const double* __restrict__ F, int 
 #undef HK_SWEEP_CASE
 }
 
-// Block argmax that also carries the signed value of the winner.
+// Block argmax of |x| (lowest index on ties) that also returns the signed
+// value of the winner, in every thread and provably warp-uniform.  Thread
+// candidates: (a.v = |x|, a.i = index or -1, val = signed x).  The element e
+// of a sweep is owned by thread e % NT, so the winning lane of a warp is
+// e & 31.  Warp stage: three REDUX reductions (warp_argmax_idx); block stage:
+// the NW warp winners through SMEM, reduced the same way by every warp.
 template <int NT>
 __device__ __forceinline__ ArgMax block_argmax_val(ArgMax a, double val, double* sv, int64_t* si,
                                                    double* sval, double& out_val) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const double ov = __shfl_down_sync(0xffffffffu, a.v, off);
-    const long long oi = __shfl_down_sync(0xffffffffu, (long long)a.i, off);
-    const double ox = __shfl_down_sync(0xffffffffu, val, off);
-    if (argmax_better(ov, oi, a.v, a.i)) { a.v = ov; a.i = oi; val = ox; }
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31;
+  const int wi = warp_argmax_idx(a.v, a.i >= 0, (int)a.i);
+  const int wl = wi & 31;
+  const double wv = __shfl_sync(0xffffffffu, a.v, wl);
+  const double wx = __shfl_sync(0xffffffffu, val, wl);
+  if (NW == 1) {
+    out_val = wx;
+    return ArgMax{wv, (int64_t)wi};
   }
-  if (NT == 32) {
-    a.v = __shfl_sync(0xffffffffu, a.v, 0);
-    a.i = __shfl_sync(0xffffffffu, (long long)a.i, 0);
-    out_val = __shfl_sync(0xffffffffu, val, 0);
-    return a;
-  }
-  if (lane == 0) { sv[warp] = a.v; si[warp] = a.i; sval[warp] = val; }
+  const int warp = uniform_warp_id();
+  if (lane == 0) { sv[warp] = wv; si[warp] = wi; sval[warp] = wx; }
   __syncthreads();
-  if (warp == 0) {
-    ArgMax b;
-    double bv = 0.0;
-    if (lane < NT / 32) { b.v = sv[lane]; b.i = si[lane]; bv = sval[lane]; }
-    else { b.v = 0.0; b.i = -1; }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const double ov = __shfl_down_sync(0xffffffffu, b.v, off);
-      const long long oi = __shfl_down_sync(0xffffffffu, (long long)b.i, off);
-      const double ox = __shfl_down_sync(0xffffffffu, bv, off);
-      if (argmax_better(ov, oi, b.v, b.i)) { b.v = ov; b.i = oi; bv = ox; }
-    }
-    if (lane == 0) { sv[0] = b.v; si[0] = b.i; sval[0] = bv; }
-  }
-  __syncthreads();
-  out_val = sval[0];
-  return ArgMax{sv[0], si[0]};
+  const bool ok = lane < NW && si[lane < NW ? lane : 0] >= 0;
+  const double cv = lane < NW ? sv[lane] : 0.0;
+  const int ci = lane < NW ? (int)si[lane] : -1;
+  const double cx = lane < NW ? sval[lane] : 0.0;
+  const int bi = warp_argmax_idx(cv, ok, ci);
+  // winner's warp slot: the smallest slot holding index bi (indices are unique)
+  const unsigned mask = __ballot_sync(0xffffffffu, ok && ci == bi);
+  const int slot = mask ? __ffs(mask) - 1 : 0;
+  out_val = __shfl_sync(0xffffffffu, cx, slot);
+  const double bv = __shfl_sync(0xffffffffu, cv, slot);
+  // sv/si/sval are next written after the caller's next block barrier
+  return ArgMax{bv, (int64_t)bi};
 }
 
 template <int NT>
@@ -312,7 +314,7 @@ __device__ __forceinline__ double stopping_estimate(const double* __restrict__ p
                                                     int r, double fro2, double cross,
                                                     double* __restrict__ prod, double* s_est) {
   constexpr int NW = NT / 32;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = uniform_warp_id();
   for (int k = tid; k < r; k += NT) {
     double du = 0.0, dv = 0.0;
 #pragma unroll
@@ -330,7 +332,7 @@ __device__ __forceinline__ double stopping_estimate(const double* __restrict__ p
     if (lane == 0) *s_est = fmax(fro2 + cross + sacc, cross);
   }
   bar<NT>();
-  const double v = *s_est;
+  const double v = __shfl_sync(0xffffffffu, *s_est, 0);
   bar<NT>();
   return v;
 }
@@ -341,13 +343,16 @@ __device__ __forceinline__ double stopping_estimate(const double* __restrict__ p
 // speculative step (and its trace events) is discarded on rejection.
 template <int NT, int EPT>
 __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int part_in_smem) {
-  const int m = t.m, n = t.n, cap = t.cap;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // task scalars and every control value below are provably warp-uniform
+  // (shuffles from lane 0), so no shuffle compiles to the divergent fallback
+  const int m = __shfl_sync(0xffffffffu, t.m, 0), n = __shfl_sync(0xffffffffu, t.n, 0);
+  const int cap = __shfl_sync(0xffffffffu, t.cap, 0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = uniform_warp_id();
   constexpr int NW = NT / 32;
   uint64_t t_start = 0;
   if (t.clock && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   extern __shared__ __align__(16) unsigned char smraw[];
-  const int ldlog = t.ldu;                   // U and V share one power-of-two leading dimension
+  const int ldlog = __shfl_sync(0xffffffffu, t.ldu, 0);   // U and V share one power-of-two LD
   const int64_t LD = int64_t(1) << ldlog;
   // SMEM layout: coef[cap+KC], partU/partV[NW*cap], prod[cap] (or global
   // scratch when they do not fit), used[m]
@@ -440,7 +445,7 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
         s_row = q;
       }
       bar<NT>();
-      row = s_row;
+      row = __shfl_sync(0xffffffffu, s_row, 0);
       bar<NT>();
       continue;
     }
@@ -473,30 +478,30 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
     sweep<NT, EPT>(ldlog, U, m, c, pending ? r : 0, coef, csrc, 1, c, r, partU, pld,
                    used, nxt, uu, bval, xv);
     {
-      nxt = warp_argmax(nxt);
+      // next row = argmax over untouched rows; uu = |u|^2, vv = |v|^2 (fixed
+      // summation order: warp tree, then the warp partials in warp order)
+      const int wi = warp_argmax_idx(nxt.v, nxt.i >= 0, (int)nxt.i);
       uu = warp_sum(uu);
       vv = warp_sum(vv);
       if (NT == 32) {
-        nxt.i = __shfl_sync(0xffffffffu, (long long)nxt.i, 0);
+        nxt.i = wi;
         uu = __shfl_sync(0xffffffffu, uu, 0);
         vv = __shfl_sync(0xffffffffu, vv, 0);
       } else {
-        if (lane == 0) { red_v[warp] = nxt.v; red_i[warp] = nxt.i; red_a[warp] = uu; red_b[warp] = vv; }
+        const double wv = __shfl_sync(0xffffffffu, nxt.v, wi & 31);
+        if (lane == 0) { red_v[warp] = wv; red_i[warp] = wi; red_a[warp] = uu; red_b[warp] = vv; }
         __syncthreads();
-        if (warp == 0) {
-          ArgMax b2;
-          double a2 = 0.0, c2 = 0.0;
-          if (lane < NW) { b2.v = red_v[lane]; b2.i = red_i[lane]; a2 = red_a[lane]; c2 = red_b[lane]; }
-          else { b2.v = 0.0; b2.i = -1; }
-          b2 = warp_argmax(b2);
-          a2 = warp_sum(a2);
-          c2 = warp_sum(c2);
-          if (lane == 0) { red_v[0] = b2.v; red_i[0] = b2.i; red_a[0] = a2; red_b[0] = c2; }
-        }
-        __syncthreads();
-        nxt.i = red_i[0];
-        uu = red_a[0];
-        vv = red_b[0];
+        const bool ok = lane < NW && red_i[lane < NW ? lane : 0] >= 0;
+        const double cv = lane < NW ? red_v[lane] : 0.0;
+        const int ci = lane < NW ? (int)red_i[lane] : -1;
+        double a2 = lane < NW ? red_a[lane] : 0.0;
+        double c2 = lane < NW ? red_b[lane] : 0.0;
+        nxt.i = warp_argmax_idx(cv, ok, ci);
+        a2 = warp_sum(a2);
+        c2 = warp_sum(c2);
+        uu = __shfl_sync(0xffffffffu, a2, 0);
+        vv = __shfl_sync(0xffffffffu, c2, 0);
+        // red_* are next written after the next step's first block barrier
       }
     }
     if (pending) {                            // stopping test of the pending cross (:269-275)
@@ -542,7 +547,7 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaTask* __restrict__ tas
   for (;;) {
     if (threadIdx.x == 0) s_task = atomicAdd(counter, 1);
     __syncthreads();
-    const int ti = s_task;
+    const int ti = __shfl_sync(0xffffffffu, s_task, 0);
     __syncthreads();
     if (ti >= ntasks) break;
     aca_block<NT, EPT>(tasks[ti], tol2, part_in_smem);
