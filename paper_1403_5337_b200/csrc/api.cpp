@@ -233,15 +233,18 @@ struct NodeRec {  // per (front, node) factor storage
 struct SolveProg {
   bool small = true;
   int s = 0;
-  // small-s
-  const MatVecTask* leaf_t = nullptr;
-  int n_leaf = 0, leaf_rows = 0, leaf_k = 0;
+  // small-s: split skinny kernels (pdot -> sgemv(S^-1) -> sgemv(update) per level)
+  struct Sg {   // one sgemv launch
+    const SgemvTask* t = nullptr;
+    const int32_t* items = nullptr;
+    int nitems = 0, max_k = 0;
+  };
+  Sg leaf;
   struct Level {
-    const DotTask* dot_t = nullptr;
-    const MatVecTask* sinv_t = nullptr;
-    const MatVecTask* upd_t = nullptr;
-    int n_dot = 0, n_sinv = 0, n_upd = 0;
-    int dot_cols = 0, dot_k = 0, sinv_rows = 0, sinv_k = 0, upd_rows = 0, upd_k = 0;
+    const PdotTask* pdot_t = nullptr;
+    const int32_t* pdot_items = nullptr;
+    int n_pdot = 0;
+    Sg sinv, upd;
     // gemm variant
     const GemmTask *g1 = nullptr, *g2 = nullptr, *g3 = nullptr;
     const int32_t *g1map = nullptr, *g2map = nullptr, *g3map = nullptr;
@@ -251,6 +254,8 @@ struct SolveProg {
   const GemmTask* leaf_g = nullptr;
   const int32_t* leaf_map = nullptr;
   int leaf_tiles = 0;
+  DevBuf pbuf;          // partial dot products of one level (levels reuse it in stream order)
+  ~SolveProg() { pbuf.release(); }
 };
 
 struct hk_plan {
@@ -1390,7 +1395,8 @@ static hk_status build_solve_prog(hk_plan* p, int front, int s, SolveProg*& out,
   int64_t f0 = front < 0 ? 0 : front, f1 = front < 0 ? p->batch : front + 1;
   // leaves
   {
-    std::vector<MatVecTask> mv;
+    std::vector<SgemvTask> sg;
+    std::vector<int32_t> items;
     TileList tl;
     for (int64_t f = f0; f < f1; ++f)
       for (int slot : p->leaves) {
@@ -1398,22 +1404,26 @@ static hk_status build_solve_prog(hk_plan* p, int front, int s, SolveProg*& out,
         const NodeRec& r = p->rec[f * nn + slot];
         const int b = (int)(nd.hi - nd.lo);
         if (sp->small) {
-          MatVecTask t{};
+          SgemvTask t{};
           t.M = F + r.inv; t.ldm = b;
-          t.x = Xin + f * xs + nd.lo; t.ldx = n;
+          t.v0 = Xin + f * xs + nd.lo; t.ldv = n;
           t.y = X2 + f * xs + nd.lo; t.ldy = n;
           t.rows = b; t.K = b; t.mode = 0;
-          mv.push_back(t);
-          sp->leaf_rows = std::max(sp->leaf_rows, b);
-          sp->leaf_k = std::max(sp->leaf_k, b);
+          for (int rb = 0; rb * HK_SGEMV_ROWS < b; ++rb) {
+            items.push_back((int32_t)sg.size());
+            items.push_back(rb);
+          }
+          sg.push_back(t);
+          sp->leaf.max_k = std::max(sp->leaf.max_k, b);
         } else {
           tl.add(gemm(F + r.inv, b, 0, Xin + f * xs + nd.lo, n, X2 + f * xs + nd.lo, n, b, s, b, 1.0, 0.0));
         }
       }
     if (sp->small) {
-      sp->n_leaf = (int)mv.size();
-      sp->leaf_t = p->pstage.push(mv, st);
-      if (!sp->leaf_t) { delete sp; return fail(HK_ERR_CUDA, "pinned staging allocation failed"); }
+      sp->leaf.t = p->pstage.push(sg, st);
+      sp->leaf.items = p->pstage.push(items, st);
+      sp->leaf.nitems = (int)(items.size() / 2);
+      if (!sp->leaf.t || !sp->leaf.items) { delete sp; return fail(HK_ERR_CUDA, "pinned staging allocation failed"); }
     } else {
       sp->leaf_tiles = tl.ntiles();
       sp->leaf_g = p->pstage.push(tl.tasks, st);
@@ -1421,11 +1431,35 @@ static hk_status build_solve_prog(hk_plan* p, int front, int s, SolveProg*& out,
       if (!sp->leaf_g || !sp->leaf_map) { delete sp; return fail(HK_ERR_CUDA, "pinned staging allocation failed"); }
     }
   }
+  // partial-dot scratch: the largest level (levels run in stream order)
+  if (sp->small) {
+    int64_t need = 0;
+    for (int lvl = 0; lvl < p->depth; ++lvl) {
+      int64_t lv = 0;
+      for (int64_t f = f0; f < f1; ++f)
+        for (int k = 0; k < (int)p->internal.size(); ++k) {
+          const Node& nd = p->nodes[p->internal[k]];
+          if (nd.level != lvl) continue;
+          const NodeRec& r = p->rec[f * nn + p->internal[k]];
+          const int64_t na = p->nodes[nd.left].hi - p->nodes[nd.left].lo;
+          const int64_t nbr = p->nodes[nd.right].hi - p->nodes[nd.right].lo;
+          lv += ((na + HK_PDOT_ROWS - 1) / HK_PDOT_ROWS) * r.rl + ((nbr + HK_PDOT_ROWS - 1) / HK_PDOT_ROWS) * r.ru;
+        }
+      need = std::max(need, lv);
+    }
+    if (sp->pbuf.ensure((size_t)need * s * 8 + 64, st) != cudaSuccess) {
+      delete sp;
+      return fail(HK_ERR_CUDA, "solve scratch allocation failed");
+    }
+  }
   for (int lvl = p->depth - 1; lvl >= 0; --lvl) {
     SolveProg::Level L;
-    std::vector<DotTask> dt;
-    std::vector<MatVecTask> sv, up;
+    std::vector<PdotTask> pd;
+    std::vector<int32_t> pitems, sitems, uitems;
+    std::vector<SgemvTask> sv, up;
     TileList t1, t2, t3;
+    int64_t poff = 0;   // doubles into pbuf
+    double* P = sp->pbuf.as<double>();
     for (int64_t f = f0; f < f1; ++f)
       for (int k = 0; k < (int)p->internal.size(); ++k) {
         const int slot = p->internal[k];
@@ -1448,18 +1482,51 @@ static hk_status build_solve_prog(hk_plan* p, int front, int s, SolveProg*& out,
         const double* dleft = Yf + a.lo + r.w * n;
         const double* dright = Yf + b.lo + r.w * n;
         if (sp->small) {
-          // g = V^T x: warp per column of V (coalesced)
-          if (rl > 0) dt.push_back(DotTask{Vlow, Xf + a.lo, g, bl.ldv, n, R, na, rl});
-          if (ru > 0) dt.push_back(DotTask{Vup, Xf + b.lo, g + rl, bu.ldv, n, R, nbr, ru});
-          L.dot_cols = std::max(L.dot_cols, std::max(rl, ru));
-          L.dot_k = std::max(L.dot_k, std::max(na, nbr));
-          sv.push_back(MatVecTask{F + r.inv, g, yv, R, R, R, R, R, 0, 0});
-          L.sinv_rows = std::max(L.sinv_rows, R);
-          L.sinv_k = std::max(L.sinv_k, R);
-          if (ru > 0) up.push_back(MatVecTask{dleft, yv + rl, Xf + a.lo, n, R, n, na, ru, 1, 0});
-          if (rl > 0) up.push_back(MatVecTask{dright, yv, Xf + b.lo, n, R, n, nbr, rl, 1, 0});
-          L.upd_rows = std::max(L.upd_rows, std::max(na, nbr));
-          L.upd_k = std::max(L.upd_k, std::max(rl, ru));
+          // g = [V_low^T x_a ; V_up^T x_b] as partial dots, reduced inside the S^-1 sgemv
+          const int nchA = (na + HK_PDOT_ROWS - 1) / HK_PDOT_ROWS;
+          const int nchB = (nbr + HK_PDOT_ROWS - 1) / HK_PDOT_ROWS;
+          double* PA = P + poff;
+          poff += (int64_t)nchA * rl * s;
+          double* PB = P + poff;
+          poff += (int64_t)nchB * ru * s;
+          auto add_pdot = [&](const double* M, int64_t ldm, const double* x, int rows, int cols, double* Pp) {
+            if (cols == 0) return;
+            const int ti = (int)pd.size();
+            pd.push_back(PdotTask{M, x, Pp, ldm, (int64_t)n, rows, cols});
+            for (int ch = 0; ch * HK_PDOT_ROWS < rows; ++ch)
+              for (int cb = 0; cb * HK_PDOT_COLS < cols; ++cb) {
+                pitems.push_back(ti);
+                pitems.push_back(ch);
+                pitems.push_back(cb);
+              }
+          };
+          add_pdot(Vlow, bl.ldv, Xf + a.lo, na, rl, PA);
+          add_pdot(Vup, bu.ldv, Xf + b.lo, nbr, ru, PB);
+          SgemvTask t{};
+          t.M = F + r.inv; t.ldm = R;
+          t.v0 = nullptr; t.PA = PA; t.PB = PB; t.KA = rl; t.nchA = nchA; t.nchB = nchB;
+          t.y = yv; t.ldy = R; t.rows = R; t.K = R; t.mode = 0;
+          for (int rb = 0; rb * HK_SGEMV_ROWS < R; ++rb) {
+            sitems.push_back((int32_t)sv.size());
+            sitems.push_back(rb);
+          }
+          sv.push_back(t);
+          L.sinv.max_k = std::max(L.sinv.max_k, R);
+          // top -= d_left y_up ; bottom -= d_right y_low
+          auto add_upd = [&](const double* M, const double* v, double* y, int rows, int K) {
+            if (K == 0 || rows == 0) return;
+            SgemvTask u{};
+            u.M = M; u.ldm = n; u.v0 = v; u.ldv = R; u.y = y; u.ldy = n;
+            u.rows = rows; u.K = K; u.mode = 1;
+            for (int rb = 0; rb * HK_SGEMV_ROWS < rows; ++rb) {
+              uitems.push_back((int32_t)up.size());
+              uitems.push_back(rb);
+            }
+            up.push_back(u);
+            L.upd.max_k = std::max(L.upd.max_k, K);
+          };
+          add_upd(dleft, yv + rl, Xf + a.lo, na, ru);
+          add_upd(dright, yv, Xf + b.lo, nbr, rl);
         } else {
           if (rl > 0) t1.add(gemm(Vlow, bl.ldv, 1, Xf + a.lo, n, g, R, rl, s, na, 1.0, 0.0));
           if (ru > 0) t1.add(gemm(Vup, bu.ldv, 1, Xf + b.lo, n, g + rl, R, ru, s, nbr, 1.0, 0.0));
@@ -1470,11 +1537,16 @@ static hk_status build_solve_prog(hk_plan* p, int front, int s, SolveProg*& out,
       }
     bool ok = true;
     if (sp->small) {
-      L.n_dot = (int)dt.size(); L.n_sinv = (int)sv.size(); L.n_upd = (int)up.size();
-      L.dot_t = p->pstage.push(dt, st);
-      L.sinv_t = p->pstage.push(sv, st);
-      L.upd_t = p->pstage.push(up, st);
-      ok = L.dot_t && L.sinv_t && L.upd_t;
+      L.n_pdot = (int)(pitems.size() / 3);
+      L.pdot_t = p->pstage.push(pd, st);
+      L.pdot_items = p->pstage.push(pitems, st);
+      L.sinv.t = p->pstage.push(sv, st);
+      L.sinv.items = p->pstage.push(sitems, st);
+      L.sinv.nitems = (int)(sitems.size() / 2);
+      L.upd.t = p->pstage.push(up, st);
+      L.upd.items = p->pstage.push(uitems, st);
+      L.upd.nitems = (int)(uitems.size() / 2);
+      ok = L.pdot_t && L.pdot_items && L.sinv.t && L.sinv.items && L.upd.t && L.upd.items;
     } else {
       L.t1 = t1.ntiles(); L.t2 = t2.ntiles(); L.t3 = t3.ntiles();
       L.g1 = p->pstage.push(t1.tasks, st); L.g1map = p->pstage.push(t1.map, st);
@@ -1530,16 +1602,25 @@ static hk_status run_solve(hk_plan* p, int front, double* rhs, int64_t ld, int64
       CU(cudaMemcpy2DAsync(p->Xin.as<double>() + f * xs, n * 8, rhs + (f - f0) * rhs_stride, ld * 8,
                            n * 8, s, cudaMemcpyDeviceToDevice, st));
   }
+  const bool prof = host_profile();
+  if (prof) {
+    g_opprof.reset();
+    g_opprof.mark("start", st);
+  }
   if (sp->small) {
-    CU(hk_launch_matvec(sp->leaf_t, sp->n_leaf, (int)s, sp->leaf_rows, st, sp->leaf_k));
+    CU(hk_launch_sgemv(sp->leaf.t, sp->leaf.items, sp->leaf.nitems, (int)s, sp->leaf.max_k, st));
+    if (prof) g_opprof.mark("leaf sgemv", st);
   } else {
     if (sp->leaf_tiles) CU(hk_launch_gemm(sp->leaf_g, sp->leaf_map, sp->leaf_tiles, st));
   }
   for (auto& L : sp->levels) {
     if (sp->small) {
-      CU(hk_launch_dot(L.dot_t, L.n_dot, (int)s, L.dot_cols, st));
-      CU(hk_launch_matvec(L.sinv_t, L.n_sinv, (int)s, L.sinv_rows, st, L.sinv_k));
-      CU(hk_launch_matvec(L.upd_t, L.n_upd, (int)s, L.upd_rows, st, L.upd_k));
+      CU(hk_launch_pdot(L.pdot_t, L.pdot_items, L.n_pdot, (int)s, st));
+      if (prof) g_opprof.mark("pdot " + std::to_string(L.n_pdot), st);
+      CU(hk_launch_sgemv(L.sinv.t, L.sinv.items, L.sinv.nitems, (int)s, L.sinv.max_k, st));
+      if (prof) g_opprof.mark("sinv " + std::to_string(L.sinv.nitems), st);
+      CU(hk_launch_sgemv(L.upd.t, L.upd.items, L.upd.nitems, (int)s, L.upd.max_k, st));
+      if (prof) g_opprof.mark("upd " + std::to_string(L.upd.nitems), st);
     } else {
       if (L.t1) CU(hk_launch_gemm(L.g1, L.g1map, L.t1, st));
       if (L.t2) CU(hk_launch_gemm(L.g2, L.g2map, L.t2, st));
@@ -1555,6 +1636,10 @@ static hk_status run_solve(hk_plan* p, int front, double* rhs, int64_t ld, int64
                            n * 8, s, cudaMemcpyDeviceToDevice, st));
   }
   hc.mark("launch");
+  if (prof) {
+    CU(cudaStreamSynchronize(st));
+    g_opprof.print("solve");
+  }
   return HK_OK;
 }
 

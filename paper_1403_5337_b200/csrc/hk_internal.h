@@ -96,6 +96,38 @@ struct DotTask {     // y[k*ldy + c] = dot(M[:,k], x[:,c]) for k < cols, column-
   int32_t rows, cols;
 };
 
+// Split skinny kernels of the few-RHS solve (s <= 16).  Work is cut into
+// items small enough that every level of the sweep fills the GPU.
+struct PdotTask {    // partial dots P[(c*cols + k)*s + r] = sum_{i in row chunk c} M[i,k] x[i,r]
+  const double* M;   // rows x cols, column-major, ld ldm
+  const double* x;   // rows x s, ld ldx
+  double* P;         // [nchunks][cols][s]
+  int64_t ldm, ldx;
+  int32_t rows, cols;
+};
+struct SgemvTask {   // y[i,r] (op)= sum_k M[i,k] v[k,r] for i < rows, M column-major rows x K
+  const double* M;
+  int64_t ldm;
+  // v: either direct (v0 = K x s, ld ldv) or the reduction of partial-dot
+  // blocks: v[k] = sum_c PA[(c*KA + k)*s + r] for k < KA, then PB for the rest
+  const double* v0;
+  int64_t ldv;
+  const double* PA;
+  const double* PB;
+  int32_t KA, nchA, nchB;
+  int32_t mode;      // 0: y = M v ; 1: y -= M v
+  double* y;
+  int64_t ldy;
+  int32_t rows, K;
+};
+constexpr int HK_PDOT_ROWS = 256;   // rows per partial-dot chunk
+constexpr int HK_PDOT_COLS = 32;    // columns per partial-dot item
+constexpr int HK_SGEMV_ROWS = 32;   // rows per sgemv item
+cudaError_t hk_launch_pdot(const PdotTask* tasks, const int32_t* items, int nitems, int s,
+                           cudaStream_t st);
+cudaError_t hk_launch_sgemv(const SgemvTask* tasks, const int32_t* items, int nitems, int s,
+                            int max_k, cudaStream_t st);
+
 // launchers (return cudaError_t)
 cudaError_t hk_launch_transpose(const double* A, double* At, int64_t n, int64_t ld, int64_t batch,
                                 int64_t stride, cudaStream_t st);

@@ -82,6 +82,136 @@ __global__ void __launch_bounds__(MV_NT) gemv_rm_kernel(const double* __restrict
   }
 }
 
+// ---------------------------------------------------------------------------
+// Split skinny kernels (few-RHS solve sweep, s <= 16).
+//
+// pdot: item = (task, 256-row chunk, 32-column block); warp w owns 4 columns,
+// each lane 8 rows of the chunk, so every thread keeps 32 independent
+// coalesced loads in flight; x's chunk is staged in SMEM.  The per-(column,
+// rhs) warp sums go to a partial array -- the reduction over row chunks
+// happens in fixed order in the consumer (deterministic).
+__global__ void __launch_bounds__(256) pdot_kernel(const PdotTask* __restrict__ tasks,
+                                                   const int32_t* __restrict__ items, int s) {
+  const int ti = items[3 * blockIdx.x], ch = items[3 * blockIdx.x + 1], cb = items[3 * blockIdx.x + 2];
+  const PdotTask t = tasks[ti];
+  const int lane = threadIdx.x & 31, warp = uniform_warp_id();
+  const int row0 = ch * HK_PDOT_ROWS;
+  const int nr = min(HK_PDOT_ROWS, t.rows - row0);
+  __shared__ double xs[HK_PDOT_ROWS * 16];
+  // the M loads go out first, so their latency overlaps the x staging
+  const int k0 = cb * HK_PDOT_COLS + warp * 4;
+  const int nk = max(0, min(4, t.cols - k0));
+  double m[4][8];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = lane + 32 * u;
+      m[j][u] = (j < nk && i < nr) ? t.M[row0 + i + (int64_t)(k0 + j) * t.ldm] : 0.0;
+    }
+  for (int idx = threadIdx.x; idx < nr * s; idx += 256) {
+    const int i = idx % nr, r = idx / nr;
+    xs[r * HK_PDOT_ROWS + i] = t.x[row0 + i + (int64_t)r * t.ldx];
+  }
+  __syncthreads();
+  if (nk == 0) return;
+  for (int r = 0; r < s; ++r) {
+    double xr[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = lane + 32 * u;
+      xr[u] = i < nr ? xs[r * HK_PDOT_ROWS + i] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double acc = 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = fma(m[j][u], xr[u], acc);
+      acc = warp_sum(acc);
+      if (lane == 0 && j < nk) t.P[((int64_t)ch * t.cols + k0 + j) * s + r] = acc;
+    }
+  }
+}
+
+// sgemv: item = (task, 32-row block); warp q sums the columns k = q, q+8, ...
+// of its 32 rows (each load a coalesced 256-byte row segment, 8 loads in
+// flight per thread), the eight partial sums are combined in fixed order
+// through SMEM.  v (K x s) is first staged in SMEM -- directly, or as the
+// fixed-order reduction of partial-dot chunks.
+__global__ void __launch_bounds__(256) sgemv_kernel(const SgemvTask* __restrict__ tasks,
+                                                    const int32_t* __restrict__ items, int s) {
+  constexpr int QS = 256 / HK_SGEMV_ROWS;   // column residue classes (= warps)
+  const int ti = items[2 * blockIdx.x], rb = items[2 * blockIdx.x + 1];
+  const SgemvTask t = tasks[ti];
+  extern __shared__ double vs[];   // v: K * s, then partials [QS][HK_SGEMV_ROWS][s]
+  const int K = t.K;
+  const int q = threadIdx.x >> 5, il = threadIdx.x & 31;
+  const int i = rb * HK_SGEMV_ROWS + il;
+  const bool live = i < t.rows;
+  const double* mrow = t.M + i;
+  // the first PF matrix entries of this thread go out before v is staged
+  constexpr int PF = 8;
+  double mpre[PF];
+#pragma unroll
+  for (int u = 0; u < PF; ++u) {
+    const int k = q + u * QS;
+    mpre[u] = (live && k < K) ? mrow[(int64_t)k * t.ldm] : 0.0;
+  }
+  for (int idx = threadIdx.x; idx < K * s; idx += 256) {
+    const int k = idx % K, r = idx / K;
+    double v;
+    if (t.v0) {
+      v = t.v0[k + (int64_t)r * t.ldv];
+    } else if (k < t.KA) {
+      v = 0.0;
+      for (int c = 0; c < t.nchA; ++c) v += t.PA[((int64_t)c * t.KA + k) * s + r];
+    } else {
+      const int KB = K - t.KA, kb = k - t.KA;
+      v = 0.0;
+      for (int c = 0; c < t.nchB; ++c) v += t.PB[((int64_t)c * KB + kb) * s + r];
+    }
+    vs[r * K + k] = v;
+  }
+  __syncthreads();
+  double* part = vs + K * s;
+  for (int r0 = 0; r0 < s; r0 += 4) {
+    const int rs = min(4, s - r0);
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    if (live) {
+#pragma unroll
+      for (int u = 0; u < PF; ++u) {
+        const int k = q + u * QS;
+        if (k < K) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            if (r < rs) a[r] = fma(mpre[u], vs[(r0 + r) * K + k], a[r]);
+        }
+      }
+#pragma unroll 8
+      for (int k = q + PF * QS; k < K; k += QS) {
+        const double mv = mrow[(int64_t)k * t.ldm];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (r < rs) a[r] = fma(mv, vs[(r0 + r) * K + k], a[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      if (r < rs) part[(q * HK_SGEMV_ROWS + il) * s + r0 + r] = a[r];
+  }
+  __syncthreads();
+  if (threadIdx.x < HK_SGEMV_ROWS && live) {
+    for (int r = 0; r < s; ++r) {
+      double v = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < QS; ++qq) v += part[(qq * HK_SGEMV_ROWS + il) * s + r];
+      double* y = t.y + i + (int64_t)r * t.ldy;
+      if (t.mode == 0) *y = v;
+      else *y -= v;
+    }
+  }
+}
+
 }  // namespace
 
 cudaError_t hk_launch_matvec(const MatVecTask* tasks_dev, int ntasks, int s, int max_rows,
@@ -114,6 +244,28 @@ cudaError_t hk_launch_gemv_rowmajor(const double* A, int64_t lda, int64_t m, int
   if (m == 0) return cudaSuccess;
   int64_t blocks = (m + MV_NT / 32 - 1) / (MV_NT / 32);
   gemv_rm_kernel<<<(unsigned)blocks, MV_NT, 0, st>>>(A, lda, m, n, x, ldx, s, y, ldy);
+  hk_count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t hk_launch_pdot(const PdotTask* tasks, const int32_t* items, int nitems, int s,
+                           cudaStream_t st) {
+  if (nitems == 0) return cudaSuccess;
+  pdot_kernel<<<nitems, 256, 0, st>>>(tasks, items, s);
+  hk_count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t hk_launch_sgemv(const SgemvTask* tasks, const int32_t* items, int nitems, int s,
+                            int max_k, cudaStream_t st) {
+  if (nitems == 0) return cudaSuccess;
+  const size_t smem = ((size_t)max_k * s + 256 * (size_t)s) * 8;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(sgemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  sgemv_kernel<<<nitems, 256, smem, st>>>(tasks, items, s);
   hk_count_launch();
   return cudaGetLastError();
 }
