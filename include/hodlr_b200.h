@@ -118,6 +118,26 @@ hk_status hk_block_shape(const hk_plan* plan, int64_t block, int64_t* m, int64_t
  * level sweep of coupling assembly, coupling LU and correction.
  * ---------------------------------------------------------------------- */
 hk_status hk_factor(hk_plan* plan, void* stream);
+/* Factor with an external extension (HODLR-subtree sharding):
+ * the plan covers one subtree of a larger front, and Zext (n x wext,
+ * column-major, ld ldz, device) holds the U factors of the subtree's
+ * top-level ancestors restricted to its rows, farthest ancestor first -- the
+ * columns _factorize_node passes down as `ext` (hodlr.py:244-245, :280-282).
+ * On return the extension holds K_T^{-1} Zext in its first wext columns.
+ * batch must be 1.  hk_factor(plan) == hk_factor_ext(plan, NULL, 0, 0). */
+hk_status hk_factor_ext(hk_plan* plan, const double* Zext, int64_t ldz, int64_t wext,
+                        void* stream);
+/* Device view of a front's extension buffer Y (n x width, column-major,
+ * ld = n): columns [0, wext) after hk_factor_ext, then the d blocks of every
+ * internal node (Coupling.d_left / d_right, hodlr.py:105-134). */
+hk_status hk_get_extension(hk_plan* plan, int64_t front, double** Y, int64_t* ld,
+                           int64_t* width);
+/* C = alpha op(A) B + beta C on the FP64 tensor pipe (column-major; op(A) = A^T
+ * when transa != 0) -- the `@` of the top-level coupling terms of a sharded
+ * factorization (hodlr.py:131-134, :270-271). */
+hk_status hk_dgemm(int transa, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
+                   int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+                   void* stream);
 /* Factor views for the test-visible attributes of HodlrFactorization
  * (hodlr.py:105-154): leaf LU (b x b row-major packed, LAPACK-style 0-based
  * swap indices `piv`) and

@@ -540,11 +540,7 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
 // blocks first), so the long root chains start at t = 0 whatever the hardware
 // dispatch order of CTAs is.
 template <int NT, int EPT>
-#ifndef HK_ACA_REGS
-#define HK_ACA_REGS 0
-#endif
-// HK_ACA_REGS > 0 caps registers per thread (occupancy experiment)
-__global__ void __launch_bounds__(NT, HK_ACA_REGS > 0 ? 65536 / (NT * HK_ACA_REGS) : 1) aca_kernel(const AcaTask* __restrict__ tasks, int ntasks,
+__global__ void __launch_bounds__(NT) aca_kernel(const AcaTask* __restrict__ tasks, int ntasks,
                                                  int* __restrict__ counter, double tol2,
                                                  int part_in_smem) {
   __shared__ int s_task;

@@ -1004,8 +1004,12 @@ static hk_status flush(hk_plan* p, std::vector<Op>& ops, cudaStream_t st) {
   return HK_OK;
 }
 
-extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
+extern "C" hk_status hk_factor_ext(hk_plan* p, const double* Zext, int64_t ldz, int64_t wext,
+                                   void* stream) {
   if (!p || !p->built) return fail(HK_ERR_STATE, "factor requires a build");
+  if (wext < 0) return fail(HK_ERR_VALUE, "negative extension width");
+  if (wext > 0 && (p->batch != 1 || !Zext || ldz < p->n))
+    return fail(HK_ERR_VALUE, "an external extension needs batch 1, a device pointer and ldz >= n");
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t n = p->n;
   const size_t nb = p->blocks.size();
@@ -1029,6 +1033,7 @@ extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
   int64_t ytot = 0, ftot = 0, itot = 0, gtot = 0;
   for (int64_t f = 0; f < p->batch; ++f) {
     std::vector<int64_t> w(nn, 0);
+    w[0] = wext;                    // the root's extension (subtree sharding, §6)
     int64_t W = 0;
     for (int s = 0; s < nn; ++s) {  // preorder: parents before children
       const Node& nd = p->nodes[s];
@@ -1119,6 +1124,13 @@ extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
         copies.push_back(c);
       }
     }
+  if (wext > 0) {                 // the caller's extension columns come first (farthest)
+    CopyTask c{};
+    c.src = Zext; c.src_rs = 1; c.src_cs = ldz;
+    c.dst = Yt + p->y_off[0]; c.dst_rs = 1; c.dst_cs = n;
+    c.rows = n; c.cols = wext;
+    copies.push_back(c);
+  }
   if (!copies.empty()) {
     Op o{Op::COPY};
     o.a = p->stage.push(copies, st);
@@ -1274,6 +1286,40 @@ extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
     }
   }
   p->factored = true;
+  return HK_OK;
+}
+
+extern "C" hk_status hk_factor(hk_plan* p, void* stream) {
+  return hk_factor_ext(p, nullptr, 0, 0, stream);
+}
+
+extern "C" hk_status hk_get_extension(hk_plan* p, int64_t front, double** Y, int64_t* ld,
+                                      int64_t* width) {
+  if (!p || !p->factored) return fail(HK_ERR_STATE, "extension requires a factorization");
+  if (front < 0 || front >= p->batch) return fail(HK_ERR_VALUE, "front out of range");
+  *Y = p->Y.as<double>() + p->y_off[front];
+  *ld = p->n;
+  *width = p->W[front];
+  return HK_OK;
+}
+
+extern "C" hk_status hk_dgemm(int transa, int64_t m, int64_t n, int64_t k, double alpha,
+                              const double* A, int64_t lda, const double* B, int64_t ldb,
+                              double beta, double* C, int64_t ldc, void* stream) {
+  if (m < 0 || n < 0 || k < 0) return fail(HK_ERR_VALUE, "negative GEMM dimension");
+  if (m == 0 || n == 0) return HK_OK;
+  if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX) return fail(HK_ERR_VALUE, "GEMM too large");
+  cudaStream_t st = (cudaStream_t)stream;
+  TileList tl;
+  tl.add(gemm(A, lda, transa ? 1 : 0, B, ldb, C, ldc, (int)m, (int)n, (int)k, alpha, beta));
+  if (tl.ntiles() == 0) return HK_OK;
+  char* d = nullptr;
+  const size_t tb = sizeof(GemmTask), mb = tl.map.size() * 4;
+  CU(cudaMallocAsync((void**)&d, tb + 256 + mb, st));
+  CU(cudaMemcpyAsync(d, tl.tasks.data(), tb, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(d + 256, tl.map.data(), mb, cudaMemcpyHostToDevice, st));
+  CU(hk_launch_gemm((const GemmTask*)d, (const int32_t*)(d + 256), tl.ntiles(), st));
+  CU(cudaFreeAsync(d, st));
   return HK_OK;
 }
 
