@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=8, help="fronts in the CPU oracle sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cfg4", action="store_true",
+                    help="skip the BASELINE config-4 line item (96^3 front, GMRES time-to-1e-10)")
     return ap.parse_args()
 
 
@@ -360,6 +362,12 @@ def run_ours(args):
                "sample": f"{k} of the {F} fronts, build+factor+solve, oracle/hodlr_oracle.py "
                          f"(numpy restatement of the reference), 1 thread, {secs:.1f} s"}
 
+    # ---- BASELINE config 4: one 96^3 front (n = 9216), GMRES time-to-1e-10 on 4 rhs;
+    # N > 1: HODLR-subtree sharding over NCCL (strong scaling)
+    c4 = None
+    if not args.no_cfg4:
+        c4 = run_cfg4(dev, rank, world, hbm_peak)
+
     # per-front ranks of every rank's fronts (the one end-of-run gather)
     all_ranks = MF.gather_front_scalars(batch.ranks.astype(np.int64), device=dev)
     if rank == 0:
@@ -368,7 +376,7 @@ def run_ours(args):
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": config_dict(args, world), "impl": "ours",
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roof,
-                "cpu_baseline": cpu, "gmres": gm,
+                "cpu_baseline": cpu, "gmres": gm, "cfg4": c4,
                 "ranks_per_level_front0": [e["max_rank"] for e in batch.report(0).ranks_per_level],
                 "fronts_gathered": int(all_ranks.shape[0]),
                 "max_block_rank_all_fronts": int(all_ranks.max())}
@@ -377,6 +385,80 @@ def run_ours(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def run_cfg4(dev, rank, world, hbm_peak):
+    """Build + factor + GMRES (tol 1e-10, 4 N(0,1) rhs, seed 3) of the config-4 front.
+
+    world == 1: one plan.  world > 1 (power of two): subtree.ShardedHodlr over
+    NCCL, every GPU holding the front; times are the max over
+    ranks.  The reference's single-thread CPU times on this config were
+    measured for SURVEY.md §6.3 (20.2 s build+factor, 4.76 s GMRES for 4 rhs)."""
+    import torch
+    import paper_1403_5337_b200 as hk
+    from paper_1403_5337_b200 import multifront as MF
+    from paper_1403_5337_b200.frontgen import layered_grid_front
+    from paper_1403_5337_b200.hodlr import HodlrBatch
+    if world & (world - 1):
+        return {"skipped": f"world size {world} is not a power of two"}
+    front = layered_grid_front((96, 96, 96), "z", 48, device=dev, return_torch=True).contiguous()
+    n = front.shape[0]
+    cfg = hk.CompressionConfig(scheme="aca", tol=1e-4)
+    B = np.random.default_rng(3).standard_normal((n, 4))
+    stream = torch.cuda.current_stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+    def timed(fn):
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        ev[0].record(stream)
+        out = fn()
+        ev[1].record(stream)
+        torch.cuda.synchronize()
+        return out, MF.max_over_ranks(ev[0].elapsed_time(ev[1]), device=dev)
+
+    if world == 1:
+        batch = HodlrBatch(n, 72, 1)
+        batch.factorize(front[None], cfg)                       # warm (allocation, attributes)
+        _, bf_ms = timed(lambda: batch.factorize(front[None], cfg))
+        fact = batch.factorization(0)
+        op = hk.DenseOperator(front)
+        ranks = [lv["max_rank"] for lv in batch.report(0).ranks_per_level]
+
+        def solve_all():
+            return [hk.gmres(op, B[:, j], hk.GmresConfig(tol=1e-10), preconditioner=fact)
+                    for j in range(4)]
+    else:
+        from paper_1403_5337_b200 import subtree as ST
+        comm = ST.TorchDistRanks(world.bit_length() - 1)
+        sh = ST.ShardedHodlr(front, 72, comm)
+        sh.factorize(cfg)
+        _, bf_ms = timed(lambda: sh.factorize(cfg))
+        ranks = None
+
+        def solve_all():
+            return [sh.gmres(torch.from_numpy(B[:, j]).to(dev), hk.GmresConfig(tol=1e-10))
+                    for j in range(4)]
+    solve_all()                                                  # warm
+    res, gm_ms = timed(solve_all)
+    # HBM bytes one GMRES iteration must stream: the dense front (GEMV) + the stored factor
+    per_iter = 8.0 * n * n
+    its = [r.iterations for r in res]
+    out = {"workload": "cfg4 large single front: 96^3 Laplacian, plane z=48, n=9216, ACA 1e-4, "
+                       "leaf 72, GMRES 1e-10 on default_rng(3) N(0,1) x 4",
+           "n_gpus": world, "sharding": "none" if world == 1 else f"HODLR subtrees, level {world.bit_length() - 1}",
+           "build_factor_ms": bf_ms, "gmres_4rhs_ms": gm_ms,
+           "gmres_time_to_tol_ms_per_rhs": gm_ms / 4, "iterations": its,
+           "true_residuals": [r.true_residual for r in res],
+           "converged": all(bool(r.converged) for r in res),
+           "gemv_bytes_per_iteration": per_iter,
+           "gemv_floor_ms_per_rhs": sum(its) / 4 * per_iter / (hbm_peak * 1e9) * 1e3,
+           "reference_cpu_1t_s": {"build_factor": 20.2, "gmres_4rhs": 4.76,
+                                  "source": "SURVEY.md §6.3 (reference run in the build container)"}}
+    if ranks is not None:
+        out["max_rank_per_level"] = ranks
+    return out
 
 
 def main():

@@ -1303,6 +1303,20 @@ extern "C" hk_status hk_get_extension(hk_plan* p, int64_t front, double** Y, int
   return HK_OK;
 }
 
+extern "C" hk_status hk_copy_extension(hk_plan* p, int64_t front, int64_t col0, int64_t ncols,
+                                       double* dst, int64_t ldd, void* stream) {
+  if (!p || !p->factored) return fail(HK_ERR_STATE, "extension requires a factorization");
+  if (front < 0 || front >= p->batch) return fail(HK_ERR_VALUE, "front out of range");
+  if (col0 < 0 || ncols < 0 || col0 + ncols > std::max<int64_t>(p->W[front], 0))
+    return fail(HK_ERR_VALUE, "extension columns out of range");
+  if (ncols == 0) return HK_OK;
+  if (ldd < p->n) return fail(HK_ERR_DIMENSION, "destination leading dimension smaller than n");
+  const double* src = p->Y.as<double>() + p->y_off[front] + col0 * p->n;
+  CU(cudaMemcpy2DAsync(dst, ldd * 8, src, p->n * 8, p->n * 8, ncols, cudaMemcpyDeviceToDevice,
+                       (cudaStream_t)stream));
+  return HK_OK;
+}
+
 extern "C" hk_status hk_dgemm(int transa, int64_t m, int64_t n, int64_t k, double alpha,
                               const double* A, int64_t lda, const double* B, int64_t ldb,
                               double beta, double* C, int64_t ldc, void* stream) {

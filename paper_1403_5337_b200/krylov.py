@@ -225,3 +225,62 @@ def _gmres_callables(apply_op, b, cfg, preconditioner) -> GmresResult:
     if breakdown:
         converged = True
     return GmresResult(xh, m, converged, history, tres, breakdown)
+
+
+def gmres_device(apply_op, b, cfg: GmresConfig, preconditioner=None) -> GmresResult:
+    """gmres() with callables that take and return CUDA tensors (no host round
+    trip per iteration): the sharded operator / preconditioner of
+    subtree.ShardedHodlr.  Same algorithm and flags as gmres()."""
+    torch = N.require_cuda()
+    bd = b if isinstance(b, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(b))
+    bd = bd.to(device="cuda", dtype=torch.float64).contiguous()
+    n = bd.numel()
+    M = (lambda r: r) if preconditioner is None else preconditioner
+    norm_b = float(torch.linalg.vector_norm(bd))
+    if norm_b == 0.0:
+        return GmresResult(np.zeros(n), 0, True, [0.0], 0.0)
+    r0 = M(bd).contiguous()
+    beta = float(torch.linalg.vector_norm(r0))
+    if beta == 0.0:
+        raise GmresBreakdownError("preconditioned rhs is exactly zero")
+    mmax = min(cfg.max_iter, n)
+    basis = torch.zeros((mmax + 1, n), dtype=torch.float64, device="cuda")
+    hess = torch.zeros((mmax, mmax + 1), dtype=torch.float64, device="cuda")
+    cs = torch.zeros(mmax, dtype=torch.float64, device="cuda")
+    sn = torch.zeros(mmax, dtype=torch.float64, device="cuda")
+    g = torch.zeros(mmax + 1, dtype=torch.float64, device="cuda")
+    basis[0] = r0 / beta
+    g[0] = beta
+    out = np.zeros(3)
+    history = []
+    converged = breakdown = False
+    k = 0
+    L = N.lib()
+    st = N.stream_handle()
+    for k in range(1, mmax + 1):
+        j = k - 1
+        w = M(apply_op(basis[j])).contiguous()
+        N.check(L.hk_arnoldi_step(n, j, mmax, N.ptr(basis), N.ptr(hess), N.ptr(cs), N.ptr(sn),
+                                  N.ptr(g), N.ptr(w), beta, N.arr_ptr(out, N.D), st))
+        if out[2] != 0.0:
+            breakdown = True
+            break
+        history.append(float(out[0]))
+        if out[0] <= cfg.tol or out[1] != 0.0:
+            converged = True
+            break
+    m = k if not breakdown else k - 1
+    x = torch.zeros(n, dtype=torch.float64, device="cuda")
+    if m > 0:
+        N.check(L.hk_gmres_combine(n, m, mmax, N.ptr(basis), N.ptr(hess), N.ptr(g), N.ptr(x), st))
+    tres = float(torch.linalg.vector_norm(bd - apply_op(x)) / norm_b)
+    if breakdown and tres > 10.0 * cfg.tol:
+        raise GmresBreakdownError(
+            f"Arnoldi norm underflow at iteration {k} with true residual {tres:.3e}")
+    if converged and tres > 10.0 * cfg.tol:
+        log.warning("gmres: preconditioned residual converged but true residual %.3e exceeds "
+                    "10*tol; reporting non-convergence", tres)
+        converged = False
+    if breakdown:
+        converged = True
+    return GmresResult(x.cpu().numpy(), m, converged, history, tres, breakdown)

@@ -309,3 +309,36 @@ def test_config4_large_front():
         assert res.converged
         assert abs(res.iterations - CFG4_ITERS[j]) <= 1, (j, res.iterations)
         assert res.true_residual <= 1e-9
+
+
+# ------------------------------------------------------------------ subtree sharding (§8(e), config 4 path)
+@pytest.mark.parametrize("G", [2, 4])
+def test_subtree_sharded_matches_single_gpu(G):
+    """ShardedHodlr over G emulated ranks on one device (GpuBackend: the rank's
+    subtree plan with hk_factor_ext, hk_aca_block for the shared top blocks,
+    hk_dgemm / hk_lu_partial for the top-level coupling terms) against the
+    single-plan factorization of the same front: the top-level blocks are the
+    same bit-exact ACA factors, only partial-sum order differs."""
+    from paper_1403_5337_b200 import subtree as ST
+    from paper_1403_5337_b200.frontgen import cell_conductivity, layered_grid_front
+    dims = (32, 32, 32)
+    front = layered_grid_front(dims, "z", 16, conductivity=cell_conductivity(dims, 0), device="cuda",
+                               return_torch=True).contiguous()
+    n = front.shape[0]
+    cfg = hk.CompressionConfig(scheme="aca", tol=1e-6)
+    single = HodlrBatch(n, 64, 1).factorize(front[None], cfg)
+    fact = single.factorization(0)
+    sh = ST.ShardedHodlr(front, 64, ST.EmulatedRanks(G))
+    sh.factorize(cfg)
+    b = torch.from_numpy(np.random.default_rng(11).standard_normal(n)).cuda()
+    x_sh = sh.solve(b)
+    x_1 = hk.solve(fact, b.cpu().numpy())
+    rel = np.linalg.norm(x_sh.cpu().numpy() - x_1) / np.linalg.norm(x_1)
+    assert rel < SOLVE_RTOL, rel
+    assert torch.allclose(sh.apply(b), front @ b, rtol=1e-13, atol=1e-12)
+    res_sh = sh.gmres(b, hk.GmresConfig(tol=1e-10))
+    res_1 = hk.gmres(hk.DenseOperator(front), b.cpu().numpy(), hk.GmresConfig(tol=1e-10),
+                     preconditioner=fact)
+    assert res_sh.converged and res_1.converged
+    assert abs(res_sh.iterations - res_1.iterations) <= 1
+    assert np.linalg.norm(res_sh.x - res_1.x) / np.linalg.norm(res_1.x) < 1e-9
