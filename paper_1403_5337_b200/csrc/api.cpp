@@ -255,7 +255,16 @@ struct SolveProg {
   const int32_t* leaf_map = nullptr;
   int leaf_tiles = 0;
   DevBuf pbuf;          // partial dot products of one level (levels reuse it in stream order)
-  ~SolveProg() { pbuf.release(); }
+  // the kernel sequence is captured into a CUDA graph at its second use (a
+  // GMRES run applies the same program every iteration); one graph launch
+  // then replaces 3 launches per level
+  int uses = 0;
+  cudaGraphExec_t gexec = nullptr;
+  int gkernels = 0;
+  ~SolveProg() {
+    pbuf.release();
+    if (gexec) cudaGraphExecDestroy(gexec);
+  }
 };
 
 struct hk_plan {
@@ -1639,6 +1648,32 @@ static hk_status ensure_solve_scratch(hk_plan* p, int s, cudaStream_t st) {
   return HK_OK;
 }
 
+// The solve program's kernel sequence: leaf solve, then per level (deepest
+// first) V^T x partial dots -> S^{-1} g -> x -= d y  (hodlr.py:298-306).
+static hk_status launch_solve_kernels(SolveProg* sp, int s, cudaStream_t st, bool prof) {
+  if (sp->small) {
+    CU(hk_launch_sgemv(sp->leaf.t, sp->leaf.items, sp->leaf.nitems, s, sp->leaf.max_k, st));
+    if (prof) g_opprof.mark("leaf sgemv", st);
+  } else {
+    if (sp->leaf_tiles) CU(hk_launch_gemm(sp->leaf_g, sp->leaf_map, sp->leaf_tiles, st));
+  }
+  for (auto& L : sp->levels) {
+    if (sp->small) {
+      CU(hk_launch_pdot(L.pdot_t, L.pdot_items, L.n_pdot, s, st));
+      if (prof) g_opprof.mark("pdot " + std::to_string(L.n_pdot), st);
+      CU(hk_launch_sgemv(L.sinv.t, L.sinv.items, L.sinv.nitems, s, L.sinv.max_k, st));
+      if (prof) g_opprof.mark("sinv " + std::to_string(L.sinv.nitems), st);
+      CU(hk_launch_sgemv(L.upd.t, L.upd.items, L.upd.nitems, s, L.upd.max_k, st));
+      if (prof) g_opprof.mark("upd " + std::to_string(L.upd.nitems), st);
+    } else {
+      if (L.t1) CU(hk_launch_gemm(L.g1, L.g1map, L.t1, st));
+      if (L.t2) CU(hk_launch_gemm(L.g2, L.g2map, L.t2, st));
+      if (L.t3) CU(hk_launch_gemm(L.g3, L.g3map, L.t3, st));
+    }
+  }
+  return HK_OK;
+}
+
 static hk_status run_solve(hk_plan* p, int front, double* rhs, int64_t ld, int64_t s,
                            int64_t rhs_stride, cudaStream_t st) {
   if (!p || !p->factored) return fail(HK_ERR_STATE, "solve requires a factorization");
@@ -1666,26 +1701,31 @@ static hk_status run_solve(hk_plan* p, int front, double* rhs, int64_t ld, int64
   if (prof) {
     g_opprof.reset();
     g_opprof.mark("start", st);
-  }
-  if (sp->small) {
-    CU(hk_launch_sgemv(sp->leaf.t, sp->leaf.items, sp->leaf.nitems, (int)s, sp->leaf.max_k, st));
-    if (prof) g_opprof.mark("leaf sgemv", st);
-  } else {
-    if (sp->leaf_tiles) CU(hk_launch_gemm(sp->leaf_g, sp->leaf_map, sp->leaf_tiles, st));
-  }
-  for (auto& L : sp->levels) {
-    if (sp->small) {
-      CU(hk_launch_pdot(L.pdot_t, L.pdot_items, L.n_pdot, (int)s, st));
-      if (prof) g_opprof.mark("pdot " + std::to_string(L.n_pdot), st);
-      CU(hk_launch_sgemv(L.sinv.t, L.sinv.items, L.sinv.nitems, (int)s, L.sinv.max_k, st));
-      if (prof) g_opprof.mark("sinv " + std::to_string(L.sinv.nitems), st);
-      CU(hk_launch_sgemv(L.upd.t, L.upd.items, L.upd.nitems, (int)s, L.upd.max_k, st));
-      if (prof) g_opprof.mark("upd " + std::to_string(L.upd.nitems), st);
-    } else {
-      if (L.t1) CU(hk_launch_gemm(L.g1, L.g1map, L.t1, st));
-      if (L.t2) CU(hk_launch_gemm(L.g2, L.g2map, L.t2, st));
-      if (L.t3) CU(hk_launch_gemm(L.g3, L.g3map, L.t3, st));
+    CHK(launch_solve_kernels(sp, (int)s, st, true));
+  } else if (++sp->uses >= 2) {
+    if (!sp->gexec) {
+      CHK(ensure_side_streams(p));
+      cudaStream_t cs = p->side[0];
+      const long long before = hk_launch_count();
+      CU(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+      const hk_status h = launch_solve_kernels(sp, (int)s, cs, false);
+      cudaGraph_t graph = nullptr;
+      const cudaError_t e = cudaStreamEndCapture(cs, &graph);
+      if (h != HK_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return h;
+      }
+      CU(e);
+      sp->gkernels = (int)(hk_launch_count() - before);
+      hk_count_launch(-sp->gkernels);       // captured, not executed
+      const cudaError_t ei = cudaGraphInstantiate(&sp->gexec, graph, 0);
+      cudaGraphDestroy(graph);
+      CU(ei);
     }
+    CU(cudaGraphLaunch(sp->gexec, st));
+    hk_count_launch(sp->gkernels);
+  } else {
+    CHK(launch_solve_kernels(sp, (int)s, st, false));
   }
   if (packed) {
     CU(cudaMemcpyAsync(rhs, p->X2.as<double>() + f0 * xs, (size_t)(f1 - f0) * xs * 8,
