@@ -118,10 +118,15 @@ __device__ __forceinline__ void chunk_load_full(double (&a)[EPT][KC], const doub
   }
 }
 
-// L1 prefetch of a whole chunk (issued one chunk ahead)
+// L1 prefetch of a whole chunk (issued one chunk ahead).  A warp's column
+// segment is 32 consecutive doubles = two 128-byte lines, and prefetches are
+// not coalesced across lanes, so only lanes 0 and 16 issue them (one request
+// per line instead of 32: the ncu capture showed the per-lane prefetches as
+// ~40% of the kernel's L2 sectors).
 template <int EPT, int LDLOG>
 __device__ __forceinline__ void chunk_prefetch(const double* const (&pk)[EPT], int kb) {
   constexpr int64_t LD = int64_t(1) << LDLOG;
+  if ((threadIdx.x & 15) != 0) return;
 #pragma unroll
   for (int q = 0; q < EPT; ++q) {
     const double* p = pk[q] + (int64_t)kb * LD;
@@ -162,7 +167,7 @@ __device__ __forceinline__ void chunk_process(double (&x)[EPT], const double (&a
 // EPT elements first and then over the warp with one transpose-reduce.  Fixed
 // reduction order (deterministic).  out_col < 0: dots only.  used != nullptr:
 // column sweep (argmax over untouched entries + sum of squares); else row sweep.
-template <int NT, int EPT, int LDLOG>
+template <int NT, int EPT, int LDLOG, int DB>
 __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len, int nk, int ndot,
                                            const double* __restrict__ coef,
                                            const double* __restrict__ src, int sstride,
@@ -202,6 +207,25 @@ __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len
     int kb = 0;
     if (gfull) {
       const int kfull = (kmax / KC) * KC;
+      if constexpr (DB != 0) {
+      // register double buffer: chunk kb+KC is in flight while chunk kb is reduced
+      if (kfull > 0) {
+        double a0[EPT][KC], a1[EPT][KC];
+        chunk_load_full<EPT, LDLOG>(a0, pk, 0);
+#pragma unroll 1
+        for (; kb + 2 * KC <= kfull; kb += 2 * KC) {
+          chunk_load_full<EPT, LDLOG>(a1, pk, kb + KC);
+          if (kb + 2 * KC < kfull) chunk_prefetch<EPT, LDLOG>(pk, kb + 2 * KC);
+          chunk_process<EPT>(x, a0, pv, coef, kb, nk, ndot, mypart, lane);
+          if (kb + 2 * KC < kfull) chunk_load_full<EPT, LDLOG>(a0, pk, kb + 2 * KC);
+          chunk_process<EPT>(x, a1, pv, coef, kb + KC, nk, ndot, mypart, lane);
+        }
+        if (kb < kfull) {
+          chunk_process<EPT>(x, a0, pv, coef, kb, nk, ndot, mypart, lane);
+          kb += KC;
+        }
+      }
+      } else {
 #pragma unroll 1
       for (; kb < kfull; kb += KC) {
         double a[EPT][KC];
@@ -210,6 +234,7 @@ __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len
         // (prefetch distance 1 measured best: 2..4 thrash L1)
         if (kb + KC < kfull) chunk_prefetch<EPT, LDLOG>(pk, kb + KC);
         chunk_process<EPT>(x, a, pv, coef, kb, nk, ndot, mypart, lane);
+      }
       }
     }
 #pragma unroll 1
@@ -245,7 +270,7 @@ __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len
 
 // One call target per (NT, EPT) for the caller (keeps its register allocation
 // small); the leading dimension is dispatched once, inside.
-template <int NT, int EPT>
+template <int NT, int EPT, int DB>
 __device__ __noinline__ void sweep(int ldlog, const double* __restrict__ F, int len, int nk, int ndot,
                                    const double* __restrict__ coef, const double* __restrict__ src,
                                    int sstride, int out_col, int pend_col, double* __restrict__ part,
@@ -253,7 +278,7 @@ __device__ __noinline__ void sweep(int ldlog, const double* __restrict__ F, int 
                                    double& sumsq, double& bestval, double* xout) {
 #define HK_SWEEP_CASE(L)                                                                       \
   case L:                                                                                      \
-    sweep_impl<NT, EPT, L>(F, len, nk, ndot, coef, src, sstride, out_col, pend_col, part, pld, \
+    sweep_impl<NT, EPT, L, DB>(F, len, nk, ndot, coef, src, sstride, out_col, pend_col, part, pld, \
                            used, best, sumsq, bestval, xout);                                  \
     return;
   switch (ldlog) {
@@ -341,7 +366,7 @@ __device__ __forceinline__ double stopping_estimate(const double* __restrict__ p
 // the sweeps of step s+1 (which assume cross s is accepted) also accumulate
 // cross s's stopping-test dot products; cross s is decided after them, and the
 // speculative step (and its trace events) is discarded on rejection.
-template <int NT, int EPT>
+template <int NT, int EPT, int DB>
 __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int part_in_smem) {
   // task scalars and every control value below are provably warp-uniform
   // (shuffles from lane 0), so no shuffle compiles to the divergent fallback
@@ -401,8 +426,8 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
     const bool can_step = pending ? (c < cap && nused < m) : (c < cap);
     if (!can_step) {
       if (pending) {                          // decide the last cross: dots only
-        sweep<NT, EPT>(ldlog, U, m, 0, r, coef, nullptr, 1, -1, r, partU, pld, nullptr, best, dummy, bval, xv);
-        sweep<NT, EPT>(ldlog, V, n, 0, r, coef, nullptr, 1, -1, r, partV, pld, nullptr, best, dummy, bval, xv);
+        sweep<NT, EPT, DB>(ldlog, U, m, 0, r, coef, nullptr, 1, -1, r, partU, pld, nullptr, best, dummy, bval, xv);
+        sweep<NT, EPT, DB>(ldlog, V, n, 0, r, coef, nullptr, 1, -1, r, partV, pld, nullptr, best, dummy, bval, xv);
         bar<NT>();
         const double cross = uu_p * vv_p;
         const double est = stopping_estimate<NT>(partU, partV, pld, r, fro2, cross, prod, &s_est);
@@ -419,14 +444,14 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
     for (int k = tid; k < c; k += NT) coef[k] = U[row + (int64_t)k * LD];
     bar<NT>();
     // residual row (:253-256) + the pending cross's v dots
-    sweep<NT, EPT>(ldlog, V, n, c, pending ? r : 0, coef, rowsrc_base + (int64_t)row * rowsrc_ld, 1,
+    sweep<NT, EPT, DB>(ldlog, V, n, c, pending ? r : 0, coef, rowsrc_base + (int64_t)row * rowsrc_ld, 1,
                    c, r, partV, pld, nullptr, best, dummy, bval, xv);
     double delta;
     best = block_argmax_val<NT>(best, bval, red_v, red_i, red_x, delta);
     const int col = (int)best.i;
     if (delta == 0.0) {                       // zero residual row (:258-264)
       if (pending) {
-        sweep<NT, EPT>(ldlog, U, m, 0, r, coef, nullptr, 1, -1, r, partU, pld, nullptr, nxt, dummy, bval, xv);
+        sweep<NT, EPT, DB>(ldlog, U, m, 0, r, coef, nullptr, 1, -1, r, partU, pld, nullptr, nxt, dummy, bval, xv);
         bar<NT>();
         const double cross = uu_p * vv_p;
         const double est = stopping_estimate<NT>(partU, partV, pld, r, fro2, cross, prod, &s_est);
@@ -475,7 +500,7 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
     bar<NT>();
     // residual column (:266-268) + next-row candidate (:283) + pending u dots
     const double* csrc = t.At + (int64_t)col * t.lda;
-    sweep<NT, EPT>(ldlog, U, m, c, pending ? r : 0, coef, csrc, 1, c, r, partU, pld,
+    sweep<NT, EPT, DB>(ldlog, U, m, c, pending ? r : 0, coef, csrc, 1, c, r, partU, pld,
                    used, nxt, uu, bval, xv);
     {
       // next row = argmax over untouched rows; uu = |u|^2, vv = |v|^2 (fixed
@@ -539,7 +564,7 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
 // Persistent: CTAs pull tasks from a global counter in list order (largest
 // blocks first), so the long root chains start at t = 0 whatever the hardware
 // dispatch order of CTAs is.
-template <int NT, int EPT>
+template <int NT, int EPT, int DB>
 __global__ void __launch_bounds__(NT) aca_kernel(const AcaTask* __restrict__ tasks, int ntasks,
                                                  int* __restrict__ counter, double tol2,
                                                  int part_in_smem) {
@@ -550,7 +575,7 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaTask* __restrict__ tas
     const int ti = __shfl_sync(0xffffffffu, s_task, 0);
     __syncthreads();
     if (ti >= ntasks) break;
-    aca_block<NT, EPT>(tasks[ti], tol2, part_in_smem);
+    aca_block<NT, EPT, DB>(tasks[ti], tol2, part_in_smem);
     __syncthreads();
   }
 }
@@ -577,27 +602,42 @@ int hk_aca_class(int m, int n) {
   return L > 256 ? 0 : L > 128 ? 1 : L > 64 ? 2 : 3;
 }
 
-template <int NT, int EPT>
+template <int NT, int EPT, int DB>
 static cudaError_t launch_cls(const AcaTask* tasks_dev, int ntasks, int max_cap, int max_m,
                               double tol2, int* counter, cudaStream_t st) {
   const size_t part_bytes = (size_t)(2 * (NT / 32) + 1) * max_cap * 8;
   const size_t base = (size_t)(max_cap + KC) * 8 + (size_t)max_m + 16;
   const int part_in_smem = (base + part_bytes <= 64 * 1024) ? 1 : 0;
   const size_t smem = base + (part_in_smem ? part_bytes : 0);
-  cudaError_t e = cudaFuncSetAttribute(aca_kernel<NT, EPT>,
+  cudaError_t e = cudaFuncSetAttribute(aca_kernel<NT, EPT, DB>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, aca_kernel<NT, EPT>, NT, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, aca_kernel<NT, EPT, DB>, NT, smem);
   if (e != cudaSuccess) return e;
   int grid = sms * (per_sm > 0 ? per_sm : 1);
   if (grid > ntasks) grid = ntasks;
-  aca_kernel<NT, EPT><<<grid, NT, smem, st>>>(tasks_dev, ntasks, counter, tol2, part_in_smem);
+  aca_kernel<NT, EPT, DB><<<grid, NT, smem, st>>>(tasks_dev, ntasks, counter, tol2, part_in_smem);
   hk_count_launch();
   return cudaGetLastError();
 }
+
+// Register double-buffered sweeps per class (HK_ACA_Dc = 1): faster steps
+// (fewer exposed L2 round trips) at more registers, i.e. fewer resident CTAs.
+#ifndef HK_ACA_D0
+#define HK_ACA_D0 0
+#endif
+#ifndef HK_ACA_D1
+#define HK_ACA_D1 1
+#endif
+#ifndef HK_ACA_D2
+#define HK_ACA_D2 1
+#endif
+#ifndef HK_ACA_D3
+#define HK_ACA_D3 1
+#endif
 
 // CTA shape (threads x elements per thread) of each size class.
 #ifndef HK_ACA_T0
@@ -614,10 +654,10 @@ static cudaError_t launch_cls(const AcaTask* tasks_dev, int ntasks, int max_cap,
 static cudaError_t launch_class_id(int cls, const AcaTask* td, int nt, int max_cap, int max_m,
                                    double tol2, int* counter, cudaStream_t st) {
   switch (cls) {
-    case 0: return launch_cls<HK_ACA_T0, HK_ACA_E0>(td, nt, max_cap, max_m, tol2, counter, st);
-    case 1: return launch_cls<HK_ACA_T1, HK_ACA_E1>(td, nt, max_cap, max_m, tol2, counter, st);
-    case 2: return launch_cls<HK_ACA_T2, HK_ACA_E2>(td, nt, max_cap, max_m, tol2, counter, st);
-    default: return launch_cls<HK_ACA_T3, HK_ACA_E3>(td, nt, max_cap, max_m, tol2, counter, st);
+    case 0: return launch_cls<HK_ACA_T0, HK_ACA_E0, HK_ACA_D0>(td, nt, max_cap, max_m, tol2, counter, st);
+    case 1: return launch_cls<HK_ACA_T1, HK_ACA_E1, HK_ACA_D1>(td, nt, max_cap, max_m, tol2, counter, st);
+    case 2: return launch_cls<HK_ACA_T2, HK_ACA_E2, HK_ACA_D2>(td, nt, max_cap, max_m, tol2, counter, st);
+    default: return launch_cls<HK_ACA_T3, HK_ACA_E3, HK_ACA_D3>(td, nt, max_cap, max_m, tol2, counter, st);
   }
 }
 

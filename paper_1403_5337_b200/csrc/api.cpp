@@ -475,9 +475,20 @@ static void drop_progs(hk_plan* p) {
   p->pstage.reset();
 }
 
+// Side streams of the four ACA size classes.  Stream priorities steer the CTA
+// scheduler when the classes do not all fit at once: the long chains (large
+// classes) get SM slots first, the short class-3 tasks fill what is left.
+// HK_ACA_PRIO="p0,p1,p2,p3" (offsets from the greatest priority) overrides.
 static hk_status ensure_side_streams(hk_plan* p) {
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  int off[4] = {0, 0, 0, 1};
+  if (const char* e = getenv("HK_ACA_PRIO"))
+    sscanf(e, "%d,%d,%d,%d", &off[0], &off[1], &off[2], &off[3]);
   for (int c = 0; c < 4; ++c) {
-    if (!p->side[c]) CU(cudaStreamCreateWithFlags(&p->side[c], cudaStreamNonBlocking));
+    int prio = greatest + off[c];
+    if (prio > least) prio = least;
+    if (!p->side[c]) CU(cudaStreamCreateWithPriority(&p->side[c], cudaStreamNonBlocking, prio));
     if (!p->side_ev[c]) CU(cudaEventCreateWithFlags(&p->side_ev[c], cudaEventDisableTiming));
   }
   return HK_OK;
