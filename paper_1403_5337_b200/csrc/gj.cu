@@ -290,8 +290,11 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_df_kernel(const GjTask* __restr
           }
         }
       } else {
-        while (__shfl_sync(0xffffffffu, ld_acquire_cta(&s_pub), 0) <= c) {
+        // every lane acquires the publication itself (a value read by lane 0
+        // alone would not order the other lanes' reads of the step's data)
+        while (ld_acquire_cta(&s_pub) <= c) {
         }
+        __syncwarp();
         const int p = __shfl_sync(0xffffffffu, lane == 0 ? p_s[c] : 0, 0);
         if (p < 0) {
           singular = true;
