@@ -132,6 +132,10 @@ hk_status hk_factor_ext(hk_plan* plan, const double* Zext, int64_t ldz, int64_t 
  * internal node (Coupling.d_left / d_right, hodlr.py:105-134). */
 hk_status hk_get_extension(hk_plan* plan, int64_t front, double** Y, int64_t* ld,
                            int64_t* width);
+/* Copy columns [col0, col0 + ncols) of a front's extension buffer into dst
+ * (n x ncols, column-major, ld ldd, device). */
+hk_status hk_copy_extension(hk_plan* plan, int64_t front, int64_t col0, int64_t ncols,
+                            double* dst, int64_t ldd, void* stream);
 /* C = alpha op(A) B + beta C on the FP64 tensor pipe (column-major; op(A) = A^T
  * when transa != 0) -- the `@` of the top-level coupling terms of a sharded
  * factorization (hodlr.py:131-134, :270-271). */

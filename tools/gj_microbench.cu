@@ -1,4 +1,4 @@
-// standalone GJ microbenchmark: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include exp/gjbench.cu
+// standalone GJ microbenchmark: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include -I paper_1403_5337_b200/csrc tools/gj_microbench.cu -o exp/gj_microbench
 #include "../paper_1403_5337_b200/csrc/gj.cu"
 #include <cstdio>
 #include <vector>
