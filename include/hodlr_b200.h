@@ -193,6 +193,11 @@ hk_status hk_gmres_combine(int64_t n, int64_t m, int64_t mmax, const double* bas
  * Dense kernels (dense.py) and compression of a single block (lowrank.py).
  * ---------------------------------------------------------------------- */
 /* dense @ x for row-major A (m x n) and column-major X (n x s): hodlr.py:309-316. */
+/* Host -> device copy of `bytes` from pinned (UVA-mapped) host memory by a
+ * `ctas`-CTA kernel with evict-first stores: streams the next batch of fronts
+ * into HBM without displacing the L2 working set of the running build. */
+hk_status hk_copy_h2d_streaming(const void* src_host, void* dst_dev, int64_t bytes, int ctas,
+                                void* stream);
 hk_status hk_gemv(const double* A_dev, int64_t lda, int64_t m, int64_t n, const double* x_dev,
                   int64_t ldx, int64_t s, double* y_dev, int64_t ldy, void* stream);
 /* Complete-pivot LU (lu_full, dense.py:133-166), bit-exact pivot order.

@@ -261,6 +261,13 @@ struct SolveProg {
   int uses = 0;
   cudaGraphExec_t gexec = nullptr;
   int gkernels = 0;
+  // device memory is returned stream-ordered by drop_progs (a plain cudaFree
+  // would synchronise the whole device, stalling copies on other streams)
+  void free_async(cudaStream_t st) {
+    if (pbuf.p) cudaFreeAsync(pbuf.p, st);
+    pbuf.p = nullptr;
+    pbuf.bytes = 0;
+  }
   ~SolveProg() {
     pbuf.release();
     if (gexec) cudaGraphExecDestroy(gexec);
@@ -469,8 +476,11 @@ extern "C" hk_status hk_block_shape(const hk_plan* p, int64_t block, int64_t* m,
 }
 
 // callers synchronise the stream first: the programs' task arrays are reused
-static void drop_progs(hk_plan* p) {
-  for (auto& kv : p->progs) delete kv.second;
+static void drop_progs(hk_plan* p, cudaStream_t st) {
+  for (auto& kv : p->progs) {
+    kv.second->free_async(st);
+    delete kv.second;
+  }
   p->progs.clear();
   p->pstage.reset();
 }
@@ -520,7 +530,7 @@ static hk_status prepare_build(hk_plan* p, const double* A, int64_t ld, int64_t 
   p->factored = false;
   if (!p->progs.empty()) {
     CU(cudaStreamSynchronize(st));
-    drop_progs(p);
+    drop_progs(p, st);
   }
   set_caps(p, max_rank);
   const size_t nb = p->blocks.size();
@@ -1036,7 +1046,7 @@ extern "C" hk_status hk_factor_ext(hk_plan* p, const double* Zext, int64_t ldz, 
   const int nn = (int)p->nodes.size();
   if (!p->progs.empty()) {
     CU(cudaStreamSynchronize(st));
-    drop_progs(p);
+    drop_progs(p, st);
   }
   p->factored = false;
   HostClock hc("factor");
@@ -1650,7 +1660,7 @@ static hk_status ensure_solve_scratch(hk_plan* p, int s, cudaStream_t st) {
   if (p->Xin.bytes < need_x || p->X2.bytes < need_x || p->G.bytes < need_g || p->Yv.bytes < need_g) {
     // buffers move: cached programs hold raw pointers -> drop them
     CU(cudaStreamSynchronize(st));
-    drop_progs(p);
+    drop_progs(p, st);
     CU(p->Xin.ensure(need_x, st));
     CU(p->X2.ensure(need_x, st));
     CU(p->G.ensure(need_g, st));
@@ -1940,6 +1950,15 @@ extern "C" hk_status hk_gmres_combine(int64_t n, int64_t m, int64_t mmax, const 
 }
 
 // ------------------------------------------------------------------ dense entry points
+extern "C" hk_status hk_copy_h2d_streaming(const void* src_host, void* dst_dev, int64_t bytes,
+                                           int ctas, void* stream) {
+  if (bytes < 0 || ctas < 1) return fail(HK_ERR_VALUE, "bad copy size or CTA count");
+  if ((reinterpret_cast<uintptr_t>(src_host) | reinterpret_cast<uintptr_t>(dst_dev)) & 15)
+    return fail(HK_ERR_VALUE, "copy buffers must be 16-byte aligned");
+  CU(hk_launch_h2d_stream(src_host, dst_dev, bytes, ctas, (cudaStream_t)stream));
+  return HK_OK;
+}
+
 extern "C" hk_status hk_gemv(const double* A, int64_t lda, int64_t m, int64_t n, const double* x,
                              int64_t ldx, int64_t s, double* y, int64_t ldy, void* stream) {
   if (hk_device_count() == 0) return fail(HK_ERR_CUDA, "no CUDA device visible");

@@ -128,6 +128,9 @@ cudaError_t hk_launch_pdot(const PdotTask* tasks, const int32_t* items, int nite
 cudaError_t hk_launch_sgemv(const SgemvTask* tasks, const int32_t* items, int nitems, int s,
                             int max_k, cudaStream_t st);
 
+cudaError_t hk_launch_h2d_stream(const void* src_host, void* dst_dev, int64_t bytes, int ctas,
+                                 cudaStream_t st);
+
 // launchers (return cudaError_t)
 cudaError_t hk_launch_transpose(const double* A, double* At, int64_t n, int64_t ld, int64_t batch,
                                 int64_t stride, cudaStream_t st);

@@ -531,6 +531,76 @@ class HodlrBatch:
                                  N.stream_handle()))
         return rhs
 
+    def run_host_stream(self, items, cfg: CompressionConfig):
+        """Factor and solve a stream of host-resident batches (a multifrontal
+        level streamed from host memory).
+
+        ``items`` is a sequence of ``(fronts, rhs, out)`` CPU tensors -- pinned
+        for asynchronous copies -- shaped (batch, n, n), (batch, n) and
+        (batch, n).  The host->device copy of item i+1 runs on a copy stream
+        while item i is built, factored and solved on the current stream (two
+        device buffers), and each solution is copied back on the copy stream,
+        so the PCIe transfer overlaps the compute.  Returns the per-front ranks
+        of the last item.  Synchronises before returning.
+        """
+        torch = N.require_cuda()
+        items = list(items)
+        if not items:
+            return self.ranks
+        B, n = self.batch, self.n
+        # both streams are pool streams (non-blocking): work on the legacy
+        # default stream would serialise with the copies
+        caller = torch.cuda.current_stream()
+        comp = torch.cuda.Stream()
+        copy = torch.cuda.Stream()
+        comp.wait_stream(caller)
+        copy.wait_stream(caller)
+        dev_f = [torch.empty((B, n, n), dtype=torch.float64, device="cuda") for _ in range(2)]
+        dev_r = [torch.empty((B, n), dtype=torch.float64, device="cuda") for _ in range(2)]
+        loaded = [torch.cuda.Event() for _ in range(2)]
+        solved = [torch.cuda.Event() for _ in range(2)]
+        freed = [torch.cuda.Event() for _ in range(2)]
+        used = [False, False]
+
+        def load(i):
+            slot = i % 2
+            fr, rh, _ = items[i]
+            if tuple(fr.shape) != (B, n, n) or tuple(rh.shape) != (B, n):
+                raise DimensionMismatchError(f"item {i}: fronts must be ({B}, {n}, {n}), rhs ({B}, {n})")
+            with torch.cuda.stream(copy):
+                if used[slot]:
+                    copy.wait_event(freed[slot])
+                if fr.is_pinned() and fr.is_contiguous() and fr.dtype == torch.float64:
+                    # a 4-SM copy kernel with evict-first stores: a DMA copy
+                    # write-allocates in L2 and slowed the concurrent build ~2x
+                    N.check(N.lib().hk_copy_h2d_streaming(N.C.c_void_p(fr.data_ptr()), N.ptr(dev_f[slot]),
+                                                          fr.numel() * 8, 4,
+                                                          N.C.c_void_p(copy.cuda_stream)))
+                else:
+                    dev_f[slot].copy_(fr, non_blocking=True)
+                dev_r[slot].copy_(rh, non_blocking=True)
+                loaded[slot].record(copy)
+            used[slot] = True
+
+        load(0)
+        for i in range(len(items)):
+            slot = i % 2
+            if i + 1 < len(items):
+                load(i + 1)
+            with torch.cuda.stream(comp):
+                comp.wait_event(loaded[slot])
+                self.factorize(dev_f[slot], cfg)
+                self.solve_(dev_r[slot])
+                solved[slot].record(comp)
+            with torch.cuda.stream(copy):
+                copy.wait_event(solved[slot])
+                items[i][2].copy_(dev_r[slot], non_blocking=True)
+                freed[slot].record(copy)
+        caller.wait_stream(copy)
+        caller.wait_stream(comp)
+        caller.synchronize()
+        return self.ranks
+
     def factorization(self, f: int) -> HodlrFactorization:
         return HodlrFactorization(self.tree, self.cfg, self.plan, f, self.ranks[f])
 

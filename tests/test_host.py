@@ -17,7 +17,7 @@ from paper_1403_5337_b200 import _native as N
 def declared_symbols():
     text = (ROOT / "include" / "hodlr_b200.h").read_text()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(hk_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(hk_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_library_exports_every_declared_symbol():
