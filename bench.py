@@ -185,7 +185,11 @@ def run_reference(args):
     n = fronts[0].shape[0]
     tasks = [(fronts[i % gen], rhs_for(i % gen, n)) for i in range(cores)]
     import multiprocessing as mp
-    ctx = mp.get_context("fork")
+    # fresh interpreters with single-threaded BLAS/OpenMP: forked children of
+    # this (torch-initialised) process oversubscribed the cores ~25x
+    for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[var] = "1"
+    ctx = mp.get_context("spawn")
     times = []
     with ctx.Pool(cores, initializer=_limit_blas) as pool:
         for k in range(args.warmup + args.steps):
