@@ -171,6 +171,15 @@ hk_status hk_solve_front(hk_plan* plan, int64_t front, double* rhs_dev, int64_t 
  * scaling (krylov.py:44-66).  history_host holds max_iter doubles.
  * flags_host[0] = converged, [1] = breakdown.
  * ---------------------------------------------------------------------- */
+/* s (1..16) right-hand sides, s independent GMRES runs in lock step: one
+ * s-column GEMV and one s-column HODLR solve per iteration, batched Arnoldi.
+ * Per-system results equal s separate hk_gmres calls.  B, X: n x s (ld n);
+ * iterations[s], history[s * max_iter] (row c = rhs c), true_residual[s],
+ * flags[2s] (converged, breakdown per rhs).  SURVEY.md §8(f)#3. */
+hk_status hk_gmres_batch(hk_plan* plan, int64_t front, const double* A_dev, int64_t lda,
+                         const double* B_dev, int64_t s, double tol, int64_t max_iter,
+                         int precond, double* X_dev, int64_t* iterations, double* history,
+                         double* true_residual, int32_t* flags, void* stream);
 hk_status hk_gmres(hk_plan* plan, int64_t front, const double* A_dev, int64_t lda,
                    const double* b_dev, double tol, int64_t max_iter, int precond,
                    double* x_dev, int64_t* iterations, double* history_host,

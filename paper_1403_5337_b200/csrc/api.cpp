@@ -1926,6 +1926,143 @@ extern "C" hk_status hk_gmres(hk_plan* p, int64_t front, const double* A, int64_
   return rc;
 }
 
+// s right-hand sides, s independent GMRES runs advanced in lock step: one
+// GEMV over the s Krylov vectors (the dense front is streamed once per
+// iteration instead of s times) and one s-column HODLR solve (the stored
+// factor streamed once), then a batched Arnoldi step.  Each system's
+// arithmetic is the single-rhs run's, column by column (GEMV and solve
+// kernels treat columns independently), so iterates, iteration counts and
+// flags are those of s separate hk_gmres calls.  B, X: n x s, ld = n.
+extern "C" hk_status hk_gmres_batch(hk_plan* p, int64_t front, const double* A, int64_t lda,
+                                    const double* B, int64_t s, double tol, int64_t max_iter,
+                                    int precond, double* X, int64_t* iterations, double* history,
+                                    double* true_residual, int32_t* flags, void* stream) {
+  if (!(tol > 0.0 && tol < 1.0)) return fail(HK_ERR_VALUE, "tol must lie strictly between 0 and 1");
+  if (max_iter < 1) return fail(HK_ERR_VALUE, "max_iter must be >= 1");
+  if (s < 1 || s > 16) return fail(HK_ERR_VALUE, "gmres_batch takes 1..16 right-hand sides");
+  if (!p) return fail(HK_ERR_VALUE, "null plan");
+  if (precond == 1 && !p->factored) return fail(HK_ERR_STATE, "HODLR preconditioner not factored");
+  const int64_t n = p->n;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t mmax = std::min<int64_t>(max_iter, n);
+  const int64_t vs = mmax + 1, bstride = n * vs, hstride = vs * mmax;
+  DevBuf basis, hess, cs, sn, g, w, yb, nrm, out, act, betad;
+  auto cleanup = [&]() {
+    DevBuf* all[] = {&basis, &hess, &cs, &sn, &g, &w, &yb, &nrm, &out, &act, &betad};
+    for (DevBuf* d : all)
+      if (d->p) cudaFreeAsync(d->p, st);
+  };
+  hk_status rc = HK_OK;
+  do {
+    if (basis.ensure((size_t)s * bstride * 8, st) != cudaSuccess ||
+        hess.ensure((size_t)s * hstride * 8, st) != cudaSuccess ||
+        cs.ensure((size_t)s * vs * 8, st) != cudaSuccess || sn.ensure((size_t)s * vs * 8, st) != cudaSuccess ||
+        g.ensure((size_t)s * vs * 8, st) != cudaSuccess || w.ensure((size_t)s * n * 8, st) != cudaSuccess ||
+        yb.ensure((size_t)vs * 8, st) != cudaSuccess || nrm.ensure((size_t)s * 8 + 8, st) != cudaSuccess ||
+        out.ensure((size_t)3 * s * 8, st) != cudaSuccess || act.ensure((size_t)s * 4, st) != cudaSuccess ||
+        betad.ensure((size_t)s * 8, st) != cudaSuccess) {
+      rc = fail(HK_ERR_CUDA, "GMRES scratch allocation failed");
+      break;
+    }
+    double* Q = basis.as<double>();
+    double* W = w.as<double>();
+    cudaMemsetAsync(hess.p, 0, (size_t)s * hstride * 8, st);
+    cudaMemsetAsync(g.p, 0, (size_t)s * vs * 8, st);
+    std::vector<double> nb(s), beta(s), outh(3 * s);
+    std::vector<int32_t> active(s, 1);
+    std::vector<int64_t> m(s, 0);
+    std::vector<char> conv(s, 0), brk(s, 0), done(s, 0);
+    // ||b_c||
+    CU(hk_launch_norms(B, n, n, (int)s, nrm.as<double>(), st));
+    CU(cudaMemcpyAsync(nb.data(), nrm.p, s * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    // r0 = M^{-1} b: the s initial vectors are the first basis vectors (column stride bstride)
+    for (int64_t c = 0; c < s; ++c)
+      CU(cudaMemcpyAsync(Q + c * bstride, B + c * n, n * 8, cudaMemcpyDeviceToDevice, st));
+    if (precond == 1) {
+      CHK(run_solve(p, (int)front, Q, bstride, s, 0, st));
+    } else if (precond == 2) {
+      for (int64_t c = 0; c < s; ++c) CU(hk_launch_diag_scale(A, lda, Q + c * bstride, Q + c * bstride, n, st));
+    }
+    CU(hk_launch_norms(Q, n, bstride, (int)s, nrm.as<double>(), st));
+    CU(cudaMemcpyAsync(beta.data(), nrm.p, s * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    for (int64_t c = 0; c < s; ++c) {
+      flags[2 * c] = flags[2 * c + 1] = 0;
+      if (nb[c] == 0.0) { done[c] = 1; conv[c] = 1; active[c] = 0; continue; }
+      if (beta[c] == 0.0) {
+        rc = fail(HK_ERR_BREAKDOWN, "preconditioned rhs is exactly zero");
+        break;
+      }
+      CU(hk_launch_scale(Q + c * bstride, n, nrm.as<double>() + c, Q + c * bstride, 0, st));
+      CU(cudaMemcpyAsync(g.as<double>() + c * vs, &beta[c], 8, cudaMemcpyHostToDevice, st));
+    }
+    if (rc != HK_OK) break;
+    CU(cudaMemcpyAsync(betad.p, beta.data(), s * 8, cudaMemcpyHostToDevice, st));
+    int64_t k = 0;
+    for (k = 1; k <= mmax; ++k) {
+      bool any = false;
+      for (int64_t c = 0; c < s; ++c) any = any || active[c];
+      if (!any) break;
+      const int64_t j = k - 1;
+      CU(cudaMemcpyAsync(act.p, active.data(), s * 4, cudaMemcpyHostToDevice, st));
+      CU(hk_launch_gemv_rowmajor(A, lda, n, n, Q + j * n, bstride, s, W, n, st));
+      if (precond == 1) {
+        CHK(run_solve(p, (int)front, W, n, s, 0, st));
+      } else if (precond == 2) {
+        for (int64_t c = 0; c < s; ++c) CU(hk_launch_diag_scale(A, lda, W + c * n, W + c * n, n, st));
+      }
+      CU(hk_launch_arnoldi_batch(n, j, mmax, Q, bstride, hess.as<double>(), hstride,
+                                 cs.as<double>(), sn.as<double>(), g.as<double>(), W,
+                                 betad.as<double>(), out.as<double>(), act.as<int32_t>(), (int)s, st));
+      CU(cudaMemcpyAsync(outh.data(), out.p, 3 * s * 8, cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      for (int64_t c = 0; c < s; ++c) {
+        if (!active[c]) continue;
+        const double* o = outh.data() + 3 * c;
+        if (o[2] != 0.0) { brk[c] = 1; m[c] = k - 1; active[c] = 0; continue; }
+        history[c * max_iter + (k - 1)] = o[0];
+        m[c] = k;
+        if (o[0] <= tol || o[1] != 0.0) { conv[c] = 1; active[c] = 0; }
+      }
+    }
+    // x_c = Q_c y_c, then the true residuals
+    for (int64_t c = 0; c < s; ++c) {
+      if (done[c]) { CU(cudaMemsetAsync(X + c * n, 0, n * 8, st)); continue; }
+      if (m[c] > 0)
+        CU(hk_launch_combine(n, m[c], mmax, Q + c * bstride, hess.as<double>() + c * hstride,
+                             g.as<double>() + c * vs, X + c * n, yb.as<double>(), st));
+      else
+        CU(cudaMemsetAsync(X + c * n, 0, n * 8, st));
+    }
+    CU(hk_launch_gemv_rowmajor(A, lda, n, n, X, n, s, W, n, st));
+    for (int64_t c = 0; c < s; ++c) CU(hk_launch_axpby(B + c * n, W + c * n, W + c * n, n, 1.0, -1.0, st));
+    CU(hk_launch_norms(W, n, n, (int)s, nrm.as<double>(), st));
+    std::vector<double> rn(s);
+    CU(cudaMemcpyAsync(rn.data(), nrm.p, s * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    for (int64_t c = 0; c < s; ++c) {
+      iterations[c] = m[c];
+      if (done[c]) { true_residual[c] = 0.0; flags[2 * c] = 1; continue; }
+      const double tr = rn[c] / nb[c];
+      true_residual[c] = tr;
+      bool cv = conv[c];
+      if (brk[c] && tr > 10.0 * tol) {
+        char msg[160];
+        snprintf(msg, sizeof msg, "rhs %lld: Arnoldi norm underflow with true residual %.3e",
+                 (long long)c, tr);
+        rc = fail(HK_ERR_BREAKDOWN, msg);
+      }
+      if (cv && tr > 10.0 * tol) cv = false;
+      if (brk[c]) cv = true;
+      flags[2 * c] = cv ? 1 : 0;
+      flags[2 * c + 1] = brk[c] ? 1 : 0;
+    }
+  } while (false);
+  cleanup();
+  return rc;
+}
+
 extern "C" hk_status hk_arnoldi_step(int64_t n, int64_t j, int64_t mmax, double* basis,
                                      double* hess, double* cs, double* sn, double* g, double* w,
                                      double beta, double* out_host, void* stream) {

@@ -166,6 +166,12 @@ cudaError_t hk_launch_combine(int64_t n, int64_t m, int64_t mmax, const double* 
                               const double* hess, const double* g, double* x, double* y_scratch,
                               cudaStream_t st);
 cudaError_t hk_launch_norm(const double* x, int64_t n, double* out, cudaStream_t st);
+cudaError_t hk_launch_arnoldi_batch(int64_t n, int64_t j, int64_t mmax, double* basis,
+                                    int64_t bstride, double* hess, int64_t hstride, double* cs,
+                                    double* sn, double* g, double* w, const double* beta,
+                                    double* out, const int32_t* active, int s, cudaStream_t st);
+cudaError_t hk_launch_norms(const double* x, int64_t n, int64_t ld, int s, double* out,
+                            cudaStream_t st);
 cudaError_t hk_launch_scale(const double* x, int64_t n, const double* num, double* y,
                             int invert, cudaStream_t st);
 cudaError_t hk_launch_axpby(const double* x, const double* y, double* z, int64_t n, double a,

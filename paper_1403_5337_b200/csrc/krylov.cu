@@ -20,10 +20,9 @@ __device__ void block_axpy(double* w, const double* q, double h, int64_t n) {
   for (int64_t i = threadIdx.x; i < n; i += KR_NT) w[i] -= h * q[i];
 }
 
-__global__ void __launch_bounds__(KR_NT) arnoldi_kernel(int64_t n, int64_t j, int64_t mmax,
-                                                        double* basis, double* hess, double* cs,
-                                                        double* sn, double* g, double* w,
-                                                        double beta, double* out) {
+__device__ __forceinline__ void arnoldi_body(int64_t n, int64_t j, int64_t mmax, double* basis,
+                                             double* hess, double* cs, double* sn, double* g,
+                                             double* w, double beta, double* out) {
   __shared__ double red[KR_NT / 32];
   const int64_t k = j + 1;
   const int64_t ldh = mmax + 1;
@@ -77,6 +76,38 @@ __global__ void __launch_bounds__(KR_NT) arnoldi_kernel(int64_t n, int64_t j, in
     out[1] = happy ? 1.0 : 0.0;
     out[2] = brk;
   }
+}
+
+__global__ void __launch_bounds__(KR_NT) arnoldi_kernel(int64_t n, int64_t j, int64_t mmax,
+                                                        double* basis, double* hess, double* cs,
+                                                        double* sn, double* g, double* w,
+                                                        double beta, double* out) {
+  arnoldi_body(n, j, mmax, basis, hess, cs, sn, g, w, beta, out);
+}
+
+// s independent GMRES systems advanced together (one CTA each): system c owns
+// basis + c*bstride, hess + c*hstride, cs/sn/g + c*(mmax+1), w + c*n, beta[c],
+// out + 3c; systems whose flag active[c] is 0 (converged) are skipped.
+__global__ void __launch_bounds__(KR_NT) arnoldi_batch_kernel(
+    int64_t n, int64_t j, int64_t mmax, double* basis, int64_t bstride, double* hess,
+    int64_t hstride, double* cs, double* sn, double* g, double* w, const double* beta,
+    double* out, const int32_t* active) {
+  const int c = blockIdx.x;
+  if (!active[c]) return;
+  const int64_t vs = mmax + 1;
+  arnoldi_body(n, j, mmax, basis + c * bstride, hess + c * hstride, cs + c * vs, sn + c * vs,
+               g + c * vs, w + c * n, beta[c], out + 3 * c);
+}
+
+// per-column 2-norms of an n x s column-major block (ld), one CTA per column
+__global__ void __launch_bounds__(KR_NT) norms_kernel(const double* x, int64_t n, int64_t ld,
+                                                     double* out) {
+  __shared__ double red[KR_NT / 32];
+  const double* xc = x + blockIdx.x * ld;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += KR_NT) s += xc[i] * xc[i];
+  s = block_sum<KR_NT>(s, red);
+  if (threadIdx.x == 0) out[blockIdx.x] = sqrt(s);
 }
 
 // y = back substitution (krylov.py:147-151) by one thread, then x = Q[:, :m] y.
@@ -182,6 +213,25 @@ cudaError_t hk_launch_axpby(const double* x, const double* y, double* z, int64_t
 cudaError_t hk_launch_diag_scale(const double* A, int64_t lda, const double* x, double* y,
                                  int64_t n, cudaStream_t st) {
   diag_scale_kernel<<<grid_for(n), 256, 0, st>>>(A, lda, x, y, n);
+  hk_count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t hk_launch_arnoldi_batch(int64_t n, int64_t j, int64_t mmax, double* basis,
+                                    int64_t bstride, double* hess, int64_t hstride, double* cs,
+                                    double* sn, double* g, double* w, const double* beta,
+                                    double* out, const int32_t* active, int s, cudaStream_t st) {
+  if (s <= 0) return cudaSuccess;
+  arnoldi_batch_kernel<<<s, KR_NT, 0, st>>>(n, j, mmax, basis, bstride, hess, hstride, cs, sn, g,
+                                            w, beta, out, active);
+  hk_count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t hk_launch_norms(const double* x, int64_t n, int64_t ld, int s, double* out,
+                            cudaStream_t st) {
+  if (s <= 0) return cudaSuccess;
+  norms_kernel<<<s, KR_NT, 0, st>>>(x, n, ld, out);
   hk_count_launch();
   return cudaGetLastError();
 }

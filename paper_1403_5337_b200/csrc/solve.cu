@@ -59,6 +59,34 @@ __global__ void __launch_bounds__(MV_NT) dot_kernel(const DotTask* __restrict__ 
 }
 
 // y(m x s, col-major) = A(m x n, row-major) x(n x s, col-major); warp per row.
+// Columns are processed in groups of up to 4 per pass over the row, so the
+// row of A is streamed from HBM once per 4 right-hand sides; per column the
+// summation (two interleaved partial sums, then the warp tree) is the same as
+// for s = 1, so a column's result does not depend on s.
+template <int CG>
+__device__ __forceinline__ void gemv_row_group(const double* __restrict__ a, const double* __restrict__ x,
+                                               int64_t ldx, int64_t n, int lane, double (&res)[CG]) {
+  double acc0[CG], acc1[CG];
+#pragma unroll
+  for (int c = 0; c < CG; ++c) acc0[c] = acc1[c] = 0.0;
+  int64_t j = lane;
+  for (; j + 32 < n; j += 64) {
+    const double a0 = a[j], a1 = a[j + 32];
+#pragma unroll
+    for (int c = 0; c < CG; ++c) {
+      acc0[c] += a0 * x[c * ldx + j];
+      acc1[c] += a1 * x[c * ldx + j + 32];
+    }
+  }
+  for (; j < n; j += 32) {
+    const double a0 = a[j];
+#pragma unroll
+    for (int c = 0; c < CG; ++c) acc0[c] += a0 * x[c * ldx + j];
+  }
+#pragma unroll
+  for (int c = 0; c < CG; ++c) res[c] = warp_sum(acc0[c] + acc1[c]);
+}
+
 __global__ void __launch_bounds__(MV_NT) gemv_rm_kernel(const double* __restrict__ A, int64_t lda,
                                                         int64_t m, int64_t n,
                                                         const double* __restrict__ x, int64_t ldx,
@@ -68,17 +96,17 @@ __global__ void __launch_bounds__(MV_NT) gemv_rm_kernel(const double* __restrict
   const int64_t row = (int64_t)blockIdx.x * (MV_NT / 32) + (threadIdx.x >> 5);
   if (row >= m) return;
   const double* a = A + row * lda;
-  for (int64_t c = 0; c < s; ++c) {
-    const double* xc = x + c * ldx;
-    double acc0 = 0.0, acc1 = 0.0;
-    int64_t j = lane;
-    for (; j + 32 < n; j += 64) {
-      acc0 += a[j] * xc[j];
-      acc1 += a[j + 32] * xc[j + 32];
-    }
-    for (; j < n; j += 32) acc0 += a[j] * xc[j];
-    double acc = warp_sum(acc0 + acc1);
-    if (lane == 0) y[row + c * ldy] = acc;
+  int64_t c0 = 0;
+  for (; c0 + 4 <= s; c0 += 4) {
+    double r[4];
+    gemv_row_group<4>(a, x + c0 * ldx, ldx, n, lane, r);
+    if (lane == 0)
+      for (int c = 0; c < 4; ++c) y[row + (c0 + c) * ldy] = r[c];
+  }
+  for (; c0 < s; ++c0) {
+    double r[1];
+    gemv_row_group<1>(a, x + c0 * ldx, ldx, n, lane, r);
+    if (lane == 0) y[row + c0 * ldy] = r[0];
   }
 }
 

@@ -284,3 +284,52 @@ def gmres_device(apply_op, b, cfg: GmresConfig, preconditioner=None) -> GmresRes
     if breakdown:
         converged = True
     return GmresResult(x.cpu().numpy(), m, converged, history, tres, breakdown)
+
+
+def gmres_batch(apply_op, B, cfg: GmresConfig, preconditioner=None) -> list:
+    """gmres() for the columns of B (n x s, s <= 16) run together on the device.
+
+    ``apply_op`` must be a DenseOperator and ``preconditioner`` a HODLR
+    factorization (or HodlrPreconditioner / DiagonalPreconditioner / None).
+    Every iteration reads the dense front and the stored factor once for all
+    s systems (hk_gmres_batch); each system's iterates, iteration count and
+    flags equal those of gmres() on that column.
+    """
+    torch = N.require_cuda()
+    from .hodlr import _Plan
+    if not isinstance(apply_op, DenseOperator):
+        raise TypeError("gmres_batch needs a DenseOperator")
+    Bn = B.cpu().numpy() if isinstance(B, torch.Tensor) else np.asarray(B, dtype=np.float64)
+    if Bn.ndim != 2 or Bn.shape[0] != apply_op.n:
+        raise ValueError("B must be n x s")
+    n, s = Bn.shape
+    if not 1 <= s <= 16:
+        raise ValueError("gmres_batch takes 1..16 right-hand sides")
+    pre = preconditioner
+    if isinstance(pre, HodlrPreconditioner):
+        pre = pre.fact
+    if _is_fact(pre):
+        plan, front, kind = pre.plan, pre.front_index, 1
+    else:
+        plan = getattr(apply_op, "_plan", None)
+        if plan is None:
+            plan = _Plan(n, max(n, 1), 1)
+            apply_op._plan = plan
+        front, kind = 0, 0 if pre is None else 2
+    bd = torch.from_numpy(np.ascontiguousarray(Bn.T)).cuda()        # (s, n) = column-major n x s
+    xd = torch.zeros_like(bd)
+    its = np.zeros(s, dtype=np.int64)
+    hist = np.zeros((s, max(cfg.max_iter, 1)))
+    tres = np.zeros(s)
+    flags = np.zeros(2 * s, dtype=np.int32)
+    N.check(N.lib().hk_gmres_batch(plan.h, front, N.ptr(apply_op.dev), n, N.ptr(bd), s, cfg.tol,
+                                   cfg.max_iter, kind, N.ptr(xd), N.arr_ptr(its, N.I64),
+                                   N.arr_ptr(hist, N.D), N.arr_ptr(tres, N.D),
+                                   N.arr_ptr(flags, N.I32), N.stream_handle()))
+    xh = xd.cpu().numpy()
+    out = []
+    for c in range(s):
+        m = int(its[c])
+        out.append(GmresResult(xh[c].copy(), m, bool(flags[2 * c]), [float(h) for h in hist[c, :m]],
+                               float(tres[c]), bool(flags[2 * c + 1])))
+    return out

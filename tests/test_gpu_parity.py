@@ -342,3 +342,24 @@ def test_subtree_sharded_matches_single_gpu(G):
     assert res_sh.converged and res_1.converged
     assert abs(res_sh.iterations - res_1.iterations) <= 1
     assert np.linalg.norm(res_sh.x - res_1.x) / np.linalg.norm(res_1.x) < 1e-9
+
+
+def test_gmres_batch_matches_single_rhs_runs():
+    """hk_gmres_batch advances s systems together; each column's iterations,
+    flags and iterates equal the single-rhs gmres() on that column."""
+    from paper_1403_5337_b200.frontgen import cell_conductivity, layered_grid_front
+    dims = (24, 24, 24)
+    front = layered_grid_front(dims, "z", 12, conductivity=cell_conductivity(dims, 2))
+    n = front.shape[0]
+    fact, _ = hk.factorize(hk.BlockAccessor.from_matrix(front), hk.build_tree(n, 32),
+                           hk.CompressionConfig(scheme="aca", tol=1e-4))
+    op = hk.DenseOperator(front)
+    B = np.random.default_rng(9).standard_normal((n, 4))
+    cfg = hk.GmresConfig(tol=1e-10)
+    batch = hk.gmres_batch(op, B, cfg, preconditioner=fact)
+    for c in range(4):
+        single = hk.gmres(op, B[:, c], cfg, preconditioner=fact)
+        assert batch[c].iterations == single.iterations, c
+        assert batch[c].converged == single.converged
+        assert np.array_equal(batch[c].x, single.x), c
+        assert batch[c].residual_history == single.residual_history
