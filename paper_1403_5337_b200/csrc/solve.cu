@@ -240,6 +240,68 @@ __global__ void __launch_bounds__(256) sgemv_kernel(const SgemvTask* __restrict_
   }
 }
 
+
+// Dense GEMV for the GMRES operator (src/cli.py:320-321): y(m x s) = A x with
+// A row-major.  Each warp owns RW = 4 rows and walks them together with
+// 16-byte loads (lane l covers columns 2l + 64t, 2l + 64t + 1), so every x
+// chunk it loads is reused by 4 rows and each lane keeps 4 independent
+// 16-byte A loads in flight; columns are processed in groups of up to 4.
+// Per (row, column) the summation order is fixed (2 interleaved partials per
+// lane, then the warp tree), independent of s.
+template <int CG>
+__device__ __forceinline__ void gemv4_group(const double* __restrict__ A, int64_t lda, int64_t row0,
+                                            int64_t m, int64_t n, const double* __restrict__ x,
+                                            int64_t ldx, int lane, double (&res)[4][CG]) {
+  constexpr int RW = 4;
+  double acc[RW][CG];
+#pragma unroll
+  for (int r = 0; r < RW; ++r)
+#pragma unroll
+    for (int c = 0; c < CG; ++c) acc[r][c] = 0.0;
+  const double* a[RW];
+#pragma unroll
+  for (int r = 0; r < RW; ++r) a[r] = A + (row0 + r < m ? row0 + r : row0) * lda;
+  for (int64_t j = 2 * lane; j < n; j += 64) {
+    double2 av[RW], xv[CG];
+#pragma unroll
+    for (int r = 0; r < RW; ++r) av[r] = __ldcs(reinterpret_cast<const double2*>(a[r] + j));
+#pragma unroll
+    for (int c = 0; c < CG; ++c) xv[c] = *reinterpret_cast<const double2*>(x + c * ldx + j);
+#pragma unroll
+    for (int r = 0; r < RW; ++r)
+#pragma unroll
+      for (int c = 0; c < CG; ++c) acc[r][c] = fma(av[r].y, xv[c].y, fma(av[r].x, xv[c].x, acc[r][c]));
+  }
+#pragma unroll
+  for (int r = 0; r < RW; ++r)
+#pragma unroll
+    for (int c = 0; c < CG; ++c) res[r][c] = warp_sum(acc[r][c]);
+}
+
+__global__ void __launch_bounds__(MV_NT) gemv4_kernel(const double* __restrict__ A, int64_t lda,
+                                                      int64_t m, int64_t n,
+                                                      const double* __restrict__ x, int64_t ldx,
+                                                      int64_t s, double* __restrict__ y, int64_t ldy) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row0 = ((int64_t)blockIdx.x * (MV_NT / 32) + (threadIdx.x >> 5)) * 4;
+  if (row0 >= m) return;
+  int64_t c0 = 0;
+  for (; c0 + 4 <= s; c0 += 4) {
+    double r[4][4];
+    gemv4_group<4>(A, lda, row0, m, n, x + c0 * ldx, ldx, lane, r);
+    if (lane == 0)
+      for (int q = 0; q < 4; ++q)
+        if (row0 + q < m)
+          for (int c = 0; c < 4; ++c) y[row0 + q + (c0 + c) * ldy] = r[q][c];
+  }
+  for (; c0 < s; ++c0) {
+    double r[4][1];
+    gemv4_group<1>(A, lda, row0, m, n, x + c0 * ldx, ldx, lane, r);
+    if (lane == 0)
+      for (int q = 0; q < 4; ++q)
+        if (row0 + q < m) y[row0 + q + c0 * ldy] = r[q][0];
+  }
+}
 }  // namespace
 
 cudaError_t hk_launch_matvec(const MatVecTask* tasks_dev, int ntasks, int s, int max_rows,
@@ -270,6 +332,15 @@ cudaError_t hk_launch_gemv_rowmajor(const double* A, int64_t lda, int64_t m, int
                                     const double* x, int64_t ldx, int64_t s, double* y,
                                     int64_t ldy, cudaStream_t st) {
   if (m == 0) return cudaSuccess;
+  const bool vec = (n % 2 == 0) && (lda % 2 == 0) && (ldx % 2 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(x)) & 15) == 0;
+  if (vec) {   // 16-byte loads, 4 rows per warp
+    const int64_t rows_per_cta = (MV_NT / 32) * 4;
+    const int64_t blocks = (m + rows_per_cta - 1) / rows_per_cta;
+    gemv4_kernel<<<(unsigned)blocks, MV_NT, 0, st>>>(A, lda, m, n, x, ldx, s, y, ldy);
+    hk_count_launch();
+    return cudaGetLastError();
+  }
   int64_t blocks = (m + MV_NT / 32 - 1) / (MV_NT / 32);
   gemv_rm_kernel<<<(unsigned)blocks, MV_NT, 0, st>>>(A, lda, m, n, x, ldx, s, y, ldy);
   hk_count_launch();

@@ -56,12 +56,13 @@ def main():
     op = hk.DenseOperator(front)
     B = np.random.default_rng(3).standard_normal((n, args.nrhs))
     its, tres, gm_ms = [], [], []
-    for j in range(args.nrhs):
+    for _k in range(2):                        # warm, then timed
         torch.cuda.synchronize()
         t1 = time.perf_counter()
-        res = hk.gmres(op, B[:, j], hk.GmresConfig(tol=1e-10), preconditioner=fact)
+        res_all = hk.gmres_batch(op, B, hk.GmresConfig(tol=1e-10), preconditioner=fact)
         torch.cuda.synchronize()
-        gm_ms.append((time.perf_counter() - t1) * 1e3)
+    gm_ms.append((time.perf_counter() - t1) * 1e3)
+    for res in res_all:
         its.append(res.iterations)
         tres.append(res.true_residual)
     # direct solve of the 4 rhs at once and its residual through the dense front
@@ -77,7 +78,7 @@ def main():
         "build_ms": [round(x, 2) for x in build_ms], "factor_ms": [round(x, 2) for x in factor_ms],
         "max_rank_per_level": [lv["max_rank"] for lv in rep.ranks_per_level],
         "gmres_iterations": its, "gmres_true_residual": tres,
-        "gmres_wall_ms": [round(x, 2) for x in gm_ms],
+        "gmres_batch_wall_ms": [round(x, 2) for x in gm_ms],
         "hodlr_solve_4rhs_ms": round(solve_ms, 3), "hodlr_solve_rel_residual": rel,
         "aca_seconds": batch.plan.aca_seconds(),
     }))
