@@ -21,6 +21,8 @@
 #include "hk_common.cuh"
 #include "hk_internal.h"
 
+#include <stdlib.h>
+
 namespace {
 
 
@@ -69,7 +71,32 @@ __device__ __forceinline__ double transpose_reduce(double (&a)[KC], int lane) {
 // ---------------------------------------------------------------------------
 // U/V column loads: plain weak loads, L1-cached (the CTA's own earlier stores
 // are visible after its barriers; no other CTA writes this block's U/V)
-__device__ __forceinline__ double ld_col(const double* p) { return *p; }
+#ifndef HK_ACA_UV_EL
+#define HK_ACA_UV_EL 0
+#endif
+#ifndef HK_ACA_SRC_CS
+#define HK_ACA_SRC_CS 0
+#endif
+__device__ __forceinline__ double ld_col(const double* p) {
+#if HK_ACA_UV_EL
+  // U/V are re-read every step: keep them in L2 ahead of the one-shot gathers
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+#else
+  return *p;
+#endif
+}
+// Row / column gathers of the front are read once per block: streaming loads
+__device__ __forceinline__ double ld_src(const double* p) {
+#if HK_ACA_SRC_CS
+  return __ldcs(p);
+#else
+  return *p;
+#endif
+}
 
 // Chunk helpers of the fused sweep (KC columns x EPT elements per thread).
 //
@@ -195,13 +222,18 @@ __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len
     double x[EPT], pv[EPT];
     const double* pk[EPT];
     bool ok[EPT];
-    const bool gfull = g0 + NT * EPT <= len;      // warp-uniform
+    // Chunks whose KC columns all lie inside the block load unpredicated even
+    // in a ragged element group: a thread past `len` reads element 0 of the
+    // column (always valid), its pv is 0 and its x is never stored, so it
+    // contributes nothing.  (Blocks of 288/144/72 entries and the cluster
+    // slices took the predicated path before: 2-3x slower sweeps.)
+    constexpr bool gfull = true;
 #pragma unroll
     for (int q = 0; q < EPT; ++q) {
       const int e = g0 + tid + q * NT;
       ok[q] = e < len;
       pk[q] = F + (ok[q] ? e : 0);
-      x[q] = (ok[q] && src) ? src[(int64_t)e * sstride] : 0.0;
+      x[q] = (ok[q] && src) ? ld_src(src + (int64_t)e * sstride) : 0.0;
       pv[q] = (ok[q] && ndot > 0) ? pk[q][(int64_t)pend_col * LD] : 0.0;
     }
     int kb = 0;
@@ -580,6 +612,352 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaTask* __restrict__ tas
   }
 }
 
+// ---------------------------------------------------------------------------
+// Cluster ACA: one block's pivot chain run by a thread-block cluster of P CTAs.
+//
+// A single CTA sweeps all m (n) entries of every cross vector; for the large
+// blocks of a big front (config 4: 4608 x 4608 at rank 227) that chain ran on
+// one SM for 53 ms while the rest of the GPU idled.  Here CTA q of the cluster
+// owns the 16-aligned slice [q*S, (q+1)*S) of the entries of both U and V, so
+// each sweep streams only its slice; the decisions that couple the slices go
+// through distributed shared memory, three cluster barriers per step:
+//   BAR1  row-sweep argmax -> pivot column and delta   (R slots)
+//   BAR2  column-sweep argmax -> next row, |u|^2, |v|^2, per-CTA dot partials
+//   BAR3  stopping-estimate partial sums               (E slots)
+// Every CTA evaluates every decision from the same slots in the same order,
+// so control stays cluster-uniform.  The residual entries are computed
+// exactly as in aca_block (reference k order, separate multiply/subtract), so
+// U, V, pivots and ranks are bit-identical to the single-CTA kernel's; only
+// the summation order of the stopping-test dots changes (decision margins,
+// SURVEY.md Appendix C).  Coefficient rows U[row, 0:c] / V[col, 0:c] written
+// by other CTAs are read from global memory after the release/acquire
+// cluster barriers; slices are 16-aligned so no 128-byte line is written by
+// two CTAs.
+struct ClSlot {
+  double v, val, a, b;
+  int idx;
+  int pad;
+};
+
+__device__ __forceinline__ void cluster_bar() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::
+                   : "memory");
+}
+__device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cl_nrank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+// generic address of the same shared variable in CTA `rank` of the cluster
+template <class T>
+__device__ __forceinline__ const T* cl_map(const T* p, unsigned rank) {
+  uint64_t out;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(p), "r"(rank));
+  return reinterpret_cast<const T*>(out);
+}
+
+// Cluster argmax over the P slots (lowest index on ties); idx, val and the
+// slot's a/b sums in fixed slot order.  Valid in every lane of every warp.
+__device__ __forceinline__ int cl_argmax(const ClSlot* slot, unsigned P, double& val, double& sa,
+                                         double& sb) {
+  const int lane = threadIdx.x & 31;
+  double v = 0.0, x = 0.0, a = 0.0, b = 0.0;
+  int i = -1;
+  if (lane < (int)P) {
+    const ClSlot* s = cl_map(slot, (unsigned)lane);
+    v = s->v;
+    x = s->val;
+    a = s->a;
+    b = s->b;
+    i = s->idx;
+  }
+  const int bi = warp_argmax_idx(v, i >= 0, i);
+  const unsigned mask = __ballot_sync(0xffffffffu, i >= 0 && i == bi);
+  const int sl = mask ? __ffs(mask) - 1 : 0;
+  val = __shfl_sync(0xffffffffu, x, sl);
+  // fixed order sums over the slots (lane p holds slot p; shfl_down tree)
+  sa = warp_sum(a);
+  sb = warp_sum(b);
+  sa = __shfl_sync(0xffffffffu, sa, 0);
+  sb = __shfl_sync(0xffffffffu, sb, 0);
+  return bi;
+}
+
+// CTA-level sums of the per-warp dot partials into cpart (k < r).
+template <int NT>
+__device__ __forceinline__ void cl_reduce_parts(const double* __restrict__ partU,
+                                                const double* __restrict__ partV, int pld, int r,
+                                                double* __restrict__ cpU, double* __restrict__ cpV) {
+  constexpr int NW = NT / 32;
+  for (int k = threadIdx.x; k < r; k += NT) {
+    double du = 0.0, dv = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      du += partU[w * pld + k];
+      dv += partV[w * pld + k];
+    }
+    cpU[k] = du;
+    cpV[k] = dv;
+  }
+}
+
+// After a cluster barrier that published cpart: this CTA's share of
+// sum_k 2 (u.u_k)(v.v_k) over k in its range, written to its E slot by warp 0.
+__device__ __forceinline__ void cl_est_share(const double* cpU, const double* cpV, int r,
+                                             unsigned q, unsigned P, double* slE) {
+  if (uniform_warp_id() != 0) return;
+  const int lane = threadIdx.x & 31;
+  const int per = (r + (int)P - 1) / (int)P;
+  const int k0 = (int)q * per, k1 = min(r, k0 + per);
+  double s = 0.0;
+  for (int k = k0 + lane; k < k1; k += 32) {
+    double du = 0.0, dv = 0.0;
+    for (unsigned p = 0; p < P; ++p) {
+      du += *cl_map(cpU + k, p);
+      dv += *cl_map(cpV + k, p);
+    }
+    s += 2.0 * du * dv;
+  }
+  s = warp_sum(s);
+  if (lane == 0) *slE = s;
+}
+
+__device__ __forceinline__ double cl_est_total(const double* slE, unsigned P) {
+  const int lane = threadIdx.x & 31;
+  double s = lane < (int)P ? *cl_map(slE, (unsigned)lane) : 0.0;
+  s = warp_sum(s);
+  return __shfl_sync(0xffffffffu, s, 0);
+}
+
+template <int NT, int EPT, int DB>
+__global__ void __launch_bounds__(NT) aca_cluster_kernel(const AcaTask* __restrict__ tasks,
+                                                         double tol2, int part_in_smem) {
+  constexpr int NW = NT / 32;
+  const unsigned P = cl_nrank(), q = cl_rank();
+  const AcaTask& t = tasks[blockIdx.x / P];
+  const int m = __shfl_sync(0xffffffffu, t.m, 0), n = __shfl_sync(0xffffffffu, t.n, 0);
+  const int cap = __shfl_sync(0xffffffffu, t.cap, 0);
+  const int tid = threadIdx.x;
+  uint64_t t_start = 0;
+  if (t.clock && tid == 0 && q == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int ldlog = __shfl_sync(0xffffffffu, t.ldu, 0);
+  const int64_t LD = int64_t(1) << ldlog;
+  // entry slices (16-aligned: no 128-byte line of U/V is written by two CTAs)
+  const int slm = (((m + (int)P - 1) / (int)P) + 15) & ~15;
+  const int sln = (((n + (int)P - 1) / (int)P) + 15) & ~15;
+  const int mu0 = min(m, (int)q * slm), mlen = min(m, mu0 + slm) - mu0;
+  const int nv0 = min(n, (int)q * sln), nlen = min(n, nv0 + sln) - nv0;
+  // SMEM: coef[cap+KC], cpU[cap], cpV[cap], (partU, partV [NW*cap] each), used[m]
+  double* coef = reinterpret_cast<double*>(smraw);
+  double* cpU = coef + cap + KC;
+  double* cpV = cpU + cap;
+  const int pld = cap;
+  double* partU = part_in_smem ? cpV + cap : t.scratch + (size_t)q * 2 * NW * cap;
+  double* partV = partU + NW * pld;
+  unsigned char* used =
+      reinterpret_cast<unsigned char*>(part_in_smem ? partV + NW * pld : cpV + cap);
+  __shared__ double red_v[NW], red_a[NW], red_b[NW], red_x[NW];
+  __shared__ int64_t red_i[NW];
+  __shared__ ClSlot slR, slC;
+  __shared__ double slE;
+  __shared__ int s_row;
+
+  const bool lead = q == 0;
+  int32_t* trows = (t.trace && lead) ? t.trace + 2 : nullptr;
+  int32_t* tcols = (t.trace && lead) ? t.trace + 2 + (m + cap + 1) : nullptr;
+  int nrow_ev = 0, ncol_ev = 0;
+  if (m == 0 || n == 0 || cap == 0) {
+    if (tid == 0 && lead) {
+      *t.rank = 0;
+      if (t.trace) { t.trace[0] = 0; t.trace[1] = 0; }
+    }
+    cluster_bar();
+    return;
+  }
+  for (int i = tid; i < m; i += NT) used[i] = 0;
+  for (int k = tid; k < cap + KC; k += NT) coef[k] = 0.0;
+  cluster_bar();
+
+  double* Us = t.U + mu0;
+  double* Vs = t.V + nv0;
+  int r = 0, row = 0, nused = 0;
+  bool pending = false;
+  double uu_p = 0.0, vv_p = 0.0, fro2 = 0.0;
+  ArgMax best, nxt;
+  double dummy, uu, bval;
+  double xv[EPT];
+
+  // decide the pending cross from partials already in partU/partV (rare paths)
+  auto decide_pending = [&](void) -> bool {   // true = accept
+    bar<NT>();
+    cl_reduce_parts<NT>(partU, partV, pld, r, cpU, cpV);
+    cluster_bar();
+    cl_est_share(cpU, cpV, r, q, P, &slE);
+    cluster_bar();
+    const double cross = uu_p * vv_p;
+    const double est = fmax(fro2 + cross + cl_est_total(&slE, P), cross);
+    const bool acc = !(cross <= tol2 * est);
+    if (acc) fro2 = est;
+    return acc;
+  };
+
+  for (;;) {
+    const int c = r + (pending ? 1 : 0);
+    const bool can_step = pending ? (c < cap && nused < m) : (c < cap);
+    if (!can_step) {
+      if (pending) {
+        sweep<NT, EPT, DB>(ldlog, Us, mlen, 0, r, coef, nullptr, 1, -1, r, partU, pld, nullptr, best, dummy, bval, xv);
+        sweep<NT, EPT, DB>(ldlog, Vs, nlen, 0, r, coef, nullptr, 1, -1, r, partV, pld, nullptr, best, dummy, bval, xv);
+        if (decide_pending()) ++r;
+      }
+      break;
+    }
+    if (tid == 0) {
+      used[row] = 1;
+      if (trows) trows[nrow_ev] = row;
+    }
+    ++nrow_ev;
+    ++nused;
+    for (int k = tid; k < c; k += NT) coef[k] = __ldcg(t.U + row + (int64_t)k * LD);
+    bar<NT>();
+    // residual row slice + the pending cross's v dots
+    sweep<NT, EPT, DB>(ldlog, Vs, nlen, c, pending ? r : 0, coef,
+                       t.A + (int64_t)row * t.lda + nv0, 1, c, r, partV, pld, nullptr, best, dummy,
+                       bval, xv);
+    {
+      double lval;
+      ArgMax lb = block_argmax_val<NT>(best, bval, red_v, red_i, red_x, lval);
+      if (tid == 0) {
+        slR.v = lb.v;
+        slR.val = lval;
+        slR.idx = lb.i >= 0 ? (int)lb.i + nv0 : -1;
+        slR.a = slR.b = 0.0;
+      }
+    }
+    cluster_bar();                                             // BAR1
+    double delta, sa, sb;
+    const int col = cl_argmax(&slR, P, delta, sa, sb);
+    if (delta == 0.0) {                       // zero residual row (:258-264)
+      if (pending) {
+        sweep<NT, EPT, DB>(ldlog, Us, mlen, 0, r, coef, nullptr, 1, -1, r, partU, pld, nullptr, nxt, dummy, bval, xv);
+        if (!decide_pending()) {
+          --nrow_ev;
+          break;
+        }
+        ++r;
+        pending = false;
+      }
+      if (nused == m) break;
+      if (tid == 0) {
+        int qq = 0;
+        while (used[qq]) ++qq;
+        s_row = qq;
+      }
+      // cluster barrier: every CTA has read this step's R slots before the
+      // next step's row sweep overwrites them
+      cluster_bar();
+      row = __shfl_sync(0xffffffffu, s_row, 0);
+      bar<NT>();
+      continue;
+    }
+    // v = res / delta over the own slice
+    double vv = 0.0;
+    if (nlen <= NT * EPT) {
+#pragma unroll
+      for (int qq = 0; qq < EPT; ++qq) {
+        const int e = tid + qq * NT;
+        if (e < nlen) {
+          const double v = div_rn(xv[qq], delta);
+          Vs[e + (int64_t)c * LD] = v;
+          vv += v * v;
+        }
+      }
+    } else {
+      for (int e = tid; e < nlen; e += NT) {
+        double* vp = Vs + e + (int64_t)c * LD;
+        const double v = div_rn(*vp, delta);
+        *vp = v;
+        vv += v * v;
+      }
+    }
+    for (int k = tid; k < c; k += NT) coef[k] = __ldcg(t.V + col + (int64_t)k * LD);
+    if (tid == 0 && tcols) tcols[ncol_ev] = col;
+    ++ncol_ev;
+    bar<NT>();
+    // residual column slice + next-row candidate + pending u dots
+    sweep<NT, EPT, DB>(ldlog, Us, mlen, c, pending ? r : 0, coef,
+                       t.At + (int64_t)col * t.lda + mu0, 1, c, r, partU, pld, used + mu0, nxt,
+                       uu, bval, xv);
+    {
+      const int lane = tid & 31, warp = uniform_warp_id();
+      const int wi = warp_argmax_idx(nxt.v, nxt.i >= 0, (int)nxt.i);
+      uu = warp_sum(uu);
+      vv = warp_sum(vv);
+      const double wv = __shfl_sync(0xffffffffu, nxt.v, wi & 31);
+      if (lane == 0) { red_v[warp] = wv; red_i[warp] = wi; red_a[warp] = uu; red_b[warp] = vv; }
+      __syncthreads();
+      const bool ok = lane < NW && red_i[lane < NW ? lane : 0] >= 0;
+      const double cv = lane < NW ? red_v[lane] : 0.0;
+      const int ci = lane < NW ? (int)red_i[lane] : -1;
+      double a2 = lane < NW ? red_a[lane] : 0.0;
+      double c2 = lane < NW ? red_b[lane] : 0.0;
+      const int bi = warp_argmax_idx(cv, ok, ci);
+      a2 = warp_sum(a2);
+      c2 = warp_sum(c2);
+      const unsigned mask = __ballot_sync(0xffffffffu, ok && ci == bi);
+      const double bv = __shfl_sync(0xffffffffu, cv, mask ? __ffs(mask) - 1 : 0);
+      if (pending) cl_reduce_parts<NT>(partU, partV, pld, r, cpU, cpV);
+      if (tid == 0) {
+        slC.v = bv;
+        slC.idx = bi >= 0 ? bi + mu0 : -1;
+        slC.val = 0.0;
+        slC.a = a2;
+        slC.b = c2;
+      }
+    }
+    cluster_bar();                                             // BAR2
+    double dum;
+    const int nrow = cl_argmax(&slC, P, dum, uu, vv);
+    if (pending) {                            // stopping test of the pending cross (:269-275)
+      cl_est_share(cpU, cpV, r, q, P, &slE);
+      cluster_bar();                                           // BAR3
+      const double cross = uu_p * vv_p;
+      const double est = fmax(fro2 + cross + cl_est_total(&slE, P), cross);
+      if (cross <= tol2 * est) {
+        --nrow_ev;
+        --ncol_ev;
+        break;
+      }
+      ++r;
+      fro2 = est;
+    }
+    pending = true;
+    uu_p = uu;
+    vv_p = vv;
+    row = nrow;
+  }
+  if (tid == 0 && lead) {
+    *t.rank = r;
+    if (t.trace) { t.trace[0] = nrow_ev; t.trace[1] = ncol_ev; }
+    if (t.clock) {
+      uint64_t t_end;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      t.clock[0] = (int64_t)t_start;
+      t.clock[1] = (int64_t)t_end;
+      t.clock[2] = smid;
+    }
+  }
+  cluster_bar();   // no CTA leaves while another may still read its SMEM
+}
+
 }  // namespace
 
 cudaError_t hk_launch_transpose(const double* A, double* At, int64_t n, int64_t ld, int64_t batch,
@@ -681,6 +1059,8 @@ cudaError_t hk_launch_aca(const AcaTask* tasks_dev, int ntasks, int max_cap, int
                           double tol2, cudaStream_t st, int max_mn) {
   // single-block API: the class of the block (max_mn = max(m, n))
   if (ntasks == 0) return cudaSuccess;
+  const int P = hk_aca_cluster_size(max_mn, max_mn);
+  if (P > 1) return hk_launch_aca_cluster(tasks_dev, ntasks, P, max_cap, max_m, tol2, st);
   int* counter = nullptr;
   cudaError_t e = cudaMallocAsync(&counter, sizeof(int), st);
   if (e != cudaSuccess) return e;
@@ -691,3 +1071,77 @@ cudaError_t hk_launch_aca(const AcaTask* tasks_dev, int ntasks, int max_cap, int
 }
 
 size_t hk_aca_scratch_doubles(int cap) { return (size_t)(2 * (512 / 32) + 1) * cap + 16; }
+
+// ---------------------------------------------------------------- cluster ACA
+#ifndef HK_ACA_CLNT
+#define HK_ACA_CLNT 160   // threads per cluster CTA: 2 entries each -> 320-entry slices
+#endif
+#ifndef HK_ACA_CLDB
+#define HK_ACA_CLDB 1
+#endif
+constexpr int kClNT = HK_ACA_CLNT, kClEPT = 2;
+
+// Blocks whose longer side exceeds HK_ACA_CLMIN (default 512) run on a
+// cluster of P = pow2ceil(ceil(L / 320)) CTAs (at most 16), so that every CTA
+// sweeps one <= 320-entry slice in a single pass; smaller blocks stay on the
+// single-CTA size classes.  Returns 1 for a single-CTA block.
+int hk_aca_cluster_size(int m, int n) {
+  static int clmin = -1;
+  if (clmin < 0) {
+    const char* e = getenv("HK_ACA_CLMIN");
+    clmin = e ? atoi(e) : 512;
+  }
+  const int L = m > n ? m : n;
+  if (L <= clmin) return 1;
+  const int need = (L + kClNT * kClEPT - 1) / (kClNT * kClEPT);
+  int P = 2;
+  while (P < need && P < 16) P <<= 1;
+  return P;
+}
+
+size_t hk_aca_scratch_doubles_cl(int cap, int P) {
+  return (size_t)P * 2 * (kClNT / 32) * cap + 16;
+}
+
+cudaError_t hk_launch_aca_cluster(const AcaTask* tasks_dev, int ntasks, int P, int max_cap,
+                                  int max_m, double tol2, cudaStream_t st) {
+  if (ntasks == 0) return cudaSuccess;
+  auto kern = aca_cluster_kernel<kClNT, kClEPT, HK_ACA_CLDB>;
+  constexpr int NW = kClNT / 32;
+  const size_t base = (size_t)(max_cap + KC) * 8 + (size_t)2 * max_cap * 8 + (size_t)max_m + 16;
+  const size_t part_bytes = (size_t)2 * NW * max_cap * 8;
+  const int part_in_smem = (base + part_bytes <= 200 * 1024) ? 1 : 0;
+  const size_t smem = base + (part_in_smem ? part_bytes : 0);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (P > 8) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  cfg.blockDim = dim3(kClNT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  // largest cluster the device can co-schedule with this footprint (the
+  // slices follow the runtime cluster size, so any P >= 1 is correct)
+  for (;;) {
+    at[0].val.clusterDim.x = (unsigned)P;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)(P * ntasks));
+    int ncl = 0;
+    e = cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg);
+    if (e == cudaSuccess && ncl >= 1) break;
+    (void)cudaGetLastError();
+    if (P == 1) return e != cudaSuccess ? e : cudaErrorLaunchOutOfResources;
+    P >>= 1;
+  }
+  e = cudaLaunchKernelEx(&cfg, kern, tasks_dev, tol2, part_in_smem);
+  hk_count_launch();
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}

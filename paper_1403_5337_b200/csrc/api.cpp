@@ -293,6 +293,8 @@ struct hk_plan {
   int64_t uv_per_front = 0, trace_per_front = 0;
   DevBuf At, UV, ranks_d, trace_d, tasks_d, aca_scr, aca_cnt;
   cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t cl_side[4] = {nullptr, nullptr, nullptr, nullptr};   // cluster ACA groups
+  cudaEvent_t cl_side_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t side_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<int32_t> ranks;       // batch * nblocks
   bool have_trace = false;
@@ -321,6 +323,10 @@ struct hk_plan {
     for (auto& x : side)
       if (x) cudaStreamDestroy(x);
     for (auto& x : side_ev)
+      if (x) cudaEventDestroy(x);
+    for (auto& x : cl_side)
+      if (x) cudaStreamDestroy(x);
+    for (auto& x : cl_side_ev)
       if (x) cudaEventDestroy(x);
     DevBuf* bufs[] = {&aca_cnt, &aca_scr, &At, &UV, &ranks_d, &trace_d, &tasks_d, &sel_d, &work_d, &perm_d,
                       &skel_status_d, &probe_d, &Y, &Ytmp, &F, &I, &ftask_d, &fmap_d, &gj_d, &gj2_d, &gjs_d,
@@ -500,6 +506,8 @@ static hk_status ensure_side_streams(hk_plan* p) {
     if (prio > least) prio = least;
     if (!p->side[c]) CU(cudaStreamCreateWithPriority(&p->side[c], cudaStreamNonBlocking, prio));
     if (!p->side_ev[c]) CU(cudaEventCreateWithFlags(&p->side_ev[c], cudaEventDisableTiming));
+    if (!p->cl_side[c]) CU(cudaStreamCreateWithPriority(&p->cl_side[c], cudaStreamNonBlocking, greatest));
+    if (!p->cl_side_ev[c]) CU(cudaEventCreateWithFlags(&p->cl_side_ev[c], cudaEventDisableTiming));
   }
   return HK_OK;
 }
@@ -574,7 +582,9 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
   std::vector<size_t> scr_off(nb);
   for (size_t bi = 0; bi < nb; ++bi) {
     scr_off[bi] = scr_per_front;
-    scr_per_front += hk_aca_scratch_doubles(p->blocks[bi].cap);
+    const BlockGeom& b = p->blocks[bi];
+    const int P = hk_aca_cluster_size(b.m, b.n);
+    scr_per_front += P > 1 ? hk_aca_scratch_doubles_cl(b.cap, P) : hk_aca_scratch_doubles(b.cap);
   }
   CU(p->aca_scr.ensure((size_t)p->batch * scr_per_front * 8 + 8, st));
   for (int64_t f = 0; f < p->batch; ++f) {
@@ -605,9 +615,15 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
   // global largest-first order across fronts: the long root chains start first
   std::vector<size_t> order(tasks.size());
   for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+  // group key: cluster tasks first (largest cluster first), then the
+  // single-CTA size classes
+  auto group_of = [](const AcaTask& a) {
+    const int P = hk_aca_cluster_size(a.m, a.n);
+    return P > 1 ? -P : hk_aca_class(a.m, a.n);
+  };
   std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) {
     const AcaTask &a = tasks[x], &b = tasks[y];
-    const int ca = hk_aca_class(a.m, a.n), cb = hk_aca_class(b.m, b.n);
+    const int ca = group_of(a), cb = group_of(b);
     if (ca != cb) return ca < cb;
     return (int64_t)(a.m + a.n) * a.cap > (int64_t)(b.m + b.n) * b.cap;
   });
@@ -628,14 +644,38 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
   const AcaTask* tasks_dev = p->stage.push(tasks, st);
   if (!tasks_dev) return fail(HK_ERR_CUDA, "pinned staging allocation failed");
   CU(p->stage.commit(st));
-  if ((size_t)(max_cap + 16) * 8 + max_m + 1024 > 220 * 1024)
-    return fail(HK_ERR_VALUE, "block too large for the single-CTA ACA kernel");
+  // cluster groups (P = 16, 8, 4, 2) then the four single-CTA classes
+  size_t ncl_tasks = 0;
+  int cl_P[4] = {0, 0, 0, 0}, cl_begin[4] = {0, 0, 0, 0}, cl_cnt[4] = {0, 0, 0, 0};
+  int cl_cap[4] = {0, 0, 0, 0}, cl_m[4] = {0, 0, 0, 0};
+  int ngroups = 0;
+  while (ncl_tasks < tasks.size()) {
+    const AcaTask& t = tasks[ncl_tasks];
+    const int P = hk_aca_cluster_size(t.m, t.n);
+    if (P == 1) break;
+    if (ngroups == 0 || cl_P[ngroups - 1] != P) {
+      if (ngroups == 4) return fail(HK_ERR_VALUE, "internal: more than four ACA cluster groups");
+      cl_P[ngroups] = P;
+      cl_begin[ngroups] = (int)ncl_tasks;
+      ++ngroups;
+    }
+    const int g = ngroups - 1;
+    cl_cnt[g]++;
+    cl_cap[g] = std::max(cl_cap[g], t.cap);
+    cl_m[g] = std::max(cl_m[g], t.m);
+    if ((size_t)(3 * t.cap + 16) * 8 + t.m + 1024 > 220 * 1024)
+      return fail(HK_ERR_VALUE, "block too large for the cluster ACA kernel");
+    ++ncl_tasks;
+  }
   int cls_begin[5] = {0, 0, 0, 0, 0}, cls_cap[4] = {0, 0, 0, 0}, cls_m[4] = {0, 0, 0, 0};
-  for (const auto& t : tasks) {
+  for (size_t i = ncl_tasks; i < tasks.size(); ++i) {
+    const AcaTask& t = tasks[i];
     const int c = hk_aca_class(t.m, t.n);
     cls_begin[c + 1]++;
     cls_cap[c] = std::max(cls_cap[c], t.cap);
     cls_m[c] = std::max(cls_m[c], t.m);
+    if ((size_t)(t.cap + 16) * 8 + t.m + 1024 > 220 * 1024)
+      return fail(HK_ERR_VALUE, "block too large for the single-CTA ACA kernel");
   }
   for (int c = 0; c < 4; ++c) cls_begin[c + 1] += cls_begin[c];
   CHK(ensure_side_streams(p));
@@ -647,11 +687,20 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
     ss[c] = p->side[c];
     CU(cudaStreamWaitEvent(ss[c], p->ev[3], 0));
   }
-  CU(hk_launch_aca_classes(tasks_dev, cls_begin, cls_cap, cls_m, tol2,
+  for (int g = 0; g < ngroups; ++g) {   // the long chains launch first
+    CU(cudaStreamWaitEvent(p->cl_side[g], p->ev[3], 0));
+    CU(hk_launch_aca_cluster(tasks_dev + cl_begin[g], cl_cnt[g], cl_P[g], cl_cap[g], cl_m[g],
+                             tol2, p->cl_side[g]));
+  }
+  CU(hk_launch_aca_classes(tasks_dev + ncl_tasks, cls_begin, cls_cap, cls_m, tol2,
                            p->aca_cnt.as<int>(), ss));
   for (int c = 0; c < 4; ++c) {   // join
     CU(cudaEventRecord(p->side_ev[c], ss[c]));
     CU(cudaStreamWaitEvent(st, p->side_ev[c], 0));
+  }
+  for (int g = 0; g < ngroups; ++g) {
+    CU(cudaEventRecord(p->cl_side_ev[g], p->cl_side[g]));
+    CU(cudaStreamWaitEvent(st, p->cl_side_ev[g], 0));
   }
   CU(cudaEventRecord(p->ev[1], st));
   hc.mark("plan+launch");
@@ -2173,7 +2222,11 @@ extern "C" hk_status hk_aca_block(const double* a, int64_t m, int64_t n, int64_t
   CU(cudaMemcpy2DAsync(sqbuf, sq * 8, a, ld * 8, n * 8, m, cudaMemcpyDeviceToDevice, st));
   CU(hk_launch_transpose(sqbuf, at, sq, sq, 1, 0, st));
   double* scr = nullptr;
-  CU(cudaMallocAsync(&scr, hk_aca_scratch_doubles((int)cap) * 8, st));
+  {
+    const int P = hk_aca_cluster_size((int)std::max(m, n), (int)std::max(m, n));
+    const size_t sd = P > 1 ? hk_aca_scratch_doubles_cl((int)cap, P) : hk_aca_scratch_doubles((int)cap);
+    CU(cudaMallocAsync(&scr, sd * 8, st));
+  }
   int lmu = 6;
   while ((1 << lmu) < std::max(m, n)) ++lmu;
   const int lmv = lmu;
