@@ -142,6 +142,15 @@ hk_status hk_copy_extension(hk_plan* plan, int64_t front, int64_t col0, int64_t 
 hk_status hk_dgemm(int transa, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
                    int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
                    void* stream);
+/* Batched explicit inverses with implicit partial pivoting (Gauss-Jordan) --
+ * the kernel behind every leaf and capacitance inverse of the factorization
+ * (replaces lu_partial(...) of hodlr.py:225 and :273, dense.py:59-81;
+ * singular iff min |pivot| < 1e-300 as dense.py:76-77).  A: `batch` row-major
+ * n x n device matrices (leading dimension lda, matrix stride `stride`
+ * elements); out: column-major device inverses, leading dimension n, stride
+ * n*n; status_host[b] = 1 when matrix b is singular. */
+hk_status hk_gj_inverse(const double* A, int64_t n, int64_t lda, int64_t batch, int64_t stride,
+                        double* out, int32_t* status_host, void* stream);
 /* Factor views for the test-visible attributes of HodlrFactorization
  * (hodlr.py:105-154): leaf LU (b x b row-major packed, LAPACK-style 0-based
  * swap indices `piv`) and

@@ -50,6 +50,7 @@ SIGNATURES = {
     "hk_copy_h2d_streaming": (C.c_int, [P, P, I64, C.c_int, P]),
     "hk_gmres_batch": (C.c_int, [P, I64, P, I64, P, I64, D, I64, C.c_int, P, PI64, PD, PD, PI32, P]),
     "hk_dgemm": (C.c_int, [C.c_int, I64, I64, I64, D, P, I64, P, I64, D, P, I64, P]),
+    "hk_gj_inverse": (C.c_int, [P, I64, I64, I64, I64, P, P, P]),
     "hk_get_leaf_lu": (C.c_int, [P, I64, I64, PD, PI32]),
     "hk_get_coupling": (C.c_int, [P, I64, I64, PD, PD, PD, PI32]),
     "hk_solve": (C.c_int, [P, P, I64, I64, I64, P]),

@@ -639,28 +639,6 @@ struct ClSlot {
   int pad;
 };
 
-__device__ __forceinline__ void cluster_bar() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::
-                   : "memory");
-}
-__device__ __forceinline__ unsigned cl_rank() {
-  unsigned r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ unsigned cl_nrank() {
-  unsigned r;
-  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
-  return r;
-}
-// generic address of the same shared variable in CTA `rank` of the cluster
-template <class T>
-__device__ __forceinline__ const T* cl_map(const T* p, unsigned rank) {
-  uint64_t out;
-  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(p), "r"(rank));
-  return reinterpret_cast<const T*>(out);
-}
-
 // Cluster argmax over the P slots (lowest index on ties); idx, val and the
 // slot's a/b sums in fixed slot order.  Valid in every lane of every warp.
 __device__ __forceinline__ int cl_argmax(const ClSlot* slot, unsigned P, double& val, double& sa,

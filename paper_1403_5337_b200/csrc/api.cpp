@@ -2196,6 +2196,49 @@ extern "C" hk_status hk_lu_partial(double* a, int64_t n, int64_t ld, int32_t* pe
   return HK_OK;
 }
 
+// Batched explicit inverses by the factor's Gauss-Jordan kernels (the
+// capacitance-matrix path of hodlr.py:273; implicit partial pivoting, so the
+// singularity test is dense.py:76-77's).  A: `batch` row-major n x n matrices
+// (leading dimension lda, matrix stride `stride` elements); out: column-major
+// inverses (leading dimension n, stride n*n).  status_host[b] = 1 if matrix b
+// is singular.
+extern "C" hk_status hk_gj_inverse(const double* A, int64_t n, int64_t lda, int64_t batch,
+                                   int64_t stride, double* out, int32_t* status_host,
+                                   void* stream) {
+  if (hk_device_count() == 0) return fail(HK_ERR_CUDA, "no CUDA device visible");
+  if (n < 0 || batch < 0 || lda < n) return fail(HK_ERR_VALUE, "bad gj_inverse dimensions");
+  if (n == 0 || batch == 0) return HK_OK;
+  if (n > INT32_MAX) return fail(HK_ERR_VALUE, "gj_inverse matrix too large");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t scr = hk_gj_scratch_bytes((int)n);
+  char* scratch = nullptr;
+  int32_t* stt = nullptr;
+  GjTask* td = nullptr;
+  if (scr) CU(cudaMallocAsync((void**)&scratch, scr * (size_t)batch, st));
+  CU(cudaMallocAsync((void**)&stt, (size_t)batch * 4, st));
+  std::vector<GjTask> tasks((size_t)batch);
+  for (int64_t b = 0; b < batch; ++b) {
+    GjTask& t = tasks[(size_t)b];
+    t.src = A + b * stride;
+    t.src_ld = lda;
+    t.out = out + b * n * n;
+    t.out_ld = n;
+    t.scratch = scr ? reinterpret_cast<double*>(scratch + scr * (size_t)b) : nullptr;
+    t.status = stt + b;
+    t.N = (int32_t)n;
+    t.mode = 0;
+  }
+  CU(cudaMallocAsync((void**)&td, sizeof(GjTask) * tasks.size(), st));
+  CU(cudaMemcpyAsync(td, tasks.data(), sizeof(GjTask) * tasks.size(), cudaMemcpyHostToDevice, st));
+  CU(hk_launch_gj(td, (int)batch, (int)n, st));
+  CU(cudaMemcpyAsync(status_host, stt, (size_t)batch * 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  cudaFreeAsync(td, st);
+  cudaFreeAsync(stt, st);
+  if (scratch) cudaFreeAsync(scratch, st);
+  return HK_OK;
+}
+
 extern "C" hk_status hk_aca_block(const double* a, int64_t m, int64_t n, int64_t ld, double tol2,
                                   int64_t cap, double* U, double* V, int64_t* rank,
                                   int32_t* trows, int64_t* nrows, int32_t* tcols, int64_t* ncols,

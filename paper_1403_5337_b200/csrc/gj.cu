@@ -343,6 +343,164 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_df_kernel(const GjTask* __restr
     }
 }
 
+// Cluster Gauss-Jordan for 160 < N <= 256 (config 4's capacitance matrices,
+// r up to 227): the matrix no longer fits one SM's registers, so it is spread
+// over a cluster of P = ceil(N / (NW*CPW)) CTAs, still register-resident.
+// Global warp g = cta*NW + warp owns columns g*CPW + jj; panel g is that
+// warp's column block.  Per panel, exactly as gj_blk_kernel: the owner runs
+// its CPW pivot steps warp-synchronously and leaves the pre-step pivot columns,
+// pivot rows and reciprocals in its CTA's SMEM (double-buffered by panel
+// parity); one cluster barrier; every other warp of every CTA reads them
+// through DSMEM and replays the steps on its own columns.  Same pivoting and
+// per-element arithmetic as gj_blk_kernel / gj_df_kernel, so the inverse is
+// bit-identical to theirs.
+template <int NW, int CPW, int RPL>
+__global__ void __launch_bounds__(NW * 32, 1) gj_cl_kernel(const GjTask* __restrict__ tasks) {
+  constexpr int NT = NW * 32;
+  constexpr int NR = 32 * RPL;
+  const unsigned P = cl_nrank(), cta = cl_rank();
+  const GjTask t = tasks[blockIdx.x / P];
+  const int N = __shfl_sync(0xffffffffu, t.N, 0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = uniform_warp_id();
+  const int gw = (int)cta * NW + warp;   // global warp = panel index it owns
+  __shared__ double ckbuf[2][CPW][NR];
+  __shared__ double rinvbuf[2][CPW];
+  __shared__ int pbuf[2][CPW];
+  __shared__ int s_sing, pivrow[NR], invp[NR];
+  if (N == 0) {
+    if (tid == 0 && cta == 0) *t.status = 0;
+    cluster_bar();
+    return;
+  }
+  double w_[CPW][RPL];
+#pragma unroll
+  for (int jj = 0; jj < CPW; ++jj)
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+      const int i = lane + 32 * q, j = gw * CPW + jj;
+      const bool in = i < N && j < N;
+      const int64_t off = t.mode == 0 ? (int64_t)i * t.src_ld + j : i + (int64_t)j * t.src_ld;
+      w_[jj][q] = in ? t.src[off] : 0.0;
+    }
+  unsigned used = 0;                     // bit q: row lane + 32q already a pivot row
+  if (tid == 0) s_sing = 0;
+  cluster_bar();
+  const int npan = (N + CPW - 1) / CPW;
+  int singular = 0;
+  for (int Pn = 0; Pn < npan; ++Pn) {
+    const int buf = Pn & 1;
+    const int nl = min(CPW, N - Pn * CPW);
+    const unsigned oc = (unsigned)(Pn / NW);     // owner CTA
+    if (gw == Pn) {
+      int sing = 0;
+#pragma unroll
+      for (int l = 0; l < CPW; ++l) {
+        if (l >= nl) break;
+        const int c = Pn * CPW + l;
+        double bv = 0.0, bw = 1.0;
+        int bi = 0x7fffffff;
+        bool have = false;
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+          const int i = lane + 32 * q;
+          const double av = fabs(w_[l][q]);
+          if (i < N && !((used >> q) & 1u) && (!have || av > bv)) {
+            bv = av; bw = w_[l][q]; bi = i; have = true;
+          }
+        }
+        const double myrinv = __drcp_rn(bw);
+        const int p = warp_argmax_idx(bv, have, bi);
+        const int lp = p & 31, qp = p >> 5;
+        const double pivabs = __shfl_sync(0xffffffffu, bv, lp);
+        if (!(pivabs >= HK_PIVOT_FLOOR)) { sing = 1; break; }
+        const double rinv = __shfl_sync(0xffffffffu, myrinv, lp);
+        double ck[RPL];
+        bool isp[RPL];
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+          const int i = lane + 32 * q;
+          ck[q] = w_[l][q];
+          isp[q] = i == p;
+          if (i < N) ckbuf[buf][l][i] = ck[q];
+        }
+        if (lane == lp) used |= 1u << qp;
+        if (lane == 0) {
+          rinvbuf[buf][l] = rinv;
+          pbuf[buf][l] = p;
+          pivrow[c] = p;
+        }
+#pragma unroll
+        for (int jj = 0; jj < CPW; ++jj) {
+          if (jj == l) {
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) w_[jj][q] = isp[q] ? rinv : -ck[q] * rinv;
+          } else {
+            double src = w_[jj][0];
+#pragma unroll
+            for (int q = 1; q < RPL; ++q) src = (qp == q) ? w_[jj][q] : src;
+            const double rj = __shfl_sync(0xffffffffu, src, lp) * rinv;
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) {
+              const double v = fma(-ck[q], rj, w_[jj][q]);
+              w_[jj][q] = isp[q] ? rj : v;
+            }
+          }
+        }
+      }
+      if (sing && lane == 0) s_sing = 1;
+    }
+    cluster_bar();
+    singular = __shfl_sync(0xffffffffu, *cl_map(&s_sing, oc), 0);
+    if (singular) break;
+    if (gw != Pn) {
+      const int* pb = cl_map(&pbuf[buf][0], oc);
+      const double* rb = cl_map(&rinvbuf[buf][0], oc);
+      const double* cb = cl_map(&ckbuf[buf][0][0], oc);
+#pragma unroll 1
+      for (int l = 0; l < nl; ++l) {
+        const int p = __shfl_sync(0xffffffffu, pb[l], 0);
+        const double rinv = rb[l];
+        if (cta != oc && tid == 0) pivrow[Pn * CPW + l] = p;
+        const int qp = p >> 5, lp = p & 31;
+        if (lane == lp) used |= 1u << qp;
+        double ck[RPL];
+        bool isp[RPL];
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+          const int i = lane + 32 * q;
+          ck[q] = (i < N) ? cb[l * NR + i] : 0.0;
+          isp[q] = i == p;
+        }
+#pragma unroll
+        for (int jj = 0; jj < CPW; ++jj) {
+          double src = w_[jj][0];
+#pragma unroll
+          for (int q = 1; q < RPL; ++q) src = (qp == q) ? w_[jj][q] : src;
+          const double rj = __shfl_sync(0xffffffffu, src, lp) * rinv;
+#pragma unroll
+          for (int q = 0; q < RPL; ++q) {
+            const double v = fma(-ck[q], rj, w_[jj][q]);
+            w_[jj][q] = isp[q] ? rj : v;
+          }
+        }
+      }
+    }
+  }
+  if (tid == 0 && cta == 0) *t.status = singular;
+  // every CTA has read every other CTA's panel buffers and recorded all pivots
+  cluster_bar();
+  if (singular) return;
+  for (int k = tid; k < N; k += NT) invp[pivrow[k]] = k;
+  __syncthreads();
+#pragma unroll
+  for (int jj = 0; jj < CPW; ++jj)
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+      const int r = lane + 32 * q, j = gw * CPW + jj;
+      if (r < N && j < N) t.out[invp[r] + (int64_t)pivrow[j] * t.out_ld] = w_[jj][q];
+    }
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT) gj_kernel(const GjTask* __restrict__ tasks, size_t smem_bytes) {
   const GjTask t = tasks[blockIdx.x];
@@ -474,11 +632,35 @@ static cudaError_t launch_gj_reg(const GjTask* tasks_dev, int ntasks, int maxN, 
   return cudaGetLastError();
 }
 
+// 160 < N <= 256: cluster of P = ceil(N / 32) CTAs (8 warps x 4 columns each)
+constexpr int kGjClNW = 8, kGjClCPW = 4, kGjClRPL = 8, kGjClRows = 32 * kGjClRPL;
+static cudaError_t launch_gj_cluster(const GjTask* tasks_dev, int ntasks, int maxN, cudaStream_t st) {
+  const int cols = kGjClNW * kGjClCPW;
+  const int P = (maxN + cols - 1) / cols;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)P;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3((unsigned)(P * ntasks));
+  cfg.blockDim = dim3(kGjClNW * 32);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gj_cl_kernel<kGjClNW, kGjClCPW, kGjClRPL>, tasks_dev);
+  hk_count_launch();
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 cudaError_t hk_launch_gj(const GjTask* tasks_dev, int ntasks, int maxN, cudaStream_t st) {
   if (ntasks == 0) return cudaSuccess;
   if (maxN <= 64) return launch_gj_reg<8, 8, 2>(tasks_dev, ntasks, maxN, st);
   if (maxN <= 128) return launch_gj_reg<16, 8, 4>(tasks_dev, ntasks, maxN, st);
   if (maxN <= 160) return launch_gj_reg<16, 10, 5>(tasks_dev, ntasks, maxN, st);
+  if (maxN <= kGjClRows) return launch_gj_cluster(tasks_dev, ntasks, maxN, st);
   size_t need = gj_bytes(maxN);
   size_t smem = need <= GJ_SMEM_CAP ? need : 0;
   cudaError_t e;
@@ -497,4 +679,6 @@ cudaError_t hk_launch_gj(const GjTask* tasks_dev, int ntasks, int maxN, cudaStre
   return cudaGetLastError();
 }
 
-size_t hk_gj_scratch_bytes(int N) { return gj_bytes(N) <= GJ_SMEM_CAP ? 0 : gj_bytes(N); }
+size_t hk_gj_scratch_bytes(int N) {
+  return (N <= kGjClRows || gj_bytes(N) <= GJ_SMEM_CAP) ? 0 : gj_bytes(N);
+}

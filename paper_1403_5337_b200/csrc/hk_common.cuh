@@ -138,6 +138,29 @@ __device__ __forceinline__ double block_sum(double a, double* s) {
   return r;
 }
 
+// ---- thread-block clusters: barrier, rank, distributed-shared-memory mapping
+__device__ __forceinline__ void cluster_bar() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::
+                   : "memory");
+}
+__device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cl_nrank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+// generic address of the same shared variable in CTA `rank` of the cluster
+template <class T>
+__device__ __forceinline__ const T* cl_map(const T* p, unsigned rank) {
+  uint64_t out;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(p), "r"(rank));
+  return reinterpret_cast<const T*>(out);
+}
+
 // FP64 tensor-core MMA (DMMA.8x8x4 on sm_100a; tcgen05 has no f64 kind).
 // Fragment layout (PTX ISA, mma.m8n8k4 .f64): gid = lane>>2, tig = lane&3;
 //   A (8x4, row):  a  = A[gid][tig]

@@ -95,6 +95,34 @@ def lu_partial(a) -> PartialPivLU:
     return PartialPivLU(at.cpu().numpy(), pv, _row_perm_from_piv(pv), inv.cpu().numpy())
 
 
+def gj_inverse(a) -> np.ndarray:
+    """Explicit inverse(s) by the factorization's batched Gauss-Jordan kernels
+    (hk_gj_inverse): `a` is (n, n) or (batch, n, n).  Same implicit partial
+    pivoting and singularity test as lu_partial (dense.py:76-77); raises
+    SingularMatrixError naming the first singular matrix."""
+    a = np.asarray(a, dtype=np.float64)
+    single = a.ndim == 2
+    a3 = a[None] if single else a
+    if a3.ndim != 3 or a3.shape[1] != a3.shape[2]:
+        raise ValueError(f"expected (n, n) or (batch, n, n), got {a.shape}")
+    if not np.all(np.isfinite(a3)):
+        raise ValueError("matrix contains NaN or Inf")
+    bsz, n, _ = a3.shape
+    if n == 0 or bsz == 0:
+        return np.zeros_like(a)
+    torch = N.require_cuda()
+    at = torch.from_numpy(np.ascontiguousarray(a3)).cuda()
+    out = torch.empty_like(at)
+    status = np.zeros(bsz, dtype=np.int32)
+    N.check(N.lib().hk_gj_inverse(N.ptr(at), n, n, bsz, n * n, N.ptr(out),
+                                  status.ctypes.data, N.stream_handle()))
+    if status.any():
+        raise SingularMatrixError(f"matrix {int(np.argmax(status))}: pivot magnitude below "
+                                  f"{PIVOT_UNDERFLOW:g}")
+    inv = out.cpu().numpy().transpose(0, 2, 1)     # column-major -> row-major
+    return np.ascontiguousarray(inv[0] if single else inv)
+
+
 @dataclass(frozen=True)
 class FullPivLU:
     """A[row_perm][:, col_perm] = L U with complete pivoting (dense.py:84-130)."""

@@ -52,6 +52,25 @@ def test_aca_kernel_bit_exact_on_golden_blocks():
         assert np.array_equal(f.v, g[f"{name}_V"]), name
 
 
+def test_aca_cluster_path_bit_exact():
+    """Every block forced onto the thread-block-cluster ACA (HK_ACA_CLMIN=0, read
+    once per process, hence the subprocess): pivots, ranks and U/V stay
+    bit-identical to the reference's goldens and to a config-0-style front's
+    single-CTA factors."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path.insert(0, 'tests'); sys.path.insert(0, '.');"
+        "import test_gpu_parity as T; T.test_aca_kernel_bit_exact_on_golden_blocks();"
+        "T.test_baseline_aca_front_parity(0, 'cfg0'); print('ok')")
+    env = dict(os.environ, HK_ACA_CLMIN="0")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-4000:]
+
+
 def test_complete_pivot_kernel_bit_exact():
     g = golden("lu_full")
     for name in g["names"]:
@@ -75,6 +94,25 @@ def test_partial_pivot_lu_and_inverse(rng):
         assert np.linalg.norm(a @ f.solve(b) - b) <= 1e-10 * np.linalg.norm(b)
     with pytest.raises(hk.SingularMatrixError):
         hk.lu_partial(np.zeros((3, 3)))
+
+
+def test_gj_inverse_all_kernel_shapes(rng):
+    """Every Gauss-Jordan variant (register dataflow N<=128, panel N<=160, the
+    thread-block-cluster kernel 160<N<=256, the global-memory one above)
+    against numpy's inverse, including batches of mixed conditioning and a
+    singular member."""
+    from paper_1403_5337_b200.dense import gj_inverse
+    for n in (1, 17, 64, 100, 128, 150, 160, 161, 190, 227, 255, 256, 300):
+        a = rng.standard_normal((3, n, n)) + 0.5 * np.sqrt(n) * np.eye(n)
+        a[1] = a[1][rng.permutation(n)]          # pivoting must find the diagonal
+        inv = gj_inverse(a)
+        for b in range(3):
+            ref = np.linalg.inv(a[b])
+            assert np.linalg.norm(inv[b] - ref) <= 1e-11 * np.linalg.norm(ref), (n, b)
+    a = rng.standard_normal((2, 200, 200))
+    a[1, :, 7] = 0.0
+    with pytest.raises(hk.SingularMatrixError):
+        gj_inverse(a)
 
 
 # ------------------------------------------------------------------ HODLR on golden fronts
