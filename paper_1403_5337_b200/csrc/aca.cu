@@ -958,12 +958,18 @@ int hk_aca_class(int m, int n) {
   return L > 256 ? 0 : L > 128 ? 1 : L > 64 ? 2 : 3;
 }
 
+// Per-warp dot partials live in SMEM when the CTA's whole footprint stays
+// under this bound (2 CTAs per SM still fit); otherwise in global scratch.
+#ifndef HK_ACA_PART_SMEM
+#define HK_ACA_PART_SMEM (112 * 1024)
+#endif
+
 template <int NT, int EPT, int DB>
 static cudaError_t launch_cls(const AcaTask* tasks_dev, int ntasks, int max_cap, int max_m,
                               double tol2, int* counter, cudaStream_t st) {
   const size_t part_bytes = (size_t)(2 * (NT / 32) + 1) * max_cap * 8;
   const size_t base = (size_t)(max_cap + KC) * 8 + (size_t)max_m + 16;
-  const int part_in_smem = (base + part_bytes <= 64 * 1024) ? 1 : 0;
+  const int part_in_smem = (base + part_bytes <= HK_ACA_PART_SMEM) ? 1 : 0;
   const size_t smem = base + (part_in_smem ? part_bytes : 0);
   cudaError_t e = cudaFuncSetAttribute(aca_kernel<NT, EPT, DB>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
