@@ -294,6 +294,8 @@ struct hk_plan {
   DevBuf At, UV, ranks_d, trace_d, tasks_d, aca_scr, aca_cnt;
   cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaStream_t cl_side[4] = {nullptr, nullptr, nullptr, nullptr};   // cluster ACA groups
+  std::vector<cudaEvent_t> fev;     // factor: staging-commit events (front-group streams)
+  size_t gjs_need = 0;              // factor: large-GJ global scratch bytes (0 = none)
   cudaEvent_t cl_side_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t side_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<int32_t> ranks;       // batch * nblocks
@@ -327,6 +329,8 @@ struct hk_plan {
     for (auto& x : cl_side)
       if (x) cudaStreamDestroy(x);
     for (auto& x : cl_side_ev)
+      if (x) cudaEventDestroy(x);
+    for (auto& x : fev)
       if (x) cudaEventDestroy(x);
     DevBuf* bufs[] = {&aca_cnt, &aca_scr, &At, &UV, &ranks_d, &trace_d, &tasks_d, &sel_d, &work_d, &perm_d,
                       &skel_status_d, &probe_d, &Y, &Ytmp, &F, &I, &ftask_d, &fmap_d, &gj_d, &gj2_d, &gjs_d,
@@ -1066,8 +1070,7 @@ struct OpProfile {
 static OpProfile g_opprof;
 
 // commit the staged task arrays and launch the ops planned so far
-static hk_status flush(hk_plan* p, std::vector<Op>& ops, cudaStream_t st) {
-  CU(p->stage.commit(st));
+static hk_status launch_ops(hk_plan* p, std::vector<Op>& ops, cudaStream_t st) {
   const bool prof = host_profile();
   for (const Op& o : ops) {
     char lbl[64] = "";
@@ -1081,6 +1084,11 @@ static hk_status flush(hk_plan* p, std::vector<Op>& ops, cudaStream_t st) {
   }
   ops.clear();
   return HK_OK;
+}
+
+static hk_status flush(hk_plan* p, std::vector<Op>& ops, cudaStream_t st) {
+  CU(p->stage.commit(st));
+  return launch_ops(p, ops, st);
 }
 
 extern "C" hk_status hk_factor_ext(hk_plan* p, const double* Zext, int64_t ldz, int64_t wext,
@@ -1171,10 +1179,50 @@ extern "C" hk_status hk_factor_ext(hk_plan* p, const double* Zext, int64_t ldz, 
         }
       need = std::max(need, lv);
     }
+    p->gjs_need = need;
     if (need) CU(p->gjs_d.ensure(need + 256, st));
   }
   p->stage.reset();
-  std::vector<Op> ops;
+  // Front groups: the fronts of a batch are independent, so G groups run
+  // their factorization chains on G streams and one group's latency-bound
+  // Gauss-Jordan phases overlap another's GEMMs (HK_FACTOR_GROUPS, default 2
+  // for batches of >= 4 fronts; 1 when large GJ systems share the scratch).
+  int G = 1;
+  {
+    const char* e = getenv("HK_FACTOR_GROUPS");
+    const int want = e ? atoi(e) : 2;
+    if (want > 1 && p->batch >= 2 * want && p->gjs_need == 0 && wext == 0) G = std::min(want, 4);
+  }
+  std::vector<std::vector<Op>> gops((size_t)G);
+  std::vector<cudaStream_t> gst((size_t)G, st);
+  if (G > 1) {
+    CHK(ensure_side_streams(p));
+    CU(cudaEventRecord(p->ev[3], st));
+    for (int g = 0; g < G; ++g) {
+      gst[g] = p->side[g];
+      CU(cudaStreamWaitEvent(gst[g], p->ev[3], 0));
+    }
+  }
+  auto grp_lo = [&](int g) { return p->batch * g / G; };
+  auto grp_hi = [&](int g) { return p->batch * (g + 1) / G; };
+  // commit the staged task arrays on `st`, then launch every group's ops on its stream
+  int phase = 0;
+  auto launch_groups = [&]() -> hk_status {
+    if (G == 1) return flush(p, gops[0], st);
+    CU(p->stage.commit(st));
+    if ((int)p->fev.size() <= phase) {
+      cudaEvent_t e;
+      CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      p->fev.push_back(e);
+    }
+    CU(cudaEventRecord(p->fev[phase], st));
+    for (int g = 0; g < G; ++g) {
+      CU(cudaStreamWaitEvent(gst[g], p->fev[phase], 0));
+      CHK(launch_ops(p, gops[g], gst[g]));
+    }
+    ++phase;
+    return HK_OK;
+  };
   double* Y = p->Y.as<double>();
   double* Yt = p->Ytmp.as<double>();
   double* F = p->F.as<double>();
@@ -1182,8 +1230,10 @@ extern "C" hk_status hk_factor_ext(hk_plan* p, const double* Zext, int64_t ldz, 
   const double* UV = p->UV.as<double>();
 
   // ---- Z gather: U of every block into the rows of its child, columns [w_p, w_p + r)
+  for (int g = 0; g < G; ++g) {
+  std::vector<Op>& ops = gops[g];
   std::vector<CopyTask> copies;
-  for (int64_t f = 0; f < p->batch; ++f)
+  for (int64_t f = grp_lo(g); f < grp_hi(g); ++f)
     for (int k = 0; k < (int)p->internal.size(); ++k) {
       const int s = p->internal[k];
       const NodeRec& r = p->rec[f * nn + s];
@@ -1221,7 +1271,7 @@ extern "C" hk_status hk_factor_ext(hk_plan* p, const double* Zext, int64_t ldz, 
   // ---- leaves: Gauss-Jordan inverse, then Y = K^{-1} Z (hodlr.py:222-232)
   {
     std::vector<GjTask> gts;
-    for (int64_t f = 0; f < p->batch; ++f)
+    for (int64_t f = grp_lo(g); f < grp_hi(g); ++f)
       for (int s : p->leaves) {
         const Node& nd = p->nodes[s];
         const NodeRec& r = p->rec[f * nn + s];
@@ -1237,7 +1287,7 @@ extern "C" hk_status hk_factor_ext(hk_plan* p, const double* Zext, int64_t ldz, 
       }
     CHK(stage_gj(p, ops, gts, st));
     TileList tl;
-    for (int64_t f = 0; f < p->batch; ++f)
+    for (int64_t f = grp_lo(g); f < grp_hi(g); ++f)
       for (int s : p->leaves) {
         const Node& nd = p->nodes[s];
         const NodeRec& r = p->rec[f * nn + s];
@@ -1248,13 +1298,14 @@ extern "C" hk_status hk_factor_ext(hk_plan* p, const double* Zext, int64_t ldz, 
       }
     CHK(stage_tiles(p, ops, tl, st));
   }
-  {
+  if (g == 0) {
     Op o{Op::EVENT};
     o.ev = 1;
     ops.push_back(o);
   }
+  }
   hc.mark("plan leaves");
-  CHK(flush(p, ops, st));        // the GPU starts on the leaves while the levels are planned
+  CHK(launch_groups());          // the GPU starts on the leaves while the levels are planned
 
   // ---- upward sweep, deepest internal level first (hodlr.py:264-282).
   // The coupling system S = [[I, X], [Y, I]] (X = V_low^T d_left, Y = V_up^T
@@ -1263,9 +1314,11 @@ extern "C" hk_status hk_factor_ext(hk_plan* p, const double* Zext, int64_t ldz, 
   // factored, with partial pivoting; S^{-1} is assembled by GEMMs and kept
   // for the solve phase.  det S = det M, so singular S <=> singular M.
   for (int lvl = p->depth - 1; lvl >= 0; --lvl) {
+  for (int g = 0; g < G; ++g) {
+    std::vector<Op>& ops = gops[g];
     TileList th, tm, t4, t5, tq, tu;
     std::vector<GjTask> gts;
-    for (int64_t f = 0; f < p->batch; ++f)
+    for (int64_t f = grp_lo(g); f < grp_hi(g); ++f)
       for (int k = 0; k < (int)p->internal.size(); ++k) {
         const int s = p->internal[k];
         const Node& nd = p->nodes[s];
@@ -1328,7 +1381,14 @@ extern "C" hk_status hk_factor_ext(hk_plan* p, const double* Zext, int64_t ldz, 
     CHK(stage_tiles(p, ops, t5, st));
     CHK(stage_tiles(p, ops, tq, st));
     CHK(stage_tiles(p, ops, tu, st));
-    CHK(flush(p, ops, st));
+  }
+    CHK(launch_groups());
+  }
+  if (G > 1) {                   // join the group streams
+    for (int g = 0; g < G; ++g) {
+      CU(cudaEventRecord(p->side_ev[g], gst[g]));
+      CU(cudaStreamWaitEvent(st, p->side_ev[g], 0));
+    }
   }
   CU(cudaEventRecord(p->ev[2], st));
   hc.mark("plan+launch levels");
