@@ -368,3 +368,191 @@ def kernel_matrix(n: int, kind: str = "inv-distance", shift: float = 0.0) -> np.
     if shift:
         a = a + shift * np.eye(n)
     return a
+
+
+# ---------------------------------------------------------------------------
+# BASELINE config 2: unstructured-graph front (not in the reference; SURVEY.md
+# §8(d) cfg 2 and Appendix A.3).  Points uniform in the unit cube, the union-
+# symmetrised k-nearest-neighbour graph Laplacian L = D - W + shift*I, the slab
+# S = {|x - 1/2| <= h} as the "separator" (not a true separator: a few kNN
+# edges cross it, so every non-slab vertex is eliminated jointly), the front
+# F = L_SS - L_SI L_II^{-1} L_IS, and S ordered by recursive coordinate
+# bisection whose split sizes match build_tree's ceil(size/2).
+
+@dataclass(frozen=True)
+class KnnFront:
+    """Dense slab front in RCB order, its induced kNN graph (same order), the
+    slab vertex ids in that order, and generation diagnostics."""
+
+    front: np.ndarray
+    graph: SparsePattern
+    ordering: np.ndarray
+    info: dict
+
+    @property
+    def n(self) -> int:
+        return self.front.shape[0]
+
+    def accessor(self) -> BlockAccessor:
+        return BlockAccessor.from_matrix(self.front, pattern=self.graph)
+
+
+def knn_points(npoints: int, seed: int = 2) -> np.ndarray:
+    """``default_rng(seed).random((npoints, 3))`` (BASELINE config 2)."""
+    return np.random.default_rng(seed).random((int(npoints), 3))
+
+
+def knn_graph(points: np.ndarray, k: int = 8, device=None, chunk: int = 2048) -> SparsePattern:
+    """Union-symmetrised k-nearest-neighbour adjacency (no self loops).
+
+    Exact squared distances (difference form, no |p|^2+|q|^2-2pq
+    cancellation), the k smallest per point by a stable sort of
+    (distance, index), so ties resolve to the lower index on any device.
+    """
+    torch = _torch()
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    npnt = pts.shape[0]
+    if k < 1 or k >= npnt:
+        raise ValueError("need 1 <= k < number of points")
+    dev = torch.device(device or "cpu")
+    if dev.type == "cpu":                  # host: a k-d tree gives the same neighbour sets
+        from scipy.spatial import cKDTree
+        _, nb = cKDTree(pts).query(pts, k + 1)
+        nb = nb[:, 1:] if np.all(nb[:, 0] == np.arange(npnt)) else _drop_self(nb, k)
+        return SparsePattern.from_edges(npnt, np.repeat(np.arange(npnt), k), nb.ravel())
+    P = torch.from_numpy(pts).to(dev)
+    nbr = np.empty((npnt, k), dtype=np.int64)
+    for c0 in range(0, npnt, chunk):
+        q = P[c0:c0 + chunk]
+        d2 = ((q[:, None, 0] - P[None, :, 0]) ** 2 + (q[:, None, 1] - P[None, :, 1]) ** 2
+              + (q[:, None, 2] - P[None, :, 2]) ** 2)
+        rows = torch.arange(q.shape[0], device=dev)
+        d2[rows, rows + c0] = float("inf")                      # no self loops
+        # k + a margin of candidates, then an exact stable (distance, index) order
+        cand_d, cand_i = torch.topk(d2, min(k + 8, npnt - 1), dim=1, largest=False, sorted=False)
+        key_i, order = torch.sort(cand_i, dim=1)
+        cand_d = torch.gather(cand_d, 1, order)
+        _, o2 = torch.sort(cand_d, dim=1, stable=True)
+        nbr[c0:c0 + q.shape[0]] = torch.gather(key_i, 1, o2)[:, :k].cpu().numpy()
+    rows = np.repeat(np.arange(npnt), k)
+    return SparsePattern.from_edges(npnt, rows, nbr.ravel())
+
+
+def _drop_self(nb: np.ndarray, k: int) -> np.ndarray:
+    out = np.empty((nb.shape[0], k), dtype=nb.dtype)
+    for i, row in enumerate(nb):
+        out[i] = row[row != i][:k]
+    return out
+
+
+def rcb_order(points: np.ndarray, leaf: int) -> np.ndarray:
+    """Recursive coordinate bisection: split along the widest coordinate, the
+    first ceil(size/2) points (stable sort by that coordinate, then index)
+    going left, until a part has <= leaf points -- the split sizes of
+    build_tree(n, leaf) (src/hodlr.py:76-102).  Returns positions into
+    ``points``."""
+    pts = np.asarray(points, dtype=np.float64)
+    out = []
+    stack = [np.arange(pts.shape[0])]
+    while stack:
+        idx = stack.pop()
+        if idx.size <= leaf:
+            out.append(idx)
+            continue
+        ext = pts[idx].max(axis=0) - pts[idx].min(axis=0)
+        ax = int(np.argmax(ext))
+        srt = idx[np.argsort(pts[idx, ax], kind="stable")]
+        half = (idx.size + 1) // 2
+        stack.append(srt[half:])
+        stack.append(srt[:half])
+    return np.concatenate(out) if out else np.zeros(0, dtype=np.intp)
+
+
+def _laplacian_csr(graph: SparsePattern, shift: float):
+    """L = D - W + shift*I as scipy CSR (unit edge weights)."""
+    import scipy.sparse as sp
+    n = graph.n
+    deg = np.diff(graph.indptr).astype(np.float64)
+    W = sp.csr_matrix((np.ones(graph.nnz), graph.indices, graph.indptr), shape=(n, n))
+    return (sp.diags(deg + shift) - W).tocsr()
+
+
+def _torch_csr(M, dev):
+    torch = _torch()
+    M = M.tocsr()
+    return torch.sparse_csr_tensor(torch.from_numpy(M.indptr.astype(np.int64)),  # noqa
+                                   torch.from_numpy(M.indices.astype(np.int64)),
+                                   torch.from_numpy(M.data.astype(np.float64)), size=M.shape,
+                                   dtype=torch.float64).to(dev)
+
+
+def _cg_solve_block(L_II, L_IS, device, tol, max_iter):
+    """Jacobi-preconditioned block CG (every column its own alpha/beta) for
+    L_II X = L_IS on `device` in fp64 with torch sparse CSR products; the
+    dense right-hand sides are formed on the device."""
+    torch = _torch()
+    dev = torch.device(device)
+    A = _torch_csr(L_II, dev)
+    dinv = torch.from_numpy(1.0 / L_II.diagonal()).to(dev)[:, None]
+    Bt = _torch_csr(L_IS, dev).to_dense()
+    X = torch.zeros_like(Bt)
+    R = Bt.clone()
+    Z = dinv * R
+    Pm = Z.clone()
+    rz = (R * Z).sum(0)
+    bn = torch.linalg.vector_norm(Bt, dim=0).clamp_min(1e-300)
+    its = 0
+    for its in range(1, max_iter + 1):
+        AP = A @ Pm
+        pap = (Pm * AP).sum(0)
+        alpha = torch.where(pap > 0, rz / torch.where(pap > 0, pap, 1.0), 0.0)
+        X += alpha * Pm
+        R -= alpha * AP
+        rel = torch.linalg.vector_norm(R, dim=0) / bn
+        if its % 10 == 0 and float(rel.max()) <= tol:
+            break
+        Z = dinv * R
+        rz_new = (R * Z).sum(0)
+        Pm = Z + torch.where(rz > 0, rz_new / torch.where(rz > 0, rz, 1.0), 0.0) * Pm
+        rz = rz_new
+    return X, its, float(rel.max())
+
+
+def knn_front(npoints: int = 200000, k: int = 8, shift: float = 1e-3, h: float = 0.005,
+              seed: int = 2, leaf: int = 64, device=None, solver: str = "auto",
+              cg_tol: float = 1e-13, cg_max_iter: int = 20000) -> KnnFront:
+    """BASELINE config 2 front (module note above).  ``solver``: "direct"
+    (scipy SuperLU on the host; small problems), "cg" (block CG on `device`,
+    the 200k-point case on a B200) or "auto" (direct below 40k interior
+    vertices)."""
+    import scipy.sparse.linalg as spla
+    pts = knn_points(npoints, seed)
+    graph = knn_graph(pts, k, device=device)
+    L = _laplacian_csr(graph, shift)
+    slab = np.flatnonzero(np.abs(pts[:, 0] - 0.5) <= h)
+    if slab.size == 0:
+        raise ValueError("empty slab")
+    order = slab[rcb_order(pts[slab], leaf)]
+    interior = np.setdiff1d(np.arange(npoints), order)
+    L_SS = L[order][:, order].toarray()
+    L_IS = L[interior][:, order].tocsc()
+    L_II = L[interior][:, interior].tocsc()
+    crossing = 0
+    left = pts[interior, 0] < 0.5
+    li = L[interior][:, interior].tocoo()
+    crossing = int(np.count_nonzero(left[li.row] != left[li.col]))
+    if solver == "auto":
+        solver = "direct" if interior.size <= 40000 else "cg"
+    info = {"npoints": int(npoints), "k": k, "shift": shift, "h": h, "n": int(order.size),
+            "crossing_directed_edges": crossing, "solver": solver}
+    if solver == "direct":
+        X = spla.splu(L_II).solve(L_IS.toarray())
+        front = L_SS - (L_IS.T @ X)
+    else:
+        torch = _torch()
+        dev = torch.device(device or "cuda")
+        Xt, its, rel = _cg_solve_block(L_II, L_IS, dev, cg_tol, cg_max_iter)
+        info.update(cg_iterations=its, cg_rel_residual=rel)
+        front = L_SS - (_torch_csr(L_IS.T, dev) @ Xt).cpu().numpy()
+        del Xt
+    return KnnFront(np.ascontiguousarray(front), graph.induced(order), order, info)
