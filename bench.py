@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cfg4", action="store_true",
                     help="skip the BASELINE config-4 line item (96^3 front, GMRES time-to-1e-10)")
+    ap.add_argument("--no-cfg12", action="store_true",
+                    help="skip the BASELINE config-1 (48^3 BDLR) and config-2 (kNN slab, ACA vs "
+                         "BDLR) line items")
     return ap.parse_args()
 
 
@@ -369,6 +372,11 @@ def run_ours(args):
     if not args.no_cfg4:
         c4 = run_cfg4(dev, rank, world, hbm_peak)
 
+    # ---- BASELINE configs 1 and 2: one front each, replicas only (rank 0 reports)
+    c1 = c2 = None
+    if not args.no_cfg12 and rank == 0:
+        c1, c2 = run_cfg12(dev)
+
     # per-front ranks of every rank's fronts (the one end-of-run gather)
     all_ranks = MF.gather_front_scalars(batch.ranks.astype(np.int64), device=dev)
     if rank == 0:
@@ -377,7 +385,7 @@ def run_ours(args):
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": config_dict(args, world), "impl": "ours",
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roof,
-                "cpu_baseline": cpu, "gmres": gm, "cfg4": c4,
+                "cpu_baseline": cpu, "gmres": gm, "cfg4": c4, "cfg1": c1, "cfg2": c2,
                 "ranks_per_level_front0": [e["max_rank"] for e in batch.report(0).ranks_per_level],
                 "fronts_gathered": int(all_ranks.shape[0]),
                 "max_block_rank_all_fronts": int(all_ranks.max())}
@@ -461,6 +469,82 @@ def run_cfg4(dev, rank, world, hbm_peak):
     if ranks is not None:
         out["max_rank_per_level"] = ranks
     return out
+
+
+def _single_front_item(dev, A, graph, schemes, leaf, gmres_tol, rhs_seed):
+    """Warm build+factor (CUDA events), GMRES time-to-tol, ranks, and the CPU
+    oracle's build+factor on the same front (1 thread), per scheme."""
+    import time
+    import torch
+    import paper_1403_5337_b200 as hk
+    from paper_1403_5337_b200.hodlr import HodlrBatch
+    from oracle import hodlr_oracle as O          # CPU side-by-side only
+    n = A.shape[0]
+    Ad = torch.from_numpy(A).to(dev).contiguous()
+    b = np.random.default_rng(rhs_seed).standard_normal(n)
+    csr = (np.asarray(graph.indptr, dtype=np.int64), np.asarray(graph.indices, dtype=np.int64)) \
+        if graph is not None else None
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    out = {}
+    for scheme, depth in schemes:
+        cfg = hk.CompressionConfig(scheme, tol=1e-4, depth=depth)
+        batch = HodlrBatch(n, leaf, 1)
+        g = csr if scheme == "bdlr" else None
+        batch.factorize(Ad[None], cfg, graph=g)                 # warm
+        ms = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            ev[0].record()
+            batch.factorize(Ad[None], cfg, graph=g)
+            ev[1].record()
+            torch.cuda.synchronize()
+            ms.append(ev[0].elapsed_time(ev[1]))
+        fact = batch.factorization(0)
+        op = hk.DenseOperator(Ad)
+        hk.gmres(op, b, hk.GmresConfig(tol=gmres_tol), preconditioner=fact)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = hk.gmres(op, b, hk.GmresConfig(tol=gmres_tol), preconditioner=fact)
+        torch.cuda.synchronize()
+        gm_ms = (time.perf_counter() - t0) * 1e3
+        _limit_blas()
+        t1 = time.perf_counter()
+        O.factorize(A, leaf, scheme, 1e-4, depth, None, csr)
+        cpu_s = time.perf_counter() - t1
+        key = scheme if scheme == "aca" else f"bdlr_d{depth}"
+        out[key] = {"build_factor_ms": min(ms), "gmres_time_to_tol_ms": gm_ms,
+                    "iterations": res.iterations, "converged": bool(res.converged),
+                    "true_residual": res.true_residual,
+                    "max_rank_per_level": [lv["max_rank"] for lv in batch.report(0).ranks_per_level],
+                    "cpu_oracle_build_factor_s_1t": cpu_s}
+    return out
+
+
+def run_cfg12(dev):
+    """BASELINE config 1 (48^3 variable-k front, n = 2304, BDLR 1e-4 d=3 -- and ACA
+    beside it) and config 2 (200k-point kNN slab front, ACA vs BDLR at 1e-4),
+    GMRES to 1e-10.  Front generation (GPU) is input manufacture, not timed."""
+    import time
+    import warnings
+    from paper_1403_5337_b200 import frontgen as fg
+    warnings.filterwarnings("ignore", message=".*[Ss]parse.*")
+    kc = fg.cell_conductivity((48, 48, 48), 1)
+    A1 = fg.layered_grid_front((48, 48, 48), 2, 24, conductivity=kc, device=dev)
+    g1 = fg.grid_graph(fg.GridSpec((48, 48, 48)), 2, 24)
+    c1 = {"workload": "cfg1: 48^3 variable-k (seed 1) front, plane z=24, n=2304, leaf 64, "
+                      "GMRES 1e-10, rhs default_rng(0)",
+          **_single_front_item(dev, A1, g1, [("bdlr", 3), ("aca", 1)], 64, 1e-10, 0),
+          "reference_cpu_1t_s": {"bdlr_d3_build_factor": 1.43, "bdlr_d3_gmres": 0.085,
+                                 "aca_build_factor": 1.29, "aca_gmres": 0.166,
+                                 "source": "SURVEY.md §6.3"}}
+    t0 = time.perf_counter()
+    kf = fg.knn_front(200000, h=0.005, leaf=64, device=dev, solver="cg")
+    gen_s = time.perf_counter() - t0
+    c2 = {"workload": "cfg2: 200k points (seed 2), 8-NN Laplacian + 1e-3 I, slab |x-0.5|<=0.005, "
+                      "RCB order, leaf 64, ACA vs BDLR 1e-4, GMRES 1e-10, rhs default_rng(2)",
+          "n": kf.n, "generation_s": gen_s, "generation": kf.info,
+          **_single_front_item(dev, kf.front, kf.graph, [("aca", 1), ("bdlr", 3)], 64, 1e-10, 2)}
+    return c1, c2
 
 
 def main():
