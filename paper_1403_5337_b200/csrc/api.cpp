@@ -255,6 +255,10 @@ struct SolveProg {
   const int32_t* leaf_map = nullptr;
   int leaf_tiles = 0;
   DevBuf pbuf;          // partial dot products of one level (levels reuse it in stream order)
+  // fused persistent sweep: phase table, grid-barrier word, launch bounds
+  const SolvePhase* phases = nullptr;
+  int nphase = 0, max_items = 0, max_k = 0;
+  DevBuf barbuf;
   // the kernel sequence is captured into a CUDA graph at its second use (a
   // GMRES run applies the same program every iteration); one graph launch
   // then replaces 3 launches per level
@@ -267,9 +271,13 @@ struct SolveProg {
     if (pbuf.p) cudaFreeAsync(pbuf.p, st);
     pbuf.p = nullptr;
     pbuf.bytes = 0;
+    if (barbuf.p) cudaFreeAsync(barbuf.p, st);
+    barbuf.p = nullptr;
+    barbuf.bytes = 0;
   }
   ~SolveProg() {
     pbuf.release();
+    barbuf.release();
     if (gexec) cudaGraphExecDestroy(gexec);
   }
 };
@@ -1757,6 +1765,28 @@ static hk_status build_solve_prog(hk_plan* p, int front, int s, SolveProg*& out,
     sp->levels.push_back(std::move(L));
   }
   (void)nb;
+  if (sp->small) {   // phase table of the fused persistent sweep (solve.cu)
+    std::vector<SolvePhase> ph;
+    auto add = [&](int kind, const void* t, const int32_t* it, int ni, int mk) {
+      if (ni <= 0) return;
+      ph.push_back(SolvePhase{kind, ni, t, it});
+      sp->max_items = std::max(sp->max_items, ni);
+      sp->max_k = std::max(sp->max_k, mk);
+    };
+    add(1, sp->leaf.t, sp->leaf.items, sp->leaf.nitems, sp->leaf.max_k);
+    for (auto& L : sp->levels) {
+      add(0, L.pdot_t, L.pdot_items, L.n_pdot, 0);
+      add(1, L.sinv.t, L.sinv.items, L.sinv.nitems, L.sinv.max_k);
+      add(1, L.upd.t, L.upd.items, L.upd.nitems, L.upd.max_k);
+    }
+    sp->nphase = (int)ph.size();
+    if (sp->nphase) {
+      sp->phases = p->pstage.push(ph, st);
+      if (!sp->phases) { delete sp; return fail(HK_ERR_CUDA, "pinned staging allocation failed"); }
+      CU(sp->barbuf.ensure(64, st));
+      CU(cudaMemsetAsync(sp->barbuf.p, 0, 64, st));
+    }
+  }
   CU(p->pstage.commit(st));
   p->progs[key] = sp;
   out = sp;
@@ -1780,7 +1810,25 @@ static hk_status ensure_solve_scratch(hk_plan* p, int s, cudaStream_t st) {
 
 // The solve program's kernel sequence: leaf solve, then per level (deepest
 // first) V^T x partial dots -> S^{-1} g -> x -= d y  (hodlr.py:298-306).
+static bool solve_fused() {
+  static int on = -1;
+  if (on < 0) {
+    // opt-in: measured slower than the graph-replayed split launches (the
+    // phases are item-latency bound; a grid barrier costs what a graph
+    // kernel boundary does)
+    const char* e = getenv("HK_SOLVE_FUSED");
+    on = e ? atoi(e) : 0;
+  }
+  return on != 0;
+}
+
 static hk_status launch_solve_kernels(SolveProg* sp, int s, cudaStream_t st, bool prof) {
+  if (sp->small && sp->nphase && solve_fused()) {
+    CU(hk_launch_solve_sweep(sp->phases, sp->nphase, sp->max_items, s, sp->max_k,
+                             sp->barbuf.as<unsigned>(), st));
+    if (prof) g_opprof.mark("fused sweep (" + std::to_string(sp->nphase) + " phases)", st);
+    return HK_OK;
+  }
   if (sp->small) {
     CU(hk_launch_sgemv(sp->leaf.t, sp->leaf.items, sp->leaf.nitems, s, sp->leaf.max_k, st));
     if (prof) g_opprof.mark("leaf sgemv", st);

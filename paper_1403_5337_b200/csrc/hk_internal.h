@@ -123,6 +123,15 @@ struct SgemvTask {   // y[i,r] (op)= sum_k M[i,k] v[k,r] for i < rows, M column-
 constexpr int HK_PDOT_ROWS = 256;   // rows per partial-dot chunk
 constexpr int HK_PDOT_COLS = 32;    // columns per partial-dot item
 constexpr int HK_SGEMV_ROWS = 32;   // rows per sgemv item
+// one phase of the fused solve sweep: kind 0 = pdot items, 1 = sgemv items
+struct SolvePhase {
+  int32_t kind, nitems;
+  const void* tasks;
+  const int32_t* items;
+};
+size_t hk_solve_sweep_smem(int s, int max_k);
+cudaError_t hk_launch_solve_sweep(const SolvePhase* phases, int nphase, int max_items, int s,
+                                  int max_k, unsigned* bar, cudaStream_t st);
 cudaError_t hk_launch_pdot(const PdotTask* tasks, const int32_t* items, int nitems, int s,
                            cudaStream_t st);
 cudaError_t hk_launch_sgemv(const SgemvTask* tasks, const int32_t* items, int nitems, int s,

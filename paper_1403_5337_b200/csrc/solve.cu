@@ -118,14 +118,14 @@ __global__ void __launch_bounds__(MV_NT) gemv_rm_kernel(const double* __restrict
 // coalesced loads in flight; x's chunk is staged in SMEM.  The per-(column,
 // rhs) warp sums go to a partial array -- the reduction over row chunks
 // happens in fixed order in the consumer (deterministic).
-__global__ void __launch_bounds__(256) pdot_kernel(const PdotTask* __restrict__ tasks,
-                                                   const int32_t* __restrict__ items, int s) {
-  const int ti = items[3 * blockIdx.x], ch = items[3 * blockIdx.x + 1], cb = items[3 * blockIdx.x + 2];
+__device__ __forceinline__ void pdot_item(const PdotTask* __restrict__ tasks,
+                                          const int32_t* __restrict__ items, int item, int s,
+                                          double* __restrict__ xs) {
+  const int ti = items[3 * item], ch = items[3 * item + 1], cb = items[3 * item + 2];
   const PdotTask t = tasks[ti];
   const int lane = threadIdx.x & 31, warp = uniform_warp_id();
   const int row0 = ch * HK_PDOT_ROWS;
   const int nr = min(HK_PDOT_ROWS, t.rows - row0);
-  __shared__ double xs[HK_PDOT_ROWS * 16];
   // the M loads go out first, so their latency overlaps the x staging
   const int k0 = cb * HK_PDOT_COLS + warp * 4;
   const int nk = max(0, min(4, t.cols - k0));
@@ -161,42 +161,62 @@ __global__ void __launch_bounds__(256) pdot_kernel(const PdotTask* __restrict__ 
   }
 }
 
+__global__ void __launch_bounds__(256) pdot_kernel(const PdotTask* __restrict__ tasks,
+                                                   const int32_t* __restrict__ items, int s) {
+  __shared__ double xs[HK_PDOT_ROWS * 16];
+  pdot_item(tasks, items, blockIdx.x, s, xs);
+}
+
 // sgemv: item = (task, 32-row block); warp q sums the columns k = q, q+8, ...
 // of its 32 rows (each load a coalesced 256-byte row segment, 8 loads in
 // flight per thread), the eight partial sums are combined in fixed order
 // through SMEM.  v (K x s) is first staged in SMEM -- directly, or as the
 // fixed-order reduction of partial-dot chunks.
-__global__ void __launch_bounds__(256) sgemv_kernel(const SgemvTask* __restrict__ tasks,
-                                                    const int32_t* __restrict__ items, int s) {
+__device__ __forceinline__ void sgemv_item(const SgemvTask* __restrict__ tasks,
+                                           const int32_t* __restrict__ items, int item, int s,
+                                           double* __restrict__ vs) {
   constexpr int QS = 256 / HK_SGEMV_ROWS;   // column residue classes (= warps)
-  const int ti = items[2 * blockIdx.x], rb = items[2 * blockIdx.x + 1];
+  const int ti = items[2 * item], rb = items[2 * item + 1];
   const SgemvTask t = tasks[ti];
-  extern __shared__ double vs[];   // v: K * s, then partials [QS][HK_SGEMV_ROWS][s]
+  // vs: v (K * s), then partials [QS][HK_SGEMV_ROWS][s]
   const int K = t.K;
   const int q = threadIdx.x >> 5, il = threadIdx.x & 31;
   const int i = rb * HK_SGEMV_ROWS + il;
   const bool live = i < t.rows;
   const double* mrow = t.M + i;
-  // the first PF matrix entries of this thread go out before v is staged
-  constexpr int PF = 8;
+  // the first PF matrix entries of this thread go out before v is staged;
+  // later chunks of PF are issued together (PF loads in flight per thread)
+  constexpr int PF = 16;
   double mpre[PF];
 #pragma unroll
   for (int u = 0; u < PF; ++u) {
     const int k = q + u * QS;
     mpre[u] = (live && k < K) ? mrow[(int64_t)k * t.ldm] : 0.0;
   }
+  // fixed-order sum over the partial-dot chunks, 8 independent loads at a time
+  auto chunk_sum = [](const double* __restrict__ P, int nch, int64_t stride, int64_t off) {
+    double v = 0.0;
+    int c = 0;
+    for (; c + 8 <= nch; c += 8) {
+      double tt[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) tt[u] = P[(int64_t)(c + u) * stride + off];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v += tt[u];
+    }
+    for (; c < nch; ++c) v += P[(int64_t)c * stride + off];
+    return v;
+  };
   for (int idx = threadIdx.x; idx < K * s; idx += 256) {
     const int k = idx % K, r = idx / K;
     double v;
     if (t.v0) {
       v = t.v0[k + (int64_t)r * t.ldv];
     } else if (k < t.KA) {
-      v = 0.0;
-      for (int c = 0; c < t.nchA; ++c) v += t.PA[((int64_t)c * t.KA + k) * s + r];
+      v = chunk_sum(t.PA, t.nchA, (int64_t)t.KA * s, (int64_t)k * s + r);
     } else {
       const int KB = K - t.KA, kb = k - t.KA;
-      v = 0.0;
-      for (int c = 0; c < t.nchB; ++c) v += t.PB[((int64_t)c * KB + kb) * s + r];
+      v = chunk_sum(t.PB, t.nchB, (int64_t)KB * s, (int64_t)kb * s + r);
     }
     vs[r * K + k] = v;
   }
@@ -215,12 +235,22 @@ __global__ void __launch_bounds__(256) sgemv_kernel(const SgemvTask* __restrict_
             if (r < rs) a[r] = fma(mpre[u], vs[(r0 + r) * K + k], a[r]);
         }
       }
-#pragma unroll 8
-      for (int k = q + PF * QS; k < K; k += QS) {
-        const double mv = mrow[(int64_t)k * t.ldm];
+      for (int kk = q + PF * QS; kk < K; kk += PF * QS) {
+        double mv[PF];
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
-          if (r < rs) a[r] = fma(mv, vs[(r0 + r) * K + k], a[r]);
+        for (int u = 0; u < PF; ++u) {
+          const int k = kk + u * QS;
+          mv[u] = k < K ? mrow[(int64_t)k * t.ldm] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+          const int k = kk + u * QS;
+          if (k < K) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+              if (r < rs) a[r] = fma(mv[u], vs[(r0 + r) * K + k], a[r]);
+          }
+        }
       }
     }
 #pragma unroll
@@ -240,6 +270,49 @@ __global__ void __launch_bounds__(256) sgemv_kernel(const SgemvTask* __restrict_
   }
 }
 
+__global__ void __launch_bounds__(256) sgemv_kernel(const SgemvTask* __restrict__ tasks,
+                                                    const int32_t* __restrict__ items, int s) {
+  extern __shared__ double vs[];
+  sgemv_item(tasks, items, blockIdx.x, s, vs);
+}
+
+// ---------------------------------------------------------------------------
+// The whole few-RHS solve sweep as ONE persistent kernel: the phases (leaf
+// sgemv, then pdot -> S^-1 g -> update per level, deepest first) run in order,
+// every CTA striding over the phase's items, with a grid-wide barrier between
+// phases instead of a kernel boundary.  Same items and per-item arithmetic as
+// the split launches (bit-identical results); on config 4 the 22 dependent
+// launches of a solve were ~15 us each, mostly launch and tail latency.
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // flip-bit barrier (self-resetting): CTA 0 adds 0x80000000 - (G - 1),
+    // every other CTA adds 1, so the top bit flips once all G have arrived
+    const unsigned nb = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+    unsigned old, cur;
+    asm volatile("atom.add.release.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(bar), "r"(nb) : "memory");
+    do {
+      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
+    } while (((old ^ cur) & 0x80000000u) == 0);
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) solve_sweep_kernel(const SolvePhase* __restrict__ phases,
+                                                          int nphase, int s, unsigned* bar) {
+  extern __shared__ double sm[];
+  for (int ph = 0; ph < nphase; ++ph) {
+    const SolvePhase P = phases[ph];
+    for (int it = blockIdx.x; it < P.nitems; it += gridDim.x) {
+      if (P.kind == 0)
+        pdot_item(reinterpret_cast<const PdotTask*>(P.tasks), P.items, it, s, sm);
+      else
+        sgemv_item(reinterpret_cast<const SgemvTask*>(P.tasks), P.items, it, s, sm);
+      __syncthreads();   // SMEM reuse by the next item
+    }
+    if (ph + 1 < nphase) grid_barrier(bar);
+  }
+}
 
 // Dense GEMV for the GMRES operator (src/cli.py:320-321): y(m x s) = A x with
 // A row-major.  Each warp owns RW = 4 rows and walks them together with
@@ -365,6 +438,35 @@ cudaError_t hk_launch_sgemv(const SgemvTask* tasks, const int32_t* items, int ni
     if (e != cudaSuccess) return e;
   }
   sgemv_kernel<<<nitems, 256, smem, st>>>(tasks, items, s);
+  hk_count_launch();
+  return cudaGetLastError();
+}
+
+size_t hk_solve_sweep_smem(int s, int max_k) {
+  const size_t pd = (size_t)HK_PDOT_ROWS * s * 8;
+  const size_t sg = ((size_t)max_k * s + 256 * (size_t)s) * 8;
+  return pd > sg ? pd : sg;
+}
+
+cudaError_t hk_launch_solve_sweep(const SolvePhase* phases, int nphase, int max_items, int s,
+                                  int max_k, unsigned* bar, cudaStream_t st) {
+  if (nphase == 0 || max_items == 0) return cudaSuccess;
+  const size_t smem = hk_solve_sweep_smem(s, max_k);
+  cudaError_t e = cudaFuncSetAttribute(solve_sweep_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_sweep_kernel, 256, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorLaunchOutOfResources;
+  // every CTA must be co-resident for the grid barrier: stay below the
+  // device's capacity (a few SMs may be held by a concurrent copy kernel)
+  int grid = sms * per_sm - 16;
+  if (grid > max_items) grid = max_items;
+  if (grid < 1) grid = 1;
+  solve_sweep_kernel<<<grid, 256, smem, st>>>(phases, nphase, s, bar);
   hk_count_launch();
   return cudaGetLastError();
 }
