@@ -231,6 +231,64 @@ def aca_algorithmic_bytes(tree, ranks):
     return total
 
 
+def factor_flops(tree, ranks):
+    """Algorithmic FP64 flops of one factorization per SURVEY.md §8(d) (leaf LU +
+    Z-solve, coupling assembly + LU + correction), from the actual ranks."""
+    total = 0.0
+    for f in range(ranks.shape[0]):
+        w = {0: 0}
+        for k, s in enumerate(tree.internal_nodes()):      # preorder: parents first
+            nd = tree.nodes[s]
+            ru, rl = int(ranks[f, 2 * k]), int(ranks[f, 2 * k + 1])
+            w[nd.left] = w[s] + ru
+            w[nd.right] = w[s] + rl
+        for s, nd in enumerate(tree.nodes):
+            ws = w.get(s, 0)
+            if nd.left < 0:
+                b = nd.size
+                total += 2.0 / 3.0 * b ** 3 + 2.0 * b * b * ws
+        for k, s in enumerate(tree.internal_nodes()):
+            nd = tree.nodes[s]
+            na, nb = tree.nodes[nd.left].size, tree.nodes[nd.right].size
+            ru, rl = int(ranks[f, 2 * k]), int(ranks[f, 2 * k + 1])
+            ws = w[s]
+            total += (2.0 * (na + nb) * ru * rl + 2.0 / 3.0 * (ru + rl) ** 3
+                      + 2.0 * ws * (na * rl + nb * ru) + 2.0 * ws * (ru + rl) ** 2
+                      + 2.0 * ws * (na * ru + nb * rl))
+    return total
+
+
+def solve_bytes(tree, ranks):
+    """HBM bytes one HODLR solve (s = 1) must stream: every
+    stored factor entry the sweep reads -- leaf inverses, V_low/V_up, S^-1 and
+    d_left/d_right -- plus the rhs read and the solution write."""
+    total = 0
+    n = tree.nodes[0].size
+    for f in range(ranks.shape[0]):
+        for s, nd in enumerate(tree.nodes):
+            if nd.left < 0:
+                total += 8 * nd.size * nd.size
+        for k, s in enumerate(tree.internal_nodes()):
+            nd = tree.nodes[s]
+            na, nb = tree.nodes[nd.left].size, tree.nodes[nd.right].size
+            ru, rl = int(ranks[f, 2 * k]), int(ranks[f, 2 * k + 1])
+            total += 8 * (na * rl + nb * ru + (ru + rl) ** 2 + na * ru + nb * rl)
+        total += 16 * n
+    return total
+
+
+def fp64_peak():
+    """Measured DMMA peak (profiles/fp64_peak.json, tools/fp64_peak.py) or the
+    B200 datasheet-class fallback."""
+    pf = ROOT / "profiles" / "fp64_peak.json"
+    if pf.exists():
+        d = json.loads(pf.read_text())
+        for key in ("dmma_tflops", "dgemm_tflops"):
+            if d.get(key):
+                return float(d[key]), f"profiles/fp64_peak.json {key}"
+    return 37.0, "fallback: B200 datasheet-class FP64 (no measured peak file)"
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -270,6 +328,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     aca_s = 0.0
+    fac_s = 0.0
     barrier()
     torch.cuda.synchronize()
     clocks.start()
@@ -280,6 +339,8 @@ def run_ours(args):
     for _ in range(args.steps):
         step()
         aca_s += batch.plan.aca_seconds()
+        tm = batch.plan.timings()
+        fac_s += tm["leaf_lu"] + tm["schur"]
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -309,6 +370,19 @@ def run_ours(args):
             "algorithmic_bytes_per_launch": algo, "launch_ms": aca_avg * 1e3,
             "share_of_step": aca_avg * 1e3 / (ms_max / args.steps),
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk.exists() else "fallback 6.65 TB/s"}
+
+    # ---- the other kernels against their rooflines: the factorization on the
+    # FP64 tensor pipe (algorithmic flops of the actual ranks / the CUDA-event
+    # time of the factor phase inside the timed steps)
+    fpk, fpk_src = fp64_peak()
+    ff = factor_flops(batch.tree, ranks)
+    fac_avg = fac_s / args.steps
+    rooflines = [{"kernel": "factorization (leaf Gauss-Jordan + level-batched DMMA GEMMs + "
+                            "capacitance Gauss-Jordan), cfg3 64 fronts",
+                  "bound": "tensor", "achieved": ff / fac_avg / 1e12, "peak": fpk,
+                  "unit": "TFLOP/s", "frac": ff / fac_avg / 1e12 / fpk,
+                  "algorithmic_flops_per_launch": ff, "launch_ms": fac_avg * 1e3,
+                  "peak_source": fpk_src}]
 
     # ---- GMRES time-to-1e-10 on front 0 (HODLR preconditioner)
     gm = {}
@@ -371,6 +445,8 @@ def run_ours(args):
     c4 = None
     if not args.no_cfg4:
         c4 = run_cfg4(dev, rank, world, hbm_peak)
+        if c4 and "rooflines" in c4:
+            rooflines += c4.pop("rooflines")
 
     # ---- BASELINE configs 1 and 2: one front each, replicas only (rank 0 reports)
     c1 = c2 = None
@@ -385,6 +461,7 @@ def run_ours(args):
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": config_dict(args, world), "impl": "ours",
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roof,
+                "rooflines": rooflines,
                 "cpu_baseline": cpu, "gmres": gm, "cfg4": c4, "cfg1": c1, "cfg2": c2,
                 "ranks_per_level_front0": [e["max_rank"] for e in batch.report(0).ranks_per_level],
                 "fronts_gathered": int(all_ranks.shape[0]),
@@ -448,10 +525,45 @@ def run_cfg4(dev, rank, world, hbm_peak):
         def solve_all():
             return [sh.gmres(torch.from_numpy(B[:, j]).to(dev), hk.GmresConfig(tol=1e-10))
                     for j in range(4)]
+    # HBM bytes one GMRES iteration must stream for the operator: the dense front
+    per_iter = 8.0 * n * n
     solve_all()                                                  # warm
     res, gm_ms = timed(solve_all)
-    # HBM bytes one GMRES iteration must stream: the dense front (GEMV) + the stored factor
-    per_iter = 8.0 * n * n
+    roofs = []
+    if world == 1:
+        # GMRES operator GEMV (4 columns, one pass over the front) and the
+        # 4-rhs HODLR solve, each timed alone over 20 launches by CUDA events
+        from paper_1403_5337_b200 import _native as N
+        X = torch.randn(n, 4, dtype=torch.float64, device=dev)
+        Y = torch.empty_like(X)
+        Xt = X.t().contiguous()
+
+        def gemv():
+            for _ in range(20):
+                N.check(N.lib().hk_gemv(N.ptr(front), n, n, n, N.ptr(Xt), n, 4, N.ptr(Y), n,
+                                        N.stream_handle()))
+        gemv()
+        _, gv_ms = timed(gemv)
+        gv_ms /= 20
+        W = Xt.clone()                                        # (s, n) = column-major n x 4
+
+        def solves():
+            for _ in range(20):
+                fact.solve_device(W)
+        solves()
+        _, sv_ms = timed(solves)
+        sv_ms /= 20
+        sb = solve_bytes(batch.tree, batch.ranks)
+        sbytes = sb + 8.0 * n * 3 * 2                           # columns 2..4 of rhs/solution
+        roofs = [
+            {"kernel": "GMRES operator GEMV (gemv4_kernel), cfg4 front 9216^2, 4 columns",
+             "bound": "hbm", "achieved": per_iter / (gv_ms * 1e-3) / 1e9, "peak": hbm_peak,
+             "unit": "GB/s", "frac": per_iter / (gv_ms * 1e-3) / 1e9 / hbm_peak,
+             "algorithmic_bytes_per_launch": per_iter, "launch_ms": gv_ms},
+            {"kernel": "HODLR solve sweep (leaf sgemv + pdot/S^-1 g/update per level), cfg4, 4 rhs",
+             "bound": "hbm", "achieved": sbytes / (sv_ms * 1e-3) / 1e9, "peak": hbm_peak,
+             "unit": "GB/s", "frac": sbytes / (sv_ms * 1e-3) / 1e9 / hbm_peak,
+             "algorithmic_bytes_per_launch": sbytes, "launch_ms": sv_ms}]
     its = [r.iterations for r in res]
     out = {"workload": "cfg4 large single front: 96^3 Laplacian, plane z=48, n=9216, ACA 1e-4, "
                        "leaf 72, GMRES 1e-10 on default_rng(3) N(0,1) x 4",
@@ -468,6 +580,8 @@ def run_cfg4(dev, rank, world, hbm_peak):
                                   "source": "SURVEY.md §6.3 (reference run in the build container)"}}
     if ranks is not None:
         out["max_rank_per_level"] = ranks
+    if roofs:
+        out["rooflines"] = roofs
     return out
 
 

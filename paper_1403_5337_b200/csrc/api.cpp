@@ -1016,6 +1016,8 @@ static GemmTask gemm(const double* A, int64_t lda, int transA, const double* B, 
   t.C = C; t.ldc = ldc;
   t.m = m; t.n = n; t.k = k;
   t.alpha = alpha; t.beta = beta;
+  t.vec = ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) % 16 == 0) &&
+          lda % 2 == 0 && ldb % 2 == 0;
   return t;
 }
 

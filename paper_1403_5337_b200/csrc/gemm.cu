@@ -23,6 +23,10 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes));
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -33,7 +37,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // register staging) so the L2 latency of the next k-tiles overlaps the DMMA
 // work of the current one; for beta != 0 the C values are fetched into
 // registers before the k loop so the epilogue does not wait on memory.
-template <int TRANSA>
+template <int TRANSA, int VEC>
 __device__ __forceinline__ void gemm_tile(const GemmTask& t, int tm, int tn, double* smem) {
   constexpr int A_STAGE = TRANSA ? BM * ST : BK * SA;
   constexpr int B_STAGE = BN * ST;
@@ -66,6 +70,34 @@ __device__ __forceinline__ void gemm_tile(const GemmTask& t, int tm, int tn, dou
     const int k0 = kt * BK;
     double* as = As + stage * A_STAGE;
     double* bs = Bs + stage * B_STAGE;
+    if constexpr (VEC != 0) {
+      // 16-byte copies of element pairs along the contiguous dimension (pairs
+      // start at even offsets, so a pair straddling the edge copies 8 bytes
+      // and zero-fills the rest); half the cp.async instructions
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int idx = tid + NT * q;
+        if (!TRANSA) {
+          const int i = 2 * (idx % (BM / 2)), l = idx / (BM / 2);
+          const int rem = M - (m0 + i);
+          const int nb = (k0 + l < K) ? (rem >= 2 ? 16 : rem == 1 ? 8 : 0) : 0;
+          const double* src = nb ? Ag + (m0 + i) + (int64_t)(k0 + l) * t.lda : Ag;
+          cp_async16(as + l * SA + i, src, nb);
+        } else {
+          const int l = 2 * (idx % (BK / 2)), i = idx / (BK / 2);
+          const int rem = K - (k0 + l);
+          const int nb = (m0 + i < M) ? (rem >= 2 ? 16 : rem == 1 ? 8 : 0) : 0;
+          const double* src = nb ? Ag + (k0 + l) + (int64_t)(m0 + i) * t.lda : Ag;
+          cp_async16(as + i * ST + l, src, nb);
+        }
+        const int l = 2 * (idx % (BK / 2)), j = idx / (BK / 2);
+        const int remb = K - (k0 + l);
+        const int nbb = (n0 + j < N) ? (remb >= 2 ? 16 : remb == 1 ? 8 : 0) : 0;
+        const double* srcb = nbb ? Bg + (k0 + l) + (int64_t)(n0 + j) * t.ldb : Bg;
+        cp_async16(bs + j * ST + l, srcb, nbb);
+      }
+      return;
+    }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int idx = tid + NT * q;
@@ -154,8 +186,13 @@ __global__ void __launch_bounds__(NT, 2) gemm_kernel(const GemmTask* __restrict_
   const int tm = tilemap[3 * blockIdx.x + 1];
   const int tn = tilemap[3 * blockIdx.x + 2];
   const GemmTask t = tasks[task];
-  if (t.transA) gemm_tile<1>(t, tm, tn, gsmem);
-  else gemm_tile<0>(t, tm, tn, gsmem);
+  if (t.vec) {
+    if (t.transA) gemm_tile<1, 1>(t, tm, tn, gsmem);
+    else gemm_tile<0, 1>(t, tm, tn, gsmem);
+  } else {
+    if (t.transA) gemm_tile<1, 0>(t, tm, tn, gsmem);
+    else gemm_tile<0, 0>(t, tm, tn, gsmem);
+  }
 }
 
 __global__ void copy_kernel(const CopyTask* __restrict__ tasks) {

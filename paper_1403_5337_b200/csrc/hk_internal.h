@@ -66,6 +66,8 @@ struct GemmTask {
   int64_t lda, ldb, ldc;
   int32_t m, n, k;
   int32_t transA;
+  int32_t vec;      // 1: A, B 16-byte aligned with even leading dimensions (16-byte cp.async)
+  int32_t pad_;
   double alpha, beta;
   double diag;      // added to C(i,i) after alpha*op(A)*B + beta*C
 };
