@@ -14,7 +14,9 @@ import re
 import sys
 from collections import defaultdict
 
-OURS = ("aca_kernel", "gemm_kernel", "gj_", "matvec_kernel", "dot_kernel", "transpose_kernel",
+OURS = ("aca_kernel", "aca_cluster_kernel", "gj_cl_kernel", "sgemv_kernel", "pdot_kernel",
+        "gemv4_kernel", "solve_sweep_kernel", "h2d_stream_kernel", "arnoldi_batch_kernel",
+        "norms_kernel", "gemm_kernel", "gj_", "matvec_kernel", "dot_kernel", "transpose_kernel",
         "copy_kernel", "fill_kernel", "skeleton_kernel", "cpiv_kernel", "lu_inv_kernel",
         "arnoldi_kernel", "combine_kernel", "gemv_rm_kernel", "norm_kernel", "scale_kernel",
         "axpby_kernel", "diag_scale_kernel")
