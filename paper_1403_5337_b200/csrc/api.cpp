@@ -848,8 +848,14 @@ extern "C" hk_status hk_build_bdlr(hk_plan* p, const double* A, int64_t ld, int6
       t.tol = tol;
       tasks.push_back(t);
     }
+  int max_bm = 0, max_bn = 0;
+  for (const SkelTask& t : tasks) {
+    max_bm = std::max(max_bm, t.m);
+    max_bn = std::max(max_bn, t.n);
+  }
   CU(upload(p->tasks_d, tasks, st));
-  CU(hk_launch_skeleton(p->tasks_d.as<SkelTask>(), (int)tasks.size(), max_k, max_kc, st));
+  CU(hk_launch_skeleton(p->tasks_d.as<SkelTask>(), (int)tasks.size(), max_k, max_kc, max_bm,
+                        max_bn, st));
   CU(cudaEventRecord(p->ev[1], st));
   CHK(fetch_ranks(p, st));
   std::vector<int32_t> status((size_t)p->batch * nb, 0);
@@ -2465,7 +2471,7 @@ extern "C" hk_status hk_skeleton_block(const double* a, int64_t m, int64_t n, in
   SkelTask* td = nullptr;
   CU(cudaMallocAsync(&td, sizeof(SkelTask), st));
   CU(cudaMemcpyAsync(td, &t, sizeof(SkelTask), cudaMemcpyHostToDevice, st));
-  CU(hk_launch_skeleton(td, 1, (int)k, (int)kc, st));
+  CU(hk_launch_skeleton(td, 1, (int)k, (int)kc, (int)m, (int)n, st));
   int32_t hs[2] = {0, 0};
   std::vector<int64_t> ph((size_t)(k + kc));
   CU(cudaMemcpyAsync(hs, small, 8, cudaMemcpyDeviceToHost, st));

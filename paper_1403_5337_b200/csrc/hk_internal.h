@@ -158,7 +158,7 @@ cudaError_t hk_launch_aca_classes(const AcaTask* tasks_dev, const int* class_beg
                                   const int* class_max_cap, const int* class_max_m, double tol2,
                                   int* counters_dev, cudaStream_t* streams);
 cudaError_t hk_launch_skeleton(const SkelTask* tasks_dev, int ntasks, int max_k, int max_kc,
-                               cudaStream_t st);
+                               int max_m, int max_n, cudaStream_t st);
 cudaError_t hk_launch_lu(const LuTask* tasks_dev, int ntasks, int maxN, cudaStream_t st);
 cudaError_t hk_launch_gemm(const GemmTask* tasks_dev, const int32_t* tilemap_dev, int ntiles,
                            cudaStream_t st);

@@ -141,65 +141,116 @@ __global__ void __launch_bounds__(NT) lu_inv_kernel(const LuTask* __restrict__ t
 }
 
 // ------------------------------------------------------------------ complete pivoting
-// Works on a row-major k x kc matrix W (ld = ldw) in global memory.  Returns
+// Works on a row-major k x kc matrix W (ld = ldw, SMEM or global).  Returns
 // the number of pivots taken; perms and |pivots| written to rp, cp, piv.
+//
+// Warp w owns rows s+1+w, s+1+w+NW, ...; lanes stride the columns (coalesced,
+// no index divisions).  The argmax of step s+1 is fused into the rank-1 update
+// of step s: the updated trailing entries are exactly the next step's search
+// set, and the flattened index (i-s-1)*(kc-s-1) + (j-s-1) keeps numpy's
+// row-major first-occurrence tie-break.  The multiplier of row i is computed
+// once (lane 0, IEEE division) and broadcast, so every entry is
+// w[i][j] - (l_i * w[s][j]) with a separate multiply and subtract, exactly as
+// dense.py:147-165 / the oracle (bit-identical packed LU and pivots).
+// Block argmax of |x| >= 0 with the lowest flattened index on ties, valid in
+// every thread after ONE barrier: REDUX-based warp stage (warp_argmax_idx),
+// the NW warp winners through SMEM, reduced again by every warp.  The caller
+// must pass another barrier before the next call reuses sv/si.
 template <int NT>
-__device__ int complete_pivot_lu(double* W, int k, int kc, int64_t ldw, int64_t* rp, int64_t* cp,
-                                 double* piv, double* red_v, int64_t* red_i) {
-  const int tid = threadIdx.x;
+__device__ __forceinline__ ArgMax block_argmax1(ArgMax a, double* sv, int64_t* si) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool ok = a.i >= 0;
+  const int wi = warp_argmax_idx(a.v, ok, ok ? (int)a.i : 0);
+  const unsigned m = __ballot_sync(0xffffffffu, ok && (int)a.i == wi);
+  const double wv = __shfl_sync(0xffffffffu, a.v, m ? __ffs(m) - 1 : 0);
+  if (lane == 0) { sv[warp] = wv; si[warp] = m ? wi : -1; }
+  __syncthreads();
+  const bool ok2 = lane < NW && si[lane < NW ? lane : 0] >= 0;
+  const double cv = lane < NW ? sv[lane] : 0.0;
+  const int ci = lane < NW ? (int)si[lane] : 0;
+  const int bi = warp_argmax_idx(cv, ok2, ci);
+  const unsigned m2 = __ballot_sync(0xffffffffu, ok2 && ci == bi);
+  const double bv = __shfl_sync(0xffffffffu, cv, m2 ? __ffs(m2) - 1 : 0);
+  return ArgMax{bv, m2 ? (int64_t)bi : (int64_t)-1};
+}
+
+template <int NT>
+__device__ int complete_pivot_lu(double* Wsm, double* Wg, int ksm, int k, int kc, int64_t ldw,
+                                 int64_t* rp, int64_t* cp, double* piv, double* red_v,
+                                 int64_t* red_i) {
+  constexpr int NW = NT / 32;
+  // rows [0, ksm) live in SMEM, the rest in global memory (same row stride)
+  auto R = [&](int i) -> double* { return (i < ksm ? Wsm : Wg) + (int64_t)i * ldw; };
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < k; i += NT) rp[i] = i;
   for (int j = tid; j < kc; j += NT) cp[j] = j;
-  __syncthreads();
+  ArgMax a{0.0, -1};
+  for (int i = warp; i < k; i += NW)
+    for (int j = lane; j < kc; j += 32) {
+      const double v = fabs(R(i)[j]);
+      const int64_t idx = (int64_t)i * kc + j;
+      if (argmax_better(v, idx, a.v, a.i)) { a.v = v; a.i = idx; }
+    }
+  a = block_argmax1<NT>(a, red_v, red_i);
   const int steps = k < kc ? k : kc;
   int taken = 0;
   for (int s = 0; s < steps; ++s) {
-    const int rr = k - s, cc = kc - s;
-    ArgMax a{0.0, -1};
-    const int64_t tot = (int64_t)rr * cc;
-    for (int64_t idx = tid; idx < tot; idx += NT) {
-      int i = s + (int)(idx / cc), j = s + (int)(idx % cc);
-      double v = fabs(W[i * ldw + j]);
-      if (argmax_better(v, idx, a.v, a.i)) { a.v = v; a.i = idx; }
-    }
-    a = block_argmax<NT>(a, red_v, red_i);
-    if (a.i < 0 || a.v == 0.0) break;
+    if (a.i < 0 || !(a.v != 0.0)) break;
+    const int cc = kc - s;
     const int pr = s + (int)(a.i / cc), pc = s + (int)(a.i % cc);
     if (pr != s) {
+      double* rs_ = R(s);
+      double* rr_ = R(pr);
       for (int j = tid; j < kc; j += NT) {
-        double x = W[s * ldw + j];
-        W[s * ldw + j] = W[pr * ldw + j];
-        W[pr * ldw + j] = x;
+        const double x = rs_[j];
+        rs_[j] = rr_[j];
+        rr_[j] = x;
       }
       if (tid == 0) {
-        int64_t x = rp[s]; rp[s] = rp[pr]; rp[pr] = x;
+        const int64_t x = rp[s]; rp[s] = rp[pr]; rp[pr] = x;
       }
+      __syncthreads();   // the column swap below reads the swapped rows
     }
-    __syncthreads();
     if (pc != s) {
       for (int i = tid; i < k; i += NT) {
-        double x = W[i * ldw + s];
-        W[i * ldw + s] = W[i * ldw + pc];
-        W[i * ldw + pc] = x;
+        double* ri = R(i);
+        const double x = ri[s];
+        ri[s] = ri[pc];
+        ri[pc] = x;
       }
       if (tid == 0) {
-        int64_t x = cp[s]; cp[s] = cp[pc]; cp[pc] = x;
+        const int64_t x = cp[s]; cp[s] = cp[pc]; cp[pc] = x;
       }
     }
     __syncthreads();
-    const double p = W[s * ldw + s];
+    const double* ps = R(s);
+    const double p = ps[s];
     if (tid == 0) piv[s] = fabs(p);
     ++taken;
+    a = ArgMax{0.0, -1};
     if (s + 1 < k) {
-      for (int i = s + 1 + tid; i < k; i += NT) W[i * ldw + s] = div_rn(W[i * ldw + s], p);
-      __syncthreads();
-      const int r2 = k - s - 1, c2 = kc - s - 1;
-      const int64_t t2 = (int64_t)r2 * c2;
-      for (int64_t idx = tid; idx < t2; idx += NT) {
-        int i = s + 1 + (int)(idx / c2), j = s + 1 + (int)(idx % c2);
-        W[i * ldw + j] = sub_rn(W[i * ldw + j], mul_rn(W[i * ldw + s], W[s * ldw + j]));
+      const int c2 = kc - s - 1;
+      for (int i = s + 1 + warp; i < k; i += NW) {
+        double* ri = R(i);
+        double l = 0.0;
+        if (lane == 0) {
+          l = div_rn(ri[s], p);
+          ri[s] = l;
+        }
+        l = __shfl_sync(0xffffffffu, l, 0);
+        const int64_t rbase = (int64_t)(i - s - 1) * c2;
+        for (int j = s + 1 + lane; j < kc; j += 32) {
+          const double v = sub_rn(ri[j], mul_rn(l, ps[j]));
+          ri[j] = v;
+          const int64_t idx = rbase + (j - s - 1);
+          if (argmax_better(fabs(v), idx, a.v, a.i)) { a.v = fabs(v); a.i = idx; }
+        }
       }
     }
-    __syncthreads();
+    // its barrier also orders this step's updates before the next swaps; the
+    // next write of sv/si comes after the next step's swap barrier
+    a = block_argmax1<NT>(a, red_v, red_i);
   }
   return taken;
 }
@@ -210,36 +261,47 @@ __global__ void __launch_bounds__(NT) cpiv_kernel(double* W, int k, int kc, int6
                                                   int64_t* npiv) {
   __shared__ double red_v[NT / 32];
   __shared__ int64_t red_i[NT / 32];
-  int taken = complete_pivot_lu<NT>(W, k, kc, ldw, rp, cp, piv, red_v, red_i);
+  int taken = complete_pivot_lu<NT>(W, W, 0, k, kc, ldw, rp, cp, piv, red_v, red_i);
   if (threadIdx.x == 0) *npiv = taken;
 }
 
 // ------------------------------------------------------------------ BDLR skeleton
 template <int NT>
 __global__ void __launch_bounds__(NT) skeleton_kernel(const SkelTask* __restrict__ tasks,
-                                                      double* pivbuf, int64_t pivstride) {
+                                                      double* pivbuf, int64_t pivstride,
+                                                      size_t smem_bytes) {
   const SkelTask t = tasks[blockIdx.x];
   const int tid = threadIdx.x;
   __shared__ double red_v[NT / 32];
   __shared__ int64_t red_i[NT / 32];
   __shared__ int s_rank;
+  extern __shared__ double wsm[];
   double* piv = pivbuf + (int64_t)blockIdx.x * pivstride;
   const int k = t.k, kc = t.kc, m = t.m, n = t.n;
-  // gather A-hat = A[rsel, csel] (row-major k x kc)
-  for (int64_t idx = tid; idx < (int64_t)k * kc; idx += NT) {
-    int a = (int)(idx / kc), b = (int)(idx % kc);
-    t.work[idx] = t.A[t.rsel[a] * t.lda + t.csel[b]];
+  // working matrix: its first ksm rows in SMEM (all of it when it fits), the
+  // rest in t.work; SMEM rows are written back to t.work after the LU
+  const int ksm = kc > 0 ? (int)min((size_t)k, smem_bytes / ((size_t)kc * 8)) : k;
+  auto R = [&](int i) -> double* { return (i < ksm ? wsm : t.work) + (int64_t)i * kc; };
+  // gather A-hat = A[rsel, csel] (row-major k x kc), warp per row
+  double amax = 0.0;   // max|A-hat| for the degenerate check, before the LU overwrites it
+  for (int a = tid >> 5; a < k; a += NT / 32) {
+    const double* arow = t.A + t.rsel[a] * t.lda;
+    double* w = R(a);
+    for (int b = tid & 31; b < kc; b += 32) {
+      const double v = arow[t.csel[b]];
+      w[b] = v;
+      amax = fmax(amax, fabs(v));
+    }
   }
   __syncthreads();
-  // keep max|A-hat| for the degenerate check before the LU overwrites it
-  double amax = 0.0;
-  for (int64_t idx = tid; idx < (int64_t)k * kc; idx += NT) amax = fmax(amax, fabs(t.work[idx]));
   {
     ArgMax a{amax, 0};
     a = block_argmax<NT>(a, red_v, red_i);
     amax = a.v;
   }
-  const int taken = complete_pivot_lu<NT>(t.work, k, kc, kc, t.rperm, t.cperm, piv, red_v, red_i);
+  const int taken = complete_pivot_lu<NT>(wsm, t.work, ksm, k, kc, kc, t.rperm, t.cperm, piv,
+                                          red_v, red_i);
+  for (int64_t idx = tid; idx < (int64_t)ksm * kc; idx += NT) t.work[idx] = wsm[idx];
   if (tid == 0) {
     int r = 0;
     if (taken > 0) {
@@ -264,24 +326,42 @@ __global__ void __launch_bounds__(NT) skeleton_kernel(const SkelTask* __restrict
     if (tid == 0 && a.v > t.tol * amax) *t.status = HK_STATUS_DEGENERATE;
     return;
   }
+}
+
+// C~ = C U11^{-1} (thread per row of the block) and R~ = L11^{-1} R[rperm[:r]]
+// (thread per column), V = R~^T -- one CTA per (task, 64-row or 64-column
+// chunk), so the triangular solves of a block spread over many SMs and each
+// CTA's rows of U stay in its L1 (the single-CTA version ran them on the SM
+// that did the LU, whose L1 was mostly carved out as SMEM).  Same per-entry
+// arithmetic and order as before (lowrank.py:315-318).
+template <int NT>
+__global__ void __launch_bounds__(NT) skeleton_trsm_kernel(const SkelTask* __restrict__ tasks) {
+  const SkelTask t = tasks[blockIdx.x];
+  const int r = *t.rank;
+  if (r == 0) return;
+  const int kc = t.kc;
   const double* W = t.work;   // packed LU, row-major ld kc
-  // C~ = C U11^{-1}: row i solves x U11 = C[i, :] (thread per row)
-  for (int i = tid; i < m; i += NT) {
+  const int nrc = (t.m + NT - 1) / NT;
+  int chunk = blockIdx.y;
+  if (chunk < nrc) {
+    const int i = chunk * NT + threadIdx.x;
+    if (i >= t.m) return;
     double* x = t.U + i;                      // row i of U (column-major, ld ldu)
     for (int l = 0; l < r; ++l) {
       double s = t.A[(int64_t)i * t.lda + t.csel[t.cperm[l]]];
       for (int p = 0; p < l; ++p) s -= x[(int64_t)p * t.ldu] * W[(int64_t)p * kc + l];
       x[(int64_t)l * t.ldu] = s / W[(int64_t)l * kc + l];
     }
+    return;
   }
-  // R~ = L11^{-1} R[rperm[:r]] (thread per column), V = R~^T
-  for (int c = tid; c < n; c += NT) {
-    double* z = t.V + c;                      // row c of V (column-major, ld ldv)
-    for (int a = 0; a < r; ++a) {
-      double s = t.A[t.rsel[t.rperm[a]] * t.lda + c];
-      for (int p = 0; p < a; ++p) s -= W[(int64_t)a * kc + p] * z[(int64_t)p * t.ldv];
-      z[(int64_t)a * t.ldv] = s;
-    }
+  chunk -= nrc;
+  const int c = chunk * NT + threadIdx.x;
+  if (c >= t.n) return;
+  double* z = t.V + c;                        // row c of V (column-major, ld ldv)
+  for (int a = 0; a < r; ++a) {
+    double s = t.A[t.rsel[t.rperm[a]] * t.lda + c];
+    for (int p = 0; p < a; ++p) s -= W[(int64_t)a * kc + p] * z[(int64_t)p * t.ldv];
+    z[(int64_t)a * t.ldv] = s;
   }
 }
 
@@ -309,15 +389,32 @@ cudaError_t hk_launch_lu_full(double* a, int64_t m, int64_t n, int64_t ld, int64
 }
 
 cudaError_t hk_launch_skeleton(const SkelTask* tasks_dev, int ntasks, int max_k, int max_kc,
-                               cudaStream_t st) {
+                               int max_m, int max_n, cudaStream_t st) {
   if (ntasks == 0) return cudaSuccess;
   double* pivbuf = nullptr;
   int64_t pstride = (max_k < max_kc ? max_k : max_kc) + 1;
   cudaError_t e = cudaMallocAsync(&pivbuf, (size_t)ntasks * pstride * 8, st);
   if (e != cudaSuccess) return e;
-  skeleton_kernel<CP_NT><<<ntasks, CP_NT, 0, st>>>(tasks_dev, pivbuf, pstride);
+  // every task whose working matrix fits takes the SMEM path (1024-thread
+  // CTAs run one per SM anyway); larger ones work in global memory
+  const size_t need = (size_t)max_k * max_kc * 8;
+  const size_t smem = need <= LU_SMEM_CAP ? need : LU_SMEM_CAP;
+  if (smem > 48 * 1024) {
+    e = cudaFuncSetAttribute(skeleton_kernel<CP_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  skeleton_kernel<CP_NT><<<ntasks, CP_NT, smem, st>>>(tasks_dev, pivbuf, pstride, smem);
   hk_count_launch();
   e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  constexpr int TR_NT = 64;
+  const int chunks = (max_m + TR_NT - 1) / TR_NT + (max_n + TR_NT - 1) / TR_NT;
+  if (chunks > 0) {
+    skeleton_trsm_kernel<TR_NT><<<dim3((unsigned)ntasks, (unsigned)chunks), TR_NT, 0, st>>>(tasks_dev);
+    hk_count_launch();
+    e = cudaGetLastError();
+  }
   cudaFreeAsync(pivbuf, st);
   return e;
 }
