@@ -78,11 +78,122 @@ __device__ __forceinline__ void arnoldi_body(int64_t n, int64_t j, int64_t mmax,
   }
 }
 
+// Register-resident variant for n <= WPT * KR_NT (every config): the new
+// vector w lives in registers (WPT entries per thread), so an MGS step is one
+// pass over q_i with the dot and the update fused, and every block reduction
+// takes one barrier (double-buffered SMEM partials reduced by every warp in a
+// fixed order).  Same algorithm and step order as arnoldi_body.
+template <int WPT>
+__device__ __forceinline__ void arnoldi_body_reg(int64_t n, int64_t j, int64_t mmax, double* basis,
+                                                 double* hess, double* cs, double* sn, double* g,
+                                                 double* w, double beta, double* out) {
+  constexpr int NW = KR_NT / 32;
+  __shared__ double red[2][NW];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int par = 0;
+  auto bsum = [&](double v) -> double {
+    v = warp_sum(v);
+    if (lane == 0) red[par][warp] = v;
+    __syncthreads();
+    double t = lane < NW ? red[par][lane] : 0.0;
+    t = warp_sum(t);
+    par ^= 1;
+    return __shfl_sync(0xffffffffu, t, 0);
+  };
+  const int64_t k = j + 1;
+  const int64_t ldh = mmax + 1;
+  double* hcol = hess + j * ldh;
+  double wr[WPT];
+#pragma unroll
+  for (int q = 0; q < WPT; ++q) {
+    const int64_t i = tid + (int64_t)q * KR_NT;
+    wr[q] = i < n ? w[i] : 0.0;
+  }
+  auto sumsq = [&]() {
+    double a = 0.0;
+#pragma unroll
+    for (int q = 0; q < WPT; ++q) a += wr[q] * wr[q];
+    return a;
+  };
+  auto mgs_pass = [&](bool add) {
+    for (int64_t i = 0; i < k; ++i) {             // MGS, krylov.py:111-114 (:115-119)
+      const double* qv = basis + i * n;
+      double d = 0.0;
+#pragma unroll
+      for (int q = 0; q < WPT; ++q) {
+        const int64_t e = tid + (int64_t)q * KR_NT;
+        d += (e < n ? qv[e] : 0.0) * wr[q];
+      }
+      const double h = bsum(d);
+      if (tid == 0) hcol[i] = add ? hcol[i] + h : h;
+#pragma unroll
+      for (int q = 0; q < WPT; ++q) {             // q_i again, from L1
+        const int64_t e = tid + (int64_t)q * KR_NT;
+        wr[q] -= h * (e < n ? qv[e] : 0.0);
+      }
+    }
+  };
+  const double norm_in = sqrt(bsum(sumsq()));
+  mgs_pass(false);
+  double nw = sqrt(bsum(sumsq()));
+  if (nw < norm_in / sqrt(2.0)) {                 // re-orthogonalise
+    mgs_pass(true);
+    nw = sqrt(bsum(sumsq()));
+  }
+  const double hk = nw;
+  const bool happy = hk <= 1e-14 * fmax(norm_in, 1e-300);   // :122
+  double* qn = basis + k * n;
+#pragma unroll
+  for (int q = 0; q < WPT; ++q) {
+    const int64_t i = tid + (int64_t)q * KR_NT;
+    if (i < n) {
+      w[i] = wr[q];
+      if (!happy) qn[i] = wr[q] / hk;
+    }
+  }
+  if (tid == 0) {
+    hcol[k] = hk;
+    for (int64_t i = 0; i < j; ++i) {               // apply previous rotations, :126-129
+      const double temp = cs[i] * hcol[i] + sn[i] * hcol[i + 1];
+      hcol[i + 1] = -sn[i] * hcol[i] + cs[i] * hcol[i + 1];
+      hcol[i] = temp;
+    }
+    const double denom = hypot(hcol[j], hcol[k]);
+    double brk = 0.0, rel = 0.0;
+    if (denom == 0.0) {
+      brk = 1.0;
+    } else {
+      cs[j] = hcol[j] / denom;
+      sn[j] = hcol[k] / denom;
+      hcol[j] = denom;
+      hcol[k] = 0.0;
+      g[k] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      rel = fabs(g[k]) / beta;
+    }
+    out[0] = rel;
+    out[1] = happy ? 1.0 : 0.0;
+    out[2] = brk;
+  }
+}
+
+// dispatch: registers for n <= 16 * 1024, the streaming body above that
+__device__ __forceinline__ void arnoldi_dispatch(int64_t n, int64_t j, int64_t mmax, double* basis,
+                                                 double* hess, double* cs, double* sn, double* g,
+                                                 double* w, double beta, double* out) {
+  if (n <= 1 * KR_NT) arnoldi_body_reg<1>(n, j, mmax, basis, hess, cs, sn, g, w, beta, out);
+  else if (n <= 3 * KR_NT) arnoldi_body_reg<3>(n, j, mmax, basis, hess, cs, sn, g, w, beta, out);
+  else if (n <= 5 * KR_NT) arnoldi_body_reg<5>(n, j, mmax, basis, hess, cs, sn, g, w, beta, out);
+  else if (n <= 10 * KR_NT) arnoldi_body_reg<10>(n, j, mmax, basis, hess, cs, sn, g, w, beta, out);
+  else if (n <= 16 * KR_NT) arnoldi_body_reg<16>(n, j, mmax, basis, hess, cs, sn, g, w, beta, out);
+  else arnoldi_body(n, j, mmax, basis, hess, cs, sn, g, w, beta, out);
+}
+
 __global__ void __launch_bounds__(KR_NT) arnoldi_kernel(int64_t n, int64_t j, int64_t mmax,
                                                         double* basis, double* hess, double* cs,
                                                         double* sn, double* g, double* w,
                                                         double beta, double* out) {
-  arnoldi_body(n, j, mmax, basis, hess, cs, sn, g, w, beta, out);
+  arnoldi_dispatch(n, j, mmax, basis, hess, cs, sn, g, w, beta, out);
 }
 
 // s independent GMRES systems advanced together (one CTA each): system c owns
@@ -95,8 +206,8 @@ __global__ void __launch_bounds__(KR_NT) arnoldi_batch_kernel(
   const int c = blockIdx.x;
   if (!active[c]) return;
   const int64_t vs = mmax + 1;
-  arnoldi_body(n, j, mmax, basis + c * bstride, hess + c * hstride, cs + c * vs, sn + c * vs,
-               g + c * vs, w + c * n, beta[c], out + 3 * c);
+  arnoldi_dispatch(n, j, mmax, basis + c * bstride, hess + c * hstride, cs + c * vs, sn + c * vs,
+                   g + c * vs, w + c * n, beta[c], out + 3 * c);
 }
 
 // per-column 2-norms of an n x s column-major block (ld), one CTA per column
