@@ -531,8 +531,11 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
     ++ncol_ev;
     bar<NT>();
     // residual column (:266-268) + next-row candidate (:283) + pending u dots
-    const double* csrc = t.At + (int64_t)col * t.lda;
-    sweep<NT, EPT, DB>(ldlog, U, m, c, pending ? r : 0, coef, csrc, 1, c, r, partU, pld,
+    // column gather: the transposed copy (coalesced) or, without one, the
+    // row-major front itself with stride lda
+    const double* csrc = t.At ? t.At + (int64_t)col * t.lda : t.A + col;
+    const int cstride = t.At ? 1 : (int)t.lda;
+    sweep<NT, EPT, DB>(ldlog, U, m, c, pending ? r : 0, coef, csrc, cstride, c, r, partU, pld,
                    used, nxt, uu, bval, xv);
     {
       // next row = argmax over untouched rows; uu = |u|^2, vv = |v|^2 (fixed
@@ -870,7 +873,8 @@ __global__ void __launch_bounds__(NT) aca_cluster_kernel(const AcaTask* __restri
     bar<NT>();
     // residual column slice + next-row candidate + pending u dots
     sweep<NT, EPT, DB>(ldlog, Us, mlen, c, pending ? r : 0, coef,
-                       t.At + (int64_t)col * t.lda + mu0, 1, c, r, partU, pld, used + mu0, nxt,
+                       t.At ? t.At + (int64_t)col * t.lda + mu0 : t.A + (int64_t)mu0 * t.lda + col,
+                       t.At ? 1 : (int)t.lda, c, r, partU, pld, used + mu0, nxt,
                        uu, bval, xv);
     {
       const int lane = tid & 31, warp = uniform_warp_id();

@@ -580,8 +580,16 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
   const int64_t n = p->n;
   // transposed copy with the same ld/stride as the fronts: At[j*ld + i] = A[i*ld + j]
   const int64_t atstride = p->batch > 1 ? fstride : 0;
-  CU(p->At.ensure((size_t)((p->batch - 1) * atstride + ld * n) * 8 + 8, st));
-  CU(hk_launch_transpose(A, p->At.as<double>(), n, ld, p->batch, atstride, st));
+  // HK_ACA_AT=0: no transposed copy; the column gathers read the front with stride ld
+  static int use_at = -1;
+  if (use_at < 0) {
+    const char* e = getenv("HK_ACA_AT");
+    use_at = e ? atoi(e) : 1;
+  }
+  if (use_at) {
+    CU(p->At.ensure((size_t)((p->batch - 1) * atstride + ld * n) * 8 + 8, st));
+    CU(hk_launch_transpose(A, p->At.as<double>(), n, ld, p->batch, atstride, st));
+  }
   const int64_t ldat = ld;
   p->have_trace = record_trace != 0;
   if (p->have_trace) CU(p->trace_d.ensure((size_t)p->batch * p->trace_per_front * 4 + 4, st));
@@ -604,7 +612,7 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
       const BlockGeom& b = p->blocks[bi];
       AcaTask t{};
       t.A = A + f * fstride + b.row0 * ld + b.col0;
-      t.At = p->At.as<double>() + f * atstride + b.col0 * ldat + b.row0;
+      t.At = use_at ? p->At.as<double>() + f * atstride + b.col0 * ldat + b.row0 : nullptr;
       t.U = p->UV.as<double>() + f * p->uv_per_front + b.u_off;
       t.V = p->UV.as<double>() + f * p->uv_per_front + b.v_off;
       t.rank = p->ranks_d.as<int32_t>() + f * nb + bi;
