@@ -303,6 +303,11 @@ struct hk_plan {
   cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaStream_t cl_side[4] = {nullptr, nullptr, nullptr, nullptr};   // cluster ACA groups
   std::vector<cudaEvent_t> fev;     // factor: staging-commit events (front-group streams)
+  // BDLR selection cache (graph hash, depth)
+  bool sel_valid = false;
+  uint64_t sel_key = 0;
+  std::vector<int64_t> probe_off, probe_cnt;
+  int sel_max_k = 0, sel_max_kc = 0;
   size_t gjs_need = 0;              // factor: large-GJ global scratch bytes (0 = none)
   cudaEvent_t cl_side_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t side_ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -781,13 +786,35 @@ extern "C" hk_status hk_build_bdlr(hk_plan* p, const double* A, int64_t ld, int6
   CHK(prepare_build(p, A, ld, fstride, max_rank, st));
   CHK(timed_begin(p, st));
   const size_t nb = p->blocks.size();
+  // the selections depend only on (graph, tree, depth): reuse them when the
+  // same graph comes back (FNV-1a over the CSR arrays; every batch of a
+  // multifrontal level shares one separator graph)
+  uint64_t key = 1469598103934665603ull;
+  auto mix = [&](const void* data, size_t bytes) {
+    const unsigned char* c = static_cast<const unsigned char*>(data);
+    for (size_t i = 0; i < bytes; ++i) key = (key ^ c[i]) * 1099511628211ull;
+  };
+  const int64_t nnz = indptr[p->n];
+  mix(&p->n, sizeof(p->n));
+  mix(&depth, sizeof(depth));
+  mix(indptr, (size_t)(p->n + 1) * 8);
+  mix(indices, (size_t)nnz * 8);
+  const bool hit = p->sel_valid && p->sel_key == key;
+  std::vector<int64_t> sel_all, probes;
+  std::vector<int64_t>& probe_off = p->probe_off;
+  std::vector<int64_t>& probe_cnt = p->probe_cnt;
+  int& max_k = p->sel_max_k;
+  int& max_kc = p->sel_max_kc;
+  if (!hit) {
+  p->sel_valid = false;
   p->rsel.assign(nb, {});
   p->csel.assign(nb, {});
-  std::vector<int64_t> sel_all, probes;
   p->sel_off_r.assign(nb, 0);
   p->sel_off_c.assign(nb, 0);
-  std::vector<int64_t> probe_off(nb, 0), probe_cnt(nb, 0);
-  int max_k = 0, max_kc = 0;
+  probe_off.assign(nb, 0);
+  probe_cnt.assign(nb, 0);
+  max_k = 0;
+  max_kc = 0;
   for (size_t bi = 0; bi < nb; ++bi) {
     const BlockGeom& b = p->blocks[bi];
     std::vector<int64_t> rv(b.m), cv(b.n);
@@ -811,6 +838,9 @@ extern "C" hk_status hk_build_bdlr(hk_plan* p, const double* A, int64_t ld, int6
   }
   CU(upload(p->sel_d, sel_all, st));
   CU(upload(p->probe_d, probes, st));
+  p->sel_key = key;
+  p->sel_valid = true;
+  }
   // scratch per (front, block) with a selection
   std::vector<SkelTask> tasks;
   int64_t work_total = 0, perm_total = 0;

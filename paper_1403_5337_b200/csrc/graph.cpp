@@ -11,11 +11,18 @@
 namespace hk {
 
 // dist[k] for own[k]: BFS distance to the boundary within own; -1 = unreachable.
+// max_depth >= 0: vertices beyond it are left at -1 (enough for a depth
+// selection; BFS distances only grow, so the <= max_depth ones are exact).
 void side_distance(int64_t nverts, const int64_t* indptr, const int64_t* indices,
                    const int64_t* own, int64_t n_own, const int64_t* other, int64_t n_other,
-                   std::vector<int64_t>& dist) {
-  std::vector<int8_t> is_other(nverts, 0);
-  std::vector<int64_t> where(nverts, -1);
+                   std::vector<int64_t>& dist, int64_t max_depth) {
+  // per-thread scratch over the whole vertex range, reset after use
+  thread_local std::vector<int8_t> is_other;
+  thread_local std::vector<int64_t> where;
+  if ((int64_t)is_other.size() < nverts) {
+    is_other.assign(nverts, 0);
+    where.assign(nverts, -1);
+  }
   for (int64_t k = 0; k < n_other; ++k) is_other[other[k]] = 1;
   for (int64_t k = 0; k < n_own; ++k) where[own[k]] = k;
   // boundary vertices sorted by id (graph.py:179-180)
@@ -37,6 +44,7 @@ void side_distance(int64_t nverts, const int64_t* indptr, const int64_t* indices
   for (size_t head = 0; head < queue.size(); ++head) {
     const int64_t v = queue[head];
     const int64_t dv = dist[where[v]];
+    if (max_depth >= 0 && dv >= max_depth) break;   // FIFO: every later vertex is as far
     for (int64_t e = indptr[v]; e < indptr[v + 1]; ++e) {
       const int64_t u = indices[e];
       const int64_t k = where[u];
@@ -46,6 +54,8 @@ void side_distance(int64_t nverts, const int64_t* indptr, const int64_t* indices
       }
     }
   }
+  for (int64_t k = 0; k < n_other; ++k) is_other[other[k]] = 0;
+  for (int64_t k = 0; k < n_own; ++k) where[own[k]] = -1;
 }
 
 bool select_by_depth(int64_t nverts, const int64_t* indptr, const int64_t* indices,
@@ -58,7 +68,7 @@ bool select_by_depth(int64_t nverts, const int64_t* indptr, const int64_t* indic
     const int64_t* oth = side == 0 ? col_verts : row_verts;
     const int64_t n_oth = side == 0 ? n_cols : n_rows;
     std::vector<int64_t> dist;
-    side_distance(nverts, indptr, indices, own, n_own, oth, n_oth, dist);
+    side_distance(nverts, indptr, indices, own, n_own, oth, n_oth, dist, depth);
     std::vector<int64_t> keep;
     for (int64_t k = 0; k < n_own; ++k)
       if (dist[k] >= 0 && dist[k] <= depth) keep.push_back(k);
