@@ -18,7 +18,8 @@ INCLUDE = PKG.parent / "include"
 LIB = Path(os.environ["HK_LIB_OUT"]) if os.environ.get("HK_LIB_OUT") else PKG / "libhodlr_b200.so"
 # experiment knob: extra nvcc flags (e.g. "-DHK_ACA_LB1") for variant builds written to HK_LIB_OUT
 EXTRA = os.environ.get("HK_NVCC_EXTRA", "").split()
-SOURCES = ["aca.cu", "lu.cu", "gj.cu", "gemm.cu", "solve.cu", "krylov.cu", "api.cpp", "graph.cpp"]
+SOURCES = ["aca.cu", "lu.cu", "gj.cu", "gemm.cu", "solve.cu", "krylov.cu", "select.cu", "api.cpp",
+           "graph.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -305,6 +305,7 @@ struct hk_plan {
   std::vector<cudaEvent_t> fev;     // factor: staging-commit events (front-group streams)
   // BDLR selection cache (graph hash, depth)
   bool sel_valid = false;
+  DevBuf gidx_d, selout_d, seltask_d;   // device graph CSR and GPU selection outputs
   uint64_t sel_key = 0;
   std::vector<int64_t> probe_off, probe_cnt;
   int sel_max_k = 0, sel_max_kc = 0;
@@ -345,7 +346,7 @@ struct hk_plan {
       if (x) cudaEventDestroy(x);
     for (auto& x : fev)
       if (x) cudaEventDestroy(x);
-    DevBuf* bufs[] = {&aca_cnt, &aca_scr, &At, &UV, &ranks_d, &trace_d, &tasks_d, &sel_d, &work_d, &perm_d,
+    DevBuf* bufs[] = {&gidx_d, &selout_d, &seltask_d, &aca_cnt, &aca_scr, &At, &UV, &ranks_d, &trace_d, &tasks_d, &sel_d, &work_d, &perm_d,
                       &skel_status_d, &probe_d, &Y, &Ytmp, &F, &I, &ftask_d, &fmap_d, &gj_d, &gj2_d, &gjs_d,
                       &Xin, &X2, &G, &Yv};
     for (DevBuf* b : bufs) b->release();
@@ -815,14 +816,73 @@ extern "C" hk_status hk_build_bdlr(hk_plan* p, const double* A, int64_t ld, int6
   probe_cnt.assign(nb, 0);
   max_k = 0;
   max_kc = 0;
+  // selections of every block: on the GPU (select.cu; default) or by the
+  // host BFS (graph.cpp; HK_BDLR_SELECT=host) -- identical results
+  std::vector<std::vector<int64_t>> all_rs(nb), all_cs(nb);
+  static int gpu_sel = -1;
+  if (gpu_sel < 0) {
+    const char* e = getenv("HK_BDLR_SELECT");
+    gpu_sel = (e && std::string(e) == "host") ? 0 : 1;
+  }
+  if (gpu_sel) {
+    CU(p->gidx_d.ensure((size_t)(p->n + 1 + nnz) * 8 + 8, st));
+    int64_t* gip = p->gidx_d.as<int64_t>();
+    CU(cudaMemcpyAsync(gip, indptr, (size_t)(p->n + 1) * 8, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(gip + p->n + 1, indices, (size_t)nnz * 8, cudaMemcpyHostToDevice, st));
+    std::vector<SelTask> sts;
+    std::vector<int64_t> off;
+    int64_t cap = 0;
+    int max_own = 1;
+    for (size_t bi = 0; bi < nb; ++bi) {
+      const BlockGeom& b = p->blocks[bi];
+      for (int side = 0; side < 2; ++side) {
+        SelTask t{};
+        t.own0 = side == 0 ? b.row0 : b.col0;
+        t.n_own = side == 0 ? b.m : b.n;
+        t.oth0 = side == 0 ? b.col0 : b.row0;
+        t.n_oth = side == 0 ? b.n : b.m;
+        off.push_back(cap);
+        cap += t.n_own;
+        max_own = std::max(max_own, t.n_own);
+        sts.push_back(t);
+      }
+    }
+    CU(p->selout_d.ensure((size_t)cap * 8 + (size_t)sts.size() * 4 + 64, st));
+    int64_t* outd = p->selout_d.as<int64_t>();
+    int32_t* cntd = reinterpret_cast<int32_t*>(outd + cap);
+    for (size_t i = 0; i < sts.size(); ++i) {
+      sts[i].out = outd + off[i];
+      sts[i].count = cntd + i;
+    }
+    CU(upload(p->seltask_d, sts, st));
+    CU(hk_launch_select(p->seltask_d.as<SelTask>(), (int)sts.size(), max_own, gip, gip + p->n + 1,
+                        depth, st));
+    std::vector<int64_t> outh((size_t)cap);
+    std::vector<int32_t> cnth(sts.size());
+    CU(cudaMemcpyAsync(outh.data(), outd, (size_t)cap * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(cnth.data(), cntd, cnth.size() * 4, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    for (size_t bi = 0; bi < nb; ++bi) {
+      all_rs[bi].assign(outh.begin() + off[2 * bi], outh.begin() + off[2 * bi] + cnth[2 * bi]);
+      all_cs[bi].assign(outh.begin() + off[2 * bi + 1],
+                        outh.begin() + off[2 * bi + 1] + cnth[2 * bi + 1]);
+    }
+  } else {
+    for (size_t bi = 0; bi < nb; ++bi) {
+      const BlockGeom& b = p->blocks[bi];
+      std::vector<int64_t> rv(b.m), cv(b.n);
+      for (int i = 0; i < b.m; ++i) rv[i] = b.row0 + i;
+      for (int j = 0; j < b.n; ++j) cv[j] = b.col0 + j;
+      hk::select_by_depth(p->n, indptr, indices, rv.data(), b.m, cv.data(), b.n, depth,
+                          all_rs[bi], all_cs[bi]);
+    }
+  }
   for (size_t bi = 0; bi < nb; ++bi) {
     const BlockGeom& b = p->blocks[bi];
-    std::vector<int64_t> rv(b.m), cv(b.n);
-    for (int i = 0; i < b.m; ++i) rv[i] = b.row0 + i;
-    for (int j = 0; j < b.n; ++j) cv[j] = b.col0 + j;
-    std::vector<int64_t> rs, cs;
-    bool ok = hk::select_by_depth(p->n, indptr, indices, rv.data(), b.m, cv.data(), b.n, depth, rs, cs);
-    if (!ok) continue;  // EmptySelectionError -> rank-0 factor (lowrank.py:345-348)
+    const std::vector<int64_t>& rs = all_rs[bi];
+    const std::vector<int64_t>& cs = all_cs[bi];
+    // EmptySelectionError -> rank-0 factor (lowrank.py:345-348)
+    if (rs.empty() || cs.empty()) continue;
     p->rsel[bi] = rs;
     p->csel[bi] = cs;
     p->sel_off_r[bi] = (int64_t)sel_all.size();

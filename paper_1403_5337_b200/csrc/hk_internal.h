@@ -38,6 +38,17 @@ struct SkelTask {
   double tol;
 };
 
+// ---------------------------------------------------------------- BDLR selection (select.cu)
+struct SelTask {      // one side of one block: own range vs other range
+  int64_t own0, oth0;
+  int32_t n_own, n_oth;
+  int64_t* out;       // capacity n_own: selected positions, (d, position) order
+  int32_t* count;
+};
+cudaError_t hk_launch_select(const SelTask* tasks_dev, int ntasks, int max_own,
+                             const int64_t* indptr_dev, const int64_t* indices_dev, int depth,
+                             cudaStream_t st);
+
 // ---------------------------------------------------------------- dense LU + inverse
 // Partial-pivot LU of an N x N matrix assembled from a source, with explicit
 // inverse.  mode 0: source is a row-major block (src, src_ld).  mode 1:
