@@ -220,6 +220,24 @@ struct BlockGeom {
   int64_t t_off;          // ints, within one front's trace region
 };
 
+struct AcaPlanKey {
+  const void* ptr[6];
+  int64_t v[4];
+  bool operator==(const AcaPlanKey& o) const {
+    for (int i = 0; i < 6; ++i) if (ptr[i] != o.ptr[i]) return false;
+    for (int i = 0; i < 4; ++i) if (v[i] != o.v[i]) return false;
+    return true;
+  }
+};
+struct AcaPlanCache {
+  AcaPlanKey key{};
+  DevBuf tasks;
+  size_t ncl_tasks = 0;
+  int ngroups = 0;
+  int cl_P[4], cl_begin[4], cl_cnt[4], cl_cap[4], cl_m[4];
+  int cls_begin[5], cls_cap[4], cls_m[4];
+};
+
 struct NodeRec {  // per (front, node) factor storage
   int64_t inv = -1, h = -1, q = -1, m = -1;         // doubles in F pool
   int64_t status = -1;                              // ints in I pool
@@ -304,6 +322,7 @@ struct hk_plan {
   cudaStream_t cl_side[4] = {nullptr, nullptr, nullptr, nullptr};   // cluster ACA groups
   std::vector<cudaEvent_t> fev;     // factor: staging-commit events (front-group streams)
   // BDLR selection cache (graph hash, depth)
+  std::vector<AcaPlanCache> aca_plans;   // cached ACA task lists (hk_build_aca)
   bool sel_valid = false;
   DevBuf gidx_d, selout_d, seltask_d;   // device graph CSR and GPU selection outputs
   uint64_t sel_key = 0;
@@ -346,6 +365,7 @@ struct hk_plan {
       if (x) cudaEventDestroy(x);
     for (auto& x : fev)
       if (x) cudaEventDestroy(x);
+    for (auto& c : aca_plans) c.tasks.release();
     DevBuf* bufs[] = {&gidx_d, &selout_d, &seltask_d, &aca_cnt, &aca_scr, &At, &UV, &ranks_d, &trace_d, &tasks_d, &sel_d, &work_d, &perm_d,
                       &skel_status_d, &probe_d, &Y, &Ytmp, &F, &I, &ftask_d, &fmap_d, &gj_d, &gj2_d, &gjs_d,
                       &Xin, &X2, &G, &Yv};
@@ -599,10 +619,6 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
   const int64_t ldat = ld;
   p->have_trace = record_trace != 0;
   if (p->have_trace) CU(p->trace_d.ensure((size_t)p->batch * p->trace_per_front * 4 + 4, st));
-  std::vector<AcaTask> tasks;
-  std::vector<int64_t> task_key;
-  tasks.reserve((size_t)p->batch * p->blocks.size());
-  int max_cap = 0, max_m = 0, max_mn = 0;
   const size_t nb = p->blocks.size();
   size_t scr_per_front = 0;
   std::vector<size_t> scr_off(nb);
@@ -613,6 +629,40 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
     scr_per_front += P > 1 ? hk_aca_scratch_doubles_cl(b.cap, P) : hk_aca_scratch_doubles(b.cap);
   }
   CU(p->aca_scr.ensure((size_t)p->batch * scr_per_front * 8 + 8, st));
+  const char* prof = getenv("HK_ACA_PROFILE");
+  // The task list depends only on the fronts pointer, the plan's buffers and
+  // the caps: a batch rebuilt in the same device buffers (every step of a
+  // level streamed through two buffers) reuses its device copy instead of
+  // planning and staging it again (~0.25 ms of host time with the GPU idle).
+  AcaPlanKey key{};
+  key.ptr[0] = A; key.ptr[1] = p->At.p; key.ptr[2] = p->UV.p; key.ptr[3] = p->ranks_d.p;
+  key.ptr[4] = p->have_trace ? p->trace_d.p : nullptr; key.ptr[5] = p->aca_scr.p;
+  key.v[0] = ld; key.v[1] = fstride; key.v[2] = max_rank; key.v[3] = use_at;
+  AcaPlanCache* hitc = nullptr;
+  if (!prof)
+    for (auto& c : p->aca_plans)
+      if (c.key == key) hitc = &c;
+  const AcaTask* tasks_dev = nullptr;
+  std::vector<AcaTask> tasks;
+  std::vector<int64_t> task_key;
+  size_t ncl_tasks = 0;
+  int cl_P[4] = {0, 0, 0, 0}, cl_begin[4] = {0, 0, 0, 0}, cl_cnt[4] = {0, 0, 0, 0};
+  int cl_cap[4] = {0, 0, 0, 0}, cl_m[4] = {0, 0, 0, 0};
+  int ngroups = 0;
+  int cls_begin[5] = {0, 0, 0, 0, 0}, cls_cap[4] = {0, 0, 0, 0}, cls_m[4] = {0, 0, 0, 0};
+  DevBuf clk;
+  if (hitc) {
+    tasks_dev = hitc->tasks.as<AcaTask>();
+    ncl_tasks = hitc->ncl_tasks;
+    ngroups = hitc->ngroups;
+    memcpy(cl_P, hitc->cl_P, sizeof cl_P); memcpy(cl_begin, hitc->cl_begin, sizeof cl_begin);
+    memcpy(cl_cnt, hitc->cl_cnt, sizeof cl_cnt); memcpy(cl_cap, hitc->cl_cap, sizeof cl_cap);
+    memcpy(cl_m, hitc->cl_m, sizeof cl_m);
+    memcpy(cls_begin, hitc->cls_begin, sizeof cls_begin); memcpy(cls_cap, hitc->cls_cap, sizeof cls_cap);
+    memcpy(cls_m, hitc->cls_m, sizeof cls_m);
+  } else {
+  tasks.reserve((size_t)p->batch * p->blocks.size());
+  int max_cap = 0, max_m = 0, max_mn = 0;
   for (int64_t f = 0; f < p->batch; ++f) {
     for (int bi : p->block_order) {
       const BlockGeom& b = p->blocks[bi];
@@ -660,21 +710,15 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
   tasks.swap(sorted);
   task_key.swap(skey);
   (void)tidx;
-  const char* prof = getenv("HK_ACA_PROFILE");
-  DevBuf clk;
   if (prof) {
     CU(clk.ensure(tasks.size() * 24 + 8, st));
     for (size_t i = 0; i < tasks.size(); ++i) tasks[i].clock = clk.as<int64_t>() + 3 * i;
   }
   p->stage.reset();
-  const AcaTask* tasks_dev = p->stage.push(tasks, st);
+  tasks_dev = p->stage.push(tasks, st);
   if (!tasks_dev) return fail(HK_ERR_CUDA, "pinned staging allocation failed");
   CU(p->stage.commit(st));
   // cluster groups (P = 16, 8, 4, 2) then the four single-CTA classes
-  size_t ncl_tasks = 0;
-  int cl_P[4] = {0, 0, 0, 0}, cl_begin[4] = {0, 0, 0, 0}, cl_cnt[4] = {0, 0, 0, 0};
-  int cl_cap[4] = {0, 0, 0, 0}, cl_m[4] = {0, 0, 0, 0};
-  int ngroups = 0;
   while (ncl_tasks < tasks.size()) {
     const AcaTask& t = tasks[ncl_tasks];
     const int P = hk_aca_cluster_size(t.m, t.n);
@@ -693,7 +737,6 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
       return fail(HK_ERR_VALUE, "block too large for the cluster ACA kernel");
     ++ncl_tasks;
   }
-  int cls_begin[5] = {0, 0, 0, 0, 0}, cls_cap[4] = {0, 0, 0, 0}, cls_m[4] = {0, 0, 0, 0};
   for (size_t i = ncl_tasks; i < tasks.size(); ++i) {
     const AcaTask& t = tasks[i];
     const int c = hk_aca_class(t.m, t.n);
@@ -704,6 +747,25 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
       return fail(HK_ERR_VALUE, "block too large for the single-CTA ACA kernel");
   }
   for (int c = 0; c < 4; ++c) cls_begin[c + 1] += cls_begin[c];
+  if (!prof) {   // keep a device copy of this task list (at most 4 cached)
+    if (p->aca_plans.size() >= 4) {
+      p->aca_plans.front().tasks.release();
+      p->aca_plans.erase(p->aca_plans.begin());
+    }
+    p->aca_plans.emplace_back();
+    AcaPlanCache& c = p->aca_plans.back();
+    c.key = key;
+    CU(c.tasks.ensure(tasks.size() * sizeof(AcaTask) + 16, st));
+    CU(cudaMemcpyAsync(c.tasks.p, tasks_dev, tasks.size() * sizeof(AcaTask), cudaMemcpyDeviceToDevice, st));
+    c.ncl_tasks = ncl_tasks;
+    c.ngroups = ngroups;
+    memcpy(c.cl_P, cl_P, sizeof cl_P); memcpy(c.cl_begin, cl_begin, sizeof cl_begin);
+    memcpy(c.cl_cnt, cl_cnt, sizeof cl_cnt); memcpy(c.cl_cap, cl_cap, sizeof cl_cap);
+    memcpy(c.cl_m, cl_m, sizeof cl_m);
+    memcpy(c.cls_begin, cls_begin, sizeof cls_begin); memcpy(c.cls_cap, cls_cap, sizeof cls_cap);
+    memcpy(c.cls_m, cls_m, sizeof cls_m);
+  }
+  }
   CHK(ensure_side_streams(p));
   CU(p->aca_cnt.ensure(64, st));
   CU(cudaMemsetAsync(p->aca_cnt.p, 0, 64, st));
@@ -1205,6 +1267,10 @@ static hk_status flush(hk_plan* p, std::vector<Op>& ops, cudaStream_t st) {
   return launch_ops(p, ops, st);
 }
 
+struct SolveProg;
+static hk_status build_solve_prog(hk_plan* p, int front, int s, SolveProg*& out, cudaStream_t st);
+static hk_status ensure_solve_scratch(hk_plan* p, int s, cudaStream_t st);
+
 extern "C" hk_status hk_factor_ext(hk_plan* p, const double* Zext, int64_t ldz, int64_t wext,
                                    void* stream) {
   if (!p || !p->built) return fail(HK_ERR_STATE, "factor requires a build");
@@ -1506,6 +1572,14 @@ extern "C" hk_status hk_factor_ext(hk_plan* p, const double* Zext, int64_t ldz, 
   }
   CU(cudaEventRecord(p->ev[2], st));
   hc.mark("plan+launch levels");
+  // The usual next call -- one solve of every front, one rhs -- gets its
+  // program planned now, on the host, while the GPU still runs the levels
+  // (otherwise ~0.2 ms of host planning per batch with the GPU idle).
+  if (wext == 0) {
+    SolveProg* sp = nullptr;
+    if (ensure_solve_scratch(p, 1, st) == HK_OK) (void)build_solve_prog(p, -1, 1, sp, st);
+    hc.mark("solve program");
+  }
   // ---- statuses: first failure in the reference's DFS event order
   std::vector<int32_t> ih((size_t)itot);
   if (itot) CU(cudaMemcpyAsync(ih.data(), I, (size_t)itot * 4, cudaMemcpyDeviceToHost, st));
