@@ -133,6 +133,22 @@ __device__ __forceinline__ void chunk_sub(double (&x)[EPT], const double (&a)[EP
   }
 }
 
+// y[e] += sum_j a[e][j] * coef2[kb + j] (PART: only kb + j < n2): the U-side
+// half of the stopping test as a coefficient sweep instead of dot products,
+// sum_k (u.u_k)(v.v_k) = u . (U b) with b_k = v.v_k (no cross-lane reduction)
+template <int EPT, bool PART>
+__device__ __forceinline__ void chunk_y(double (&y)[EPT], const double (&a)[EPT][KC],
+                                        const double* __restrict__ coef2, int kb, int n2) {
+#pragma unroll
+  for (int j = 0; j < KC; ++j) {
+    const double c = coef2[kb + j];
+    if (!PART || kb + j < n2) {
+#pragma unroll
+      for (int q = 0; q < EPT; ++q) y[q] = fma(a[q][j], c, y[q]);
+    }
+  }
+}
+
 template <int EPT, int LDLOG>
 __device__ __forceinline__ void chunk_load_full(double (&a)[EPT][KC], const double* const (&pk)[EPT],
                                                 int kb) {
@@ -167,10 +183,15 @@ template <int EPT>
 __device__ __forceinline__ void chunk_process(double (&x)[EPT], const double (&a)[EPT][KC],
                                               const double (&pv)[EPT], const double* __restrict__ coef,
                                               int kb, int nk, int ndot, double* __restrict__ mypart,
-                                              int lane) {
+                                              int lane, double (&y)[EPT],
+                                              const double* __restrict__ coef2, int n2) {
   if (kb < ndot) {                               // warp-uniform
     if (kb + KC <= ndot) chunk_dots<EPT, false>(a, pv, kb, ndot, mypart, lane);
     else chunk_dots<EPT, true>(a, pv, kb, ndot, mypart, lane);
+  }
+  if (kb < n2) {                                 // warp-uniform
+    if (kb + KC <= n2) chunk_y<EPT, false>(y, a, coef2, kb, n2);
+    else chunk_y<EPT, true>(y, a, coef2, kb, n2);
   }
   if (kb + KC <= nk) chunk_sub<EPT, false>(x, a, coef, kb, nk);
   else if (kb < nk) chunk_sub<EPT, true>(x, a, coef, kb, nk);
@@ -201,14 +222,17 @@ __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len
                                            int out_col, int pend_col, double* __restrict__ part,
                                            int pld, const unsigned char* __restrict__ used,
                                            ArgMax& best, double& sumsq, double& bestval,
-                                           double* __restrict__ xout) {
+                                           double* __restrict__ xout,
+                                           const double* __restrict__ coef2, int n2, double& ydot) {
   constexpr int64_t LD = int64_t(1) << LDLOG;
   const int tid = threadIdx.x, lane = tid & 31, warp = uniform_warp_id();
   // call arguments are not provably uniform across the call boundary
   len = __shfl_sync(0xffffffffu, len, 0);
   nk = __shfl_sync(0xffffffffu, nk, 0);
   ndot = __shfl_sync(0xffffffffu, ndot, 0);
+  n2 = __shfl_sync(0xffffffffu, n2, 0);
   out_col = __shfl_sync(0xffffffffu, out_col, 0);
+  ydot = 0.0;
   best.v = 0.0;
   best.i = -1;
   bestval = 0.0;
@@ -219,7 +243,7 @@ __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len
   const int kmax = nk > ndot ? nk : ndot;
 #pragma unroll 1
   for (int g0 = 0; g0 < len; g0 += NT * EPT) {
-    double x[EPT], pv[EPT];
+    double x[EPT], pv[EPT], y[EPT];
     const double* pk[EPT];
     bool ok[EPT];
     // Chunks whose KC columns all lie inside the block load unpredicated even
@@ -234,7 +258,8 @@ __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len
       ok[q] = e < len;
       pk[q] = F + (ok[q] ? e : 0);
       x[q] = (ok[q] && src) ? ld_src(src + (int64_t)e * sstride) : 0.0;
-      pv[q] = (ok[q] && ndot > 0) ? pk[q][(int64_t)pend_col * LD] : 0.0;
+      pv[q] = (ok[q] && (ndot > 0 || n2 > 0)) ? pk[q][(int64_t)pend_col * LD] : 0.0;
+      y[q] = 0.0;
     }
     int kb = 0;
     if (gfull) {
@@ -248,12 +273,12 @@ __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len
         for (; kb + 2 * KC <= kfull; kb += 2 * KC) {
           chunk_load_full<EPT, LDLOG>(a1, pk, kb + KC);
           if (kb + 2 * KC < kfull) chunk_prefetch<EPT, LDLOG>(pk, kb + 2 * KC);
-          chunk_process<EPT>(x, a0, pv, coef, kb, nk, ndot, mypart, lane);
+          chunk_process<EPT>(x, a0, pv, coef, kb, nk, ndot, mypart, lane, y, coef2, n2);
           if (kb + 2 * KC < kfull) chunk_load_full<EPT, LDLOG>(a0, pk, kb + 2 * KC);
-          chunk_process<EPT>(x, a1, pv, coef, kb + KC, nk, ndot, mypart, lane);
+          chunk_process<EPT>(x, a1, pv, coef, kb + KC, nk, ndot, mypart, lane, y, coef2, n2);
         }
         if (kb < kfull) {
-          chunk_process<EPT>(x, a0, pv, coef, kb, nk, ndot, mypart, lane);
+          chunk_process<EPT>(x, a0, pv, coef, kb, nk, ndot, mypart, lane, y, coef2, n2);
           kb += KC;
         }
       }
@@ -265,7 +290,7 @@ __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len
         // the next chunk's lines are pulled into L1 while this one is reduced
         // (prefetch distance 1 measured best: 2..4 thrash L1)
         if (kb + KC < kfull) chunk_prefetch<EPT, LDLOG>(pk, kb + KC);
-        chunk_process<EPT>(x, a, pv, coef, kb, nk, ndot, mypart, lane);
+        chunk_process<EPT>(x, a, pv, coef, kb, nk, ndot, mypart, lane, y, coef2, n2);
       }
       }
     }
@@ -277,7 +302,11 @@ __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len
 #pragma unroll
         for (int j = 0; j < KC; ++j)
           a[q][j] = (ok[q] && kb + j < kmax) ? ld_col(pk[q] + (int64_t)(kb + j) * LD) : 0.0;
-      chunk_process<EPT>(x, a, pv, coef, kb, nk, ndot, mypart, lane);
+      chunk_process<EPT>(x, a, pv, coef, kb, nk, ndot, mypart, lane, y, coef2, n2);
+    }
+    if (n2 > 0) {
+#pragma unroll
+      for (int q = 0; q < EPT; ++q) ydot = fma(pv[q], y[q], ydot);
     }
     if (out_col >= 0) {
 #pragma unroll
@@ -308,10 +337,34 @@ __device__ __noinline__ void sweep(int ldlog, const double* __restrict__ F, int 
                                    int sstride, int out_col, int pend_col, double* __restrict__ part,
                                    int pld, const unsigned char* __restrict__ used, ArgMax& best,
                                    double& sumsq, double& bestval, double* xout) {
+  double yd;
 #define HK_SWEEP_CASE(L)                                                                       \
   case L:                                                                                      \
     sweep_impl<NT, EPT, L, DB>(F, len, nk, ndot, coef, src, sstride, out_col, pend_col, part, pld, \
-                           used, best, sumsq, bestval, xout);                                  \
+                           used, best, sumsq, bestval, xout, nullptr, 0, yd);                  \
+    return;
+  switch (ldlog) {
+    HK_SWEEP_CASE(6) HK_SWEEP_CASE(7) HK_SWEEP_CASE(8) HK_SWEEP_CASE(9) HK_SWEEP_CASE(10)
+    HK_SWEEP_CASE(11) HK_SWEEP_CASE(12) HK_SWEEP_CASE(13)
+    default: return;
+  }
+#undef HK_SWEEP_CASE
+}
+
+// The column sweep of the main ACA step with the coefficient sweep of the
+// stopping test (y = U b, ydot = u_r . y), a separate call target so the
+// other sweeps keep their register allocation.
+template <int NT, int EPT, int DB>
+__device__ __noinline__ void sweep_y(int ldlog, const double* __restrict__ F, int len, int nk,
+                                     const double* __restrict__ coef, const double* __restrict__ src,
+                                     int sstride, int out_col, int pend_col,
+                                     const unsigned char* __restrict__ used, ArgMax& best,
+                                     double& sumsq, double& bestval, double* xout,
+                                     const double* __restrict__ coef2, int n2, double& ydot) {
+#define HK_SWEEP_CASE(L)                                                                       \
+  case L:                                                                                      \
+    sweep_impl<NT, EPT, L, DB>(F, len, nk, 0, coef, src, sstride, out_col, pend_col, nullptr, 0, \
+                           used, best, sumsq, bestval, xout, coef2, n2, ydot);                 \
     return;
   switch (ldlog) {
     HK_SWEEP_CASE(6) HK_SWEEP_CASE(7) HK_SWEEP_CASE(8) HK_SWEEP_CASE(9) HK_SWEEP_CASE(10)
@@ -411,18 +464,19 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
   extern __shared__ __align__(16) unsigned char smraw[];
   const int ldlog = __shfl_sync(0xffffffffu, t.ldu, 0);   // U and V share one power-of-two LD
   const int64_t LD = int64_t(1) << ldlog;
-  // SMEM layout: coef[cap+KC], partU/partV[NW*cap], prod[cap] (or global
-  // scratch when they do not fit), used[m]
+  // SMEM layout: coef[cap+KC], bv[cap+KC], partU/partV[NW*cap], prod[cap]
+  // (or global scratch when they do not fit), used[m]
   double* sbase = reinterpret_cast<double*>(smraw);
   double* U = t.U;
   double* V = t.V;
   double* coef = sbase;
   const int pld = cap;
   const bool pin = part_in_smem;
-  double* partU = pin ? coef + cap + KC : t.scratch;
+  double* bv = coef + cap + KC;     // b_k = v_r . v_k of the pending cross (stopping test)
+  double* partU = pin ? bv + cap + KC : t.scratch;
   double* partV = partU + NW * pld;
   double* prod = partV + NW * pld;
-  unsigned char* used = reinterpret_cast<unsigned char*>(pin ? prod + cap : coef + cap + KC);
+  unsigned char* used = reinterpret_cast<unsigned char*>(pin ? prod + cap : bv + cap + KC);
   __shared__ double red_v[NW > 0 ? NW : 1], red_a[NW > 0 ? NW : 1], red_b[NW > 0 ? NW : 1],
       red_x[NW > 0 ? NW : 1];
   __shared__ int64_t red_i[NW > 0 ? NW : 1];
@@ -441,7 +495,7 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
     return;
   }
   for (int i = tid; i < m; i += NT) used[i] = 0;
-  for (int k = tid; k < cap + KC; k += NT) coef[k] = 0.0;
+  for (int k = tid; k < cap + KC; k += NT) coef[k] = bv[k] = 0.0;
   __syncthreads();
 
   const double* rowsrc_base = t.A;
@@ -506,6 +560,17 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
       bar<NT>();
       continue;
     }
+    // b = V^T v_r of the pending cross (the row sweep's dots), fixed warp
+    // order; the U side of the stopping test becomes a coefficient sweep
+    if (pending) {
+      if (NT == 32) __syncwarp();
+      for (int k = tid; k < r; k += NT) {
+        double sb = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) sb += partV[w * pld + k];
+        bv[k] = sb;
+      }
+    }
     // v = res / delta (:265) over own elements
     double vv = 0.0;
     if (n <= NT * EPT) {
@@ -535,38 +600,47 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
     // row-major front itself with stride lda
     const double* csrc = t.At ? t.At + (int64_t)col * t.lda : t.A + col;
     const int cstride = t.At ? 1 : (int)t.lda;
-    sweep<NT, EPT, DB>(ldlog, U, m, c, pending ? r : 0, coef, csrc, cstride, c, r, partU, pld,
-                   used, nxt, uu, bval, xv);
+    double ydot = 0.0;
+    sweep_y<NT, EPT, DB>(ldlog, U, m, c, coef, csrc, cstride, c, r, used, nxt, uu, bval, xv, bv,
+                         pending ? r : 0, ydot);
     {
       // next row = argmax over untouched rows; uu = |u|^2, vv = |v|^2 (fixed
       // summation order: warp tree, then the warp partials in warp order)
       const int wi = warp_argmax_idx(nxt.v, nxt.i >= 0, (int)nxt.i);
       uu = warp_sum(uu);
       vv = warp_sum(vv);
+      ydot = warp_sum(ydot);
       if (NT == 32) {
         nxt.i = wi;
         uu = __shfl_sync(0xffffffffu, uu, 0);
         vv = __shfl_sync(0xffffffffu, vv, 0);
+        ydot = __shfl_sync(0xffffffffu, ydot, 0);
       } else {
         const double wv = __shfl_sync(0xffffffffu, nxt.v, wi & 31);
-        if (lane == 0) { red_v[warp] = wv; red_i[warp] = wi; red_a[warp] = uu; red_b[warp] = vv; }
+        if (lane == 0) {
+          red_v[warp] = wv; red_i[warp] = wi; red_a[warp] = uu; red_b[warp] = vv; red_x[warp] = ydot;
+        }
         __syncthreads();
         const bool ok = lane < NW && red_i[lane < NW ? lane : 0] >= 0;
         const double cv = lane < NW ? red_v[lane] : 0.0;
         const int ci = lane < NW ? (int)red_i[lane] : -1;
         double a2 = lane < NW ? red_a[lane] : 0.0;
         double c2 = lane < NW ? red_b[lane] : 0.0;
+        double y2 = lane < NW ? red_x[lane] : 0.0;
         nxt.i = warp_argmax_idx(cv, ok, ci);
         a2 = warp_sum(a2);
         c2 = warp_sum(c2);
+        y2 = warp_sum(y2);
         uu = __shfl_sync(0xffffffffu, a2, 0);
         vv = __shfl_sync(0xffffffffu, c2, 0);
+        ydot = __shfl_sync(0xffffffffu, y2, 0);
         // red_* are next written after the next step's first block barrier
       }
     }
     if (pending) {                            // stopping test of the pending cross (:269-275)
+      // sum_k 2 (u_r.u_k)(v_r.v_k) = 2 u_r . (U b): the column sweep's ydot
       const double cross = uu_p * vv_p;
-      const double est = stopping_estimate<NT>(partU, partV, pld, r, fro2, cross, prod, &s_est);
+      const double est = fmax(fro2 + cross + 2.0 * ydot, cross);
       if (cross <= tol2 * est) {              // reject: drop the speculative step's reads
         --nrow_ev;
         --ncol_ev;
@@ -767,6 +841,10 @@ __global__ void __launch_bounds__(NT) aca_cluster_kernel(const AcaTask* __restri
 
   double* Us = t.U + mu0;
   double* Vs = t.V + nv0;
+  // column gathers: column col of the slice starts at cbase + col * cstep
+  const double* cbase = t.At ? t.At + mu0 : t.A + (int64_t)mu0 * t.lda;
+  const int64_t cstep = t.At ? t.lda : 1;
+  const int cstride = t.At ? 1 : (int)t.lda;
   int r = 0, row = 0, nused = 0;
   bool pending = false;
   double uu_p = 0.0, vv_p = 0.0, fro2 = 0.0;
@@ -872,9 +950,8 @@ __global__ void __launch_bounds__(NT) aca_cluster_kernel(const AcaTask* __restri
     ++ncol_ev;
     bar<NT>();
     // residual column slice + next-row candidate + pending u dots
-    sweep<NT, EPT, DB>(ldlog, Us, mlen, c, pending ? r : 0, coef,
-                       t.At ? t.At + (int64_t)col * t.lda + mu0 : t.A + (int64_t)mu0 * t.lda + col,
-                       t.At ? 1 : (int)t.lda, c, r, partU, pld, used + mu0, nxt,
+    sweep<NT, EPT, DB>(ldlog, Us, mlen, c, pending ? r : 0, coef, cbase + (int64_t)col * cstep,
+                       cstride, c, r, partU, pld, used + mu0, nxt,
                        uu, bval, xv);
     {
       const int lane = tid & 31, warp = uniform_warp_id();
@@ -972,7 +1049,7 @@ template <int NT, int EPT, int DB>
 static cudaError_t launch_cls(const AcaTask* tasks_dev, int ntasks, int max_cap, int max_m,
                               double tol2, int* counter, cudaStream_t st) {
   const size_t part_bytes = (size_t)(2 * (NT / 32) + 1) * max_cap * 8;
-  const size_t base = (size_t)(max_cap + KC) * 8 + (size_t)max_m + 16;
+  const size_t base = (size_t)2 * (max_cap + KC) * 8 + (size_t)max_m + 16;   // coef, bv, used
   const int part_in_smem = (base + part_bytes <= HK_ACA_PART_SMEM) ? 1 : 0;
   const size_t smem = base + (part_in_smem ? part_bytes : 0);
   cudaError_t e = cudaFuncSetAttribute(aca_kernel<NT, EPT, DB>,

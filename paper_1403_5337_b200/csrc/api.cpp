@@ -743,7 +743,7 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
     cls_begin[c + 1]++;
     cls_cap[c] = std::max(cls_cap[c], t.cap);
     cls_m[c] = std::max(cls_m[c], t.m);
-    if ((size_t)(t.cap + 16) * 8 + t.m + 1024 > 220 * 1024)
+    if ((size_t)(2 * t.cap + 32) * 8 + t.m + 1024 > 220 * 1024)
       return fail(HK_ERR_VALUE, "block too large for the single-CTA ACA kernel");
   }
   for (int c = 0; c < 4; ++c) cls_begin[c + 1] += cls_begin[c];
