@@ -790,7 +790,7 @@ __device__ __forceinline__ double cl_est_total(const double* slE, unsigned P) {
 }
 
 template <int NT, int EPT, int DB>
-__global__ void __launch_bounds__(NT) aca_cluster_kernel(const AcaTask* __restrict__ tasks,
+__global__ void __maxnreg__(200) aca_cluster_kernel(const AcaTask* __restrict__ tasks,
                                                          double tol2, int part_in_smem) {
   constexpr int NW = NT / 32;
   const unsigned P = cl_nrank(), q = cl_rank();
@@ -808,15 +808,16 @@ __global__ void __launch_bounds__(NT) aca_cluster_kernel(const AcaTask* __restri
   const int sln = (((n + (int)P - 1) / (int)P) + 15) & ~15;
   const int mu0 = min(m, (int)q * slm), mlen = min(m, mu0 + slm) - mu0;
   const int nv0 = min(n, (int)q * sln), nlen = min(n, nv0 + sln) - nv0;
-  // SMEM: coef[cap+KC], cpU[cap], cpV[cap], (partU, partV [NW*cap] each), used[m]
+  // SMEM: coef[cap+KC], cpU[cap], cpV[cap], bvc[cap+KC], (partU, partV [NW*cap] each), used[m]
   double* coef = reinterpret_cast<double*>(smraw);
   double* cpU = coef + cap + KC;
   double* cpV = cpU + cap;
+  double* bvc = cpV + cap;          // b_k = v_r . v_k over the whole cluster (stopping test)
   const int pld = cap;
-  double* partU = part_in_smem ? cpV + cap : t.scratch + (size_t)q * 2 * NW * cap;
+  double* partU = part_in_smem ? bvc + cap + KC : t.scratch + (size_t)q * 2 * NW * cap;
   double* partV = partU + NW * pld;
   unsigned char* used =
-      reinterpret_cast<unsigned char*>(part_in_smem ? partV + NW * pld : cpV + cap);
+      reinterpret_cast<unsigned char*>(part_in_smem ? partV + NW * pld : bvc + cap + KC);
   __shared__ double red_v[NW], red_a[NW], red_b[NW], red_x[NW];
   __shared__ int64_t red_i[NW];
   __shared__ ClSlot slR, slC;
@@ -836,7 +837,7 @@ __global__ void __launch_bounds__(NT) aca_cluster_kernel(const AcaTask* __restri
     return;
   }
   for (int i = tid; i < m; i += NT) used[i] = 0;
-  for (int k = tid; k < cap + KC; k += NT) coef[k] = 0.0;
+  for (int k = tid; k < cap + KC; k += NT) coef[k] = bvc[k] = 0.0;
   cluster_bar();
 
   double* Us = t.U + mu0;
@@ -898,6 +899,14 @@ __global__ void __launch_bounds__(NT) aca_cluster_kernel(const AcaTask* __restri
         slR.idx = lb.i >= 0 ? (int)lb.i + nv0 : -1;
         slR.a = slR.b = 0.0;
       }
+      // this CTA's share of b = V^T v_r (its warps' partials, fixed order)
+      if (pending)
+        for (int k = tid; k < r; k += NT) {
+          double sb = 0.0;
+#pragma unroll
+          for (int w = 0; w < NW; ++w) sb += partV[w * pld + k];
+          cpV[k] = sb;
+        }
     }
     cluster_bar();                                             // BAR1
     double delta, sa, sb;
@@ -945,37 +954,48 @@ __global__ void __launch_bounds__(NT) aca_cluster_kernel(const AcaTask* __restri
         vv += v * v;
       }
     }
+    // b over the cluster (slot order), the coefficients of the U-side sweep
+    if (pending)
+      for (int k = tid; k < r; k += NT) {
+        double sb = 0.0;
+        for (unsigned pp = 0; pp < P; ++pp) sb += *cl_map(cpV + k, pp);
+        bvc[k] = sb;
+      }
     for (int k = tid; k < c; k += NT) coef[k] = __ldcg(t.V + col + (int64_t)k * LD);
     if (tid == 0 && tcols) tcols[ncol_ev] = col;
     ++ncol_ev;
     bar<NT>();
-    // residual column slice + next-row candidate + pending u dots
-    sweep<NT, EPT, DB>(ldlog, Us, mlen, c, pending ? r : 0, coef, cbase + (int64_t)col * cstep,
-                       cstride, c, r, partU, pld, used + mu0, nxt,
-                       uu, bval, xv);
+    // residual column slice + next-row candidate + y = U b for the pending cross
+    double ydot = 0.0;
+    sweep_y<NT, EPT, DB>(ldlog, Us, mlen, c, coef, cbase + (int64_t)col * cstep, cstride, c, r,
+                         used + mu0, nxt, uu, bval, xv, bvc, pending ? r : 0, ydot);
     {
       const int lane = tid & 31, warp = uniform_warp_id();
       const int wi = warp_argmax_idx(nxt.v, nxt.i >= 0, (int)nxt.i);
       uu = warp_sum(uu);
       vv = warp_sum(vv);
+      ydot = warp_sum(ydot);
       const double wv = __shfl_sync(0xffffffffu, nxt.v, wi & 31);
-      if (lane == 0) { red_v[warp] = wv; red_i[warp] = wi; red_a[warp] = uu; red_b[warp] = vv; }
+      if (lane == 0) {
+        red_v[warp] = wv; red_i[warp] = wi; red_a[warp] = uu; red_b[warp] = vv; red_x[warp] = ydot;
+      }
       __syncthreads();
       const bool ok = lane < NW && red_i[lane < NW ? lane : 0] >= 0;
       const double cv = lane < NW ? red_v[lane] : 0.0;
       const int ci = lane < NW ? (int)red_i[lane] : -1;
       double a2 = lane < NW ? red_a[lane] : 0.0;
       double c2 = lane < NW ? red_b[lane] : 0.0;
+      double y2 = lane < NW ? red_x[lane] : 0.0;
       const int bi = warp_argmax_idx(cv, ok, ci);
       a2 = warp_sum(a2);
       c2 = warp_sum(c2);
+      y2 = warp_sum(y2);
       const unsigned mask = __ballot_sync(0xffffffffu, ok && ci == bi);
       const double bv = __shfl_sync(0xffffffffu, cv, mask ? __ffs(mask) - 1 : 0);
-      if (pending) cl_reduce_parts<NT>(partU, partV, pld, r, cpU, cpV);
       if (tid == 0) {
         slC.v = bv;
         slC.idx = bi >= 0 ? bi + mu0 : -1;
-        slC.val = 0.0;
+        slC.val = y2;                     // this CTA's u_r . (U b)
         slC.a = a2;
         slC.b = c2;
       }
@@ -984,10 +1004,13 @@ __global__ void __launch_bounds__(NT) aca_cluster_kernel(const AcaTask* __restri
     double dum;
     const int nrow = cl_argmax(&slC, P, dum, uu, vv);
     if (pending) {                            // stopping test of the pending cross (:269-275)
-      cl_est_share(cpU, cpV, r, q, P, &slE);
-      cluster_bar();                                           // BAR3
+      // sum_k 2 (u_r.u_k)(v_r.v_k) = 2 u_r . (U b), summed over the slots in order
+      const int lane = tid & 31;
+      double ys = lane < (int)P ? cl_map(&slC, (unsigned)lane)->val : 0.0;
+      ys = warp_sum(ys);
+      ys = __shfl_sync(0xffffffffu, ys, 0);
       const double cross = uu_p * vv_p;
-      const double est = fmax(fro2 + cross + cl_est_total(&slE, P), cross);
+      const double est = fmax(fro2 + cross + 2.0 * ys, cross);
       if (cross <= tol2 * est) {
         --nrow_ev;
         --ncol_ev;
@@ -1173,7 +1196,7 @@ cudaError_t hk_launch_aca_cluster(const AcaTask* tasks_dev, int ntasks, int P, i
   if (ntasks == 0) return cudaSuccess;
   auto kern = aca_cluster_kernel<kClNT, kClEPT, HK_ACA_CLDB>;
   constexpr int NW = kClNT / 32;
-  const size_t base = (size_t)(max_cap + KC) * 8 + (size_t)2 * max_cap * 8 + (size_t)max_m + 16;
+  const size_t base = (size_t)2 * (max_cap + KC) * 8 + (size_t)2 * max_cap * 8 + (size_t)max_m + 16;
   const size_t part_bytes = (size_t)2 * NW * max_cap * 8;
   const int part_in_smem = (base + part_bytes <= 200 * 1024) ? 1 : 0;
   const size_t smem = base + (part_in_smem ? part_bytes : 0);

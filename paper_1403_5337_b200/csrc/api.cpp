@@ -733,7 +733,7 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
     cl_cnt[g]++;
     cl_cap[g] = std::max(cl_cap[g], t.cap);
     cl_m[g] = std::max(cl_m[g], t.m);
-    if ((size_t)(3 * t.cap + 16) * 8 + t.m + 1024 > 220 * 1024)
+    if ((size_t)(4 * t.cap + 32) * 8 + t.m + 1024 > 220 * 1024)
       return fail(HK_ERR_VALUE, "block too large for the cluster ACA kernel");
     ++ncl_tasks;
   }
