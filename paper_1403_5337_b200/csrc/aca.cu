@@ -697,10 +697,13 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaTask* __restrict__ tas
 // one SM for 53 ms while the rest of the GPU idled.  Here CTA q of the cluster
 // owns the 16-aligned slice [q*S, (q+1)*S) of the entries of both U and V, so
 // each sweep streams only its slice; the decisions that couple the slices go
-// through distributed shared memory, three cluster barriers per step:
-//   BAR1  row-sweep argmax -> pivot column and delta   (R slots)
-//   BAR2  column-sweep argmax -> next row, |u|^2, |v|^2, per-CTA dot partials
-//   BAR3  stopping-estimate partial sums               (E slots)
+// through distributed shared memory, two cluster barriers per step:
+//   BAR1  row-sweep argmax -> pivot column and delta (R slots); per-CTA
+//         b = V^T v_r partials, summed over the cluster for the column sweep
+//   BAR2  column-sweep argmax -> next row, |u|^2, |v|^2 and the per-CTA
+//         u_r . (U b) of the stopping test (C slots)
+// (the rare paths -- zero residual row, last step -- still decide through
+// explicit dot partials and the E slots)
 // Every CTA evaluates every decision from the same slots in the same order,
 // so control stays cluster-uniform.  The residual entries are computed
 // exactly as in aca_block (reference k order, separate multiply/subtract), so
