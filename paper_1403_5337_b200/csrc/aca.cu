@@ -48,6 +48,12 @@ __global__ void transpose_kernel(const double* __restrict__ A, double* __restric
 #define HK_ACA_KC 8
 #endif
 constexpr int KC = HK_ACA_KC;   // columns per chunk (one transpose-reduce each): 8 or 16
+#ifndef HK_ACA_KCY
+#define HK_ACA_KCY 8
+#endif
+constexpr int KCY = HK_ACA_KCY;  // columns per chunk of the dot-free column sweep (sweep_y);
+                                 // 16 measured slower (4.19 vs 3.96 ms: registers, occupancy)
+constexpr int KPAD = 16;         // coefficient arrays are padded by this many entries
 
 // Lane l of the warp receives the warp-wide sum of a[l & (KC-1)] (butterfly
 // reduce-scatter inside groups of KC lanes, then exchanges between groups).
@@ -120,11 +126,11 @@ __device__ __forceinline__ void chunk_dots(const double (&a)[EPT][KC], const dou
 
 // residual update x[e] -= coef[k] * a[e][k] in k order (separate IEEE
 // multiply and subtract: bit-exact with the reference); PART: only k < nk.
-template <int EPT, bool PART>
-__device__ __forceinline__ void chunk_sub(double (&x)[EPT], const double (&a)[EPT][KC],
+template <int EPT, bool PART, int KW>
+__device__ __forceinline__ void chunk_sub(double (&x)[EPT], const double (&a)[EPT][KW],
                                           const double* __restrict__ coef, int kb, int nk) {
 #pragma unroll
-  for (int j = 0; j < KC; ++j) {
+  for (int j = 0; j < KW; ++j) {
     const double c = coef[kb + j];
     if (!PART || kb + j < nk) {
 #pragma unroll
@@ -136,11 +142,11 @@ __device__ __forceinline__ void chunk_sub(double (&x)[EPT], const double (&a)[EP
 // y[e] += sum_j a[e][j] * coef2[kb + j] (PART: only kb + j < n2): the U-side
 // half of the stopping test as a coefficient sweep instead of dot products,
 // sum_k (u.u_k)(v.v_k) = u . (U b) with b_k = v.v_k (no cross-lane reduction)
-template <int EPT, bool PART>
-__device__ __forceinline__ void chunk_y(double (&y)[EPT], const double (&a)[EPT][KC],
+template <int EPT, bool PART, int KW>
+__device__ __forceinline__ void chunk_y(double (&y)[EPT], const double (&a)[EPT][KW],
                                         const double* __restrict__ coef2, int kb, int n2) {
 #pragma unroll
-  for (int j = 0; j < KC; ++j) {
+  for (int j = 0; j < KW; ++j) {
     const double c = coef2[kb + j];
     if (!PART || kb + j < n2) {
 #pragma unroll
@@ -149,15 +155,15 @@ __device__ __forceinline__ void chunk_y(double (&y)[EPT], const double (&a)[EPT]
   }
 }
 
-template <int EPT, int LDLOG>
-__device__ __forceinline__ void chunk_load_full(double (&a)[EPT][KC], const double* const (&pk)[EPT],
+template <int EPT, int LDLOG, int KW>
+__device__ __forceinline__ void chunk_load_full(double (&a)[EPT][KW], const double* const (&pk)[EPT],
                                                 int kb) {
   constexpr int64_t LD = int64_t(1) << LDLOG;
 #pragma unroll
   for (int q = 0; q < EPT; ++q) {
     const double* p = pk[q] + (int64_t)kb * LD;
 #pragma unroll
-    for (int j = 0; j < KC; ++j) a[q][j] = ld_col(p + j * LD);
+    for (int j = 0; j < KW; ++j) a[q][j] = ld_col(p + j * LD);
   }
 }
 
@@ -166,7 +172,7 @@ __device__ __forceinline__ void chunk_load_full(double (&a)[EPT][KC], const doub
 // not coalesced across lanes, so only lanes 0 and 16 issue them (one request
 // per line instead of 32: the ncu capture showed the per-lane prefetches as
 // ~40% of the kernel's L2 sectors).
-template <int EPT, int LDLOG>
+template <int EPT, int LDLOG, int KW>
 __device__ __forceinline__ void chunk_prefetch(const double* const (&pk)[EPT], int kb) {
   constexpr int64_t LD = int64_t(1) << LDLOG;
   if ((threadIdx.x & 15) != 0) return;
@@ -174,27 +180,29 @@ __device__ __forceinline__ void chunk_prefetch(const double* const (&pk)[EPT], i
   for (int q = 0; q < EPT; ++q) {
     const double* p = pk[q] + (int64_t)kb * LD;
 #pragma unroll
-    for (int j = 0; j < KC; ++j) asm volatile("prefetch.global.L1 [%0];" ::"l"(p + j * LD));
+    for (int j = 0; j < KW; ++j) asm volatile("prefetch.global.L1 [%0];" ::"l"(p + j * LD));
   }
 }
 
 // Both halves of a full chunk's work; the chunk's column range is [kb, kb+KC).
-template <int EPT>
-__device__ __forceinline__ void chunk_process(double (&x)[EPT], const double (&a)[EPT][KC],
+template <int EPT, int KW>
+__device__ __forceinline__ void chunk_process(double (&x)[EPT], const double (&a)[EPT][KW],
                                               const double (&pv)[EPT], const double* __restrict__ coef,
                                               int kb, int nk, int ndot, double* __restrict__ mypart,
                                               int lane, double (&y)[EPT],
                                               const double* __restrict__ coef2, int n2) {
-  if (kb < ndot) {                               // warp-uniform
-    if (kb + KC <= ndot) chunk_dots<EPT, false>(a, pv, kb, ndot, mypart, lane);
-    else chunk_dots<EPT, true>(a, pv, kb, ndot, mypart, lane);
+  if constexpr (KW == KC) {
+    if (kb < ndot) {                             // warp-uniform
+      if (kb + KC <= ndot) chunk_dots<EPT, false>(a, pv, kb, ndot, mypart, lane);
+      else chunk_dots<EPT, true>(a, pv, kb, ndot, mypart, lane);
+    }
   }
   if (kb < n2) {                                 // warp-uniform
-    if (kb + KC <= n2) chunk_y<EPT, false>(y, a, coef2, kb, n2);
-    else chunk_y<EPT, true>(y, a, coef2, kb, n2);
+    if (kb + KW <= n2) chunk_y<EPT, false, KW>(y, a, coef2, kb, n2);
+    else chunk_y<EPT, true, KW>(y, a, coef2, kb, n2);
   }
-  if (kb + KC <= nk) chunk_sub<EPT, false>(x, a, coef, kb, nk);
-  else if (kb < nk) chunk_sub<EPT, true>(x, a, coef, kb, nk);
+  if (kb + KW <= nk) chunk_sub<EPT, false, KW>(x, a, coef, kb, nk);
+  else if (kb < nk) chunk_sub<EPT, true, KW>(x, a, coef, kb, nk);
 }
 
 // ---------------------------------------------------------------------------
@@ -215,7 +223,7 @@ __device__ __forceinline__ void chunk_process(double (&x)[EPT], const double (&a
 // EPT elements first and then over the warp with one transpose-reduce.  Fixed
 // reduction order (deterministic).  out_col < 0: dots only.  used != nullptr:
 // column sweep (argmax over untouched entries + sum of squares); else row sweep.
-template <int NT, int EPT, int LDLOG, int DB>
+template <int NT, int EPT, int LDLOG, int DB, int KW>
 __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len, int nk, int ndot,
                                            const double* __restrict__ coef,
                                            const double* __restrict__ src, int sstride,
@@ -263,46 +271,46 @@ __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len
     }
     int kb = 0;
     if (gfull) {
-      const int kfull = (kmax / KC) * KC;
+      const int kfull = (kmax / KW) * KW;
       if constexpr (DB != 0) {
       // register double buffer: chunk kb+KC is in flight while chunk kb is reduced
       if (kfull > 0) {
-        double a0[EPT][KC], a1[EPT][KC];
-        chunk_load_full<EPT, LDLOG>(a0, pk, 0);
+        double a0[EPT][KW], a1[EPT][KW];
+        chunk_load_full<EPT, LDLOG, KW>(a0, pk, 0);
 #pragma unroll 1
-        for (; kb + 2 * KC <= kfull; kb += 2 * KC) {
-          chunk_load_full<EPT, LDLOG>(a1, pk, kb + KC);
-          if (kb + 2 * KC < kfull) chunk_prefetch<EPT, LDLOG>(pk, kb + 2 * KC);
-          chunk_process<EPT>(x, a0, pv, coef, kb, nk, ndot, mypart, lane, y, coef2, n2);
-          if (kb + 2 * KC < kfull) chunk_load_full<EPT, LDLOG>(a0, pk, kb + 2 * KC);
-          chunk_process<EPT>(x, a1, pv, coef, kb + KC, nk, ndot, mypart, lane, y, coef2, n2);
+        for (; kb + 2 * KW <= kfull; kb += 2 * KW) {
+          chunk_load_full<EPT, LDLOG, KW>(a1, pk, kb + KW);
+          if (kb + 2 * KW < kfull) chunk_prefetch<EPT, LDLOG, KW>(pk, kb + 2 * KW);
+          chunk_process<EPT, KW>(x, a0, pv, coef, kb, nk, ndot, mypart, lane, y, coef2, n2);
+          if (kb + 2 * KW < kfull) chunk_load_full<EPT, LDLOG, KW>(a0, pk, kb + 2 * KW);
+          chunk_process<EPT, KW>(x, a1, pv, coef, kb + KW, nk, ndot, mypart, lane, y, coef2, n2);
         }
         if (kb < kfull) {
-          chunk_process<EPT>(x, a0, pv, coef, kb, nk, ndot, mypart, lane, y, coef2, n2);
-          kb += KC;
+          chunk_process<EPT, KW>(x, a0, pv, coef, kb, nk, ndot, mypart, lane, y, coef2, n2);
+          kb += KW;
         }
       }
       } else {
 #pragma unroll 1
-      for (; kb < kfull; kb += KC) {
-        double a[EPT][KC];
-        chunk_load_full<EPT, LDLOG>(a, pk, kb);
+      for (; kb < kfull; kb += KW) {
+        double a[EPT][KW];
+        chunk_load_full<EPT, LDLOG, KW>(a, pk, kb);
         // the next chunk's lines are pulled into L1 while this one is reduced
         // (prefetch distance 1 measured best: 2..4 thrash L1)
-        if (kb + KC < kfull) chunk_prefetch<EPT, LDLOG>(pk, kb + KC);
-        chunk_process<EPT>(x, a, pv, coef, kb, nk, ndot, mypart, lane, y, coef2, n2);
+        if (kb + KW < kfull) chunk_prefetch<EPT, LDLOG, KW>(pk, kb + KW);
+        chunk_process<EPT, KW>(x, a, pv, coef, kb, nk, ndot, mypart, lane, y, coef2, n2);
       }
       }
     }
 #pragma unroll 1
-    for (; kb < kmax; kb += KC) {                 // ragged tail (predicated loads)
-      double a[EPT][KC];
+    for (; kb < kmax; kb += KW) {                 // ragged tail (predicated loads)
+      double a[EPT][KW];
 #pragma unroll
       for (int q = 0; q < EPT; ++q)
 #pragma unroll
-        for (int j = 0; j < KC; ++j)
+        for (int j = 0; j < KW; ++j)
           a[q][j] = (ok[q] && kb + j < kmax) ? ld_col(pk[q] + (int64_t)(kb + j) * LD) : 0.0;
-      chunk_process<EPT>(x, a, pv, coef, kb, nk, ndot, mypart, lane, y, coef2, n2);
+      chunk_process<EPT, KW>(x, a, pv, coef, kb, nk, ndot, mypart, lane, y, coef2, n2);
     }
     if (n2 > 0) {
 #pragma unroll
@@ -340,7 +348,7 @@ __device__ __noinline__ void sweep(int ldlog, const double* __restrict__ F, int 
   double yd;
 #define HK_SWEEP_CASE(L)                                                                       \
   case L:                                                                                      \
-    sweep_impl<NT, EPT, L, DB>(F, len, nk, ndot, coef, src, sstride, out_col, pend_col, part, pld, \
+    sweep_impl<NT, EPT, L, DB, KC>(F, len, nk, ndot, coef, src, sstride, out_col, pend_col, part, pld, \
                            used, best, sumsq, bestval, xout, nullptr, 0, yd);                  \
     return;
   switch (ldlog) {
@@ -363,7 +371,7 @@ __device__ __noinline__ void sweep_y(int ldlog, const double* __restrict__ F, in
                                      const double* __restrict__ coef2, int n2, double& ydot) {
 #define HK_SWEEP_CASE(L)                                                                       \
   case L:                                                                                      \
-    sweep_impl<NT, EPT, L, DB>(F, len, nk, 0, coef, src, sstride, out_col, pend_col, nullptr, 0, \
+    sweep_impl<NT, EPT, L, DB, KCY>(F, len, nk, 0, coef, src, sstride, out_col, pend_col, nullptr, 0, \
                            used, best, sumsq, bestval, xout, coef2, n2, ydot);                 \
     return;
   switch (ldlog) {
@@ -472,11 +480,11 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
   double* coef = sbase;
   const int pld = cap;
   const bool pin = part_in_smem;
-  double* bv = coef + cap + KC;     // b_k = v_r . v_k of the pending cross (stopping test)
-  double* partU = pin ? bv + cap + KC : t.scratch;
+  double* bv = coef + cap + KPAD;     // b_k = v_r . v_k of the pending cross (stopping test)
+  double* partU = pin ? bv + cap + KPAD : t.scratch;
   double* partV = partU + NW * pld;
   double* prod = partV + NW * pld;
-  unsigned char* used = reinterpret_cast<unsigned char*>(pin ? prod + cap : bv + cap + KC);
+  unsigned char* used = reinterpret_cast<unsigned char*>(pin ? prod + cap : bv + cap + KPAD);
   __shared__ double red_v[NW > 0 ? NW : 1], red_a[NW > 0 ? NW : 1], red_b[NW > 0 ? NW : 1],
       red_x[NW > 0 ? NW : 1];
   __shared__ int64_t red_i[NW > 0 ? NW : 1];
@@ -495,7 +503,7 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
     return;
   }
   for (int i = tid; i < m; i += NT) used[i] = 0;
-  for (int k = tid; k < cap + KC; k += NT) coef[k] = bv[k] = 0.0;
+  for (int k = tid; k < cap + KPAD; k += NT) coef[k] = bv[k] = 0.0;
   __syncthreads();
 
   const double* rowsrc_base = t.A;
@@ -813,14 +821,14 @@ __global__ void __maxnreg__(200) aca_cluster_kernel(const AcaTask* __restrict__ 
   const int nv0 = min(n, (int)q * sln), nlen = min(n, nv0 + sln) - nv0;
   // SMEM: coef[cap+KC], cpU[cap], cpV[cap], bvc[cap+KC], (partU, partV [NW*cap] each), used[m]
   double* coef = reinterpret_cast<double*>(smraw);
-  double* cpU = coef + cap + KC;
+  double* cpU = coef + cap + KPAD;
   double* cpV = cpU + cap;
   double* bvc = cpV + cap;          // b_k = v_r . v_k over the whole cluster (stopping test)
   const int pld = cap;
-  double* partU = part_in_smem ? bvc + cap + KC : t.scratch + (size_t)q * 2 * NW * cap;
+  double* partU = part_in_smem ? bvc + cap + KPAD : t.scratch + (size_t)q * 2 * NW * cap;
   double* partV = partU + NW * pld;
   unsigned char* used =
-      reinterpret_cast<unsigned char*>(part_in_smem ? partV + NW * pld : bvc + cap + KC);
+      reinterpret_cast<unsigned char*>(part_in_smem ? partV + NW * pld : bvc + cap + KPAD);
   __shared__ double red_v[NW], red_a[NW], red_b[NW], red_x[NW];
   __shared__ int64_t red_i[NW];
   __shared__ ClSlot slR, slC;
@@ -840,7 +848,7 @@ __global__ void __maxnreg__(200) aca_cluster_kernel(const AcaTask* __restrict__ 
     return;
   }
   for (int i = tid; i < m; i += NT) used[i] = 0;
-  for (int k = tid; k < cap + KC; k += NT) coef[k] = bvc[k] = 0.0;
+  for (int k = tid; k < cap + KPAD; k += NT) coef[k] = bvc[k] = 0.0;
   cluster_bar();
 
   double* Us = t.U + mu0;
@@ -1075,7 +1083,7 @@ template <int NT, int EPT, int DB>
 static cudaError_t launch_cls(const AcaTask* tasks_dev, int ntasks, int max_cap, int max_m,
                               double tol2, int* counter, cudaStream_t st) {
   const size_t part_bytes = (size_t)(2 * (NT / 32) + 1) * max_cap * 8;
-  const size_t base = (size_t)2 * (max_cap + KC) * 8 + (size_t)max_m + 16;   // coef, bv, used
+  const size_t base = (size_t)2 * (max_cap + KPAD) * 8 + (size_t)max_m + 16;   // coef, bv, used
   const int part_in_smem = (base + part_bytes <= HK_ACA_PART_SMEM) ? 1 : 0;
   const size_t smem = base + (part_in_smem ? part_bytes : 0);
   cudaError_t e = cudaFuncSetAttribute(aca_kernel<NT, EPT, DB>,
@@ -1199,7 +1207,7 @@ cudaError_t hk_launch_aca_cluster(const AcaTask* tasks_dev, int ntasks, int P, i
   if (ntasks == 0) return cudaSuccess;
   auto kern = aca_cluster_kernel<kClNT, kClEPT, HK_ACA_CLDB>;
   constexpr int NW = kClNT / 32;
-  const size_t base = (size_t)2 * (max_cap + KC) * 8 + (size_t)2 * max_cap * 8 + (size_t)max_m + 16;
+  const size_t base = (size_t)2 * (max_cap + KPAD) * 8 + (size_t)2 * max_cap * 8 + (size_t)max_m + 16;
   const size_t part_bytes = (size_t)2 * NW * max_cap * 8;
   const int part_in_smem = (base + part_bytes <= 200 * 1024) ? 1 : 0;
   const size_t smem = base + (part_in_smem ? part_bytes : 0);
