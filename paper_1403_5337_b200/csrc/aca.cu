@@ -681,8 +681,19 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
 // Persistent: CTAs pull tasks from a global counter in list order (largest
 // blocks first), so the long root chains start at t = 0 whatever the hardware
 // dispatch order of CTAs is.
+// HK_ACA_REGCAP: registers of the single-CTA classes capped through the
+// minimum-blocks launch bound, so more pivot chains are co-resident per SM
+// (measured same-run A/B on config 3: 128 -> ACA 3.88 ms, uncapped 160-168
+// registers -> 4.28 ms, 96 -> 4.40 ms; config 4 build 6.5 vs 7.2 ms)
+#ifndef HK_ACA_REGCAP
+#define HK_ACA_REGCAP 128
+#endif
+constexpr int aca_minb(int nt) {
+  return HK_ACA_REGCAP ? (65536 / (nt * HK_ACA_REGCAP) > 0 ? 65536 / (nt * HK_ACA_REGCAP) : 1) : 1;
+}
+
 template <int NT, int EPT, int DB>
-__global__ void __launch_bounds__(NT) aca_kernel(const AcaTask* __restrict__ tasks, int ntasks,
+__global__ void __launch_bounds__(NT, aca_minb(NT)) aca_kernel(const AcaTask* __restrict__ tasks, int ntasks,
                                                  int* __restrict__ counter, double tol2,
                                                  int part_in_smem) {
   __shared__ int s_task;
