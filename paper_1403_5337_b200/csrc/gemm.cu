@@ -195,17 +195,24 @@ __global__ void __launch_bounds__(NT, 2) gemm_kernel(const GemmTask* __restrict_
   }
 }
 
-__global__ void copy_kernel(const CopyTask* __restrict__ tasks) {
+// dst(i, j) = src(i, j).  Column-major destinations (the Z gather of the
+// factorization) walk columns across CTAs and rows across threads, so both
+// sides are coalesced when the source is column-major too; otherwise rows
+// across CTAs and columns across threads.  No per-element index division.
+__global__ void __launch_bounds__(256) copy_kernel(const CopyTask* __restrict__ tasks) {
   const CopyTask t = tasks[blockIdx.y];
-  const int64_t tot = (int64_t)t.rows * t.cols;
-  // rows fastest when the destination is column-major (the Z gather), else columns
-  const bool rows_fast = t.dst_rs == 1;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < tot;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    int i, j;
-    if (rows_fast) { i = (int)(idx % t.rows); j = (int)(idx / t.rows); }
-    else { j = (int)(idx % t.cols); i = (int)(idx / t.cols); }
-    t.dst[i * t.dst_rs + j * t.dst_cs] = t.src[i * t.src_rs + j * t.src_cs];
+  if (t.dst_rs == 1) {
+    for (int j = blockIdx.x; j < t.cols; j += gridDim.x) {
+      const double* s = t.src + (int64_t)j * t.src_cs;
+      double* d = t.dst + (int64_t)j * t.dst_cs;
+      for (int i = threadIdx.x; i < t.rows; i += blockDim.x) d[i] = s[(int64_t)i * t.src_rs];
+    }
+  } else {
+    for (int i = blockIdx.x; i < t.rows; i += gridDim.x) {
+      const double* s = t.src + (int64_t)i * t.src_rs;
+      double* d = t.dst + (int64_t)i * t.dst_rs;
+      for (int j = threadIdx.x; j < t.cols; j += blockDim.x) d[(int64_t)j * t.dst_cs] = s[(int64_t)j * t.src_cs];
+    }
   }
 }
 
@@ -255,7 +262,7 @@ cudaError_t hk_launch_gemm(const GemmTask* tasks_dev, const int32_t* tilemap_dev
 
 cudaError_t hk_launch_copy(const CopyTask* tasks_dev, int ntasks, cudaStream_t st) {
   if (ntasks == 0) return cudaSuccess;
-  copy_kernel<<<dim3(16, ntasks), 256, 0, st>>>(tasks_dev);
+  copy_kernel<<<dim3(8, ntasks), 256, 0, st>>>(tasks_dev);
   hk_count_launch();
   return cudaGetLastError();
 }
