@@ -444,14 +444,20 @@ def run_ours(args):
     # N > 1: HODLR-subtree sharding over NCCL (strong scaling)
     c4 = None
     if not args.no_cfg4:
-        c4 = run_cfg4(dev, rank, world, hbm_peak)
+        try:
+            c4 = run_cfg4(dev, rank, world, hbm_peak)
+        except Exception as exc:                 # a line item must not sink the headline line
+            c4 = {"error": repr(exc)[:400]}
         if c4 and "rooflines" in c4:
             rooflines += c4.pop("rooflines")
 
     # ---- BASELINE configs 1 and 2: one front each, replicas only (rank 0 reports)
     c1 = c2 = None
     if not args.no_cfg12 and rank == 0:
-        c1, c2 = run_cfg12(dev)
+        try:
+            c1, c2 = run_cfg12(dev)
+        except Exception as exc:
+            c1 = c2 = {"error": repr(exc)[:400]}
 
     # per-front ranks of every rank's fronts (the one end-of-run gather)
     all_ranks = MF.gather_front_scalars(batch.ranks.astype(np.int64), device=dev)
