@@ -11,6 +11,8 @@
 #include "hk_common.cuh"
 #include "hk_internal.h"
 
+#include <stdlib.h>
+
 namespace {
 
 constexpr int GJ_NT = 256;
@@ -501,6 +503,193 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_cl_kernel(const GjTask* __restr
     }
 }
 
+// Dataflow variant of the cluster Gauss-Jordan (no cluster barrier inside the
+// elimination): the warp owning column c runs pivot step c on its registers,
+// leaves the pre-step pivot column, pivot row and 1/pivot in its CTA's SMEM
+// slot for that step (slots are never reused: each CTA owns NW*CPW steps),
+// and publishes it with a cluster-scope release store of its CTA's step
+// counter.  Every other warp of every CTA waits for that counter (lane 0
+// polls, then every lane acquires), reads the step through DSMEM and replays
+// it on its own columns.  The critical path per step is one pivot search plus
+// one DSMEM publication instead of a cluster barrier per panel.  Same
+// distribution, pivoting and per-element arithmetic as gj_cl_kernel (bit-
+// identical inverses).
+__device__ __forceinline__ unsigned cl_shared_addr(const void* p, unsigned rank) {
+  unsigned ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+               : "=r"(ra) : "r"((unsigned)__cvta_generic_to_shared(p)), "r"(rank));
+  return ra;
+}
+__device__ __forceinline__ int ld_acquire_cluster(unsigned addr) {
+  int v;
+  asm volatile("ld.acquire.cluster.shared::cluster.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_relaxed_cluster(unsigned addr) {
+  int v;
+  asm volatile("ld.relaxed.cluster.shared::cluster.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cluster(int* p, int v) {
+  asm volatile("st.release.cluster.shared::cta.b32 [%0], %1;"
+               ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+
+template <int NW, int CPW, int RPL>
+__global__ void __launch_bounds__(NW * 32, 1) gj_cldf_kernel(const GjTask* __restrict__ tasks) {
+  constexpr int NT = NW * 32;
+  constexpr int NR = 32 * RPL;
+  constexpr int COLS = NW * CPW;                    // steps owned by one CTA
+  const unsigned P = cl_nrank(), cta = cl_rank();
+  const GjTask t = tasks[blockIdx.x / P];
+  const int N = __shfl_sync(0xffffffffu, t.N, 0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = uniform_warp_id();
+  const int gw = (int)cta * NW + warp;
+  extern __shared__ __align__(16) double ckall[];   // [COLS][NR] pre-step pivot columns
+  __shared__ double rinv_s[COLS];
+  __shared__ int p_s[COLS];
+  __shared__ int s_pub;                             // steps of this CTA published
+  __shared__ int pivrow[NR], invp[NR];
+  double w_[CPW][RPL];
+#pragma unroll
+  for (int jj = 0; jj < CPW; ++jj)
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+      const int i = lane + 32 * q, j = gw * CPW + jj;
+      const bool in = i < N && j < N;
+      const int64_t off = t.mode == 0 ? (int64_t)i * t.src_ld + j : i + (int64_t)j * t.src_ld;
+      w_[jj][q] = in ? t.src[off] : 0.0;
+    }
+  unsigned used = 0;
+  if (tid == 0) s_pub = 0;
+  cluster_bar();                                    // every counter is 0 before anyone polls
+  bool singular = false;
+  for (int c = 0; c < N; ++c) {
+    const unsigned oc = (unsigned)(c / COLS);
+    const int lc = c - (int)oc * COLS;
+    const int ow = lc / CPW, l = lc - ow * CPW;
+    if (cta == oc && warp == ow) {
+      double bv = 0.0, bw = 1.0;
+      int bi = 0x7fffffff;
+      bool have = false;
+      double colv[RPL];
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) {
+        double x = w_[0][q];
+#pragma unroll
+        for (int jj = 1; jj < CPW; ++jj) x = (jj == l) ? w_[jj][q] : x;
+        colv[q] = x;
+        const int i = lane + 32 * q;
+        const double av = fabs(x);
+        if (i < N && !((used >> q) & 1u) && (!have || av > bv)) {
+          bv = av; bw = x; bi = i; have = true;
+        }
+      }
+      const double myrinv = __drcp_rn(bw);
+      const int p = warp_argmax_idx(bv, have, bi);
+      const int lp = p & 31, qp = p >> 5;
+      const double pivabs = __shfl_sync(0xffffffffu, bv, lp);
+      if (!(pivabs >= HK_PIVOT_FLOOR)) {
+        if (lane == 0) {
+          p_s[lc] = -1;
+          st_release_cluster(&s_pub, lc + 1);
+        }
+        singular = true;
+        break;
+      }
+      const double rinv = __shfl_sync(0xffffffffu, myrinv, lp);
+      double* ck_s = ckall + (size_t)lc * NR;
+      bool isp[RPL];
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) {
+        const int i = lane + 32 * q;
+        isp[q] = i == p;
+        if (i < N) ck_s[i] = colv[q];
+      }
+      if (lane == lp) used |= 1u << qp;
+      if (lane == 0) {
+        rinv_s[lc] = rinv;
+        p_s[lc] = p;
+        pivrow[c] = p;
+      }
+      __syncwarp();
+      if (lane == 0) st_release_cluster(&s_pub, lc + 1);
+#pragma unroll
+      for (int jj = 0; jj < CPW; ++jj) {
+        if (jj == l) {
+#pragma unroll
+          for (int q = 0; q < RPL; ++q) w_[jj][q] = isp[q] ? rinv : -colv[q] * rinv;
+        } else {
+          double src = w_[jj][0];
+#pragma unroll
+          for (int q = 1; q < RPL; ++q) src = (qp == q) ? w_[jj][q] : src;
+          const double rj = __shfl_sync(0xffffffffu, src, lp) * rinv;
+#pragma unroll
+          for (int q = 0; q < RPL; ++q) {
+            const double v = fma(-colv[q], rj, w_[jj][q]);
+            w_[jj][q] = isp[q] ? rj : v;
+          }
+        }
+      }
+    } else {
+      const unsigned fa = cl_shared_addr(&s_pub, oc);
+      if (lane == 0)
+        while (ld_relaxed_cluster(fa) <= lc) {
+        }
+      __syncwarp();
+      (void)ld_acquire_cluster(fa);               // every lane orders its own reads
+      const int p = __shfl_sync(0xffffffffu, lane == 0 ? *cl_map(&p_s[lc], oc) : 0, 0);
+      if (p < 0) {
+        singular = true;
+        break;
+      }
+      const double rinv = *cl_map(&rinv_s[lc], oc);
+      if (cta != oc && warp == 0 && lane == 0) pivrow[c] = p;
+      const int qp = p >> 5, lp = p & 31;
+      if (lane == lp) used |= 1u << qp;
+      const double* ckr = cl_map(ckall + (size_t)lc * NR, oc);
+      double ck[RPL];
+      bool isp[RPL];
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) {
+        const int i = lane + 32 * q;
+        ck[q] = (i < N) ? ckr[i] : 0.0;
+        isp[q] = i == p;
+      }
+#pragma unroll
+      for (int jj = 0; jj < CPW; ++jj) {
+        double src = w_[jj][0];
+#pragma unroll
+        for (int q = 1; q < RPL; ++q) src = (qp == q) ? w_[jj][q] : src;
+        const double rj = __shfl_sync(0xffffffffu, src, lp) * rinv;
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+          const double v = fma(-ck[q], rj, w_[jj][q]);
+          w_[jj][q] = isp[q] ? rj : v;
+        }
+      }
+    }
+  }
+  const int sing = __any_sync(0xffffffffu, singular) ? 1 : 0;
+  __shared__ int s_sing;
+  if (tid == 0) s_sing = 0;
+  __syncthreads();
+  if (sing && lane == 0) atomicOr(&s_sing, 1);
+  cluster_bar();                                    // all DSMEM reads done; s_sing complete
+  const int any_sing = s_sing;
+  if (tid == 0 && cta == 0) *t.status = any_sing;
+  if (any_sing) return;
+  for (int k = tid; k < N; k += NT) invp[pivrow[k]] = k;
+  __syncthreads();
+#pragma unroll
+  for (int jj = 0; jj < CPW; ++jj)
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+      const int r = lane + 32 * q, j = gw * CPW + jj;
+      if (r < N && j < N) t.out[invp[r] + (int64_t)pivrow[j] * t.out_ld] = w_[jj][q];
+    }
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT) gj_kernel(const GjTask* __restrict__ tasks, size_t smem_bytes) {
   const GjTask t = tasks[blockIdx.x];
@@ -649,7 +838,28 @@ static cudaError_t launch_gj_cluster(const GjTask* tasks_dev, int ntasks, int ma
   cfg.stream = st;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, gj_cl_kernel<kGjClNW, kGjClCPW, kGjClRPL>, tasks_dev);
+  static int df = -1;
+  if (df < 0) {
+    // opt-in: measured no faster than the panel version on config 4 (the per-
+    // step DSMEM round trips cost what the per-panel barrier did)
+    const char* ev = getenv("HK_GJ_CLUSTER_DF");
+    df = ev ? atoi(ev) : 0;
+  }
+  cudaError_t e;
+  if (df) {
+    auto kern = gj_cldf_kernel<kGjClNW, kGjClCPW, kGjClRPL>;
+    const size_t smem = (size_t)kGjClNW * kGjClCPW * 32 * kGjClRPL * 8;
+    static bool attr = false;
+    if (!attr) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    cfg.dynamicSmemBytes = smem;
+    e = cudaLaunchKernelEx(&cfg, kern, tasks_dev);
+  } else {
+    e = cudaLaunchKernelEx(&cfg, gj_cl_kernel<kGjClNW, kGjClCPW, kGjClRPL>, tasks_dev);
+  }
   hk_count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
