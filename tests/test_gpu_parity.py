@@ -314,6 +314,30 @@ def test_error_contract():
                      hk.CompressionConfig(scheme="aca"))
 
 
+@pytest.mark.parametrize("n,leaf,max_rank", [(1, 1, None), (2, 1, None), (3, 8, None), (17, 4, None),
+                                              (65, 8, 1), (65, 8, 3), (100, 100, None),
+                                              (129, 16, None), (257, 32, 5)])
+def test_edge_shapes_vs_oracle(n, leaf, max_rank):
+    """Ragged trees, a single leaf, n = 1, and rank caps: ranks equal to the oracle's,
+    solves within 1e-10, on a perturbed kernel matrix (test_acceptance.py:66-71 style)."""
+    from paper_1403_5337_b200 import frontgen as fg
+    rng = np.random.default_rng(n * 7 + leaf)
+    A = fg.kernel_matrix(n, "exp-decay", shift=2.0) + 1e-3 * rng.standard_normal((n, n))
+    cfg = hk.CompressionConfig(scheme="aca", tol=1e-8, max_rank=max_rank)
+    fact, report = hk.factorize(hk.BlockAccessor.from_matrix(A), hk.build_tree(n, leaf), cfg)
+    ofact = O.factorize(A, leaf, "aca", 1e-8, 1, max_rank)
+    assert [e["max_rank"] for e in report.ranks_per_level] == \
+        [e["max_rank"] for e in O.ranks_per_level(ofact)]
+    b = rng.standard_normal(n)
+    x = hk.solve(fact, b)
+    xo = O.solve(ofact, b)
+    assert np.linalg.norm(x - xo) <= SOLVE_RTOL * max(np.linalg.norm(xo), 1e-300)
+    B = rng.standard_normal((n, 3))
+    X = hk.solve(fact, B)
+    assert X.shape == (n, 3)
+    assert np.linalg.norm(X - O.solve(ofact, B)) <= SOLVE_RTOL * np.linalg.norm(O.solve(ofact, B))
+
+
 # ------------------------------------------------------------------ BASELINE config 4 (n = 9216)
 # The reference's own numbers on this front, measured in this container by running it
 # (SURVEY.md §6.3): max rank per level 227,227,227,195,193,98,53; GMRES to 1e-10 on
