@@ -15,7 +15,15 @@ namespace {
 // and 2 stages / 4 CTAs per SM spill at the implied register caps (3.9-4.1 ms
 // vs 3.46 ms); a persistent CTA walking its tiles through one cp.async ring
 // was ~20% slower than one tile per CTA with two CTAs per SM.
-constexpr int BM = 64, BN = 64, BK = 16, NT = 256, STAGES = 4;
+#ifndef HK_GEMM_BK
+#define HK_GEMM_BK 16
+#endif
+#ifndef HK_GEMM_STAGES
+#define HK_GEMM_STAGES 4
+#endif
+constexpr int BM = 64, BN = 64, BK = HK_GEMM_BK, NT = 256, STAGES = HK_GEMM_STAGES;
+constexpr int QV = BM * BK / 2 / NT;   // 16-byte pair copies per thread per operand and stage
+constexpr int QS = BM * BK / NT;       // 8-byte copies per thread per operand and stage
 constexpr int SA = BM + 4;   // k-major A rows (transA = 0): conflict-free DMMA fragment loads
 constexpr int ST = BK + 4;   // m/n-major rows (transA = 1 and B)
 
@@ -75,7 +83,7 @@ __device__ __forceinline__ void gemm_tile(const GemmTask& t, int tm, int tn, dou
       // start at even offsets, so a pair straddling the edge copies 8 bytes
       // and zero-fills the rest); half the cp.async instructions
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
+      for (int q = 0; q < QV; ++q) {
         const int idx = tid + NT * q;
         if (!TRANSA) {
           const int i = 2 * (idx % (BM / 2)), l = idx / (BM / 2);
@@ -99,7 +107,7 @@ __device__ __forceinline__ void gemm_tile(const GemmTask& t, int tm, int tn, dou
       return;
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < QS; ++q) {
       const int idx = tid + NT * q;
       if (!TRANSA) {
         const int i = idx % BM, l = idx / BM;
