@@ -821,8 +821,13 @@ static cudaError_t launch_gj_reg(const GjTask* tasks_dev, int ntasks, int maxN, 
   return cudaGetLastError();
 }
 
-// 160 < N <= 256: cluster of P = ceil(N / 32) CTAs (8 warps x 4 columns each)
-constexpr int kGjClNW = 8, kGjClCPW = 4, kGjClRPL = 8, kGjClRows = 32 * kGjClRPL;
+// 160 < N <= 256: cluster of P = ceil(N / 64) CTAs (8 warps x 8 columns each; 4
+// columns per warp measured 20% slower on config 4, 2 columns 2x slower: every
+// panel costs a cluster barrier, and it grows with the cluster size)
+#ifndef HK_GJ_CL_CPW
+#define HK_GJ_CL_CPW 8
+#endif
+constexpr int kGjClNW = 8, kGjClCPW = HK_GJ_CL_CPW, kGjClRPL = 8, kGjClRows = 32 * kGjClRPL;
 static cudaError_t launch_gj_cluster(const GjTask* tasks_dev, int ntasks, int maxN, cudaStream_t st) {
   const int cols = kGjClNW * kGjClCPW;
   const int P = (maxN + cols - 1) / cols;
@@ -846,6 +851,14 @@ static cudaError_t launch_gj_cluster(const GjTask* tasks_dev, int ntasks, int ma
     df = ev ? atoi(ev) : 0;
   }
   cudaError_t e;
+  if (P > 8) {
+    e = cudaFuncSetAttribute(gj_cl_kernel<kGjClNW, kGjClCPW, kGjClRPL>,
+                             cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(gj_cldf_kernel<kGjClNW, kGjClCPW, kGjClRPL>,
+                             cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
   if (df) {
     auto kern = gj_cldf_kernel<kGjClNW, kGjClCPW, kGjClRPL>;
     const size_t smem = (size_t)kGjClNW * kGjClCPW * 32 * kGjClRPL * 8;
