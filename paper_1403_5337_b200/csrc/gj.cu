@@ -803,7 +803,7 @@ __global__ void __launch_bounds__(NT) gj_kernel(const GjTask* __restrict__ tasks
 
 template <int NW, int CPW, int RPL>
 static cudaError_t launch_gj_reg(const GjTask* tasks_dev, int ntasks, int maxN, cudaStream_t st) {
-  if constexpr (CPW * RPL > 32) {   // 512 threads x 128 registers: the dataflow variant would spill
+  if constexpr (CPW * RPL > 32 && NW > 8) {   // 512 threads x 128 registers: the dataflow variant would spill
     gj_blk_kernel<NW, CPW, RPL><<<ntasks, NW * 32, 0, st>>>(tasks_dev);
   } else {
     const size_t smem = (size_t)maxN * 32 * RPL * 8;
@@ -881,7 +881,12 @@ static cudaError_t launch_gj_cluster(const GjTask* tasks_dev, int ntasks, int ma
 cudaError_t hk_launch_gj(const GjTask* tasks_dev, int ntasks, int maxN, cudaStream_t st) {
   if (ntasks == 0) return cudaSuccess;
   if (maxN <= 64) return launch_gj_reg<8, 8, 2>(tasks_dev, ntasks, maxN, st);
-  if (maxN <= 128) return launch_gj_reg<16, 8, 4>(tasks_dev, ntasks, maxN, st);
+// HK_GJ128_NW: warps of the N <= 128 dataflow kernel (8 warps x 16 columns measured
+// slower: factor 3.5 vs 2.95 ms on config 3)
+#ifndef HK_GJ128_NW
+#define HK_GJ128_NW 16
+#endif
+  if (maxN <= 128) return launch_gj_reg<HK_GJ128_NW, 128 / HK_GJ128_NW, 4>(tasks_dev, ntasks, maxN, st);
   if (maxN <= 160) return launch_gj_reg<16, 10, 5>(tasks_dev, ntasks, maxN, st);
   if (maxN <= kGjClRows) return launch_gj_cluster(tasks_dev, ntasks, maxN, st);
   size_t need = gj_bytes(maxN);
