@@ -1203,9 +1203,14 @@ int hk_aca_cluster_size(int m, int n) {
   }
   const int L = m > n ? m : n;
   if (L <= clmin) return 1;
+  static int pmax = -1;
+  if (pmax < 0) {
+    const char* e = getenv("HK_ACA_PMAX");
+    pmax = e ? atoi(e) : 16;
+  }
   const int need = (L + kClNT * kClEPT - 1) / (kClNT * kClEPT);
   int P = 2;
-  while (P < need && P < 16) P <<= 1;
+  while (P < need && P < pmax) P <<= 1;
   return P;
 }
 
