@@ -813,9 +813,13 @@ __device__ __forceinline__ double cl_est_total(const double* slE, unsigned P) {
 
 template <int NT, int EPT, int DB>
 __global__ void __maxnreg__(200) aca_cluster_kernel(const AcaTask* __restrict__ tasks,
-                                                         double tol2, int part_in_smem) {
+                                                         double tol2, int part_in_smem,
+                                                         int* started) {
   constexpr int NW = NT / 32;
   const unsigned P = cl_nrank(), q = cl_rank();
+  // residency signal for the host (mapped pinned memory): the launches that
+  // follow wait until the largest clusters hold their SMs (see hk_build_aca)
+  if (started && q == 0 && threadIdx.x == 0) atomicAdd_system(started, 1);
   const AcaTask& t = tasks[blockIdx.x / P];
   const int m = __shfl_sync(0xffffffffu, t.m, 0), n = __shfl_sync(0xffffffffu, t.n, 0);
   const int cap = __shfl_sync(0xffffffffu, t.cap, 0);
@@ -1170,7 +1174,8 @@ cudaError_t hk_launch_aca(const AcaTask* tasks_dev, int ntasks, int max_cap, int
   // single-block API: the class of the block (max_mn = max(m, n))
   if (ntasks == 0) return cudaSuccess;
   const int P = hk_aca_cluster_size(max_mn, max_mn);
-  if (P > 1) return hk_launch_aca_cluster(tasks_dev, ntasks, P, max_cap, max_m, tol2, st);
+  if (P > 1) return hk_launch_aca_cluster(tasks_dev, ntasks, P, max_cap, max_m, tol2, st, nullptr,
+                                          nullptr);
   int* counter = nullptr;
   cudaError_t e = cudaMallocAsync(&counter, sizeof(int), st);
   if (e != cudaSuccess) return e;
@@ -1219,7 +1224,8 @@ size_t hk_aca_scratch_doubles_cl(int cap, int P) {
 }
 
 cudaError_t hk_launch_aca_cluster(const AcaTask* tasks_dev, int ntasks, int P, int max_cap,
-                                  int max_m, double tol2, cudaStream_t st) {
+                                  int max_m, double tol2, cudaStream_t st, int* started,
+                                  int* max_active) {
   if (ntasks == 0) return cudaSuccess;
   auto kern = aca_cluster_kernel<kClNT, kClEPT, HK_ACA_CLDB>;
   constexpr int NW = kClNT / 32;
@@ -1250,12 +1256,15 @@ cudaError_t hk_launch_aca_cluster(const AcaTask* tasks_dev, int ntasks, int P, i
     cfg.gridDim = dim3((unsigned)(P * ntasks));
     int ncl = 0;
     e = cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg);
-    if (e == cudaSuccess && ncl >= 1) break;
+    if (e == cudaSuccess && ncl >= 1) {
+      if (max_active) *max_active = ncl;
+      break;
+    }
     (void)cudaGetLastError();
     if (P == 1) return e != cudaSuccess ? e : cudaErrorLaunchOutOfResources;
     P >>= 1;
   }
-  e = cudaLaunchKernelEx(&cfg, kern, tasks_dev, tol2, part_in_smem);
+  e = cudaLaunchKernelEx(&cfg, kern, tasks_dev, tol2, part_in_smem, started);
   hk_count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

@@ -323,6 +323,8 @@ struct hk_plan {
   std::vector<cudaEvent_t> fev;     // factor: staging-commit events (front-group streams)
   // BDLR selection cache (graph hash, depth)
   std::vector<AcaPlanCache> aca_plans;   // cached ACA task lists (hk_build_aca)
+  int* started_h = nullptr;         // mapped pinned residency counter of the largest ACA clusters
+  int* started_d = nullptr;
   bool sel_valid = false;
   DevBuf gidx_d, selout_d, seltask_d;   // device graph CSR and GPU selection outputs
   uint64_t sel_key = 0;
@@ -366,6 +368,7 @@ struct hk_plan {
     for (auto& x : fev)
       if (x) cudaEventDestroy(x);
     for (auto& c : aca_plans) c.tasks.release();
+    if (started_h) cudaFreeHost(started_h);
     DevBuf* bufs[] = {&gidx_d, &selout_d, &seltask_d, &aca_cnt, &aca_scr, &At, &UV, &ranks_d, &trace_d, &tasks_d, &sel_d, &work_d, &perm_d,
                       &skel_status_d, &probe_d, &Y, &Ytmp, &F, &I, &ftask_d, &fmap_d, &gj_d, &gj2_d, &gjs_d,
                       &Xin, &X2, &G, &Yv};
@@ -767,6 +770,18 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
   }
   }
   CHK(ensure_side_streams(p));
+  if (ngroups > 0 && !p->started_h) {
+    if (cudaHostAlloc((void**)&p->started_h, 64, cudaHostAllocMapped) == cudaSuccess) {
+      if (cudaHostGetDevicePointer((void**)&p->started_d, p->started_h, 0) != cudaSuccess) {
+        cudaFreeHost(p->started_h);
+        p->started_h = nullptr;
+        p->started_d = nullptr;
+      }
+    } else {
+      p->started_h = nullptr;
+    }
+    (void)cudaGetLastError();
+  }
   CU(p->aca_cnt.ensure(64, st));
   CU(cudaMemsetAsync(p->aca_cnt.p, 0, 64, st));
   CU(cudaEventRecord(p->ev[3], st));
@@ -777,8 +792,26 @@ extern "C" hk_status hk_build_aca(hk_plan* p, const double* A, int64_t ld, int64
   }
   for (int g = 0; g < ngroups; ++g) {   // the long chains launch first
     CU(cudaStreamWaitEvent(p->cl_side[g], p->ev[3], 0));
+    int* started_d = nullptr;
+    if (g == 0 && p->started_h) {
+      *(volatile int*)p->started_h = 0;
+      started_d = p->started_d;
+    }
+    int max_active = 0;
     CU(hk_launch_aca_cluster(tasks_dev + cl_begin[g], cl_cnt[g], cl_P[g], cl_cap[g], cl_m[g],
-                             tol2, p->cl_side[g]));
+                             tol2, p->cl_side[g], started_d, &max_active));
+    if (g == 0 && started_d && (ngroups > 1 || cls_begin[4] > 0)) {
+      // The largest clusters (config 4: two 16-CTA clusters on the root
+      // blocks, the longest chains) need 16 free SMs of one GPC at once; when
+      // the other groups and classes launched beside them got the SMs first,
+      // the root chains started only after ~5.7 ms.  Hold the other launches
+      // until those clusters are resident (bounded wait).
+      const int want = std::min(cl_cnt[0], std::max(max_active, 1));
+      const auto t0 = std::chrono::steady_clock::now();
+      while (*(volatile int*)p->started_h < want &&
+             std::chrono::steady_clock::now() - t0 < std::chrono::milliseconds(20)) {
+      }
+    }
   }
   CU(hk_launch_aca_classes(tasks_dev + ncl_tasks, cls_begin, cls_cap, cls_m, tol2,
                            p->aca_cnt.as<int>(), ss));

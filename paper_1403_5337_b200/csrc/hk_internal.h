@@ -163,7 +163,8 @@ size_t hk_aca_scratch_doubles(int cap);
 int hk_aca_cluster_size(int m, int n);   // 1 = single-CTA size class
 size_t hk_aca_scratch_doubles_cl(int cap, int P);
 cudaError_t hk_launch_aca_cluster(const AcaTask* tasks_dev, int ntasks, int P, int max_cap,
-                                  int max_m, double tol2, cudaStream_t st);
+                                  int max_m, double tol2, cudaStream_t st, int* started,
+                                  int* max_active);
 int hk_aca_class(int m, int n);   // 0..3 -> 512/256/128/64-thread CTAs
 cudaError_t hk_launch_aca_classes(const AcaTask* tasks_dev, const int* class_begin,
                                   const int* class_max_cap, const int* class_max_m, double tol2,
