@@ -688,8 +688,12 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
 #ifndef HK_ACA_REGCAP
 #define HK_ACA_REGCAP 128
 #endif
+#ifndef HK_ACA_REGCAP_BIG
+#define HK_ACA_REGCAP_BIG HK_ACA_REGCAP   // classes 0 and 1 (NT >= 128)
+#endif
+constexpr int aca_cap(int nt) { return nt >= 128 ? HK_ACA_REGCAP_BIG : HK_ACA_REGCAP; }
 constexpr int aca_minb(int nt) {
-  return HK_ACA_REGCAP ? (65536 / (nt * HK_ACA_REGCAP) > 0 ? 65536 / (nt * HK_ACA_REGCAP) : 1) : 1;
+  return aca_cap(nt) ? (65536 / (nt * aca_cap(nt)) > 0 ? 65536 / (nt * aca_cap(nt)) : 1) : 1;
 }
 
 template <int NT, int EPT, int DB>
