@@ -104,8 +104,7 @@ __device__ __forceinline__ void gemm_tile(const GemmTask& t, int tm, int tn, dou
         const double* srcb = nbb ? Bg + (k0 + l) + (int64_t)(n0 + j) * t.ldb : Bg;
         cp_async16(bs + j * ST + l, srcb, nbb);
       }
-      return;
-    }
+    } else {
 #pragma unroll
     for (int q = 0; q < QS; ++q) {
       const int idx = tid + NT * q;
@@ -124,6 +123,7 @@ __device__ __forceinline__ void gemm_tile(const GemmTask& t, int tm, int tn, dou
       const bool okb = (n0 + j < N) && (k0 + l < K);
       const double* srcb = okb ? Bg + (k0 + l) + (int64_t)(n0 + j) * t.ldb : Bg;
       cp_async8(bs + j * ST + l, srcb, okb ? 8 : 0);
+    }
     }
   };
 

@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(NT) skeleton_kernel(const SkelTask* __restrict
   __shared__ int s_rank;
   extern __shared__ double wsm[];
   double* piv = pivbuf + (int64_t)blockIdx.x * pivstride;
-  const int k = t.k, kc = t.kc, m = t.m, n = t.n;
+  const int k = t.k, kc = t.kc, n = t.n;
   // working matrix: its first ksm rows in SMEM (all of it when it fits), the
   // rest in t.work; SMEM rows are written back to t.work after the LU
   const int ksm = kc > 0 ? (int)min((size_t)k, smem_bytes / ((size_t)kc * 8)) : k;
