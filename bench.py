@@ -384,6 +384,23 @@ def run_ours(args):
                   "algorithmic_flops_per_launch": ff, "launch_ms": fac_avg * 1e3,
                   "peak_source": fpk_src}]
 
+    # the batch HODLR solve (s = 1, all fronts) alone: stored-factor bytes / time
+    sv0 = torch.cuda.Event(enable_timing=True)
+    sv1 = torch.cuda.Event(enable_timing=True)
+    batch.solve_(work)
+    torch.cuda.synchronize()
+    sv0.record(stream)
+    for _ in range(10):
+        batch.solve_(work)
+    sv1.record(stream)
+    torch.cuda.synchronize()
+    sv_ms = sv0.elapsed_time(sv1) / 10
+    sb = solve_bytes(batch.tree, ranks)
+    rooflines.append({"kernel": "HODLR solve sweep, cfg3 64 fronts, 1 rhs each", "bound": "hbm",
+                      "achieved": sb / (sv_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                      "frac": sb / (sv_ms * 1e-3) / 1e9 / hbm_peak,
+                      "algorithmic_bytes_per_launch": sb, "launch_ms": sv_ms})
+
     # ---- GMRES time-to-1e-10 on front 0 (HODLR preconditioner)
     gm = {}
     if rank == 0:
