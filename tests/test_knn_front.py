@@ -121,3 +121,43 @@ def test_cfg2_reduced_parity(cfg2_small, scheme, depth):
     ores = O.gmres(lambda v: A @ v, b0, 1e-10, 1000, lambda r: O.solve(ofact, r))
     assert res.converged and abs(res.iterations - ores["iterations"]) <= 1
     assert np.linalg.norm(res.x - ores["x"]) <= 1e-10 * np.linalg.norm(ores["x"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("npts,h,leaf,depth", [(3000, 0.05, 16, 0), (3000, 0.05, 16, 2),
+                                               (6000, 0.02, 32, 1), (1500, 0.1, 8, 4)])
+def test_bdlr_small_knn_fronts_edge_depths(npts, h, leaf, depth):
+    """BDLR on small unstructured fronts with shallow/deep selections and small
+    leaves: GPU skeletons (GPU BFS selection + complete-pivot LU) identical to
+    the oracle's, ranks equal, solves within 1e-10."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_1403_5337_b200.hodlr import factorize_traced
+    kf = fg.knn_front(npts, h=h, leaf=leaf)
+    A, graph = kf.front, kf.graph
+    n = A.shape[0]
+    cfg = hk.CompressionConfig(scheme="bdlr", tol=1e-4, depth=depth)
+    try:
+        ofact = O.factorize(A, leaf, "bdlr", 1e-4, depth, None, (graph.indptr, graph.indices))
+    except Exception as exc:                       # the reference raises -> so must we
+        with pytest.raises(type(exc)):
+            factorize_traced(hk.BlockAccessor.from_matrix(A, pattern=graph), hk.build_tree(n, leaf), cfg)
+        return
+    fact, report, recs = factorize_traced(hk.BlockAccessor.from_matrix(A, pattern=graph),
+                                          hk.build_tree(n, leaf), cfg)
+    for k, sl in enumerate(_internal(ofact.nodes)):
+        for side in (0, 1):
+            rows, cols = recs[2 * k + side]
+            info = ofact.skeletons[sl][side]
+            if info is None:
+                assert rows.size == 0
+                continue
+            assert np.array_equal(rows, info["rows"]) and np.array_equal(cols, info["cols"])
+    assert [e["max_rank"] for e in report.ranks_per_level] == \
+        [e["max_rank"] for e in O.ranks_per_level(ofact)]
+    b0 = np.random.default_rng(5).standard_normal(n)
+    x = hk.solve(fact, b0)
+    xo = O.solve(ofact, b0)
+    assert np.linalg.norm(x - xo) <= 1e-10 * np.linalg.norm(xo)
+
