@@ -346,6 +346,7 @@ def run_ours(args):
     barrier()
     clk = clocks.stop()
     launches = N.launch_count() - launches0
+    x_ref = work.clone()          # S(rhs) of the last timed step: the e2e path's expected output
     ms_max = MF.max_over_ranks(e0.elapsed_time(e1), device=dev)
     value = world * F * args.steps / (ms_max * 1e-3)
 
@@ -437,12 +438,16 @@ def run_ours(args):
         e1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = MF.max_over_ranks(e0.elapsed_time(e1), device=dev)
-        x_check = float((outs[(args.steps - 1) % 2] - work.cpu()).abs().max())
+        xr = x_ref.cpu()
+        x_out = outs[(args.steps - 1) % 2]
+        x_check = float((x_out - xr).abs().max())
+        x_rel = float((x_out - xr).norm() / xr.norm())
         e2e = {"value": world * F * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(host_fronts.numel() * 8 + host_rhs.numel() * 8),
                "d2h_bytes_per_step": int(host_rhs.numel() * 8),
                "ms_per_step": e2e_ms / args.steps,
                "max_abs_diff_vs_device_path": x_check,
+               "rel_diff_vs_device_path": x_rel,
                "path": "HodlrBatch.run_host_stream (public API): pinned host fronts/rhs -> "
                        "build+factor+solve -> host solution, copies overlapped with compute"}
 

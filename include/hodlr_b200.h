@@ -175,24 +175,32 @@ hk_status hk_solve_front(hk_plan* plan, int64_t front, double* rhs_dev, int64_t 
 /* ------------------------------------------------------------------------
  * GMRES (krylov.py:69-166): left preconditioned, no restart, MGS with one
  * conditional re-orthogonalisation, Givens, true-residual guard.
- * Operator: the dense row-major front A_dev (cli.py:320-321 `dense @ v`).
- * precond: 0 = none, 1 = the plan's HODLR solve for `front`, 2 = diagonal
- * scaling (krylov.py:44-66).  history_host holds max_iter doubles.
- * flags_host[0] = converged, [1] = breakdown.
+ * Operator: the dense row-major front A_dev, n x n with leading dimension
+ * lda (cli.py:320-321 `dense @ v`).  precond: 0 = none, 1 = the plan's HODLR
+ * solve for `front`, 2 = division by diag_dev (n entries, zeros already
+ * replaced by 1: DiagonalPreconditioner, krylov.py:44-62).  n must equal the
+ * plan's order (HK_ERR_DIMENSION otherwise: the reference's solve() raises
+ * DimensionMismatchError, hodlr.py:291-293).
+ * The whole iteration runs on the device: one CUDA graph whose conditional
+ * WHILE node repeats GEMV -> preconditioner -> Arnoldi until every system has
+ * converged; the host synchronises once, after the loop.
  * ---------------------------------------------------------------------- */
 /* s (1..16) right-hand sides, s independent GMRES runs in lock step: one
  * s-column GEMV and one s-column HODLR solve per iteration, batched Arnoldi.
- * Per-system results equal s separate hk_gmres calls.  B, X: n x s (ld n);
- * iterations[s], history[s * max_iter] (row c = rhs c), true_residual[s],
- * flags[2s] (converged, breakdown per rhs).  SURVEY.md §8(f)#3. */
-hk_status hk_gmres_batch(hk_plan* plan, int64_t front, const double* A_dev, int64_t lda,
+ * Per-system results equal s separate hk_gmres calls.  B, X: n x s (ld n),
+ * device; iterations[s], history[s * max_iter] (row c = rhs c),
+ * true_residual[s], flags[2s] (converged, breakdown per rhs), all host.
+ * SURVEY.md §8(f)#3. */
+hk_status hk_gmres_batch(hk_plan* plan, int64_t front, const double* A_dev, int64_t lda, int64_t n,
                          const double* B_dev, int64_t s, double tol, int64_t max_iter,
-                         int precond, double* X_dev, int64_t* iterations, double* history,
-                         double* true_residual, int32_t* flags, void* stream);
-hk_status hk_gmres(hk_plan* plan, int64_t front, const double* A_dev, int64_t lda,
+                         int precond, const double* diag_dev, double* X_dev, int64_t* iterations,
+                         double* history, double* true_residual, int32_t* flags, void* stream);
+/* One right-hand side: history_host holds max_iter doubles, flags_host[0] =
+ * converged, [1] = breakdown. */
+hk_status hk_gmres(hk_plan* plan, int64_t front, const double* A_dev, int64_t lda, int64_t n,
                    const double* b_dev, double tol, int64_t max_iter, int precond,
-                   double* x_dev, int64_t* iterations, double* history_host,
-                   double* true_residual, int32_t* flags_host, void* stream);
+                   const double* diag_dev, double* x_dev, int64_t* iterations,
+                   double* history_host, double* true_residual, int32_t* flags_host, void* stream);
 
 /* Building blocks for GMRES with arbitrary operator callables. */
 /* One Arnoldi/MGS/Givens column update for column j (krylov.py:110-145):

@@ -273,10 +273,6 @@ struct SolveProg {
   const int32_t* leaf_map = nullptr;
   int leaf_tiles = 0;
   DevBuf pbuf;          // partial dot products of one level (levels reuse it in stream order)
-  // fused persistent sweep: phase table, grid-barrier word, launch bounds
-  const SolvePhase* phases = nullptr;
-  int nphase = 0, max_items = 0, max_k = 0;
-  DevBuf barbuf;
   // the kernel sequence is captured into a CUDA graph at its second use (a
   // GMRES run applies the same program every iteration); one graph launch
   // then replaces 3 launches per level
@@ -289,16 +285,15 @@ struct SolveProg {
     if (pbuf.p) cudaFreeAsync(pbuf.p, st);
     pbuf.p = nullptr;
     pbuf.bytes = 0;
-    if (barbuf.p) cudaFreeAsync(barbuf.p, st);
-    barbuf.p = nullptr;
-    barbuf.bytes = 0;
   }
   ~SolveProg() {
     pbuf.release();
-    barbuf.release();
     if (gexec) cudaGraphExecDestroy(gexec);
   }
 };
+
+struct GmresGraph;
+static void destroy_gmres_graph(GmresGraph* g);
 
 struct hk_plan {
   int64_t n = 0, leaf = 0, batch = 0;
@@ -349,6 +344,7 @@ struct hk_plan {
   Staging pstage;                   // task arrays of the cached solve programs
   int64_t g_per_col = 0;            // doubles of G/Yv scratch per rhs column (all fronts)
   std::map<std::pair<int, int>, SolveProg*> progs;
+  std::vector<GmresGraph*> gmres_graphs;   // cached device-resident GMRES loops (hk_gmres_batch)
   DevBuf Xin, X2, G, Yv;
   // timings
   double t_lowrank = 0, t_leaf = 0, t_schur = 0, t_aca = 0;
@@ -356,6 +352,7 @@ struct hk_plan {
 
   int nblocks() const { return (int)blocks.size(); }
   ~hk_plan() {
+    for (GmresGraph* g : gmres_graphs) destroy_gmres_graph(g);
     for (auto& kv : progs) delete kv.second;
     for (auto& x : side)
       if (x) cudaStreamDestroy(x);
@@ -524,6 +521,9 @@ extern "C" hk_status hk_block_shape(const hk_plan* p, int64_t block, int64_t* m,
 
 // callers synchronise the stream first: the programs' task arrays are reused
 static void drop_progs(hk_plan* p, cudaStream_t st) {
+  // the cached GMRES graphs replay the programs' kernels: drop them too
+  for (GmresGraph* g : p->gmres_graphs) destroy_gmres_graph(g);
+  p->gmres_graphs.clear();
   for (auto& kv : p->progs) {
     kv.second->free_async(st);
     delete kv.second;
@@ -1300,6 +1300,8 @@ static hk_status flush(hk_plan* p, std::vector<Op>& ops, cudaStream_t st) {
   return launch_ops(p, ops, st);
 }
 
+static hk_status lu_on_demand(const LuTask& proto, int N, double* lu_host, int32_t* piv_host,
+                              int* singular);
 struct SolveProg;
 static hk_status build_solve_prog(hk_plan* p, int front, int s, SolveProg*& out, cudaStream_t st);
 static hk_status ensure_solve_scratch(hk_plan* p, int s, cudaStream_t st);
@@ -1370,8 +1372,9 @@ extern "C" hk_status hk_factor_ext(hk_plan* p, const double* Zext, int64_t ldz, 
   CU(p->Y.ensure((size_t)ytot * 8 + 8, st));
   CU(p->Ytmp.ensure((size_t)ytot * 8 + 8, st));
   CU(p->F.ensure((size_t)ftot * 8 + 8, st));
-  CU(p->I.ensure((size_t)itot * 4 + 4, st));
-  CU(cudaMemsetAsync(p->I.p, 0, (size_t)itot * 4 + 4, st));
+  // statuses [0, itot) and near-singular flags of the coupling systems [itot, 2 itot)
+  CU(p->I.ensure((size_t)2 * itot * 4 + 4, st));
+  CU(cudaMemsetAsync(p->I.p, 0, (size_t)2 * itot * 4 + 4, st));
   // large Gauss-Jordan scratch: the largest single stage (stages run in order)
   {
     size_t need = 0, leaf_need = 0;
@@ -1560,6 +1563,7 @@ extern "C" hk_status hk_factor_ext(hk_plan* p, const double* Zext, int64_t ldz, 
         g.src_ld = 0;
         g.out_ld = R;
         g.status = I + r.status;
+        g.near = I + itot + r.status;
         g.mode = 1;
         if (ru <= rl) {
           // M = I_u - Y X ; S^{-1} = [[I - X (-M^{-1} Y), -X M^{-1}], [-M^{-1} Y, M^{-1}]]
@@ -1614,9 +1618,33 @@ extern "C" hk_status hk_factor_ext(hk_plan* p, const double* Zext, int64_t ldz, 
     hc.mark("solve program");
   }
   // ---- statuses: first failure in the reference's DFS event order
-  std::vector<int32_t> ih((size_t)itot);
-  if (itot) CU(cudaMemcpyAsync(ih.data(), I, (size_t)itot * 4, cudaMemcpyDeviceToHost, st));
+  std::vector<int32_t> ih((size_t)2 * itot);
+  if (itot) CU(cudaMemcpyAsync(ih.data(), I, (size_t)2 * itot * 4, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
+  // A coupling system whose capacitance matrix M had a pivot below
+  // HK_NEAR_PIVOT (or none above 1e-300) is re-decided the reference's way:
+  // partial-pivot LU of S itself, singular iff min |U_kk| < 1e-300
+  // (hodlr.py:272-277, dense.py:76-77).  det S = det M, but the pivots of the
+  // two eliminations differ, so only this keeps the raise/no-raise decision
+  // identical near singularity.  Never triggered on well-conditioned fronts.
+  for (int64_t f = 0; f < p->batch; ++f)
+    for (int s : p->internal) {
+      const NodeRec& r = p->rec[f * nn + s];
+      if (r.status < 0 || r.R == 0) continue;
+      if (ih[r.status] == 0 && ih[itot + r.status] == 0) continue;
+      LuTask t{};
+      t.src = F + r.h;
+      t.src_ld = r.R;
+      t.mode = 1;
+      t.rl = r.rl;
+      t.ru = r.ru;
+      t.h_col0 = r.w;
+      int sing = 0;
+      CHK(lu_on_demand(t, r.R, nullptr, nullptr, &sing));
+      // an exactly singular M cannot be inverted: it stays singular even if
+      // S's rounding gave pivots above the floor (measure-zero case)
+      ih[r.status] = (sing || ih[r.status]) ? 1 : 0;
+    }
   hc.mark("wait");
   if (host_profile()) g_opprof.print("factor");
   float ms1 = 0, ms2 = 0;
@@ -1719,7 +1747,9 @@ static void colmajor_to_rowmajor(const std::vector<double>& cm, int64_t rows, in
 
 // On-demand partial-pivot LU (inspection of leaf_lus / couplings[].schur_lu;
 // the hot path keeps explicit inverses instead).
-static hk_status lu_on_demand(const LuTask& proto, int N, double* lu_host, int32_t* piv_host) {
+static hk_status lu_on_demand(const LuTask& proto, int N, double* lu_host, int32_t* piv_host,
+                              int* singular) {
+  if (singular) *singular = 0;
   if (N == 0) return HK_OK;
   double* lu = nullptr;
   int32_t *ip = nullptr, *pm = nullptr, *stt = nullptr;
@@ -1733,11 +1763,16 @@ static hk_status lu_on_demand(const LuTask& proto, int N, double* lu_host, int32
   t.lu = lu; t.ipiv = ip; t.perm = pm; t.status = stt; t.inv = nullptr; t.N = N;
   CU(cudaMemcpy(td, &t, sizeof(LuTask), cudaMemcpyHostToDevice));
   CU(hk_launch_lu(td, 1, N, 0));
-  std::vector<double> h((size_t)N * N);
-  CU(cudaMemcpy(h.data(), lu, h.size() * 8, cudaMemcpyDeviceToHost));
-  CU(cudaMemcpy(piv_host, ip, (size_t)N * 4, cudaMemcpyDeviceToHost));
-  for (int i = 0; i < N; ++i)
-    for (int j = 0; j < N; ++j) lu_host[(int64_t)i * N + j] = h[i + (int64_t)j * N];
+  if (lu_host) {
+    std::vector<double> h((size_t)N * N);
+    CU(cudaMemcpy(h.data(), lu, h.size() * 8, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j < N; ++j) lu_host[(int64_t)i * N + j] = h[i + (int64_t)j * N];
+  }
+  if (piv_host) CU(cudaMemcpy(piv_host, ip, (size_t)N * 4, cudaMemcpyDeviceToHost));
+  int32_t sg = 0;
+  CU(cudaMemcpy(&sg, stt, 4, cudaMemcpyDeviceToHost));
+  if (singular) *singular = sg != 0;
   cudaFree(lu); cudaFree(ip); cudaFree(pm); cudaFree(stt); cudaFree(td);
   return HK_OK;
 }
@@ -1750,7 +1785,7 @@ extern "C" hk_status hk_get_leaf_lu(hk_plan* p, int64_t f, int64_t slot, double*
   t.src = p->A + f * p->fstride + nd.lo * p->lda + nd.lo;
   t.src_ld = p->lda;
   t.mode = 0;
-  return lu_on_demand(t, (int)(nd.hi - nd.lo), lu, perm);
+  return lu_on_demand(t, (int)(nd.hi - nd.lo), lu, perm, nullptr);
 }
 
 extern "C" hk_status hk_get_coupling(hk_plan* p, int64_t f, int64_t slot, double* dl, double* dr,
@@ -1783,7 +1818,7 @@ extern "C" hk_status hk_get_coupling(hk_plan* p, int64_t f, int64_t slot, double
     t.rl = r.rl;
     t.ru = r.ru;
     t.h_col0 = r.w;
-    CHK(lu_on_demand(t, r.R, slu, sperm));
+    CHK(lu_on_demand(t, r.R, slu, sperm, nullptr));
   }
   return HK_OK;
 }
@@ -1978,28 +2013,6 @@ static hk_status build_solve_prog(hk_plan* p, int front, int s, SolveProg*& out,
     sp->levels.push_back(std::move(L));
   }
   (void)nb;
-  if (sp->small) {   // phase table of the fused persistent sweep (solve.cu)
-    std::vector<SolvePhase> ph;
-    auto add = [&](int kind, const void* t, const int32_t* it, int ni, int mk) {
-      if (ni <= 0) return;
-      ph.push_back(SolvePhase{kind, ni, t, it});
-      sp->max_items = std::max(sp->max_items, ni);
-      sp->max_k = std::max(sp->max_k, mk);
-    };
-    add(1, sp->leaf.t, sp->leaf.items, sp->leaf.nitems, sp->leaf.max_k);
-    for (auto& L : sp->levels) {
-      add(0, L.pdot_t, L.pdot_items, L.n_pdot, 0);
-      add(1, L.sinv.t, L.sinv.items, L.sinv.nitems, L.sinv.max_k);
-      add(1, L.upd.t, L.upd.items, L.upd.nitems, L.upd.max_k);
-    }
-    sp->nphase = (int)ph.size();
-    if (sp->nphase) {
-      sp->phases = p->pstage.push(ph, st);
-      if (!sp->phases) { delete sp; return fail(HK_ERR_CUDA, "pinned staging allocation failed"); }
-      CU(sp->barbuf.ensure(64, st));
-      CU(cudaMemsetAsync(sp->barbuf.p, 0, 64, st));
-    }
-  }
   CU(p->pstage.commit(st));
   p->progs[key] = sp;
   out = sp;
@@ -2023,25 +2036,7 @@ static hk_status ensure_solve_scratch(hk_plan* p, int s, cudaStream_t st) {
 
 // The solve program's kernel sequence: leaf solve, then per level (deepest
 // first) V^T x partial dots -> S^{-1} g -> x -= d y  (hodlr.py:298-306).
-static bool solve_fused() {
-  static int on = -1;
-  if (on < 0) {
-    // opt-in: measured slower than the graph-replayed split launches (the
-    // phases are item-latency bound; a grid barrier costs what a graph
-    // kernel boundary does)
-    const char* e = getenv("HK_SOLVE_FUSED");
-    on = e ? atoi(e) : 0;
-  }
-  return on != 0;
-}
-
 static hk_status launch_solve_kernels(SolveProg* sp, int s, cudaStream_t st, bool prof) {
-  if (sp->small && sp->nphase && solve_fused()) {
-    CU(hk_launch_solve_sweep(sp->phases, sp->nphase, sp->max_items, s, sp->max_k,
-                             sp->barbuf.as<unsigned>(), st));
-    if (prof) g_opprof.mark("fused sweep (" + std::to_string(sp->nphase) + " phases)", st);
-    return HK_OK;
-  }
   if (sp->small) {
     CU(hk_launch_sgemv(sp->leaf.t, sp->leaf.items, sp->leaf.nitems, s, sp->leaf.max_k, st));
     if (prof) g_opprof.mark("leaf sgemv", st);
@@ -2147,290 +2142,355 @@ extern "C" hk_status hk_solve_front(hk_plan* p, int64_t front, double* rhs, int6
 }
 
 // ------------------------------------------------------------------ GMRES
-struct GmresScratch {
-  DevBuf basis, hess, cs, sn, g, w, y, scal, out;
+// Device-resident GMRES (krylov.py:69-166) for s <= 16 right-hand sides of one
+// front, advanced in lock step.  One CUDA graph per (front, s, operator,
+// preconditioner, tol, max_iter):
+//
+//   pre   ||b_c||, r0 = M^{-1} b, beta_c = ||r0_c||, Q_c[:,0] = r0_c / beta_c
+//   WHILE (any system active and k < min(max_iter, n))        krylov.py:107
+//         W = A V (one s-column GEMV, the front streamed once)   :110
+//         W = M^{-1} W (the s-column HODLR sweep, factor streamed once)
+//         Arnoldi/MGS/Givens per system; the last CTA updates the flags,
+//         the history and the loop condition (cudaGraphSetConditional)  :111-145
+//   post  x_c = Q_c y_c, true residuals                          :147-156
+//
+// The host launches the graph and reads the state once, after the loop:
+// no per-iteration round trip.  Per system the arithmetic is that of a
+// single-rhs run (the GEMV and the sweep treat columns independently), so
+// iterates, counts and flags do not depend on s.  The Krylov basis starts
+// with room for min(mmax, 64) vectors; when a system needs more, the loop
+// stops at the capacity, the host grows the buffers (copying the basis,
+// Hessenberg and rotations) and relaunches the loop alone.
+struct GmresGraph {
+  int64_t front = 0;
+  int s = 0, precond = 0;
+  const double* A = nullptr;
+  int64_t lda = 0;
+  const double* diag = nullptr;
+  double tol = 0;
+  int64_t max_iter = 0, mmax = 0, cap = 0;
+  DevBuf basis, hess, cs, sn, g, V, W, B, X, hist, y, state;
+  cudaGraphExec_t main = nullptr, resume = nullptr;
+  long long k_pre = 0, k_body = 0, k_post = 0;   // kernels per part (launch counter)
 };
 
-static hk_status read_scalar(const double* d, double* h, cudaStream_t st) {
-  CU(cudaMemcpyAsync(h, d, 8, cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
-  return HK_OK;
+static void destroy_gmres_graph(GmresGraph* g) {
+  if (!g) return;
+  if (g->main) cudaGraphExecDestroy(g->main);
+  if (g->resume) cudaGraphExecDestroy(g->resume);
+  DevBuf* all[] = {&g->basis, &g->hess, &g->cs, &g->sn, &g->g, &g->V, &g->W, &g->B, &g->X,
+                   &g->hist, &g->y, &g->state};
+  for (DevBuf* d : all) d->release();
+  delete g;
 }
 
-static hk_status apply_precond(hk_plan* p, int64_t front, int precond, const double* A,
-                               int64_t lda, double* v, int64_t n, cudaStream_t st) {
-  if (precond == 1) return hk_solve_front(p, front, v, n, 1, st);
-  if (precond == 2) {
-    CU(hk_launch_diag_scale(A, lda, v, v, n, st));
+static GmParams gm_params(const hk_plan* p, const GmresGraph* g) {
+  GmParams P{};
+  P.n = p->n;
+  P.cap = g->cap;
+  P.mmax = g->mmax;
+  P.max_iter = g->max_iter;
+  P.s = g->s;
+  P.tol = g->tol;
+  P.vs = g->cap + 1;
+  P.bstride = p->n * (g->cap + 1);
+  P.hstride = (g->cap + 1) * g->cap;
+  P.basis = g->basis.as<double>();
+  P.hess = g->hess.as<double>();
+  P.cs = g->cs.as<double>();
+  P.sn = g->sn.as<double>();
+  P.g = g->g.as<double>();
+  P.V = g->V.as<double>();
+  P.hist = g->hist.as<double>();
+  P.y = g->y.as<double>();
+  P.st = g->state.as<GmState>();
+  return P;
+}
+
+// Krylov buffers for capacity `cap` (fresh allocations; the caller copies).
+static cudaError_t gm_alloc_krylov(const hk_plan* p, GmresGraph* g, int64_t cap, DevBuf* basis,
+                                   DevBuf* hess, DevBuf* cs, DevBuf* sn, DevBuf* gv, DevBuf* y,
+                                   cudaStream_t st) {
+  const size_t s = (size_t)g->s, vs = (size_t)cap + 1;
+  cudaError_t e;
+  if ((e = basis->ensure(s * p->n * vs * 8, st)) != cudaSuccess) return e;
+  if ((e = hess->ensure(s * vs * cap * 8, st)) != cudaSuccess) return e;
+  if ((e = cs->ensure(s * vs * 8, st)) != cudaSuccess) return e;
+  if ((e = sn->ensure(s * vs * 8, st)) != cudaSuccess) return e;
+  if ((e = gv->ensure(s * vs * 8, st)) != cudaSuccess) return e;
+  return y->ensure(s * vs * 8, st);
+}
+
+// body of the WHILE loop: W = M^{-1} A V, then the Arnoldi step of every system
+static hk_status gm_body_ops(hk_plan* p, GmresGraph* g, SolveProg* sp, const GmParams& P,
+                             cudaGraphConditionalHandle h, cudaStream_t cs) {
+  const int64_t n = p->n;
+  double* W = g->W.as<double>();
+  if (g->precond == 1) {
+    double* xin = p->Xin.as<double>() + g->front * n * g->s;
+    CU(hk_launch_gemv_rowmajor(g->A, g->lda, n, n, P.V, n, g->s, xin, n, cs));
+    CHK(launch_solve_kernels(sp, g->s, cs, false));
+    W = p->X2.as<double>() + g->front * n * g->s;
+  } else {
+    CU(hk_launch_gemv_rowmajor(g->A, g->lda, n, n, P.V, n, g->s, W, n, cs));
+    if (g->precond == 2) CU(hk_launch_vdiv(W, g->diag, W, n, g->s, cs));
   }
+  CU(hk_launch_gm_arnoldi(P, W, h, cs));
   return HK_OK;
 }
 
-extern "C" hk_status hk_gmres(hk_plan* p, int64_t front, const double* A, int64_t lda,
-                              const double* b, double tol, int64_t max_iter, int precond,
-                              double* x, int64_t* iterations, double* history,
-                              double* true_residual, int32_t* flags, void* stream) {
+// Capture one executable graph: [pre] -> WHILE(body) -> post.  The resume
+// variant (with_pre = false) starts the loop with the condition set.
+static hk_status gm_capture(hk_plan* p, GmresGraph* g, SolveProg* sp, bool with_pre,
+                            cudaGraphExec_t* out) {
+  CHK(ensure_side_streams(p));
+  cudaStream_t cs = p->side[0], bs = p->side[1];
+  const int64_t n = p->n;
+  const int s = g->s;
+  const GmParams P = gm_params(p, g);
+  GmState* stt = g->state.as<GmState>();
+  const long long c0 = hk_launch_count();
+  long long c_pre = 0, c_body = 0;
+  CU(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+  auto record = [&]() -> hk_status {
+    cudaStreamCaptureStatus cst;
+    cudaGraph_t cg = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CU(cudaStreamGetCaptureInfo(cs, &cst, nullptr, &cg, &deps, &nd));
+    cudaGraphConditionalHandle h;
+    CU(cudaGraphConditionalHandleCreate(&h, cg, with_pre ? 0u : 1u, cudaGraphCondAssignDefault));
+    if (with_pre) {
+      CU(cudaMemsetAsync(stt, 0, sizeof(GmState), cs));
+      CU(cudaMemsetAsync(P.hess, 0, (size_t)s * P.hstride * 8, cs));
+      CU(cudaMemsetAsync(P.g, 0, (size_t)s * P.vs * 8, cs));
+      const double* B = g->B.as<double>();
+      CU(hk_launch_norms(B, n, n, s, stt->nb, cs));
+      const double* R0 = B;
+      if (g->precond == 1) {
+        double* xin = p->Xin.as<double>() + g->front * n * s;
+        CU(cudaMemcpyAsync(xin, B, (size_t)n * s * 8, cudaMemcpyDeviceToDevice, cs));
+        CHK(launch_solve_kernels(sp, s, cs, false));
+        R0 = p->X2.as<double>() + g->front * n * s;
+      } else if (g->precond == 2) {
+        CU(hk_launch_vdiv(B, g->diag, g->W.as<double>(), n, s, cs));
+        R0 = g->W.as<double>();
+      }
+      CU(hk_launch_norms(R0, n, n, s, stt->beta, cs));
+      CU(hk_launch_gm_start(P, R0, h, cs));
+      c_pre = hk_launch_count() - c0;
+    }
+    CU(cudaStreamGetCaptureInfo(cs, &cst, nullptr, &cg, &deps, &nd));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    CU(cudaGraphAddNode(&cnode, cg, deps, nd, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CU(cudaStreamUpdateCaptureDependencies(cs, &cnode, 1, cudaStreamSetCaptureDependencies));
+    const long long cb0 = hk_launch_count();
+    CU(cudaStreamBeginCaptureToGraph(bs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    const hk_status rb = gm_body_ops(p, g, sp, P, h, bs);
+    cudaGraph_t tmp = nullptr;
+    const cudaError_t eb = cudaStreamEndCapture(bs, &tmp);
+    if (rb != HK_OK) return rb;
+    CU(eb);
+    c_body = hk_launch_count() - cb0;
+    // post: x = Q y, true residuals (both no-ops unless the loop finished)
+    CU(hk_launch_gm_combine(P, g->X.as<double>(), cs));
+    CU(hk_launch_gemv_rowmajor(g->A, g->lda, n, n, g->X.as<double>(), n, s, g->W.as<double>(), n, cs));
+    CU(hk_launch_gm_resid(P, g->B.as<double>(), g->W.as<double>(), cs));
+    return HK_OK;
+  };
+  const hk_status rc = record();
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ee = cudaStreamEndCapture(cs, &graph);
+  const long long captured = hk_launch_count() - c0;
+  hk_count_launch(-(int)captured);          // captured, not executed
+  if (rc != HK_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  CU(ee);
+  const cudaError_t ei = cudaGraphInstantiate(out, graph, 0);
+  cudaGraphDestroy(graph);
+  CU(ei);
+  g->k_pre = c_pre;
+  g->k_body = c_body;
+  g->k_post = captured - c_pre - c_body;
+  return HK_OK;
+}
+
+// Grow the Krylov capacity of a graph to cap2 columns, keeping the first
+// k+1 basis vectors, the Hessenberg columns and the rotations.
+static hk_status gm_grow(hk_plan* p, GmresGraph* g, int64_t cap2, cudaStream_t st) {
+  DevBuf basis, hess, cs, sn, gv, y;
+  CU(gm_alloc_krylov(p, g, cap2, &basis, &hess, &cs, &sn, &gv, &y, st));
+  const int64_t n = p->n, cap = g->cap, vs = cap + 1, vs2 = cap2 + 1;
+  const size_t s = (size_t)g->s;
+  CU(cudaMemsetAsync(hess.p, 0, s * vs2 * cap2 * 8, st));
+  CU(cudaMemsetAsync(gv.p, 0, s * vs2 * 8, st));
+  CU(cudaMemcpy2DAsync(basis.p, (size_t)n * vs2 * 8, g->basis.p, (size_t)n * vs * 8, (size_t)n * vs * 8,
+                       s, cudaMemcpyDeviceToDevice, st));
+  // Hessenberg: s * cap columns of length vs -> ld vs2, per-system stride vs2 * cap2
+  for (size_t c = 0; c < s; ++c)
+    CU(cudaMemcpy2DAsync(hess.as<double>() + c * vs2 * cap2, (size_t)vs2 * 8,
+                         g->hess.as<double>() + c * vs * cap, (size_t)vs * 8, (size_t)vs * 8, cap,
+                         cudaMemcpyDeviceToDevice, st));
+  DevBuf* src[3] = {&g->cs, &g->sn, &g->g};
+  DevBuf* dst[3] = {&cs, &sn, &gv};
+  for (int i = 0; i < 3; ++i)
+    CU(cudaMemcpy2DAsync(dst[i]->p, (size_t)vs2 * 8, src[i]->p, (size_t)vs * 8, (size_t)vs * 8, s,
+                         cudaMemcpyDeviceToDevice, st));
+  CU(cudaStreamSynchronize(st));
+  std::swap(g->basis, basis);
+  std::swap(g->hess, hess);
+  std::swap(g->cs, cs);
+  std::swap(g->sn, sn);
+  std::swap(g->g, gv);
+  std::swap(g->y, y);
+  DevBuf* old[] = {&basis, &hess, &cs, &sn, &gv, &y};
+  for (DevBuf* d : old) d->release();
+  g->cap = cap2;
+  if (g->main) cudaGraphExecDestroy(g->main);
+  if (g->resume) cudaGraphExecDestroy(g->resume);
+  g->main = g->resume = nullptr;
+  return HK_OK;
+}
+
+static hk_status gmres_run(hk_plan* p, int64_t front, const double* A, int64_t lda, int64_t n,
+                           const double* B, int64_t s, double tol, int64_t max_iter, int precond,
+                           const double* diag, double* X, int64_t* iterations, double* history,
+                           double* true_residual, int32_t* flags, cudaStream_t st) {
   if (!(tol > 0.0 && tol < 1.0)) return fail(HK_ERR_VALUE, "tol must lie strictly between 0 and 1");
   if (max_iter < 1) return fail(HK_ERR_VALUE, "max_iter must be >= 1");
-  if (precond == 1 && (!p || !p->factored)) return fail(HK_ERR_STATE, "HODLR preconditioner not factored");
-  if (!p && precond == 1) return fail(HK_ERR_VALUE, "null plan");
-  const int64_t n = p ? p->n : 0;
-  if (n <= 0) return fail(HK_ERR_VALUE, "plan required for the problem size");
-  cudaStream_t st = (cudaStream_t)stream;
+  if (s < 1 || s > HK_GM_MAXS) return fail(HK_ERR_VALUE, "gmres takes 1..16 right-hand sides");
+  if (!p) return fail(HK_ERR_VALUE, "null plan");
+  if (n != p->n) return fail(HK_ERR_DIMENSION, "operator size differs from the preconditioner's");
+  if (lda < n) return fail(HK_ERR_DIMENSION, "operator leading dimension smaller than n");
+  if (precond < 0 || precond > 2) return fail(HK_ERR_VALUE, "precond must be 0, 1 or 2");
+  if (precond == 1 && !p->factored) return fail(HK_ERR_STATE, "HODLR preconditioner not factored");
+  if (precond == 1 && (front < 0 || front >= p->batch)) return fail(HK_ERR_VALUE, "front out of range");
+  if (precond == 2 && !diag) return fail(HK_ERR_VALUE, "diagonal preconditioner needs its diagonal");
+  if (!A || !B || !X) return fail(HK_ERR_VALUE, "null operand");
+  if (hk_device_count() == 0) return fail(HK_ERR_CUDA, "no CUDA device visible");
+  init_pool_once();
   const int64_t mmax = std::min<int64_t>(max_iter, n);
-  GmresScratch sc;
-  auto cleanup = [&]() {
-    DevBuf* all[] = {&sc.basis, &sc.hess, &sc.cs, &sc.sn, &sc.g, &sc.w, &sc.y, &sc.scal, &sc.out};
-    for (DevBuf* d : all)
-      if (d->p) cudaFreeAsync(d->p, st);
-  };
-  hk_status rc = HK_OK;
-  do {
-    if (sc.basis.ensure((size_t)n * (mmax + 1) * 8, st) != cudaSuccess ||
-        sc.hess.ensure((size_t)(mmax + 1) * mmax * 8, st) != cudaSuccess ||
-        sc.cs.ensure((size_t)mmax * 8, st) != cudaSuccess ||
-        sc.sn.ensure((size_t)mmax * 8, st) != cudaSuccess ||
-        sc.g.ensure((size_t)(mmax + 1) * 8, st) != cudaSuccess ||
-        sc.w.ensure((size_t)n * 8, st) != cudaSuccess ||
-        sc.y.ensure((size_t)(mmax + 1) * 8, st) != cudaSuccess ||
-        sc.scal.ensure(64, st) != cudaSuccess || sc.out.ensure(64, st) != cudaSuccess) {
-      rc = fail(HK_ERR_CUDA, "GMRES scratch allocation failed");
+  SolveProg* sp = nullptr;
+  if (precond == 1) {
+    CHK(ensure_solve_scratch(p, (int)s, st));        // may drop cached programs and graphs
+    CHK(build_solve_prog(p, (int)front, (int)s, sp, st));
+  }
+  GmresGraph* g = nullptr;
+  for (GmresGraph* c : p->gmres_graphs)
+    if (c->front == (precond == 1 ? front : 0) && c->s == s && c->precond == precond && c->A == A &&
+        c->lda == lda && c->diag == (precond == 2 ? diag : nullptr) && c->tol == tol &&
+        c->max_iter == max_iter) {
+      g = c;
       break;
     }
-    double* Q = sc.basis.as<double>();
-    double* Hs = sc.hess.as<double>();
-    double* g = sc.g.as<double>();
-    double* w = sc.w.as<double>();
-    double* scal = sc.scal.as<double>();
-    cudaMemsetAsync(Hs, 0, (size_t)(mmax + 1) * mmax * 8, st);
-    cudaMemsetAsync(g, 0, (size_t)(mmax + 1) * 8, st);
-    // ||b||
-    double nb = 0;
-    if (hk_launch_norm(b, n, scal, st) != cudaSuccess || (rc = read_scalar(scal, &nb, st)) != HK_OK) {
-      if (rc == HK_OK) rc = fail(HK_ERR_CUDA, "norm");
-      break;
-    }
-    flags[0] = flags[1] = 0;
-    if (nb == 0.0) {
-      cudaMemsetAsync(x, 0, (size_t)n * 8, st);
+  if (!g) {
+    g = new GmresGraph();
+    g->front = precond == 1 ? front : 0;
+    g->s = (int)s;
+    g->precond = precond;
+    g->A = A;
+    g->lda = lda;
+    g->diag = precond == 2 ? diag : nullptr;
+    g->tol = tol;
+    g->max_iter = max_iter;
+    g->mmax = mmax;
+    g->cap = std::min<int64_t>(mmax, 64);
+    cudaError_t e = gm_alloc_krylov(p, g, g->cap, &g->basis, &g->hess, &g->cs, &g->sn, &g->g, &g->y, st);
+    const size_t ns = (size_t)n * s * 8;
+    if (e == cudaSuccess) e = g->V.ensure(ns, st);
+    if (e == cudaSuccess) e = g->W.ensure(ns, st);
+    if (e == cudaSuccess) e = g->B.ensure(ns, st);
+    if (e == cudaSuccess) e = g->X.ensure(ns, st);
+    if (e == cudaSuccess) e = g->hist.ensure((size_t)s * max_iter * 8, st);
+    if (e == cudaSuccess) e = g->state.ensure(sizeof(GmState), st);
+    if (e != cudaSuccess) {
       cudaStreamSynchronize(st);
-      *iterations = 0;
-      history[0] = 0.0;
-      *true_residual = 0.0;
-      flags[0] = 1;
-      break;
+      destroy_gmres_graph(g);
+      return fail(HK_ERR_CUDA, std::string("GMRES buffers: ") + cudaGetErrorString(e));
     }
-    // r0 = M^{-1} b; beta = ||r0||; Q[:,0] = r0 / beta; g[0] = beta
-    cudaMemcpyAsync(Q, b, (size_t)n * 8, cudaMemcpyDeviceToDevice, st);
-    if ((rc = apply_precond(p, front, precond, A, lda, Q, n, st)) != HK_OK) break;
-    double beta = 0;
-    hk_launch_norm(Q, n, scal, st);
-    if ((rc = read_scalar(scal, &beta, st)) != HK_OK) break;
-    if (beta == 0.0) {
+    p->gmres_graphs.push_back(g);
+  }
+  if (!g->main) {
+    CU(cudaStreamSynchronize(st));              // buffers allocated on st are ready for capture
+    CHK(gm_capture(p, g, sp, true, &g->main));
+  }
+  CU(cudaMemcpyAsync(g->B.p, B, (size_t)n * s * 8, cudaMemcpyDeviceToDevice, st));
+  CU(cudaGraphLaunch(g->main, st));
+  GmState hs{};
+  CU(cudaMemcpyAsync(&hs, g->state.p, sizeof(GmState), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  long long launched = g->k_pre + g->k_post + g->k_body * hs.k;
+  while (!hs.finished) {                        // Krylov capacity exhausted: grow, resume
+    const int64_t k0 = hs.k;
+    CHK(gm_grow(p, g, std::min<int64_t>(mmax, 4 * g->cap), st));
+    CHK(gm_capture(p, g, sp, false, &g->resume));
+    CU(cudaGraphLaunch(g->resume, st));
+    CU(cudaMemcpyAsync(&hs, g->state.p, sizeof(GmState), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    launched += g->k_post + g->k_body * (hs.k - k0);
+    if (g->main) cudaGraphExecDestroy(g->main);   // recaptured at the new capacity on next use
+    g->main = nullptr;
+  }
+  hk_count_launch((int)launched);
+  CU(cudaMemcpyAsync(X, g->X.p, (size_t)n * s * 8, cudaMemcpyDeviceToDevice, st));
+  CU(cudaMemcpyAsync(history, g->hist.p, (size_t)s * max_iter * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  hk_status rc = HK_OK;
+  for (int64_t c = 0; c < s; ++c) {
+    iterations[c] = hs.m[c];
+    flags[2 * c] = flags[2 * c + 1] = 0;
+    true_residual[c] = hs.tres[c];
+    if (hs.zero[c]) {                            // krylov.py:85-87
+      iterations[c] = 0;
+      history[c * max_iter] = 0.0;
+      true_residual[c] = 0.0;
+      flags[2 * c] = 1;
+      continue;
+    }
+    if (hs.err[c]) {                             // krylov.py:91-92
       rc = fail(HK_ERR_BREAKDOWN, "preconditioned rhs is exactly zero");
-      break;
+      continue;
     }
-    hk_launch_scale(Q, n, scal, Q, 0, st);
-    cudaMemcpyAsync(g, &beta, 8, cudaMemcpyHostToDevice, st);
-    bool conv = false, brk = false;
-    int64_t k = 0;
-    double outh[3];
-    for (k = 1; k <= mmax; ++k) {
-      const int64_t j = k - 1;
-      if (hk_launch_gemv_rowmajor(A, lda, n, n, Q + j * n, n, 1, w, n, st) != cudaSuccess) {
-        rc = fail(HK_ERR_CUDA, "gemv");
-        break;
-      }
-      if ((rc = apply_precond(p, front, precond, A, lda, w, n, st)) != HK_OK) break;
-      if (hk_launch_arnoldi(n, j, mmax, Q, Hs, sc.cs.as<double>(), sc.sn.as<double>(), g, w, beta,
-                            sc.out.as<double>(), st) != cudaSuccess) {
-        rc = fail(HK_ERR_CUDA, "arnoldi");
-        break;
-      }
-      cudaMemcpyAsync(outh, sc.out.p, 24, cudaMemcpyDeviceToHost, st);
-      if (cudaStreamSynchronize(st) != cudaSuccess) {
-        rc = fail(HK_ERR_CUDA, "arnoldi sync");
-        break;
-      }
-      if (outh[2] != 0.0) {
-        brk = true;
-        break;
-      }
-      history[k - 1] = outh[0];
-      if (outh[0] <= tol || outh[1] != 0.0) {
-        conv = true;
-        break;
-      }
-    }
-    if (rc != HK_OK) break;
-    if (k > mmax) k = mmax;
-    const int64_t m = brk ? k - 1 : k;
-    if (m > 0) {
-      hk_launch_combine(n, m, mmax, Q, Hs, g, x, sc.y.as<double>(), st);
-    } else {
-      cudaMemsetAsync(x, 0, (size_t)n * 8, st);
-    }
-    // true residual ||b - A x|| / ||b||
-    hk_launch_gemv_rowmajor(A, lda, n, n, x, n, 1, w, n, st);
-    hk_launch_axpby(b, w, w, n, 1.0, -1.0, st);
-    hk_launch_norm(w, n, scal, st);
-    double rn = 0;
-    if ((rc = read_scalar(scal, &rn, st)) != HK_OK) break;
-    const double tr = rn / nb;
-    *true_residual = tr;
-    *iterations = m;
-    if (brk && tr > 10.0 * tol) {
+    const double tr = hs.tres[c];
+    bool cv = hs.conv[c] != 0;
+    const bool bk = hs.brk[c] != 0;
+    if (bk && tr > 10.0 * tol) {                 // krylov.py:157-159
       char msg[160];
       snprintf(msg, sizeof msg, "Arnoldi norm underflow at iteration %lld with true residual %.3e",
-               (long long)k, tr);
+               (long long)(hs.m[c] + 1), tr);
       rc = fail(HK_ERR_BREAKDOWN, msg);
-      break;
     }
-    if (conv && tr > 10.0 * tol) conv = false;
-    if (brk) conv = true;
-    flags[0] = conv ? 1 : 0;
-    flags[1] = brk ? 1 : 0;
-  } while (false);
-  cleanup();
-  cudaStreamSynchronize(st);
+    if (cv && tr > 10.0 * tol) cv = false;       // true-residual guard, :160-163
+    if (bk) cv = true;
+    flags[2 * c] = cv ? 1 : 0;
+    flags[2 * c + 1] = bk ? 1 : 0;
+  }
   return rc;
 }
 
-// s right-hand sides, s independent GMRES runs advanced in lock step: one
-// GEMV over the s Krylov vectors (the dense front is streamed once per
-// iteration instead of s times) and one s-column HODLR solve (the stored
-// factor streamed once), then a batched Arnoldi step.  Each system's
-// arithmetic is the single-rhs run's, column by column (GEMV and solve
-// kernels treat columns independently), so iterates, iteration counts and
-// flags are those of s separate hk_gmres calls.  B, X: n x s, ld = n.
+extern "C" hk_status hk_gmres(hk_plan* p, int64_t front, const double* A, int64_t lda, int64_t n,
+                              const double* b, double tol, int64_t max_iter, int precond,
+                              const double* diag, double* x, int64_t* iterations, double* history,
+                              double* true_residual, int32_t* flags, void* stream) {
+  return gmres_run(p, front, A, lda, n, b, 1, tol, max_iter, precond, diag, x, iterations, history,
+                   true_residual, flags, (cudaStream_t)stream);
+}
+
 extern "C" hk_status hk_gmres_batch(hk_plan* p, int64_t front, const double* A, int64_t lda,
-                                    const double* B, int64_t s, double tol, int64_t max_iter,
-                                    int precond, double* X, int64_t* iterations, double* history,
-                                    double* true_residual, int32_t* flags, void* stream) {
-  if (!(tol > 0.0 && tol < 1.0)) return fail(HK_ERR_VALUE, "tol must lie strictly between 0 and 1");
-  if (max_iter < 1) return fail(HK_ERR_VALUE, "max_iter must be >= 1");
-  if (s < 1 || s > 16) return fail(HK_ERR_VALUE, "gmres_batch takes 1..16 right-hand sides");
-  if (!p) return fail(HK_ERR_VALUE, "null plan");
-  if (precond == 1 && !p->factored) return fail(HK_ERR_STATE, "HODLR preconditioner not factored");
-  const int64_t n = p->n;
-  cudaStream_t st = (cudaStream_t)stream;
-  const int64_t mmax = std::min<int64_t>(max_iter, n);
-  const int64_t vs = mmax + 1, bstride = n * vs, hstride = vs * mmax;
-  DevBuf basis, hess, cs, sn, g, w, yb, nrm, out, act, betad;
-  auto cleanup = [&]() {
-    DevBuf* all[] = {&basis, &hess, &cs, &sn, &g, &w, &yb, &nrm, &out, &act, &betad};
-    for (DevBuf* d : all)
-      if (d->p) cudaFreeAsync(d->p, st);
-  };
-  hk_status rc = HK_OK;
-  do {
-    if (basis.ensure((size_t)s * bstride * 8, st) != cudaSuccess ||
-        hess.ensure((size_t)s * hstride * 8, st) != cudaSuccess ||
-        cs.ensure((size_t)s * vs * 8, st) != cudaSuccess || sn.ensure((size_t)s * vs * 8, st) != cudaSuccess ||
-        g.ensure((size_t)s * vs * 8, st) != cudaSuccess || w.ensure((size_t)s * n * 8, st) != cudaSuccess ||
-        yb.ensure((size_t)vs * 8, st) != cudaSuccess || nrm.ensure((size_t)s * 8 + 8, st) != cudaSuccess ||
-        out.ensure((size_t)3 * s * 8, st) != cudaSuccess || act.ensure((size_t)s * 4, st) != cudaSuccess ||
-        betad.ensure((size_t)s * 8, st) != cudaSuccess) {
-      rc = fail(HK_ERR_CUDA, "GMRES scratch allocation failed");
-      break;
-    }
-    double* Q = basis.as<double>();
-    double* W = w.as<double>();
-    cudaMemsetAsync(hess.p, 0, (size_t)s * hstride * 8, st);
-    cudaMemsetAsync(g.p, 0, (size_t)s * vs * 8, st);
-    std::vector<double> nb(s), beta(s), outh(3 * s);
-    std::vector<int32_t> active(s, 1);
-    std::vector<int64_t> m(s, 0);
-    std::vector<char> conv(s, 0), brk(s, 0), done(s, 0);
-    // ||b_c||
-    CU(hk_launch_norms(B, n, n, (int)s, nrm.as<double>(), st));
-    CU(cudaMemcpyAsync(nb.data(), nrm.p, s * 8, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    // r0 = M^{-1} b: the s initial vectors are the first basis vectors (column stride bstride)
-    for (int64_t c = 0; c < s; ++c)
-      CU(cudaMemcpyAsync(Q + c * bstride, B + c * n, n * 8, cudaMemcpyDeviceToDevice, st));
-    if (precond == 1) {
-      CHK(run_solve(p, (int)front, Q, bstride, s, 0, st));
-    } else if (precond == 2) {
-      for (int64_t c = 0; c < s; ++c) CU(hk_launch_diag_scale(A, lda, Q + c * bstride, Q + c * bstride, n, st));
-    }
-    CU(hk_launch_norms(Q, n, bstride, (int)s, nrm.as<double>(), st));
-    CU(cudaMemcpyAsync(beta.data(), nrm.p, s * 8, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    for (int64_t c = 0; c < s; ++c) {
-      flags[2 * c] = flags[2 * c + 1] = 0;
-      if (nb[c] == 0.0) { done[c] = 1; conv[c] = 1; active[c] = 0; continue; }
-      if (beta[c] == 0.0) {
-        rc = fail(HK_ERR_BREAKDOWN, "preconditioned rhs is exactly zero");
-        break;
-      }
-      CU(hk_launch_scale(Q + c * bstride, n, nrm.as<double>() + c, Q + c * bstride, 0, st));
-      CU(cudaMemcpyAsync(g.as<double>() + c * vs, &beta[c], 8, cudaMemcpyHostToDevice, st));
-    }
-    if (rc != HK_OK) break;
-    CU(cudaMemcpyAsync(betad.p, beta.data(), s * 8, cudaMemcpyHostToDevice, st));
-    int64_t k = 0;
-    for (k = 1; k <= mmax; ++k) {
-      bool any = false;
-      for (int64_t c = 0; c < s; ++c) any = any || active[c];
-      if (!any) break;
-      const int64_t j = k - 1;
-      CU(cudaMemcpyAsync(act.p, active.data(), s * 4, cudaMemcpyHostToDevice, st));
-      CU(hk_launch_gemv_rowmajor(A, lda, n, n, Q + j * n, bstride, s, W, n, st));
-      if (precond == 1) {
-        CHK(run_solve(p, (int)front, W, n, s, 0, st));
-      } else if (precond == 2) {
-        for (int64_t c = 0; c < s; ++c) CU(hk_launch_diag_scale(A, lda, W + c * n, W + c * n, n, st));
-      }
-      CU(hk_launch_arnoldi_batch(n, j, mmax, Q, bstride, hess.as<double>(), hstride,
-                                 cs.as<double>(), sn.as<double>(), g.as<double>(), W,
-                                 betad.as<double>(), out.as<double>(), act.as<int32_t>(), (int)s, st));
-      CU(cudaMemcpyAsync(outh.data(), out.p, 3 * s * 8, cudaMemcpyDeviceToHost, st));
-      CU(cudaStreamSynchronize(st));
-      for (int64_t c = 0; c < s; ++c) {
-        if (!active[c]) continue;
-        const double* o = outh.data() + 3 * c;
-        if (o[2] != 0.0) { brk[c] = 1; m[c] = k - 1; active[c] = 0; continue; }
-        history[c * max_iter + (k - 1)] = o[0];
-        m[c] = k;
-        if (o[0] <= tol || o[1] != 0.0) { conv[c] = 1; active[c] = 0; }
-      }
-    }
-    // x_c = Q_c y_c, then the true residuals
-    for (int64_t c = 0; c < s; ++c) {
-      if (done[c]) { CU(cudaMemsetAsync(X + c * n, 0, n * 8, st)); continue; }
-      if (m[c] > 0)
-        CU(hk_launch_combine(n, m[c], mmax, Q + c * bstride, hess.as<double>() + c * hstride,
-                             g.as<double>() + c * vs, X + c * n, yb.as<double>(), st));
-      else
-        CU(cudaMemsetAsync(X + c * n, 0, n * 8, st));
-    }
-    CU(hk_launch_gemv_rowmajor(A, lda, n, n, X, n, s, W, n, st));
-    for (int64_t c = 0; c < s; ++c) CU(hk_launch_axpby(B + c * n, W + c * n, W + c * n, n, 1.0, -1.0, st));
-    CU(hk_launch_norms(W, n, n, (int)s, nrm.as<double>(), st));
-    std::vector<double> rn(s);
-    CU(cudaMemcpyAsync(rn.data(), nrm.p, s * 8, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    for (int64_t c = 0; c < s; ++c) {
-      iterations[c] = m[c];
-      if (done[c]) { true_residual[c] = 0.0; flags[2 * c] = 1; continue; }
-      const double tr = rn[c] / nb[c];
-      true_residual[c] = tr;
-      bool cv = conv[c];
-      if (brk[c] && tr > 10.0 * tol) {
-        char msg[160];
-        snprintf(msg, sizeof msg, "rhs %lld: Arnoldi norm underflow with true residual %.3e",
-                 (long long)c, tr);
-        rc = fail(HK_ERR_BREAKDOWN, msg);
-      }
-      if (cv && tr > 10.0 * tol) cv = false;
-      if (brk[c]) cv = true;
-      flags[2 * c] = cv ? 1 : 0;
-      flags[2 * c + 1] = brk[c] ? 1 : 0;
-    }
-  } while (false);
-  cleanup();
-  return rc;
+                                    int64_t n, const double* B, int64_t s, double tol,
+                                    int64_t max_iter, int precond, const double* diag, double* X,
+                                    int64_t* iterations, double* history, double* true_residual,
+                                    int32_t* flags, void* stream) {
+  return gmres_run(p, front, A, lda, n, B, s, tol, max_iter, precond, diag, X, iterations, history,
+                   true_residual, flags, (cudaStream_t)stream);
 }
 
 extern "C" hk_status hk_arnoldi_step(int64_t n, int64_t j, int64_t mmax, double* basis,

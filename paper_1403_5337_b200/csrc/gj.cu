@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_blk_kernel(const GjTask* __rest
         const int p = warp_argmax_idx(bv, have, bi);
         const int lp = p & 31, qp = p >> 5;
         const double pivabs = __shfl_sync(0xffffffffu, bv, lp);
+        if (t.near && lane == 0 && pivabs < HK_NEAR_PIVOT) *t.near = 1;
         if (!(pivabs >= HK_PIVOT_FLOOR)) { sing = 1; break; }
         const double rinv = __shfl_sync(0xffffffffu, myrinv, lp);
         double ck[RPL];
@@ -249,6 +250,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_df_kernel(const GjTask* __restr
         const int p = warp_argmax_idx(bv, have, bi);
         const int lp = p & 31, qp = p >> 5;
         const double pivabs = __shfl_sync(0xffffffffu, bv, lp);
+        if (t.near && lane == 0 && pivabs < HK_NEAR_PIVOT) *t.near = 1;
         if (__any_sync(0xffffffffu, !(pivabs >= HK_PIVOT_FLOOR))) {
           if (lane == 0) {
             p_s[c] = -1;
@@ -414,6 +416,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_cl_kernel(const GjTask* __restr
         const int p = warp_argmax_idx(bv, have, bi);
         const int lp = p & 31, qp = p >> 5;
         const double pivabs = __shfl_sync(0xffffffffu, bv, lp);
+        if (t.near && lane == 0 && pivabs < HK_NEAR_PIVOT) *t.near = 1;
         if (!(pivabs >= HK_PIVOT_FLOOR)) { sing = 1; break; }
         const double rinv = __shfl_sync(0xffffffffu, myrinv, lp);
         double ck[RPL];
@@ -589,6 +592,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_cldf_kernel(const GjTask* __res
       const int p = warp_argmax_idx(bv, have, bi);
       const int lp = p & 31, qp = p >> 5;
       const double pivabs = __shfl_sync(0xffffffffu, bv, lp);
+      if (t.near && lane == 0 && pivabs < HK_NEAR_PIVOT) *t.near = 1;
       if (!(pivabs >= HK_PIVOT_FLOOR)) {
         if (lane == 0) {
           p_s[lc] = -1;
@@ -728,6 +732,7 @@ __global__ void __launch_bounds__(NT) gj_kernel(const GjTask* __restrict__ tasks
     if (lane == 0) {
       s_p = (int)a.i;
       s_sing = !(a.v >= HK_PIVOT_FLOOR);
+      if (t.near && a.v < HK_NEAR_PIVOT) *t.near = 1;
     }
   }
   __syncthreads();
@@ -775,6 +780,7 @@ __global__ void __launch_bounds__(NT) gj_kernel(const GjTask* __restrict__ tasks
         if (lane == 0) {
           s_p = (int)a.i;
           s_sing = !(a.v >= HK_PIVOT_FLOOR);
+          if (t.near && a.v < HK_NEAR_PIVOT) *t.near = 1;
         }
       }
     }

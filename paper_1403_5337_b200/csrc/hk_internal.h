@@ -136,15 +136,6 @@ struct SgemvTask {   // y[i,r] (op)= sum_k M[i,k] v[k,r] for i < rows, M column-
 constexpr int HK_PDOT_ROWS = 256;   // rows per partial-dot chunk
 constexpr int HK_PDOT_COLS = 32;    // columns per partial-dot item
 constexpr int HK_SGEMV_ROWS = 32;   // rows per sgemv item
-// one phase of the fused solve sweep: kind 0 = pdot items, 1 = sgemv items
-struct SolvePhase {
-  int32_t kind, nitems;
-  const void* tasks;
-  const int32_t* items;
-};
-size_t hk_solve_sweep_smem(int s, int max_k);
-cudaError_t hk_launch_solve_sweep(const SolvePhase* phases, int nphase, int max_items, int s,
-                                  int max_k, unsigned* bar, cudaStream_t st);
 cudaError_t hk_launch_pdot(const PdotTask* tasks, const int32_t* items, int nitems, int s,
                            cudaStream_t st);
 cudaError_t hk_launch_sgemv(const SgemvTask* tasks, const int32_t* items, int nitems, int s,
@@ -209,6 +200,51 @@ cudaError_t hk_launch_diag_scale(const double* A, int64_t lda, const double* x, 
 
 void hk_count_launch(int k = 1);
 
+// ---------------------------------------------------------------- device-resident GMRES
+// State of up to HK_GM_MAXS systems advanced in lock step by one CUDA graph
+// whose conditional WHILE node runs the Arnoldi iteration until every system
+// has converged, broken down or hit the iteration cap (krylov.py:107-145):
+// the host reads this struct once, after the loop.
+constexpr int HK_GM_MAXS = 16;
+struct GmState {
+  int32_t k;          // iterations completed (the loop's k, 1-based after the first)
+  int32_t cont;       // loop condition of the last control step
+  int32_t finished;   // no active system left, or k == mmax
+  int32_t counter;    // last-CTA-done counter of the Arnoldi / start kernels
+  int32_t active[HK_GM_MAXS], m[HK_GM_MAXS], conv[HK_GM_MAXS], brk[HK_GM_MAXS];
+  int32_t zero[HK_GM_MAXS];   // ||b|| == 0: x = 0, converged, 0 iterations (krylov.py:85-87)
+  int32_t err[HK_GM_MAXS];    // preconditioned rhs exactly zero (krylov.py:91-92)
+  double nb[HK_GM_MAXS], beta[HK_GM_MAXS], tres[HK_GM_MAXS];
+  double out[3 * HK_GM_MAXS]; // rel, happy, breakdown of each system's last Arnoldi step
+};
+struct GmParams {
+  int64_t n, cap, mmax, max_iter;   // cap: basis columns - 1 currently allocated
+  int32_t s, pad_;
+  double tol;
+  double* basis;  int64_t bstride;  // system c: n x (cap+1), column-major, at basis + c*bstride
+  double* hess;   int64_t hstride;  // (cap+1) x cap per system
+  double *cs, *sn, *g;  int64_t vs; // cap+1 per system
+  double* V;                        // n x s: the vector the next GEMV multiplies
+  double* hist;                     // s x max_iter preconditioned residual history
+  double* y;                        // s x vs back-substitution scratch
+  GmState* st;
+};
+// start: per system, q0 = r0 / beta (r0 = column c of R0, n x s ld n), g[0] = beta,
+// then the first loop-condition evaluation
+cudaError_t hk_launch_gm_start(const GmParams& P, const double* R0, cudaGraphConditionalHandle h,
+                               cudaStream_t st);
+// one Arnoldi/MGS/Givens step of every active system on W (n x s, ld n), then
+// (last CTA) the convergence bookkeeping and the loop condition
+cudaError_t hk_launch_gm_arnoldi(const GmParams& P, double* W, cudaGraphConditionalHandle h,
+                                 cudaStream_t st);
+// x_c = basis_c y_c after back substitution (krylov.py:147-154), when finished
+cudaError_t hk_launch_gm_combine(const GmParams& P, double* X, cudaStream_t st);
+// true residuals ||b_c - (A x)_c|| / ||b_c|| (krylov.py:152-156), when finished
+cudaError_t hk_launch_gm_resid(const GmParams& P, const double* B, const double* AX, cudaStream_t st);
+// y[c*n + i] = x[c*n + i] / d[i] for s columns (DiagonalPreconditioner, krylov.py:58-62)
+cudaError_t hk_launch_vdiv(const double* x, const double* d, double* y, int64_t n, int s,
+                           cudaStream_t st);
+
 // ---------------------------------------------------------------- Gauss-Jordan inverse
 // In-place Gauss-Jordan with partial (row) pivoting -> explicit inverse.
 // Pivots equal those of LU with partial pivoting (rows >= k see the same
@@ -220,8 +256,13 @@ struct GjTask {
   int64_t out_ld;
   double* scratch;     // hk_gj_scratch_bytes(N) used when N is too large for SMEM (else null)
   int32_t* status;     // 0 ok, 1 singular
+  int32_t* near;       // optional: set to 1 when some |pivot| < HK_NEAR_PIVOT (not singular)
   int32_t N;
   int32_t mode;
 };
+// A Gauss-Jordan pivot below this (absolute) magnitude makes the factorization
+// re-decide the coupling system's singularity with the reference's own
+// partial-pivot LU of S (hodlr.py:272-277; api.cpp hk_factor_ext).
+#define HK_NEAR_PIVOT 1e-8
 cudaError_t hk_launch_gj(const GjTask* tasks_dev, int ntasks, int maxN, cudaStream_t st);
 size_t hk_gj_scratch_bytes(int N);     // 0 when N fits SMEM

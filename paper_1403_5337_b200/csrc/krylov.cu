@@ -22,7 +22,7 @@ __device__ void block_axpy(double* w, const double* q, double h, int64_t n) {
 
 __device__ __forceinline__ void arnoldi_body(int64_t n, int64_t j, int64_t mmax, double* basis,
                                              double* hess, double* cs, double* sn, double* g,
-                                             double* w, double beta, double* out) {
+                                             double* w, double beta, double* out, double* vout) {
   __shared__ double red[KR_NT / 32];
   const int64_t k = j + 1;
   const int64_t ldh = mmax + 1;
@@ -50,7 +50,11 @@ __device__ __forceinline__ void arnoldi_body(int64_t n, int64_t j, int64_t mmax,
   const bool happy = hk <= 1e-14 * fmax(norm_in, 1e-300);   // :122
   if (!happy) {
     double* qn = basis + k * n;
-    for (int64_t i = threadIdx.x; i < n; i += KR_NT) qn[i] = w[i] / hk;
+    for (int64_t i = threadIdx.x; i < n; i += KR_NT) {
+      const double q = w[i] / hk;
+      qn[i] = q;
+      if (vout) vout[i] = q;
+    }
   }
   if (threadIdx.x == 0) {
     hcol[k] = hk;
@@ -86,7 +90,7 @@ __device__ __forceinline__ void arnoldi_body(int64_t n, int64_t j, int64_t mmax,
 template <int WPT>
 __device__ __forceinline__ void arnoldi_body_reg(int64_t n, int64_t j, int64_t mmax, double* basis,
                                                  double* hess, double* cs, double* sn, double* g,
-                                                 double* w, double beta, double* out) {
+                                                 double* w, double beta, double* out, double* vout) {
   constexpr int NW = KR_NT / 32;
   __shared__ double red[2][NW];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -148,7 +152,11 @@ __device__ __forceinline__ void arnoldi_body_reg(int64_t n, int64_t j, int64_t m
     const int64_t i = tid + (int64_t)q * KR_NT;
     if (i < n) {
       w[i] = wr[q];
-      if (!happy) qn[i] = wr[q] / hk;
+      if (!happy) {
+        const double v = wr[q] / hk;
+        qn[i] = v;
+        if (vout) vout[i] = v;
+      }
     }
   }
   if (tid == 0) {
@@ -180,13 +188,14 @@ __device__ __forceinline__ void arnoldi_body_reg(int64_t n, int64_t j, int64_t m
 // dispatch: registers for n <= 16 * 1024, the streaming body above that
 __device__ __forceinline__ void arnoldi_dispatch(int64_t n, int64_t j, int64_t mmax, double* basis,
                                                  double* hess, double* cs, double* sn, double* g,
-                                                 double* w, double beta, double* out) {
-  if (n <= 1 * KR_NT) arnoldi_body_reg<1>(n, j, mmax, basis, hess, cs, sn, g, w, beta, out);
-  else if (n <= 3 * KR_NT) arnoldi_body_reg<3>(n, j, mmax, basis, hess, cs, sn, g, w, beta, out);
-  else if (n <= 5 * KR_NT) arnoldi_body_reg<5>(n, j, mmax, basis, hess, cs, sn, g, w, beta, out);
-  else if (n <= 10 * KR_NT) arnoldi_body_reg<10>(n, j, mmax, basis, hess, cs, sn, g, w, beta, out);
-  else if (n <= 16 * KR_NT) arnoldi_body_reg<16>(n, j, mmax, basis, hess, cs, sn, g, w, beta, out);
-  else arnoldi_body(n, j, mmax, basis, hess, cs, sn, g, w, beta, out);
+                                                 double* w, double beta, double* out,
+                                                 double* vout = nullptr) {
+  if (n <= 1 * KR_NT) arnoldi_body_reg<1>(n, j, mmax, basis, hess, cs, sn, g, w, beta, out, vout);
+  else if (n <= 3 * KR_NT) arnoldi_body_reg<3>(n, j, mmax, basis, hess, cs, sn, g, w, beta, out, vout);
+  else if (n <= 5 * KR_NT) arnoldi_body_reg<5>(n, j, mmax, basis, hess, cs, sn, g, w, beta, out, vout);
+  else if (n <= 10 * KR_NT) arnoldi_body_reg<10>(n, j, mmax, basis, hess, cs, sn, g, w, beta, out, vout);
+  else if (n <= 16 * KR_NT) arnoldi_body_reg<16>(n, j, mmax, basis, hess, cs, sn, g, w, beta, out, vout);
+  else arnoldi_body(n, j, mmax, basis, hess, cs, sn, g, w, beta, out, vout);
 }
 
 __global__ void __launch_bounds__(KR_NT) arnoldi_kernel(int64_t n, int64_t j, int64_t mmax,
@@ -275,6 +284,150 @@ __global__ void diag_scale_kernel(const double* A, int64_t lda, const double* x,
   }
 }
 
+// ---------------------------------------------------------------- device-resident GMRES
+// Loop bookkeeping of krylov.py:121-145 after an Arnoldi step (first = false)
+// or at the start (first = true), then the WHILE condition of the graph.
+// Runs on one thread after every system's step is visible.
+__device__ void gm_control(const GmParams& P, cudaGraphConditionalHandle h, bool first) {
+  GmState* st = P.st;
+  int k = st->k;
+  if (!first) {
+    ++k;                                              // iteration k just completed
+    for (int c = 0; c < P.s; ++c) {
+      if (!st->active[c]) continue;
+      const volatile double* o = st->out + 3 * c;
+      if (o[2] != 0.0) {                              // Givens breakdown: m = k - 1
+        st->brk[c] = 1;
+        st->m[c] = k - 1;
+        st->active[c] = 0;
+        continue;
+      }
+      P.hist[c * P.max_iter + (k - 1)] = o[0];
+      st->m[c] = k;
+      if (o[0] <= P.tol || o[1] != 0.0) {             // converged or happy breakdown
+        st->conv[c] = 1;
+        st->active[c] = 0;
+      }
+    }
+    st->k = k;
+  }
+  int any = 0;
+  for (int c = 0; c < P.s; ++c) any |= st->active[c];
+  const int cont = any && k < P.mmax && k < P.cap;
+  st->cont = cont;
+  st->finished = (!any || k >= P.mmax) ? 1 : 0;
+  cudaGraphSetConditional(h, cont ? 1u : 0u);
+}
+
+// the last CTA of the grid to arrive runs the control step
+__device__ __forceinline__ void gm_last_cta(const GmParams& P, cudaGraphConditionalHandle h, bool first) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int t = atomicAdd(&P.st->counter, 1);
+    if (t == (int)gridDim.x - 1) {
+      __threadfence();
+      gm_control(P, h, first);
+      P.st->counter = 0;
+      __threadfence();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) gm_start_kernel(GmParams P, const double* R0,
+                                                       cudaGraphConditionalHandle h) {
+  const int c = blockIdx.x;
+  GmState* st = P.st;
+  const double nb = st->nb[c], beta = st->beta[c];
+  const bool zero = nb == 0.0, err = !zero && beta == 0.0, go = !zero && !err;
+  if (go) {                                          // Q[:,0] = r0 / beta (krylov.py:89-93)
+    const double* r = R0 + (int64_t)c * P.n;
+    double* q = P.basis + c * P.bstride;
+    double* v = P.V + (int64_t)c * P.n;
+    for (int64_t i = threadIdx.x; i < P.n; i += blockDim.x) {
+      const double x = r[i] / beta;
+      q[i] = x;
+      v[i] = x;
+    }
+  }
+  if (threadIdx.x == 0) {
+    st->zero[c] = zero;
+    st->err[c] = err;
+    st->active[c] = go;
+    st->m[c] = st->conv[c] = st->brk[c] = 0;
+    st->tres[c] = 0.0;
+    if (go) P.g[c * P.vs] = beta;
+  }
+  gm_last_cta(P, h, true);
+}
+
+__global__ void __launch_bounds__(KR_NT) gm_arnoldi_kernel(GmParams P, double* W,
+                                                           cudaGraphConditionalHandle h) {
+  const int c = blockIdx.x;
+  GmState* st = P.st;
+  const int64_t j = *(volatile int32_t*)&st->k;     // read before this CTA's arrival count
+  if (*(volatile int32_t*)&st->active[c]) {
+    const int64_t vs = P.vs;
+    arnoldi_dispatch(P.n, j, P.cap, P.basis + c * P.bstride, P.hess + c * P.hstride, P.cs + c * vs,
+                     P.sn + c * vs, P.g + c * vs, W + c * P.n, st->beta[c], st->out + 3 * c,
+                     P.V + c * P.n);
+  }
+  gm_last_cta(P, h, false);
+}
+
+// back substitution (krylov.py:147-151) and x = Q[:, :m] y (:152)
+__global__ void __launch_bounds__(KR_NT) gm_combine_kernel(GmParams P, double* X) {
+  const GmState* st = P.st;
+  if (!st->finished) return;
+  const int c = blockIdx.x;
+  const int64_t m = st->m[c], n = P.n, ldh = P.cap + 1;
+  double* x = X + (int64_t)c * n;
+  if (st->zero[c] || st->err[c] || m == 0) {
+    for (int64_t r = threadIdx.x; r < n; r += KR_NT) x[r] = 0.0;
+    return;
+  }
+  const double* hess = P.hess + c * P.hstride;
+  const double* g = P.g + c * P.vs;
+  double* y = P.y + c * P.vs;
+  if (threadIdx.x == 0) {
+    for (int64_t i = m - 1; i >= 0; --i) {
+      double s = 0.0;
+      for (int64_t l = i + 1; l < m; ++l) s += hess[i + l * ldh] * y[l];
+      y[i] = (g[i] - s) / hess[i + i * ldh];
+    }
+  }
+  __syncthreads();
+  const double* basis = P.basis + c * P.bstride;
+  for (int64_t r = threadIdx.x; r < n; r += KR_NT) {
+    double s = 0.0;
+    for (int64_t l = 0; l < m; ++l) s += basis[r + l * n] * y[l];
+    x[r] = s;
+  }
+}
+
+__global__ void __launch_bounds__(KR_NT) gm_resid_kernel(GmParams P, const double* B, const double* AX) {
+  __shared__ double red[KR_NT / 32];
+  GmState* st = P.st;
+  if (!st->finished) return;
+  const int c = blockIdx.x;
+  const double* b = B + (int64_t)c * P.n;
+  const double* ax = AX + (int64_t)c * P.n;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < P.n; i += KR_NT) {
+    const double d = b[i] - ax[i];
+    s += d * d;
+  }
+  s = block_sum<KR_NT>(s, red);
+  if (threadIdx.x == 0) st->tres[c] = st->zero[c] ? 0.0 : sqrt(s) / st->nb[c];
+}
+
+__global__ void vdiv_kernel(const double* x, const double* d, double* y, int64_t n, int s) {
+  const int64_t total = n * s;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x)
+    y[t] = x[t] / d[t % n];
+}
+
 int grid_for(int64_t n) {
   int64_t b = (n + 255) / 256;
   if (b > 2048) b = 2048;
@@ -343,6 +496,40 @@ cudaError_t hk_launch_norms(const double* x, int64_t n, int64_t ld, int s, doubl
                             cudaStream_t st) {
   if (s <= 0) return cudaSuccess;
   norms_kernel<<<s, KR_NT, 0, st>>>(x, n, ld, out);
+  hk_count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t hk_launch_gm_start(const GmParams& P, const double* R0, cudaGraphConditionalHandle h,
+                               cudaStream_t st) {
+  gm_start_kernel<<<P.s, 256, 0, st>>>(P, R0, h);
+  hk_count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t hk_launch_gm_arnoldi(const GmParams& P, double* W, cudaGraphConditionalHandle h,
+                                 cudaStream_t st) {
+  gm_arnoldi_kernel<<<P.s, KR_NT, 0, st>>>(P, W, h);
+  hk_count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t hk_launch_gm_combine(const GmParams& P, double* X, cudaStream_t st) {
+  gm_combine_kernel<<<P.s, KR_NT, 0, st>>>(P, X);
+  hk_count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t hk_launch_gm_resid(const GmParams& P, const double* B, const double* AX, cudaStream_t st) {
+  gm_resid_kernel<<<P.s, KR_NT, 0, st>>>(P, B, AX);
+  hk_count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t hk_launch_vdiv(const double* x, const double* d, double* y, int64_t n, int s,
+                           cudaStream_t st) {
+  if (n <= 0 || s <= 0) return cudaSuccess;
+  vdiv_kernel<<<grid_for(n * s), 256, 0, st>>>(x, d, y, n, s);
   hk_count_launch();
   return cudaGetLastError();
 }

@@ -276,44 +276,6 @@ __global__ void __launch_bounds__(256) sgemv_kernel(const SgemvTask* __restrict_
   sgemv_item(tasks, items, blockIdx.x, s, vs);
 }
 
-// ---------------------------------------------------------------------------
-// The whole few-RHS solve sweep as ONE persistent kernel: the phases (leaf
-// sgemv, then pdot -> S^-1 g -> update per level, deepest first) run in order,
-// every CTA striding over the phase's items, with a grid-wide barrier between
-// phases instead of a kernel boundary.  Same items and per-item arithmetic as
-// the split launches (bit-identical results); on config 4 the 22 dependent
-// launches of a solve were ~15 us each, mostly launch and tail latency.
-__device__ __forceinline__ void grid_barrier(unsigned* bar) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    // flip-bit barrier (self-resetting): CTA 0 adds 0x80000000 - (G - 1),
-    // every other CTA adds 1, so the top bit flips once all G have arrived
-    const unsigned nb = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
-    unsigned old, cur;
-    asm volatile("atom.add.release.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(bar), "r"(nb) : "memory");
-    do {
-      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
-    } while (((old ^ cur) & 0x80000000u) == 0);
-  }
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(256) solve_sweep_kernel(const SolvePhase* __restrict__ phases,
-                                                          int nphase, int s, unsigned* bar) {
-  extern __shared__ double sm[];
-  for (int ph = 0; ph < nphase; ++ph) {
-    const SolvePhase P = phases[ph];
-    for (int it = blockIdx.x; it < P.nitems; it += gridDim.x) {
-      if (P.kind == 0)
-        pdot_item(reinterpret_cast<const PdotTask*>(P.tasks), P.items, it, s, sm);
-      else
-        sgemv_item(reinterpret_cast<const SgemvTask*>(P.tasks), P.items, it, s, sm);
-      __syncthreads();   // SMEM reuse by the next item
-    }
-    if (ph + 1 < nphase) grid_barrier(bar);
-  }
-}
-
 // Dense GEMV for the GMRES operator (src/cli.py:320-321): y(m x s) = A x with
 // A row-major.  Each warp owns RW = 4 rows and walks them together with
 // 16-byte loads (lane l covers columns 2l + 64t, 2l + 64t + 1), so every x
@@ -442,31 +404,3 @@ cudaError_t hk_launch_sgemv(const SgemvTask* tasks, const int32_t* items, int ni
   return cudaGetLastError();
 }
 
-size_t hk_solve_sweep_smem(int s, int max_k) {
-  const size_t pd = (size_t)HK_PDOT_ROWS * s * 8;
-  const size_t sg = ((size_t)max_k * s + 256 * (size_t)s) * 8;
-  return pd > sg ? pd : sg;
-}
-
-cudaError_t hk_launch_solve_sweep(const SolvePhase* phases, int nphase, int max_items, int s,
-                                  int max_k, unsigned* bar, cudaStream_t st) {
-  if (nphase == 0 || max_items == 0) return cudaSuccess;
-  const size_t smem = hk_solve_sweep_smem(s, max_k);
-  cudaError_t e = cudaFuncSetAttribute(solve_sweep_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_sweep_kernel, 256, smem);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) return cudaErrorLaunchOutOfResources;
-  // every CTA must be co-resident for the grid barrier: stay below the
-  // device's capacity (a few SMs may be held by a concurrent copy kernel)
-  int grid = sms * per_sm - 16;
-  if (grid > max_items) grid = max_items;
-  if (grid < 1) grid = 1;
-  solve_sweep_kernel<<<grid, 256, smem, st>>>(phases, nphase, s, bar);
-  hk_count_launch();
-  return cudaGetLastError();
-}

@@ -522,11 +522,22 @@ class HodlrBatch:
         N.check(N.lib().hk_factor(self.plan.h, N.stream_handle()))
 
     def solve_(self, rhs):
-        """In-place device solve of rhs shaped (batch, s, n) (column-major n x s per front)."""
-        if rhs.dim() == 2:
+        """In-place device solve of rhs shaped (batch, n) or (batch, s, n)
+        (column-major n x s per front): a contiguous CUDA float64 tensor."""
+        torch = N.require_cuda()
+        if not isinstance(rhs, torch.Tensor) or not rhs.is_cuda or rhs.dtype != torch.float64:
+            raise ValueError("rhs must be a CUDA float64 tensor")
+        if not rhs.is_contiguous():
+            raise ValueError("rhs must be contiguous")
+        if rhs.dim() == 2 and tuple(rhs.shape) == (self.batch, self.n):
             s = 1
-        else:
+        elif rhs.dim() == 3 and rhs.shape[0] == self.batch and rhs.shape[2] == self.n:
             s = rhs.shape[1]
+        else:
+            raise DimensionMismatchError(f"rhs has shape {tuple(rhs.shape)}, expected "
+                                         f"({self.batch}, {self.n}) or ({self.batch}, s, {self.n})")
+        if self.ranks is None:
+            raise ValueError("solve_ before factorize")
         N.check(N.lib().hk_solve(self.plan.h, N.ptr(rhs), self.n, s, self.n * s,
                                  N.stream_handle()))
         return rhs

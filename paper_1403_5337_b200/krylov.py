@@ -2,9 +2,9 @@
 
 Fast path: ``gmres(DenseOperator(front), b, cfg, preconditioner=fact)`` (or
 ``HodlrPreconditioner`` / ``DiagonalPreconditioner``) runs entirely on the
-device through ``hk_gmres``: fp64 GEMV operator, HODLR solve, MGS + Givens in
-one single-CTA kernel per iteration, three scalars back to the host per
-iteration.
+device through ``hk_gmres``: fp64 GEMV operator, HODLR solve, MGS + Givens,
+the whole iteration captured in one CUDA graph with a conditional WHILE node,
+so the host synchronises once per solve, not once per iteration.
 
 General path: any Python callables (as in the reference's tests,
 ``lambda v: a @ v``).  The Krylov basis, Hessenberg and Givens state still
@@ -20,7 +20,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as N
-from .errors import GmresBreakdownError
+from .errors import DimensionMismatchError, GmresBreakdownError
 
 log = logging.getLogger("hodlrkit")
 
@@ -66,6 +66,14 @@ class DiagonalPreconditioner:
     @property
     def flagged(self) -> bool:
         return self.zero_count > 0
+
+    def device_diag(self):
+        """The (zero-replaced) diagonal as a CUDA tensor, uploaded once."""
+        dev = getattr(self, "_dev", None)
+        if dev is None:
+            torch = N.require_cuda()
+            dev = self._dev = torch.from_numpy(self.diag).cuda()
+        return dev
 
     def __call__(self, r):
         return r / self.diag
@@ -130,39 +138,68 @@ def gmres(apply_op, b, cfg: GmresConfig, preconditioner=None) -> GmresResult:
     return _gmres_callables(apply_op, b, cfg, preconditioner)
 
 
-def _gmres_device(op: DenseOperator, b, cfg, pre) -> GmresResult:
-    torch = N.require_cuda()
-    from .hodlr import HodlrBatch, _Plan
-    n = b.size
-    if op.n != n:
-        raise ValueError("operator and rhs sizes differ")
+def _device_target(op: DenseOperator, n: int, pre):
+    """(plan, front, precond kind, diag pointer) of the device GMRES, with the
+    reference's shape errors: a HODLR preconditioner of another order raises
+    DimensionMismatchError as its solve() would (hodlr.py:291-293); an
+    operator of another order raises ValueError as ``dense @ v`` does."""
+    from .hodlr import _Plan
+    diag = None
     if _is_fact(pre):
+        if pre.n != n:
+            raise DimensionMismatchError(f"rhs has {n} rows, preconditioner expects {pre.n}")
         plan, front, kind = pre.plan, pre.front_index, 1
     else:
+        front, kind = 0, 0
+        if isinstance(pre, DiagonalPreconditioner):
+            if pre.diag.size != n:
+                raise ValueError(f"diagonal preconditioner has {pre.diag.size} entries, rhs {n}")
+            diag, kind = pre.device_diag(), 2
         plan = getattr(op, "_plan", None)
         if plan is None:
-            plan = _Plan(n, max(n, 1), 1)
+            plan = _Plan(op.n, max(op.n, 1), 1)
             op._plan = plan
-        front, kind = 0, 0 if pre is None else 2
-    bd = torch.from_numpy(np.ascontiguousarray(b)).cuda()
-    x = torch.zeros(n, dtype=torch.float64, device="cuda")
-    mmax = min(cfg.max_iter, n)
-    hist = np.zeros(max(mmax, 1))
-    iters = N.I64(0)
-    tres = N.D(0.0)
-    flags = np.zeros(2, dtype=np.int32)
-    N.check(N.lib().hk_gmres(plan.h, front, N.ptr(op.dev), n, N.ptr(bd), cfg.tol, cfg.max_iter,
-                             kind, N.ptr(x), N.C.byref(iters), N.arr_ptr(hist, N.D),
-                             N.C.byref(tres), N.arr_ptr(flags, N.I32), N.stream_handle()))
-    m = iters.value
-    conv = bool(flags[0])
-    if float(np.linalg.norm(b)) == 0.0:
-        return GmresResult(np.zeros(n), 0, True, [0.0], 0.0)
-    if not conv and not flags[1] and tres.value > 10 * cfg.tol and m and hist[m - 1] <= cfg.tol:
-        log.warning("gmres: preconditioned residual converged but true residual %.3e exceeds "
-                    "10*tol; reporting non-convergence", tres.value)
-    return GmresResult(x.cpu().numpy(), m, conv, [float(h) for h in hist[:m]], tres.value,
-                       bool(flags[1]))
+    if op.n != n:
+        raise ValueError(f"operator is {op.n}x{op.n}, rhs has {n} rows")
+    return plan, front, kind, diag
+
+
+def _run_device(op: DenseOperator, Bn: np.ndarray, cfg: GmresConfig, pre) -> list:
+    """hk_gmres_batch on the columns of Bn (n x s): the whole Arnoldi loop runs
+    on the device as one CUDA graph; the host reads the results once."""
+    torch = N.require_cuda()
+    n, s = Bn.shape
+    plan, front, kind, diag = _device_target(op, n, pre)
+    bd = torch.from_numpy(np.ascontiguousarray(Bn.T)).cuda()        # (s, n) = column-major n x s
+    xd = torch.zeros_like(bd)
+    its = np.zeros(s, dtype=np.int64)
+    hist = np.zeros((s, cfg.max_iter))
+    tres = np.zeros(s)
+    flags = np.zeros(2 * s, dtype=np.int32)
+    N.check(N.lib().hk_gmres_batch(plan.h, front, N.ptr(op.dev), op.dev.stride(0), n, N.ptr(bd), s,
+                                   cfg.tol, cfg.max_iter, kind,
+                                   N.ptr(diag) if diag is not None else None, N.ptr(xd),
+                                   N.arr_ptr(its, N.I64), N.arr_ptr(hist, N.D),
+                                   N.arr_ptr(tres, N.D), N.arr_ptr(flags, N.I32),
+                                   N.stream_handle()))
+    xh = xd.cpu().numpy()
+    out = []
+    for c in range(s):
+        m = int(its[c])
+        if not np.any(Bn[:, c]):                 # krylov.py:85-87
+            out.append(GmresResult(np.zeros(n), 0, True, [0.0], 0.0))
+            continue
+        conv, brk = bool(flags[2 * c]), bool(flags[2 * c + 1])
+        if not conv and not brk and tres[c] > 10 * cfg.tol and m and hist[c, m - 1] <= cfg.tol:
+            log.warning("gmres: preconditioned residual converged but true residual %.3e exceeds "
+                        "10*tol; reporting non-convergence", tres[c])
+        out.append(GmresResult(xh[c].copy(), m, conv, [float(h) for h in hist[c, :m]],
+                               float(tres[c]), brk))
+    return out
+
+
+def _gmres_device(op: DenseOperator, b, cfg, pre) -> GmresResult:
+    return _run_device(op, b[:, None], cfg, pre)[0]
 
 
 def _gmres_callables(apply_op, b, cfg, preconditioner) -> GmresResult:
@@ -296,40 +333,16 @@ def gmres_batch(apply_op, B, cfg: GmresConfig, preconditioner=None) -> list:
     flags equal those of gmres() on that column.
     """
     torch = N.require_cuda()
-    from .hodlr import _Plan
     if not isinstance(apply_op, DenseOperator):
         raise TypeError("gmres_batch needs a DenseOperator")
     Bn = B.cpu().numpy() if isinstance(B, torch.Tensor) else np.asarray(B, dtype=np.float64)
-    if Bn.ndim != 2 or Bn.shape[0] != apply_op.n:
+    if Bn.ndim != 2:
         raise ValueError("B must be n x s")
-    n, s = Bn.shape
-    if not 1 <= s <= 16:
+    if not 1 <= Bn.shape[1] <= 16:
         raise ValueError("gmres_batch takes 1..16 right-hand sides")
     pre = preconditioner
     if isinstance(pre, HodlrPreconditioner):
         pre = pre.fact
-    if _is_fact(pre):
-        plan, front, kind = pre.plan, pre.front_index, 1
-    else:
-        plan = getattr(apply_op, "_plan", None)
-        if plan is None:
-            plan = _Plan(n, max(n, 1), 1)
-            apply_op._plan = plan
-        front, kind = 0, 0 if pre is None else 2
-    bd = torch.from_numpy(np.ascontiguousarray(Bn.T)).cuda()        # (s, n) = column-major n x s
-    xd = torch.zeros_like(bd)
-    its = np.zeros(s, dtype=np.int64)
-    hist = np.zeros((s, max(cfg.max_iter, 1)))
-    tres = np.zeros(s)
-    flags = np.zeros(2 * s, dtype=np.int32)
-    N.check(N.lib().hk_gmres_batch(plan.h, front, N.ptr(apply_op.dev), n, N.ptr(bd), s, cfg.tol,
-                                   cfg.max_iter, kind, N.ptr(xd), N.arr_ptr(its, N.I64),
-                                   N.arr_ptr(hist, N.D), N.arr_ptr(tres, N.D),
-                                   N.arr_ptr(flags, N.I32), N.stream_handle()))
-    xh = xd.cpu().numpy()
-    out = []
-    for c in range(s):
-        m = int(its[c])
-        out.append(GmresResult(xh[c].copy(), m, bool(flags[2 * c]), [float(h) for h in hist[c, :m]],
-                               float(tres[c]), bool(flags[2 * c + 1])))
-    return out
+    if not (pre is None or _is_fact(pre) or isinstance(pre, DiagonalPreconditioner)):
+        raise TypeError("gmres_batch takes a HODLR factorization, a DiagonalPreconditioner or None")
+    return _run_device(apply_op, np.asarray(Bn, dtype=np.float64), cfg, pre)
