@@ -70,6 +70,43 @@ def env_rank():
             int(os.environ.get("WORLD_SIZE", 1)))
 
 
+# ---------------------------------------------------------------- rank launch
+def _free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _rank_entry(rank, world, port, target, args):
+    os.environ.update(RANK=str(rank), LOCAL_RANK=str(rank), WORLD_SIZE=str(world),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    rc = target(args)
+    if rc:
+        raise SystemExit(rc)
+
+
+def launch_ranks(world, target, args):
+    """One process per rank when bench.py is started without a launcher
+    (``python bench.py --gpus N``): the same environment torchrun would set
+    (RANK / LOCAL_RANK / WORLD_SIZE / MASTER_ADDR=127.0.0.1 / MASTER_PORT),
+    then ``target(args)`` in every rank.  torch.distributed.run launches
+    (WORLD_SIZE already set) bypass this."""
+    import torch.multiprocessing as mp
+    mp.spawn(_rank_entry, args=(world, _free_port(), target, args), nprocs=world, join=True)
+    return 0
+
+
+def init_dist(backend, device=None):
+    """Process group from the launcher's environment (torchrun or launch_ranks)."""
+    import torch.distributed as dist
+    rank, _, world = env_rank()
+    if world > 1 and not dist.is_initialized():
+        kw = {"device_id": device} if device is not None else {}
+        dist.init_process_group(backend, rank=rank, world_size=world, **kw)
+    return dist
+
+
 def config_dict(args, world):
     return {"workload": "cfg3-batched-level", "fronts_per_gpu": args.fronts_per_gpu,
             "total_fronts": args.fronts_per_gpu * world, "n": 1024, "grid": "32^3 variable-k, plane z=16",
@@ -302,8 +339,7 @@ def run_ours(args):
     rank, local, world = env_rank()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    init_dist("nccl", dev)
     F = args.fronts_per_gpu
     seeds = MF.shard_range(rank, world, F)
     fronts = torch.stack([make_front(s, dev) for s in seeds]).contiguous()
@@ -552,9 +588,8 @@ def run_cfg4(dev, rank, world, hbm_peak):
         _, bf_ms = timed(lambda: sh.factorize(cfg))
         ranks = None
 
-        def solve_all():
-            return [sh.gmres(torch.from_numpy(B[:, j]).to(dev), hk.GmresConfig(tol=1e-10))
-                    for j in range(4)]
+        def solve_all():   # 4 systems in lock step: one sharded GEMV + solve per iteration
+            return sh.gmres_batch(torch.from_numpy(B).to(dev), hk.GmresConfig(tol=1e-10))
     # HBM bytes one GMRES iteration must stream for the operator: the dense front
     per_iter = 8.0 * n * n
     solve_all()                                                  # warm
@@ -603,9 +638,11 @@ def run_cfg4(dev, rank, world, hbm_peak):
            "true_residuals": [r.true_residual for r in res],
            "converged": all(bool(r.converged) for r in res),
            "gemv_bytes_per_iteration": per_iter,
-           "gemv_floor_ms_4rhs": (max(its) if world == 1 else sum(its)) * per_iter / (hbm_peak * 1e9) * 1e3,
-           "gmres_mode": "hk_gmres_batch: 4 systems in lock step" if world == 1 else
-                         "subtree-sharded gmres per rhs",
+           "gemv_floor_ms_4rhs": max(its) * per_iter / (hbm_peak * 1e9) * 1e3 / world,
+           "gmres_mode": "hk_gmres_batch: 4 systems in lock step, one CUDA graph (conditional "
+                         "WHILE node)" if world == 1 else
+                         "subtree-sharded gmres_batch: 4 systems in lock step, row-slab GEMV + "
+                         "sharded solve per iteration (NCCL all-reduce/all-gather)",
            "reference_cpu_1t_s": {"build_factor": 20.2, "gmres_4rhs": 4.76,
                                   "source": "SURVEY.md §6.3 (reference run in the build container)"}}
     if ranks is not None:
@@ -693,9 +730,18 @@ def run_cfg12(dev):
 
 def main():
     args = parse()
-    if args.impl == "reference":
-        return run_reference(args)
-    return run_ours(args)
+    target = run_reference if args.impl == "reference" else run_ours
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        if args.impl == "reference":
+            # only rank 0 of the reference arm does work (the CPU path)
+            os.environ.update(RANK="0", LOCAL_RANK="0", WORLD_SIZE=str(args.gpus))
+            return run_reference(args)
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible")
+        return launch_ranks(args.gpus, target, args)
+    return target(args)
 
 
 if __name__ == "__main__":

@@ -153,13 +153,15 @@ hk_status hk_gj_inverse(const double* A, int64_t n, int64_t lda, int64_t batch, 
                         double* out, int32_t* status_host, void* stream);
 /* Factor views for the test-visible attributes of HodlrFactorization
  * (hodlr.py:105-154): leaf LU (b x b row-major packed, LAPACK-style 0-based
- * swap indices `piv`) and
- * per internal node d_left (na x r_u), d_right (nb x r_l), Schur LU
- * ((r_l+r_u)^2) -- all row-major host copies. */
+ * swap indices `piv`) and per internal node d_left (na x r_u), d_right
+ * (nb x r_l), Schur LU ((r_l+r_u)^2) -- all row-major host copies, computed on
+ * demand by the partial-pivot LU kernel.  inv_host / schur_inv_host (may be
+ * NULL) receive the row-major inverse, which PartialPivLU.solve applies. */
 hk_status hk_get_leaf_lu(hk_plan* plan, int64_t front, int64_t node, double* lu_host,
-                         int32_t* perm_host);
+                         int32_t* perm_host, double* inv_host);
 hk_status hk_get_coupling(hk_plan* plan, int64_t front, int64_t node, double* d_left_host,
-                          double* d_right_host, double* schur_lu_host, int32_t* schur_perm_host);
+                          double* d_right_host, double* schur_lu_host, int32_t* schur_perm_host,
+                          double* schur_inv_host);
 
 /* ------------------------------------------------------------------------
  * Solve (solve, hodlr.py:285-306) in place on device right-hand sides of
@@ -210,6 +212,17 @@ hk_status hk_gmres(hk_plan* plan, int64_t front, const double* A_dev, int64_t ld
 hk_status hk_arnoldi_step(int64_t n, int64_t j, int64_t mmax, double* basis_dev,
                           double* hess_dev, double* cs_dev, double* sn_dev, double* g_dev,
                           double* w_dev, double beta, double* out_host, void* stream);
+/* s systems' column updates in one launch, device-only (no host sync): system
+ * c lives at basis_dev + c*bstride, hess_dev + c*hstride, cs/sn/g_dev +
+ * c*(mmax+1), w_dev + c*n, beta_dev[c]; out_dev[3c..3c+2] = rel, happy,
+ * breakdown; systems with active_dev[c] == 0 are skipped.  Used by the
+ * sharded (multi-GPU) GMRES, whose operator and preconditioner are
+ * collectives, to advance all right-hand sides with one readback per step. */
+hk_status hk_arnoldi_step_batch(int64_t n, int64_t j, int64_t mmax, double* basis_dev,
+                                int64_t bstride, double* hess_dev, int64_t hstride, double* cs_dev,
+                                double* sn_dev, double* g_dev, double* w_dev,
+                                const double* beta_dev, double* out_dev, const int32_t* active_dev,
+                                int64_t s, void* stream);
 /* Back substitution + x = basis[:, :m] y (krylov.py:147-154). */
 hk_status hk_gmres_combine(int64_t n, int64_t m, int64_t mmax, const double* basis_dev,
                            const double* hess_dev, const double* g_dev, double* x_dev,

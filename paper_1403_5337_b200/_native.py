@@ -51,13 +51,14 @@ SIGNATURES = {
     "hk_gmres_batch": (C.c_int, [P, I64, P, I64, I64, P, I64, D, I64, C.c_int, P, P, PI64, PD, PD, PI32, P]),
     "hk_dgemm": (C.c_int, [C.c_int, I64, I64, I64, D, P, I64, P, I64, D, P, I64, P]),
     "hk_gj_inverse": (C.c_int, [P, I64, I64, I64, I64, P, P, P]),
-    "hk_get_leaf_lu": (C.c_int, [P, I64, I64, PD, PI32]),
-    "hk_get_coupling": (C.c_int, [P, I64, I64, PD, PD, PD, PI32]),
+    "hk_get_leaf_lu": (C.c_int, [P, I64, I64, PD, PI32, PD]),
+    "hk_get_coupling": (C.c_int, [P, I64, I64, PD, PD, PD, PI32, PD]),
     "hk_solve": (C.c_int, [P, P, I64, I64, I64, P]),
     "hk_solve_front": (C.c_int, [P, I64, P, I64, I64, P]),
     "hk_gmres": (C.c_int, [P, I64, P, I64, I64, P, D, I64, C.c_int, P, P, PI64, PD, PD, PI32, P]),
     "hk_arnoldi_step": (C.c_int, [I64, I64, I64, P, P, P, P, P, P, D, PD, P]),
     "hk_gmres_combine": (C.c_int, [I64, I64, I64, P, P, P, P, P]),
+    "hk_arnoldi_step_batch": (C.c_int, [I64, I64, I64, P, I64, P, I64, P, P, P, P, P, P, P, I64, P]),
     "hk_gemv": (C.c_int, [P, I64, I64, I64, P, I64, I64, P, I64, P]),
     "hk_lu_full": (C.c_int, [P, I64, I64, I64, P, P, P, PI64, P]),
     "hk_lu_partial": (C.c_int, [P, I64, I64, P, P, P]),

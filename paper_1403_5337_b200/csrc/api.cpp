@@ -1301,7 +1301,7 @@ static hk_status flush(hk_plan* p, std::vector<Op>& ops, cudaStream_t st) {
 }
 
 static hk_status lu_on_demand(const LuTask& proto, int N, double* lu_host, int32_t* piv_host,
-                              int* singular);
+                              int* singular, double* inv_host = nullptr);
 struct SolveProg;
 static hk_status build_solve_prog(hk_plan* p, int front, int s, SolveProg*& out, cudaStream_t st);
 static hk_status ensure_solve_scratch(hk_plan* p, int s, cudaStream_t st);
@@ -1748,10 +1748,12 @@ static void colmajor_to_rowmajor(const std::vector<double>& cm, int64_t rows, in
 // On-demand partial-pivot LU (inspection of leaf_lus / couplings[].schur_lu;
 // the hot path keeps explicit inverses instead).
 static hk_status lu_on_demand(const LuTask& proto, int N, double* lu_host, int32_t* piv_host,
-                              int* singular) {
+                              int* singular, double* inv_host) {
   if (singular) *singular = 0;
   if (N == 0) return HK_OK;
   double* lu = nullptr;
+  double* inv = nullptr;
+  if (inv_host) CU(cudaMalloc(&inv, (size_t)N * N * 8));
   int32_t *ip = nullptr, *pm = nullptr, *stt = nullptr;
   LuTask* td = nullptr;
   CU(cudaMalloc(&lu, (size_t)N * N * 8));
@@ -1760,7 +1762,7 @@ static hk_status lu_on_demand(const LuTask& proto, int N, double* lu_host, int32
   CU(cudaMalloc(&stt, 8));
   CU(cudaMalloc(&td, sizeof(LuTask)));
   LuTask t = proto;
-  t.lu = lu; t.ipiv = ip; t.perm = pm; t.status = stt; t.inv = nullptr; t.N = N;
+  t.lu = lu; t.ipiv = ip; t.perm = pm; t.status = stt; t.inv = inv; t.N = N;
   CU(cudaMemcpy(td, &t, sizeof(LuTask), cudaMemcpyHostToDevice));
   CU(hk_launch_lu(td, 1, N, 0));
   if (lu_host) {
@@ -1773,11 +1775,19 @@ static hk_status lu_on_demand(const LuTask& proto, int N, double* lu_host, int32
   int32_t sg = 0;
   CU(cudaMemcpy(&sg, stt, 4, cudaMemcpyDeviceToHost));
   if (singular) *singular = sg != 0;
+  if (inv_host && !sg) {   // column-major inverse -> row-major host copy
+    std::vector<double> h((size_t)N * N);
+    CU(cudaMemcpy(h.data(), inv, h.size() * 8, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j < N; ++j) inv_host[(int64_t)i * N + j] = h[i + (int64_t)j * N];
+  }
+  if (inv) cudaFree(inv);
   cudaFree(lu); cudaFree(ip); cudaFree(pm); cudaFree(stt); cudaFree(td);
   return HK_OK;
 }
 
-extern "C" hk_status hk_get_leaf_lu(hk_plan* p, int64_t f, int64_t slot, double* lu, int32_t* perm) {
+extern "C" hk_status hk_get_leaf_lu(hk_plan* p, int64_t f, int64_t slot, double* lu, int32_t* perm,
+                                    double* inv) {
   if (!p || !p->factored) return fail(HK_ERR_STATE, "plan not factored");
   const Node& nd = p->nodes[slot];
   if (nd.left >= 0) return fail(HK_ERR_VALUE, "not a leaf");
@@ -1785,11 +1795,11 @@ extern "C" hk_status hk_get_leaf_lu(hk_plan* p, int64_t f, int64_t slot, double*
   t.src = p->A + f * p->fstride + nd.lo * p->lda + nd.lo;
   t.src_ld = p->lda;
   t.mode = 0;
-  return lu_on_demand(t, (int)(nd.hi - nd.lo), lu, perm, nullptr);
+  return lu_on_demand(t, (int)(nd.hi - nd.lo), lu, perm, nullptr, inv);
 }
 
 extern "C" hk_status hk_get_coupling(hk_plan* p, int64_t f, int64_t slot, double* dl, double* dr,
-                                     double* slu, int32_t* sperm) {
+                                     double* slu, int32_t* sperm, double* sinv) {
   if (!p || !p->factored) return fail(HK_ERR_STATE, "plan not factored");
   const Node& nd = p->nodes[slot];
   if (nd.left < 0) return fail(HK_ERR_VALUE, "not an internal node");
@@ -1818,7 +1828,7 @@ extern "C" hk_status hk_get_coupling(hk_plan* p, int64_t f, int64_t slot, double
     t.rl = r.rl;
     t.ru = r.ru;
     t.h_col0 = r.w;
-    CHK(lu_on_demand(t, r.R, slu, sperm, nullptr));
+    CHK(lu_on_demand(t, r.R, slu, sperm, nullptr, sinv));
   }
   return HK_OK;
 }
@@ -2503,6 +2513,23 @@ extern "C" hk_status hk_arnoldi_step(int64_t n, int64_t j, int64_t mmax, double*
   CU(cudaMemcpyAsync(out_host, outd, 24, cudaMemcpyDeviceToHost, st));
   CU(cudaFreeAsync(outd, st));
   CU(cudaStreamSynchronize(st));
+  return HK_OK;
+}
+
+// s systems' Arnoldi steps in one launch (one CTA each), device-only: the
+// caller reads out_dev (3 doubles per system) once per iteration for all of
+// them.  System c: basis + c*bstride (n x (mmax+1)), hess + c*hstride,
+// cs/sn/g + c*(mmax+1), w + c*n, beta_dev[c]; systems with active_dev[c] == 0
+// are skipped.
+extern "C" hk_status hk_arnoldi_step_batch(int64_t n, int64_t j, int64_t mmax, double* basis,
+                                           int64_t bstride, double* hess, int64_t hstride,
+                                           double* cs, double* sn, double* g, double* w,
+                                           const double* beta_dev, double* out_dev,
+                                           const int32_t* active_dev, int64_t s, void* stream) {
+  if (s < 1 || s > 1024) return fail(HK_ERR_VALUE, "1..1024 systems");
+  if (j < 0 || j >= mmax) return fail(HK_ERR_VALUE, "column index out of range");
+  CU(hk_launch_arnoldi_batch(n, j, mmax, basis, bstride, hess, hstride, cs, sn, g, w, beta_dev,
+                             out_dev, active_dev, (int)s, (cudaStream_t)stream));
   return HK_OK;
 }
 

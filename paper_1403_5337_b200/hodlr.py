@@ -251,11 +251,12 @@ class HodlrFactorization:
             return None
         b = node.size
         lu = np.zeros((b, b))
+        inv = np.zeros((b, b))
         piv = np.zeros(b, dtype=np.int32)
         N.check(N.lib().hk_get_leaf_lu(self._plan.h, self._f, slot, N.arr_ptr(lu, N.D),
-                                       N.arr_ptr(piv, N.I32)))
+                                       N.arr_ptr(piv, N.I32), N.arr_ptr(inv, N.D)))
         piv = piv.astype(np.intp)
-        return PartialPivLU(lu, piv, _row_perm_from_piv(piv), None)
+        return PartialPivLU(lu, piv, _row_perm_from_piv(piv), inv)
 
     def block_factor(self, block):
         m, n, cap = N.I64(), N.I64(), N.I64()
@@ -282,12 +283,13 @@ class HodlrFactorization:
         dl = np.zeros((na, ru))
         dr = np.zeros((nb, rl))
         slu = np.zeros((R, R))
+        sinv = np.zeros((R, R))
         sp = np.zeros(max(R, 1), dtype=np.int32)
         N.check(N.lib().hk_get_coupling(self._plan.h, self._f, slot, N.arr_ptr(dl, N.D),
                                         N.arr_ptr(dr, N.D), N.arr_ptr(slu, N.D),
-                                        N.arr_ptr(sp, N.I32)))
+                                        N.arr_ptr(sp, N.I32), N.arr_ptr(sinv, N.D)))
         piv = sp[:R].astype(np.intp)
-        return Coupling(v_up, v_low, dl, dr, PartialPivLU(slu, piv, _row_perm_from_piv(piv), None))
+        return Coupling(v_up, v_low, dl, dr, PartialPivLU(slu, piv, _row_perm_from_piv(piv), sinv))
 
     # device-side application (used by solve and the GMRES preconditioner)
     def solve_device(self, x, in_place=True):

@@ -265,62 +265,98 @@ def _gmres_callables(apply_op, b, cfg, preconditioner) -> GmresResult:
 
 
 def gmres_device(apply_op, b, cfg: GmresConfig, preconditioner=None) -> GmresResult:
-    """gmres() with callables that take and return CUDA tensors (no host round
-    trip per iteration): the sharded operator / preconditioner of
-    subtree.ShardedHodlr.  Same algorithm and flags as gmres()."""
+    """gmres() with callables on CUDA tensors (the sharded operator and
+    preconditioner of subtree.ShardedHodlr): ``gmres_device_batch`` with one
+    column."""
     torch = N.require_cuda()
     bd = b if isinstance(b, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(b))
-    bd = bd.to(device="cuda", dtype=torch.float64).contiguous()
-    n = bd.numel()
-    M = (lambda r: r) if preconditioner is None else preconditioner
-    norm_b = float(torch.linalg.vector_norm(bd))
-    if norm_b == 0.0:
-        return GmresResult(np.zeros(n), 0, True, [0.0], 0.0)
-    r0 = M(bd).contiguous()
-    beta = float(torch.linalg.vector_norm(r0))
-    if beta == 0.0:
+    bd = bd.to(device="cuda", dtype=torch.float64).reshape(1, -1)
+    return gmres_device_batch(lambda X: apply_op(X[0])[None],
+                              bd, cfg, None if preconditioner is None else
+                              (lambda X: preconditioner(X[0])[None]))[0]
+
+
+def gmres_device_batch(apply_op, B, cfg: GmresConfig, preconditioner=None) -> list:
+    """s GMRES systems in lock step with callables that map an (s, n) CUDA
+    tensor (row c = the vector of system c) to (s, n): the sharded operator and
+    preconditioner, whose collectives then carry all s columns at once.  The
+    Arnoldi steps of all systems run in one launch (hk_arnoldi_step_batch) and
+    the host reads their three flags once per iteration.  Same algorithm,
+    flags and results per system as gmres() (krylov.py:69-166)."""
+    torch = N.require_cuda()
+    Bd = B.to(device="cuda", dtype=torch.float64).contiguous()
+    s, n = Bd.shape
+    M = (lambda X: X) if preconditioner is None else preconditioner
+    norm_b = torch.linalg.vector_norm(Bd, dim=1).cpu().numpy()
+    zero = norm_b == 0.0
+    R0 = M(Bd).contiguous()
+    beta = torch.linalg.vector_norm(R0, dim=1)
+    bh = beta.cpu().numpy()
+    if np.any((bh == 0.0) & ~zero):
         raise GmresBreakdownError("preconditioned rhs is exactly zero")
     mmax = min(cfg.max_iter, n)
-    basis = torch.zeros((mmax + 1, n), dtype=torch.float64, device="cuda")
-    hess = torch.zeros((mmax, mmax + 1), dtype=torch.float64, device="cuda")
-    cs = torch.zeros(mmax, dtype=torch.float64, device="cuda")
-    sn = torch.zeros(mmax, dtype=torch.float64, device="cuda")
-    g = torch.zeros(mmax + 1, dtype=torch.float64, device="cuda")
-    basis[0] = r0 / beta
-    g[0] = beta
-    out = np.zeros(3)
-    history = []
-    converged = breakdown = False
-    k = 0
+    vs = mmax + 1
+    basis = torch.zeros((s, vs, n), dtype=torch.float64, device="cuda")
+    hess = torch.zeros((s, mmax, vs), dtype=torch.float64, device="cuda")
+    cs = torch.zeros((s, vs), dtype=torch.float64, device="cuda")
+    sn = torch.zeros((s, vs), dtype=torch.float64, device="cuda")
+    g = torch.zeros((s, vs), dtype=torch.float64, device="cuda")
+    safe = torch.where(beta == 0.0, torch.ones_like(beta), beta)
+    basis[:, 0] = R0 / safe[:, None]
+    g[:, 0] = beta
+    active = ~zero
+    act_d = torch.from_numpy(active.astype(np.int32)).cuda()
+    out = torch.zeros((s, 3), dtype=torch.float64, device="cuda")
+    hist = [[] for _ in range(s)]
+    m = np.zeros(s, dtype=np.int64)
+    conv = zero.copy()
+    brk = np.zeros(s, dtype=bool)
     L = N.lib()
     st = N.stream_handle()
+    k = 0
     for k in range(1, mmax + 1):
+        if not active.any():
+            break
         j = k - 1
-        w = M(apply_op(basis[j])).contiguous()
-        N.check(L.hk_arnoldi_step(n, j, mmax, N.ptr(basis), N.ptr(hess), N.ptr(cs), N.ptr(sn),
-                                  N.ptr(g), N.ptr(w), beta, N.arr_ptr(out, N.D), st))
-        if out[2] != 0.0:
-            breakdown = True
-            break
-        history.append(float(out[0]))
-        if out[0] <= cfg.tol or out[1] != 0.0:
-            converged = True
-            break
-    m = k if not breakdown else k - 1
-    x = torch.zeros(n, dtype=torch.float64, device="cuda")
-    if m > 0:
-        N.check(L.hk_gmres_combine(n, m, mmax, N.ptr(basis), N.ptr(hess), N.ptr(g), N.ptr(x), st))
-    tres = float(torch.linalg.vector_norm(bd - apply_op(x)) / norm_b)
-    if breakdown and tres > 10.0 * cfg.tol:
-        raise GmresBreakdownError(
-            f"Arnoldi norm underflow at iteration {k} with true residual {tres:.3e}")
-    if converged and tres > 10.0 * cfg.tol:
-        log.warning("gmres: preconditioned residual converged but true residual %.3e exceeds "
-                    "10*tol; reporting non-convergence", tres)
-        converged = False
-    if breakdown:
-        converged = True
-    return GmresResult(x.cpu().numpy(), m, converged, history, tres, breakdown)
+        W = M(apply_op(basis[:, j].contiguous())).contiguous()
+        N.check(L.hk_arnoldi_step_batch(n, j, mmax, N.ptr(basis), vs * n, N.ptr(hess), mmax * vs,
+                                        N.ptr(cs), N.ptr(sn), N.ptr(g), N.ptr(W), N.ptr(beta),
+                                        N.ptr(out), N.ptr(act_d), s, st))
+        o = out.cpu().numpy()                   # the one host round trip of the iteration
+        for c in np.flatnonzero(active):
+            if o[c, 2] != 0.0:
+                brk[c], m[c], active[c] = True, k - 1, False
+                continue
+            hist[c].append(float(o[c, 0]))
+            m[c] = k
+            if o[c, 0] <= cfg.tol or o[c, 1] != 0.0:
+                conv[c], active[c] = True, False
+        act_d.copy_(torch.from_numpy(active.astype(np.int32)))
+    X = torch.zeros((s, n), dtype=torch.float64, device="cuda")
+    for c in range(s):
+        if m[c] > 0 and not zero[c]:
+            N.check(L.hk_gmres_combine(n, int(m[c]), mmax, N.ptr(basis[c]), N.ptr(hess[c]),
+                                       N.ptr(g[c]), N.ptr(X[c]), st))
+    tres = (torch.linalg.vector_norm(Bd - apply_op(X), dim=1).cpu().numpy()
+            / np.where(zero, 1.0, norm_b))
+    results = []
+    for c in range(s):
+        if zero[c]:
+            results.append(GmresResult(np.zeros(n), 0, True, [0.0], 0.0))
+            continue
+        tr = float(tres[c])
+        if brk[c] and tr > 10.0 * cfg.tol:
+            raise GmresBreakdownError(
+                f"rhs {c}: Arnoldi norm underflow at iteration {m[c] + 1} with true residual {tr:.3e}")
+        cv = bool(conv[c])
+        if cv and tr > 10.0 * cfg.tol:
+            log.warning("gmres: preconditioned residual converged but true residual %.3e exceeds "
+                        "10*tol; reporting non-convergence", tr)
+            cv = False
+        if brk[c]:
+            cv = True
+        results.append(GmresResult(X[c].cpu().numpy(), int(m[c]), cv, hist[c], tr, bool(brk[c])))
+    return results
 
 
 def gmres_batch(apply_op, B, cfg: GmresConfig, preconditioner=None) -> list:

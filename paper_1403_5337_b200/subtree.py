@@ -58,7 +58,7 @@ class EmulatedRanks:
         return {r: (total if i == 0 else total.clone())
                 for i, r in enumerate(r for r in sorted(group) if r in parts)}
 
-    def allgather(self, parts: dict) -> list:
+    def allgather(self, parts: dict, sizes=None) -> list:
         return [parts[r] for r in range(self.world)]
 
     def broadcast(self, value, owner: int):
@@ -92,19 +92,18 @@ class TorchDistRanks:
         self.dist.all_reduce(t, group=self.groups.get(key))
         return {self.rank: t}
 
-    def allgather(self, parts: dict) -> list:
+    def allgather(self, parts: dict, sizes) -> list:
+        """Gather every rank's (s, sizes[r]) block.  The sizes come from the
+        tree (every rank knows them), so nothing but the data crosses ranks:
+        one all_gather of blocks padded to the largest size."""
         import torch
         t = parts[self.rank]
-        n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
-        sizes = [torch.zeros_like(n) for _ in range(self.world)]
-        self.dist.all_gather(sizes, n)
-        sizes = [int(s.item()) for s in sizes]
-        m = max(sizes)
-        pad = torch.zeros((m,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-        pad[: t.shape[0]] = t
+        width = max(sizes)
+        pad = t.new_zeros(t.shape[:-1] + (width,))
+        pad[..., : t.shape[-1]] = t
         outs = [torch.empty_like(pad) for _ in range(self.world)]
         self.dist.all_gather(outs, pad)
-        return [o[:k] for o, k in zip(outs, sizes)]
+        return [o[..., :k] for o, k in zip(outs, sizes)]
 
     def broadcast(self, value, owner: int):
         """value: tuple of fp64 tensors on the owner (None elsewhere); returns it everywhere."""
@@ -188,9 +187,10 @@ class GpuBackend:
         return E
 
     def solve_local_(self, x):
+        """x: (s, n_loc) contiguous = column-major n_loc x s; solved in place."""
         N = self.N
-        N.check(N.lib().hk_solve(self.plan.h, N.ptr(x), x.shape[0], 1, x.shape[0],
-                                 N.stream_handle()))
+        s, nl = x.shape
+        N.check(N.lib().hk_solve(self.plan.h, N.ptr(x), nl, s, nl * s, N.stream_handle()))
         return x
 
     def gemm(self, C, A, B, trans_a=False, alpha=1.0, beta=0.0):
@@ -225,13 +225,15 @@ class GpuBackend:
             raise SingularSchurError(f"top-level coupling system singular: {exc}") from exc
         return inv.t().contiguous()            # row-major inverse -> cm
 
-    def rows_matvec(self, x):
-        """A[lo:hi, :] x (row slab of the dense front)."""
+    def rows_matvec(self, X):
+        """A[lo:hi, :] X for X (s, n) (row slab of the dense front); (s, rows)."""
         N, torch = self.N, self.torch
-        y = torch.empty(self.hi - self.lo, dtype=torch.float64, device="cuda")
+        s = X.shape[0]
+        rows = self.hi - self.lo
+        y = torch.empty((s, rows), dtype=torch.float64, device="cuda")
         a = self.front[self.lo:]
-        N.check(N.lib().hk_gemv(N.ptr(a), self.n, self.hi - self.lo, self.n, N.ptr(x), self.n, 1,
-                                N.ptr(y), self.hi - self.lo, N.stream_handle()))
+        N.check(N.lib().hk_gemv(N.ptr(a), self.n, rows, self.n, N.ptr(X), self.n, s,
+                                N.ptr(y), rows, N.stream_handle()))
         return y
 
 
@@ -393,18 +395,31 @@ class ShardedHodlr:
         return self
 
     # solve ---------------------------------------------------------------------
+    def _sizes(self):
+        return [self.tree.nodes[self.owned[r]].size for r in range(self.G)]
+
     def solve(self, x):
         """HODLR solve of a full (n,) right-hand side; returns the full solution."""
-        if not self._factored:
-            raise RuntimeError("solve requires factorize()")
         if x.shape != (self.n,):
             raise DimensionMismatchError(f"rhs has shape {tuple(x.shape)}, expected ({self.n},)")
+        return self.solve_batch(x[None])[0]
+
+    def solve_batch(self, X):
+        """HODLR solve of s right-hand sides X (s, n) (row c = rhs c); (s, n).
+        Per top node one all-reduce of the R x s projection V^T x."""
+        if not self._factored:
+            raise RuntimeError("solve requires factorize()")
+        if X.dim() != 2 or X.shape[1] != self.n:
+            raise DimensionMismatchError(f"rhs has shape {tuple(X.shape)}, expected (s, {self.n})")
         torch = self._torch()
         hosted = self.comm.hosted
+        s = X.shape[0]
         xl = {}
         for r in hosted:
             nd = self.tree.nodes[self.owned[r]]
-            xl[r] = self.local[r].solve_local_(x[nd.lo:nd.hi].clone())
+            xr = torch.empty((s, nd.hi - nd.lo), dtype=torch.float64, device=X.device)
+            xr.copy_(X[:, nd.lo:nd.hi])           # a private copy: solved in place
+            xl[r] = self.local[r].solve_local_(xr)
         for level in range(self.g - 1, -1, -1):
             for top in [t for t in self.tops if t.node.level == level]:
                 group = self.ranks_under(top.node)
@@ -417,39 +432,52 @@ class ShardedHodlr:
                 for r in mine:
                     _, side, w, _ = next(p for p in self._path(r) if p[0] is top)
                     nd = self.tree.nodes[self.owned[r]]
-                    gp = torch.zeros((1, R), dtype=torch.float64, device=self.front.device)
+                    gp = torch.zeros((s, R), dtype=torch.float64, device=self.front.device)
                     if side == 0 and rl > 0:
                         Vl = top.Vl[:, nd.lo - top.a.lo: nd.hi - top.a.lo]
-                        self.local[r].gemm(gp[:, 0:rl], Vl, xl[r][None, :], trans_a=True)
+                        self.local[r].gemm(gp[:, 0:rl], Vl, xl[r], trans_a=True)
                     if side == 1 and ru > 0:
                         Vu = top.Vu[:, nd.lo - top.b.lo: nd.hi - top.b.lo]
-                        self.local[r].gemm(gp[:, rl:R], Vu, xl[r][None, :], trans_a=True)
+                        self.local[r].gemm(gp[:, rl:R], Vu, xl[r], trans_a=True)
                     parts[r] = gp
                 full = self.comm.allreduce(parts, group)
                 for r in mine:
                     _, side, w, _ = next(p for p in self._path(r) if p[0] is top)
-                    y = torch.empty((1, R), dtype=torch.float64, device=self.front.device)
+                    y = torch.empty((s, R), dtype=torch.float64, device=self.front.device)
                     self.local[r].gemm(y, top.Sinv[r], full[r])
                     E = self.E[r]
                     if side == 0 and ru > 0:
-                        self.local[r].gemm(xl[r][None, :], E[w:w + ru], y[:, rl:R].contiguous(),
+                        self.local[r].gemm(xl[r], E[w:w + ru], y[:, rl:R].contiguous(),
                                            alpha=-1.0, beta=1.0)
                     if side == 1 and rl > 0:
-                        self.local[r].gemm(xl[r][None, :], E[w:w + rl], y[:, 0:rl].contiguous(),
+                        self.local[r].gemm(xl[r], E[w:w + rl], y[:, 0:rl].contiguous(),
                                            alpha=-1.0, beta=1.0)
-        return torch.cat(self.comm.allgather(xl))
+        return torch.cat(self.comm.allgather(xl, self._sizes()), dim=1)
 
     def apply(self, x):
         """Dense product A x with row-slab ownership (src/cli.py:320-321)."""
+        return self.apply_batch(x[None])[0]
+
+    def apply_batch(self, X):
+        """A X for X (s, n): each rank multiplies its row slab, one all-gather."""
         torch = self._torch()
-        parts = {r: self.local[r].rows_matvec(x) for r in self.comm.hosted}
-        return torch.cat(self.comm.allgather(parts))
+        X = X.contiguous()
+        parts = {r: self.local[r].rows_matvec(X) for r in self.comm.hosted}
+        return torch.cat(self.comm.allgather(parts, self._sizes()), dim=1)
 
     def gmres(self, b, cfg: GmresConfig) -> GmresResult:
         """Left-preconditioned GMRES with the sharded operator and preconditioner;
         the Arnoldi step runs redundantly on the replicated Krylov vectors."""
-        from .krylov import gmres_device
-        return gmres_device(self.apply, b, cfg, self.solve)
+        return self.gmres_batch(b.reshape(-1, 1), cfg)[0]
+
+    def gmres_batch(self, B, cfg: GmresConfig) -> list:
+        """GMRES for the columns of B (n x s) in lock step: per iteration one
+        sharded GEMV and one sharded solve carry all s columns, so the
+        collectives per iteration do not grow with s."""
+        from .krylov import gmres_device_batch
+        torch = self._torch()
+        Bt = B.t() if isinstance(B, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(np.asarray(B).T))
+        return gmres_device_batch(self.apply_batch, Bt.to(self.front.device), cfg, self.solve_batch)
 
     def _torch(self):
         import torch

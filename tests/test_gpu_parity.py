@@ -404,6 +404,16 @@ def test_subtree_sharded_matches_single_gpu(G):
     assert res_sh.converged and res_1.converged
     assert abs(res_sh.iterations - res_1.iterations) <= 1
     assert np.linalg.norm(res_sh.x - res_1.x) / np.linalg.norm(res_1.x) < 1e-9
+    # 3 right-hand sides in lock step (one sharded GEMV + solve per iteration)
+    B = np.random.default_rng(12).standard_normal((n, 3))
+    bat_sh = sh.gmres_batch(torch.from_numpy(B).cuda(), hk.GmresConfig(tol=1e-10))
+    bat_1 = hk.gmres_batch(hk.DenseOperator(front), B, hk.GmresConfig(tol=1e-10), preconditioner=fact)
+    for c in range(3):
+        assert bat_sh[c].converged and abs(bat_sh[c].iterations - bat_1[c].iterations) <= 1
+        assert np.linalg.norm(bat_sh[c].x - bat_1[c].x) / np.linalg.norm(bat_1[c].x) < 1e-9
+    Xs = sh.solve_batch(torch.from_numpy(B.T.copy()).cuda()).cpu().numpy()
+    X1 = hk.solve(fact, B).T
+    assert np.linalg.norm(Xs - X1) / np.linalg.norm(X1) < SOLVE_RTOL
 
 
 def test_gmres_batch_matches_single_rhs_runs():

@@ -39,8 +39,8 @@ class DenseCpuBackend:
     def factor_ext(self, Z):
         return (self.Kinv @ Z.T).T.contiguous()
 
-    def solve_local_(self, x):
-        x[:] = self.Kinv @ x
+    def solve_local_(self, x):                  # x: (s, n_loc)
+        x[:] = (self.Kinv @ x.T).T
         return x
 
     def gemm(self, C, A, B, trans_a=False, alpha=1.0, beta=0.0):
@@ -52,8 +52,8 @@ class DenseCpuBackend:
     def inverse(self, S):
         return torch.linalg.inv(S.T).T.contiguous()
 
-    def rows_matvec(self, x):
-        return self.front[self.lo:self.hi] @ x
+    def rows_matvec(self, X):                   # X: (s, n) -> (s, rows)
+        return (self.front[self.lo:self.hi] @ X.T).T
 
 
 def _front():
@@ -71,6 +71,17 @@ def _run(comm, front, b):
     return sh.solve(b), sh.apply(b)
 
 
+def _run_batch(comm, front, B):
+    """s = 3 right-hand sides through one sharded sweep / GEMV (rows = rhs)."""
+    sh = ST.ShardedHodlr(front, LEAF, comm, backend_factory=DenseCpuBackend)
+    sh.factorize(CFG)
+    return sh.solve_batch(B), sh.apply_batch(B)
+
+
+def _rhs3(n):
+    return torch.from_numpy(np.random.default_rng(8).standard_normal((3, n)))
+
+
 @pytest.mark.parametrize("G", [2, 4])
 def test_emulated_ranks_match_dense_solve(G):
     front = _front()
@@ -80,6 +91,11 @@ def test_emulated_ranks_match_dense_solve(G):
     # top-level blocks compressed at 1e-12, subtrees exact: the sharded HODLR inverse is exact
     assert float(torch.linalg.vector_norm(x - exact) / torch.linalg.vector_norm(exact)) < 1e-9
     assert torch.allclose(ax, front @ b, rtol=0, atol=1e-12)
+    B = _rhs3(front.shape[0])
+    X, AX = _run_batch(ST.EmulatedRanks(G), front, B)
+    exact = torch.linalg.solve(front, B.T).T
+    assert float(torch.linalg.vector_norm(X - exact) / torch.linalg.vector_norm(exact)) < 1e-9
+    assert torch.allclose(AX, B @ front.T, rtol=0, atol=1e-12)
 
 
 def test_emulated_rejects_shallow_trees():
@@ -104,7 +120,8 @@ def _worker(rank, world, port, out):
         front = _front()
         b = torch.from_numpy(np.random.default_rng(7).standard_normal(front.shape[0]))
         x, ax = _run(ST.TorchDistRanks(1), front, b)
-        out[rank] = (x.numpy().tolist(), ax.numpy().tolist())
+        X, AX = _run_batch(ST.TorchDistRanks(1), front, _rhs3(front.shape[0]))
+        out[rank] = (x.numpy().tolist(), ax.numpy().tolist(), X.numpy().tolist(), AX.numpy().tolist())
     finally:
         dist.destroy_process_group()
 
@@ -120,6 +137,9 @@ def test_two_rank_gloo_matches_emulated():
     front = _front()
     b = torch.from_numpy(np.random.default_rng(7).standard_normal(front.shape[0]))
     x_em, ax_em = _run(ST.EmulatedRanks(2), front, b)
+    X_em, AX_em = _run_batch(ST.EmulatedRanks(2), front, _rhs3(front.shape[0]))
     for r in range(world):
         assert np.array_equal(np.array(res[r][0]), x_em.numpy()), r   # same sums, same bits
         assert np.array_equal(np.array(res[r][1]), ax_em.numpy()), r
+        assert np.array_equal(np.array(res[r][2]), X_em.numpy()), r
+        assert np.array_equal(np.array(res[r][3]), AX_em.numpy()), r
