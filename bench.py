@@ -62,6 +62,11 @@ def parse():
     ap.add_argument("--no-cfg12", action="store_true",
                     help="skip the BASELINE config-1 (48^3 BDLR) and config-2 (kNN slab, ACA vs "
                          "BDLR) line items")
+    ap.add_argument("--no-cfg0", action="store_true",
+                    help="skip the BASELINE config-0 line item (32^3 front, GMRES to 1e-12)")
+    ap.add_argument("--level-fronts", type=int, default=512,
+                    help="fronts of the whole-level line item at N=1 (BASELINE config 3's 512; "
+                         "0 skips it)")
     return ap.parse_args()
 
 
@@ -517,6 +522,19 @@ def run_ours(args):
         except Exception as exc:
             c1 = c2 = {"error": repr(exc)[:400]}
 
+    # ---- BASELINE config 0 (GMRES to 1e-12) and the whole 512-front level at N = 1
+    c0 = lvl = None
+    if not args.no_cfg0 and rank == 0:
+        try:
+            c0 = run_cfg0(dev)
+        except Exception as exc:
+            c0 = {"error": repr(exc)[:400]}
+    if args.level_fronts > 0 and world == 1:
+        try:
+            lvl = run_level(dev, args.level_fronts, stream)
+        except Exception as exc:
+            lvl = {"error": repr(exc)[:400]}
+
     # per-front ranks of every rank's fronts (the one end-of-run gather)
     all_ranks = MF.gather_front_scalars(batch.ranks.astype(np.int64), device=dev)
     if rank == 0:
@@ -526,7 +544,8 @@ def run_ours(args):
                 "data": "synthetic", "config": config_dict(args, world), "impl": "ours",
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roof,
                 "rooflines": rooflines,
-                "cpu_baseline": cpu, "gmres": gm, "cfg4": c4, "cfg1": c1, "cfg2": c2,
+                "cpu_baseline": cpu, "gmres": gm, "cfg0": c0, "level": lvl, "cfg4": c4,
+                "cfg1": c1, "cfg2": c2,
                 "ranks_per_level_front0": [e["max_rank"] for e in batch.report(0).ranks_per_level],
                 "fronts_gathered": int(all_ranks.shape[0]),
                 "max_block_rank_all_fronts": int(all_ranks.max())}
@@ -652,9 +671,12 @@ def run_cfg4(dev, rank, world, hbm_peak):
     return out
 
 
-def _single_front_item(dev, A, graph, schemes, leaf, gmres_tol, rhs_seed):
-    """Warm build+factor (CUDA events), GMRES time-to-tol, ranks, and the CPU
-    oracle's build+factor on the same front (1 thread), per scheme."""
+def _single_front_item(dev, A, graph, schemes, leaf, gmres_tol, rhs_seed, tol=1e-4):
+    """Cold and warm build+factor (CUDA events), GMRES time-to-tol, ranks, and
+    the CPU oracle's build+factor on the same front (1 thread), per scheme.
+    Cold = the first factorize of a fresh HodlrBatch (planning, allocation
+    and, for BDLR, the GPU graph-distance selection, which a plan caches per
+    graph); warm = the same plan again (selection cached)."""
     import time
     import torch
     import paper_1403_5337_b200 as hk
@@ -668,10 +690,16 @@ def _single_front_item(dev, A, graph, schemes, leaf, gmres_tol, rhs_seed):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     out = {}
     for scheme, depth in schemes:
-        cfg = hk.CompressionConfig(scheme, tol=1e-4, depth=depth)
-        batch = HodlrBatch(n, leaf, 1)
+        cfg = hk.CompressionConfig(scheme, tol=tol, depth=depth)
         g = csr if scheme == "bdlr" else None
-        batch.factorize(Ad[None], cfg, graph=g)                 # warm
+        HodlrBatch(n, leaf, 1).factorize(Ad[None], cfg, graph=g)   # module / allocator warm-up
+        torch.cuda.synchronize()
+        batch = HodlrBatch(n, leaf, 1)
+        ev[0].record()
+        batch.factorize(Ad[None], cfg, graph=g)                 # cold: fresh plan and selection
+        ev[1].record()
+        torch.cuda.synchronize()
+        cold_ms = ev[0].elapsed_time(ev[1])
         ms = []
         for _ in range(3):
             torch.cuda.synchronize()
@@ -690,14 +718,71 @@ def _single_front_item(dev, A, graph, schemes, leaf, gmres_tol, rhs_seed):
         gm_ms = (time.perf_counter() - t0) * 1e3
         _limit_blas()
         t1 = time.perf_counter()
-        O.factorize(A, leaf, scheme, 1e-4, depth, None, csr)
+        O.factorize(A, leaf, scheme, tol, depth, None, csr)
         cpu_s = time.perf_counter() - t1
         key = scheme if scheme == "aca" else f"bdlr_d{depth}"
-        out[key] = {"build_factor_ms": min(ms), "gmres_time_to_tol_ms": gm_ms,
+        out[key] = {"build_factor_ms": min(ms), "build_factor_cold_ms": cold_ms,
+                    "gmres_time_to_tol_ms": gm_ms,
                     "iterations": res.iterations, "converged": bool(res.converged),
                     "true_residual": res.true_residual,
                     "max_rank_per_level": [lv["max_rank"] for lv in batch.report(0).ranks_per_level],
                     "cpu_oracle_build_factor_s_1t": cpu_s}
+    return out
+
+
+def run_cfg0(dev):
+    """BASELINE config 0: the constant-coefficient 32^3 front (plane z=16,
+    n = 1024), ACA 1e-6, leaf 64, GMRES to 1e-12 on default_rng(0)."""
+    from paper_1403_5337_b200 import frontgen as fg
+    A0 = fg.layered_grid_front(DIMS, 2, PLANE, device=dev)
+    return {"workload": "cfg0: 32^3 constant-coefficient front, plane z=16, n=1024, ACA 1e-6, "
+                        "leaf 64, GMRES 1e-12, rhs default_rng(0)",
+            **_single_front_item(dev, A0, None, [("aca", 1)], LEAF, 1e-12, 0, tol=TOL),
+            "reference_cpu_1t_s": {"build_factor": 0.50, "gmres_to_1e-12": 0.014,
+                                   "gmres_iterations": 4, "max_rank_per_level": [78, 78, 79, 64],
+                                   "source": "SURVEY.md §6.3 (reference run in the build container)"}}
+
+
+def run_level(dev, nfronts, stream):
+    """The whole BASELINE config-3 level on one GPU: `nfronts` (512) fronts in
+    one HodlrBatch, build+factor+solve per step, CUDA-event timed over 3 steps
+    after one warm-up.  Front generation is input manufacture, not timed."""
+    import time
+    import torch
+    import paper_1403_5337_b200 as hk
+    from paper_1403_5337_b200.hodlr import HodlrBatch
+    t0 = time.perf_counter()
+    fronts = torch.empty(nfronts, 1024, 1024, dtype=torch.float64, device=dev)
+    for s in range(nfronts):
+        fronts[s] = make_front(s, dev)
+    rhs = torch.from_numpy(np.stack([rhs_for(s, 1024) for s in range(nfronts)])).to(dev)
+    gen_s = time.perf_counter() - t0
+    work = torch.empty_like(rhs)
+    cfg = hk.CompressionConfig(scheme="aca", tol=TOL)
+    batch = HodlrBatch(1024, LEAF, nfronts)
+
+    def step():
+        batch.factorize(fronts, cfg)
+        work.copy_(rhs)
+        batch.solve_(work)
+    step()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    steps = 3
+    aca = 0.0
+    ev[0].record(stream)
+    for _ in range(steps):
+        step()
+        aca += batch.plan.aca_seconds()
+    ev[1].record(stream)
+    torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1]) / steps
+    out = {"workload": f"cfg3 whole level on 1 GPU: {nfronts} fronts in one batch (seeds "
+                       f"0..{nfronts - 1}), build+factor+solve", "fronts": nfronts,
+           "value": nfronts / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "steps": steps,
+           "aca_ms": 1e3 * aca / steps, "generation_s": gen_s}
+    del fronts, rhs, work, batch
+    torch.cuda.empty_cache()
     return out
 
 
