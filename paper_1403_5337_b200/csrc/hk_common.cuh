@@ -161,6 +161,51 @@ __device__ __forceinline__ const T* cl_map(const T* p, unsigned rank) {
   return reinterpret_cast<const T*>(out);
 }
 
+// ---- TMA bulk copies (cp.async.bulk -> UBLKCP) completing on mbarriers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// arm the barrier's current phase with `bytes` of expected transactions (+1 arrival)
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> own shared memory, `bytes` (multiple of 16, both ends 16-byte aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// order this thread's earlier generic-proxy global writes before later
+// async-proxy (bulk copy) reads of the same addresses
+#ifndef HK_TMA_GPUFENCE
+#define HK_TMA_GPUFENCE 0
+#endif
+__device__ __forceinline__ void fence_proxy_async_global() {
+  if (HK_TMA_GPUFENCE) __threadfence();
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // FP64 tensor-core MMA (DMMA.8x8x4 on sm_100a; tcgen05 has no f64 kind).
 // Fragment layout (PTX ISA, mma.m8n8k4 .f64): gid = lane>>2, tig = lane&3;
 //   A (8x4, row):  a  = A[gid][tig]
