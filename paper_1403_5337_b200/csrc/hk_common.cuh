@@ -161,6 +161,16 @@ __device__ __forceinline__ const T* cl_map(const T* p, unsigned rank) {
   return reinterpret_cast<const T*>(out);
 }
 
+// ---- programmatic dependent launch: a kernel launched with the
+// programmatic-stream-serialization attribute may start while its predecessor
+// drains; it must call griddep_wait() before reading anything the predecessor
+// writes (independent loads -- stored factors -- go out before the wait).
+// Both are no-ops for a kernel launched without the attribute.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---- TMA bulk copies (cp.async.bulk -> UBLKCP) completing on mbarriers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);

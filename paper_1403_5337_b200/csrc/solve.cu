@@ -1,6 +1,8 @@
 // Few-right-hand-side kernels: the HODLR solve sweep (src/hodlr.py:285-306 ->
 // Coupling.correct :129-134) and the dense operator GEMV (src/cli.py:320-321).
 // These are HBM-bound: every stored factor byte is read once per application.
+#include <stdlib.h>
+
 #include "hk_common.cuh"
 #include "hk_internal.h"
 
@@ -137,6 +139,7 @@ __device__ __forceinline__ void pdot_item(const PdotTask* __restrict__ tasks,
       const int i = lane + 32 * u;
       m[j][u] = (j < nk && i < nr) ? t.M[row0 + i + (int64_t)(k0 + j) * t.ldm] : 0.0;
     }
+  griddep_wait();                              // x is the previous phase's output
   for (int idx = threadIdx.x; idx < nr * s; idx += 256) {
     const int i = idx % nr, r = idx / nr;
     xs[r * HK_PDOT_ROWS + i] = t.x[row0 + i + (int64_t)r * t.ldx];
@@ -164,6 +167,7 @@ __device__ __forceinline__ void pdot_item(const PdotTask* __restrict__ tasks,
 __global__ void __launch_bounds__(256) pdot_kernel(const PdotTask* __restrict__ tasks,
                                                    const int32_t* __restrict__ items, int s) {
   __shared__ double xs[HK_PDOT_ROWS * 16];
+  griddep_launch();
   pdot_item(tasks, items, blockIdx.x, s, xs);
 }
 
@@ -193,6 +197,7 @@ __device__ __forceinline__ void sgemv_item(const SgemvTask* __restrict__ tasks,
     const int k = q + u * QS;
     mpre[u] = (live && k < K) ? mrow[(int64_t)k * t.ldm] : 0.0;
   }
+  griddep_wait();                              // v / partials / y come from earlier phases
   // fixed-order sum over the partial-dot chunks, 8 independent loads at a time
   auto chunk_sum = [](const double* __restrict__ P, int nch, int64_t stride, int64_t off) {
     double v = 0.0;
@@ -273,21 +278,54 @@ __device__ __forceinline__ void sgemv_item(const SgemvTask* __restrict__ tasks,
 __global__ void __launch_bounds__(256) sgemv_kernel(const SgemvTask* __restrict__ tasks,
                                                     const int32_t* __restrict__ items, int s) {
   extern __shared__ double vs[];
+  griddep_launch();
   sgemv_item(tasks, items, blockIdx.x, s, vs);
 }
 
+// ---------------------------------------------------------------------------
+// Fused per-front solve sweep: one thread-block cluster runs a front's whole
+// program -- the leaf GEMVs, then per level (deepest first) the V^T x partial
+// dots, the S^{-1} g GEMV and the x -= d y update (hodlr.py:298-306) -- with
+// a cluster barrier between dependent phases instead of a kernel boundary.
+// CTA q of the cluster takes items q, q+P, ... of every phase (the same item
+// bodies as the split kernels, so results are bit-identical).  Fronts of a
+// batch run in independent clusters, so a front never waits for another
+// front's phase: the 3*depth+1 dependent phases of a batch no longer cost
+// 3*depth+1 grid-wide drains.  Phase outputs (partials, S^{-1} g, x) go
+// through global memory; barrier.cluster.wait.acquire orders them (and drops
+// stale L1 lines) for the next phase's readers in the other CTAs.
+__global__ void __launch_bounds__(256) solve_fused_kernel(const FusedPhase* __restrict__ phases,
+                                                          int nph, int s) {
+  extern __shared__ double dyn[];
+  const unsigned P = cl_nrank(), q = cl_rank();
+  const FusedPhase* fp = phases + (size_t)(blockIdx.x / P) * nph;
+  for (int k = 0; k < nph; ++k) {
+    const FusedPhase f = fp[k];
+    for (int it = (int)q; it < f.nitems; it += (int)P) {
+      if (f.type == 0) pdot_item(static_cast<const PdotTask*>(f.t), f.items, it, s, dyn);
+      else sgemv_item(static_cast<const SgemvTask*>(f.t), f.items, it, s, dyn);
+      __syncthreads();                       // SMEM reuse by the next item
+    }
+    cluster_bar();
+  }
+}
+
 // Dense GEMV for the GMRES operator (src/cli.py:320-321): y(m x s) = A x with
-// A row-major.  Each warp owns RW = 4 rows and walks them together with
-// 16-byte loads (lane l covers columns 2l + 64t, 2l + 64t + 1), so every x
-// chunk it loads is reused by 4 rows and each lane keeps 4 independent
-// 16-byte A loads in flight; columns are processed in groups of up to 4.
-// Per (row, column) the summation order is fixed (2 interleaved partials per
-// lane, then the warp tree), independent of s.
-template <int CG>
-__device__ __forceinline__ void gemv4_group(const double* __restrict__ A, int64_t lda, int64_t row0,
-                                            int64_t m, int64_t n, const double* __restrict__ x,
-                                            int64_t ldx, int lane, double (&res)[4][CG]) {
-  constexpr int RW = 4;
+// A row-major.  Each warp owns RW rows and walks them together with 16-byte
+// loads (lane l covers columns 2l + 64t, 2l + 64t + 1), so every x chunk it
+// loads is reused by RW rows; U chunks of A are issued before any is
+// consumed (U * RW independent 16-byte loads in flight per lane).  Columns
+// are processed in groups of up to 4.  Per (row, column) the summation order
+// is fixed -- t ascending, two interleaved partials per lane, then the warp
+// tree -- independent of s, RW and U, so every variant gives the same bits.
+// RW = 4, U = 1 for the large fronts (one pass over A per 4 right-hand sides
+// at the HBM roofline); RW = 1, U = 8 for small ones, where 4 rows per warp
+// left too few warps and a 16-deep chain of dependent round trips per lane.
+template <int RW, int CG, int U>
+__device__ __forceinline__ void gemv_group(const double* __restrict__ A, int64_t lda, int64_t row0,
+                                           int64_t m, int64_t n, const double* __restrict__ x,
+                                           int64_t ldx, int lane, double (&res)[RW][CG],
+                                           bool& waited) {
   double acc[RW][CG];
 #pragma unroll
   for (int r = 0; r < RW; ++r)
@@ -296,16 +334,32 @@ __device__ __forceinline__ void gemv4_group(const double* __restrict__ A, int64_
   const double* a[RW];
 #pragma unroll
   for (int r = 0; r < RW; ++r) a[r] = A + (row0 + r < m ? row0 + r : row0) * lda;
-  for (int64_t j = 2 * lane; j < n; j += 64) {
-    double2 av[RW], xv[CG];
+  for (int64_t j0 = 2 * lane; j0 < n; j0 += 64 * U) {
+    double2 av[U][RW];
 #pragma unroll
-    for (int r = 0; r < RW; ++r) av[r] = __ldcs(reinterpret_cast<const double2*>(a[r] + j));
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = j0 + 64 * u;
 #pragma unroll
-    for (int c = 0; c < CG; ++c) xv[c] = *reinterpret_cast<const double2*>(x + c * ldx + j);
+      for (int r = 0; r < RW; ++r)
+        av[u][r] = j < n ? __ldcs(reinterpret_cast<const double2*>(a[r] + j)) : make_double2(0.0, 0.0);
+    }
+    if (!waited) {                     // the operator is independent of the previous kernel, x is not
+      griddep_wait();
+      waited = true;
+    }
 #pragma unroll
-    for (int r = 0; r < RW; ++r)
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = j0 + 64 * u;
+      if (j >= n) break;
+      double2 xv[CG];
 #pragma unroll
-      for (int c = 0; c < CG; ++c) acc[r][c] = fma(av[r].y, xv[c].y, fma(av[r].x, xv[c].x, acc[r][c]));
+      for (int c = 0; c < CG; ++c) xv[c] = *reinterpret_cast<const double2*>(x + c * ldx + j);
+#pragma unroll
+      for (int r = 0; r < RW; ++r)
+#pragma unroll
+        for (int c = 0; c < CG; ++c)
+          acc[r][c] = fma(av[u][r].y, xv[c].y, fma(av[u][r].x, xv[c].x, acc[r][c]));
+    }
   }
 #pragma unroll
   for (int r = 0; r < RW; ++r)
@@ -313,29 +367,61 @@ __device__ __forceinline__ void gemv4_group(const double* __restrict__ A, int64_
     for (int c = 0; c < CG; ++c) res[r][c] = warp_sum(acc[r][c]);
 }
 
+template <int RW, int U4, int U1>
 __global__ void __launch_bounds__(MV_NT) gemv4_kernel(const double* __restrict__ A, int64_t lda,
                                                       int64_t m, int64_t n,
                                                       const double* __restrict__ x, int64_t ldx,
                                                       int64_t s, double* __restrict__ y, int64_t ldy) {
+  griddep_launch();
   const int lane = threadIdx.x & 31;
-  const int64_t row0 = ((int64_t)blockIdx.x * (MV_NT / 32) + (threadIdx.x >> 5)) * 4;
-  if (row0 >= m) return;
-  int64_t c0 = 0;
-  for (; c0 + 4 <= s; c0 += 4) {
-    double r[4][4];
-    gemv4_group<4>(A, lda, row0, m, n, x + c0 * ldx, ldx, lane, r);
-    if (lane == 0)
-      for (int q = 0; q < 4; ++q)
-        if (row0 + q < m)
-          for (int c = 0; c < 4; ++c) y[row0 + q + (c0 + c) * ldy] = r[q][c];
+  const int64_t row0 = ((int64_t)blockIdx.x * (MV_NT / 32) + (threadIdx.x >> 5)) * RW;
+  bool waited = false;
+  if (row0 < m) {
+    int64_t c0 = 0;
+    for (; c0 + 4 <= s; c0 += 4) {
+      double r[RW][4];
+      gemv_group<RW, 4, U4>(A, lda, row0, m, n, x + c0 * ldx, ldx, lane, r, waited);
+      if (lane == 0)
+        for (int q = 0; q < RW; ++q)
+          if (row0 + q < m)
+            for (int c = 0; c < 4; ++c) y[row0 + q + (c0 + c) * ldy] = r[q][c];
+    }
+    for (; c0 < s; ++c0) {
+      double r[RW][1];
+      gemv_group<RW, 1, U1>(A, lda, row0, m, n, x + c0 * ldx, ldx, lane, r, waited);
+      if (lane == 0)
+        for (int q = 0; q < RW; ++q)
+          if (row0 + q < m) y[row0 + q + c0 * ldy] = r[q][0];
+    }
   }
-  for (; c0 < s; ++c0) {
-    double r[4][1];
-    gemv4_group<1>(A, lda, row0, m, n, x + c0 * ldx, ldx, lane, r);
-    if (lane == 0)
-      for (int q = 0; q < 4; ++q)
-        if (row0 + q < m) y[row0 + q + c0 * ldy] = r[q][0];
+  if (!waited) griddep_wait();
+}
+
+// launch with programmatic dependent launch (HK_PDL=0 turns it off): the
+// kernel may start while its predecessor in the stream drains and must
+// griddep_wait() before reading the predecessor's output
+static bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HK_PDL");
+    v = e ? atoi(e) : 1;
   }
+  return v != 0;
+}
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, args...);
 }
 }  // namespace
 
@@ -369,11 +455,20 @@ cudaError_t hk_launch_gemv_rowmajor(const double* A, int64_t lda, int64_t m, int
   if (m == 0) return cudaSuccess;
   const bool vec = (n % 2 == 0) && (lda % 2 == 0) && (ldx % 2 == 0) &&
                    ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(x)) & 15) == 0;
-  if (vec) {   // 16-byte loads, 4 rows per warp
-    const int64_t rows_per_cta = (MV_NT / 32) * 4;
-    const int64_t blocks = (m + rows_per_cta - 1) / rows_per_cta;
-    gemv4_kernel<<<(unsigned)blocks, MV_NT, 0, st>>>(A, lda, m, n, x, ldx, s, y, ldy);
+  if (vec) {   // 16-byte loads
+    cudaError_t e;
+    if (m <= 8192) {            // one row per warp, 8 chunks in flight per lane
+      const int64_t blocks = (m + MV_NT / 32 - 1) / (MV_NT / 32);
+      e = launch_pdl(gemv4_kernel<1, 4, 8>, dim3((unsigned)blocks), dim3(MV_NT), 0, st, A, lda, m, n,
+                     x, ldx, s, y, ldy);
+    } else {                    // 4 rows per warp: x reuse, HBM-bound
+      const int64_t rows_per_cta = (MV_NT / 32) * 4;
+      const int64_t blocks = (m + rows_per_cta - 1) / rows_per_cta;
+      e = launch_pdl(gemv4_kernel<4, 1, 1>, dim3((unsigned)blocks), dim3(MV_NT), 0, st, A, lda, m, n,
+                     x, ldx, s, y, ldy);
+    }
     hk_count_launch();
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
   }
   int64_t blocks = (m + MV_NT / 32 - 1) / (MV_NT / 32);
@@ -385,8 +480,44 @@ cudaError_t hk_launch_gemv_rowmajor(const double* A, int64_t lda, int64_t m, int
 cudaError_t hk_launch_pdot(const PdotTask* tasks, const int32_t* items, int nitems, int s,
                            cudaStream_t st) {
   if (nitems == 0) return cudaSuccess;
-  pdot_kernel<<<nitems, 256, 0, st>>>(tasks, items, s);
+  const cudaError_t e = launch_pdl(pdot_kernel, dim3(nitems), dim3(256), 0, st, tasks, items, s);
   hk_count_launch();
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t hk_launch_solve_fused(const FusedPhase* phases, int nph, int nfronts, int s, int P,
+                                  size_t smem, cudaStream_t st) {
+  if (nfronts == 0 || nph == 0) return cudaSuccess;
+  static size_t attr_smem = 0;
+  static bool nonportable = false;
+  if (smem > 48 * 1024 && smem > attr_smem) {
+    cudaError_t e = cudaFuncSetAttribute(solve_fused_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_smem = smem;
+  }
+  if (P > 8 && !nonportable) {
+    cudaError_t e = cudaFuncSetAttribute(solve_fused_kernel,
+                                         cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    nonportable = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)P;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3((unsigned)(nfronts * P));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, solve_fused_kernel, phases, nph, s);
+  hk_count_launch();
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -399,8 +530,9 @@ cudaError_t hk_launch_sgemv(const SgemvTask* tasks, const int32_t* items, int ni
                                          (int)smem);
     if (e != cudaSuccess) return e;
   }
-  sgemv_kernel<<<nitems, 256, smem, st>>>(tasks, items, s);
+  const cudaError_t e = launch_pdl(sgemv_kernel, dim3(nitems), dim3(256), smem, st, tasks, items, s);
   hk_count_launch();
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
