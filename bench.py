@@ -273,6 +273,29 @@ def aca_algorithmic_bytes(tree, ranks):
     return total
 
 
+def aca_l2_bytes(tree, ranks):
+    """The L2 stream of one ACA launch beyond its compulsory bytes: pivot step
+    s re-reads the s accepted crosses of both U (m x s) and V (n x s) for its
+    residual row and column, 8 * (m + n) * r (r + 1) / 2 bytes per block of
+    rank r (SURVEY.md §8(d) counts this as L2/SMEM traffic, not algorithmic)."""
+    total = 0
+    for f in range(ranks.shape[0]):
+        for k, s in enumerate(tree.internal_nodes()):
+            nd = tree.nodes[s]
+            mn = tree.nodes[nd.left].size + tree.nodes[nd.right].size
+            for r in (int(ranks[f, 2 * k]), int(ranks[f, 2 * k + 1])):
+                total += 8 * mn * r * (r + 1) // 2
+    return total
+
+
+def l2_peak():
+    """Measured full-chip L2 read bandwidth (tools/l2_peak.cu -> profiles/l2_peak.json)."""
+    pf = ROOT / "profiles" / "l2_peak.json"
+    if pf.exists():
+        return float(json.loads(pf.read_text())["l2_gbs"]), "profiles/l2_peak.json l2_gbs (tools/l2_peak.cu)"
+    return None, "no measured L2 peak"
+
+
 def factor_flops(tree, ranks):
     """Algorithmic FP64 flops of one factorization per SURVEY.md §8(d) (leaf LU +
     Z-solve, coupling assembly + LU + correction), from the actual ranks."""
@@ -401,17 +424,29 @@ def run_ours(args):
     algo = aca_algorithmic_bytes(batch.tree, ranks)
     aca_avg = aca_s / args.steps
     achieved = algo / aca_avg / 1e9
-    traffic = None
-    tf = ROOT / "profiles" / "r01_aca_traffic.json"
+    traffic = l2_traffic = None
+    tf = ROOT / "profiles" / "r02_aca_traffic.json"
     if tf.exists():
-        traffic = json.loads(tf.read_text()).get("dram_bytes_per_build")
+        tj = json.loads(tf.read_text())
+        traffic = tj.get("dram_bytes_per_build")
+        l2_traffic = tj.get("l2_bytes_per_build")
+    l2pk, l2src = l2_peak()
+    l2b = aca_l2_bytes(batch.tree, ranks) + algo
     roof = {"kernel": "ACA build: aca_kernel size classes (4 persistent launches, all blocks of "
                       "all fronts), timed by CUDA events around the fork/join",
             "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
             "frac": achieved / hbm_peak, "traffic": traffic,
             "algorithmic_bytes_per_launch": algo, "launch_ms": aca_avg * 1e3,
             "share_of_step": aca_avg * 1e3 / (ms_max / args.steps),
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk.exists() else "fallback 6.65 TB/s"}
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk.exists() else "fallback 6.65 TB/s",
+            # the same launch against the L2 roofline: the re-streaming of earlier
+            # crosses (what bounds the pivot chains' sweeps) plus the compulsory bytes
+            "l2": {"bound": "l2", "achieved": l2b / aca_avg / 1e9, "peak": l2pk, "unit": "GB/s",
+                   "frac": (l2b / aca_avg / 1e9 / l2pk) if l2pk else None,
+                   "traffic": l2_traffic, "algorithmic_bytes_per_launch": l2b,
+                   "peak_source": l2src,
+                   "traffic_source": "profiles/r02_aca_traffic.json (ncu lts__t_sectors_srcunit_tex "
+                                     "read+write x 32 B, the four class launches serialised)"}}
 
     # ---- the other kernels against their rooflines: the factorization on the
     # FP64 tensor pipe (algorithmic flops of the actual ranks / the CUDA-event

@@ -294,6 +294,15 @@ hk_status hk_get_aca_time(hk_plan* plan, double* seconds);
 /* Kernel launches issued by this library since load (evidence counter). */
 int64_t hk_launch_count(void);
 
+/* Task-extent validation (environment HK_VALIDATE=1, read once at first use):
+ * every task array staged for a kernel is checked on the host against the
+ * device allocations its matrix regions fall in (the substitute for
+ * compute-sanitizer memcheck on this library's kernels; csrc/validate.cpp).
+ * Returns the number of regions found outside their allocation since load;
+ * *checked (optional) receives the number of regions checked.  No reference
+ * counterpart (debugging aid). */
+int64_t hk_debug_violations(int64_t* checked);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -71,6 +71,7 @@ SIGNATURES = {
     "hk_get_timings": (C.c_int, [P, PD, PD, PD]),
     "hk_get_aca_time": (C.c_int, [P, PD]),
     "hk_launch_count": (I64, []),
+    "hk_debug_violations": (I64, [C.POINTER(I64)]),
 }
 
 HK_OK = 0

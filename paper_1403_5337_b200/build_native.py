@@ -19,7 +19,7 @@ LIB = Path(os.environ["HK_LIB_OUT"]) if os.environ.get("HK_LIB_OUT") else PKG / 
 # experiment knob: extra nvcc flags (e.g. "-DHK_ACA_LB1") for variant builds written to HK_LIB_OUT
 EXTRA = os.environ.get("HK_NVCC_EXTRA", "").split()
 SOURCES = ["aca.cu", "lu.cu", "gj.cu", "gemm.cu", "solve.cu", "krylov.cu", "select.cu", "api.cpp",
-           "graph.cpp"]
+           "graph.cpp", "validate.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -1181,11 +1181,11 @@ cudaError_t hk_launch_aca(const AcaTask* tasks_dev, int ntasks, int max_cap, int
   if (P > 1) return hk_launch_aca_cluster(tasks_dev, ntasks, P, max_cap, max_m, tol2, st, nullptr,
                                           nullptr);
   int* counter = nullptr;
-  cudaError_t e = cudaMallocAsync(&counter, sizeof(int), st);
+  cudaError_t e = hk_dev_malloc(&counter, sizeof(int), st);
   if (e != cudaSuccess) return e;
   cudaMemsetAsync(counter, 0, sizeof(int), st);
   e = launch_class_id(hk_aca_class(max_mn, max_mn), tasks_dev, ntasks, max_cap, max_m, tol2, counter, st);
-  cudaFreeAsync(counter, st);
+  hk_dev_free(counter, st);
   return e;
 }
 

@@ -93,11 +93,11 @@ struct DevBuf {
   size_t bytes = 0;
   cudaError_t ensure(size_t need, cudaStream_t st) {
     if (need <= bytes && p) return cudaSuccess;
-    if (p) cudaFreeAsync(p, st);
+    if (p) hk_dev_free(p, st);
     p = nullptr;
     bytes = 0;
     size_t alloc = need < 256 ? 256 : need;
-    cudaError_t e = cudaMallocAsync(&p, alloc, st);
+    cudaError_t e = hk_dev_malloc(&p, alloc, st);
     if (e == cudaSuccess) bytes = alloc;
     return e;
   }
@@ -144,7 +144,7 @@ struct Staging {
         Seg g;
         g.cap = std::max(kSeg, bytes + 256);
         if (cudaHostAlloc((void**)&g.host, g.cap, cudaHostAllocDefault) != cudaSuccess) return nullptr;
-        if (cudaMallocAsync((void**)&g.dev, g.cap, st) != cudaSuccess) {
+        if (hk_dev_malloc((void**)&g.dev, g.cap, st) != cudaSuccess) {
           cudaFreeHost(g.host);
           return nullptr;
         }
@@ -163,6 +163,8 @@ struct Staging {
   }
   template <class T>
   T* push(const std::vector<T>& v, cudaStream_t st) {
+    if (hk_validate_enabled())
+      for (const T& t : v) hk_validate(t);
     return reinterpret_cast<T*>(push(v.data(), v.size() * sizeof(T), st));
   }
   static cudaError_t commit_seg(Seg& g, cudaStream_t st) {
@@ -288,7 +290,7 @@ struct SolveProg {
   // device memory is returned stream-ordered by drop_progs (a plain cudaFree
   // would synchronise the whole device, stalling copies on other streams)
   void free_async(cudaStream_t st) {
-    if (pbuf.p) cudaFreeAsync(pbuf.p, st);
+    if (pbuf.p) hk_dev_free(pbuf.p, st);
     pbuf.p = nullptr;
     pbuf.bytes = 0;
   }
@@ -1723,11 +1725,11 @@ extern "C" hk_status hk_dgemm(int transa, int64_t m, int64_t n, int64_t k, doubl
   if (tl.ntiles() == 0) return HK_OK;
   char* d = nullptr;
   const size_t tb = sizeof(GemmTask), mb = tl.map.size() * 4;
-  CU(cudaMallocAsync((void**)&d, tb + 256 + mb, st));
+  CU(hk_dev_malloc((void**)&d, tb + 256 + mb, st));
   CU(cudaMemcpyAsync(d, tl.tasks.data(), tb, cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(d + 256, tl.map.data(), mb, cudaMemcpyHostToDevice, st));
   CU(hk_launch_gemm((const GemmTask*)d, (const int32_t*)(d + 256), tl.ntiles(), st));
-  CU(cudaFreeAsync(d, st));
+  CU(hk_dev_free(d, st));
   return HK_OK;
 }
 
@@ -2572,10 +2574,10 @@ extern "C" hk_status hk_arnoldi_step(int64_t n, int64_t j, int64_t mmax, double*
                                      double beta, double* out_host, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   double* outd = nullptr;
-  CU(cudaMallocAsync(&outd, 32, st));
+  CU(hk_dev_malloc(&outd, 32, st));
   CU(hk_launch_arnoldi(n, j, mmax, basis, hess, cs, sn, g, w, beta, outd, st));
   CU(cudaMemcpyAsync(out_host, outd, 24, cudaMemcpyDeviceToHost, st));
-  CU(cudaFreeAsync(outd, st));
+  CU(hk_dev_free(outd, st));
   CU(cudaStreamSynchronize(st));
   return HK_OK;
 }
@@ -2601,9 +2603,9 @@ extern "C" hk_status hk_gmres_combine(int64_t n, int64_t m, int64_t mmax, const 
                                       const double* hess, const double* g, double* x, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   double* y = nullptr;
-  CU(cudaMallocAsync(&y, (size_t)(m + 1) * 8, st));
+  CU(hk_dev_malloc(&y, (size_t)(m + 1) * 8, st));
   CU(hk_launch_combine(n, m, mmax, basis, hess, g, x, y, st));
-  CU(cudaFreeAsync(y, st));
+  CU(hk_dev_free(y, st));
   return HK_OK;
 }
 
@@ -2629,10 +2631,10 @@ extern "C" hk_status hk_lu_full(double* a, int64_t m, int64_t n, int64_t ld, int
   if (hk_device_count() == 0) return fail(HK_ERR_CUDA, "no CUDA device visible");
   cudaStream_t st = (cudaStream_t)stream;
   int64_t* d = nullptr;
-  CU(cudaMallocAsync(&d, 8, st));
+  CU(hk_dev_malloc(&d, 8, st));
   CU(hk_launch_lu_full(a, m, n, ld, rp, cp, piv, d, st));
   CU(cudaMemcpyAsync(npiv, d, 8, cudaMemcpyDeviceToHost, st));
-  CU(cudaFreeAsync(d, st));
+  CU(hk_dev_free(d, st));
   CU(cudaStreamSynchronize(st));
   return HK_OK;
 }
@@ -2645,15 +2647,15 @@ extern "C" hk_status hk_lu_partial(double* a, int64_t n, int64_t ld, int32_t* pe
   cudaStream_t st = (cudaStream_t)stream;
   double *lu = nullptr, *iv = nullptr;
   int32_t *ip = nullptr, *stt = nullptr;
-  CU(cudaMallocAsync(&lu, (size_t)n * n * 8, st));
-  CU(cudaMallocAsync(&iv, (size_t)n * n * 8, st));
-  CU(cudaMallocAsync(&ip, (size_t)n * 4 + 4, st));
-  CU(cudaMallocAsync(&stt, 8, st));
+  CU(hk_dev_malloc(&lu, (size_t)n * n * 8, st));
+  CU(hk_dev_malloc(&iv, (size_t)n * n * 8, st));
+  CU(hk_dev_malloc(&ip, (size_t)n * 4 + 4, st));
+  CU(hk_dev_malloc(&stt, 8, st));
   LuTask t{};
   t.src = a; t.src_ld = ld; t.lu = lu; t.inv = inv ? iv : nullptr;
   t.perm = ip; t.ipiv = perm; t.status = stt; t.N = (int)n; t.mode = 0;
   LuTask* td = nullptr;
-  CU(cudaMallocAsync(&td, sizeof(LuTask), st));
+  CU(hk_dev_malloc(&td, sizeof(LuTask), st));
   CU(cudaMemcpyAsync(td, &t, sizeof(LuTask), cudaMemcpyHostToDevice, st));
   CU(hk_launch_lu(td, 1, (int)n, st));
   // column-major results -> row-major outputs
@@ -2662,8 +2664,8 @@ extern "C" hk_status hk_lu_partial(double* a, int64_t n, int64_t ld, int32_t* pe
   int32_t sing = 0;
   CU(cudaMemcpyAsync(&sing, stt, 4, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
-  cudaFreeAsync(lu, st); cudaFreeAsync(iv, st); cudaFreeAsync(ip, st);
-  cudaFreeAsync(stt, st); cudaFreeAsync(td, st);
+  hk_dev_free(lu, st); hk_dev_free(iv, st); hk_dev_free(ip, st);
+  hk_dev_free(stt, st); hk_dev_free(td, st);
   if (sing) return fail(HK_ERR_SINGULAR, "pivot magnitude below 1e-300");
   return HK_OK;
 }
@@ -2686,8 +2688,8 @@ extern "C" hk_status hk_gj_inverse(const double* A, int64_t n, int64_t lda, int6
   char* scratch = nullptr;
   int32_t* stt = nullptr;
   GjTask* td = nullptr;
-  if (scr) CU(cudaMallocAsync((void**)&scratch, scr * (size_t)batch, st));
-  CU(cudaMallocAsync((void**)&stt, (size_t)batch * 4, st));
+  if (scr) CU(hk_dev_malloc((void**)&scratch, scr * (size_t)batch, st));
+  CU(hk_dev_malloc((void**)&stt, (size_t)batch * 4, st));
   std::vector<GjTask> tasks((size_t)batch);
   for (int64_t b = 0; b < batch; ++b) {
     GjTask& t = tasks[(size_t)b];
@@ -2700,14 +2702,14 @@ extern "C" hk_status hk_gj_inverse(const double* A, int64_t n, int64_t lda, int6
     t.N = (int32_t)n;
     t.mode = 0;
   }
-  CU(cudaMallocAsync((void**)&td, sizeof(GjTask) * tasks.size(), st));
+  CU(hk_dev_malloc((void**)&td, sizeof(GjTask) * tasks.size(), st));
   CU(cudaMemcpyAsync(td, tasks.data(), sizeof(GjTask) * tasks.size(), cudaMemcpyHostToDevice, st));
   CU(hk_launch_gj(td, (int)batch, (int)n, st));
   CU(cudaMemcpyAsync(status_host, stt, (size_t)batch * 4, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
-  cudaFreeAsync(td, st);
-  cudaFreeAsync(stt, st);
-  if (scratch) cudaFreeAsync(scratch, st);
+  hk_dev_free(td, st);
+  hk_dev_free(stt, st);
+  if (scratch) hk_dev_free(scratch, st);
   return HK_OK;
 }
 
@@ -2729,10 +2731,10 @@ extern "C" hk_status hk_aca_block(const double* a, int64_t m, int64_t n, int64_t
   const int64_t tlen = 2 + (m + cap + 1) + (cap + 1);
   double *sqbuf = nullptr, *at = nullptr;
   int32_t *rk = nullptr, *tr = nullptr;
-  CU(cudaMallocAsync(&sqbuf, (size_t)sq * sq * 8, st));
-  CU(cudaMallocAsync(&at, (size_t)sq * sq * 8, st));
-  CU(cudaMallocAsync(&rk, 8, st));
-  CU(cudaMallocAsync(&tr, (size_t)tlen * 4, st));
+  CU(hk_dev_malloc(&sqbuf, (size_t)sq * sq * 8, st));
+  CU(hk_dev_malloc(&at, (size_t)sq * sq * 8, st));
+  CU(hk_dev_malloc(&rk, 8, st));
+  CU(hk_dev_malloc(&tr, (size_t)tlen * 4, st));
   CU(cudaMemsetAsync(sqbuf, 0, (size_t)sq * sq * 8, st));
   CU(cudaMemcpy2DAsync(sqbuf, sq * 8, a, ld * 8, n * 8, m, cudaMemcpyDeviceToDevice, st));
   CU(hk_launch_transpose(sqbuf, at, sq, sq, 1, 0, st));
@@ -2740,15 +2742,15 @@ extern "C" hk_status hk_aca_block(const double* a, int64_t m, int64_t n, int64_t
   {
     const int P = hk_aca_cluster_size((int)std::max(m, n), (int)std::max(m, n));
     const size_t sd = P > 1 ? hk_aca_scratch_doubles_cl((int)cap, P) : hk_aca_scratch_doubles((int)cap);
-    CU(cudaMallocAsync(&scr, sd * 8, st));
+    CU(hk_dev_malloc(&scr, sd * 8, st));
   }
   int lmu = 6;
   while ((1 << lmu) < std::max(m, n)) ++lmu;
   const int lmv = lmu;
   if (lmu > 13 || lmv > 13) return fail(HK_ERR_VALUE, "block too large for the ACA kernel (max 8192 rows)");
   double *Ur = nullptr, *Vr = nullptr;
-  CU(cudaMallocAsync(&Ur, ((size_t)1 << lmu) * (cap + 8) * 8, st));
-  CU(cudaMallocAsync(&Vr, ((size_t)1 << lmv) * (cap + 8) * 8, st));
+  CU(hk_dev_malloc(&Ur, ((size_t)1 << lmu) * (cap + 8) * 8, st));
+  CU(hk_dev_malloc(&Vr, ((size_t)1 << lmv) * (cap + 8) * 8, st));
   AcaTask t{};
   t.scratch = scr;
   t.A = sqbuf;
@@ -2764,7 +2766,7 @@ extern "C" hk_status hk_aca_block(const double* a, int64_t m, int64_t n, int64_t
   t.n = (int)n;
   t.cap = (int)cap;
   AcaTask* td = nullptr;
-  CU(cudaMallocAsync(&td, sizeof(AcaTask), st));
+  CU(hk_dev_malloc(&td, sizeof(AcaTask), st));
   CU(cudaMemcpyAsync(td, &t, sizeof(AcaTask), cudaMemcpyHostToDevice, st));
   CU(hk_launch_aca(td, 1, (int)cap, (int)m, tol2, st, (int)std::max(m, n)));
   std::vector<int32_t> h(tlen);
@@ -2777,21 +2779,21 @@ extern "C" hk_status hk_aca_block(const double* a, int64_t m, int64_t n, int64_t
     ct[0] = CopyTask{Ur, U, 1, (int64_t)1 << lmu, 1, m, (int32_t)m, r32};
     ct[1] = CopyTask{Vr, V, 1, (int64_t)1 << lmv, 1, n, (int32_t)n, r32};
     CopyTask* ctd = nullptr;
-    CU(cudaMallocAsync(&ctd, sizeof(CopyTask) * 2, st));
+    CU(hk_dev_malloc(&ctd, sizeof(CopyTask) * 2, st));
     CU(cudaMemcpyAsync(ctd, ct.data(), sizeof(CopyTask) * 2, cudaMemcpyHostToDevice, st));
     CU(hk_launch_copy(ctd, 2, st));
     CU(cudaStreamSynchronize(st));
-    cudaFreeAsync(ctd, st);
+    hk_dev_free(ctd, st);
   }
-  cudaFreeAsync(Ur, st);
-  cudaFreeAsync(Vr, st);
+  hk_dev_free(Ur, st);
+  hk_dev_free(Vr, st);
   *rank = r32;
   if (nrows) *nrows = h[0];
   if (ncols) *ncols = h[1];
   if (trows) std::memcpy(trows, h.data() + 2, (size_t)h[0] * 4);
   if (tcols) std::memcpy(tcols, h.data() + 2 + (m + cap + 1), (size_t)h[1] * 4);
-  cudaFreeAsync(at, st); cudaFreeAsync(rk, st); cudaFreeAsync(tr, st);
-  cudaFreeAsync(sqbuf, st); cudaFreeAsync(td, st); cudaFreeAsync(scr, st);
+  hk_dev_free(at, st); hk_dev_free(rk, st); hk_dev_free(tr, st);
+  hk_dev_free(sqbuf, st); hk_dev_free(td, st); hk_dev_free(scr, st);
   return HK_OK;
 }
 
@@ -2811,10 +2813,10 @@ extern "C" hk_status hk_skeleton_block(const double* a, int64_t m, int64_t n, in
   int64_t *seld = nullptr, *perm = nullptr;
   double* work = nullptr;
   int32_t* small = nullptr;  // [rank, status]
-  CU(cudaMallocAsync(&seld, sel.size() * 8, st));
-  CU(cudaMallocAsync(&perm, (size_t)(k + kc) * 8, st));
-  CU(cudaMallocAsync(&work, (size_t)k * kc * 8, st));
-  CU(cudaMallocAsync(&small, 8, st));
+  CU(hk_dev_malloc(&seld, sel.size() * 8, st));
+  CU(hk_dev_malloc(&perm, (size_t)(k + kc) * 8, st));
+  CU(hk_dev_malloc(&work, (size_t)k * kc * 8, st));
+  CU(hk_dev_malloc(&small, 8, st));
   CU(cudaMemcpyAsync(seld, sel.data(), sel.size() * 8, cudaMemcpyHostToDevice, st));
   SkelTask t{};
   t.A = a; t.lda = ld;
@@ -2825,7 +2827,7 @@ extern "C" hk_status hk_skeleton_block(const double* a, int64_t m, int64_t n, in
   t.probe = seld + k + kc; t.nprobe = (int32_t)pr.size();
   t.m = (int)m; t.n = (int)n; t.k = (int)k; t.kc = (int)kc; t.cap = (int)cap; t.tol = tol;
   SkelTask* td = nullptr;
-  CU(cudaMallocAsync(&td, sizeof(SkelTask), st));
+  CU(hk_dev_malloc(&td, sizeof(SkelTask), st));
   CU(cudaMemcpyAsync(td, &t, sizeof(SkelTask), cudaMemcpyHostToDevice, st));
   CU(hk_launch_skeleton(td, 1, (int)k, (int)kc, (int)m, (int)n, st));
   int32_t hs[2] = {0, 0};
@@ -2833,8 +2835,8 @@ extern "C" hk_status hk_skeleton_block(const double* a, int64_t m, int64_t n, in
   CU(cudaMemcpyAsync(hs, small, 8, cudaMemcpyDeviceToHost, st));
   CU(cudaMemcpyAsync(ph.data(), perm, ph.size() * 8, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
-  cudaFreeAsync(seld, st); cudaFreeAsync(perm, st); cudaFreeAsync(work, st);
-  cudaFreeAsync(small, st); cudaFreeAsync(td, st);
+  hk_dev_free(seld, st); hk_dev_free(perm, st); hk_dev_free(work, st);
+  hk_dev_free(small, st); hk_dev_free(td, st);
   *rank = hs[0];
   for (int64_t i = 0; i < hs[0]; ++i) {
     if (rows_out) rows_out[i] = rsel[ph[i]];

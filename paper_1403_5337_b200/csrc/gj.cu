@@ -186,6 +186,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_blk_kernel(const GjTask* __rest
 // and replays the step on its own columns.  The owner of the next panel is
 // therefore never more than one step behind, and the critical path is one
 // pivot search + update per step instead of a CTA barrier per panel.
+#ifndef HK_GJ_SPIN_NS
+#define HK_GJ_SPIN_NS 0
+#endif
 __device__ __forceinline__ int ld_acquire_cta(const int* p) {
   int v;
   asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
@@ -297,6 +300,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_df_kernel(const GjTask* __restr
         // every lane acquires the publication itself (a value read by lane 0
         // alone would not order the other lanes' reads of the step's data)
         while (ld_acquire_cta(&s_pub) <= c) {
+#if HK_GJ_SPIN_NS
+          __nanosleep(HK_GJ_SPIN_NS);   // back off: the spinning warps share the MIO pipe with the owner
+#endif
         }
         __syncwarp();
         const int p = __shfl_sync(0xffffffffu, lane == 0 ? p_s[c] : 0, 0);

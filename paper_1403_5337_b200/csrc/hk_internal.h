@@ -275,3 +275,29 @@ struct GjTask {
 #define HK_NEAR_PIVOT 1e-8
 cudaError_t hk_launch_gj(const GjTask* tasks_dev, int ntasks, int maxN, cudaStream_t st);
 size_t hk_gj_scratch_bytes(int N);     // 0 when N fits SMEM
+
+// ---------------------------------------------------------------- validation (validate.cpp)
+// HK_VALIDATE=1: every staged task's memory regions are checked against the
+// device allocation that holds them, and the library's own buffers become
+// plain cudaMalloc allocations (exact ranges); see validate.cpp.
+bool hk_validate_enabled();
+cudaError_t hk_dev_malloc_raw(void** p, size_t bytes, cudaStream_t st);
+cudaError_t hk_dev_free(void* p, cudaStream_t st);
+template <class T>
+inline cudaError_t hk_dev_malloc(T** p, size_t bytes, cudaStream_t st) {
+  return hk_dev_malloc_raw(reinterpret_cast<void**>(p), bytes, st);
+}
+void hk_validate(const GemmTask& t);
+void hk_validate(const CopyTask& t);
+void hk_validate(const AcaTask& t);
+void hk_validate(const SkelTask& t);
+void hk_validate(const GjTask& t);
+void hk_validate(const LuTask& t);
+void hk_validate(const PdotTask& t);
+void hk_validate(const SgemvTask& t);
+void hk_validate(const MatVecTask& t);
+void hk_validate(const DotTask& t);
+void hk_validate(const SelTask& t);
+template <class T>
+inline void hk_validate(const T&) {}   // index arrays and other plain data
+

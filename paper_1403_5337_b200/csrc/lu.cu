@@ -393,7 +393,7 @@ cudaError_t hk_launch_skeleton(const SkelTask* tasks_dev, int ntasks, int max_k,
   if (ntasks == 0) return cudaSuccess;
   double* pivbuf = nullptr;
   int64_t pstride = (max_k < max_kc ? max_k : max_kc) + 1;
-  cudaError_t e = cudaMallocAsync(&pivbuf, (size_t)ntasks * pstride * 8, st);
+  cudaError_t e = hk_dev_malloc(&pivbuf, (size_t)ntasks * pstride * 8, st);
   if (e != cudaSuccess) return e;
   // every task whose working matrix fits takes the SMEM path (1024-thread
   // CTAs run one per SM anyway); larger ones work in global memory
@@ -415,6 +415,6 @@ cudaError_t hk_launch_skeleton(const SkelTask* tasks_dev, int ntasks, int max_k,
     hk_count_launch();
     e = cudaGetLastError();
   }
-  cudaFreeAsync(pivbuf, st);
+  hk_dev_free(pivbuf, st);
   return e;
 }

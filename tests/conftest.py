@@ -35,3 +35,19 @@ def rng():
 
 def random_low_rank(rng, m, n, r):
     return rng.standard_normal((m, r)) @ rng.standard_normal((r, n))
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Under HK_VALIDATE=1 (tests/test_gpu_validate.py runs the GPU suite that
+    way) report the task-extent validator's counts and fail the session on any
+    region found outside its device allocation."""
+    import os
+    if os.environ.get("HK_VALIDATE") != "1" or "paper_1403_5337_b200._native" not in sys.modules:
+        return
+    import ctypes
+    from paper_1403_5337_b200 import _native as N
+    checked = ctypes.c_int64(0)
+    viol = int(N.lib().hk_debug_violations(ctypes.byref(checked)))
+    print(f"\n[hk validate] {checked.value} task regions checked, {viol} violations")
+    if viol:
+        session.exitstatus = 1

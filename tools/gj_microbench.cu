@@ -1,12 +1,18 @@
 // standalone GJ microbenchmark: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include -I paper_1403_5337_b200/csrc tools/gj_microbench.cu -o exp/gj_microbench
 #include "../paper_1403_5337_b200/csrc/gj.cu"
+#ifndef GJ_MB_NS
+#define GJ_MB_NS 64, 110, 128
+#endif
+#ifndef GJ_MB_TASKS
+#define GJ_MB_TASKS 1, 128, 512
+#endif
 #include <cstdio>
 #include <vector>
 #include <random>
 void hk_count_launch(int) {}
 int main() {
-  for (int N : {32, 64, 96, 114, 128}) {
-    for (int ntask : {1, 64, 1024}) {
+  for (int N : {GJ_MB_NS}) {
+    for (int ntask : {GJ_MB_TASKS}) {
       std::vector<double> A((size_t)ntask * N * N);
       std::mt19937_64 g(1);
       std::normal_distribution<double> d;
@@ -18,7 +24,12 @@ int main() {
       cudaMalloc(&dt, ntask * sizeof(GjTask));
       cudaMemcpy(dA, A.data(), A.size() * 8, cudaMemcpyHostToDevice);
       std::vector<GjTask> ts(ntask);
-      for (int t = 0; t < ntask; ++t) ts[t] = GjTask{dA + (size_t)t * N * N, N, dO + (size_t)t * N * N, N, nullptr, st + t, N, 1};
+      for (int t = 0; t < ntask; ++t) {
+        GjTask x{};
+        x.src = dA + (size_t)t * N * N; x.src_ld = N; x.out = dO + (size_t)t * N * N; x.out_ld = N;
+        x.status = st + t; x.N = N; x.mode = 1;
+        ts[t] = x;
+      }
       cudaMemcpy(dt, ts.data(), ntask * sizeof(GjTask), cudaMemcpyHostToDevice);
       cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
       for (int it = 0; it < 3; ++it) hk_launch_gj(dt, ntask, N, 0);
