@@ -15,6 +15,43 @@
 
 namespace {
 
+// One pivot step applied to CPW register columns (rows lane + 32 q): for
+// every column but `skip`, rj = W[p][j] / pivot (through rinv), W[i][j] -=
+// ck[i] rj for i != p and W[p][j] = rj -- the arithmetic of the loop this
+// replaces, so the bits are unchanged.  QP = p >> 5 is warp-uniform, so the
+// caller dispatches it once per step (switch) and the pivot row's register is
+// a compile-time index: no per-element selects (the select-based form spent
+// 85% of the kernel's instructions on FSEL/LOP3/ISETP).
+template <int CPW, int RPL, int QP>
+__device__ __forceinline__ void gj_apply_step(double (&w)[CPW][RPL], const double (&ck)[RPL],
+                                              double rinv, int lp, int lane, int skip) {
+#pragma unroll
+  for (int jj = 0; jj < CPW; ++jj) {
+    if (jj == skip) continue;
+    const double rj = __shfl_sync(0xffffffffu, w[jj][QP], lp) * rinv;
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) w[jj][q] = fma(-ck[q], rj, w[jj][q]);
+    if (lane == lp) w[jj][QP] = rj;
+  }
+}
+template <int CPW, int RPL>
+__device__ __forceinline__ void gj_apply_step_dyn(double (&w)[CPW][RPL], const double (&ck)[RPL],
+                                                  double rinv, int qp, int lp, int lane, int skip) {
+  static_assert(RPL <= 8, "RPL <= 8");
+  switch (qp) {
+    case 0: gj_apply_step<CPW, RPL, 0>(w, ck, rinv, lp, lane, skip); break;
+    case 1: if constexpr (RPL > 1) gj_apply_step<CPW, RPL, (RPL > 1 ? 1 : 0)>(w, ck, rinv, lp, lane, skip); break;
+    case 2: if constexpr (RPL > 2) gj_apply_step<CPW, RPL, (RPL > 2 ? 2 : 0)>(w, ck, rinv, lp, lane, skip); break;
+    case 3: if constexpr (RPL > 3) gj_apply_step<CPW, RPL, (RPL > 3 ? 3 : 0)>(w, ck, rinv, lp, lane, skip); break;
+    case 4: if constexpr (RPL > 4) gj_apply_step<CPW, RPL, (RPL > 4 ? 4 : 0)>(w, ck, rinv, lp, lane, skip); break;
+    case 5: if constexpr (RPL > 5) gj_apply_step<CPW, RPL, (RPL > 5 ? 5 : 0)>(w, ck, rinv, lp, lane, skip); break;
+    case 6: if constexpr (RPL > 6) gj_apply_step<CPW, RPL, (RPL > 6 ? 6 : 0)>(w, ck, rinv, lp, lane, skip); break;
+    default: if constexpr (RPL > 7) gj_apply_step<CPW, RPL, (RPL > 7 ? 7 : 0)>(w, ck, rinv, lp, lane, skip); break;
+  }
+}
+
+
+
 constexpr int GJ_NT = 256;
 constexpr size_t GJ_SMEM_CAP = 224 * 1024;
 
@@ -110,23 +147,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_blk_kernel(const GjTask* __rest
           pbuf[buf][l] = p;
           pivrow[c] = p;
         }
+        gj_apply_step_dyn<CPW, RPL>(w_, ck, rinv, qp, lp, lane, l);
 #pragma unroll
-        for (int jj = 0; jj < CPW; ++jj) {
-          if (jj == l) {
-#pragma unroll
-            for (int q = 0; q < RPL; ++q) w_[jj][q] = isp[q] ? rinv : -ck[q] * rinv;
-          } else {
-            double src = w_[jj][0];
-#pragma unroll
-            for (int q = 1; q < RPL; ++q) src = (qp == q) ? w_[jj][q] : src;
-            const double rj = __shfl_sync(0xffffffffu, src, lp) * rinv;
-#pragma unroll
-            for (int q = 0; q < RPL; ++q) {
-              const double v = fma(-ck[q], rj, w_[jj][q]);
-              w_[jj][q] = isp[q] ? rj : v;
-            }
-          }
-        }
+        for (int q = 0; q < RPL; ++q) w_[l][q] = isp[q] ? rinv : -ck[q] * rinv;
       }
       if (sing && lane == 0) s_sing = 1;
     }
@@ -147,18 +170,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_blk_kernel(const GjTask* __rest
           ck[q] = (i < N) ? ckbuf[buf][l][i] : 0.0;
           isp[q] = i == p;
         }
-#pragma unroll
-        for (int jj = 0; jj < CPW; ++jj) {
-          double src = w_[jj][0];
-#pragma unroll
-          for (int q = 1; q < RPL; ++q) src = (qp == q) ? w_[jj][q] : src;
-          const double rj = __shfl_sync(0xffffffffu, src, lp) * rinv;
-#pragma unroll
-          for (int q = 0; q < RPL; ++q) {
-            const double v = fma(-ck[q], rj, w_[jj][q]);
-            w_[jj][q] = isp[q] ? rj : v;
-          }
-        }
+        gj_apply_step_dyn<CPW, RPL>(w_, ck, rinv, qp, lp, lane, -1);
       }
     }
   }
@@ -186,6 +198,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_blk_kernel(const GjTask* __rest
 // and replays the step on its own columns.  The owner of the next panel is
 // therefore never more than one step behind, and the critical path is one
 // pivot search + update per step instead of a CTA barrier per panel.
+#ifndef HK_GJ_LAZY
+#define HK_GJ_LAZY 0
+#endif
 #ifndef HK_GJ_SPIN_NS
 #define HK_GJ_SPIN_NS 0
 #endif
@@ -257,7 +272,8 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_df_kernel(const GjTask* __restr
         if (__any_sync(0xffffffffu, !(pivabs >= HK_PIVOT_FLOOR))) {
           if (lane == 0) {
             p_s[c] = -1;
-            st_release_cta(&s_pub, c + 1);
+            // release every waiter, lazy ones included: they stop at step c
+            st_release_cta(&s_pub, HK_GJ_LAZY ? N + 1 : c + 1);
           }
           singular = true;
           break;
@@ -279,27 +295,19 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_df_kernel(const GjTask* __restr
         }
         __syncwarp();
         if (lane == 0) st_release_cta(&s_pub, c + 1);
+        gj_apply_step_dyn<CPW, RPL>(w_, ck, rinv, qp, lp, lane, l);
 #pragma unroll
-        for (int jj = 0; jj < CPW; ++jj) {
-          if (jj == l) {
-#pragma unroll
-            for (int q = 0; q < RPL; ++q) w_[jj][q] = isp[q] ? rinv : -ck[q] * rinv;
-          } else {
-            double src = w_[jj][0];
-#pragma unroll
-            for (int q = 1; q < RPL; ++q) src = (qp == q) ? w_[jj][q] : src;
-            const double rj = __shfl_sync(0xffffffffu, src, lp) * rinv;
-#pragma unroll
-            for (int q = 0; q < RPL; ++q) {
-              const double v = fma(-ck[q], rj, w_[jj][q]);
-              w_[jj][q] = isp[q] ? rj : v;
-            }
-          }
-        }
+        for (int q = 0; q < RPL; ++q) w_[l][q] = isp[q] ? rinv : -ck[q] * rinv;
       } else {
         // every lane acquires the publication itself (a value read by lane 0
-        // alone would not order the other lanes' reads of the step's data)
-        while (ld_acquire_cta(&s_pub) <= c) {
+        // alone would not order the other lanes' reads of the step's data).
+        // Lazy replay: only the next panel's owner follows the owner step by
+        // step; every other warp waits for the whole panel and then replays its
+        // steps in the same order (same arithmetic, same bits), so the owner's
+        // pivot chain no longer shares its SM sub-partition's issue slots with
+        // NW-2 warps replaying every step.
+        const int need = (!HK_GJ_LAZY || warp == P + 1) ? c : min(N, (P + 1) * CPW) - 1;
+        while (ld_acquire_cta(&s_pub) <= need) {
 #if HK_GJ_SPIN_NS
           __nanosleep(HK_GJ_SPIN_NS);   // back off: the spinning warps share the MIO pipe with the owner
 #endif
@@ -321,18 +329,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_df_kernel(const GjTask* __restr
           ck[q] = (i < N) ? ck_s[i] : 0.0;
           isp[q] = i == p;
         }
-#pragma unroll
-        for (int jj = 0; jj < CPW; ++jj) {
-          double src = w_[jj][0];
-#pragma unroll
-          for (int q = 1; q < RPL; ++q) src = (qp == q) ? w_[jj][q] : src;
-          const double rj = __shfl_sync(0xffffffffu, src, lp) * rinv;
-#pragma unroll
-          for (int q = 0; q < RPL; ++q) {
-            const double v = fma(-ck[q], rj, w_[jj][q]);
-            w_[jj][q] = isp[q] ? rj : v;
-          }
-        }
+        gj_apply_step_dyn<CPW, RPL>(w_, ck, rinv, qp, lp, lane, -1);
       }
     }
   }
@@ -440,23 +437,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_cl_kernel(const GjTask* __restr
           pbuf[buf][l] = p;
           pivrow[c] = p;
         }
+        gj_apply_step_dyn<CPW, RPL>(w_, ck, rinv, qp, lp, lane, l);
 #pragma unroll
-        for (int jj = 0; jj < CPW; ++jj) {
-          if (jj == l) {
-#pragma unroll
-            for (int q = 0; q < RPL; ++q) w_[jj][q] = isp[q] ? rinv : -ck[q] * rinv;
-          } else {
-            double src = w_[jj][0];
-#pragma unroll
-            for (int q = 1; q < RPL; ++q) src = (qp == q) ? w_[jj][q] : src;
-            const double rj = __shfl_sync(0xffffffffu, src, lp) * rinv;
-#pragma unroll
-            for (int q = 0; q < RPL; ++q) {
-              const double v = fma(-ck[q], rj, w_[jj][q]);
-              w_[jj][q] = isp[q] ? rj : v;
-            }
-          }
-        }
+        for (int q = 0; q < RPL; ++q) w_[l][q] = isp[q] ? rinv : -ck[q] * rinv;
       }
       if (sing && lane == 0) s_sing = 1;
     }
@@ -482,18 +465,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_cl_kernel(const GjTask* __restr
           ck[q] = (i < N) ? cb[l * NR + i] : 0.0;
           isp[q] = i == p;
         }
-#pragma unroll
-        for (int jj = 0; jj < CPW; ++jj) {
-          double src = w_[jj][0];
-#pragma unroll
-          for (int q = 1; q < RPL; ++q) src = (qp == q) ? w_[jj][q] : src;
-          const double rj = __shfl_sync(0xffffffffu, src, lp) * rinv;
-#pragma unroll
-          for (int q = 0; q < RPL; ++q) {
-            const double v = fma(-ck[q], rj, w_[jj][q]);
-            w_[jj][q] = isp[q] ? rj : v;
-          }
-        }
+        gj_apply_step_dyn<CPW, RPL>(w_, ck, rinv, qp, lp, lane, -1);
       }
     }
   }
@@ -666,18 +638,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_cldf_kernel(const GjTask* __res
         ck[q] = (i < N) ? ckr[i] : 0.0;
         isp[q] = i == p;
       }
-#pragma unroll
-      for (int jj = 0; jj < CPW; ++jj) {
-        double src = w_[jj][0];
-#pragma unroll
-        for (int q = 1; q < RPL; ++q) src = (qp == q) ? w_[jj][q] : src;
-        const double rj = __shfl_sync(0xffffffffu, src, lp) * rinv;
-#pragma unroll
-        for (int q = 0; q < RPL; ++q) {
-          const double v = fma(-ck[q], rj, w_[jj][q]);
-          w_[jj][q] = isp[q] ? rj : v;
-        }
-      }
+        gj_apply_step_dyn<CPW, RPL>(w_, ck, rinv, qp, lp, lane, -1);
     }
   }
   const int sing = __any_sync(0xffffffffu, singular) ? 1 : 0;

@@ -7,6 +7,7 @@
 #define GJ_MB_TASKS 1, 128, 512
 #endif
 #include <cstdio>
+#include <cstring>
 #include <vector>
 #include <random>
 void hk_count_launch(int) {}
@@ -50,7 +51,11 @@ int main() {
         double s = 0; for (int k = 0; k < N; ++k) s += A[i + k * N] * O[k + j * N];
         err = std::max(err, std::fabs(s - (i == j)));
       }
-      printf("N=%3d tasks=%5d  %8.1f us/launch  err=%.1e  %s\n", N, ntask, ms * 100, err, cudaGetErrorString(cudaGetLastError()));
+      std::vector<double> all((size_t)ntask * N * N);
+      cudaMemcpy(all.data(), dO, all.size() * 8, cudaMemcpyDeviceToHost);
+      unsigned long long hsh = 1469598103934665603ull;
+      for (double v : all) { unsigned long long u; memcpy(&u, &v, 8); hsh = (hsh ^ u) * 1099511628211ull; }
+      printf("N=%3d tasks=%5d  %8.1f us/launch  err=%.1e  hash=%016llx %s\n", N, ntask, ms * 100, err, hsh, cudaGetErrorString(cudaGetLastError()));
       cudaFree(dA); cudaFree(dO); cudaFree(st); cudaFree(dt);
     }
   }
