@@ -1200,6 +1200,8 @@ struct Op {
   const int32_t* map = nullptr;
   int n = 0, maxN = 0;       // tasks / tiles, largest GJ order
   int ev = 0;
+  double flops = 0;          // GEMM: sum of 2 m n k over the tasks (profile labels)
+  int kmin = 0, kmax = 0;    // GEMM: range of the tasks' k (profile labels)
 };
 
 static hk_status stage_tiles(hk_plan* p, std::vector<Op>& ops, const TileList& tl, cudaStream_t st) {
@@ -1209,6 +1211,14 @@ static hk_status stage_tiles(hk_plan* p, std::vector<Op>& ops, const TileList& t
   o.map = p->stage.push(tl.map, st);
   if (!o.a || !o.map) return fail(HK_ERR_CUDA, "pinned staging allocation failed");
   o.n = tl.ntiles();
+  if (host_profile()) {
+    o.kmin = 1 << 30;
+    for (const GemmTask& t : tl.tasks) {
+      o.flops += 2.0 * t.m * t.n * t.k;
+      o.kmin = std::min(o.kmin, t.k);
+      o.kmax = std::max(o.kmax, t.k);
+    }
+  }
   ops.push_back(o);
   return HK_OK;
 }
@@ -1293,7 +1303,7 @@ static hk_status launch_ops(hk_plan* p, std::vector<Op>& ops, cudaStream_t st) {
     char lbl[64] = "";
     switch (o.kind) {
       case Op::COPY: CU(hk_launch_copy((const CopyTask*)o.a, o.n, st)); snprintf(lbl, 64, "copy x%d", o.n); break;
-      case Op::GEMM: CU(hk_launch_gemm((const GemmTask*)o.a, o.map, o.n, st)); snprintf(lbl, 64, "gemm %d tiles", o.n); break;
+      case Op::GEMM: CU(hk_launch_gemm((const GemmTask*)o.a, o.map, o.n, st)); snprintf(lbl, 64, "gemm %d tiles %.0f MF k %d-%d", o.n, o.flops * 1e-6, o.kmin, o.kmax); break;
       case Op::GJ: CU(hk_launch_gj((const GjTask*)o.a, o.n, o.maxN, st)); snprintf(lbl, 64, "gj x%d N<=%d", o.n, o.maxN); break;
       case Op::EVENT: CU(cudaEventRecord(p->ev[o.ev], st)); break;
     }
