@@ -353,6 +353,11 @@ struct hk_plan {
   int64_t g_per_col = 0;            // doubles of G/Yv scratch per rhs column (all fronts)
   std::map<std::pair<int, int>, SolveProg*> progs;
   std::vector<GmresGraph*> gmres_graphs;   // cached device-resident GMRES loops (hk_gmres_batch)
+  // TMA tensor map of the fronts for the leaf Gauss-Jordan (hk_gj_leaf_map)
+  alignas(64) unsigned char leafmap[128] = {};
+  const double* leafmap_base = nullptr;
+  int64_t leafmap_key[3] = {0, 0, 0};   // lda, fstride, batch
+  bool leafmap_ok = false;
   DevBuf Xin, X2, G, Yv;
   // timings
   double t_lowrank = 0, t_leaf = 0, t_schur = 0, t_aca = 0;
@@ -1195,7 +1200,7 @@ struct TileList {
 // A factorization phase is planned on the host into a list of ops whose task
 // arrays live in the pinned staging; flush() commits and launches them.
 struct Op {
-  enum Kind { COPY, GEMM, GJ, EVENT } kind;
+  enum Kind { COPY, GEMM, GJ, GJ_LEAF_TMA, EVENT } kind;
   const void* a = nullptr;   // device task array
   const int32_t* map = nullptr;
   int n = 0, maxN = 0;       // tasks / tiles, largest GJ order
@@ -1270,6 +1275,31 @@ static hk_status stage_gj(hk_plan* p, std::vector<Op>& ops, std::vector<GjTask>&
   return HK_OK;
 }
 
+// Leaf Gauss-Jordan through the TMA (HK_GJ_LEAF_TMA=0 turns it off): every leaf
+// is a row-major block of <= 64 of the fronts, and a tensor map of the fronts
+// can be encoded (16-byte aligned base and strides).  The map is cached per
+// (fronts pointer, lda, fstride, batch).
+static bool leaf_tma_ok(hk_plan* p, const std::vector<GjTask>& gts) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("HK_GJ_LEAF_TMA");
+    on = e ? atoi(e) : 1;
+  }
+  if (!on || gts.empty()) return false;
+  // the box origin's inner coordinate must sit on a 16-byte boundary (the TMA
+  // raises an illegal instruction otherwise): every leaf offset even
+  for (const GjTask& t : gts)
+    if (t.N > 64 || t.mode != 0 || t.src_ld != p->lda || ((t.src - p->A) & 1)) return false;
+  const int64_t key[3] = {p->lda, p->fstride, p->batch};
+  if (!(p->leafmap_ok && p->leafmap_base == p->A && key[0] == p->leafmap_key[0] &&
+        key[1] == p->leafmap_key[1] && key[2] == p->leafmap_key[2])) {
+    p->leafmap_ok = hk_gj_leaf_map(p->leafmap, p->A, p->n, p->lda, p->fstride, p->batch) == 0;
+    p->leafmap_base = p->A;
+    for (int i = 0; i < 3; ++i) p->leafmap_key[i] = key[i];
+  }
+  return p->leafmap_ok;
+}
+
 // HK_HOST_PROFILE: an event after every launched op gives in-situ per-op GPU
 // times (kernel + any idle gap before it) for the factorization.
 struct OpProfile {
@@ -1305,6 +1335,10 @@ static hk_status launch_ops(hk_plan* p, std::vector<Op>& ops, cudaStream_t st) {
       case Op::COPY: CU(hk_launch_copy((const CopyTask*)o.a, o.n, st)); snprintf(lbl, 64, "copy x%d", o.n); break;
       case Op::GEMM: CU(hk_launch_gemm((const GemmTask*)o.a, o.map, o.n, st)); snprintf(lbl, 64, "gemm %d tiles %.0f MF k %d-%d", o.n, o.flops * 1e-6, o.kmin, o.kmax); break;
       case Op::GJ: CU(hk_launch_gj((const GjTask*)o.a, o.n, o.maxN, st)); snprintf(lbl, 64, "gj x%d N<=%d", o.n, o.maxN); break;
+      case Op::GJ_LEAF_TMA:
+        CU(hk_launch_gj_leaf_tma((const GjTask*)o.a, o.n, p->leafmap, p->A, p->lda, p->fstride, st));
+        snprintf(lbl, 64, "gj leaves (TMA) x%d N<=%d", o.n, o.maxN);
+        break;
       case Op::EVENT: CU(cudaEventRecord(p->ev[o.ev], st)); break;
     }
     if (prof && lbl[0]) g_opprof.mark(lbl, st);
@@ -1519,7 +1553,16 @@ extern "C" hk_status hk_factor_ext(hk_plan* p, const double* Zext, int64_t ldz, 
         t.mode = 0;
         gts.push_back(t);
       }
-    CHK(stage_gj(p, ops, gts, st));
+    if (leaf_tma_ok(p, gts)) {
+      Op o{Op::GJ_LEAF_TMA};
+      o.a = p->stage.push(gts, st);
+      if (!o.a) return fail(HK_ERR_CUDA, "pinned staging allocation failed");
+      o.n = (int)gts.size();
+      o.maxN = 64;
+      ops.push_back(o);
+    } else {
+      CHK(stage_gj(p, ops, gts, st));
+    }
     TileList tl;
     for (int64_t f = grp_lo(g); f < grp_hi(g); ++f)
       for (int s : p->leaves) {

@@ -8,6 +8,8 @@
 // is partial (largest |entry| among rows not yet used, lowest row on ties), so
 // the singularity test min|pivot| < 1e-300 is the reference's
 // (src/dense.py:76-77).
+#include <cuda.h>
+
 #include "hk_common.cuh"
 #include "hk_internal.h"
 
@@ -213,8 +215,21 @@ __device__ __forceinline__ void st_release_cta(int* p, int v) {
   asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
 }
 
-template <int NW, int CPW, int RPL>
-__global__ void __launch_bounds__(NW * 32, 1) gj_df_kernel(const GjTask* __restrict__ tasks) {
+// Leaf tiles through the TMA: with a tensor map of the batch of row-major
+// fronts ([batch][n][n], box 64 x 64 x 1), the CTA stages its leaf block
+// K = A[lo:lo+N, lo:lo+N] into SMEM with one cp.async.bulk.tensor.3d (rows
+// beyond n are zero-filled by the TMA unit) and fills its registers from there,
+// instead of 32 row-strided global loads per warp instruction.  The block's
+// coordinates follow from its source pointer: src = A + f*fstride + lo*lda + lo.
+struct GjLeafMap {
+  const double* base;
+  int64_t lda, fstride;
+};
+
+template <int NW, int CPW, int RPL, bool TMA>
+__global__ void __launch_bounds__(NW * 32, 1) gj_df_kernel(const GjTask* __restrict__ tasks,
+                                                           const __grid_constant__ CUtensorMap tmap,
+                                                           GjLeafMap lm) {
   constexpr int NT = NW * 32;
   constexpr int NR = 32 * RPL;
   const GjTask t = tasks[blockIdx.x];
@@ -229,15 +244,47 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_df_kernel(const GjTask* __restr
     return;
   }
   double w_[CPW][RPL];
-#pragma unroll
-  for (int jj = 0; jj < CPW; ++jj)
-#pragma unroll
-    for (int q = 0; q < RPL; ++q) {
-      const int i = lane + 32 * q, j = warp * CPW + jj;
-      const bool in = i < N && j < N;
-      const int64_t off = t.mode == 0 ? (int64_t)i * t.src_ld + j : i + (int64_t)j * t.src_ld;
-      w_[jj][q] = in ? t.src[off] : 0.0;
+  if constexpr (TMA) {
+    // the 64 x 64 box lands in ckall (sized for it); ckall is rewritten only
+    // after every warp has moved the box into registers (barrier below)
+    __shared__ __align__(8) uint64_t bar;
+    // bulk tensor copies need a 128-byte aligned destination (launch adds 128 B)
+    double* stage = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(ckall) + 127) & ~uintptr_t(127));
+    if (tid == 0) {
+      const int64_t off = t.src - lm.base;
+      const int f = (int)(off / lm.fstride);
+      const int64_t rem = off - (int64_t)f * lm.fstride;
+      const int row = (int)(rem / lm.lda), col = (int)(rem - (int64_t)row * lm.lda);
+      mbar_init(&bar, 1);
+      mbar_init_fence();
+      mbar_arrive_tx(&bar, 64 * 64 * 8);
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(stage)),
+          "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(col), "r"(row), "r"(f), "r"(smem_u32(&bar))
+          : "memory");
     }
+    __syncthreads();
+    mbar_wait(&bar, 0);
+#pragma unroll
+    for (int jj = 0; jj < CPW; ++jj)
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) {
+        const int i = lane + 32 * q, j = warp * CPW + jj;
+        w_[jj][q] = (i < N && j < N) ? stage[i * 64 + j] : 0.0;
+      }
+    __syncthreads();
+  } else {
+#pragma unroll
+    for (int jj = 0; jj < CPW; ++jj)
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) {
+        const int i = lane + 32 * q, j = warp * CPW + jj;
+        const bool in = i < N && j < N;
+        const int64_t off = t.mode == 0 ? (int64_t)i * t.src_ld + j : i + (int64_t)j * t.src_ld;
+        w_[jj][q] = in ? t.src[off] : 0.0;
+      }
+  }
   unsigned used = 0;
   if (tid == 0) s_pub = 0;
   __syncthreads();
@@ -782,13 +829,14 @@ static cudaError_t launch_gj_reg(const GjTask* tasks_dev, int ntasks, int maxN, 
     const size_t smem = (size_t)maxN * 32 * RPL * 8;
     static bool attr = false;   // one attribute call per instantiation
     if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(gj_df_kernel<NW, CPW, RPL>,
+      cudaError_t e = cudaFuncSetAttribute(gj_df_kernel<NW, CPW, RPL, false>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)((size_t)NW * CPW * 32 * RPL * 8));
       if (e != cudaSuccess) return e;
       attr = true;
     }
-    gj_df_kernel<NW, CPW, RPL><<<ntasks, NW * 32, smem, st>>>(tasks_dev);
+    CUtensorMap none{};
+    gj_df_kernel<NW, CPW, RPL, false><<<ntasks, NW * 32, smem, st>>>(tasks_dev, none, GjLeafMap{});
   }
   hk_count_launch();
   return cudaGetLastError();
@@ -878,6 +926,57 @@ cudaError_t hk_launch_gj(const GjTask* tasks_dev, int ntasks, int maxN, cudaStre
   }
   hk_count_launch();
   return cudaGetLastError();
+}
+
+// Leaf Gauss-Jordan inverses (N <= 64, row-major blocks of the fronts) with
+// the blocks staged by the TMA (tensor map built by the caller, hk_gj_leaf_map).
+cudaError_t hk_launch_gj_leaf_tma(const GjTask* tasks_dev, int ntasks, const void* tmap,
+                                  const double* base, int64_t lda, int64_t fstride,
+                                  cudaStream_t st) {
+  if (ntasks == 0) return cudaSuccess;
+  constexpr size_t smem = (size_t)64 * 64 * 8 + 128;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gj_df_kernel<8, 8, 2, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  gj_df_kernel<8, 8, 2, true><<<ntasks, 256, smem, st>>>(
+      tasks_dev, *static_cast<const CUtensorMap*>(tmap), GjLeafMap{base, lda, fstride});
+  hk_count_launch();
+  return cudaGetLastError();
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda
+// at link time): a [batch][n][n] row-major fp64 tensor, box 64 x 64 x 1.
+int hk_gj_leaf_map(void* out, const double* base, int64_t n, int64_t lda, int64_t fstride,
+                   int64_t batch) {
+  typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                               CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  }
+  if (!fn) return 1;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (lda * 8) % 16 || (fstride * 8) % 16) return 1;
+  const cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)batch};
+  const cuuint64_t strides[2] = {(cuuint64_t)lda * 8, (cuuint64_t)fstride * 8};
+  const cuuint32_t box[3] = {64, 64, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = fn(static_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+                        const_cast<double*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : 1;
 }
 
 size_t hk_gj_scratch_bytes(int N) {

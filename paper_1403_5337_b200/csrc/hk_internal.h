@@ -274,6 +274,13 @@ struct GjTask {
 // partial-pivot LU of S (hodlr.py:272-277; api.cpp hk_factor_ext).
 #define HK_NEAR_PIVOT 1e-8
 cudaError_t hk_launch_gj(const GjTask* tasks_dev, int ntasks, int maxN, cudaStream_t st);
+// leaf inverses (N <= 64, mode 0 blocks of the fronts) staged by the TMA; tmap is
+// a CUtensorMap (128 bytes) from hk_gj_leaf_map over the same fronts
+cudaError_t hk_launch_gj_leaf_tma(const GjTask* tasks_dev, int ntasks, const void* tmap,
+                                  const double* base, int64_t lda, int64_t fstride,
+                                  cudaStream_t st);
+int hk_gj_leaf_map(void* out, const double* base, int64_t n, int64_t lda, int64_t fstride,
+                   int64_t batch);   // 0 on success
 size_t hk_gj_scratch_bytes(int N);     // 0 when N fits SMEM
 
 // ---------------------------------------------------------------- validation (validate.cpp)
