@@ -184,6 +184,37 @@ def make_front(seed, device):
     return fg.layered_grid_front(DIMS, 2, PLANE, conductivity=kc, device=device, return_torch=True)
 
 
+def frontgen_flops(n, dims=DIMS, plane=PLANE):
+    """FP64 flops of one front's plane-by-plane elimination: every eliminated
+    layer (all but the separator plane) costs one n x n inverse, 2 n^3."""
+    return (dims[2] - 1) * 2.0 * n ** 3
+
+
+def make_fronts(seeds, device, chunk=64):
+    """The config-3 fronts of `seeds`, generated on the GPU in batches of
+    `chunk` (frontgen.layered_grid_fronts: this library's batched block
+    Gauss-Jordan, hk_spd_inverse).  Input manufacture -- timed and reported
+    (`frontgen`), part of no metric."""
+    import torch
+    from paper_1403_5337_b200 import frontgen as fg
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    parts = []
+    for i in range(0, len(seeds), chunk):
+        kcs = [fg.cell_conductivity(DIMS, s) for s in seeds[i:i + chunk]]
+        parts.append(fg.layered_grid_fronts(DIMS, 2, PLANE, kcs, device=device))
+    fronts = torch.cat(parts).contiguous()
+    torch.cuda.synchronize()
+    secs = time.perf_counter() - t0
+    n = fronts.shape[1]
+    fl = frontgen_flops(n) * len(seeds)
+    return fronts, {"fronts": len(seeds), "seconds": secs, "ms_per_front": 1e3 * secs / len(seeds),
+                    "flops": fl, "tflops": fl / secs / 1e12, "solver": fg.frontgen_solver(),
+                    "method": "plane-by-plane elimination, batched block Gauss-Jordan inverses "
+                              "(hk_spd_inverse: 64 x 64 pivot blocks, DMMA GEMM updates), wall "
+                              "time incl. host-side layer assembly"}
+
+
 def rhs_for(seed, n):
     return np.random.default_rng(seed).standard_normal(n)
 
@@ -370,7 +401,7 @@ def run_ours(args):
     init_dist("nccl", dev)
     F = args.fronts_per_gpu
     seeds = MF.shard_range(rank, world, F)
-    fronts = torch.stack([make_front(s, dev) for s in seeds]).contiguous()
+    fronts, gen = make_fronts(list(seeds), dev)
     n = fronts.shape[1]
     rhs = torch.from_numpy(np.stack([rhs_for(s, n) for s in seeds])).to(dev)
     work = torch.empty_like(rhs)
@@ -580,7 +611,7 @@ def run_ours(args):
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roof,
                 "rooflines": rooflines,
                 "cpu_baseline": cpu, "gmres": gm, "cfg0": c0, "level": lvl, "cfg4": c4,
-                "cfg1": c1, "cfg2": c2,
+                "cfg1": c1, "cfg2": c2, "frontgen": gen,
                 "ranks_per_level_front0": [e["max_rank"] for e in batch.report(0).ranks_per_level],
                 "fronts_gathered": int(all_ranks.shape[0]),
                 "max_block_rank_all_fronts": int(all_ranks.max())}
@@ -786,12 +817,9 @@ def run_level(dev, nfronts, stream):
     import torch
     import paper_1403_5337_b200 as hk
     from paper_1403_5337_b200.hodlr import HodlrBatch
-    t0 = time.perf_counter()
-    fronts = torch.empty(nfronts, 1024, 1024, dtype=torch.float64, device=dev)
-    for s in range(nfronts):
-        fronts[s] = make_front(s, dev)
+    fronts, gen = make_fronts(list(range(nfronts)), dev)
     rhs = torch.from_numpy(np.stack([rhs_for(s, 1024) for s in range(nfronts)])).to(dev)
-    gen_s = time.perf_counter() - t0
+    gen_s = gen["seconds"]
     work = torch.empty_like(rhs)
     cfg = hk.CompressionConfig(scheme="aca", tol=TOL)
     batch = HodlrBatch(1024, LEAF, nfronts)

@@ -151,6 +151,15 @@ hk_status hk_dgemm(int transa, int64_t m, int64_t n, int64_t k, double alpha, co
  * n*n; status_host[b] = 1 when matrix b is singular. */
 hk_status hk_gj_inverse(const double* A, int64_t n, int64_t lda, int64_t batch, int64_t stride,
                         double* out, int32_t* status_host, void* stream);
+
+/* In-place inverses of `batch` symmetric positive definite n x n matrices
+ * (leading dimension lda, matrix stride `stride` elements) by block
+ * Gauss-Jordan with 64 x 64 pivot blocks (128 for n > 2048) on the DMMA GEMM; status_host[b] = 1
+ * if a pivot block of matrix b was singular.  Replaces torch.linalg.solve
+ * (cuSOLVER) in the plane-by-plane front elimination (frontgen.py; the
+ * reference's dense elimination src/frontgen.py:159-189). */
+hk_status hk_spd_inverse(double* A, int64_t n, int64_t lda, int64_t batch, int64_t stride,
+                         int32_t* status_host, void* stream);
 /* Factor views for the test-visible attributes of HodlrFactorization
  * (hodlr.py:105-154): leaf LU (b x b row-major packed, LAPACK-style 0-based
  * swap indices `piv`) and per internal node d_left (na x r_u), d_right

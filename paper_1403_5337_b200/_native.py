@@ -72,6 +72,7 @@ SIGNATURES = {
     "hk_get_aca_time": (C.c_int, [P, PD]),
     "hk_launch_count": (I64, []),
     "hk_debug_violations": (I64, [C.POINTER(I64)]),
+    "hk_spd_inverse": (C.c_int, [P, I64, I64, I64, I64, PI32, P]),
 }
 
 HK_OK = 0

@@ -2766,6 +2766,139 @@ extern "C" hk_status hk_gj_inverse(const double* A, int64_t n, int64_t lda, int6
   return HK_OK;
 }
 
+// In-place inverses of `batch` symmetric positive definite n x n matrices
+// (column-major view, leading dimension lda, matrix stride `stride`) by block
+// Gauss-Jordan with 64 x 64 pivot blocks (128 for n > 2048): per block k, P = A_kk^{-1}
+// (Gauss-Jordan kernel, partial pivoting inside the block), R = P A_k*,
+// A_ij -= A_ik R_kj (DMMA GEMM, the 2 n^2 b flops of the step), A_ik = -A_ik P,
+// A_kj = R_kj, A_kk = P -- every front of the batch in the same launches.
+// No pivoting across blocks: the fronts' plane Schur complements are SPD.
+// Used by frontgen's plane-by-plane elimination (the step before the path,
+// SURVEY.md §8(f)#1).  status_host[b] = 1 if a pivot block of matrix b was
+// singular.  A row-major matrix is the transpose of its column-major view, and
+// (A^T)^{-1} = (A^{-1})^T, so row-major input works unchanged.
+extern "C" hk_status hk_spd_inverse(double* A, int64_t n, int64_t lda, int64_t batch,
+                                    int64_t stride, int32_t* status_host, void* stream) {
+  if (hk_device_count() == 0) return fail(HK_ERR_CUDA, "no CUDA device visible");
+  if (n < 0 || batch < 0 || lda < n) return fail(HK_ERR_VALUE, "bad spd_inverse dimensions");
+  if (n == 0 || batch == 0) return HK_OK;
+  if (n > INT32_MAX / 2) return fail(HK_ERR_VALUE, "spd_inverse matrix too large");
+  if (batch > 1 && stride < lda * n) return fail(HK_ERR_DIMENSION, "matrix stride too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  // pivot blocks of 64 (128 above n = 2048: the trailing GEMMs' K doubles,
+  // which lifts the DMMA kernel from ~10 to ~20 TFLOP/s; the register-resident
+  // Gauss-Jordan still takes 128 x 128)
+  const int64_t NB = n > 2048 ? 128 : 64;
+  const int64_t per = NB * NB + 2 * NB * n;             // P, R (NB x n), Cc (n x NB)
+  double* scr = nullptr;
+  int32_t* stt = nullptr;
+  CU(hk_dev_malloc((void**)&scr, (size_t)batch * per * 8, st));
+  const int64_t nsteps = (n + NB - 1) / NB;   // one status per (front, pivot block)
+  CU(hk_dev_malloc((void**)&stt, (size_t)batch * nsteps * 4, st));
+  CU(cudaMemsetAsync(stt, 0, (size_t)batch * nsteps * 4, st));
+  // task arrays of every block step of one call, in one pinned arena (the call
+  // synchronises at the end, before a later call may rewrite it)
+  static Staging stage;
+  stage.reset();
+  std::vector<Op> ops;
+  hk_status rc = HK_OK;
+  for (int64_t k0 = 0; k0 < n && rc == HK_OK; k0 += NB) {
+    const int64_t k1 = std::min(n, k0 + NB), b = k1 - k0;
+    std::vector<GjTask> gts;
+    TileList trc, tup;
+    std::vector<CopyTask> cps;
+    for (int64_t f = 0; f < batch; ++f) {
+      double* Af = A + f * stride;
+      double* P = scr + f * per;
+      double* R = P + NB * NB;            // b x n, ld NB
+      double* Cc = R + NB * n;            // n x b, ld n
+      GjTask g{};
+      g.src = Af + k0 + k0 * lda; g.src_ld = lda; g.mode = 1;
+      g.out = P; g.out_ld = NB; g.status = stt + f * nsteps + k0 / NB; g.N = (int32_t)b;
+      gts.push_back(g);
+      // R = P A[k, :];  Cc = -A[:, k] P   (both read the pre-step A)
+      trc.add(gemm(P, NB, 0, Af + k0, lda, R, NB, (int)b, (int)n, (int)b, 1.0, 0.0));
+      trc.add(gemm(Af + k0 * lda, lda, 0, P, NB, Cc, n, (int)n, (int)b, (int)b, -1.0, 0.0));
+      // A_ij -= A_ik R_kj for i, j outside block k
+      const int64_t rr[2][2] = {{0, k0}, {k1, n}};
+      for (auto& ri : rr)
+        for (auto& cj : rr) {
+          const int64_t mi = ri[1] - ri[0], nj = cj[1] - cj[0];
+          if (mi <= 0 || nj <= 0) continue;
+          tup.add(gemm(Af + k0 * lda + ri[0], lda, 0, R + cj[0] * NB, NB, Af + ri[0] + cj[0] * lda,
+                       lda, (int)mi, (int)nj, (int)b, -1.0, 1.0));
+        }
+      // write back: column block (rows outside k) <- Cc, row block <- R, A_kk <- P
+      for (auto& ri : rr) {
+        if (ri[1] <= ri[0]) continue;
+        CopyTask c{};
+        c.src = Cc + ri[0]; c.src_rs = 1; c.src_cs = n;
+        c.dst = Af + ri[0] + k0 * lda; c.dst_rs = 1; c.dst_cs = lda;
+        c.rows = (int)(ri[1] - ri[0]); c.cols = (int)b;
+        cps.push_back(c);
+        CopyTask d{};
+        d.src = R + ri[0] * NB; d.src_rs = 1; d.src_cs = NB;
+        d.dst = Af + k0 + ri[0] * lda; d.dst_rs = 1; d.dst_cs = lda;
+        d.rows = (int)b; d.cols = (int)(ri[1] - ri[0]);
+        cps.push_back(d);
+      }
+      CopyTask e{};
+      e.src = P; e.src_rs = 1; e.src_cs = NB;
+      e.dst = Af + k0 + k0 * lda; e.dst_rs = 1; e.dst_cs = lda;
+      e.rows = (int)b; e.cols = (int)b;
+      cps.push_back(e);
+    }
+    // the GJ tasks read A_kk; the copies rewrite it last
+    {
+      Op o{Op::GJ};
+      o.a = stage.push(gts, st);
+      o.n = (int)gts.size();
+      o.maxN = (int)b;
+      if (!o.a) { rc = fail(HK_ERR_CUDA, "pinned staging allocation failed"); break; }
+      ops.push_back(o);
+    }
+    for (TileList* tl : {&trc, &tup}) {
+      if (tl->ntiles() == 0) continue;
+      Op o{Op::GEMM};
+      o.a = stage.push(tl->tasks, st);
+      o.map = stage.push(tl->map, st);
+      o.n = tl->ntiles();
+      if (!o.a || !o.map) { rc = fail(HK_ERR_CUDA, "pinned staging allocation failed"); break; }
+      ops.push_back(o);
+    }
+    if (rc != HK_OK) break;
+    Op o{Op::COPY};
+    o.a = stage.push(cps, st);
+    o.n = (int)cps.size();
+    if (!o.a) { rc = fail(HK_ERR_CUDA, "pinned staging allocation failed"); break; }
+    ops.push_back(o);
+    if (stage.commit(st) != cudaSuccess) { rc = fail(HK_ERR_CUDA, "staging commit failed"); break; }
+    for (const Op& op : ops) {
+      cudaError_t e = cudaSuccess;
+      switch (op.kind) {
+        case Op::GJ: e = hk_launch_gj((const GjTask*)op.a, op.n, op.maxN, st); break;
+        case Op::GEMM: e = hk_launch_gemm((const GemmTask*)op.a, op.map, op.n, st); break;
+        case Op::COPY: e = hk_launch_copy((const CopyTask*)op.a, op.n, st); break;
+        default: break;
+      }
+      if (e != cudaSuccess) { rc = fail(HK_ERR_CUDA, cudaGetErrorString(e)); break; }
+    }
+    ops.clear();
+  }
+  std::vector<int32_t> sh((size_t)batch * nsteps, 0);
+  if (rc == HK_OK)
+    CU(cudaMemcpyAsync(sh.data(), stt, sh.size() * 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  for (int64_t f = 0; f < batch; ++f) {
+    int32_t any = 0;
+    for (int64_t k = 0; k < nsteps; ++k) any |= sh[(size_t)(f * nsteps + k)];
+    status_host[f] = any ? 1 : 0;
+  }
+  hk_dev_free(scr, st);
+  hk_dev_free(stt, st);
+  return rc;
+}
+
 extern "C" hk_status hk_aca_block(const double* a, int64_t m, int64_t n, int64_t ld, double tol2,
                                   int64_t cap, double* U, double* V, int64_t* rank,
                                   int32_t* trows, int64_t* nrows, int32_t* tcols, int64_t* ncols,

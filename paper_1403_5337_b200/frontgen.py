@@ -232,6 +232,25 @@ def _edge_weights(dims, kcell):
     return out
 
 
+def frontgen_solver() -> str:
+    """Dense inverse behind the GPU plane elimination: "hk" (this library's
+    block Gauss-Jordan, the default) or "torch" (cuSOLVER); HK_FRONTGEN picks."""
+    import os
+    return os.environ.get("HK_FRONTGEN", "hk")
+
+
+def _spd_inverse_(X):
+    """In place: X[b] <- X[b]^{-1} for a contiguous CUDA float64 (B, n, n) batch
+    of SPD matrices (hk_spd_inverse: block Gauss-Jordan, one call per batch)."""
+    import ctypes
+    from . import _native as N
+    B, n = X.shape[0], X.shape[1]
+    st = (ctypes.c_int32 * B)()
+    N.check(N.lib().hk_spd_inverse(N.ptr(X), n, n, B, n * n, st, N.stream_handle()))
+    if any(st):
+        raise ValueError("plane elimination: singular pivot block in a layer Schur complement")
+
+
 def layered_grid_front(dims, axis, plane, conductivity=None, device=None,
                        dtype=None, return_torch=False):
     """Separator front of a scalar grid Laplacian by plane-by-plane elimination.
@@ -241,6 +260,18 @@ def layered_grid_front(dims, axis, plane, conductivity=None, device=None,
     n x n front (numpy, or a torch tensor on ``device``) with rows ordered like
     src/frontgen.py:126-156 orders the separator.
     """
+    F = layered_grid_fronts(dims, axis, plane, [conductivity], device=device, dtype=dtype)[0]
+    if return_torch:
+        return F
+    return F.cpu().numpy()
+
+
+def layered_grid_fronts(dims, axis, plane, conductivities, device=None, dtype=None):
+    """The fronts of several conductivity fields of one grid (a batch of the
+    multifrontal level of config 3), eliminated together: every plane step
+    inverts the whole batch's layer Schur complements in one hk_spd_inverse
+    call (block Gauss-Jordan on the DMMA GEMM) on the GPU.  Returns a
+    (len(conductivities), n, n) torch tensor on ``device``."""
     torch = _torch()
     dims = tuple(int(x) for x in dims)
     d = len(dims)
@@ -251,28 +282,35 @@ def layered_grid_front(dims, axis, plane, conductivity=None, device=None,
         raise InvalidPlaneError(f"plane {plane} is not strictly interior to extent {ext}")
     dev = torch.device(device or "cpu")
     dt = dtype or torch.float64
-    w = _edge_weights(dims, conductivity)
     # move the separator axis to the front; remaining axes keep their order
     perm = [axis] + [b for b in range(d) if b != axis]
-    wl = [np.transpose(w[b], perm) for b in range(d)]
+    wls = []
+    for kc in conductivities:
+        w = _edge_weights(dims, kc)
+        wls.append([np.transpose(w[b], perm) for b in range(d)])
+    B = len(wls)
     layer_shape = tuple(dims[b] for b in perm[1:])
     nl = int(np.prod(layer_shape)) if layer_shape else 1
     ids = np.arange(nl).reshape(layer_shape)
 
+    # every front of the batch has the same stencil pattern: stack the weights
+    # (leading batch axis) and scatter all fronts' layer operators at once
+    wlb = [np.stack([wl[b] for wl in wls]) for b in range(d)]
+
     def layer_matrix(t):
-        """In-layer operator T_t (nl x nl)."""
-        diag = np.zeros(layer_shape)
+        """In-layer operators T_t of the batch (B x nl x nl)."""
+        diag = np.zeros((B,) + layer_shape)
         # edges along the separator axis: t and t+1 (in w's indexing)
-        wa = wl[axis]
-        diag += wa[t] + wa[t + 1]
+        wa = wlb[axis]
+        diag += wa[:, t] + wa[:, t + 1]
         rows, cols, vals = [], [], []
         for j, b in enumerate(perm[1:]):
-            wb = wl[b][t]                         # shape: layer dims with +1 on axis j
+            wb = wlb[b][:, t]                     # (B, layer dims with +1 on axis j)
             n_b = layer_shape[j]
-            lo = [slice(None)] * len(layer_shape)
-            hi = [slice(None)] * len(layer_shape)
-            lo[j] = slice(0, n_b)
-            hi[j] = slice(1, n_b + 1)
+            lo = [slice(None)] * (len(layer_shape) + 1)
+            hi = [slice(None)] * (len(layer_shape) + 1)
+            lo[j + 1] = slice(0, n_b)
+            hi[j + 1] = slice(1, n_b + 1)
             diag += wb[tuple(lo)] + wb[tuple(hi)]
             if n_b > 1:
                 a_sl = [slice(None)] * len(layer_shape)
@@ -281,32 +319,44 @@ def layered_grid_front(dims, axis, plane, conductivity=None, device=None,
                 inner[j] = slice(1, n_b)
                 src = ids[tuple(a_sl)].ravel()
                 dst = ids[tuple(inner)].ravel()
-                ww = wb[tuple(inner)].ravel()
+                ww = wb[(slice(None),) + tuple(inner)].reshape(B, -1)
                 rows += [src, dst]
                 cols += [dst, src]
                 vals += [-ww, -ww]
-        T = torch.zeros((nl, nl), dtype=dt, device=dev)
+        T = torch.zeros((B, nl, nl), dtype=dt, device=dev)
         if rows:
             r = torch.from_numpy(np.concatenate(rows)).to(dev)
             c = torch.from_numpy(np.concatenate(cols)).to(dev)
-            v = torch.from_numpy(np.concatenate(vals)).to(device=dev, dtype=dt)
-            T[r, c] = v
+            v = torch.from_numpy(np.concatenate(vals, axis=1)).to(device=dev, dtype=dt)
+            T[:, r, c] = v
         idx = torch.arange(nl, device=dev)
-        T[idx, idx] = torch.from_numpy(diag.ravel()).to(device=dev, dtype=dt)
+        T[:, idx, idx] = torch.from_numpy(diag.reshape(B, nl)).to(device=dev, dtype=dt)
         return T
 
     def coupling(t):
-        """Diagonal of the coupling between layers t-1 and t (edge t)."""
-        return torch.from_numpy(np.ascontiguousarray(wl[axis][t]).ravel()).to(device=dev, dtype=dt)
+        """Diagonals of the coupling between layers t-1 and t (edge t), B x nl."""
+        return torch.from_numpy(np.ascontiguousarray(wlb[axis][:, t]).reshape(B, -1)).to(
+            device=dev, dtype=dt)
+
+    use_hk = dev.type == "cuda" and dt == torch.float64 and frontgen_solver() == "hk"
+
+    def schur_term(D, c):
+        """C D^{-1} C for the batch (C = diag(c)): this library's block
+        Gauss-Jordan on the GPU, torch.linalg.solve (cuSOLVER / LAPACK) otherwise."""
+        if use_hk:
+            X = D.contiguous().clone()
+            _spd_inverse_(X)
+            return c[:, :, None] * X * c[:, None, :]
+        return c[:, :, None] * torch.linalg.solve(D, torch.diag_embed(c))
 
     def eliminate(order):
-        """Schur complement contribution of the layers in ``order`` (far to near)."""
+        """Schur complement of the layers in ``order`` (far to near):
+        D_k = T_k - C D_{k-1}^{-1} C with C the diagonal plane coupling."""
         D = None
         for k, t in enumerate(order):
             T = layer_matrix(t)
             if D is not None:
-                c = coupling(max(t, order[k - 1]))
-                T = T - c[:, None] * torch.linalg.solve(D, torch.diag(c))
+                T = T - schur_term(D, coupling(max(t, order[k - 1])))
             D = T
         return D
 
@@ -317,14 +367,11 @@ def layered_grid_front(dims, axis, plane, conductivity=None, device=None,
         if not layers:
             continue
         D = eliminate(layers)
-        c = coupling(max(plane, layers[-1]))
         try:
-            front = front - c[:, None] * torch.linalg.solve(D, torch.diag(c))
-        except RuntimeError as exc:
+            front = front - schur_term(D, coupling(max(plane, layers[-1])))
+        except (RuntimeError, ValueError) as exc:
             raise SingularInteriorError(str(exc)) from exc
-    if return_torch:
-        return front
-    return front.cpu().numpy()
+    return front
 
 
 def grid_graph(spec: GridSpec, axis, plane) -> SparsePattern:
