@@ -2553,10 +2553,15 @@ static hk_status gmres_run(hk_plan* p, int64_t front, const double* A, int64_t l
   }
   CU(cudaMemcpyAsync(g->B.p, B, (size_t)n * s * 8, cudaMemcpyDeviceToDevice, st));
   CU(cudaGraphLaunch(g->main, st));
+  // the state, the iterates and the histories in one round trip (the usual
+  // case: the loop finished inside the first graph launch)
   GmState hs{};
   CU(cudaMemcpyAsync(&hs, g->state.p, sizeof(GmState), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(X, g->X.p, (size_t)n * s * 8, cudaMemcpyDeviceToDevice, st));
+  CU(cudaMemcpyAsync(history, g->hist.p, (size_t)s * max_iter * 8, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
   long long launched = g->k_pre + g->k_post + g->k_body * hs.k;
+  const bool resumed = !hs.finished;
   while (!hs.finished) {                        // Krylov capacity exhausted: grow, resume
     const int64_t k0 = hs.k;
     CHK(gm_grow(p, g, std::min<int64_t>(mmax, 4 * g->cap), st));
@@ -2569,9 +2574,11 @@ static hk_status gmres_run(hk_plan* p, int64_t front, const double* A, int64_t l
     g->main = nullptr;
   }
   hk_count_launch((int)launched);
-  CU(cudaMemcpyAsync(X, g->X.p, (size_t)n * s * 8, cudaMemcpyDeviceToDevice, st));
-  CU(cudaMemcpyAsync(history, g->hist.p, (size_t)s * max_iter * 8, cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
+  if (resumed) {
+    CU(cudaMemcpyAsync(X, g->X.p, (size_t)n * s * 8, cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemcpyAsync(history, g->hist.p, (size_t)s * max_iter * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+  }
   hk_status rc = HK_OK;
   for (int64_t c = 0; c < s; ++c) {
     iterations[c] = hs.m[c];
