@@ -275,12 +275,6 @@ struct SolveProg {
   const int32_t* leaf_map = nullptr;
   int leaf_tiles = 0;
   DevBuf pbuf;          // partial dot products of one level (levels reuse it in stream order)
-  // fused variant: one thread-block cluster per front runs all its phases
-  // (solve_fused_kernel); partial dots then need a region per level
-  bool fused = false;
-  const FusedPhase* fphases = nullptr;
-  int nph = 0, nfronts = 0, fP = 8;
-  size_t fsmem = 0;
   // the kernel sequence is captured into a CUDA graph at its second use (a
   // GMRES run applies the same program every iteration); one graph launch
   // then replaces 3 launches per level
@@ -1909,17 +1903,6 @@ static hk_status build_solve_prog(hk_plan* p, int front, int s, SolveProg*& out,
   sp->s = s;
   sp->small = s <= 16;
   const int64_t n = p->n;
-  // fused per-front cluster program (HK_SOLVE_FUSED=1, opt-in): measured
-  // slower than the split kernels for one front (0.086 vs 0.064 ms, cfg3) and
-  // only ~10% faster for the 64-front batch at 4-CTA clusters
-  {
-    const char* e = getenv("HK_SOLVE_FUSED");
-    const int mode = e ? atoi(e) : -1;
-    sp->fused = sp->small && mode == 1;
-    const char* ep = getenv("HK_SOLVE_FUSED_P");
-    sp->fP = ep ? atoi(ep) : 16;
-    if (sp->fP != 16) sp->fP = sp->fP >= 8 ? 8 : (sp->fP >= 4 ? 4 : 2);
-  }
   const int nn = (int)p->nodes.size();
   const size_t nb = p->blocks.size();
   const double* UV = p->UV.as<double>();
@@ -1930,16 +1913,12 @@ static hk_status build_solve_prog(hk_plan* p, int front, int s, SolveProg*& out,
   double* Yv = p->Yv.as<double>();
   const int64_t xs = n * s;  // per-front stride of Xin/X2
   int64_t f0 = front < 0 ? 0 : front, f1 = front < 0 ? p->batch : front + 1;
-  // per-front item ranges of every phase (fused variant): [front] -> start, plus the end
-  std::vector<int> leaf_start;
-  std::vector<std::vector<int>> lv_pstart, lv_sstart, lv_ustart;
   // leaves
   {
     std::vector<SgemvTask> sg;
     std::vector<int32_t> items;
     TileList tl;
     for (int64_t f = f0; f < f1; ++f) {
-      leaf_start.push_back((int)(items.size() / 2));
       for (int slot : p->leaves) {
         const Node& nd = p->nodes[slot];
         const NodeRec& r = p->rec[f * nn + slot];
@@ -1961,7 +1940,6 @@ static hk_status build_solve_prog(hk_plan* p, int front, int s, SolveProg*& out,
         }
       }
     }
-    leaf_start.push_back((int)(items.size() / 2));
     if (sp->small) {
       sp->leaf.t = p->pstage.push(sg, st);
       sp->leaf.items = p->pstage.push(items, st);
@@ -1988,29 +1966,22 @@ static hk_status build_solve_prog(hk_plan* p, int front, int s, SolveProg*& out,
           const int64_t nbr = p->nodes[nd.right].hi - p->nodes[nd.right].lo;
           lv += ((na + HK_PDOT_ROWS - 1) / HK_PDOT_ROWS) * r.rl + ((nbr + HK_PDOT_ROWS - 1) / HK_PDOT_ROWS) * r.ru;
         }
-      need = sp->fused ? need + lv : std::max(need, lv);
+      need = std::max(need, lv);
     }
     if (sp->pbuf.ensure((size_t)need * s * 8 + 64, st) != cudaSuccess) {
       delete sp;
       return fail(HK_ERR_CUDA, "solve scratch allocation failed");
     }
   }
-  int64_t poff = 0;   // doubles into pbuf
   for (int lvl = p->depth - 1; lvl >= 0; --lvl) {
     SolveProg::Level L;
     std::vector<PdotTask> pd;
     std::vector<int32_t> pitems, sitems, uitems;
     std::vector<SgemvTask> sv, up;
     TileList t1, t2, t3;
-    // fused: every level owns its own partial-dot region (the fronts' clusters
-    // run their levels concurrently); split: levels reuse one region in stream order
-    if (!sp->fused) poff = 0;
+    int64_t poff = 0;   // doubles into pbuf (levels reuse it in stream order)
     double* P = sp->pbuf.as<double>();
-    std::vector<int> ps, ss, us;
     for (int64_t f = f0; f < f1; ++f) {
-      ps.push_back((int)(pitems.size() / 3));
-      ss.push_back((int)(sitems.size() / 2));
-      us.push_back((int)(uitems.size() / 2));
       for (int k = 0; k < (int)p->internal.size(); ++k) {
         const int slot = p->internal[k];
         const Node& nd = p->nodes[slot];
@@ -2086,12 +2057,6 @@ static hk_status build_solve_prog(hk_plan* p, int front, int s, SolveProg*& out,
         }
       }
     }
-    ps.push_back((int)(pitems.size() / 3));
-    ss.push_back((int)(sitems.size() / 2));
-    us.push_back((int)(uitems.size() / 2));
-    lv_pstart.push_back(ps);
-    lv_sstart.push_back(ss);
-    lv_ustart.push_back(us);
     bool ok = true;
     if (sp->small) {
       L.n_pdot = (int)(pitems.size() / 3);
@@ -2115,28 +2080,6 @@ static hk_status build_solve_prog(hk_plan* p, int front, int s, SolveProg*& out,
     sp->levels.push_back(std::move(L));
   }
   (void)nb;
-  if (sp->fused) {
-    const int nf = (int)(f1 - f0);
-    std::vector<FusedPhase> ph;
-    int max_k = sp->leaf.max_k;
-    for (int fi = 0; fi < nf; ++fi) {
-      ph.push_back(FusedPhase{1, leaf_start[fi + 1] - leaf_start[fi], sp->leaf.t,
-                              sp->leaf.items + 2 * leaf_start[fi]});
-      for (size_t li = 0; li < sp->levels.size(); ++li) {
-        const SolveProg::Level& L = sp->levels[li];
-        const auto &ps = lv_pstart[li], &ss = lv_sstart[li], &us = lv_ustart[li];
-        ph.push_back(FusedPhase{0, ps[fi + 1] - ps[fi], L.pdot_t, L.pdot_items + 3 * ps[fi]});
-        ph.push_back(FusedPhase{1, ss[fi + 1] - ss[fi], L.sinv.t, L.sinv.items + 2 * ss[fi]});
-        ph.push_back(FusedPhase{1, us[fi + 1] - us[fi], L.upd.t, L.upd.items + 2 * us[fi]});
-        if (fi == 0) max_k = std::max(max_k, std::max(L.sinv.max_k, L.upd.max_k));
-      }
-    }
-    sp->nph = 1 + 3 * (int)sp->levels.size();
-    sp->nfronts = nf;
-    sp->fsmem = ((size_t)max_k * s + 256 * (size_t)s) * 8;
-    sp->fphases = p->pstage.push(ph, st);
-    if (!sp->fphases) { delete sp; return fail(HK_ERR_CUDA, "pinned staging allocation failed"); }
-  }
   CU(p->pstage.commit(st));
   p->progs[key] = sp;
   out = sp;
@@ -2161,11 +2104,6 @@ static hk_status ensure_solve_scratch(hk_plan* p, int s, cudaStream_t st) {
 // The solve program's kernel sequence: leaf solve, then per level (deepest
 // first) V^T x partial dots -> S^{-1} g -> x -= d y  (hodlr.py:298-306).
 static hk_status launch_solve_kernels(SolveProg* sp, int s, cudaStream_t st, bool prof) {
-  if (sp->fused) {
-    CU(hk_launch_solve_fused(sp->fphases, sp->nph, sp->nfronts, s, sp->fP, sp->fsmem, st));
-    if (prof) g_opprof.mark("fused " + std::to_string(sp->nfronts), st);
-    return HK_OK;
-  }
   if (sp->small) {
     CU(hk_launch_sgemv(sp->leaf.t, sp->leaf.items, sp->leaf.nitems, s, sp->leaf.max_k, st));
     if (prof) g_opprof.mark("leaf sgemv", st);

@@ -171,7 +171,7 @@ __device__ __forceinline__ void griddep_launch() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// ---- TMA bulk copies (cp.async.bulk -> UBLKCP) completing on mbarriers
+// ---- mbarriers (completion of the TMA tensor loads, gj.cu)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -198,24 +198,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
-// global -> own shared memory, `bytes` (multiple of 16, both ends 16-byte aligned)
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-// order this thread's earlier generic-proxy global writes before later
-// async-proxy (bulk copy) reads of the same addresses
-#ifndef HK_TMA_GPUFENCE
-#define HK_TMA_GPUFENCE 0
-#endif
-__device__ __forceinline__ void fence_proxy_async_global() {
-  if (HK_TMA_GPUFENCE) __threadfence();
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-
 // FP64 tensor-core MMA (DMMA.8x8x4 on sm_100a; tcgen05 has no f64 kind).
 // Fragment layout (PTX ISA, mma.m8n8k4 .f64): gid = lane>>2, tig = lane&3;
 //   A (8x4, row):  a  = A[gid][tig]

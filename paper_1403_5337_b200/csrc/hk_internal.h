@@ -133,18 +133,9 @@ struct SgemvTask {   // y[i,r] (op)= sum_k M[i,k] v[k,r] for i < rows, M column-
   int64_t ldy;
   int32_t rows, K;
 };
-// one phase of a front's fused solve program (solve_fused_kernel)
-struct FusedPhase {
-  int32_t type;            // 0: pdot items, 1: sgemv items
-  int32_t nitems;
-  const void* t;           // PdotTask* / SgemvTask* (the level's task array)
-  const int32_t* items;    // this front's items (3 / 2 ints each)
-};
 constexpr int HK_PDOT_ROWS = 256;   // rows per partial-dot chunk
 constexpr int HK_PDOT_COLS = 32;    // columns per partial-dot item
 constexpr int HK_SGEMV_ROWS = 32;   // rows per sgemv item
-cudaError_t hk_launch_solve_fused(const FusedPhase* phases, int nph, int nfronts, int s, int P,
-                                  size_t smem, cudaStream_t st);
 cudaError_t hk_launch_pdot(const PdotTask* tasks, const int32_t* items, int nitems, int s,
                            cudaStream_t st);
 cudaError_t hk_launch_sgemv(const SgemvTask* tasks, const int32_t* items, int nitems, int s,

@@ -282,34 +282,6 @@ __global__ void __launch_bounds__(256) sgemv_kernel(const SgemvTask* __restrict_
   sgemv_item(tasks, items, blockIdx.x, s, vs);
 }
 
-// ---------------------------------------------------------------------------
-// Fused per-front solve sweep: one thread-block cluster runs a front's whole
-// program -- the leaf GEMVs, then per level (deepest first) the V^T x partial
-// dots, the S^{-1} g GEMV and the x -= d y update (hodlr.py:298-306) -- with
-// a cluster barrier between dependent phases instead of a kernel boundary.
-// CTA q of the cluster takes items q, q+P, ... of every phase (the same item
-// bodies as the split kernels, so results are bit-identical).  Fronts of a
-// batch run in independent clusters, so a front never waits for another
-// front's phase: the 3*depth+1 dependent phases of a batch no longer cost
-// 3*depth+1 grid-wide drains.  Phase outputs (partials, S^{-1} g, x) go
-// through global memory; barrier.cluster.wait.acquire orders them (and drops
-// stale L1 lines) for the next phase's readers in the other CTAs.
-__global__ void __launch_bounds__(256) solve_fused_kernel(const FusedPhase* __restrict__ phases,
-                                                          int nph, int s) {
-  extern __shared__ double dyn[];
-  const unsigned P = cl_nrank(), q = cl_rank();
-  const FusedPhase* fp = phases + (size_t)(blockIdx.x / P) * nph;
-  for (int k = 0; k < nph; ++k) {
-    const FusedPhase f = fp[k];
-    for (int it = (int)q; it < f.nitems; it += (int)P) {
-      if (f.type == 0) pdot_item(static_cast<const PdotTask*>(f.t), f.items, it, s, dyn);
-      else sgemv_item(static_cast<const SgemvTask*>(f.t), f.items, it, s, dyn);
-      __syncthreads();                       // SMEM reuse by the next item
-    }
-    cluster_bar();
-  }
-}
-
 // Dense GEMV for the GMRES operator (src/cli.py:320-321): y(m x s) = A x with
 // A row-major.  Each warp owns RW rows and walks them together with 16-byte
 // loads (lane l covers columns 2l + 64t, 2l + 64t + 1), so every x chunk it
@@ -481,41 +453,6 @@ cudaError_t hk_launch_pdot(const PdotTask* tasks, const int32_t* items, int nite
                            cudaStream_t st) {
   if (nitems == 0) return cudaSuccess;
   const cudaError_t e = launch_pdl(pdot_kernel, dim3(nitems), dim3(256), 0, st, tasks, items, s);
-  hk_count_launch();
-  if (e != cudaSuccess) return e;
-  return cudaGetLastError();
-}
-
-cudaError_t hk_launch_solve_fused(const FusedPhase* phases, int nph, int nfronts, int s, int P,
-                                  size_t smem, cudaStream_t st) {
-  if (nfronts == 0 || nph == 0) return cudaSuccess;
-  static size_t attr_smem = 0;
-  static bool nonportable = false;
-  if (smem > 48 * 1024 && smem > attr_smem) {
-    cudaError_t e = cudaFuncSetAttribute(solve_fused_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_smem = smem;
-  }
-  if (P > 8 && !nonportable) {
-    cudaError_t e = cudaFuncSetAttribute(solve_fused_kernel,
-                                         cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-    nonportable = true;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = (unsigned)P;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.gridDim = dim3((unsigned)(nfronts * P));
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, solve_fused_kernel, phases, nph, s);
   hk_count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
