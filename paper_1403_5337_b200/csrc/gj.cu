@@ -200,6 +200,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_blk_kernel(const GjTask* __rest
 // and replays the step on its own columns.  The owner of the next panel is
 // therefore never more than one step behind, and the critical path is one
 // pivot search + update per step instead of a CTA barrier per panel.
+#ifndef HK_GJ_MBAR
+#define HK_GJ_MBAR 1
+#endif
 #ifndef HK_GJ_LAZY
 #define HK_GJ_LAZY 0
 #endif
@@ -239,6 +242,11 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_df_kernel(const GjTask* __restr
   __shared__ double rinv_s[NR];
   __shared__ int p_s[NR], invp[NR];
   __shared__ int s_pub;                             // number of published steps
+#if HK_GJ_MBAR
+  // one mbarrier per step (never reused): waiters sleep in try_wait instead of
+  // spinning on s_pub, so the owner's pivot chain keeps the issue slots
+  __shared__ __align__(8) uint64_t stepbar[NR];
+#endif
   if (N == 0) {
     if (tid == 0) *t.status = 0;
     return;
@@ -287,6 +295,12 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_df_kernel(const GjTask* __restr
   }
   unsigned used = 0;
   if (tid == 0) s_pub = 0;
+#if HK_GJ_MBAR
+  if (tid == 0) {
+    for (int k = 0; k < N; ++k) mbar_init(&stepbar[k], 1);
+    mbar_init_fence();
+  }
+#endif
   __syncthreads();
   bool singular = false;
   // walk every step in order (panel-major, so the column slot l is a compile-
@@ -321,6 +335,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_df_kernel(const GjTask* __restr
             p_s[c] = -1;
             // release every waiter, lazy ones included: they stop at step c
             st_release_cta(&s_pub, HK_GJ_LAZY ? N + 1 : c + 1);
+#if HK_GJ_MBAR
+            mbar_arrive(&stepbar[c]);
+#endif
           }
           singular = true;
           break;
@@ -341,7 +358,11 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_df_kernel(const GjTask* __restr
           p_s[c] = p;
         }
         __syncwarp();
+#if HK_GJ_MBAR
+        if (lane == 0) mbar_arrive(&stepbar[c]);   // release: the step's SMEM slots are visible
+#else
         if (lane == 0) st_release_cta(&s_pub, c + 1);
+#endif
         gj_apply_step_dyn<CPW, RPL>(w_, ck, rinv, qp, lp, lane, l);
 #pragma unroll
         for (int q = 0; q < RPL; ++q) w_[l][q] = isp[q] ? rinv : -ck[q] * rinv;
@@ -353,12 +374,16 @@ __global__ void __launch_bounds__(NW * 32, 1) gj_df_kernel(const GjTask* __restr
         // steps in the same order (same arithmetic, same bits), so the owner's
         // pivot chain no longer shares its SM sub-partition's issue slots with
         // NW-2 warps replaying every step.
+#if HK_GJ_MBAR
+        mbar_wait(&stepbar[c], 0);                  // acquire
+#else
         const int need = (!HK_GJ_LAZY || warp == P + 1) ? c : min(N, (P + 1) * CPW) - 1;
         while (ld_acquire_cta(&s_pub) <= need) {
 #if HK_GJ_SPIN_NS
           __nanosleep(HK_GJ_SPIN_NS);   // back off: the spinning warps share the MIO pipe with the owner
 #endif
         }
+#endif
         __syncwarp();
         const int p = __shfl_sync(0xffffffffu, lane == 0 ? p_s[c] : 0, 0);
         if (p < 0) {
