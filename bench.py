@@ -622,6 +622,12 @@ def run_ours(args):
             c0 = run_cfg0(dev)
         except Exception as exc:
             c0 = {"error": repr(exc)[:400]}
+    grid = None
+    if not args.no_cfg0 and rank == 0:
+        try:
+            grid = run_grid_solve(dev)
+        except Exception as exc:
+            grid = {"error": repr(exc)[:400]}
     if args.level_fronts > 0 and world == 1:
         try:
             lvl = run_level(dev, args.level_fronts, stream)
@@ -638,7 +644,7 @@ def run_ours(args):
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roof,
                 "rooflines": rooflines,
                 "cpu_baseline": cpu, "gmres": gm, "cfg0": c0, "level": lvl, "cfg4": c4,
-                "cfg1": c1, "cfg2": c2, "frontgen": gen,
+                "cfg1": c1, "cfg2": c2, "frontgen": gen, "grid_solve": grid,
                 "ranks_per_level_front0": [e["max_rank"] for e in batch.report(0).ranks_per_level],
                 "fronts_gathered": int(all_ranks.shape[0]),
                 "max_block_rank_all_fronts": int(all_ranks.max())}
@@ -854,6 +860,40 @@ def run_cfg0(dev):
             "reference_cpu_1t_s": {"build_factor": 0.50, "gmres_to_1e-12": 0.014,
                                    "gmres_iterations": 4, "max_rank_per_level": [78, 78, 79, 64],
                                    "source": "SURVEY.md §6.3 (reference run in the build container)"}}
+
+
+def run_grid_solve(dev):
+    """The whole config-3 grid (32^3, variable k, seed 0) solved through its
+    separator front (nested.PlaneNestedSolver: plane elimination on
+    hk_spd_inverse, HODLR-ACA 1e-6 front factorization, HODLR-preconditioned
+    GMRES to 1e-12 on the separator, plane forward/back substitution on
+    hk_gemv), checked by the residual of the grid operator."""
+    import time
+    import torch
+    import paper_1403_5337_b200 as hk
+    from paper_1403_5337_b200 import frontgen as fg
+    from paper_1403_5337_b200.nested import PlaneNestedSolver
+    kc = fg.cell_conductivity(DIMS, 0)
+    PlaneNestedSolver(DIMS, 2, PLANE, conductivity=kc, leaf=LEAF,
+                      cfg=hk.CompressionConfig(scheme="aca", tol=TOL))          # warm
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s = PlaneNestedSolver(DIMS, 2, PLANE, conductivity=kc, leaf=LEAF,
+                          cfg=hk.CompressionConfig(scheme="aca", tol=TOL))
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t0
+    b = np.random.default_rng(0).standard_normal((s.ext, s.nl))
+    s.solve(b, hk.GmresConfig(tol=1e-12))
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    x, res = s.solve(b, hk.GmresConfig(tol=1e-12))
+    torch.cuda.synchronize()
+    solve = time.perf_counter() - t1
+    rel = float(np.linalg.norm(s.apply(x) - b) / np.linalg.norm(b))
+    return {"workload": "cfg3 grid 32^3 (variable k, seed 0, 30752 unknowns) solved through its "
+                        "z=16 separator front: forward/back plane substitution + HODLR-GMRES",
+            "setup_ms": 1e3 * setup, "solve_ms": 1e3 * solve, "separator_gmres_iterations": res.iterations,
+            "relative_residual": rel, "unknowns": int(s.ext * s.nl)}
 
 
 def run_level(dev, nfronts, stream):

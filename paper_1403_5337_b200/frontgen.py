@@ -266,45 +266,45 @@ def layered_grid_front(dims, axis, plane, conductivity=None, device=None,
     return F.cpu().numpy()
 
 
-def layered_grid_fronts(dims, axis, plane, conductivities, device=None, dtype=None):
-    """The fronts of several conductivity fields of one grid (a batch of the
-    multifrontal level of config 3), eliminated together: every plane step
-    inverts the whole batch's layer Schur complements in one hk_spd_inverse
-    call (block Gauss-Jordan on the DMMA GEMM) on the GPU.  Returns a
-    (len(conductivities), n, n) torch tensor on ``device``."""
-    torch = _torch()
-    dims = tuple(int(x) for x in dims)
-    d = len(dims)
-    if isinstance(axis, str):
-        axis = AXIS_NAMES[axis]
-    ext = dims[axis]
-    if not 0 < plane < ext - 1:
-        raise InvalidPlaneError(f"plane {plane} is not strictly interior to extent {ext}")
-    dev = torch.device(device or "cpu")
-    dt = dtype or torch.float64
-    # move the separator axis to the front; remaining axes keep their order
-    perm = [axis] + [b for b in range(d) if b != axis]
-    wls = []
-    for kc in conductivities:
-        w = _edge_weights(dims, kc)
-        wls.append([np.transpose(w[b], perm) for b in range(d)])
-    B = len(wls)
-    layer_shape = tuple(dims[b] for b in perm[1:])
-    nl = int(np.prod(layer_shape)) if layer_shape else 1
-    ids = np.arange(nl).reshape(layer_shape)
+class PlaneOperator:
+    """The grid Laplacian of one or more conductivity fields, split into planes
+    along `axis`: block tridiagonal with the in-plane operators T_t (nl x nl)
+    on the diagonal and -diag(c_t) (the edges between planes t-1 and t) off it.
+    Every field of a batch has the same stencil pattern, so the batch's plane
+    operators are assembled with one scatter (leading batch axis)."""
 
-    # every front of the batch has the same stencil pattern: stack the weights
-    # (leading batch axis) and scatter all fronts' layer operators at once
-    wlb = [np.stack([wl[b] for wl in wls]) for b in range(d)]
+    def __init__(self, dims, axis, conductivities, device=None, dtype=None):
+        torch = _torch()
+        self.dims = tuple(int(x) for x in dims)
+        d = len(self.dims)
+        if isinstance(axis, str):
+            axis = AXIS_NAMES[axis]
+        self.axis = axis
+        self.ext = self.dims[axis]
+        self.dev = torch.device(device or "cpu")
+        self.dt = dtype or torch.float64
+        # move the separator axis to the front; remaining axes keep their order
+        self.perm = [axis] + [b for b in range(d) if b != axis]
+        wls = []
+        for kc in conductivities:
+            w = _edge_weights(self.dims, kc)
+            wls.append([np.transpose(w[b], self.perm) for b in range(d)])
+        self.B = len(wls)
+        self.layer_shape = tuple(self.dims[b] for b in self.perm[1:])
+        self.nl = int(np.prod(self.layer_shape)) if self.layer_shape else 1
+        self._ids = np.arange(self.nl).reshape(self.layer_shape)
+        self._wlb = [np.stack([wl[b] for wl in wls]) for b in range(d)]
 
-    def layer_matrix(t):
+    def layer_matrix(self, t):
         """In-layer operators T_t of the batch (B x nl x nl)."""
+        torch = _torch()
+        B, nl, layer_shape, ids, wlb = self.B, self.nl, self.layer_shape, self._ids, self._wlb
         diag = np.zeros((B,) + layer_shape)
         # edges along the separator axis: t and t+1 (in w's indexing)
-        wa = wlb[axis]
+        wa = wlb[self.axis]
         diag += wa[:, t] + wa[:, t + 1]
         rows, cols, vals = [], [], []
-        for j, b in enumerate(perm[1:]):
+        for j, b in enumerate(self.perm[1:]):
             wb = wlb[b][:, t]                     # (B, layer dims with +1 on axis j)
             n_b = layer_shape[j]
             lo = [slice(None)] * (len(layer_shape) + 1)
@@ -323,22 +323,45 @@ def layered_grid_fronts(dims, axis, plane, conductivities, device=None, dtype=No
                 rows += [src, dst]
                 cols += [dst, src]
                 vals += [-ww, -ww]
-        T = torch.zeros((B, nl, nl), dtype=dt, device=dev)
+        T = torch.zeros((B, nl, nl), dtype=self.dt, device=self.dev)
         if rows:
-            r = torch.from_numpy(np.concatenate(rows)).to(dev)
-            c = torch.from_numpy(np.concatenate(cols)).to(dev)
-            v = torch.from_numpy(np.concatenate(vals, axis=1)).to(device=dev, dtype=dt)
+            r = torch.from_numpy(np.concatenate(rows)).to(self.dev)
+            c = torch.from_numpy(np.concatenate(cols)).to(self.dev)
+            v = torch.from_numpy(np.concatenate(vals, axis=1)).to(device=self.dev, dtype=self.dt)
             T[:, r, c] = v
-        idx = torch.arange(nl, device=dev)
-        T[:, idx, idx] = torch.from_numpy(diag.reshape(B, nl)).to(device=dev, dtype=dt)
+        idx = torch.arange(nl, device=self.dev)
+        T[:, idx, idx] = torch.from_numpy(diag.reshape(B, nl)).to(device=self.dev, dtype=self.dt)
         return T
 
-    def coupling(t):
+    def coupling(self, t):
         """Diagonals of the coupling between layers t-1 and t (edge t), B x nl."""
-        return torch.from_numpy(np.ascontiguousarray(wlb[axis][:, t]).reshape(B, -1)).to(
-            device=dev, dtype=dt)
+        torch = _torch()
+        return torch.from_numpy(np.ascontiguousarray(self._wlb[self.axis][:, t]).reshape(self.B, -1)).to(
+            device=self.dev, dtype=self.dt)
 
-    use_hk = dev.type == "cuda" and dt == torch.float64 and frontgen_solver() == "hk"
+    def inverse(self, D):
+        """D^{-1} for a (B, nl, nl) batch of SPD plane Schur complements: this
+        library's block Gauss-Jordan on the GPU, torch.linalg.inv otherwise."""
+        torch = _torch()
+        if self.dev.type == "cuda" and self.dt == torch.float64 and frontgen_solver() == "hk":
+            X = D.contiguous().clone()
+            _spd_inverse_(X)
+            return X
+        return torch.linalg.inv(D)
+
+
+def layered_grid_fronts(dims, axis, plane, conductivities, device=None, dtype=None):
+    """The fronts of several conductivity fields of one grid (a batch of the
+    multifrontal level of config 3), eliminated together: every plane step
+    inverts the whole batch's layer Schur complements in one hk_spd_inverse
+    call (block Gauss-Jordan on the DMMA GEMM) on the GPU.  Returns a
+    (len(conductivities), n, n) torch tensor on ``device``."""
+    torch = _torch()
+    op = PlaneOperator(dims, axis, conductivities, device=device, dtype=dtype)
+    ext = op.ext
+    if not 0 < plane < ext - 1:
+        raise InvalidPlaneError(f"plane {plane} is not strictly interior to extent {ext}")
+    use_hk = op.dev.type == "cuda" and op.dt == torch.float64 and frontgen_solver() == "hk"
 
     def schur_term(D, c):
         """C D^{-1} C for the batch (C = diag(c)): this library's block
@@ -354,13 +377,13 @@ def layered_grid_fronts(dims, axis, plane, conductivities, device=None, dtype=No
         D_k = T_k - C D_{k-1}^{-1} C with C the diagonal plane coupling."""
         D = None
         for k, t in enumerate(order):
-            T = layer_matrix(t)
+            T = op.layer_matrix(t)
             if D is not None:
-                T = T - schur_term(D, coupling(max(t, order[k - 1])))
+                T = T - schur_term(D, op.coupling(max(t, order[k - 1])))
             D = T
         return D
 
-    front = layer_matrix(plane)
+    front = op.layer_matrix(plane)
     left_layers = list(range(0, plane))
     right_layers = list(range(ext - 1, plane, -1))
     for layers in (left_layers, right_layers):
@@ -368,7 +391,7 @@ def layered_grid_fronts(dims, axis, plane, conductivities, device=None, dtype=No
             continue
         D = eliminate(layers)
         try:
-            front = front - schur_term(D, coupling(max(plane, layers[-1])))
+            front = front - schur_term(D, op.coupling(max(plane, layers[-1])))
         except (RuntimeError, ValueError) as exc:
             raise SingularInteriorError(str(exc)) from exc
     return front
