@@ -21,6 +21,7 @@
 #include "hk_common.cuh"
 #include "hk_internal.h"
 
+#include <stdio.h>
 #include <stdlib.h>
 
 namespace {
@@ -104,6 +105,22 @@ __device__ __forceinline__ double ld_src(const double* p) {
 #endif
 }
 
+// L2 prefetch of the first ncols columns of a U/V panel (one bulk prefetch per
+// column, issued by ncols threads): the panel the NEXT sweep streams.  The
+// U/V pool of a 64-front batch exceeds the L2, so part of every re-stream
+// misses to DRAM; the prefetch moves that latency off the sweep's chunk chain.
+#ifndef HK_ACA_L2PF
+#define HK_ACA_L2PF 0
+#endif
+__device__ __forceinline__ void l2_prefetch_cols(const double* F, int len, int ncols, int64_t LD) {
+#if HK_ACA_L2PF
+  const uint32_t bytes = ((uint32_t)len * 8u + 15u) & ~15u;
+  for (int k = threadIdx.x; k < ncols; k += blockDim.x)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(F + (int64_t)k * LD), "r"(bytes)
+                 : "memory");
+#endif
+}
+
 // Chunk helpers of the fused sweep (KC columns x EPT elements per thread).
 //
 // dots: part[w*pld + kb + j] += sum over the warp's elements of pv[e] * a[e][j]
@@ -172,6 +189,27 @@ __device__ __forceinline__ void chunk_load_full(double (&a)[EPT][KW], const doub
 // not coalesced across lanes, so only lanes 0 and 16 issue them (one request
 // per line instead of 32: the ncu capture showed the per-lane prefetches as
 // ~40% of the kernel's L2 sectors).
+#ifndef HK_ACA_PF
+#define HK_ACA_PF 1   // 0: no L1 prefetch; 1: lanes 0/16, one instruction per line; 2: lane-mapped
+#endif
+// Lane-mapped variant: the chunk's EPT*KW*2 lines (32 for 2 x 8) are spread over
+// the lanes, so one prefetch instruction per thread covers the whole chunk.
+template <int NT, int EPT, int LDLOG, int KW>
+__device__ __forceinline__ void chunk_prefetch_lanes(const double* __restrict__ F, int g0, int len, int kb) {
+  constexpr int64_t LD = int64_t(1) << LDLOG;
+  constexpr int LINES = EPT * KW * 2;
+  const int lane = threadIdx.x & 31;
+  const int wbase = g0 + (threadIdx.x & ~31);
+#pragma unroll
+  for (int i0 = 0; i0 < LINES; i0 += 32) {
+    const int i = i0 + lane;
+    const int half = i & 1, j = (i >> 1) % KW, q = (i >> 1) / KW;
+    const int e = wbase + q * NT + half * 16;
+    if (i < LINES && e < len)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(F + e + (int64_t)(kb + j) * LD));
+  }
+}
+
 template <int EPT, int LDLOG, int KW>
 __device__ __forceinline__ void chunk_prefetch(const double* const (&pk)[EPT], int kb) {
   constexpr int64_t LD = int64_t(1) << LDLOG;
@@ -227,7 +265,8 @@ template <int NT, int EPT, int LDLOG, int DB, int KW>
 __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len, int nk, int ndot,
                                            const double* __restrict__ coef,
                                            const double* __restrict__ src, int sstride,
-                                           int out_col, int pend_col, double* __restrict__ part,
+                                           int out_col, bool store, int pend_col,
+                                           double* __restrict__ part,
                                            int pld, const unsigned char* __restrict__ used,
                                            ArgMax& best, double& sumsq, double& bestval,
                                            double* __restrict__ xout,
@@ -280,7 +319,10 @@ __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len
 #pragma unroll 1
         for (; kb + 2 * KW <= kfull; kb += 2 * KW) {
           chunk_load_full<EPT, LDLOG, KW>(a1, pk, kb + KW);
-          if (kb + 2 * KW < kfull) chunk_prefetch<EPT, LDLOG, KW>(pk, kb + 2 * KW);
+          if (kb + 2 * KW < kfull) {
+            if constexpr (HK_ACA_PF == 1) chunk_prefetch<EPT, LDLOG, KW>(pk, kb + 2 * KW);
+            if constexpr (HK_ACA_PF == 2) chunk_prefetch_lanes<NT, EPT, LDLOG, KW>(F, g0, len, kb + 2 * KW);
+          }
           chunk_process<EPT, KW>(x, a0, pv, coef, kb, nk, ndot, mypart, lane, y, coef2, n2);
           if (kb + 2 * KW < kfull) chunk_load_full<EPT, LDLOG, KW>(a0, pk, kb + 2 * KW);
           chunk_process<EPT, KW>(x, a1, pv, coef, kb + KW, nk, ndot, mypart, lane, y, coef2, n2);
@@ -297,7 +339,10 @@ __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len
         chunk_load_full<EPT, LDLOG, KW>(a, pk, kb);
         // the next chunk's lines are pulled into L1 while this one is reduced
         // (prefetch distance 1 measured best: 2..4 thrash L1)
-        if (kb + KW < kfull) chunk_prefetch<EPT, LDLOG, KW>(pk, kb + KW);
+        if (kb + KW < kfull) {
+          if constexpr (HK_ACA_PF == 1) chunk_prefetch<EPT, LDLOG, KW>(pk, kb + KW);
+          if constexpr (HK_ACA_PF == 2) chunk_prefetch_lanes<NT, EPT, LDLOG, KW>(F, g0, len, kb + KW);
+        }
         chunk_process<EPT, KW>(x, a, pv, coef, kb, nk, ndot, mypart, lane, y, coef2, n2);
       }
       }
@@ -321,7 +366,9 @@ __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len
       for (int q = 0; q < EPT; ++q) {
         if (!ok[q]) continue;
         const int e = g0 + tid + q * NT;
-        const_cast<double*>(F)[e + (int64_t)out_col * LD] = x[q];
+        // store == false: the caller keeps the residual in registers (xout) and
+        // writes the scaled cross itself, so this store would be overwritten
+        if (store) const_cast<double*>(F)[e + (int64_t)out_col * LD] = x[q];
         xout[q] = x[q];
         const double ax = fabs(x[q]);
         if (used) {
@@ -338,48 +385,111 @@ __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len
 }
 
 // One call target per (NT, EPT) for the caller (keeps its register allocation
-// small); the leading dimension is dispatched once, inside.
+// small); the leading dimension is dispatched once, inside.  The results come
+// back BY VALUE (a struct of <= 64 bytes returns in registers): with reference
+// out-parameters every call spilled them through the thread's stack, and those
+// local-memory stores were 85% of the kernel's L2 write sectors (ncu:
+// 3.8M of 4.45M write sectors per class-0 launch at 8 fronts).
+template <int EPT>
+struct SweepOut {
+  double bv, sumsq, bestval, ydot;
+  int bi;
+  double x[EPT];
+};
+
 template <int NT, int EPT, int DB>
-__device__ __noinline__ void sweep(int ldlog, const double* __restrict__ F, int len, int nk, int ndot,
-                                   const double* __restrict__ coef, const double* __restrict__ src,
-                                   int sstride, int out_col, int pend_col, double* __restrict__ part,
-                                   int pld, const unsigned char* __restrict__ used, ArgMax& best,
-                                   double& sumsq, double& bestval, double* xout) {
-  double yd;
+__device__ __noinline__ SweepOut<EPT> sweep_r(int ldlog, const double* __restrict__ F, int len, int nk,
+                                              int ndot, const double* __restrict__ coef,
+                                              const double* __restrict__ src, int sstride, int out_col,
+                                              bool store, int pend_col, double* __restrict__ part,
+                                              int pld, const unsigned char* __restrict__ used) {
+  SweepOut<EPT> o;
+  ArgMax best;
+  best.v = 0.0;
+  best.i = -1;
+  o.sumsq = o.bestval = o.ydot = 0.0;
+#pragma unroll
+  for (int q = 0; q < EPT; ++q) o.x[q] = 0.0;
 #define HK_SWEEP_CASE(L)                                                                       \
   case L:                                                                                      \
-    sweep_impl<NT, EPT, L, DB, KC>(F, len, nk, ndot, coef, src, sstride, out_col, pend_col, part, pld, \
-                           used, best, sumsq, bestval, xout, nullptr, 0, yd);                  \
-    return;
+    sweep_impl<NT, EPT, L, DB, KC>(F, len, nk, ndot, coef, src, sstride, out_col, store, pend_col, part, pld, \
+                           used, best, o.sumsq, o.bestval, o.x, nullptr, 0, o.ydot);           \
+    break;
   switch (ldlog) {
     HK_SWEEP_CASE(6) HK_SWEEP_CASE(7) HK_SWEEP_CASE(8) HK_SWEEP_CASE(9) HK_SWEEP_CASE(10)
     HK_SWEEP_CASE(11) HK_SWEEP_CASE(12) HK_SWEEP_CASE(13)
-    default: return;
+    default: break;
   }
 #undef HK_SWEEP_CASE
+  o.bv = best.v;
+  o.bi = (int)best.i;
+  return o;
+}
+
+template <int NT, int EPT, int DB>
+__device__ __forceinline__ void sweep(int ldlog, const double* __restrict__ F, int len, int nk, int ndot,
+                                      const double* __restrict__ coef, const double* __restrict__ src,
+                                      int sstride, int out_col, int pend_col, double* __restrict__ part,
+                                      int pld, const unsigned char* __restrict__ used, ArgMax& best,
+                                      double& sumsq, double& bestval, double* xout, bool store = true) {
+  const SweepOut<EPT> o = sweep_r<NT, EPT, DB>(ldlog, F, len, nk, ndot, coef, src, sstride, out_col, store,
+                                               pend_col, part, pld, used);
+  best.v = o.bv;
+  best.i = o.bi;
+  sumsq = o.sumsq;
+  bestval = o.bestval;
+#pragma unroll
+  for (int q = 0; q < EPT; ++q) xout[q] = o.x[q];
 }
 
 // The column sweep of the main ACA step with the coefficient sweep of the
 // stopping test (y = U b, ydot = u_r . y), a separate call target so the
 // other sweeps keep their register allocation.
 template <int NT, int EPT, int DB>
-__device__ __noinline__ void sweep_y(int ldlog, const double* __restrict__ F, int len, int nk,
-                                     const double* __restrict__ coef, const double* __restrict__ src,
-                                     int sstride, int out_col, int pend_col,
-                                     const unsigned char* __restrict__ used, ArgMax& best,
-                                     double& sumsq, double& bestval, double* xout,
-                                     const double* __restrict__ coef2, int n2, double& ydot) {
+__device__ __noinline__ SweepOut<EPT> sweep_y_r(int ldlog, const double* __restrict__ F, int len, int nk,
+                                                const double* __restrict__ coef,
+                                                const double* __restrict__ src, int sstride, int out_col,
+                                                int pend_col, const unsigned char* __restrict__ used,
+                                                const double* __restrict__ coef2, int n2) {
+  SweepOut<EPT> o;
+  ArgMax best;
+  best.v = 0.0;
+  best.i = -1;
+  o.sumsq = o.bestval = o.ydot = 0.0;
+#pragma unroll
+  for (int q = 0; q < EPT; ++q) o.x[q] = 0.0;
 #define HK_SWEEP_CASE(L)                                                                       \
   case L:                                                                                      \
-    sweep_impl<NT, EPT, L, DB, KCY>(F, len, nk, 0, coef, src, sstride, out_col, pend_col, nullptr, 0, \
-                           used, best, sumsq, bestval, xout, coef2, n2, ydot);                 \
-    return;
+    sweep_impl<NT, EPT, L, DB, KCY>(F, len, nk, 0, coef, src, sstride, out_col, true, pend_col, nullptr, 0, \
+                           used, best, o.sumsq, o.bestval, o.x, coef2, n2, o.ydot);            \
+    break;
   switch (ldlog) {
     HK_SWEEP_CASE(6) HK_SWEEP_CASE(7) HK_SWEEP_CASE(8) HK_SWEEP_CASE(9) HK_SWEEP_CASE(10)
     HK_SWEEP_CASE(11) HK_SWEEP_CASE(12) HK_SWEEP_CASE(13)
-    default: return;
+    default: break;
   }
 #undef HK_SWEEP_CASE
+  o.bv = best.v;
+  o.bi = (int)best.i;
+  return o;
+}
+
+template <int NT, int EPT, int DB>
+__device__ __forceinline__ void sweep_y(int ldlog, const double* __restrict__ F, int len, int nk,
+                                        const double* __restrict__ coef, const double* __restrict__ src,
+                                        int sstride, int out_col, int pend_col,
+                                        const unsigned char* __restrict__ used, ArgMax& best,
+                                        double& sumsq, double& bestval, double* xout,
+                                        const double* __restrict__ coef2, int n2, double& ydot) {
+  const SweepOut<EPT> o =
+      sweep_y_r<NT, EPT, DB>(ldlog, F, len, nk, coef, src, sstride, out_col, pend_col, used, coef2, n2);
+  best.v = o.bv;
+  best.i = o.bi;
+  sumsq = o.sumsq;
+  bestval = o.bestval;
+  ydot = o.ydot;
+#pragma unroll
+  for (int q = 0; q < EPT; ++q) xout[q] = o.x[q];
 }
 
 // Block argmax of |x| (lowest index on ties) that also returns the signed
@@ -537,9 +647,10 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
     ++nused;
     for (int k = tid; k < c; k += NT) coef[k] = U[row + (int64_t)k * LD];
     bar<NT>();
+    l2_prefetch_cols(U, m, c, LD);             // the column sweep's panel
     // residual row (:253-256) + the pending cross's v dots
     sweep<NT, EPT, DB>(ldlog, V, n, c, pending ? r : 0, coef, rowsrc_base + (int64_t)row * rowsrc_ld, 1,
-                   c, r, partV, pld, nullptr, best, dummy, bval, xv);
+                   c, r, partV, pld, nullptr, best, dummy, bval, xv, n > NT * EPT);
     double delta;
     best = block_argmax_val<NT>(best, bval, red_v, red_i, red_x, delta);
     const int col = (int)best.i;
@@ -609,6 +720,7 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
     const double* csrc = t.At ? t.At + (int64_t)col * t.lda : t.A + col;
     const int cstride = t.At ? 1 : (int)t.lda;
     double ydot = 0.0;
+    l2_prefetch_cols(V, n, c + 1, LD);         // the next row sweep's panel
     sweep_y<NT, EPT, DB>(ldlog, U, m, c, coef, csrc, cstride, c, r, used, nxt, uu, bval, xv, bv,
                          pending ? r : 0, ydot);
     {
@@ -919,7 +1031,7 @@ __global__ void __maxnreg__(200) aca_cluster_kernel(const AcaTask* __restrict__ 
     // residual row slice + the pending cross's v dots
     sweep<NT, EPT, DB>(ldlog, Vs, nlen, c, pending ? r : 0, coef,
                        t.A + (int64_t)row * t.lda + nv0, 1, c, r, partV, pld, nullptr, best, dummy,
-                       bval, xv);
+                       bval, xv, nlen > NT * EPT);
     {
       double lval;
       ArgMax lb = block_argmax_val<NT>(best, bval, red_v, red_i, red_x, lval);
@@ -1115,6 +1227,14 @@ static cudaError_t launch_cls(const AcaTask* tasks_dev, int ntasks, int max_cap,
   if (e != cudaSuccess) return e;
   int grid = sms * (per_sm > 0 ? per_sm : 1);
   if (grid > ntasks) grid = ntasks;
+  // experiment knob: HK_ACA_GRID="g0,g1,g2,g3" caps the persistent grid of each
+  // size class (fewer co-resident chains -> smaller U/V working set in L2)
+  if (const char* e = getenv("HK_ACA_GRID")) {
+    int g[4] = {0, 0, 0, 0};
+    sscanf(e, "%d,%d,%d,%d", &g[0], &g[1], &g[2], &g[3]);
+    const int c = NT >= 256 ? 0 : NT >= 128 ? 1 : NT >= 64 ? 2 : 3;
+    if (g[c] > 0 && grid > g[c]) grid = g[c];
+  }
   aca_kernel<NT, EPT, DB><<<grid, NT, smem, st>>>(tasks_dev, ntasks, counter, tol2, part_in_smem);
   hk_count_launch();
   return cudaGetLastError();
