@@ -1280,12 +1280,30 @@ static cudaError_t launch_class_id(int cls, const AcaTask* td, int nt, int max_c
 // Tasks arrive grouped by size class and largest-first inside a class; each
 // class is one persistent launch; classes run concurrently on the given
 // streams (the caller forks/joins them).
+// experiment: HK_ACA_DELAY="d0,d1,d2,d3" (microseconds) holds back the start of a
+// size class on its stream (staggers the chains' L2 demand)
+__global__ void delay_kernel(long long ns) {
+  long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
 cudaError_t hk_launch_aca_classes(const AcaTask* tasks_dev, const int* class_begin,
                                   const int* class_max_cap, const int* class_max_m, double tol2,
                                   int* counters_dev, cudaStream_t* streams) {
-  for (int c = 0; c < 4; ++c) {
+  int order[4] = {0, 1, 2, 3};
+  if (const char* o = getenv("HK_ACA_ORDER")) sscanf(o, "%d,%d,%d,%d", &order[0], &order[1], &order[2], &order[3]);
+  for (int oi = 0; oi < 4; ++oi) {
+    const int c = order[oi] & 3;
     const int nt = class_begin[c + 1] - class_begin[c];
     if (nt == 0) continue;
+    if (const char* d = getenv("HK_ACA_DELAY")) {
+      int us[4] = {0, 0, 0, 0};
+      sscanf(d, "%d,%d,%d,%d", &us[0], &us[1], &us[2], &us[3]);
+      if (us[c] > 0) delay_kernel<<<1, 1, 0, streams[c]>>>((long long)us[c] * 1000);
+    }
     cudaError_t e = launch_class_id(c, tasks_dev + class_begin[c], nt, class_max_cap[c],
                                     class_max_m[c], tol2, counters_dev + c, streams[c]);
     if (e != cudaSuccess) return e;
