@@ -21,7 +21,6 @@
 #include "hk_common.cuh"
 #include "hk_internal.h"
 
-#include <stdio.h>
 #include <stdlib.h>
 
 namespace {
@@ -105,22 +104,6 @@ __device__ __forceinline__ double ld_src(const double* p) {
 #endif
 }
 
-// L2 prefetch of the first ncols columns of a U/V panel (one bulk prefetch per
-// column, issued by ncols threads): the panel the NEXT sweep streams.  The
-// U/V pool of a 64-front batch exceeds the L2, so part of every re-stream
-// misses to DRAM; the prefetch moves that latency off the sweep's chunk chain.
-#ifndef HK_ACA_L2PF
-#define HK_ACA_L2PF 0
-#endif
-__device__ __forceinline__ void l2_prefetch_cols(const double* F, int len, int ncols, int64_t LD) {
-#if HK_ACA_L2PF
-  const uint32_t bytes = ((uint32_t)len * 8u + 15u) & ~15u;
-  for (int k = threadIdx.x; k < ncols; k += blockDim.x)
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(F + (int64_t)k * LD), "r"(bytes)
-                 : "memory");
-#endif
-}
-
 // Chunk helpers of the fused sweep (KC columns x EPT elements per thread).
 //
 // dots: part[w*pld + kb + j] += sum over the warp's elements of pv[e] * a[e][j]
@@ -190,26 +173,8 @@ __device__ __forceinline__ void chunk_load_full(double (&a)[EPT][KW], const doub
 // per line instead of 32: the ncu capture showed the per-lane prefetches as
 // ~40% of the kernel's L2 sectors).
 #ifndef HK_ACA_PF
-#define HK_ACA_PF 1   // 0: no L1 prefetch; 1: lanes 0/16, one instruction per line; 2: lane-mapped
+#define HK_ACA_PF 1   // 0: no L1 prefetch (measured equal in round 2, profiles/r02_aca_experiments.md)
 #endif
-// Lane-mapped variant: the chunk's EPT*KW*2 lines (32 for 2 x 8) are spread over
-// the lanes, so one prefetch instruction per thread covers the whole chunk.
-template <int NT, int EPT, int LDLOG, int KW>
-__device__ __forceinline__ void chunk_prefetch_lanes(const double* __restrict__ F, int g0, int len, int kb) {
-  constexpr int64_t LD = int64_t(1) << LDLOG;
-  constexpr int LINES = EPT * KW * 2;
-  const int lane = threadIdx.x & 31;
-  const int wbase = g0 + (threadIdx.x & ~31);
-#pragma unroll
-  for (int i0 = 0; i0 < LINES; i0 += 32) {
-    const int i = i0 + lane;
-    const int half = i & 1, j = (i >> 1) % KW, q = (i >> 1) / KW;
-    const int e = wbase + q * NT + half * 16;
-    if (i < LINES && e < len)
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(F + e + (int64_t)(kb + j) * LD));
-  }
-}
-
 template <int EPT, int LDLOG, int KW>
 __device__ __forceinline__ void chunk_prefetch(const double* const (&pk)[EPT], int kb) {
   constexpr int64_t LD = int64_t(1) << LDLOG;
@@ -319,10 +284,7 @@ __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len
 #pragma unroll 1
         for (; kb + 2 * KW <= kfull; kb += 2 * KW) {
           chunk_load_full<EPT, LDLOG, KW>(a1, pk, kb + KW);
-          if (kb + 2 * KW < kfull) {
-            if constexpr (HK_ACA_PF == 1) chunk_prefetch<EPT, LDLOG, KW>(pk, kb + 2 * KW);
-            if constexpr (HK_ACA_PF == 2) chunk_prefetch_lanes<NT, EPT, LDLOG, KW>(F, g0, len, kb + 2 * KW);
-          }
+          if (HK_ACA_PF == 1 && kb + 2 * KW < kfull) chunk_prefetch<EPT, LDLOG, KW>(pk, kb + 2 * KW);
           chunk_process<EPT, KW>(x, a0, pv, coef, kb, nk, ndot, mypart, lane, y, coef2, n2);
           if (kb + 2 * KW < kfull) chunk_load_full<EPT, LDLOG, KW>(a0, pk, kb + 2 * KW);
           chunk_process<EPT, KW>(x, a1, pv, coef, kb + KW, nk, ndot, mypart, lane, y, coef2, n2);
@@ -339,10 +301,7 @@ __device__ __forceinline__ void sweep_impl(const double* __restrict__ F, int len
         chunk_load_full<EPT, LDLOG, KW>(a, pk, kb);
         // the next chunk's lines are pulled into L1 while this one is reduced
         // (prefetch distance 1 measured best: 2..4 thrash L1)
-        if (kb + KW < kfull) {
-          if constexpr (HK_ACA_PF == 1) chunk_prefetch<EPT, LDLOG, KW>(pk, kb + KW);
-          if constexpr (HK_ACA_PF == 2) chunk_prefetch_lanes<NT, EPT, LDLOG, KW>(F, g0, len, kb + KW);
-        }
+        if (HK_ACA_PF == 1 && kb + KW < kfull) chunk_prefetch<EPT, LDLOG, KW>(pk, kb + KW);
         chunk_process<EPT, KW>(x, a, pv, coef, kb, nk, ndot, mypart, lane, y, coef2, n2);
       }
       }
@@ -647,7 +606,6 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
     ++nused;
     for (int k = tid; k < c; k += NT) coef[k] = U[row + (int64_t)k * LD];
     bar<NT>();
-    l2_prefetch_cols(U, m, c, LD);             // the column sweep's panel
     // residual row (:253-256) + the pending cross's v dots
     sweep<NT, EPT, DB>(ldlog, V, n, c, pending ? r : 0, coef, rowsrc_base + (int64_t)row * rowsrc_ld, 1,
                    c, r, partV, pld, nullptr, best, dummy, bval, xv, n > NT * EPT);
@@ -720,7 +678,6 @@ __device__ __forceinline__ void aca_block(const AcaTask& t, double tol2, int par
     const double* csrc = t.At ? t.At + (int64_t)col * t.lda : t.A + col;
     const int cstride = t.At ? 1 : (int)t.lda;
     double ydot = 0.0;
-    l2_prefetch_cols(V, n, c + 1, LD);         // the next row sweep's panel
     sweep_y<NT, EPT, DB>(ldlog, U, m, c, coef, csrc, cstride, c, r, used, nxt, uu, bval, xv, bv,
                          pending ? r : 0, ydot);
     {
@@ -1227,14 +1184,6 @@ static cudaError_t launch_cls(const AcaTask* tasks_dev, int ntasks, int max_cap,
   if (e != cudaSuccess) return e;
   int grid = sms * (per_sm > 0 ? per_sm : 1);
   if (grid > ntasks) grid = ntasks;
-  // experiment knob: HK_ACA_GRID="g0,g1,g2,g3" caps the persistent grid of each
-  // size class (fewer co-resident chains -> smaller U/V working set in L2)
-  if (const char* e = getenv("HK_ACA_GRID")) {
-    int g[4] = {0, 0, 0, 0};
-    sscanf(e, "%d,%d,%d,%d", &g[0], &g[1], &g[2], &g[3]);
-    const int c = NT >= 256 ? 0 : NT >= 128 ? 1 : NT >= 64 ? 2 : 3;
-    if (g[c] > 0 && grid > g[c]) grid = g[c];
-  }
   aca_kernel<NT, EPT, DB><<<grid, NT, smem, st>>>(tasks_dev, ntasks, counter, tol2, part_in_smem);
   hk_count_launch();
   return cudaGetLastError();
@@ -1280,30 +1229,12 @@ static cudaError_t launch_class_id(int cls, const AcaTask* td, int nt, int max_c
 // Tasks arrive grouped by size class and largest-first inside a class; each
 // class is one persistent launch; classes run concurrently on the given
 // streams (the caller forks/joins them).
-// experiment: HK_ACA_DELAY="d0,d1,d2,d3" (microseconds) holds back the start of a
-// size class on its stream (staggers the chains' L2 demand)
-__global__ void delay_kernel(long long ns) {
-  long long t0, t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  do {
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  } while (t - t0 < ns);
-}
-
 cudaError_t hk_launch_aca_classes(const AcaTask* tasks_dev, const int* class_begin,
                                   const int* class_max_cap, const int* class_max_m, double tol2,
                                   int* counters_dev, cudaStream_t* streams) {
-  int order[4] = {0, 1, 2, 3};
-  if (const char* o = getenv("HK_ACA_ORDER")) sscanf(o, "%d,%d,%d,%d", &order[0], &order[1], &order[2], &order[3]);
-  for (int oi = 0; oi < 4; ++oi) {
-    const int c = order[oi] & 3;
+  for (int c = 0; c < 4; ++c) {
     const int nt = class_begin[c + 1] - class_begin[c];
     if (nt == 0) continue;
-    if (const char* d = getenv("HK_ACA_DELAY")) {
-      int us[4] = {0, 0, 0, 0};
-      sscanf(d, "%d,%d,%d,%d", &us[0], &us[1], &us[2], &us[3]);
-      if (us[c] > 0) delay_kernel<<<1, 1, 0, streams[c]>>>((long long)us[c] * 1000);
-    }
     cudaError_t e = launch_class_id(c, tasks_dev + class_begin[c], nt, class_max_cap[c],
                                     class_max_m[c], tol2, counters_dev + c, streams[c]);
     if (e != cudaSuccess) return e;
