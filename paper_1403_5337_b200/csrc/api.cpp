@@ -15,6 +15,7 @@
 // and its children's d blocks are Y[rows, w_p : w_p + r].  Nothing is ever
 // concatenated (the reference's hstack/vstack at :244-245, :282 disappear).
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -41,10 +42,19 @@ static bool host_profile() {
   if (on < 0) on = getenv("HK_HOST_PROFILE") ? 1 : 0;
   return on == 1;
 }
+// NVTX range over an API entry point (SURVEY.md §5 tracing): a no-op unless a
+// tool that injects NVTX (ncu --nvtx, nsys) is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 struct HostClock {
   const char* what;
+  NvtxRange range;
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
-  explicit HostClock(const char* w) : what(w) {}
+  explicit HostClock(const char* w) : what(w), range(w) {}
   void mark(const char* phase) {
     if (!host_profile()) return;
     auto t1 = std::chrono::steady_clock::now();
@@ -888,6 +898,7 @@ static std::vector<int64_t> probe_rows(int64_t m) {
 extern "C" hk_status hk_build_bdlr(hk_plan* p, const double* A, int64_t ld, int64_t fstride,
                                    double tol, int32_t depth, int64_t max_rank,
                                    const int64_t* indptr, const int64_t* indices, void* stream) {
+  NvtxRange nvtx_range("hk_build_bdlr");
   if (!p) return fail(HK_ERR_VALUE, "null plan");
   if (!(tol > 0.0 && tol < 1.0)) return fail(HK_ERR_VALUE, "tol must lie strictly between 0 and 1");
   if (depth < 0) return fail(HK_ERR_VALUE, "depth must be >= 0");
@@ -2561,6 +2572,7 @@ extern "C" hk_status hk_gmres(hk_plan* p, int64_t front, const double* A, int64_
                               const double* b, double tol, int64_t max_iter, int precond,
                               const double* diag, double* x, int64_t* iterations, double* history,
                               double* true_residual, int32_t* flags, void* stream) {
+  NvtxRange nvtx_range("hk_gmres");
   return gmres_run(p, front, A, lda, n, b, 1, tol, max_iter, precond, diag, x, iterations, history,
                    true_residual, flags, (cudaStream_t)stream);
 }
@@ -2570,6 +2582,7 @@ extern "C" hk_status hk_gmres_batch(hk_plan* p, int64_t front, const double* A, 
                                     int64_t max_iter, int precond, const double* diag, double* X,
                                     int64_t* iterations, double* history, double* true_residual,
                                     int32_t* flags, void* stream) {
+  NvtxRange nvtx_range("hk_gmres_batch");
   return gmres_run(p, front, A, lda, n, B, s, tol, max_iter, precond, diag, X, iterations, history,
                    true_residual, flags, (cudaStream_t)stream);
 }
@@ -2731,6 +2744,7 @@ extern "C" hk_status hk_gj_inverse(const double* A, int64_t n, int64_t lda, int6
 // (A^T)^{-1} = (A^{-1})^T, so row-major input works unchanged.
 extern "C" hk_status hk_spd_inverse(double* A, int64_t n, int64_t lda, int64_t batch,
                                     int64_t stride, int32_t* status_host, void* stream) {
+  NvtxRange nvtx_range("hk_spd_inverse");
   if (hk_device_count() == 0) return fail(HK_ERR_CUDA, "no CUDA device visible");
   if (n < 0 || batch < 0 || lda < n) return fail(HK_ERR_VALUE, "bad spd_inverse dimensions");
   if (n == 0 || batch == 0) return HK_OK;

@@ -42,9 +42,15 @@ def main():
     cnt = defaultdict(int)
     with open(path) as fh:
         lines = [ln for ln in fh if ln.startswith('"')]
-    for row in csv.DictReader(lines):
-        if row.get("Metric Name") != "gpu__time_duration.sum":
-            continue
+    rows = [r for r in csv.DictReader(lines) if r.get("Metric Name") == "gpu__time_duration.sum"]
+    # --from-first NAME / --before-first NAME: split the list at the first launch whose
+    # kernel name contains NAME (e.g. transpose_kernel = the first HODLR build)
+    for flag in ("--from-first", "--before-first"):
+        if flag in sys.argv:
+            name = sys.argv[sys.argv.index(flag) + 1]
+            first = next((i for i, r in enumerate(rows) if name in r["Kernel Name"]), len(rows))
+            rows = rows[first:] if flag == "--from-first" else rows[:first]
+    for row in rows:
         k = short(row["Kernel Name"])
         if ours and not k.startswith(OURS):
             continue
