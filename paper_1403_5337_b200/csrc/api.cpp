@@ -1509,7 +1509,42 @@ extern "C" hk_status hk_factor_ext(hk_plan* p, const double* Zext, int64_t ldz, 
   int32_t* I = p->I.as<int32_t>();
   const double* UV = p->UV.as<double>();
 
-  // ---- Z gather: U of every block into the rows of its child, columns [w_p, w_p + r)
+  // ---- leaves first: the Gauss-Jordan inverses of the diagonal blocks need only the
+  // front, so they are staged and launched before the (larger) Z gather and leaf GEMM
+  // task lists are planned; the GPU inverts the leaves meanwhile (hodlr.py:222-232)
+  for (int g = 0; g < G; ++g) {
+  std::vector<Op>& ops = gops[g];
+  {
+    std::vector<GjTask> gts;
+    for (int64_t f = grp_lo(g); f < grp_hi(g); ++f)
+      for (int s : p->leaves) {
+        const Node& nd = p->nodes[s];
+        const NodeRec& r = p->rec[f * nn + s];
+        GjTask t{};
+        t.src = p->A + f * p->fstride + nd.lo * p->lda + nd.lo;
+        t.src_ld = p->lda;
+        t.out = F + r.inv;
+        t.out_ld = nd.hi - nd.lo;
+        t.status = I + r.status;
+        t.N = (int)(nd.hi - nd.lo);
+        t.mode = 0;
+        gts.push_back(t);
+      }
+    if (leaf_tma_ok(p, gts)) {
+      Op o{Op::GJ_LEAF_TMA};
+      o.a = p->stage.push(gts, st);
+      if (!o.a) return fail(HK_ERR_CUDA, "pinned staging allocation failed");
+      o.n = (int)gts.size();
+      o.maxN = 64;
+      ops.push_back(o);
+    } else {
+      CHK(stage_gj(p, ops, gts, st));
+    }
+  }
+  }
+  CHK(launch_groups());
+  // ---- Z gather: U of every block into the rows of its child, columns [w_p, w_p + r),
+  // then Y = K^{-1} Z
   for (int g = 0; g < G; ++g) {
   std::vector<Op>& ops = gops[g];
   std::vector<CopyTask> copies;
@@ -1548,33 +1583,7 @@ extern "C" hk_status hk_factor_ext(hk_plan* p, const double* Zext, int64_t ldz, 
     ops.push_back(o);
   }
 
-  // ---- leaves: Gauss-Jordan inverse, then Y = K^{-1} Z (hodlr.py:222-232)
   {
-    std::vector<GjTask> gts;
-    for (int64_t f = grp_lo(g); f < grp_hi(g); ++f)
-      for (int s : p->leaves) {
-        const Node& nd = p->nodes[s];
-        const NodeRec& r = p->rec[f * nn + s];
-        GjTask t{};
-        t.src = p->A + f * p->fstride + nd.lo * p->lda + nd.lo;
-        t.src_ld = p->lda;
-        t.out = F + r.inv;
-        t.out_ld = nd.hi - nd.lo;
-        t.status = I + r.status;
-        t.N = (int)(nd.hi - nd.lo);
-        t.mode = 0;
-        gts.push_back(t);
-      }
-    if (leaf_tma_ok(p, gts)) {
-      Op o{Op::GJ_LEAF_TMA};
-      o.a = p->stage.push(gts, st);
-      if (!o.a) return fail(HK_ERR_CUDA, "pinned staging allocation failed");
-      o.n = (int)gts.size();
-      o.maxN = 64;
-      ops.push_back(o);
-    } else {
-      CHK(stage_gj(p, ops, gts, st));
-    }
     TileList tl;
     for (int64_t f = grp_lo(g); f < grp_hi(g); ++f)
       for (int s : p->leaves) {
