@@ -172,3 +172,29 @@ def test_no_cpu_fallback_without_gpu():
         hk.factorize(acc, hk.build_tree(8, 4), hk.CompressionConfig(scheme="aca"))
     with pytest.raises(RuntimeError, match="CUDA"):
         hk.lu_full(np.eye(3))
+
+
+def test_aca_kernels_keep_their_sweep_results_in_registers():
+    """The ACA sweeps return their results by value.  With reference out-parameters
+    every call went through the thread's stack, and those local-memory stores were
+    85% of the kernel's L2 write sectors (profiles/r02_aca_experiments.md §5): a
+    regression shows up as hundreds of STL instructions in the aca kernels' SASS."""
+    import shutil
+    import subprocess
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not shutil.which(cuobjdump):
+        pytest.skip("cuobjdump not available")
+    if not N.LIB_PATH.exists():
+        pytest.skip("library not built")
+    sass = subprocess.run([cuobjdump, "-sass", str(N.LIB_PATH)], capture_output=True, text=True,
+                          check=True).stdout
+    stl, fn = {}, None
+    for line in sass.splitlines():
+        if "Function :" in line:
+            fn = line.split("Function :")[1].strip()
+            stl.setdefault(fn, 0)
+        elif fn and " STL" in line:
+            stl[fn] += 1
+    aca = {k: v for k, v in stl.items() if "aca_kernel" in k or "aca_cluster_kernel" in k}
+    assert len(aca) >= 5, sorted(stl)
+    assert max(aca.values()) <= 16, aca
