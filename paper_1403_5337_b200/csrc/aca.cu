@@ -173,7 +173,7 @@ __device__ __forceinline__ void chunk_load_full(double (&a)[EPT][KW], const doub
 // per line instead of 32: the ncu capture showed the per-lane prefetches as
 // ~40% of the kernel's L2 sectors).
 #ifndef HK_ACA_PF
-#define HK_ACA_PF 1   // 0: no L1 prefetch (measured equal in round 2, profiles/r02_aca_experiments.md)
+#define HK_ACA_PF 1   // 0: no L1 prefetch (config-3 build 3.66 vs 3.46 ms, profiles/r02_aca_experiments.md)
 #endif
 template <int EPT, int LDLOG, int KW>
 __device__ __forceinline__ void chunk_prefetch(const double* const (&pk)[EPT], int kb) {
